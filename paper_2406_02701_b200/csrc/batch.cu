@@ -1,0 +1,151 @@
+// Batched tile kernels for the MPCRTile scheduler: precision conversion of a
+// list of equally sized contiguous tiles (the "cast panel tiles to their
+// consumer precisions once" step, array.cpp:187-191 semantics), zero fill,
+// triangle zeroing and the leaf inverses of TRTRI.  blockIdx.y = item.
+#include "batch.hpp"
+#include "device.cuh"
+#include "internal.hpp"
+
+namespace mpcr {
+namespace {
+
+template <typename TI, typename TO> __device__ __forceinline__ TO cv(TI x);
+template <> __device__ __forceinline__ uint16_t cv<uint16_t, uint16_t>(uint16_t x) {
+    return ((x & 0x7C00u) == 0x7C00u && (x & 0x3FFu)) ? uint16_t(0x7E00u) : x;
+}
+template <> __device__ __forceinline__ float cv<uint16_t, float>(uint16_t x) { return h2f(x); }
+template <> __device__ __forceinline__ double cv<uint16_t, double>(uint16_t x) { return h2d(x); }
+template <> __device__ __forceinline__ uint16_t cv<float, uint16_t>(float x) { return f2h(x); }
+template <> __device__ __forceinline__ float cv<float, float>(float x) { return x; }
+template <> __device__ __forceinline__ double cv<float, double>(float x) { return f2d(x); }
+template <> __device__ __forceinline__ uint16_t cv<double, uint16_t>(double x) { return d2h(x); }
+template <> __device__ __forceinline__ float cv<double, float>(double x) { return d2f(x); }
+template <> __device__ __forceinline__ double cv<double, double>(double x) { return x; }
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256) batched_convert_kernel(const CopyItem* __restrict__ items,
+                                                              int64_t n) {
+    const CopyItem it = items[blockIdx.y];
+    const TI* __restrict__ src = static_cast<const TI*>(it.src);
+    TO* __restrict__ dst = static_cast<TO*>(it.dst);
+    const int64_t n4 = n / 4;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n4;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        TI a[4];
+        TO b[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a[k] = src[t * 4 + k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) b[k] = cv<TI, TO>(a[k]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dst[t * 4 + k] = b[k];
+    }
+    for (int64_t t = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x)
+        dst[t] = cv<TI, TO>(src[t]);
+}
+
+template <typename T>
+__global__ void batched_zero_kernel(void* const* __restrict__ ptrs, int64_t n) {
+    T* p = static_cast<T*>(ptrs[blockIdx.y]);
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x)
+        p[t] = T(0);
+}
+
+template <typename T>
+__global__ void batched_zero_upper_kernel(void* const* __restrict__ ptrs, int64_t nb) {
+    T* p = static_cast<T*>(ptrs[blockIdx.y]);
+    const int64_t total = nb * nb;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / nb, i = t - j * nb;
+        if (i < j) p[t] = T(0);
+    }
+}
+
+// Inverse of each 64x64 diagonal block of a lower-triangular FP64 matrix:
+// column c by forward substitution, all in shared memory.
+__global__ void __launch_bounds__(64) leaf_inverse_kernel(const double* __restrict__ L,
+                                                          int64_t ldl, int64_t n,
+                                                          double* __restrict__ Linv,
+                                                          int64_t ldi) {
+    __shared__ double D[64][65];
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 64;
+    const int bb = static_cast<int>(n - r0 < 64 ? n - r0 : 64);
+    for (int c = 0; c < 64; ++c) {
+        const int r = threadIdx.x;
+        D[r][c] = (r < bb && c < bb) ? L[(r0 + c) * ldl + r0 + r] : 0.0;
+    }
+    __syncthreads();
+    // column c of the inverse is private to thread c: written straight to
+    // Linv and re-read from there (L1-resident).
+    const int c = threadIdx.x;
+    if (c < bb) {
+        double* X = Linv + (r0 + c) * ldi + r0;
+        for (int i = 0; i < bb; ++i) {
+            double x = 0.0;
+            if (i >= c) {
+                double s = (i == c) ? 1.0 : 0.0;
+                for (int k = c; k < i; ++k) s -= D[i][k] * X[k];
+                x = s / D[i][i];
+            }
+            X[i] = x;
+        }
+    }
+}
+
+template <int P>
+using ST = typename Storage<P>::T;
+
+}  // namespace
+
+void launch_batched_convert(Ctx* ctx, cudaStream_t s, mp_precision pin, mp_precision pout,
+                            const CopyItem* dev_items, int64_t count, int64_t elems) {
+    if (count == 0 || elems == 0) return;
+    int gx = static_cast<int>((elems / 4 + 255) / 256);
+    const int cap = static_cast<int>(4 * ctx->sm_count / (count < 1 ? 1 : count)) + 1;
+    if (gx > cap) gx = cap;
+    if (gx < 1) gx = 1;
+    const dim3 grid(gx, static_cast<unsigned>(count));
+    ProfScope ps(ctx, MP_PROF_CAST, s,
+                 static_cast<double>(count) * elems * (elem_bytes(pin) + elem_bytes(pout)));
+#define MP_BC(PI, PO)                                                                      \
+    if (pin == PI && pout == PO) {                                                         \
+        batched_convert_kernel<ST<PI>, ST<PO>><<<grid, 256, 0, s>>>(dev_items, elems);     \
+    } else
+    MP_BC(0, 0) MP_BC(0, 1) MP_BC(0, 2) MP_BC(1, 0) MP_BC(1, 1) MP_BC(1, 2) MP_BC(2, 0)
+        MP_BC(2, 1) MP_BC(2, 2) fail(MP_INVALID_PARAM, "batched convert: precision");
+#undef MP_BC
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+void launch_batched_zero(Ctx* ctx, cudaStream_t s, mp_precision p, void* const* dev_ptrs,
+                         int64_t count, int64_t elems, bool upper_only, int64_t nb) {
+    if (count == 0) return;
+    int gx = static_cast<int>((elems + 255) / 256);
+    if (gx > 64) gx = 64;
+    const dim3 grid(gx, static_cast<unsigned>(count));
+    if (upper_only) {
+        if (p == MP_HALF) batched_zero_upper_kernel<uint16_t><<<grid, 256, 0, s>>>(dev_ptrs, nb);
+        else if (p == MP_SINGLE) batched_zero_upper_kernel<float><<<grid, 256, 0, s>>>(dev_ptrs, nb);
+        else batched_zero_upper_kernel<double><<<grid, 256, 0, s>>>(dev_ptrs, nb);
+    } else {
+        if (p == MP_HALF) batched_zero_kernel<uint16_t><<<grid, 256, 0, s>>>(dev_ptrs, elems);
+        else if (p == MP_SINGLE) batched_zero_kernel<float><<<grid, 256, 0, s>>>(dev_ptrs, elems);
+        else batched_zero_kernel<double><<<grid, 256, 0, s>>>(dev_ptrs, elems);
+    }
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+void launch_leaf_inverse(Ctx* ctx, cudaStream_t s, const double* L, int64_t ldl, int64_t n,
+                         double* Linv, int64_t ldi) {
+    const int nblk = static_cast<int>((n + 63) / 64);
+    leaf_inverse_kernel<<<nblk, 64, 0, s>>>(L, ldl, n, Linv, ldi);
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+}  // namespace mpcr

@@ -1,0 +1,22 @@
+// Host interface of the batched tile kernels (batch.cu).
+#pragma once
+
+#include "internal.hpp"
+
+namespace mpcr {
+
+struct CopyItem {
+    const void* src;
+    void* dst;
+};
+
+void launch_batched_convert(Ctx* ctx, cudaStream_t s, mp_precision pin, mp_precision pout,
+                            const CopyItem* dev_items, int64_t count, int64_t elems);
+void launch_batched_zero(Ctx* ctx, cudaStream_t s, mp_precision p, void* const* dev_ptrs,
+                         int64_t count, int64_t elems, bool upper_only, int64_t nb);
+// Leaf (64x64 diagonal block) inverses of a lower-triangular FP64 matrix,
+// written onto the diagonal blocks of Linv.
+void launch_leaf_inverse(Ctx* ctx, cudaStream_t s, const double* L, int64_t ldl, int64_t n,
+                         double* Linv, int64_t ldi);
+
+}  // namespace mpcr

@@ -1,0 +1,437 @@
+// Elementwise, reduction and layout kernels (array.cpp:228-429) plus the
+// small helpers the factorizations need.  All HBM-streaming, grid-stride,
+// grid sized to a multiple of the SM count.
+#include <cfloat>
+
+#include "device.cuh"
+#include "internal.hpp"
+
+namespace mpcr {
+namespace {
+
+template <int P>
+using ST = typename Storage<P>::T;
+
+// ---- ew_binary (array.cpp:252-272) ----------------------------------------
+template <int PA, int PB, int PO>
+__global__ void ew_binary_kernel(int op, const ST<PA>* __restrict__ a, int64_t lda,
+                                 const ST<PB>* __restrict__ b, int64_t ldb,
+                                 ST<PO>* __restrict__ o, int64_t ldo, int64_t rows,
+                                 int64_t cols) {
+    using C = typename std::conditional<PO == 2, double, float>::type;
+    const int64_t n = rows * cols;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / rows, i = t - j * rows;
+        const C x = load_as<C>(a, j * lda + i);
+        const C y = load_as<C>(b, j * ldb + i);
+        store_from(o, j * ldo + i, op_rn(op, x, y));
+    }
+}
+
+// ---- ew_scalar (array.cpp:274-291); y pre-rounded by the host ------------
+template <int P>
+__global__ void ew_scalar_kernel(int op, const ST<P>* __restrict__ a, int64_t lda,
+                                 ST<P>* __restrict__ o, int64_t ldo, int64_t rows,
+                                 int64_t cols, double yd) {
+    using C = typename std::conditional<P == 2, double, float>::type;
+    const C y = static_cast<C>(yd);
+    const int64_t n = rows * cols;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / rows, i = t - j * rows;
+        store_from(o, j * ldo + i, op_rn(op, load_as<C>(a, j * lda + i), y));
+    }
+}
+
+// ---- ew_unary (array.cpp:293-322) -----------------------------------------
+template <int P>
+__global__ void ew_unary_kernel(int op, const ST<P>* __restrict__ a, int64_t lda,
+                                ST<P>* __restrict__ o, int64_t ldo, int64_t rows,
+                                int64_t cols) {
+    const int64_t n = rows * cols;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / rows, i = t - j * rows;
+        if (P == 2) {
+            const double x = load_as<double>(a, j * lda + i);
+            double v;
+            switch (op) {
+                case 0: v = log(x); break;
+                case 1: v = exp(x); break;
+                case 2: v = __dsqrt_rn(x); break;
+                default: v = fabs(x); break;
+            }
+            store_from(o, j * ldo + i, v);
+        } else {
+            const double xd = load_as<double>(a, j * lda + i);
+            const float x = d2f(xd);
+            double v;
+            switch (op) {
+                case 0: v = f2d(logf(x)); break;
+                case 1: v = f2d(expf(x)); break;
+                case 2: v = f2d(__fsqrt_rn(x)); break;
+                default: v = fabs(xd); break;
+            }
+            store_from(o, j * ldo + i, v);
+        }
+    }
+}
+
+// ---- reduce (array.cpp:336-369): deterministic two-pass -------------------
+constexpr int kRedBlocks = 296;  // 2 x 148 SMs
+constexpr int kRedThreads = 256;
+
+struct MinMax {
+    double v;
+    int64_t i;
+};
+
+__device__ __forceinline__ MinMax better(MinMax a, MinMax b, bool is_min) {
+    // Sequential std::min/std::max keeps the earliest element among equals
+    // and never adopts a NaN after the first element.
+    if (b.i < 0) return a;
+    if (a.i < 0) return b;
+    const bool b_wins = is_min ? (b.v < a.v) : (a.v < b.v);
+    if (b_wins) return b;
+    if (!(a.v < b.v) && !(b.v < a.v) && b.i < a.i && b.v == b.v && a.v == a.v) return b;
+    return a;
+}
+
+template <int P>
+__global__ void __launch_bounds__(kRedThreads) reduce_pass1(int op, const ST<P>* __restrict__ a,
+                                                            int64_t lda, int64_t rows,
+                                                            int64_t cols, double* part,
+                                                            int64_t* part_i) {
+    const int64_t n = rows * cols;
+    const bool is_mm = (op == 2 || op == 3);
+    double acc = 0.0;
+    MinMax mm{0.0, -1};
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / rows, i = t - j * rows;
+        const double x = load_as<double>(a, j * lda + i);
+        if (is_mm) {
+            if (x == x) mm = better(mm, MinMax{x, t}, op == 2);
+        } else {
+            acc += (op == 1) ? x * x : x;
+        }
+    }
+    __shared__ double sacc[kRedThreads];
+    __shared__ double sv[kRedThreads];
+    __shared__ int64_t si[kRedThreads];
+    sacc[threadIdx.x] = acc;
+    sv[threadIdx.x] = mm.v;
+    si[threadIdx.x] = mm.i;
+    __syncthreads();
+    for (int w = kRedThreads / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            sacc[threadIdx.x] += sacc[threadIdx.x + w];
+            MinMax r = better(MinMax{sv[threadIdx.x], si[threadIdx.x]},
+                              MinMax{sv[threadIdx.x + w], si[threadIdx.x + w]}, op == 2);
+            sv[threadIdx.x] = r.v;
+            si[threadIdx.x] = r.i;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[blockIdx.x] = is_mm ? sv[0] : sacc[0];
+        part_i[blockIdx.x] = si[0];
+    }
+}
+
+__global__ void reduce_pass2(int op, const double* part, const int64_t* part_i, int nparts,
+                             double first, double* out) {
+    if (threadIdx.x != 0) return;
+    if (op == 2 || op == 3) {
+        MinMax mm{0.0, -1};
+        for (int b = 0; b < nparts; ++b) mm = better(mm, MinMax{part[b], part_i[b]}, op == 2);
+        // A leading NaN sticks (std::min/max never replace it); all-NaN -> NaN.
+        *out = (first != first || mm.i < 0) ? first : mm.v;
+    } else {
+        double acc = 0.0;
+        for (int b = 0; b < nparts; ++b) acc += part[b];
+        *out = acc;
+    }
+}
+
+// ---- transpose (array.cpp:422-429) via 32x33 smem tiles -------------------
+template <typename T>
+__global__ void transpose_kernel(const T* __restrict__ in, int64_t ldi, int64_t rows,
+                                 int64_t cols, T* __restrict__ out, int64_t ldo) {
+    __shared__ T tile[32][33];
+    const int64_t i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t i = i0 + threadIdx.x, j = j0 + r;
+        if (i < rows && j < cols) tile[r][threadIdx.x] = in[j * ldi + i];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t oi = j0 + threadIdx.x, oj = i0 + r;  // out is cols x rows
+        if (oi < cols && oj < rows) out[oj * ldo + oi] = tile[threadIdx.x][r];
+    }
+}
+
+template <typename T>
+__global__ void diag_kernel(const T* __restrict__ a, int64_t lda, int64_t n, T* __restrict__ o) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x)
+        o[t] = a[t * lda + t];
+}
+
+template <typename T>
+__global__ void fill_kernel(T* __restrict__ a, int64_t lda, int64_t rows, int64_t cols, T v) {
+    const int64_t n = rows * cols;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / rows, i = t - j * rows;
+        a[j * lda + i] = v;
+    }
+}
+
+template <typename T>
+__global__ void zero_triangle_kernel(T* __restrict__ a, int64_t lda, int64_t n, bool upper) {
+    const int64_t total = n * n;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / n, i = t - j * n;
+        if (upper ? (i < j) : (i > j)) a[j * lda + i] = T(0);
+    }
+}
+
+template <typename T>
+__global__ void mirror_lower_kernel(T* __restrict__ a, int64_t lda, int64_t n) {
+    const int64_t total = n * n;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / n, i = t - j * n;
+        if (i < j) a[j * lda + i] = a[i * lda + j];
+    }
+}
+
+template <int P>
+__global__ void logdiag_kernel(const ST<P>* __restrict__ a, int64_t lda, int64_t n,
+                               double* out) {
+    __shared__ double s[256];
+    double acc = 0.0;
+    for (int64_t t = threadIdx.x; t < n; t += blockDim.x) acc += log(load_as<double>(a, t * lda + t));
+    s[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) s[threadIdx.x] += s[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out += s[0];
+}
+
+// Matern closed forms (covariance.cpp:44-72) on a side x side unit grid with
+// x fastest (covariance.cpp:15-21); point p = (p % side, p / side)/(side-1).
+template <int P>
+__global__ void matern_kernel(ST<P>* __restrict__ dst, int64_t ld, int64_t row0, int64_t col0,
+                              int64_t rows, int64_t cols, int64_t side, double nu,
+                              double range, double var) {
+    const int64_t n = rows * cols;
+    const double inv = 1.0 / static_cast<double>(side - 1);
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / rows, i = t - j * rows;
+        const int64_t pi = row0 + i, pj = col0 + j;
+        const double xi = static_cast<double>(pi % side) * inv;
+        const double yi = static_cast<double>(pi / side) * inv;
+        const double xj = static_cast<double>(pj % side) * inv;
+        const double yj = static_cast<double>(pj / side) * inv;
+        // The reference divides i / (side - 1); replicate that rounding.
+        const double xi2 = static_cast<double>(pi % side) / static_cast<double>(side - 1);
+        const double yi2 = static_cast<double>(pi / side) / static_cast<double>(side - 1);
+        const double xj2 = static_cast<double>(pj % side) / static_cast<double>(side - 1);
+        const double yj2 = static_cast<double>(pj / side) / static_cast<double>(side - 1);
+        (void)xi;
+        (void)yi;
+        (void)xj;
+        (void)yj;
+        const double d = hypot(xi2 - xj2, yi2 - yj2);
+        double v;
+        if (nu == 0.5) {
+            v = var * exp(-d / range);
+        } else if (nu == 1.5) {
+            const double r = sqrt(3.0) * d / range;
+            v = var * (1.0 + r) * exp(-r);
+        } else {
+            const double r = sqrt(5.0) * d / range;
+            v = var * (1.0 + r + r * r / 3.0) * exp(-r);
+        }
+        store_from(dst, j * ld + i, v);
+    }
+}
+
+template <typename F>
+void dispatch_p(mp_precision p, F&& f) {
+    if (p == MP_HALF) f(std::integral_constant<int, 0>{});
+    else if (p == MP_SINGLE) f(std::integral_constant<int, 1>{});
+    else f(std::integral_constant<int, 2>{});
+}
+
+}  // namespace
+
+void launch_ew_binary(Ctx* ctx, cudaStream_t s, int op, const Array& a, const Array& b,
+                      Array& out) {
+    const int g = grid_for(a.size(), 256, ctx->sm_count);
+    dispatch_p(a.prec, [&](auto pa) {
+        dispatch_p(b.prec, [&](auto pb) {
+            constexpr int PA = decltype(pa)::value, PB = decltype(pb)::value;
+            constexpr int PO = PA > PB ? PA : PB;
+            ew_binary_kernel<PA, PB, PO><<<g, 256, 0, s>>>(
+                op, static_cast<const ST<PA>*>(a.data), a.ld, static_cast<const ST<PB>*>(b.data),
+                b.ld, static_cast<ST<PO>*>(out.data), out.ld, a.rows, a.cols);
+        });
+    });
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+void launch_ew_scalar(Ctx* ctx, cudaStream_t s, int op, const Array& a, double v, Array& out) {
+    const int g = grid_for(a.size(), 256, ctx->sm_count);
+    dispatch_p(a.prec, [&](auto pa) {
+        constexpr int P = decltype(pa)::value;
+        ew_scalar_kernel<P><<<g, 256, 0, s>>>(op, static_cast<const ST<P>*>(a.data), a.ld,
+                                             static_cast<ST<P>*>(out.data), out.ld, a.rows,
+                                             a.cols, v);
+    });
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+void launch_ew_unary(Ctx* ctx, cudaStream_t s, int op, const Array& a, Array& out) {
+    const int g = grid_for(a.size(), 256, ctx->sm_count);
+    dispatch_p(a.prec, [&](auto pa) {
+        constexpr int P = decltype(pa)::value;
+        ew_unary_kernel<P><<<g, 256, 0, s>>>(op, static_cast<const ST<P>*>(a.data), a.ld,
+                                            static_cast<ST<P>*>(out.data), out.ld, a.rows,
+                                            a.cols);
+    });
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+double run_reduce(Ctx* ctx, cudaStream_t s, int op, const Array& a) {
+    auto* part = static_cast<double*>(ctx->ensure_scratch(
+        kRedBlocks * (sizeof(double) + sizeof(int64_t)) + 64, 0));
+    auto* part_i = reinterpret_cast<int64_t*>(part + kRedBlocks);
+    double* out = reinterpret_cast<double*>(part_i + kRedBlocks);
+    double first = 0.0;
+    dispatch_p(a.prec, [&](auto pa) {
+        constexpr int P = decltype(pa)::value;
+        reduce_pass1<P><<<kRedBlocks, kRedThreads, 0, s>>>(op, static_cast<const ST<P>*>(a.data),
+                                                          a.ld, a.rows, a.cols, part, part_i);
+    });
+    // first element (for the NaN-stickiness rule of min/max), as a double
+    double* firstd = out + 1;
+    launch_convert(ctx, s, a.prec, a.data, 1, MP_DOUBLE, firstd, 1, 1, 1);
+    MP_CUDA(cudaMemcpyAsync(&first, firstd, sizeof(double), cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    reduce_pass2<<<1, 32, 0, s>>>(op, part, part_i, kRedBlocks, first, out);
+    count_launch(ctx, 2);
+    double r = 0.0;
+    MP_CUDA(cudaMemcpyAsync(&r, out, sizeof(double), cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    if (op == 4) r /= static_cast<double>(a.size());
+    return r;
+}
+
+void launch_transpose_raw(Ctx* ctx, cudaStream_t s, mp_precision p, const void* in,
+                          int64_t ldi, int64_t rows, int64_t cols, void* out, int64_t ldo) {
+    if (rows == 0 || cols == 0) return;
+    dim3 grid(static_cast<unsigned>((rows + 31) / 32), static_cast<unsigned>((cols + 31) / 32));
+    dim3 block(32, 8);
+    dispatch_p(p, [&](auto pp) {
+        constexpr int P = decltype(pp)::value;
+        transpose_kernel<ST<P>><<<grid, block, 0, s>>>(static_cast<const ST<P>*>(in), ldi, rows,
+                                                      cols, static_cast<ST<P>*>(out), ldo);
+    });
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+void launch_transpose(Ctx* ctx, cudaStream_t s, const Array& a, Array& out) {
+    launch_transpose_raw(ctx, s, a.prec, a.data, a.ld, a.rows, a.cols, out.data, out.ld);
+}
+
+void launch_diag(Ctx* ctx, cudaStream_t s, const Array& a, Array& out) {
+    const int64_t n = a.rows < a.cols ? a.rows : a.cols;
+    if (n == 0) return;
+    dispatch_p(a.prec, [&](auto pp) {
+        constexpr int P = decltype(pp)::value;
+        diag_kernel<ST<P>><<<grid_for(n, 256, ctx->sm_count), 256, 0, s>>>(
+            static_cast<const ST<P>*>(a.data), a.ld, n, static_cast<ST<P>*>(out.data));
+    });
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+void launch_fill(Ctx* ctx, cudaStream_t s, mp_precision p, void* dst, int64_t ld, int64_t rows,
+                 int64_t cols, double value) {
+    if (rows * cols == 0) return;
+    const int g = grid_for(rows * cols, 256, ctx->sm_count);
+    if (p == MP_HALF) {
+        // host-side encode of the constant (value is a plain literal here)
+        const __half h = __double2half(value);
+        fill_kernel<<<g, 256, 0, s>>>(static_cast<uint16_t*>(dst), ld, rows, cols,
+                                      *reinterpret_cast<const uint16_t*>(&h));
+    } else if (p == MP_SINGLE) {
+        fill_kernel<<<g, 256, 0, s>>>(static_cast<float*>(dst), ld, rows, cols,
+                                      static_cast<float>(value));
+    } else {
+        fill_kernel<<<g, 256, 0, s>>>(static_cast<double*>(dst), ld, rows, cols, value);
+    }
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+void launch_zero_triangle(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64_t lda,
+                          int64_t n, bool upper) {
+    if (n <= 1) return;
+    const int g = grid_for(n * n, 256, ctx->sm_count);
+    dispatch_p(p, [&](auto pp) {
+        constexpr int P = decltype(pp)::value;
+        zero_triangle_kernel<ST<P>><<<g, 256, 0, s>>>(static_cast<ST<P>*>(A), lda, n, upper);
+    });
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+void launch_mirror_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64_t lda,
+                         int64_t n) {
+    if (n <= 1) return;
+    const int g = grid_for(n * n, 256, ctx->sm_count);
+    dispatch_p(p, [&](auto pp) {
+        constexpr int P = decltype(pp)::value;
+        mirror_lower_kernel<ST<P>><<<g, 256, 0, s>>>(static_cast<ST<P>*>(A), lda, n);
+    });
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+void launch_logdiag_sum(Ctx* ctx, cudaStream_t s, mp_precision p, const void* A, int64_t lda,
+                        int64_t n, double* dev_out) {
+    dispatch_p(p, [&](auto pp) {
+        constexpr int P = decltype(pp)::value;
+        logdiag_kernel<P><<<1, 256, 0, s>>>(static_cast<const ST<P>*>(A), lda, n, dev_out);
+    });
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+void launch_matern_tile(Ctx* ctx, cudaStream_t s, mp_precision p, void* dst, int64_t ld,
+                        int64_t row0, int64_t col0, int64_t rows, int64_t cols, int64_t side,
+                        double nu, double range, double variance) {
+    const int g = grid_for(rows * cols, 256, ctx->sm_count);
+    dispatch_p(p, [&](auto pp) {
+        constexpr int P = decltype(pp)::value;
+        matern_kernel<P><<<g, 256, 0, s>>>(static_cast<ST<P>*>(dst), ld, row0, col0, rows, cols,
+                                           side, nu, range, variance);
+    });
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+}  // namespace mpcr

@@ -1,0 +1,56 @@
+// GEMM dispatch: picks the kernel family from the precisions
+// (linalg.cpp:340 branches on compute_precision(prec(C))).
+//   A, B half and C half/single  -> tcgen05 FP16 tensor cores (gemm_tc.cu)
+//   everything else              -> SIMT in C's compute type (gemm_simt.cu)
+#include "gemm_simt.hpp"
+#include "gemm_tc.hpp"
+#include "internal.hpp"
+
+namespace mpcr {
+
+void launch_gemm(Ctx* ctx, cudaStream_t s, const GemmDesc& g) {
+    if (g.m == 0 || g.n == 0) return;
+    if (g.pa == MP_HALF && g.pb == MP_HALF && (g.pc == MP_HALF || g.pc == MP_SINGLE) && g.k > 0) {
+        TcGemm t;
+        t.pc = g.pc;
+        t.ta = g.ta;
+        t.tb = g.tb;
+        t.m = g.m;
+        t.n = g.n;
+        t.k = g.k;
+        t.alpha = g.alpha;
+        t.beta = g.beta;
+        t.A = g.A;
+        t.lda = g.lda;
+        t.a_tile_stride = g.lda * (g.ta ? g.m : g.k);
+        t.B = g.B;
+        t.ldb = g.ldb;
+        t.b_tile_stride = g.ldb * (g.tb ? g.k : g.n);
+        t.C = g.C;
+        t.ldc = g.ldc;
+        t.lower_only = g.lower_only;
+        if (tc_gemm_supported(t)) {
+            launch_tc_gemm(ctx, s, t);
+            return;
+        }
+    }
+    SimtArgs a{g.pa, g.pb, g.pc, g.ta, g.tb, g.m, g.n, g.k, g.alpha, g.beta, g.A, g.lda,
+               g.B, g.ldb, g.C, g.ldc, g.lower_only, nullptr};
+    const int cls = g.pc == MP_DOUBLE ? MP_PROF_GEMM_F64
+                    : (g.pa == MP_HALF && g.pb == MP_HALF) ? MP_PROF_GEMM_F16
+                                                            : MP_PROF_GEMM_F32;
+    ProfScope ps(ctx, cls, s, 2.0 * g.m * g.n * g.k * (g.lower_only ? 0.5 : 1.0));
+    launch_gemm_simt(ctx, s, a, 1);
+}
+
+void launch_grouped_gemm(Ctx* ctx, cudaStream_t s, const GroupedGemm& g) {
+    if (g.count == 0) return;
+    SimtArgs a{g.pab, g.pab, g.pc, false, g.tb, g.m, g.n, g.k, g.alpha, g.beta, nullptr, g.lda,
+               nullptr, g.ldb, nullptr, g.ldc, false, g.problems};
+    const int cls = g.pc == MP_DOUBLE ? MP_PROF_GEMM_F64
+                    : g.pab == MP_HALF ? MP_PROF_GEMM_F16 : MP_PROF_GEMM_F32;
+    ProfScope ps(ctx, cls, s, 2.0 * g.m * g.n * g.k * g.count);
+    launch_gemm_simt(ctx, s, a, g.count);
+}
+
+}  // namespace mpcr

@@ -1,0 +1,350 @@
+// FP16 GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// Serves linalg::gemm / matmul / crossprod (linalg.cpp:316-357, :284-314) when
+// both operands are half and C is half or single (the reference computes
+// these in float, linalg.cpp:340-348; FP16 x FP16 products are exact in FP32
+// and the tensor core accumulates in FP32), and the FP16 trailing-update
+// tiles of the MPCRTile Cholesky (grouped, one launch per step).
+//
+// Structure (persistent, warp-specialised, one CTA per SM):
+//   warp 0      TMA producer: 4-stage ring of {A 128x64, B 256x64} FP16 tiles
+//               in 128B-swizzled shared memory, one mbarrier pair per stage.
+//   warp 1      MMA issuer: one elected thread issues tcgen05.mma
+//               (M=128, N=256, K=16) into a double-buffered TMEM accumulator
+//               (2 x 256 columns of FP32); tcgen05.commit frees smem stages
+//               and signals the epilogue.
+//   warp 2      TMEM allocator (512 columns).
+//   warps 4-7   epilogue: tcgen05.ld 32 lanes x 32 columns, C = alpha*acc +
+//               beta*C (beta == 0 never reads C), rounded to C's precision,
+//               coalesced column-major stores (lanes walk consecutive rows).
+// Operand majorness follows the column-major storage: op(A) = A is
+// MN-major, op(A) = A^T is K-major; op(B) = B is K-major, B^T MN-major.
+#include <cuda.h>
+
+#include <mutex>
+
+#include "device.cuh"
+#include "gemm_tc.hpp"
+#include "internal.hpp"
+#include "tc_ptx.cuh"
+
+namespace mpcr {
+namespace tc {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_STAGE = BM * BK * 2;  // 16 KB
+constexpr int B_STAGE = BN * BK * 2;  // 32 KB
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int TMEM_COLS = 512;
+
+struct Params {
+    CUtensorMap map_a;
+    CUtensorMap map_b;
+    const TcProblem* problems;  // nullptr -> use `single`
+    TcProblem single;
+    int32_t nprob;
+    int32_t M, N, K;
+    int64_t ldc;
+    float alpha, beta;
+    int32_t mblocks, nblocks, kblocks;
+};
+
+__device__ __forceinline__ bool skip_tile(const TcProblem& pr, int m0, int n0) {
+    return pr.lower_only && (m0 + BM - 1 < n0);
+}
+
+template <typename TC> __device__ __forceinline__ float load_c(const TC* c, int64_t i);
+template <> __device__ __forceinline__ float load_c<uint16_t>(const uint16_t* c, int64_t i) {
+    return h2f(c[i]);
+}
+template <> __device__ __forceinline__ float load_c<float>(const float* c, int64_t i) {
+    return c[i];
+}
+
+template <bool A_MN, bool B_MN, typename TC>
+__global__ void __launch_bounds__(256, 1) gemm_f16_tc_kernel(const __grid_constant__ Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_STAGE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&p.map_a);
+        ptx::tma_prefetch_desc(&p.map_b);
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            ptx::mbar_init(&tfull[s], 1);
+            ptx::mbar_init(&tempty[s], 128);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int tiles_per_prob = p.mblocks * p.nblocks;
+    const int64_t total = static_cast<int64_t>(p.nprob) * tiles_per_prob;
+
+    auto decode = [&](int64_t t, TcProblem& pr, int& m0, int& n0) {
+        const int64_t pi = t / tiles_per_prob;
+        const int r = static_cast<int>(t - pi * tiles_per_prob);
+        pr = p.problems ? p.problems[pi] : p.single;
+        m0 = (r % p.mblocks) * BM;
+        n0 = (r / p.mblocks) * BN;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+                TcProblem pr;
+                int m0, n0;
+                decode(t, pr, m0, n0);
+                if (skip_tile(pr, m0, n0)) continue;
+                for (int kb = 0; kb < p.kblocks; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full[stage], A_STAGE + B_STAGE);
+                    uint8_t* a_dst = sA + stage * A_STAGE;
+                    uint8_t* b_dst = sB + stage * B_STAGE;
+                    if (A_MN) {
+#pragma unroll
+                        for (int j = 0; j < BM / 64; ++j)
+                            ptx::tma_load_3d(a_dst + j * 8192, &p.map_a, &full[stage], m0 + j * 64,
+                                             kb * BK, pr.a_tile);
+                    } else {
+                        ptx::tma_load_3d(a_dst, &p.map_a, &full[stage], kb * BK, m0, pr.a_tile);
+                    }
+                    if (B_MN) {
+#pragma unroll
+                        for (int j = 0; j < BN / 64; ++j)
+                            ptx::tma_load_3d(b_dst + j * 8192, &p.map_b, &full[stage], n0 + j * 64,
+                                             kb * BK, pr.b_tile);
+                    } else {
+                        ptx::tma_load_3d(b_dst, &p.map_b, &full[stage], kb * BK, n0, pr.b_tile);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::umma_idesc(BM, BN, A_MN, B_MN, 0);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+                TcProblem pr;
+                int m0, n0;
+                decode(t, pr, m0, n0);
+                if (skip_tile(pr, m0, n0)) continue;
+                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+                for (int kb = 0; kb < p.kblocks; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a_base = ptx::smem_u32(sA + stage * A_STAGE);
+                    const uint32_t b_base = ptx::smem_u32(sB + stage * B_STAGE);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t ad = A_MN ? ptx::umma_desc_sw128(a_base + k * 2048, 8192, 1024)
+                                                 : ptx::umma_desc_sw128(a_base + k * 32, 0, 1024);
+                        const uint64_t bd = B_MN ? ptx::umma_desc_sw128(b_base + k * 2048, 8192, 1024)
+                                                 : ptx::umma_desc_sw128(b_base + k * 32, 0, 1024);
+                        ptx::mma_f16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                    }
+                    ptx::mma_commit(&empty[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                ptx::mma_commit(&tfull[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        const int q = warp - 4;
+        TC* __restrict__ Cbase = nullptr;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+            TcProblem pr;
+            int m0, n0;
+            decode(t, pr, m0, n0);
+            if (skip_tile(pr, m0, n0)) continue;
+            Cbase = static_cast<TC*>(pr.C);
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            const int row = m0 + q * 32 + lane;
+            const bool row_ok = row < p.M;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                ptx::tmem_ld_32x32b_x32(
+                    tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, r);
+                ptx::tmem_ld_wait();
+                const int nb = n0 + c * 32;
+                if (row_ok && nb < p.N) {
+                    float old[32];
+                    if (p.beta != 0.0f) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            old[j] = (nb + j < p.N) ? load_c(Cbase, (int64_t)(nb + j) * p.ldc + row)
+                                                    : 0.0f;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int col = nb + j;
+                        if (col < p.N && !(pr.lower_only && row < col)) {
+                            const float a = __fmul_rn(p.alpha, __uint_as_float(r[j]));
+                            const float v = p.beta != 0.0f ? __fadd_rn(a, __fmul_rn(p.beta, old[j])) : a;
+                            store_from(Cbase, (int64_t)col * p.ldc + row, v);
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&tempty[acc]);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
+    }
+}
+
+// ---- host side ---------------------------------------------------------------
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    if (!fn) fail(MP_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// 3-D map over [d2 tiles][d1][d0] 16-bit elements; d0 contiguous.
+void make_map(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+              uint64_t ld_elems, uint64_t tile_stride_elems, uint32_t box0, uint32_t box1) {
+    const cuuint64_t dims[3] = {d0, d1, d2};
+    const cuuint64_t strides[2] = {ld_elems * 2, tile_stride_elems * 2};
+    const cuuint32_t box[3] = {box0, box1, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = get_encode()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
+                                    const_cast<void*>(base), dims, strides, box, estr,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(MP_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+
+template <bool A_MN, bool B_MN, typename TC>
+void launch_kernel(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total) {
+    auto kern = gemm_f16_tc_kernel<A_MN, B_MN, TC>;
+    static bool configured = false;
+    if (!configured) {
+        MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        configured = true;
+    }
+    int grid = static_cast<int>(total < ctx->sm_count ? total : ctx->sm_count);
+    if (grid < 1) grid = 1;
+    kern<<<grid, 256, SMEM_BYTES, s>>>(p);
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+}  // namespace tc
+
+bool tc_gemm_supported(const TcGemm& g) {
+    // TMA: 16-byte aligned bases and leading strides.
+    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+    if (!al(g.A) || !al(g.B)) return false;
+    if ((g.lda * 2) % 16 || (g.ldb * 2) % 16) return false;
+    if (g.m < 1 || g.n < 1 || g.k < 1) return false;
+    if (g.m >= (1ll << 31) || g.n >= (1ll << 31) || g.k >= (1ll << 31)) return false;
+    return true;
+}
+
+void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
+    using namespace tc;
+    Params p;
+    memset(&p, 0, sizeof(p));
+    const bool a_mn = !g.ta, b_mn = g.tb;
+    // op(A): m x k.  MN-major: storage m x k (ld lda).  K-major: storage k x m.
+    if (a_mn)
+        make_map(&p.map_a, g.A, g.m, g.k, g.a_tiles, g.lda, g.a_tile_stride, 64, 64);
+    else
+        make_map(&p.map_a, g.A, g.k, g.m, g.a_tiles, g.lda, g.a_tile_stride, 64, BM);
+    if (b_mn)
+        make_map(&p.map_b, g.B, g.n, g.k, g.b_tiles, g.ldb, g.b_tile_stride, 64, 64);
+    else
+        make_map(&p.map_b, g.B, g.k, g.n, g.b_tiles, g.ldb, g.b_tile_stride, 64, BN);
+    p.problems = g.problems;
+    p.single = TcProblem{0, 0, g.lower_only ? 1 : 0, 0, g.C};
+    p.nprob = g.problems ? static_cast<int32_t>(g.count) : 1;
+    p.M = static_cast<int32_t>(g.m);
+    p.N = static_cast<int32_t>(g.n);
+    p.K = static_cast<int32_t>(g.k);
+    p.ldc = g.ldc;
+    p.alpha = static_cast<float>(g.alpha);
+    p.beta = static_cast<float>(g.beta);
+    p.mblocks = static_cast<int32_t>((g.m + BM - 1) / BM);
+    p.nblocks = static_cast<int32_t>((g.n + BN - 1) / BN);
+    p.kblocks = static_cast<int32_t>((g.k + BK - 1) / BK);
+    const int64_t total = static_cast<int64_t>(p.nprob) * p.mblocks * p.nblocks;
+    ProfScope ps(ctx, MP_PROF_GEMM_F16, s,
+                 2.0 * static_cast<double>(g.m) * g.n * g.k * p.nprob *
+                     (g.lower_only ? 0.5 : 1.0));
+#define MP_TC(AM, BMJ)                                                            \
+    if (a_mn == AM && b_mn == BMJ) {                                              \
+        if (g.pc == MP_HALF)                                                      \
+            launch_kernel<AM, BMJ, uint16_t>(ctx, s, p, total);                   \
+        else                                                                      \
+            launch_kernel<AM, BMJ, float>(ctx, s, p, total);                      \
+        return;                                                                   \
+    }
+    MP_TC(true, true)
+    MP_TC(true, false)
+    MP_TC(false, true)
+    MP_TC(false, false)
+#undef MP_TC
+}
+
+}  // namespace mpcr

@@ -1,0 +1,42 @@
+// Host interface of the tcgen05 FP16 GEMM (gemm_tc.cu).
+#pragma once
+
+#include <cstdint>
+
+#include "internal.hpp"
+
+namespace mpcr {
+
+// One problem of a grouped launch: operand tiles are indices into the
+// operand slabs' third TMA dimension; C is a direct pointer.
+struct TcProblem {
+    int32_t a_tile;
+    int32_t b_tile;
+    int32_t lower_only;
+    int32_t pad;
+    void* C;
+};
+
+// C <- alpha op(A) op(B) + beta C with FP16 A, B and half/single C.
+// Dense: a_tiles = b_tiles = 1, problems = nullptr.  Grouped: A and B are
+// slabs of `*_tiles` column-major tiles `*_tile_stride` elements apart.
+struct TcGemm {
+    mp_precision pc = MP_HALF;
+    bool ta = false, tb = false;
+    int64_t m = 0, n = 0, k = 0;
+    double alpha = 1.0, beta = 0.0;
+    const void* A = nullptr;
+    int64_t lda = 0, a_tiles = 1, a_tile_stride = 0;
+    const void* B = nullptr;
+    int64_t ldb = 0, b_tiles = 1, b_tile_stride = 0;
+    void* C = nullptr;
+    int64_t ldc = 0;
+    bool lower_only = false;
+    const TcProblem* problems = nullptr;
+    int64_t count = 0;
+};
+
+bool tc_gemm_supported(const TcGemm& g);
+void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g);
+
+}  // namespace mpcr

@@ -1,0 +1,204 @@
+// Internal types of the B200-native MPCR engine (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mpcr_b200.h"
+
+struct mp_tile_s;
+
+namespace mpcr {
+
+// Thrown inside the library, converted to mp_status at the C-ABI edge.
+struct Error : std::runtime_error {
+    mp_status status;
+    int64_t info;
+    Error(mp_status s, const std::string& msg, int64_t inf = -1)
+        : std::runtime_error(msg), status(s), info(inf) {}
+};
+
+[[noreturn]] inline void fail(mp_status s, const std::string& msg) { throw Error(s, msg); }
+
+#define MP_CUDA(expr)                                                                   \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            ::mpcr::fail(e_ == cudaErrorMemoryAllocation ? MP_OUT_OF_MEMORY : MP_CUDA_ERROR, \
+                         std::string(#expr) + ": " + cudaGetErrorString(e_));           \
+    } while (0)
+
+inline int elem_bytes(mp_precision p) { return p == MP_HALF ? 2 : p == MP_SINGLE ? 4 : 8; }
+inline mp_precision promote(mp_precision a, mp_precision b) { return a >= b ? a : b; }
+// array.hpp:109-111 — Half kernels compute in Single.
+inline mp_precision compute_precision(mp_precision p) { return p == MP_HALF ? MP_SINGLE : p; }
+inline const char* prec_name(mp_precision p) {
+    return p == MP_HALF ? "half" : p == MP_SINGLE ? "single" : "double";
+}
+
+struct Ctx;
+
+// Event-pair profiler per kernel class (mp_prof_*).
+struct Prof {
+    bool enabled = false;
+    struct Rec {
+        cudaEvent_t a, b;
+        int cls;
+        double work;
+    };
+    std::vector<Rec> pending;
+    std::vector<cudaEvent_t> pool;
+    double ms[MP_PROF_NUM_CLASSES] = {};
+    int64_t launches[MP_PROF_NUM_CLASSES] = {};
+    double work[MP_PROF_NUM_CLASSES] = {};
+};
+
+struct Ctx {
+    int device = 0;
+    int sm_count = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;   // current (own or external)
+    cudaStream_t aux[4] = {};        // scheduler side streams
+    cudaStream_t hi = nullptr;       // high-priority critical-path stream
+    int64_t launches = 0;            // kernels launched by this library
+    Prof prof;
+    // Scratch device memory (grown on demand, freed with the context).
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    void* scratch2 = nullptr;
+    size_t scratch2_bytes = 0;
+    void* ensure_scratch(size_t bytes, int which = 0);
+};
+
+struct Array {
+    Ctx* ctx = nullptr;
+    mp_precision prec = MP_DOUBLE;
+    int64_t rows = 0, cols = 0, ld = 0;
+    bool is_matrix = false;
+    bool owner = true;
+    void* data = nullptr;
+    int64_t size() const { return rows * cols; }
+    size_t bytes() const { return static_cast<size_t>(ld * cols) * elem_bytes(prec); }
+};
+
+// Begin/end an event-timed region for kernel class `cls` on `s`.
+struct ProfScope {
+    Ctx* ctx;
+    int cls;
+    cudaStream_t s;
+    double work;
+    cudaEvent_t a = nullptr;
+    ProfScope(Ctx* c, int k, cudaStream_t st, double w);
+    ~ProfScope();
+};
+
+void prof_collect(Ctx* ctx);  // drain pending event pairs (syncs them)
+
+// ---- kernels (each returns after enqueueing on stream s) -----------------
+// casts: cast.cu
+void launch_convert(Ctx* ctx, cudaStream_t s, mp_precision pin, const void* src, int64_t lds,
+                    mp_precision pout, void* dst, int64_t ldd, int64_t rows, int64_t cols);
+void launch_from_doubles(Ctx* ctx, cudaStream_t s, const double* src, mp_precision pout,
+                         void* dst, int64_t n);
+// ew.cu
+void launch_ew_binary(Ctx* ctx, cudaStream_t s, int op, const Array& a, const Array& b,
+                      Array& out);
+void launch_ew_scalar(Ctx* ctx, cudaStream_t s, int op, const Array& a, double v, Array& out);
+void launch_ew_unary(Ctx* ctx, cudaStream_t s, int op, const Array& a, Array& out);
+double run_reduce(Ctx* ctx, cudaStream_t s, int op, const Array& a);
+void launch_transpose(Ctx* ctx, cudaStream_t s, const Array& a, Array& out);
+void launch_diag(Ctx* ctx, cudaStream_t s, const Array& a, Array& out);
+void launch_fill(Ctx* ctx, cudaStream_t s, mp_precision p, void* dst, int64_t ld,
+                 int64_t rows, int64_t cols, double value);
+
+// GEMM: gemm.cu.  Dense column-major C <- alpha op(A) op(B) + beta C, computed
+// in compute_precision(pc).  lower_only: skip C entries strictly above the
+// diagonal (SYRK on the lower triangle).
+struct GemmDesc {
+    mp_precision pa, pb, pc;
+    bool ta, tb;
+    int64_t m, n, k;
+    double alpha, beta;
+    const void* A;
+    int64_t lda;
+    const void* B;
+    int64_t ldb;
+    void* C;
+    int64_t ldc;
+    bool lower_only = false;
+};
+void launch_gemm(Ctx* ctx, cudaStream_t s, const GemmDesc& g);
+
+// Grouped tile GEMM used by the MPCRTile scheduler: every problem is
+// C_p <- alpha A_p op(B_p) + beta C_p with identical shapes.
+struct TileProblem {
+    const void* A;  // m x k, column-major, lda
+    const void* B;  // (tb ? n x k : k x n), column-major, ldb
+    void* C;        // m x n, column-major, ldc
+    int32_t lower_only;
+    int32_t pad;
+};
+struct GroupedGemm {
+    mp_precision pab;   // operand precision (A and B)
+    mp_precision pc;    // output precision
+    bool tb;            // B transposed (the tiled-chol update is NT)
+    int64_t m, n, k, lda, ldb, ldc;
+    double alpha, beta;
+    const TileProblem* problems;  // device array
+    int64_t count;
+    // Optional: all operand tiles are slices of one slab (enables TMA maps).
+    const void* slab = nullptr;
+    int64_t slab_tiles = 0;
+};
+void launch_grouped_gemm(Ctx* ctx, cudaStream_t s, const GroupedGemm& g);
+
+// Cholesky / triangular kernels: potrf.cu, trsm.cu
+// In-place lower Cholesky of a column-major n x n matrix (compute in the
+// compute precision of p); writes the failing column (or -1) to dev_info.
+void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64_t lda,
+                        int64_t n, int64_t* dev_info, int64_t info_offset);
+// Inverse of a lower triangular FP64 matrix, out of place.  The strictly
+// upper part of Linv is written with zeros.
+void launch_trtri_lower(Ctx* ctx, cudaStream_t s, const double* L, int64_t ldl, double* Linv,
+                        int64_t ldi, int64_t n);
+// General triangular solve (linalg.cpp:130-159 semantics): op(T) X = B for
+// every column of B (in place), computing in compute type of pb.
+void launch_tri_solve(Ctx* ctx, cudaStream_t s, mp_precision pt, const void* T, int64_t ldt,
+                      int64_t n, bool upper, bool trans, mp_precision pb, void* B,
+                      int64_t ldb, int64_t ncols, double alpha, bool right_side,
+                      int64_t brows);
+// Scan the diagonal of T for exact zeros; returns first index or -1 (syncs).
+int64_t find_zero_diag(Ctx* ctx, cudaStream_t s, mp_precision p, const void* T, int64_t ldt,
+                       int64_t n, mp_precision compute);
+// Zero the strictly-upper (upper=true) or strictly-lower part.
+void launch_zero_triangle(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64_t lda,
+                          int64_t n, bool upper);
+// out = in^T for square or rectangular (generic, precision preserving).
+void launch_transpose_raw(Ctx* ctx, cudaStream_t s, mp_precision p, const void* in,
+                          int64_t ldi, int64_t rows, int64_t cols, void* out, int64_t ldo);
+// Mirror the lower triangle into the upper (exact symmetry).
+void launch_mirror_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64_t lda,
+                         int64_t n);
+// sum of log(diag) over n entries with stride (double accumulate) into dev_out.
+void launch_logdiag_sum(Ctx* ctx, cudaStream_t s, mp_precision p, const void* A, int64_t lda,
+                        int64_t n, double* dev_out);
+// Matern fill of a column-major tile block.
+void launch_matern_tile(Ctx* ctx, cudaStream_t s, mp_precision p, void* dst, int64_t ld,
+                        int64_t row0, int64_t col0, int64_t rows, int64_t cols,
+                        int64_t side, double nu, double range, double variance);
+
+inline void count_launch(Ctx* ctx, int n = 1) { ctx->launches += n; }
+
+extern thread_local std::string g_last_error;
+double host_round(double x, mp_precision p);
+int64_t tile_chol_inplace(Ctx* c, ::mp_tile_s& t);
+
+}  // namespace mpcr
+
+struct mp_ctx_s : mpcr::Ctx {};
+struct mp_array_s : mpcr::Array {};

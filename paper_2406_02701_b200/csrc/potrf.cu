@@ -1,0 +1,396 @@
+// Cholesky (POTRF), triangular inverse (TRTRI) and triangular solve kernels.
+//
+// POTRF: one cooperative launch per matrix/tile.  Right-looking, 64-wide
+// blocks; per block step three phases separated by a grid barrier:
+//   1. CTA 0 factors the 64x64 diagonal block in shared memory (checking the
+//      pivots exactly like chol_kernel's `!(d > 0)`, linalg.cpp:121) and
+//      inverts it (kept in `dinv` for the panel and for TRTRI);
+//   2. panel rows below: X = A_panel * inv(L_kk)^T, one 64-row block per CTA;
+//   3. trailing SYRK/GEMM update of the lower triangle, 64x64 blocks.
+// The failing pivot is reported as the 0-based column (errors.hpp:25-31);
+// every CTA stops at the next barrier.
+//
+// TRTRI: recursive 2x2 block inverse inv([[A,0],[B,C]]) = [[A^-1,0],
+// [-C^-1 B A^-1, C^-1]] on top of POTRF's 64x64 leaf inverses, each level one
+// grouped FP64 GEMM pair.  The MPCRTile scheduler turns the panel TRSM into a
+// tensor-core GEMM with this inverse (see tile.cpp).
+#include <cooperative_groups.h>
+
+#include <type_traits>
+#include <vector>
+
+#include "batch.hpp"
+#include "device.cuh"
+#include "internal.hpp"
+
+namespace mpcr {
+namespace {
+
+constexpr int PB = 64;   // block size
+constexpr int PT = 256;  // threads per CTA
+
+struct GridBar {
+    unsigned int count;
+    unsigned int gen;
+};
+
+__device__ __forceinline__ void grid_sync(GridBar* bar, unsigned int nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned int* vgen = &bar->gen;
+        const unsigned int g = *vgen;
+        __threadfence();
+        if (atomicAdd(&bar->count, 1u) == nblocks - 1) {
+            atomicExch(&bar->count, 0u);
+            __threadfence();
+            atomicAdd(&bar->gen, 1u);
+        } else {
+            while (*vgen == g) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// acc(64x64 per CTA, 4x4 per thread) += P (64 x kk, ldp) * Q (64 x kk, ldq)^T
+// with P/Q rows limited to pr/qr valid rows.
+template <typename T>
+__device__ __forceinline__ void block_nt(T (&acc)[4][4], const T* P, int64_t ldp, int pr,
+                                         const T* Q, int64_t ldq, int qr, int kk,
+                                         T (*Ps)[PB + 1], T (*Qs)[PB + 1]) {
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    for (int k0 = 0; k0 < kk; k0 += 16) {
+        for (int idx = threadIdx.x; idx < 16 * PB; idx += PT) {
+            const int r = idx % PB, c = idx / PB;
+            const int k = k0 + c;
+            Ps[c][r] = (r < pr && k < kk) ? P[k * ldp + r] : T(0);
+            Qs[c][r] = (r < qr && k < kk) ? Q[k * ldq + r] : T(0);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+            T a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = Ps[c][tx + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = Qs[c][ty + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(PT) potrf_coop_kernel(T* A, int64_t lda, int n, T* dinv,
+                                                        int64_t* info, int64_t info_off,
+                                                        GridBar* bar, int* abort_flag) {
+    // phase 1 (diagonal block) and phases 2/3 (panel blocks) never overlap
+    __shared__ union {
+        T d[PB][PB + 1];
+        struct {
+            T p[16][PB + 1];
+            T q[16][PB + 1];
+        } pq;
+    } sm;
+    auto& D = sm.d;
+    auto& Ps = sm.pq.p;
+    auto& Qs = sm.pq.q;
+    __shared__ int s_fail;
+    const int nblk = (n + PB - 1) / PB;
+    const unsigned int G = gridDim.x;
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+
+    for (int kb = 0; kb < nblk; ++kb) {
+        const int k0 = kb * PB;
+        const int bb = min(PB, n - k0);
+        // ---- phase 1: diagonal block -----------------------------------
+        if (blockIdx.x == 0) {
+            if (threadIdx.x == 0) s_fail = -1;
+            for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
+                const int r = idx % PB, c = idx / PB;
+                D[r][c] = (r < bb && c < bb && r >= c) ? A[(int64_t)(k0 + c) * lda + k0 + r] : T(0);
+            }
+            __syncthreads();
+            for (int j = 0; j < bb; ++j) {
+                // pivot (every thread reads the same value)
+                const T d = D[j][j];
+                if (!(d > T(0))) {
+                    if (threadIdx.x == 0) s_fail = j;
+                    __syncthreads();
+                    break;
+                }
+                const T sd = sqrt(d);
+                __syncthreads();
+                if (threadIdx.x == 0) D[j][j] = sd;
+                for (int i = j + 1 + threadIdx.x; i < bb; i += PT) D[i][j] = D[i][j] / sd;
+                __syncthreads();
+                // rank-1 update of the trailing lower triangle
+                const int rem = bb - j - 1;
+                for (int idx = threadIdx.x; idx < rem * rem; idx += PT) {
+                    const int i = j + 1 + idx % rem, l = j + 1 + idx / rem;
+                    if (i >= l) D[i][l] -= D[i][j] * D[l][j];
+                }
+                __syncthreads();
+            }
+            if (s_fail >= 0) {
+                if (threadIdx.x == 0) {
+                    if (*info < 0) *info = info_off + k0 + s_fail;
+                    atomicExch(abort_flag, 1);
+                }
+            } else {
+                // write L_kk back (lower part only)
+                for (int idx = threadIdx.x; idx < bb * bb; idx += PT) {
+                    const int r = idx % bb, c = idx / bb;
+                    if (r >= c) A[(int64_t)(k0 + c) * lda + k0 + r] = D[r][c];
+                }
+                // inverse of the lower-triangular block: column c by forward
+                // substitution (one thread per column), into dinv[kb] (64x64).
+                T* Di = dinv + (int64_t)kb * PB * PB;
+                if (threadIdx.x < PB) {
+                    const int c = threadIdx.x;
+                    for (int i = 0; i < PB; ++i) {
+                        T x = T(0);
+                        if (c < bb && i < bb && i >= c) {
+                            T s = (i == c) ? T(1) : T(0);
+                            for (int k = c; k < i; ++k) s -= D[i][k] * Di[c * PB + k];
+                            x = s / D[i][i];
+                        }
+                        Di[c * PB + i] = x;
+                    }
+                }
+            }
+        }
+        grid_sync(bar, G);
+        if (*(volatile int*)abort_flag) return;
+        // ---- phase 2: panel X = A_panel * Dinv^T ------------------------
+        const T* Di = dinv + (int64_t)kb * PB * PB;
+        for (int ib = kb + 1 + blockIdx.x; ib < nblk; ib += G) {
+            const int r0 = ib * PB, rb = min(PB, n - r0);
+            T acc[4][4] = {};
+            // acc = P (rb x bb) * Di^T where Di is bb x bb (ld PB)
+            block_nt(acc, A + (int64_t)k0 * lda + r0, lda, rb, Di, PB, bb, bb, Ps, Qs);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int r = tx + 16 * i, c = ty + 16 * j;
+                    if (r < rb && c < bb) A[(int64_t)(k0 + c) * lda + r0 + r] = acc[i][j];
+                }
+            __syncthreads();
+        }
+        grid_sync(bar, G);
+        // ---- phase 3: trailing update, lower triangle ---------------------
+        const int rest = nblk - kb - 1;
+        const int items = rest * (rest + 1) / 2;
+        for (int it = blockIdx.x; it < items; it += G) {
+            // map it -> (ib >= jb) over the trailing blocks
+            int jj = 0, rem = it;
+            while (rem >= rest - jj) {
+                rem -= rest - jj;
+                ++jj;
+            }
+            const int jb = kb + 1 + jj, ib = jb + rem;
+            const int r0 = ib * PB, c0 = jb * PB;
+            const int rb = min(PB, n - r0), cb = min(PB, n - c0);
+            T acc[4][4] = {};
+            block_nt(acc, A + (int64_t)k0 * lda + r0, lda, rb, A + (int64_t)k0 * lda + c0, lda,
+                     cb, bb, Ps, Qs);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int r = tx + 16 * i, c = ty + 16 * j;
+                    if (r < rb && c < cb && (ib != jb || r >= c)) {
+                        T* p = A + (int64_t)(c0 + c) * lda + r0 + r;
+                        *p = *p - acc[i][j];
+                    }
+                }
+            __syncthreads();
+        }
+        grid_sync(bar, G);
+    }
+}
+
+// ---- triangular solve (linalg.cpp:130-159), one thread per RHS vector ----
+// Left:  op(T) x = alpha b for every column of B (rows n).
+// Right: x op(T) = alpha b for every row of B, i.e. op(T)^T x^T = alpha b^T.
+template <typename TT, typename TB, typename Acc>
+__global__ void tri_solve_kernel(const TT* __restrict__ Tm, int64_t ldt, int64_t n, bool upper,
+                                 bool trans, TB* __restrict__ B, int64_t ldb, int64_t nvec,
+                                 Acc alpha, bool right) {
+    const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (v >= nvec) return;
+    // element k of vector v
+    auto bidx = [&](int64_t k) { return right ? k * ldb + v : v * ldb + k; };
+    const bool tr = right ? !trans : trans;
+    auto coef = [&](int64_t i, int64_t k) {
+        return load_as<Acc>(Tm, tr ? i * ldt + k : k * ldt + i);
+    };
+    const bool eff_lower = (upper == tr);
+    if (eff_lower) {
+        for (int64_t i = 0; i < n; ++i) {
+            Acc acc = load_as<Acc>(B, bidx(i)) * alpha;
+            for (int64_t k = 0; k < i; ++k) acc -= coef(i, k) * load_as<Acc>(B, bidx(k));
+            store_from(B, bidx(i), acc / coef(i, i));
+        }
+    } else {
+        for (int64_t i = n; i-- > 0;) {
+            Acc acc = load_as<Acc>(B, bidx(i)) * alpha;
+            for (int64_t k = i + 1; k < n; ++k) acc -= coef(i, k) * load_as<Acc>(B, bidx(k));
+            store_from(B, bidx(i), acc / coef(i, i));
+        }
+    }
+}
+
+template <typename TT, typename Acc>
+__global__ void zero_diag_kernel(const TT* __restrict__ Tm, int64_t ldt, int64_t n,
+                                 unsigned long long* first) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (load_as<Acc>(Tm, i * ldt + i) == Acc(0)) atomicMin(first, (unsigned long long)i);
+}
+
+template <int P>
+using ST = typename Storage<P>::T;
+
+template <typename F>
+void dispatch_p(mp_precision p, F&& f) {
+    if (p == MP_HALF) f(std::integral_constant<int, 0>{});
+    else if (p == MP_SINGLE) f(std::integral_constant<int, 1>{});
+    else f(std::integral_constant<int, 2>{});
+}
+
+}  // namespace
+
+void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64_t lda,
+                        int64_t n, int64_t* dev_info, int64_t info_offset) {
+    if (p == MP_HALF) fail(MP_INVALID_PARAM, "potrf: half storage must be widened first");
+    if (n == 0) return;
+    const int nblk = static_cast<int>((n + PB - 1) / PB);
+    // scratch: barrier + abort flag + leaf inverses (kept for TRTRI)
+    const size_t elem = p == MP_DOUBLE ? 8 : 4;
+    const size_t dinv_bytes = static_cast<size_t>(nblk) * PB * PB * elem;
+    char* scr = static_cast<char*>(ctx->ensure_scratch(256 + dinv_bytes, 1));
+    MP_CUDA(cudaMemsetAsync(scr, 0, 256, s));
+    GridBar* bar = reinterpret_cast<GridBar*>(scr);
+    int* abort_flag = reinterpret_cast<int*>(scr + 64);
+    void* dinv = scr + 256;
+    int grid = nblk * (nblk + 1) / 2;
+    if (grid > ctx->sm_count) grid = ctx->sm_count;
+    if (grid < 1) grid = 1;
+    int ni = static_cast<int>(n);
+    ProfScope ps(ctx, MP_PROF_POTRF, s, static_cast<double>(n) * n * n / 3.0);
+    if (p == MP_DOUBLE) {
+        double* a = static_cast<double*>(A);
+        double* d = static_cast<double*>(dinv);
+        void* args[] = {&a, &lda, &ni, &d, &dev_info, &info_offset, &bar, &abort_flag};
+        MP_CUDA(cudaLaunchCooperativeKernel((void*)potrf_coop_kernel<double>, grid, PT, args, 0, s));
+    } else {
+        float* a = static_cast<float*>(A);
+        float* d = static_cast<float*>(dinv);
+        void* args[] = {&a, &lda, &ni, &d, &dev_info, &info_offset, &bar, &abort_flag};
+        MP_CUDA(cudaLaunchCooperativeKernel((void*)potrf_coop_kernel<float>, grid, PT, args, 0, s));
+    }
+    count_launch(ctx);
+}
+
+// Inverse of a lower-triangular FP64 matrix: leaf inverses, then the
+// recursive 2x2 block formula level by level (grouped FP64 GEMMs).
+void launch_trtri_lower(Ctx* ctx, cudaStream_t s, const double* L, int64_t ldl, double* Linv,
+                        int64_t ldi, int64_t n) {
+    launch_fill(ctx, s, MP_DOUBLE, Linv, ldi, n, n, 0.0);
+    launch_leaf_inverse(ctx, s, L, ldl, n, Linv, ldi);
+    // T workspace: up to n/2 x n/2 per level problem set; sized n*n/2 total.
+    double* T = static_cast<double*>(ctx->ensure_scratch(static_cast<size_t>(n) * n * sizeof(double), 0));
+    std::vector<TileProblem> p1, p2;
+    TileProblem* dprob = reinterpret_cast<TileProblem*>(T + static_cast<size_t>(n) * n / 2 + 64);
+    for (int64_t sz = 2 * PB; sz / 2 < n; sz *= 2) {
+        const int64_t h = sz / 2;
+        p1.clear();
+        p2.clear();
+        int64_t toff = 0;
+        // uniform problems (full h x h lower-right) and one ragged tail
+        struct Rag {
+            int64_t r, rows2;
+        };
+        std::vector<Rag> rag;
+        for (int64_t r = 0; r + h < n; r += sz) {
+            const int64_t rows2 = (n - r - h) < h ? (n - r - h) : h;
+            if (rows2 == h) {
+                // T = B * Ainv (h x h), Linv21 = -Cinv * T
+                p1.push_back(TileProblem{L + r * ldl + r + h, Linv + r * ldi + r, T + toff, 0, 0});
+                p2.push_back(TileProblem{Linv + (r + h) * ldi + r + h, T + toff, Linv + r * ldi + r + h, 0, 0});
+                toff += h * h;
+            } else {
+                rag.push_back({r, rows2});
+            }
+        }
+        if (!p1.empty()) {
+            const int64_t cnt = static_cast<int64_t>(p1.size());
+            MP_CUDA(cudaMemcpyAsync(dprob, p1.data(), cnt * sizeof(TileProblem), cudaMemcpyHostToDevice, s));
+            MP_CUDA(cudaMemcpyAsync(dprob + cnt, p2.data(), cnt * sizeof(TileProblem), cudaMemcpyHostToDevice, s));
+            GroupedGemm g1{MP_DOUBLE, MP_DOUBLE, false, h, h, h, ldl, ldi, h, 1.0, 0.0, dprob, cnt};
+            launch_grouped_gemm(ctx, s, g1);
+            GroupedGemm g2{MP_DOUBLE, MP_DOUBLE, false, h, h, h, ldi, h, ldi, -1.0, 0.0, dprob + cnt, cnt};
+            launch_grouped_gemm(ctx, s, g2);
+            // host vectors must outlive the async copies
+            MP_CUDA(cudaStreamSynchronize(s));
+        }
+        for (const Rag& rg : rag) {
+            const int64_t r = rg.r, rows2 = rg.rows2;
+            GemmDesc g1{MP_DOUBLE, MP_DOUBLE, MP_DOUBLE, false, false, rows2, h, h, 1.0, 0.0,
+                        L + r * ldl + r + h, ldl, Linv + r * ldi + r, ldi, T, rows2};
+            launch_gemm(ctx, s, g1);
+            GemmDesc g2{MP_DOUBLE, MP_DOUBLE, MP_DOUBLE, false, false, rows2, h, rows2, -1.0, 0.0,
+                        Linv + (r + h) * ldi + r + h, ldi, T, rows2, Linv + r * ldi + r + h, ldi};
+            launch_gemm(ctx, s, g2);
+        }
+    }
+}
+
+void launch_tri_solve(Ctx* ctx, cudaStream_t s, mp_precision pt, const void* T, int64_t ldt,
+                      int64_t n, bool upper, bool trans, mp_precision pb, void* B, int64_t ldb,
+                      int64_t ncols, double alpha, bool right_side, int64_t brows) {
+    const int64_t nvec = right_side ? brows : ncols;
+    if (nvec == 0 || n == 0) return;
+    const int threads = 128;
+    const int grid = static_cast<int>((nvec + threads - 1) / threads);
+    ProfScope ps(ctx, MP_PROF_TRSM, s, static_cast<double>(n) * n * nvec);
+    dispatch_p(pt, [&](auto ptt) {
+        dispatch_p(pb, [&](auto pbb) {
+            constexpr int PT_ = decltype(ptt)::value, PB_ = decltype(pbb)::value;
+            using Acc = typename std::conditional<PB_ == 2, double, float>::type;
+            tri_solve_kernel<ST<PT_>, ST<PB_>, Acc><<<grid, threads, 0, s>>>(
+                static_cast<const ST<PT_>*>(T), ldt, n, upper, trans, static_cast<ST<PB_>*>(B),
+                ldb, nvec, static_cast<Acc>(alpha), right_side);
+        });
+    });
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+int64_t find_zero_diag(Ctx* ctx, cudaStream_t s, mp_precision p, const void* T, int64_t ldt,
+                       int64_t n, mp_precision compute) {
+    auto* first = static_cast<unsigned long long*>(ctx->ensure_scratch(64, 0));
+    const unsigned long long init = ~0ull;
+    MP_CUDA(cudaMemcpyAsync(first, &init, sizeof(init), cudaMemcpyHostToDevice, s));
+    dispatch_p(p, [&](auto pp) {
+        constexpr int P = decltype(pp)::value;
+        if (compute == MP_DOUBLE)
+            zero_diag_kernel<ST<P>, double><<<grid_for(n, 256, ctx->sm_count), 256, 0, s>>>(
+                static_cast<const ST<P>*>(T), ldt, n, first);
+        else
+            zero_diag_kernel<ST<P>, float><<<grid_for(n, 256, ctx->sm_count), 256, 0, s>>>(
+                static_cast<const ST<P>*>(T), ldt, n, first);
+    });
+    count_launch(ctx);
+    unsigned long long r = 0;
+    MP_CUDA(cudaMemcpyAsync(&r, first, sizeof(r), cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    return r == ~0ull ? -1 : static_cast<int64_t>(r);
+}
+
+}  // namespace mpcr

@@ -1,0 +1,676 @@
+// MPCRTile on the device, and its mixed-precision tiled
+// Cholesky scheduler.
+//
+// Storage: one slab per precision; every tile is one contiguous
+// rows_per_tile x cols_per_tile column-major buffer inside the slab of its
+// precision (so a single 3-D TMA map addresses every FP16 tile).
+//
+// Tiled Cholesky (right-looking, lower), per step k — the device version of
+// the reference composition in oracle/ref_shim.cpp:ref_tile_chol:
+//   1. POTRF of A_kk in its compute precision (cooperative kernel), then
+//      TRTRI of the stored factor in FP64 -> Linv.
+//   2. Linv rounded once to each panel precision present.
+//   3. TRSM as GEMM: L_ik = A_ik * Linv^T in p_ik (tcgen05 FP16 for half
+//      tiles), written to the panel buffer of p_ik and back to the tile.
+//   4. Panel tiles converted once to every precision their consumers need
+//      (A_ik.converted(p_ij) of the reference composition).
+//   5. Trailing update A_ij -= L_ik L_jk^T, one grouped launch per precision
+//      (lower triangle only on diagonal tiles).
+// All per-step work lists are built on the host once per factorization and
+// uploaded in one copy; the step loop is launch-only (no host sync).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "batch.hpp"
+#include "gemm_tc.hpp"
+#include "internal.hpp"
+
+using namespace mpcr;
+
+struct mp_tile_s {
+    Ctx* ctx = nullptr;
+    int64_t rows = 0, cols = 0, br = 0, bc = 0, tr = 0, tc = 0;
+    std::vector<mp_precision> prec;  // tile (i, j) at j * tr + i
+    std::vector<int64_t> slot;
+    void* slab[3] = {nullptr, nullptr, nullptr};
+    int64_t nslot[3] = {0, 0, 0};
+    // scheduler workspace (grown on demand)
+    void* panel[3] = {nullptr, nullptr, nullptr};
+    void* work = nullptr;  // FP64 nb x nb x 2 + FP32 nb x nb + Linv{H,S}
+    void* lists = nullptr;
+    size_t lists_bytes = 0;
+
+    int64_t tt() const { return br * bc; }
+    mp_precision p(int64_t i, int64_t j) const { return prec[j * tr + i]; }
+    void* ptr(int64_t i, int64_t j) const {
+        const mp_precision q = p(i, j);
+        return static_cast<char*>(slab[q]) + slot[j * tr + i] * tt() * elem_bytes(q);
+    }
+    void* panel_ptr(mp_precision q, int64_t i) const {
+        return static_cast<char*>(panel[q]) + i * tt() * elem_bytes(q);
+    }
+    ~mp_tile_s() {
+        for (int q = 0; q < 3; ++q) {
+            if (slab[q]) cudaFree(slab[q]);
+            if (panel[q]) cudaFree(panel[q]);
+        }
+        if (work) cudaFree(work);
+        if (lists) cudaFree(lists);
+    }
+};
+
+namespace {
+
+#define MP_API_BEGIN try {
+#define MP_API_END                                       \
+    return MP_OK;                                        \
+    }                                                    \
+    catch (const mpcr::Error& e) {                       \
+        mpcr::g_last_error = e.what();                   \
+        return e.status;                                 \
+    }                                                    \
+    catch (const std::exception& e) {                    \
+        mpcr::g_last_error = e.what();                   \
+        return MP_INTERNAL_ERROR;                        \
+    }
+
+mp_tile_s& T_(mp_tile t) {
+    if (!t) fail(MP_INVALID_PARAM, "null MPCRTile");
+    return *t;
+}
+
+void ensure_panels(mp_tile_s& t) {
+    for (int q = 0; q < 3; ++q)
+        if (!t.panel[q])
+            MP_CUDA(cudaMalloc(&t.panel[q], static_cast<size_t>(t.tr) * t.tt() * elem_bytes((mp_precision)q)));
+    if (!t.work) {
+        const size_t nn = static_cast<size_t>(t.br) * t.br;
+        // FP64 work, FP64 Linv, FP32 work, FP32 LinvS, FP16 LinvH, info
+        MP_CUDA(cudaMalloc(&t.work, nn * (8 + 8 + 4 + 4 + 2) + 256));
+    }
+}
+
+template <typename V>
+void append(std::vector<char>& buf, const std::vector<V>& v, size_t& off) {
+    off = (buf.size() + 255) / 256 * 256;
+    buf.resize(off + v.size() * sizeof(V));
+    if (!v.empty()) std::memcpy(buf.data() + off, v.data(), v.size() * sizeof(V));
+}
+
+struct StepLists {
+    // offsets into the device list buffer and counts
+    size_t trsm_tc = 0, trsm_s = 0, trsm_d = 0, trsm_h_simt = 0;
+    int64_t n_trsm_tc = 0, n_trsm_s = 0, n_trsm_d = 0, n_trsm_h_simt = 0;
+    size_t wb[3] = {0, 0, 0};
+    int64_t n_wb[3] = {0, 0, 0};
+    size_t cv[3][3] = {};
+    int64_t n_cv[3][3] = {};
+    size_t up_tc = 0, up_h_simt = 0, up_s = 0, up_d = 0;
+    int64_t n_up_tc = 0, n_up_h_simt = 0, n_up_s = 0, n_up_d = 0;
+    bool need_linv[3] = {false, false, false};
+};
+
+}  // namespace
+
+namespace mpcr {
+
+// Tiled Cholesky of an MPCRTile in place.  Returns the global failing column
+// (or -1); the caller maps it to MP_NOT_POSITIVE_DEFINITE.
+int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
+    cudaStream_t s = c->stream;
+    const int64_t nb = t.br, NT = t.tr, tt = t.tt();
+    ensure_panels(t);
+    const bool tc_ok = (nb % 8) == 0;  // TMA stride alignment for FP16 tiles
+
+    // ---- host plan ----------------------------------------------------------
+    std::vector<char> buf;
+    std::vector<StepLists> steps(NT);
+    for (int64_t k = 0; k < NT; ++k) {
+        StepLists& L = steps[k];
+        std::vector<TcProblem> trsm_tc;
+        std::vector<TileProblem> trsm_p[3];
+        std::vector<CopyItem> wb[3];
+        std::vector<CopyItem> cv[3][3];
+        std::vector<TcProblem> up_tc;
+        std::vector<TileProblem> up_p[3];
+        char* linv_base = static_cast<char*>(t.work);
+        const size_t nn = static_cast<size_t>(nb) * nb;
+        const void* linv[3] = {linv_base + nn * 24, linv_base + nn * 20, linv_base + nn * 8};
+        for (int64_t i = k + 1; i < NT; ++i) {
+            const mp_precision q = t.p(i, k);
+            L.need_linv[q] = true;
+            if (q == MP_HALF && tc_ok)
+                trsm_tc.push_back(TcProblem{static_cast<int32_t>(t.slot[k * NT + i]), 0, 0, 0,
+                                            t.panel_ptr(MP_HALF, i)});
+            else
+                trsm_p[q].push_back(TileProblem{t.ptr(i, k), linv[q], t.panel_ptr(q, i), 0, 0});
+            wb[q].push_back(CopyItem{t.panel_ptr(q, i), t.ptr(i, k)});
+            bool need[3] = {false, false, false};
+            for (int64_t j = k + 1; j <= i; ++j) need[t.p(i, j)] = true;  // A operand of row i
+            for (int64_t m = i; m < NT; ++m) need[t.p(m, i)] = true;      // B operand of column i
+            for (int r = 0; r < 3; ++r)
+                if (need[r] && r != q) cv[q][r].push_back(CopyItem{t.panel_ptr(q, i), t.panel_ptr((mp_precision)r, i)});
+        }
+        for (int64_t j = k + 1; j < NT; ++j)
+            for (int64_t i = j; i < NT; ++i) {
+                const mp_precision q = t.p(i, j);
+                const int32_t lo = (i == j) ? 1 : 0;
+                if (q == MP_HALF && tc_ok)
+                    up_tc.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j), lo, 0, t.ptr(i, j)});
+                else
+                    up_p[q].push_back(TileProblem{t.panel_ptr(q, i), t.panel_ptr(q, j), t.ptr(i, j), lo, 0});
+            }
+        append(buf, trsm_tc, L.trsm_tc);
+        L.n_trsm_tc = trsm_tc.size();
+        append(buf, trsm_p[MP_HALF], L.trsm_h_simt);
+        L.n_trsm_h_simt = trsm_p[MP_HALF].size();
+        append(buf, trsm_p[MP_SINGLE], L.trsm_s);
+        L.n_trsm_s = trsm_p[MP_SINGLE].size();
+        append(buf, trsm_p[MP_DOUBLE], L.trsm_d);
+        L.n_trsm_d = trsm_p[MP_DOUBLE].size();
+        for (int q = 0; q < 3; ++q) {
+            append(buf, wb[q], L.wb[q]);
+            L.n_wb[q] = wb[q].size();
+            for (int r = 0; r < 3; ++r) {
+                append(buf, cv[q][r], L.cv[q][r]);
+                L.n_cv[q][r] = cv[q][r].size();
+            }
+        }
+        append(buf, up_tc, L.up_tc);
+        L.n_up_tc = up_tc.size();
+        append(buf, up_p[MP_HALF], L.up_h_simt);
+        L.n_up_h_simt = up_p[MP_HALF].size();
+        append(buf, up_p[MP_SINGLE], L.up_s);
+        L.n_up_s = up_p[MP_SINGLE].size();
+        append(buf, up_p[MP_DOUBLE], L.up_d);
+        L.n_up_d = up_p[MP_DOUBLE].size();
+    }
+    // final clean-up lists: upper part of diagonal tiles, strictly-upper tiles
+    std::vector<void*> diag_ptrs[3], upper_ptrs[3];
+    for (int64_t j = 0; j < NT; ++j)
+        for (int64_t i = 0; i <= j; ++i)
+            (i == j ? diag_ptrs : upper_ptrs)[t.p(i, j)].push_back(t.ptr(i, j));
+    size_t off_diag[3], off_upper[3];
+    for (int q = 0; q < 3; ++q) {
+        append(buf, diag_ptrs[q], off_diag[q]);
+        append(buf, upper_ptrs[q], off_upper[q]);
+    }
+    if (buf.size() > t.lists_bytes) {
+        if (t.lists) MP_CUDA(cudaFree(t.lists));
+        MP_CUDA(cudaMalloc(&t.lists, buf.size()));
+        t.lists_bytes = buf.size();
+    }
+    char* dl = static_cast<char*>(t.lists);
+    MP_CUDA(cudaMemcpyAsync(dl, buf.data(), buf.size(), cudaMemcpyHostToDevice, s));
+
+    // ---- workspace ------------------------------------------------------------
+    const size_t nn = static_cast<size_t>(nb) * nb;
+    char* w = static_cast<char*>(t.work);
+    double* dwork = reinterpret_cast<double*>(w);
+    double* linv64 = reinterpret_cast<double*>(w + nn * 8);
+    float* swork = reinterpret_cast<float*>(w + nn * 16);
+    float* linvS = reinterpret_cast<float*>(w + nn * 20);
+    uint16_t* linvH = reinterpret_cast<uint16_t*>(w + nn * 24);
+    int64_t* dinfo = reinterpret_cast<int64_t*>(w + nn * 26 + 64);
+    const int64_t neg = -1;
+    MP_CUDA(cudaMemcpyAsync(dinfo, &neg, sizeof(neg), cudaMemcpyHostToDevice, s));
+
+    for (int64_t k = 0; k < NT; ++k) {
+        const StepLists& L = steps[k];
+        // 1. diagonal factor + FP64 inverse of the stored factor
+        const mp_precision pk = t.p(k, k);
+        void* akk = t.ptr(k, k);
+        if (pk == MP_DOUBLE) {
+            launch_potrf_lower(c, s, MP_DOUBLE, akk, nb, nb, dinfo, k * nb);
+            if (k + 1 < NT) launch_trtri_lower(c, s, static_cast<double*>(akk), nb, linv64, nb, nb);
+        } else {
+            if (pk == MP_SINGLE) {
+                launch_potrf_lower(c, s, MP_SINGLE, akk, nb, nb, dinfo, k * nb);
+            } else {
+                launch_convert(c, s, MP_HALF, akk, nb, MP_SINGLE, swork, nb, nb, nb);
+                launch_potrf_lower(c, s, MP_SINGLE, swork, nb, nb, dinfo, k * nb);
+                launch_convert(c, s, MP_SINGLE, swork, nb, MP_HALF, akk, nb, nb, nb);
+            }
+            if (k + 1 < NT) {
+                launch_convert(c, s, pk, akk, nb, MP_DOUBLE, dwork, nb, nb, nb);
+                launch_trtri_lower(c, s, dwork, nb, linv64, nb, nb);
+            }
+        }
+        if (k + 1 == NT) break;
+        // 2. Linv rounded to the panel precisions (the reference rounds U_kk
+        //    to p_ik before trsm: U_kk.converted(p_ik))
+        if (L.need_linv[MP_HALF]) launch_convert(c, s, MP_DOUBLE, linv64, nb, MP_HALF, linvH, nb, nb, nb);
+        if (L.need_linv[MP_SINGLE]) launch_convert(c, s, MP_DOUBLE, linv64, nb, MP_SINGLE, linvS, nb, nb, nb);
+        // 3. TRSM as GEMM: panel_q[i] = A_ik * Linv_q^T
+        if (L.n_trsm_tc) {
+            TcGemm g;
+            g.pc = MP_HALF;
+            g.ta = false;
+            g.tb = true;
+            g.m = nb;
+            g.n = nb;
+            g.k = nb;
+            g.alpha = 1.0;
+            g.beta = 0.0;
+            g.A = t.slab[MP_HALF];
+            g.lda = nb;
+            g.a_tiles = t.nslot[MP_HALF];
+            g.a_tile_stride = tt;
+            g.B = linvH;
+            g.ldb = nb;
+            g.b_tiles = 1;
+            g.b_tile_stride = tt;
+            g.ldc = nb;
+            g.problems = reinterpret_cast<const TcProblem*>(dl + L.trsm_tc);
+            g.count = L.n_trsm_tc;
+            launch_tc_gemm(c, s, g);
+        }
+        const struct {
+            int64_t n;
+            size_t off;
+            mp_precision q;
+        } tr_simt[3] = {{L.n_trsm_h_simt, L.trsm_h_simt, MP_HALF},
+                        {L.n_trsm_s, L.trsm_s, MP_SINGLE},
+                        {L.n_trsm_d, L.trsm_d, MP_DOUBLE}};
+        for (const auto& e : tr_simt)
+            if (e.n) {
+                GroupedGemm g{e.q, e.q, true, nb, nb, nb, nb, nb, nb, 1.0, 0.0,
+                              reinterpret_cast<const TileProblem*>(dl + e.off), e.n};
+                launch_grouped_gemm(c, s, g);
+            }
+        // write the factor back into the tiles
+        for (int q = 0; q < 3; ++q)
+            if (L.n_wb[q])
+                launch_batched_convert(c, s, (mp_precision)q, (mp_precision)q,
+                                       reinterpret_cast<const CopyItem*>(dl + L.wb[q]), L.n_wb[q], tt);
+        // 4. consumer-precision copies of the panel
+        for (int q = 0; q < 3; ++q)
+            for (int r = 0; r < 3; ++r)
+                if (L.n_cv[q][r])
+                    launch_batched_convert(c, s, (mp_precision)q, (mp_precision)r,
+                                           reinterpret_cast<const CopyItem*>(dl + L.cv[q][r]),
+                                           L.n_cv[q][r], tt);
+        // 5. trailing update
+        if (L.n_up_tc) {
+            TcGemm g;
+            g.pc = MP_HALF;
+            g.ta = false;
+            g.tb = true;
+            g.m = nb;
+            g.n = nb;
+            g.k = nb;
+            g.alpha = -1.0;
+            g.beta = 1.0;
+            g.A = t.panel[MP_HALF];
+            g.lda = nb;
+            g.a_tiles = NT;
+            g.a_tile_stride = tt;
+            g.B = t.panel[MP_HALF];
+            g.ldb = nb;
+            g.b_tiles = NT;
+            g.b_tile_stride = tt;
+            g.ldc = nb;
+            g.problems = reinterpret_cast<const TcProblem*>(dl + L.up_tc);
+            g.count = L.n_up_tc;
+            launch_tc_gemm(c, s, g);
+        }
+        const struct {
+            int64_t n;
+            size_t off;
+            mp_precision q;
+        } up_simt[3] = {{L.n_up_h_simt, L.up_h_simt, MP_HALF},
+                        {L.n_up_s, L.up_s, MP_SINGLE},
+                        {L.n_up_d, L.up_d, MP_DOUBLE}};
+        for (const auto& e : up_simt)
+            if (e.n) {
+                GroupedGemm g{e.q, e.q, true, nb, nb, nb, nb, nb, nb, -1.0, 1.0,
+                              reinterpret_cast<const TileProblem*>(dl + e.off), e.n};
+                launch_grouped_gemm(c, s, g);
+            }
+    }
+    // ---- zero everything above the diagonal (lower L output) ------------------
+    for (int q = 0; q < 3; ++q) {
+        if (!diag_ptrs[q].empty())
+            launch_batched_zero(c, s, (mp_precision)q, reinterpret_cast<void* const*>(dl + off_diag[q]),
+                                diag_ptrs[q].size(), tt, true, nb);
+        if (!upper_ptrs[q].empty())
+            launch_batched_zero(c, s, (mp_precision)q, reinterpret_cast<void* const*>(dl + off_upper[q]),
+                                upper_ptrs[q].size(), tt, false, nb);
+    }
+    int64_t info = -1;
+    MP_CUDA(cudaMemcpyAsync(&info, dinfo, sizeof(info), cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    return info;
+}
+
+}  // namespace mpcr
+
+extern "C" {
+
+mp_status mp_tile_create(mp_ctx ctx, int64_t rows, int64_t cols, int64_t rpt, int64_t cpt,
+                         const int* precisions, mp_tile* out) {
+    MP_API_BEGIN
+    if (!ctx || !out || !precisions) fail(MP_INVALID_PARAM, "null argument");
+    if (rows < 1 || cols < 1 || rpt < 1 || cpt < 1)
+        fail(MP_INVALID_PARAM, "MPCRTile: sizes must be >= 1");
+    if (rows % rpt || cols % cpt)
+        fail(MP_SHAPE_MISMATCH, "MPCRTile: tile size must divide the matrix size");
+    auto* t = new mp_tile_s();
+    t->ctx = ctx;
+    t->rows = rows;
+    t->cols = cols;
+    t->br = rpt;
+    t->bc = cpt;
+    t->tr = rows / rpt;
+    t->tc = cols / cpt;
+    const int64_t nt = t->tr * t->tc;
+    t->prec.resize(nt);
+    t->slot.resize(nt);
+    for (int64_t q = 0; q < nt; ++q) {
+        if (precisions[q] < 0 || precisions[q] > 2) {
+            delete t;
+            fail(MP_INVALID_PARAM, "MPCRTile: unknown precision code");
+        }
+        t->prec[q] = static_cast<mp_precision>(precisions[q]);
+        t->slot[q] = t->nslot[precisions[q]]++;
+    }
+    try {
+        for (int q = 0; q < 3; ++q)
+            if (t->nslot[q]) {
+                const size_t bytes = static_cast<size_t>(t->nslot[q]) * t->tt() * elem_bytes((mp_precision)q);
+                MP_CUDA(cudaMalloc(&t->slab[q], bytes));
+                MP_CUDA(cudaMemsetAsync(t->slab[q], 0, bytes, ctx->stream));
+            }
+    } catch (...) {
+        delete t;
+        throw;
+    }
+    *out = t;
+    MP_API_END
+}
+
+mp_status mp_tile_destroy(mp_tile t) {
+    MP_API_BEGIN
+    if (t) {
+        cudaStreamSynchronize(t->ctx->stream);
+        delete t;
+    }
+    MP_API_END
+}
+
+mp_status mp_tile_info(mp_tile t, int64_t* rows, int64_t* cols, int64_t* rpt, int64_t* cpt,
+                       int64_t* tiles_r, int64_t* tiles_c) {
+    MP_API_BEGIN
+    mp_tile_s& x = T_(t);
+    if (rows) *rows = x.rows;
+    if (cols) *cols = x.cols;
+    if (rpt) *rpt = x.br;
+    if (cpt) *cpt = x.bc;
+    if (tiles_r) *tiles_r = x.tr;
+    if (tiles_c) *tiles_c = x.tc;
+    MP_API_END
+}
+
+mp_status mp_tile_set_values_device(mp_tile t, const double* dev, int64_t ld) {
+    MP_API_BEGIN
+    mp_tile_s& x = T_(t);
+    Ctx* c = x.ctx;
+    for (int64_t j = 0; j < x.tc; ++j)
+        for (int64_t i = 0; i < x.tr; ++i)
+            launch_convert(c, c->stream, MP_DOUBLE, dev + (j * x.bc) * ld + i * x.br, ld, x.p(i, j),
+                           x.ptr(i, j), x.br, x.br, x.bc);
+    MP_API_END
+}
+
+mp_status mp_tile_set_values(mp_tile t, const double* host) {
+    MP_API_BEGIN
+    mp_tile_s& x = T_(t);
+    Ctx* c = x.ctx;
+    // one tile-column panel at a time (rows x bc doubles)
+    const size_t panel = static_cast<size_t>(x.rows) * x.bc;
+    double* tmp = static_cast<double*>(c->ensure_scratch(panel * sizeof(double), 1));
+    for (int64_t j = 0; j < x.tc; ++j) {
+        MP_CUDA(cudaMemcpyAsync(tmp, host + j * x.bc * x.rows, panel * sizeof(double),
+                                cudaMemcpyHostToDevice, c->stream));
+        for (int64_t i = 0; i < x.tr; ++i)
+            launch_convert(c, c->stream, MP_DOUBLE, tmp + i * x.br, x.rows, x.p(i, j), x.ptr(i, j),
+                           x.br, x.br, x.bc);
+        MP_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    MP_API_END
+}
+
+mp_status mp_tile_get_values(mp_tile t, double* host) {
+    MP_API_BEGIN
+    mp_tile_s& x = T_(t);
+    Ctx* c = x.ctx;
+    const size_t panel = static_cast<size_t>(x.rows) * x.bc;
+    double* tmp = static_cast<double*>(c->ensure_scratch(panel * sizeof(double), 1));
+    for (int64_t j = 0; j < x.tc; ++j) {
+        for (int64_t i = 0; i < x.tr; ++i)
+            launch_convert(c, c->stream, x.p(i, j), x.ptr(i, j), x.br, MP_DOUBLE, tmp + i * x.br,
+                           x.rows, x.br, x.bc);
+        MP_CUDA(cudaMemcpyAsync(host + j * x.bc * x.rows, tmp, panel * sizeof(double),
+                                cudaMemcpyDeviceToHost, c->stream));
+        MP_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    MP_API_END
+}
+
+mp_status mp_tile_get_tile(mp_tile t, int64_t i, int64_t j, mp_array* view) {
+    MP_API_BEGIN
+    mp_tile_s& x = T_(t);
+    if (i < 0 || j < 0 || i >= x.tr || j >= x.tc)
+        fail(MP_INDEX_OUT_OF_RANGE, "GetTile: tile index out of range");
+    return mp_array_wrap(static_cast<mp_ctx>(x.ctx), x.p(i, j), x.br, x.bc, x.br, x.ptr(i, j), view);
+    MP_API_END
+}
+
+mp_status mp_tile_precision(mp_tile t, int64_t i, int64_t j, mp_precision* p) {
+    MP_API_BEGIN
+    mp_tile_s& x = T_(t);
+    if (i < 0 || j < 0 || i >= x.tr || j >= x.tc)
+        fail(MP_INDEX_OUT_OF_RANGE, "tile index out of range");
+    *p = x.p(i, j);
+    MP_API_END
+}
+
+mp_status mp_tile_chol(mp_ctx ctx, mp_tile a, int overwrite_input, mp_tile* out, int64_t* info) {
+    MP_API_BEGIN
+    mp_tile_s& x = T_(a);
+    if (info) *info = -1;
+    if (!ctx) fail(MP_INVALID_PARAM, "null context");
+    if (x.rows != x.cols || x.br != x.bc)
+        fail(MP_SHAPE_MISMATCH, "chol: MPCRTile must be square with square tiles");
+    mp_tile_s* target = &x;
+    if (!overwrite_input) {
+        if (!out) fail(MP_INVALID_PARAM, "chol: out is required when overwrite_input is false");
+        std::vector<int> pr(x.prec.begin(), x.prec.end());
+        mp_tile nt = nullptr;
+        const mp_status st = mp_tile_create(ctx, x.rows, x.cols, x.br, x.bc, pr.data(), &nt);
+        if (st != MP_OK) return st;
+        for (int q = 0; q < 3; ++q)
+            if (x.nslot[q])
+                MP_CUDA(cudaMemcpyAsync(nt->slab[q], x.slab[q],
+                                        static_cast<size_t>(x.nslot[q]) * x.tt() * elem_bytes((mp_precision)q),
+                                        cudaMemcpyDeviceToDevice, ctx->stream));
+        target = nt;
+        *out = nt;
+    }
+    const int64_t inf = tile_chol_inplace(ctx, *target);
+    if (inf >= 0) {
+        if (info) *info = inf;
+        throw Error(MP_NOT_POSITIVE_DEFINITE,
+                    "matrix is not positive definite at pivot column " + std::to_string(inf), inf);
+    }
+    MP_API_END
+}
+
+// MPCRTile.gemm: every tile product in C-tile precision,
+// operands converted to it (oracle: ref_tile_gemm).
+mp_status mp_tile_gemm(mp_ctx ctx, mp_tile a, mp_tile b, mp_tile cc, int ta, int tb, double alpha,
+                       double beta) {
+    MP_API_BEGIN
+    mp_tile_s &A = T_(a), &B = T_(b), &C = T_(cc);
+    Ctx* c = ctx;
+    if (!c) fail(MP_INVALID_PARAM, "null context");
+    const int64_t kt = ta ? A.tr : A.tc, kb = tb ? B.tc : B.tr;
+    const int64_t mt = ta ? A.tc : A.tr, ntl = tb ? B.tr : B.tc;
+    const int64_t abr = ta ? A.bc : A.br, abk = ta ? A.br : A.bc;
+    const int64_t bbk = tb ? B.bc : B.br, bbn = tb ? B.br : B.bc;
+    if (kt != kb || mt != C.tr || ntl != C.tc || abk != bbk || abr != C.br || bbn != C.bc)
+        fail(MP_SHAPE_MISMATCH, "tile gemm: incompatible tile grids");
+    const size_t amax = static_cast<size_t>(A.tt()) * 8, bmax = static_cast<size_t>(B.tt()) * 8;
+    char* scr = static_cast<char*>(c->ensure_scratch(amax + bmax + 256, 0));
+    void* xa = scr;
+    void* xb = scr + ((amax + 255) / 256) * 256;
+    for (int64_t j = 0; j < C.tc; ++j)
+        for (int64_t i = 0; i < C.tr; ++i) {
+            const mp_precision pc = C.p(i, j);
+            for (int64_t l = 0; l < kt; ++l) {
+                const int64_t ai = ta ? l : i, aj = ta ? i : l;
+                const int64_t bi = tb ? j : l, bj = tb ? l : j;
+                const void* pa = A.ptr(ai, aj);
+                const void* pb = B.ptr(bi, bj);
+                if (A.p(ai, aj) != pc) {
+                    launch_convert(c, c->stream, A.p(ai, aj), pa, A.br, pc, xa, A.br, A.br, A.bc);
+                    pa = xa;
+                }
+                if (B.p(bi, bj) != pc) {
+                    launch_convert(c, c->stream, B.p(bi, bj), pb, B.br, pc, xb, B.br, B.br, B.bc);
+                    pb = xb;
+                }
+                GemmDesc g{pc, pc, pc, ta != 0, tb != 0, C.br, C.bc, abk, alpha, l == 0 ? beta : 1.0,
+                           pa, A.br, pb, B.br, C.ptr(i, j), C.br};
+                launch_gemm(c, c->stream, g);
+            }
+        }
+    MP_API_END
+}
+
+// MPCRTile.trsm: tile substitution in B-tile precision
+// (oracle: ref_tile_trsm).  All diagonal tiles are checked for exact zeros
+// before B is touched.
+mp_status mp_tile_trsm(mp_ctx ctx, mp_tile a, mp_tile b, mp_side side, int upper, int trans,
+                       double alpha) {
+    MP_API_BEGIN
+    mp_tile_s &A = T_(a), &B = T_(b);
+    Ctx* c = ctx;
+    if (!c) fail(MP_INVALID_PARAM, "null context");
+    if (A.rows != A.cols || A.br != A.bc) fail(MP_SHAPE_MISMATCH, "tile trsm: A must be square");
+    const int64_t nt = A.tr, nb = A.br;
+    const bool right = side == MP_RIGHT;
+    if (!right && (B.tr != nt || B.br != nb)) fail(MP_SHAPE_MISMATCH, "tile trsm: B row tiling");
+    if (right && (B.tc != nt || B.bc != nb)) fail(MP_SHAPE_MISMATCH, "tile trsm: B col tiling");
+    for (int64_t d = 0; d < nt; ++d) {
+        // zero check in the compute precision of every B tile that uses A_dd
+        mp_precision worst = MP_DOUBLE;
+        for (int64_t q = 0; q < (right ? B.tr : B.tc); ++q) {
+            const mp_precision pb = right ? B.p(q, d) : B.p(d, q);
+            worst = std::min(worst, compute_precision(pb));
+        }
+        if (find_zero_diag(c, c->stream, A.p(d, d), A.ptr(d, d), nb, nb, worst) >= 0)
+            fail(MP_SINGULAR_MATRIX, "triangular solve: zero diagonal in tile " + std::to_string(d));
+    }
+    const bool eff_lower = (upper != 0) == (trans != 0);
+    const size_t tmax = static_cast<size_t>(std::max(A.tt(), B.tt())) * 8;
+    char* scr = static_cast<char*>(c->ensure_scratch(2 * tmax + 256, 0));
+    void* xa = scr;
+    void* xb = scr + ((tmax + 255) / 256) * 256;
+    auto opA = [&](int64_t r, int64_t k, int64_t& si, int64_t& sj) {
+        si = trans ? k : r;
+        sj = trans ? r : k;
+    };
+    auto conv = [&](const mp_tile_s& T, int64_t i, int64_t j, mp_precision to, void* tmp) -> const void* {
+        if (T.p(i, j) == to) return T.ptr(i, j);
+        launch_convert(c, c->stream, T.p(i, j), T.ptr(i, j), T.br, to, tmp, T.br, T.br, T.bc);
+        return tmp;
+    };
+    if (!right) {
+        for (int64_t s = 0; s < nt; ++s) {
+            const int64_t r = eff_lower ? s : nt - 1 - s;
+            for (int64_t cidx = 0; cidx < B.tc; ++cidx) {
+                const mp_precision pt = B.p(r, cidx);
+                bool first = true;
+                for (int64_t q = 0; q < s; ++q) {
+                    const int64_t k = eff_lower ? q : nt - 1 - q;
+                    int64_t si, sj;
+                    opA(r, k, si, sj);
+                    const void* pa = conv(A, si, sj, pt, xa);
+                    const void* pbp = conv(B, k, cidx, pt, xb);
+                    GemmDesc g{pt, pt, pt, trans != 0, false, nb, B.bc, nb, -1.0, first ? alpha : 1.0,
+                               pa, nb, pbp, B.br, B.ptr(r, cidx), B.br};
+                    launch_gemm(c, c->stream, g);
+                    first = false;
+                }
+                const void* pd = conv(A, r, r, pt, xa);
+                launch_tri_solve(c, c->stream, pt, pd, nb, nb, upper != 0, trans != 0, pt,
+                                 B.ptr(r, cidx), B.br, B.bc, first ? alpha : 1.0, false, B.br);
+            }
+        }
+    } else {
+        for (int64_t s = 0; s < nt; ++s) {
+            const int64_t cidx = eff_lower ? nt - 1 - s : s;
+            for (int64_t r = 0; r < B.tr; ++r) {
+                const mp_precision pt = B.p(r, cidx);
+                bool first = true;
+                for (int64_t q = 0; q < s; ++q) {
+                    const int64_t k = eff_lower ? nt - 1 - q : q;
+                    int64_t si, sj;
+                    opA(k, cidx, si, sj);
+                    const void* pbp = conv(B, r, k, pt, xb);
+                    const void* pa = conv(A, si, sj, pt, xa);
+                    GemmDesc g{pt, pt, pt, false, trans != 0, B.br, nb, nb, -1.0, first ? alpha : 1.0,
+                               pbp, B.br, pa, nb, B.ptr(r, cidx), B.br};
+                    launch_gemm(c, c->stream, g);
+                    first = false;
+                }
+                const void* pd = conv(A, cidx, cidx, pt, xa);
+                launch_tri_solve(c, c->stream, pt, pd, nb, nb, upper != 0, trans != 0, pt,
+                                 B.ptr(r, cidx), B.br, B.bc, first ? alpha : 1.0, true, B.br);
+            }
+        }
+    }
+    MP_API_END
+}
+
+mp_status mp_tile_logdet(mp_ctx ctx, mp_tile l, double* logdet) {
+    MP_API_BEGIN
+    mp_tile_s& x = T_(l);
+    Ctx* c = ctx;
+    if (!c) fail(MP_INVALID_PARAM, "null context");
+    if (x.rows != x.cols || x.br != x.bc) fail(MP_SHAPE_MISMATCH, "logdet: square MPCRTile required");
+    double* acc = static_cast<double*>(c->ensure_scratch(64, 1));
+    MP_CUDA(cudaMemsetAsync(acc, 0, sizeof(double), c->stream));
+    for (int64_t d = 0; d < x.tr; ++d)
+        launch_logdiag_sum(c, c->stream, x.p(d, d), x.ptr(d, d), x.br, x.br, acc);
+    double h = 0;
+    MP_CUDA(cudaMemcpyAsync(&h, acc, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    MP_CUDA(cudaStreamSynchronize(c->stream));
+    *logdet = 2.0 * h;
+    MP_API_END
+}
+
+mp_status mp_tile_fill_matern(mp_ctx ctx, mp_tile t, int64_t side, double nu, double range,
+                              double variance) {
+    MP_API_BEGIN
+    mp_tile_s& x = T_(t);
+    Ctx* c = ctx;
+    if (!c) fail(MP_INVALID_PARAM, "null context");
+    if (side < 2) fail(MP_INVALID_PARAM, "grid_locations: side length must be >= 2");
+    if (side * side < x.rows || side * side < x.cols)
+        fail(MP_INVALID_PARAM, "matern: grid has fewer points than the matrix");
+    if (range <= 0.0 || variance <= 0.0)
+        fail(MP_INVALID_PARAM, "matern_cov: range and variance must be positive");
+    if (nu != 0.5 && nu != 1.5 && nu != 2.5) fail(MP_INVALID_PARAM, "matern_cov: nu must be 0.5, 1.5, or 2.5");
+    for (int64_t j = 0; j < x.tc; ++j)
+        for (int64_t i = 0; i < x.tr; ++i)
+            launch_matern_tile(c, c->stream, x.p(i, j), x.ptr(i, j), x.br, i * x.br, j * x.bc, x.br,
+                               x.bc, side, nu, range, variance);
+    MP_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,262 @@
+"""GPU parity: dense kernels (linalg.hpp:23-54) vs the reference oracle.
+
+Tolerances (north star: normwise relative error <= c * n * u_p):
+GEMM family rel. Frobenius error <= 4 * k * u(compute precision); Cholesky
+factors <= 100 * n * u; exact cases (A*I, symmetry, beta-only,
+error codes) are exact."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+H, S, D = 0, 1, 2
+U = {H: 2.0 ** -24, S: 2.0 ** -24, D: 2.0 ** -53}  # compute precision roundoff
+UST = {H: 2.0 ** -11, S: 2.0 ** -24, D: 2.0 ** -53}  # storage roundoff
+
+
+def rel(a, b):
+    d = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (d if d else 1.0)
+
+
+def gemm_tol(k, pc):
+    return 4 * max(k, 1) * U[pc] + 2 * UST[pc]
+
+
+def mk(rng, shape, p):
+    from oracle.oracle import round_to
+
+    return round_to(rng.random(shape), p)
+
+
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+@pytest.mark.parametrize("pc", [H, S, D])
+def test_gemm_trans_precisions(ctx, ref, rng, ta, tb, pc):
+    import paper_2406_02701_b200 as mp
+
+    m, n, k = 67, 45, 33
+    for pa in range(pc + 1):
+        for pb in range(pc + 1):
+            A = mk(rng, (k, m) if ta else (m, k), pa)
+            B = mk(rng, (n, k) if tb else (k, n), pb)
+            Cm = mk(rng, (m, n), pc)
+            for alpha, beta in ((1.0, 0.0), (0.7, 0.3), (-1.0, 1.0)):
+                da = mp.MPArray.from_numpy(A, mp.Precision(pa), ctx)
+                db = mp.MPArray.from_numpy(B, mp.Precision(pb), ctx)
+                dc = mp.MPArray.from_numpy(Cm, mp.Precision(pc), ctx)
+                mp.linalg.gemm(da, db, dc, ta, tb, alpha, beta)
+                want = ref.gemm(pa, pb, pc, A, B, Cm, ta, tb, alpha, beta)
+                assert rel(dc.to_numpy(), want) <= gemm_tol(k, pc)
+
+
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+@pytest.mark.parametrize("pc", [H, S])
+def test_gemm_fp16_tensor_core(ctx, ref, rng, ta, tb, pc):
+    """Half x half -> half/single runs on tcgen05 (shapes with ragged edges)."""
+    import paper_2406_02701_b200 as mp
+
+    for (m, n, k) in ((256, 256, 64), (384, 512, 320), (200, 300, 136), (128, 1000, 1000)):
+        A = mk(rng, (k, m) if ta else (m, k), H) - 0.5
+        B = mk(rng, (n, k) if tb else (k, n), H) - 0.5
+        Cm = mk(rng, (m, n), pc)
+        da = mp.MPArray.from_numpy(A, mp.Precision.Half, ctx)
+        db = mp.MPArray.from_numpy(B, mp.Precision.Half, ctx)
+        dc = mp.MPArray.from_numpy(Cm, mp.Precision(pc), ctx)
+        mp.linalg.gemm(da, db, dc, ta, tb, -1.0, 1.0)
+        want = ref.gemm(H, H, pc, A, B, Cm, ta, tb, -1.0, 1.0)
+        err = rel(dc.to_numpy(), want)
+        assert err <= gemm_tol(k, pc), (m, n, k, err)
+
+
+def test_gemm_fp16_large_vs_fp64(ctx, rng):
+    """n=2048 half GEMM against an exact FP64 product of the same halves."""
+    import paper_2406_02701_b200 as mp
+    from oracle.oracle import round_to
+
+    n = 2048
+    A = round_to(rng.random((n, n)), H)
+    B = round_to(rng.random((n, n)), H)
+    da = mp.MPArray.from_numpy(A, mp.Precision.Half, ctx)
+    db = mp.MPArray.from_numpy(B, mp.Precision.Half, ctx)
+    dc = mp.MPArray.zeros_matrix(n, n, mp.Precision.Single, ctx)
+    mp.linalg.gemm(da, db, dc)
+    exact = A @ B
+    assert rel(dc.to_numpy(), exact) < 1e-6
+    dh = mp.MPArray.zeros_matrix(n, n, mp.Precision.Half, ctx)
+    mp.linalg.gemm(da, db, dh)
+    assert rel(dh.to_numpy(), exact) < 2 * 2.0 ** -11
+
+
+def test_gemm_exact_cases(ctx, rng):
+    """test_linalg.cpp:152-183: A*I = A exactly, beta-only, PrecisionMismatch."""
+    import paper_2406_02701_b200 as mp
+
+    for p in (H, S, D):
+        A = mk(rng, (256, 256), p)
+        da = mp.MPArray.from_numpy(A, mp.Precision(p), ctx)
+        eye = mp.MPArray.from_numpy(np.eye(256), mp.Precision(p), ctx)
+        dc = mp.MPArray.zeros_matrix(256, 256, mp.Precision(p), ctx)
+        mp.linalg.gemm(da, eye, dc)
+        np.testing.assert_array_equal(dc.to_numpy(), A)
+    a = mp.MPArray.from_numpy(mk(rng, (3, 3), D), mp.Precision.Double, ctx)
+    zero = mp.MPArray.zeros_matrix(3, 3, mp.Precision.Double, ctx)
+    ones = mp.MPArray.from_numpy(np.ones((3, 3)), mp.Precision.Double, ctx)
+    mp.linalg.gemm(a, zero, ones, False, False, 1.0, 0.5)
+    np.testing.assert_array_equal(ones.to_numpy(), np.full((3, 3), 0.5))
+    low = mp.MPArray.zeros_matrix(3, 3, mp.Precision.Single, ctx)
+    with pytest.raises(mp.MPError) as e:
+        mp.linalg.gemm(a, a, low)
+    assert e.value.kind == "PrecisionMismatch"
+    with pytest.raises(mp.MPError) as e:
+        mp.linalg.gemm(a, mp.MPArray.zeros_matrix(4, 4, mp.Precision.Double, ctx), zero)
+    assert e.value.kind == "ShapeMismatch"
+
+
+def test_matmul_crossprod(ctx, ref, rng):
+    import paper_2406_02701_b200 as mp
+
+    for pa in (H, S, D):
+        for pb in (H, S, D):
+            A = mk(rng, (40, 30), pa)
+            B = mk(rng, (30, 20), pb)
+            da = mp.MPArray.from_numpy(A, mp.Precision(pa), ctx)
+            db = mp.MPArray.from_numpy(B, mp.Precision(pb), ctx)
+            out = mp.linalg.matmul(da, db)
+            assert out.precision() == max(pa, pb)
+            pc = max(pa, pb)
+            assert rel(out.to_numpy(), ref.matmul(pa, pb, A, B)) <= gemm_tol(30, pc)
+    for p in (H, S, D):
+        for n in (5, 300):
+            A = mk(rng, (n + 7, n), p)
+            da = mp.MPArray.from_numpy(A, mp.Precision(p), ctx)
+            c = mp.linalg.crossprod(da).to_numpy()
+            np.testing.assert_array_equal(c, c.T)  # exactly symmetric (test_linalg.cpp:132-135)
+            assert rel(c, ref.crossprod(p, A)) <= gemm_tol(n + 7, p)
+
+
+def test_crossprod_error_bands_1024(ctx, ref):
+    """acceptance.cpp:153-177 criterion 4 at n=1024 on the reference's inputs."""
+    import paper_2406_02701_b200 as mp
+
+    n = 1024
+    A = ref.rng_uniform(1000 + n, n * n).reshape((n, n), order="F")
+    oracle = ref.crossprod(D, A)
+    errs = {}
+    for p in (H, S, D):
+        da = mp.MPArray.from_numpy(A, mp.Precision(p), ctx)
+        errs[p] = rel(mp.linalg.crossprod(da).to_numpy(), oracle)
+    assert 1e-4 <= errs[H] <= 2e-2
+    assert 1e-8 <= errs[S] <= 1e-5
+    assert errs[D] <= 1e-13
+    assert errs[H] > errs[S] > errs[D]
+
+
+def spd(rng, n):
+    B = rng.random((n, n))
+    return B.T @ B + n * np.eye(n)
+
+
+@pytest.mark.parametrize("n", [1, 2, 8, 63, 64, 65, 200, 1024])
+def test_chol(ctx, ref, rng, n):
+    import paper_2406_02701_b200 as mp
+    from oracle.oracle import round_to
+
+    A0 = spd(rng, n)
+    for p in (H, S, D):
+        A = round_to(A0, p)
+        da = mp.MPArray.from_numpy(A, mp.Precision(p), ctx)
+        U = mp.linalg.chol(da).to_numpy()
+        Uref = ref.chol(p, A)
+        assert np.all(np.tril(U, -1) == 0)
+        tol = 100 * n * (2.0 ** -24 if p != D else 2.0 ** -53) + 2 * UST[p]
+        assert rel(U, Uref) <= tol, (p, rel(U, Uref))
+
+
+def test_chol_known_and_failures(ctx):
+    """test_linalg.cpp:185-221."""
+    import paper_2406_02701_b200 as mp
+
+    a = mp.MPArray.from_doubles([4, 2, 2, 3], 2, 2, mp.Precision.Double, ctx)
+    u = mp.linalg.chol(a).to_numpy()
+    assert u[0, 0] == 2.0 and u[0, 1] == 1.0 and u[1, 0] == 0.0
+    assert abs(u[1, 1] - np.sqrt(2.0)) < 1e-15
+    eye = mp.MPArray.from_numpy(np.eye(4), mp.Precision.Double, ctx)
+    np.testing.assert_array_equal(mp.linalg.chol(eye).to_numpy(), np.eye(4))
+    bad = mp.MPArray.from_doubles([1, 2, 2, 1], 2, 2, mp.Precision.Double, ctx)
+    with pytest.raises(mp.MPError) as e:
+        mp.linalg.chol(bad)
+    assert e.value.kind == "NotPositiveDefinite" and e.value.info == 1
+    neg = mp.MPArray.from_doubles([-1.0], 1, 1, mp.Precision.Double, ctx)
+    with pytest.raises(mp.MPError) as e:
+        mp.linalg.chol(neg)
+    assert e.value.info == 0
+    # a failing pivot deep inside a blocked factorization
+    n = 300
+    M = np.eye(n)
+    M[200, 200] = -1.0
+    with pytest.raises(mp.MPError) as e:
+        mp.linalg.chol(mp.MPArray.from_numpy(M, mp.Precision.Double, ctx))
+    assert e.value.info == 200
+    with pytest.raises(mp.MPError) as e:
+        mp.linalg.chol(mp.MPArray.zeros_matrix(2, 3, mp.Precision.Double, ctx))
+    assert e.value.kind == "ShapeMismatch"
+
+
+def test_chol_reads_upper_triangle(ctx, ref, rng):
+    """chol_kernel reads the upper triangle only (linalg.cpp:110-127)."""
+    import paper_2406_02701_b200 as mp
+
+    A = spd(rng, 50)
+    A[np.tril_indices(50, -1)] = 7.0  # garbage below the diagonal
+    da = mp.MPArray.from_numpy(A, mp.Precision.Double, ctx)
+    assert rel(mp.linalg.chol(da).to_numpy(), ref.chol(D, A)) < 1e-13
+
+
+@pytest.mark.parametrize("side_right", [False, True])
+@pytest.mark.parametrize("upper", [False, True])
+@pytest.mark.parametrize("trans", [False, True])
+def test_trsm(ctx, ref, rng, side_right, upper, trans):
+    import paper_2406_02701_b200 as mp
+    from oracle.oracle import round_to
+
+    n = 48
+    U0 = np.linalg.cholesky(spd(rng, n)).T
+    T0 = U0 if upper else U0.T
+    for pa in (H, S, D):
+        for pb in (H, S, D):
+            T = round_to(T0, pa)
+            B = round_to(rng.random((7, n) if side_right else (n, 7)), pb)
+            da = mp.MPArray.from_numpy(T, mp.Precision(pa), ctx)
+            db = mp.MPArray.from_numpy(B, mp.Precision(pb), ctx)
+            mp.linalg.trsm(da, db, mp.Side(int(side_right)), upper, trans, 1.5)
+            want = ref.trsm(pa, pb, T, B, side_right, upper, trans, 1.5)
+            tol = 100 * n * U[pb] + 2 * UST[pb]
+            assert rel(db.to_numpy(), want) <= tol
+
+
+def test_trsm_singular_and_solves(ctx, ref, rng):
+    import paper_2406_02701_b200 as mp
+
+    z = np.eye(3)
+    z[2, 2] = 0.0
+    dz = mp.MPArray.from_numpy(z, mp.Precision.Double, ctx)
+    b = mp.MPArray.from_numpy(rng.random((3, 1)), mp.Precision.Double, ctx)
+    with pytest.raises(mp.MPError) as e:
+        mp.linalg.backsolve(dz, b)
+    assert e.value.kind == "SingularMatrix"
+    L = np.linalg.cholesky(spd(rng, 20))
+    B = rng.random((20, 3))
+    for pt in (S, D):
+        for pb in (S, D):
+            from oracle.oracle import round_to
+
+            Lr, Br = round_to(L, pt), round_to(B, pb)
+            dl = mp.MPArray.from_numpy(Lr, mp.Precision(pt), ctx)
+            db = mp.MPArray.from_numpy(Br, mp.Precision(pb), ctx)
+            f = mp.linalg.forwardsolve(dl, db)
+            assert rel(f.to_numpy(), ref.trisolve(False, pt, pb, Lr, Br)) < 1e-5
+            du = mp.MPArray.from_numpy(Lr.T.copy(), mp.Precision(pt), ctx)
+            g = mp.linalg.backsolve(du, db)
+            assert rel(g.to_numpy(), ref.trisolve(True, pt, pb, Lr.T, Br)) < 1e-5

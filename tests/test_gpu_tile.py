@@ -1,0 +1,209 @@
+"""GPU parity: MPCRTile vs the composed reference oracle
+(oracle/ref_shim.cpp: ref_tile_chol / ref_tile_gemm / ref_tile_trsm) and the
+paper's printed known answers."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+H, S, D = 0, 1, 2
+
+
+def paper_M():
+    xs = np.array([(x, y) for y in (0.0, 1.0) for x in (0.0, 1.0)])
+    d = np.sqrt(((xs[:, None] - xs[None]) ** 2).sum(-1))
+    return np.exp(-d)
+
+
+def test_paper_chol_4x4(ctx, ref):
+    """PAPER.md:585-588 (diag double, off-diag single, 2x2 tiles)."""
+    import paper_2406_02701_b200 as mp
+
+    M = paper_M()
+    prec = [["double", "single"], ["single", "double"]]
+    t = mp.MPCRTile(4, 4, 2, 2, M, prec, ctx)
+    L = mp.tile_chol(t, overwrite_input=False).to_numpy()
+    printed = np.array([[1, 0, 0, 0], [0.3678794, 0.9298735, 0, 0],
+                        [0.3678795, 0.1159098, 0.9226211, 0],
+                        [0.2431167, 0.2994405, 0.2641753, 0.8839915]])
+    np.testing.assert_allclose(L, printed, atol=6e-8)
+    Lref = ref.tile_chol(4, 2, np.array([[2, 1], [1, 2]]), M)
+    np.testing.assert_allclose(L, Lref, rtol=1e-6, atol=1e-7)
+    # the FP32-tile signature of the printout (0.3678795 vs dense 0.3678794)
+    assert abs(L[2, 0] - 0.3678795) < 5e-8
+    # the input is untouched when overwrite_input = FALSE
+    np.testing.assert_array_equal(t.to_numpy(), ref_round_grid(M, np.array([[2, 1], [1, 2]]), 2))
+
+
+def test_paper_trsm_4x4(ctx, ref):
+    """L X = I with B in single tiles."""
+    import paper_2406_02701_b200 as mp
+
+    M = paper_M()
+    t = mp.MPCRTile(4, 4, 2, 2, M, [["double", "single"], ["single", "double"]], ctx)
+    Lt = mp.tile_chol(t, overwrite_input=False)
+    b = mp.MPCRTile(4, 4, 2, 2, np.eye(4), [["single", "single"], ["single", "single"]], ctx)
+    mp.tile_trsm(Lt, b, "L", False, False, 1.0)
+    X = b.to_numpy()
+    printed = np.array([[1, 0, 0, 0], [-0.3956231, 1.075415, 0, 0],
+                        [-0.3490305, -0.1351055, 1.083869, 0],
+                        [-0.03670389, -0.3239073, -0.3239073, 1.131233]])
+    np.testing.assert_allclose(X, printed, atol=2e-7)
+    L = Lt.to_numpy()
+    Xref = ref.tile_trsm(L, np.array([[2, 1], [1, 2]]), 2, np.eye(4), np.ones((2, 2), int),
+                         (2, 2), False, False, False, 1.0)
+    np.testing.assert_allclose(X, Xref, rtol=1e-6, atol=1e-7)
+
+
+def test_paper_gemm_half(ctx):
+    """PAPER.md:585-588 example: C = A*0 + 0.5*1 -> 0.5."""
+    import paper_2406_02701_b200 as mp
+
+    A = np.arange(1, 25, dtype=float).reshape((4, 6), order="F")
+    a = mp.MPCRTile(4, 6, 2, 6, A, [["single"], ["single"]], ctx)
+    b = mp.MPCRTile(6, 1, 6, 1, np.zeros((6, 1)), [["single"]], ctx)
+    c = mp.MPCRTile(4, 1, 2, 1, np.ones((4, 1)), [["single"], ["single"]], ctx)
+    mp.tile_gemm(a, b, c, False, False, 1.0, 0.5, num_threads=4)
+    np.testing.assert_array_equal(c.to_numpy(), np.full((4, 1), 0.5))
+
+
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+def test_tile_gemm_mixed(ctx, ref, rng, ta, tb):
+    import paper_2406_02701_b200 as mp
+
+    nb = 32
+    A = rng.random((96, 64)) if not ta else rng.random((64, 96))
+    B = rng.random((64, 128)) if not tb else rng.random((128, 64))
+    Cm = rng.random((96, 128))
+    gA = rng.integers(0, 3, (A.shape[0] // nb, A.shape[1] // nb))
+    gB = rng.integers(0, 3, (B.shape[0] // nb, B.shape[1] // nb))
+    gC = rng.integers(0, 3, (3, 4))
+    a = mp.MPCRTile(*A.shape, nb, nb, A, gA, ctx)
+    b = mp.MPCRTile(*B.shape, nb, nb, B, gB, ctx)
+    c = mp.MPCRTile(96, 128, nb, nb, Cm, gC, ctx)
+    mp.tile_gemm(a, b, c, ta, tb, 0.75, 0.25)
+    want = ref.tile_gemm(a.to_numpy(), gA, (nb, nb), b.to_numpy(), gB, (nb, nb),
+                         ref_round_grid(Cm, gC, nb), gC, (nb, nb), ta, tb, 0.75, 0.25)
+    got = c.to_numpy()
+    # tile-wise tolerance by destination precision
+    for i in range(3):
+        for j in range(4):
+            g = got[i * nb:(i + 1) * nb, j * nb:(j + 1) * nb]
+            w = want[i * nb:(i + 1) * nb, j * nb:(j + 1) * nb]
+            tol = {0: 2e-3, 1: 1e-5, 2: 1e-13}[gC[i, j]]
+            assert np.linalg.norm(g - w) <= tol * np.linalg.norm(w)
+
+
+def ref_round_grid(M, grid, nb):
+    from oracle.oracle import round_to
+
+    out = M.copy()
+    for i in range(grid.shape[0]):
+        for j in range(grid.shape[1]):
+            sl = (slice(i * nb, (i + 1) * nb), slice(j * nb, (j + 1) * nb))
+            out[sl] = round_to(M[sl], int(grid[i, j]))
+    return out
+
+
+@pytest.mark.parametrize("side", ["L", "R"])
+@pytest.mark.parametrize("upper", [False, True])
+@pytest.mark.parametrize("trans", [False, True])
+def test_tile_trsm_general(ctx, ref, rng, side, upper, trans):
+    import paper_2406_02701_b200 as mp
+
+    n, nb = 96, 32
+    B0 = rng.random((n, n))
+    L0 = np.linalg.cholesky(B0.T @ B0 + n * np.eye(n))
+    T0 = L0.T if upper else L0
+    gA = np.array([[2, 1, 1], [1, 2, 1], [1, 1, 2]])
+    a = mp.MPCRTile(n, n, nb, nb, T0, gA, ctx)
+    Bm = rng.random((n, 64)) if side == "L" else rng.random((64, n))
+    gB = np.ones((3, 2), int) * 2 if side == "L" else np.ones((2, 3), int) * 2
+    gB[0, 0] = 1
+    b = mp.MPCRTile(*Bm.shape, nb, nb, Bm, gB, ctx)
+    mp.tile_trsm(a, b, side, upper, trans, 2.0)
+    want = ref.tile_trsm(a.to_numpy(), gA, nb, ref_round_grid(Bm, gB, nb), gB, (nb, nb),
+                         side == "R", upper, trans, 2.0)
+    got = b.to_numpy()
+    assert np.linalg.norm(got - want) <= 1e-5 * np.linalg.norm(want)
+
+
+def band_map(nt, b64=1, b32=2):
+    g = np.zeros((nt, nt), int)
+    for i in range(nt):
+        for j in range(nt):
+            d = abs(i - j)
+            g[i, j] = 2 if d < b64 else (1 if d < b32 else 0)
+    return g
+
+
+@pytest.mark.parametrize("n,nb,b64,b32", [(512, 128, 1, 2), (1024, 128, 1, 3),
+                                         (1024, 256, 1, 2), (768, 64, 2, 4),
+                                         (1024, 128, 0, 0), (1024, 128, 9, 9)])
+def test_tile_chol_matern_vs_oracle(ctx, ref, n, nb, b64, b32):
+    """Mixed-precision tiled Cholesky vs the composed reference oracle on an
+    exponential (Matern 0.5, range 0.1) covariance; relFrob(L) and logdet."""
+    import paper_2406_02701_b200 as mp
+
+    side = int(np.ceil(np.sqrt(n)))
+    cov = ref.grid_matern(side, n, 0.5, 0.1, 1.0, 2)
+    nt = n // nb
+    g = band_map(nt, b64, b32)
+    if b64 == 0:  # all-half except an FP32 diagonal: harsher
+        g = np.where(np.eye(nt) > 0, 1, 0)
+    t = mp.MPCRTile(n, n, nb, nb, cov, g, ctx)
+    mp.tile_chol(t)
+    L = t.to_numpy()
+    Lref = ref.tile_chol(n, nb, g, cov)
+    err = np.linalg.norm(L - Lref) / np.linalg.norm(Lref)
+    dense = np.linalg.cholesky(cov)
+    err_dense = np.linalg.norm(Lref - dense) / np.linalg.norm(dense)
+    # the GPU factor is as close to the oracle as the oracle is to exact FP64
+    # (same mixed-precision rounding budget), with a floor at FP64 level
+    assert err <= max(4 * err_dense, 1e-12), (err, err_dense)
+    ld = t.logdet()
+    ld_ref = 2 * np.log(np.diag(Lref)).sum()
+    assert abs(ld - ld_ref) <= max(4 * abs(2 * np.log(np.diag(dense)).sum() - ld_ref), 1e-10 * abs(ld_ref))
+    assert np.all(np.triu(L, 1) == 0)
+
+
+def test_tile_chol_not_pd(ctx):
+    import paper_2406_02701_b200 as mp
+
+    n, nb = 256, 64
+    M = np.eye(n)
+    M[150, 150] = -2.0
+    t = mp.MPCRTile(n, n, nb, nb, M, np.full((4, 4), 2), ctx)
+    with pytest.raises(mp.MPError) as e:
+        mp.tile_chol(t)
+    assert e.value.kind == "NotPositiveDefinite" and e.value.info == 150
+
+
+def test_tile_fill_matern_matches_reference(ctx, ref):
+    import paper_2406_02701_b200 as mp
+
+    n, nb, side = 300, 60, 18
+    g = band_map(5, 1, 2)
+    t = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+    t.fill_matern(side, 0.5, 0.1, 1.0)
+    got = t.to_numpy()
+    want = ref_round_grid(ref.grid_matern(side, n, 0.5, 0.1, 1.0, 2), g, nb)
+    np.testing.assert_allclose(got, want, rtol=2e-15, atol=0)
+    for nu in (1.5, 2.5):
+        t.fill_matern(side, nu, 0.2, 2.0)
+        want = ref_round_grid(ref.grid_matern(side, n, nu, 0.2, 2.0, 2), g, nb)
+        # half tiles may straddle a rounding boundary by 1 ulp of half
+        np.testing.assert_allclose(t.to_numpy(), want, rtol=2.0 ** -10, atol=0)
+
+
+def test_get_tile_view(ctx):
+    import paper_2406_02701_b200 as mp
+
+    M = np.arange(64, dtype=float).reshape((8, 8), order="F")
+    t = mp.MPCRTile(8, 8, 4, 4, M, [["double", "single"], ["half", "double"]], ctx)
+    v = t.GetTile(2, 1)
+    assert v.precision() == mp.Precision.Half
+    np.testing.assert_array_equal(v.to_numpy(), M[4:8, 0:4])
+    with pytest.raises(mp.MPError):
+        t.GetTile(3, 1)
