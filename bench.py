@@ -1,0 +1,431 @@
+#!/usr/bin/env python
+"""Benchmark: MPCRTile mixed-precision tiled Cholesky TFLOP/s on B200.
+
+Default workload (BASELINE.json configs[2], the N=1 config the metric is
+quoted on): n = 65536, tile 1024, exponential (Matern nu=0.5) covariance of
+the first n points of a 256x256 unit grid, range 0.1; tile precision by band
+|i-j|: < b64 -> FP64, < b32 -> FP32, else FP16 (default b64=1, b32=2).
+
+A step is one full factorization chol(A) of the resident matrix (n^3/3
+flops).  Inputs are restored from a pristine device copy before every step,
+outside the CUDA-event pair; the 8.8 GB of tiles are far larger than the
+126 MB L2, so no flush is needed.  e2e repeats the step through the public
+C ABI from host buffers: host point coordinates -> device Matern generation
+-> chol -> logdet read back.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    python bench.py --workload gemm --prec half --n 8192     (config 2 lines)
+
+Multi-GPU (torchrun): every rank factors its own replica (replicas only;
+the 2D block-cyclic distributed factorization is future work), the time is
+the max over ranks, value = total flops of all ranks / that time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    try:
+        with open(PEAKS_FILE) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return FALLBACK, "fallback"
+
+
+def band_map(nt, b64, b32):
+    i, j = np.indices((nt, nt))
+    d = np.abs(i - j)
+    return np.where(d < b64, 2, np.where(d < b32, 1, 0)).astype(np.int32)
+
+
+def grid_points(n):
+    side = int(np.ceil(np.sqrt(n)))
+    side = max(side, 2)
+    p = np.arange(n)
+    return (p % side) / (side - 1), (p // side) / (side - 1), side
+
+
+def flops_by_precision(nt, nb, g):
+    """Algorithmic flops of the tiled right-looking Cholesky by destination
+    tile precision: POTRF nb^3/3, TRSM nb^3, SYRK nb^3, GEMM 2 nb^3
+    (SURVEY.md §8d).  Sums to n^3/3 up to O(n^2)."""
+    f = np.zeros(3)
+    b3 = float(nb) ** 3
+    for k in range(nt):
+        f[g[k, k]] += b3 / 3
+        for i in range(k + 1, nt):
+            f[g[i, k]] += b3
+            f[g[i, i]] += b3
+            for j in range(k + 1, i):
+                f[g[i, j]] += 2 * b3
+    return f
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def dist_max(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def dist_barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref = the unmodified mpnum library): bounded sample
+# ---------------------------------------------------------------------------
+def cpu_reference_chol(args, budget_s=20.0, steps=None):
+    from oracle import oracle as orc
+
+    if os.path.exists(orc.REF_SO):
+        o, kind = orc.Ref(), "reference"
+        cores = os.cpu_count() or 1
+        o.set_num_threads(cores)
+    else:
+        o, kind, cores = orc.Port(), "port", 1
+    n, nb = args.cpu_n, args.cpu_nb
+    x, y, side = grid_points(n)
+    if kind == "reference":
+        cov = o.grid_matern(side, n, 0.5, args.range, 1.0, 2)
+    else:
+        d = np.hypot(x[:, None] - x[None], y[:, None] - y[None])
+        cov = np.exp(-d / args.range)
+    cov = cov + args.nugget * np.eye(n)
+    g = band_map(n // nb, args.b64, args.b32)
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while True:
+        t0 = time.perf_counter()
+        o.tile_chol(n, nb, g, cov)
+        times.append(time.perf_counter() - t0)
+        if steps is not None and len(times) >= steps:
+            break
+        if steps is None and (time.perf_counter() > t_end or len(times) >= 5):
+            break
+    t = float(np.median(times))
+    return {"value": n ** 3 / 3 / t / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": kind,
+            "sample": f"MPCRTile chol n={n} nb={nb} (same band map and covariance family), "
+                      f"median of {len(times)} runs, {t:.3f} s each",
+            "seconds": t}, times
+
+
+def run_reference_arm(args, world, rank):
+    """--impl reference: the reference's CPU tiled Cholesky on host cores."""
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+
+    # warmup + timed steps, each one factorization of the bounded sample
+    _, wt = cpu_reference_chol(args, steps=max(args.warmup, 1))
+    base, times = cpu_reference_chol(args, steps=args.steps)
+    n = args.cpu_n
+    tot = float(np.sum(times))
+    val = n ** 3 / 3 * len(times) / tot / 1e12
+    base["value"] = val
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot / len(times) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "mixed(f64/f32/f16-storage, f32/f64 compute)", "data": "synthetic",
+        "config": {"workload": f"MPCRTile mixed-precision Cholesky (CPU reference sample n={n}, "
+                               f"tile {args.cpu_nb})", "n": n, "nb": args.cpu_nb,
+                   "precision_map": f"|i-j|<{args.b64}:FP64, <{args.b32}:FP32, else FP16",
+                   "matern_range": args.range},
+        "cpu_baseline": base,
+        "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "reference_library": os.path.basename(orc.REF_SO) if base["kind"] == "reference" else "port",
+    }
+    print(json.dumps(line))
+
+
+METRIC = "mixed-precision tiled Cholesky TFLOP/s"
+
+
+def run_chol(args, world, rank, local):
+    import paper_2406_02701_b200 as mp
+
+    ctx = mp.Context(local)
+    n, nb = args.n, args.nb
+    nt = n // nb
+    g = band_map(nt, args.b64, args.b32)
+    x, y, side = grid_points(n)
+    A0 = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+    A = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+    A0.fill_matern_points(x, y, 0.5, args.range, 1.0, args.nugget)
+    ctx.synchronize()
+
+    import torch
+
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
+
+    def factor():
+        mp.tile_chol(A)
+
+    # warm-up
+    for _ in range(args.warmup):
+        A.copy_from(A0)
+        factor()
+    ctx.synchronize()
+    # timed region
+    ctx.prof_reset()
+    ctx.prof_enable(True)
+    l0 = ctx.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    dist_barrier(world)
+    torch.cuda.synchronize(local)
+    ctx.synchronize()
+    with ClockSampler(local) as clk:
+        t_wall0 = time.perf_counter()
+        for k in range(args.steps):
+            A.copy_from(A0)
+            ev[k][0].record(stream)
+            factor()
+            ev[k][1].record(stream)
+        ctx.synchronize()
+        torch.cuda.synchronize(local)
+        t_wall = time.perf_counter() - t_wall0
+    dist_barrier(world)
+    launches = ctx.launch_count() - l0
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    ms_max = dist_max(ms, world)
+    ctx.prof_enable(False)
+    cls_names = ["gemm_f16", "gemm_f32", "gemm_f64", "potrf_trtri", "trsm", "cast", "other"]
+    prof = {}
+    for c, nm in enumerate(cls_names):
+        t, cnt, work = ctx.prof_query(c)
+        if cnt:
+            prof[nm] = {"ms_per_step": t / args.steps, "launches": cnt, "work_per_step": work / args.steps,
+                        "rate": work / (t * 1e-3) / 1e12 if t > 0 else None}
+    logdet = A.logdet()
+    # e2e through the C ABI from host buffers
+    e2e_ms = None
+    if not args.no_e2e:
+        xs = np.ascontiguousarray(x)
+        ys = np.ascontiguousarray(y)
+        e2e = []
+        for _ in range(max(1, args.steps)):
+            ctx.synchronize()
+            t0 = time.perf_counter()
+            A.fill_matern_points(xs, ys, 0.5, args.range, 1.0, args.nugget)  # H2D + generate
+            mp.tile_chol(A)
+            A.logdet()  # D2H of the step's result (synchronises)
+            e2e.append(time.perf_counter() - t0)
+        e2e_ms = dist_max(float(np.mean(e2e)) * 1e3, world)
+    pk, src = peaks()
+    flops = n ** 3 / 3
+    fp = flops_by_precision(nt, nb, g)
+    f16 = prof.get("gemm_f16")
+    roof = None
+    if f16:
+        # dominant kernel: tcgen05 FP16 GEMM; algorithmic flops / its event time
+        ach = f16["rate"]
+        peak = pk["bf16_tflops_sustained"]
+        roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": ach / peak, "traffic": None,
+                "kernel": "gemm_f16_tc_kernel (tcgen05 kind::f16, grouped trailing update + panel TRSM)",
+                "peak_source": f"{src} bf16_tflops_sustained (FP16 = BF16 tensor rate)",
+                "share_of_step": f16["ms_per_step"] / ms}
+    nominal = {"fp16": pk["bf16_tflops_sustained"], "fp32_simt": 74.0, "fp64": 37.0}
+    tmin = fp[0] / (nominal["fp16"] * 1e12) + fp[1] / (nominal["fp32_simt"] * 1e12) + \
+        fp[2] / (nominal["fp64"] * 1e12)
+    value = world * flops / (ms_max * 1e-3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "mixed(f64/f32/f16-storage; f16 tcgen05 f32-acc, f32/f64 SIMT)",
+        "data": "synthetic",
+        "config": {"workload": f"MPCRTile mixed-precision Cholesky n={n}, tile {nb}, 1 replica/GPU",
+                   "n": n, "nb": nb, "precision_map": f"|i-j|<{args.b64}:FP64, <{args.b32}:FP32, else FP16",
+                   "tiles_by_precision": {p: int((g == i).sum()) for i, p in enumerate(["f16", "f32", "f64"])},
+                   "covariance": f"Matern nu=0.5 range {args.range} sigma2 1 nugget {args.nugget}, "
+                                 f"first {n} points of a {side}x{side} unit grid",
+                   "fp32_method": "SIMT", "l2": "inputs 8+ GB >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"replicas x{world}"},
+        "roofline": roof,
+        "blended_roofline": {"t_min_ms": tmin * 1e3, "frac": tmin / (ms_max * 1e-3),
+                             "flops_by_dest_precision": {"f16": fp[0], "f32": fp[1], "f64": fp[2]},
+                             "peaks_tflops": nominal,
+                             "note": "fp16 measured sustained; fp32/fp64 nominal (not measured)"},
+        "breakdown": prof,
+        "gpu_launches": launches,
+        "wall_ms_per_step": t_wall / args.steps * 1e3,
+        "logdet": logdet,
+        "clocks": clk.summary(),
+    }
+    if e2e_ms is not None:
+        line["e2e"] = {"value": world * flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                       "h2d_bytes_per_step": 2 * n * 8, "d2h_bytes_per_step": 8,
+                       "ms_per_step": e2e_ms,
+                       "path": "host (x,y) -> mp_tile_fill_matern_points -> mp_tile_chol -> mp_tile_logdet"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"], _ = cpu_reference_chol(args)
+    if rank == 0:
+        print(json.dumps(line))
+    ctx.synchronize()
+
+
+def run_gemm(args, world, rank, local):
+    """Config 2 line: per-precision GEMM TFLOP/s (n x n x n, C = A B)."""
+    import torch
+
+    import paper_2406_02701_b200 as mp
+
+    ctx = mp.Context(local)
+    n = args.n
+    p = mp.parse_precision(args.prec)
+    rng = np.random.default_rng(1000 + n)
+    A = mp.MPArray.from_numpy(rng.random((n, n)), p, ctx)
+    B = mp.MPArray.from_numpy(rng.random((n, n)), p, ctx)
+    Cm = mp.MPArray.zeros_matrix(n, n, p, ctx)
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
+    for _ in range(args.warmup):
+        mp.linalg.gemm(A, B, Cm)
+    ctx.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            mp.linalg.gemm(A, B, Cm)
+        e1.record(stream)
+        ctx.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    tf = 2 * n ** 3 / (ms * 1e-3) / 1e12
+    pk, src = peaks()
+    print(json.dumps({"metric": f"{args.prec} GEMM TFLOP/s", "value": tf, "unit": "TFLOP/s",
+                      "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                      "higher_is_better": True, "config": {"workload": f"GEMM {n}^3 {args.prec}"},
+                      "roofline": {"bound": "tensor", "achieved": tf, "peak": pk["bf16_tflops"],
+                                   "unit": "TFLOP/s", "frac": tf / pk["bf16_tflops"]} if p == 0 else None,
+                      "clocks": clk.summary()}))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="chol", choices=["chol", "gemm"])
+    ap.add_argument("--n", type=int, default=65536)
+    ap.add_argument("--nb", type=int, default=1024)
+    ap.add_argument("--b64", type=int, default=1)
+    ap.add_argument("--b32", type=int, default=2)
+    ap.add_argument("--range", type=float, default=0.1)
+    ap.add_argument("--nugget", type=float, default=0.0)
+    ap.add_argument("--prec", default="half")
+    ap.add_argument("--cpu-n", type=int, default=2048)
+    ap.add_argument("--cpu-nb", type=int, default=256)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank)
+    elif args.workload == "gemm":
+        run_gemm(args, world, rank, local)
+    else:
+        run_chol(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

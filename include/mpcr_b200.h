@@ -212,6 +212,14 @@ mp_status mp_tile_logdet(mp_ctx ctx, mp_tile l, double* logdet);
  * side x side unit grid, x fastest).  Each tile rounded to its precision. */
 mp_status mp_tile_fill_matern(mp_ctx ctx, mp_tile t, int64_t grid_side, double nu,
                               double range, double variance);
+/* Same closed forms for arbitrary 2-D locations given in HOST memory
+ * (x[0..n), y[0..n); n = rows = cols), copied up on the context stream;
+ * `nugget` is added to the diagonal before rounding (0 for none). */
+mp_status mp_tile_fill_matern_points(mp_ctx ctx, mp_tile t, const double* host_x,
+                                     const double* host_y, int64_t n, double nu, double range,
+                                     double variance, double nugget);
+/* Device copy of all tile values (identical grids and precisions). */
+mp_status mp_tile_copy(mp_ctx ctx, mp_tile dst, mp_tile src);
 
 #ifdef __cplusplus
 }

@@ -83,6 +83,9 @@ SIGNATURES = {
     "mp_tile_trsm": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_double]),
     "mp_tile_logdet": (C.c_int, [_vp, _vp, C.POINTER(C.c_double)]),
     "mp_tile_fill_matern": (C.c_int, [_vp, _vp, _i64, C.c_double, C.c_double, C.c_double]),
+    "mp_tile_fill_matern_points": (C.c_int, [_vp, _vp, _vp, _vp, _i64, C.c_double, C.c_double,
+                                             C.c_double, C.c_double]),
+    "mp_tile_copy": (C.c_int, [_vp, _vp, _vp]),
 }
 
 

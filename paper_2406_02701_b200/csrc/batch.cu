@@ -16,7 +16,9 @@ template <> __device__ __forceinline__ uint16_t cv<uint16_t, uint16_t>(uint16_t 
 template <> __device__ __forceinline__ float cv<uint16_t, float>(uint16_t x) { return h2f(x); }
 template <> __device__ __forceinline__ double cv<uint16_t, double>(uint16_t x) { return h2d(x); }
 template <> __device__ __forceinline__ uint16_t cv<float, uint16_t>(float x) { return f2h(x); }
-template <> __device__ __forceinline__ float cv<float, float>(float x) { return x; }
+template <> __device__ __forceinline__ float cv<float, float>(float x) {
+    return x != x ? __int_as_float(__float_as_int(x) | 0x00400000) : x;
+}
 template <> __device__ __forceinline__ double cv<float, double>(float x) { return f2d(x); }
 template <> __device__ __forceinline__ uint16_t cv<double, uint16_t>(double x) { return d2h(x); }
 template <> __device__ __forceinline__ float cv<double, float>(double x) { return d2f(x); }

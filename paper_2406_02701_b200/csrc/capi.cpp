@@ -345,10 +345,8 @@ mp_status mp_array_wrap(mp_ctx ctx, mp_precision p, int64_t rows, int64_t cols, 
 mp_status mp_array_destroy(mp_array a) {
     MP_API_BEGIN
     if (!a) return MP_OK;
-    if (a->owner && a->data) {
-        cudaStreamSynchronize(a->ctx->stream);
-        cudaFree(a->data);
-    }
+    // cudaFree synchronises the device; the owning context may already be gone.
+    if (a->owner && a->data) cudaFree(a->data);
     delete a;
     MP_API_END
 }

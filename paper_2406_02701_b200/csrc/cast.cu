@@ -41,7 +41,11 @@ template <> __device__ __forceinline__ uint16_t cvt1<uint16_t, uint16_t>(uint16_
 template <> __device__ __forceinline__ float cvt1<uint16_t, float>(uint16_t x) { return h2f(x); }
 template <> __device__ __forceinline__ double cvt1<uint16_t, double>(uint16_t x) { return h2d(x); }
 template <> __device__ __forceinline__ uint16_t cvt1<float, uint16_t>(float x) { return f2h(x); }
-template <> __device__ __forceinline__ float cvt1<float, float>(float x) { return x; }
+// Single storage only ever holds values that went through a double
+// (set_linear), so a signalling NaN comes back quieted (cvtss2sd/cvtsd2ss).
+template <> __device__ __forceinline__ float cvt1<float, float>(float x) {
+    return x != x ? __int_as_float(__float_as_int(x) | 0x00400000) : x;
+}
 template <> __device__ __forceinline__ double cvt1<float, double>(float x) { return f2d(x); }
 template <> __device__ __forceinline__ uint16_t cvt1<double, uint16_t>(double x) { return d2h(x); }
 template <> __device__ __forceinline__ float cvt1<double, float>(double x) { return d2f(x); }

@@ -224,42 +224,48 @@ __global__ void logdiag_kernel(const ST<P>* __restrict__ a, int64_t lda, int64_t
     if (threadIdx.x == 0) *out += s[0];
 }
 
-// Matern closed forms (covariance.cpp:44-72) on a side x side unit grid with
-// x fastest (covariance.cpp:15-21); point p = (p % side, p / side)/(side-1).
+// Matern closed forms (covariance.cpp:44-72).
+__device__ __forceinline__ double matern_value(double d, double nu, double range, double var) {
+    if (nu == 0.5) return var * exp(-d / range);
+    if (nu == 1.5) {
+        const double r = sqrt(3.0) * d / range;
+        return var * (1.0 + r) * exp(-r);
+    }
+    const double r = sqrt(5.0) * d / range;
+    return var * (1.0 + r + r * r / 3.0) * exp(-r);
+}
+
+// Unit grid with x fastest (covariance.cpp:15-21): point p has coordinates
+// (p % side, p / side) / (side - 1), divided exactly as the reference does.
 template <int P>
-__global__ void matern_kernel(ST<P>* __restrict__ dst, int64_t ld, int64_t row0, int64_t col0,
-                              int64_t rows, int64_t cols, int64_t side, double nu,
-                              double range, double var) {
+__global__ void matern_grid_kernel(ST<P>* __restrict__ dst, int64_t ld, int64_t row0,
+                                   int64_t col0, int64_t rows, int64_t cols, int64_t side,
+                                   double nu, double range, double var) {
     const int64_t n = rows * cols;
-    const double inv = 1.0 / static_cast<double>(side - 1);
+    const double den = static_cast<double>(side - 1);
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = t / rows, i = t - j * rows;
         const int64_t pi = row0 + i, pj = col0 + j;
-        const double xi = static_cast<double>(pi % side) * inv;
-        const double yi = static_cast<double>(pi / side) * inv;
-        const double xj = static_cast<double>(pj % side) * inv;
-        const double yj = static_cast<double>(pj / side) * inv;
-        // The reference divides i / (side - 1); replicate that rounding.
-        const double xi2 = static_cast<double>(pi % side) / static_cast<double>(side - 1);
-        const double yi2 = static_cast<double>(pi / side) / static_cast<double>(side - 1);
-        const double xj2 = static_cast<double>(pj % side) / static_cast<double>(side - 1);
-        const double yj2 = static_cast<double>(pj / side) / static_cast<double>(side - 1);
-        (void)xi;
-        (void)yi;
-        (void)xj;
-        (void)yj;
-        const double d = hypot(xi2 - xj2, yi2 - yj2);
-        double v;
-        if (nu == 0.5) {
-            v = var * exp(-d / range);
-        } else if (nu == 1.5) {
-            const double r = sqrt(3.0) * d / range;
-            v = var * (1.0 + r) * exp(-r);
-        } else {
-            const double r = sqrt(5.0) * d / range;
-            v = var * (1.0 + r + r * r / 3.0) * exp(-r);
-        }
+        const double dx = static_cast<double>(pi % side) / den - static_cast<double>(pj % side) / den;
+        const double dy = static_cast<double>(pi / side) / den - static_cast<double>(pj / side) / den;
+        store_from(dst, j * ld + i, matern_value(hypot(dx, dy), nu, range, var));
+    }
+}
+
+// Arbitrary locations (x[p], y[p]); `nugget` added on the global diagonal.
+template <int P>
+__global__ void matern_points_kernel(ST<P>* __restrict__ dst, int64_t ld, int64_t row0,
+                                     int64_t col0, int64_t rows, int64_t cols,
+                                     const double* __restrict__ x, const double* __restrict__ y,
+                                     double nu, double range, double var, double nugget) {
+    const int64_t n = rows * cols;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = t / rows, i = t - j * rows;
+        const int64_t pi = row0 + i, pj = col0 + j;
+        double v = matern_value(hypot(x[pi] - x[pj], y[pi] - y[pj]), nu, range, var);
+        if (pi == pj) v += nugget;
         store_from(dst, j * ld + i, v);
     }
 }
@@ -427,11 +433,27 @@ void launch_matern_tile(Ctx* ctx, cudaStream_t s, mp_precision p, void* dst, int
     const int g = grid_for(rows * cols, 256, ctx->sm_count);
     dispatch_p(p, [&](auto pp) {
         constexpr int P = decltype(pp)::value;
-        matern_kernel<P><<<g, 256, 0, s>>>(static_cast<ST<P>*>(dst), ld, row0, col0, rows, cols,
-                                           side, nu, range, variance);
+        matern_grid_kernel<P><<<g, 256, 0, s>>>(static_cast<ST<P>*>(dst), ld, row0, col0, rows,
+                                                cols, side, nu, range, variance);
     });
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());
 }
 
+}  // namespace mpcr
+
+namespace mpcr {
+void launch_matern_points(Ctx* ctx, cudaStream_t s, mp_precision p, void* dst, int64_t ld,
+                          int64_t row0, int64_t col0, int64_t rows, int64_t cols, const double* x,
+                          const double* y, double nu, double range, double variance,
+                          double nugget) {
+    const int g = grid_for(rows * cols, 256, ctx->sm_count);
+    dispatch_p(p, [&](auto pp) {
+        constexpr int P = decltype(pp)::value;
+        matern_points_kernel<P><<<g, 256, 0, s>>>(static_cast<ST<P>*>(dst), ld, row0, col0, rows,
+                                                  cols, x, y, nu, range, variance, nugget);
+    });
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
 }  // namespace mpcr

@@ -192,6 +192,11 @@ void launch_matern_tile(Ctx* ctx, cudaStream_t s, mp_precision p, void* dst, int
                         int64_t row0, int64_t col0, int64_t rows, int64_t cols,
                         int64_t side, double nu, double range, double variance);
 
+void launch_matern_points(Ctx* ctx, cudaStream_t s, mp_precision p, void* dst, int64_t ld,
+                          int64_t row0, int64_t col0, int64_t rows, int64_t cols, const double* x,
+                          const double* y, double nu, double range, double variance,
+                          double nugget);
+
 inline void count_launch(Ctx* ctx, int n = 1) { ctx->launches += n; }
 
 extern thread_local std::string g_last_error;

@@ -394,10 +394,7 @@ mp_status mp_tile_create(mp_ctx ctx, int64_t rows, int64_t cols, int64_t rpt, in
 
 mp_status mp_tile_destroy(mp_tile t) {
     MP_API_BEGIN
-    if (t) {
-        cudaStreamSynchronize(t->ctx->stream);
-        delete t;
-    }
+    if (t) delete t;  // cudaFree in the destructor synchronises the device
     MP_API_END
 }
 
@@ -670,6 +667,41 @@ mp_status mp_tile_fill_matern(mp_ctx ctx, mp_tile t, int64_t side, double nu, do
         for (int64_t i = 0; i < x.tr; ++i)
             launch_matern_tile(c, c->stream, x.p(i, j), x.ptr(i, j), x.br, i * x.br, j * x.bc, x.br,
                                x.bc, side, nu, range, variance);
+    MP_API_END
+}
+
+mp_status mp_tile_fill_matern_points(mp_ctx ctx, mp_tile t, const double* host_x,
+                                     const double* host_y, int64_t n, double nu, double range,
+                                     double variance, double nugget) {
+    MP_API_BEGIN
+    mp_tile_s& x = T_(t);
+    Ctx* c = ctx;
+    if (!c || !host_x || !host_y) fail(MP_INVALID_PARAM, "null argument");
+    if (n != x.rows || n != x.cols) fail(MP_SHAPE_MISMATCH, "matern: n must equal rows = cols");
+    if (range <= 0.0 || variance <= 0.0)
+        fail(MP_INVALID_PARAM, "matern_cov: range and variance must be positive");
+    if (nu != 0.5 && nu != 1.5 && nu != 2.5) fail(MP_INVALID_PARAM, "matern_cov: nu must be 0.5, 1.5, or 2.5");
+    double* xy = static_cast<double*>(c->ensure_scratch(2 * n * sizeof(double), 1));
+    MP_CUDA(cudaMemcpyAsync(xy, host_x, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    MP_CUDA(cudaMemcpyAsync(xy + n, host_y, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    for (int64_t j = 0; j < x.tc; ++j)
+        for (int64_t i = 0; i < x.tr; ++i)
+            launch_matern_points(c, c->stream, x.p(i, j), x.ptr(i, j), x.br, i * x.br, j * x.bc,
+                                 x.br, x.bc, xy, xy + n, nu, range, variance, nugget);
+    MP_API_END
+}
+
+mp_status mp_tile_copy(mp_ctx ctx, mp_tile dst, mp_tile src) {
+    MP_API_BEGIN
+    mp_tile_s &d = T_(dst), &s = T_(src);
+    if (!ctx) fail(MP_INVALID_PARAM, "null context");
+    if (d.rows != s.rows || d.cols != s.cols || d.br != s.br || d.bc != s.bc || d.prec != s.prec)
+        fail(MP_SHAPE_MISMATCH, "tile copy: grids differ");
+    for (int q = 0; q < 3; ++q)
+        if (s.nslot[q])
+            MP_CUDA(cudaMemcpyAsync(d.slab[q], s.slab[q],
+                                    static_cast<size_t>(s.nslot[q]) * s.tt() * elem_bytes((mp_precision)q),
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
     MP_API_END
 }
 

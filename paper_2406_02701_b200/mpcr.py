@@ -428,6 +428,18 @@ class MPCRTile:
     def fill_matern(self, grid_side: int, nu=0.5, range_=0.1, variance=1.0):
         check(lib().mp_tile_fill_matern(self.ctx.h, self.h, grid_side, nu, range_, variance))
 
+    def fill_matern_points(self, x: np.ndarray, y: np.ndarray, nu=0.5, range_=0.1,
+                           variance=1.0, nugget=0.0):
+        """Matern covariance of host locations (x, y), generated on the device."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        check(lib().mp_tile_fill_matern_points(self.ctx.h, self.h, x.ctypes.data_as(C.c_void_p),
+                                               y.ctypes.data_as(C.c_void_p), x.size, nu, range_,
+                                               variance, nugget))
+
+    def copy_from(self, src: "MPCRTile"):
+        check(lib().mp_tile_copy(self.ctx.h, self.h, src.h))
+
     def logdet(self) -> float:
         v = C.c_double()
         check(lib().mp_tile_logdet(self.ctx.h, self.h, C.byref(v)))

@@ -83,7 +83,9 @@ def test_gemm_fp16_large_vs_fp64(ctx, rng):
     dc = mp.MPArray.zeros_matrix(n, n, mp.Precision.Single, ctx)
     mp.linalg.gemm(da, db, dc)
     exact = A @ B
-    assert rel(dc.to_numpy(), exact) < 1e-6
+    # the tensor core's FP32 accumulator truncates (measured bias ~1e-5 at
+    # k=2048); still inside the reference's k*u_single bound (1.2e-4)
+    assert rel(dc.to_numpy(), exact) < 2048 * 2.0 ** -24
     dh = mp.MPArray.zeros_matrix(n, n, mp.Precision.Half, ctx)
     mp.linalg.gemm(da, db, dh)
     assert rel(dh.to_numpy(), exact) < 2 * 2.0 ** -11
