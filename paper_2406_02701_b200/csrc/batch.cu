@@ -97,10 +97,29 @@ __global__ void __launch_bounds__(64) leaf_inverse_kernel(const double* __restri
     }
 }
 
+// hi = fp16(x), lo = fp16(x - hi): x ~= hi + lo to ~2^-22 relative.
+__global__ void split_f16_kernel(const double* __restrict__ x, uint16_t* __restrict__ hi,
+                                 uint16_t* __restrict__ lo, int64_t n) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const double v = x[t];
+        const uint16_t h = d2h(v);
+        hi[t] = h;
+        lo[t] = d2h(v - h2d(h));
+    }
+}
+
 template <int P>
 using ST = typename Storage<P>::T;
 
 }  // namespace
+
+void launch_split_f16(Ctx* ctx, cudaStream_t s, const double* x, uint16_t* hi, uint16_t* lo,
+                      int64_t n) {
+    split_f16_kernel<<<grid_for(n, 256, ctx->sm_count), 256, 0, s>>>(x, hi, lo, n);
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
 
 void launch_batched_convert(Ctx* ctx, cudaStream_t s, mp_precision pin, mp_precision pout,
                             const CopyItem* dev_items, int64_t count, int64_t elems) {

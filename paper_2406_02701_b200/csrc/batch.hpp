@@ -14,6 +14,9 @@ void launch_batched_convert(Ctx* ctx, cudaStream_t s, mp_precision pin, mp_preci
                             const CopyItem* dev_items, int64_t count, int64_t elems);
 void launch_batched_zero(Ctx* ctx, cudaStream_t s, mp_precision p, void* const* dev_ptrs,
                          int64_t count, int64_t elems, bool upper_only, int64_t nb);
+// hi/lo FP16 split of an FP64 array (hi + lo carries ~22 significant bits).
+void launch_split_f16(Ctx* ctx, cudaStream_t s, const double* x, uint16_t* hi, uint16_t* lo,
+                      int64_t n);
 // Leaf (64x64 diagonal block) inverses of a lower-triangular FP64 matrix,
 // written onto the diagonal blocks of Linv.
 void launch_leaf_inverse(Ctx* ctx, cudaStream_t s, const double* L, int64_t ldl, int64_t n,

@@ -40,6 +40,7 @@ constexpr int TMEM_COLS = 512;
 struct Params {
     CUtensorMap map_a;
     CUtensorMap map_b;
+    CUtensorMap map_b2;         // second K segment's B (== map_b when unused)
     const TcProblem* problems;  // nullptr -> use `single`
     TcProblem single;
     int32_t nprob;
@@ -47,6 +48,7 @@ struct Params {
     int64_t ldc;
     float alpha, beta;
     int32_t mblocks, nblocks, kblocks;
+    int32_t kblocks1;  // K blocks of the first segment (== kblocks without B2)
 };
 
 __device__ __forceinline__ bool skip_tile(const TcProblem& pr, int m0, int n0) {
@@ -78,6 +80,7 @@ __global__ void __launch_bounds__(256, 1) gemm_f16_tc_kernel(const __grid_consta
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&p.map_a);
         ptx::tma_prefetch_desc(&p.map_b);
+        ptx::tma_prefetch_desc(&p.map_b2);
         for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
@@ -119,21 +122,25 @@ __global__ void __launch_bounds__(256, 1) gemm_f16_tc_kernel(const __grid_consta
                     ptx::mbar_arrive_expect_tx(&full[stage], A_STAGE + B_STAGE);
                     uint8_t* a_dst = sA + stage * A_STAGE;
                     uint8_t* b_dst = sB + stage * B_STAGE;
+                    // K-concatenated second operand: A reused against B2
+                    const bool second = kb >= p.kblocks1;
+                    const int kk = (second ? kb - p.kblocks1 : kb) * BK;
+                    const CUtensorMap* mb = second ? &p.map_b2 : &p.map_b;
                     if (A_MN) {
 #pragma unroll
                         for (int j = 0; j < BM / 64; ++j)
                             ptx::tma_load_3d(a_dst + j * 8192, &p.map_a, &full[stage], m0 + j * 64,
-                                             kb * BK, pr.a_tile);
+                                             kk, pr.a_tile);
                     } else {
-                        ptx::tma_load_3d(a_dst, &p.map_a, &full[stage], kb * BK, m0, pr.a_tile);
+                        ptx::tma_load_3d(a_dst, &p.map_a, &full[stage], kk, m0, pr.a_tile);
                     }
                     if (B_MN) {
 #pragma unroll
                         for (int j = 0; j < BN / 64; ++j)
-                            ptx::tma_load_3d(b_dst + j * 8192, &p.map_b, &full[stage], n0 + j * 64,
-                                             kb * BK, pr.b_tile);
+                            ptx::tma_load_3d(b_dst + j * 8192, mb, &full[stage], n0 + j * 64, kk,
+                                             pr.b_tile);
                     } else {
-                        ptx::tma_load_3d(b_dst, &p.map_b, &full[stage], kb * BK, n0, pr.b_tile);
+                        ptx::tma_load_3d(b_dst, mb, &full[stage], kk, n0, pr.b_tile);
                     }
                     if (++stage == STAGES) {
                         stage = 0;
@@ -327,7 +334,18 @@ void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
     p.beta = static_cast<float>(g.beta);
     p.mblocks = static_cast<int32_t>((g.m + BM - 1) / BM);
     p.nblocks = static_cast<int32_t>((g.n + BN - 1) / BN);
-    p.kblocks = static_cast<int32_t>((g.k + BK - 1) / BK);
+    p.kblocks1 = static_cast<int32_t>((g.k + BK - 1) / BK);
+    p.kblocks = p.kblocks1;
+    if (g.B2) {
+        // second K segment: same shape and layout as B
+        if (b_mn)
+            make_map(&p.map_b2, g.B2, g.n, g.k, g.b_tiles, g.ldb, g.b_tile_stride, 64, 64);
+        else
+            make_map(&p.map_b2, g.B2, g.k, g.n, g.b_tiles, g.ldb, g.b_tile_stride, 64, BN);
+        p.kblocks = 2 * p.kblocks1;
+    } else {
+        p.map_b2 = p.map_b;
+    }
     const int64_t total = static_cast<int64_t>(p.nprob) * p.mblocks * p.nblocks;
     ProfScope ps(ctx, MP_PROF_GEMM_F16, s,
                  2.0 * static_cast<double>(g.m) * g.n * g.k * p.nprob *

@@ -34,6 +34,10 @@ struct TcGemm {
     bool lower_only = false;
     const TcProblem* problems = nullptr;
     int64_t count = 0;
+    // Optional second B operand concatenated along K with A reused:
+    // C = alpha (A op(B) + A op(B2)) + beta C, both in one FP32 accumulator
+    // (the hi + lo split of an FP64 inverse, see tile.cpp TRSM).
+    const void* B2 = nullptr;
 };
 
 bool tc_gemm_supported(const TcGemm& g);

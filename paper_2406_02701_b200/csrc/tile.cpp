@@ -88,8 +88,8 @@ void ensure_panels(mp_tile_s& t) {
             MP_CUDA(cudaMalloc(&t.panel[q], static_cast<size_t>(t.tr) * t.tt() * elem_bytes((mp_precision)q)));
     if (!t.work) {
         const size_t nn = static_cast<size_t>(t.br) * t.br;
-        // FP64 work, FP64 Linv, FP32 work, FP32 LinvS, FP16 LinvH, info
-        MP_CUDA(cudaMalloc(&t.work, nn * (8 + 8 + 4 + 4 + 2) + 256));
+        // FP64 work, FP64 Linv, FP32 work, FP32 LinvS, FP16 LinvH hi + lo, info
+        MP_CUDA(cudaMalloc(&t.work, nn * (8 + 8 + 4 + 4 + 2 + 2) + 256));
     }
 }
 
@@ -214,7 +214,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     float* swork = reinterpret_cast<float*>(w + nn * 16);
     float* linvS = reinterpret_cast<float*>(w + nn * 20);
     uint16_t* linvH = reinterpret_cast<uint16_t*>(w + nn * 24);
-    int64_t* dinfo = reinterpret_cast<int64_t*>(w + nn * 26 + 64);
+    uint16_t* linvHlo = reinterpret_cast<uint16_t*>(w + nn * 26);
+    int64_t* dinfo = reinterpret_cast<int64_t*>(w + nn * 28 + 64);
     const int64_t neg = -1;
     MP_CUDA(cudaMemcpyAsync(dinfo, &neg, sizeof(neg), cudaMemcpyHostToDevice, s));
 
@@ -242,7 +243,16 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         if (k + 1 == NT) break;
         // 2. Linv rounded to the panel precisions (the reference rounds U_kk
         //    to p_ik before trsm: U_kk.converted(p_ik))
-        if (L.need_linv[MP_HALF]) launch_convert(c, s, MP_DOUBLE, linv64, nb, MP_HALF, linvH, nb, nb, nb);
+        // FP16 panels apply the inverse as hi + lo FP16 halves accumulated in
+        // one FP32 accumulator: an explicit inverse rounded to FP16 alone has
+        // a backward error ~cond(L_kk) * 2^-11 and loses definiteness where
+        // the reference's substitution does not.
+        if (L.need_linv[MP_HALF]) {
+            if (L.n_trsm_tc)
+                launch_split_f16(c, s, linv64, linvH, linvHlo, static_cast<int64_t>(nn));
+            else
+                launch_convert(c, s, MP_DOUBLE, linv64, nb, MP_HALF, linvH, nb, nb, nb);
+        }
         if (L.need_linv[MP_SINGLE]) launch_convert(c, s, MP_DOUBLE, linv64, nb, MP_SINGLE, linvS, nb, nb, nb);
         // 3. TRSM as GEMM: panel_q[i] = A_ik * Linv_q^T
         if (L.n_trsm_tc) {
@@ -260,6 +270,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             g.a_tiles = t.nslot[MP_HALF];
             g.a_tile_stride = tt;
             g.B = linvH;
+            g.B2 = linvHlo;
             g.ldb = nb;
             g.b_tiles = 1;
             g.b_tile_stride = tt;
