@@ -374,13 +374,13 @@ def run_gemm(args, world, rank, local):
     Cm = mp.MPArray.zeros_matrix(n, n, p, ctx)
     stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
     for _ in range(args.warmup):
-        mp.linalg.gemm(A, B, Cm)
+        mp.linalg.gemm(A, B, Cm, args.ta, args.tb, 1.0, args.beta)
     ctx.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
-            mp.linalg.gemm(A, B, Cm)
+            mp.linalg.gemm(A, B, Cm, args.ta, args.tb, 1.0, args.beta)
         e1.record(stream)
         ctx.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
@@ -408,6 +408,9 @@ def main():
     ap.add_argument("--range", type=float, default=0.1)
     ap.add_argument("--nugget", type=float, default=0.0)
     ap.add_argument("--prec", default="half")
+    ap.add_argument("--ta", action="store_true")
+    ap.add_argument("--tb", action="store_true")
+    ap.add_argument("--beta", type=float, default=0.0)
     ap.add_argument("--cpu-n", type=int, default=2048)
     ap.add_argument("--cpu-nb", type=int, default=256)
     ap.add_argument("--no-e2e", action="store_true")

@@ -28,6 +28,7 @@ void launch_gemm(Ctx* ctx, cudaStream_t s, const GemmDesc& g) {
         t.b_tile_stride = g.ldb * (g.tb ? g.k : g.n);
         t.C = g.C;
         t.ldc = g.ldc;
+        t.c_tile_stride = g.ldc * g.n;
         t.lower_only = g.lower_only;
         if (tc_gemm_supported(t)) {
             launch_tc_gemm(ctx, s, t);

@@ -3,24 +3,28 @@
 // Serves linalg::gemm / matmul / crossprod (linalg.cpp:316-357, :284-314) when
 // both operands are half and C is half or single (the reference computes
 // these in float, linalg.cpp:340-348; FP16 x FP16 products are exact in FP32
-// and the tensor core accumulates in FP32), and the FP16 trailing-update
-// tiles of the MPCRTile Cholesky (grouped, one launch per step).
+// and the tensor core accumulates in FP32), and the FP16 trailing-update and
+// panel-TRSM tiles of the MPCRTile Cholesky (grouped, one launch per step).
 //
-// Structure (persistent, warp-specialised, one CTA per SM):
-//   warp 0      TMA producer: 4-stage ring of {A 128x64, B 256x64} FP16 tiles
-//               in 128B-swizzled shared memory, one mbarrier pair per stage.
-//   warp 1      MMA issuer: one elected thread issues tcgen05.mma
-//               (M=128, N=256, K=16) into a double-buffered TMEM accumulator
-//               (2 x 256 columns of FP32); tcgen05.commit frees smem stages
-//               and signals the epilogue.
+// Persistent, warp-specialised, one CTA per SM (grid <= 148):
+//   warp 0      TMA producer: 4-stage ring of {A 128x64, B 256x64} FP16
+//               tiles in 128B-swizzled shared memory (mbarrier full/empty).
+//   warp 1      MMA issuer: one thread issues tcgen05.mma (M=128, N=256,
+//               K=16) into a double-buffered TMEM accumulator (2 x 256 FP32
+//               columns); tcgen05.commit frees smem stages / signals TMEM full.
 //   warp 2      TMEM allocator (512 columns).
+//   warp 3      C loader: TMA-loads the C tile chunk (128 x 256B) into a
+//               shared buffer while the MMAs of that tile run (beta != 0 only).
 //   warps 4-7   epilogue: tcgen05.ld 32 lanes x 32 columns, C = alpha*acc +
-//               beta*C (beta == 0 never reads C), rounded to C's precision,
-//               coalesced column-major stores (lanes walk consecutive rows).
-// Operand majorness follows the column-major storage: op(A) = A is
-// MN-major, op(A) = A^T is K-major; op(B) = B is K-major, B^T MN-major.
+//               beta*C in FP32 (beta == 0 never reads C), rounded to C's
+//               precision in the shared chunk, then one TMA store per chunk.
+// Operand majorness follows the column-major storage: op(A) = A is MN-major,
+// A^T K-major; op(B) = B is K-major, B^T MN-major.  All three matrices are
+// addressed by 3-D TMA maps [tile][col][row], so a grouped launch can take any
+// tiles of a slab by index.
 #include <cuda.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "device.cuh"
@@ -34,18 +38,19 @@ namespace tc {
 constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_STAGE = BM * BK * 2;  // 16 KB
 constexpr int B_STAGE = BN * BK * 2;  // 32 KB
-constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int C_CHUNK = BM * 256;     // 32 KB: 128 rows x 256 bytes
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + C_CHUNK + 1024 /*align*/ + 256;
 constexpr int TMEM_COLS = 512;
 
 struct Params {
     CUtensorMap map_a;
     CUtensorMap map_b;
-    CUtensorMap map_b2;         // second K segment's B (== map_b when unused)
+    CUtensorMap map_b2;  // second K segment's B (== map_b when unused)
+    CUtensorMap map_c;
     const TcProblem* problems;  // nullptr -> use `single`
     TcProblem single;
     int32_t nprob;
     int32_t M, N, K;
-    int64_t ldc;
     float alpha, beta;
     int32_t mblocks, nblocks, kblocks;
     int32_t kblocks1;  // K blocks of the first segment (== kblocks without B2)
@@ -55,32 +60,35 @@ __device__ __forceinline__ bool skip_tile(const TcProblem& pr, int m0, int n0) {
     return pr.lower_only && (m0 + BM - 1 < n0);
 }
 
-template <typename TC> __device__ __forceinline__ float load_c(const TC* c, int64_t i);
-template <> __device__ __forceinline__ float load_c<uint16_t>(const uint16_t* c, int64_t i) {
-    return h2f(c[i]);
-}
-template <> __device__ __forceinline__ float load_c<float>(const float* c, int64_t i) {
-    return c[i];
-}
+__device__ __forceinline__ float ld_c(const uint16_t* c, int i) { return h2f(c[i]); }
+__device__ __forceinline__ float ld_c(const float* c, int i) { return c[i]; }
+__device__ __forceinline__ void st_c(uint16_t* c, int i, float v) { c[i] = f2h(v); }
+__device__ __forceinline__ void st_c(float* c, int i, float v) { c[i] = v; }
 
 template <bool A_MN, bool B_MN, typename TC>
 __global__ void __launch_bounds__(256, 1) gemm_f16_tc_kernel(const __grid_constant__ Params p) {
+    constexpr int CW = 256 / sizeof(TC);  // chunk width in columns (128 half / 64 float)
+    constexpr int NCHUNK = BN / CW;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~static_cast<uintptr_t>(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_STAGE;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+    TC* cbuf = reinterpret_cast<TC*>(sB + STAGES * B_STAGE);  // [CW cols][BM rows]
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(cbuf) + C_CHUNK);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* cfull = tempty + 2;
+    uint64_t* cempty = cfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 1);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&p.map_a);
         ptx::tma_prefetch_desc(&p.map_b);
         ptx::tma_prefetch_desc(&p.map_b2);
+        ptx::tma_prefetch_desc(&p.map_c);
         for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
@@ -89,6 +97,8 @@ __global__ void __launch_bounds__(256, 1) gemm_f16_tc_kernel(const __grid_consta
             ptx::mbar_init(&tfull[s], 1);
             ptx::mbar_init(&tempty[s], 128);
         }
+        ptx::mbar_init(cfull, 1);
+        ptx::mbar_init(cempty, 1);
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
@@ -99,6 +109,7 @@ __global__ void __launch_bounds__(256, 1) gemm_f16_tc_kernel(const __grid_consta
 
     const int tiles_per_prob = p.mblocks * p.nblocks;
     const int64_t total = static_cast<int64_t>(p.nprob) * tiles_per_prob;
+    const bool read_c = p.beta != 0.0f;
 
     auto decode = [&](int64_t t, TcProblem& pr, int& m0, int& n0) {
         const int64_t pi = t / tiles_per_prob;
@@ -109,6 +120,7 @@ __global__ void __launch_bounds__(256, 1) gemm_f16_tc_kernel(const __grid_consta
     };
 
     if (warp == 0) {
+        // ===== TMA producer =====
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
@@ -150,6 +162,7 @@ __global__ void __launch_bounds__(256, 1) gemm_f16_tc_kernel(const __grid_consta
             }
         }
     } else if (warp == 1) {
+        // ===== MMA issuer =====
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::umma_idesc(BM, BN, A_MN, B_MN, 0);
             int stage = 0;
@@ -190,45 +203,75 @@ __global__ void __launch_bounds__(256, 1) gemm_f16_tc_kernel(const __grid_consta
                 }
             }
         }
+    } else if (warp == 3) {
+        // ===== C loader: one chunk at a time into the shared C buffer =====
+        if (lane == 0) {
+            uint32_t cphase = 0;
+            for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+                TcProblem pr;
+                int m0, n0;
+                decode(t, pr, m0, n0);
+                if (skip_tile(pr, m0, n0)) continue;
+                for (int h = 0; h < NCHUNK; ++h) {
+                    ptx::mbar_wait(cempty, cphase ^ 1);
+                    if (read_c) {
+                        ptx::mbar_arrive_expect_tx(cfull, C_CHUNK);
+                        ptx::tma_load_3d(cbuf, &p.map_c, cfull, m0, n0 + h * CW, pr.c_tile);
+                    } else {
+                        ptx::mbar_arrive(cfull);
+                    }
+                    cphase ^= 1;
+                }
+            }
+        }
     } else if (warp >= 4) {
+        // ===== epilogue =====
         const int q = warp - 4;
-        TC* __restrict__ Cbase = nullptr;
+        const int r = q * 32 + lane;  // tile row owned by this thread (TMEM lane)
+        const bool is_leader = threadIdx.x == 128;
         int acc = 0;
-        uint32_t acc_phase = 0;
+        uint32_t acc_phase = 0, cphase = 0;
         for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
             TcProblem pr;
             int m0, n0;
             decode(t, pr, m0, n0);
             if (skip_tile(pr, m0, n0)) continue;
-            Cbase = static_cast<TC*>(pr.C);
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
-            const int row = m0 + q * 32 + lane;
-            const bool row_ok = row < p.M;
+            const int row = m0 + r;
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t r[32];
-                ptx::tmem_ld_32x32b_x32(
-                    tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + c * 32, r);
-                ptx::tmem_ld_wait();
-                const int nb = n0 + c * 32;
-                if (row_ok && nb < p.N) {
-                    float old[32];
-                    if (p.beta != 0.0f) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            old[j] = (nb + j < p.N) ? load_c(Cbase, (int64_t)(nb + j) * p.ldc + row)
-                                                    : 0.0f;
-                    }
+            for (int h = 0; h < NCHUNK; ++h) {
+                ptx::mbar_wait(cfull, cphase);
+                cphase ^= 1;
+#pragma unroll 1
+                for (int c = 0; c < CW / 32; ++c) {
+                    uint32_t v[32];
+                    const int col0 = h * CW + c * 32;  // column within the tile
+                    ptx::tmem_ld_32x32b_x32(
+                        tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + col0, v);
+                    ptx::tmem_ld_wait();
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        const int col = nb + j;
-                        if (col < p.N && !(pr.lower_only && row < col)) {
-                            const float a = __fmul_rn(p.alpha, __uint_as_float(r[j]));
-                            const float v = p.beta != 0.0f ? __fadd_rn(a, __fmul_rn(p.beta, old[j])) : a;
-                            store_from(Cbase, (int64_t)col * p.ldc + row, v);
+                        const int cc = c * 32 + j;  // column within the chunk
+                        const float a = __fmul_rn(p.alpha, __uint_as_float(v[j]));
+                        float out = a;
+                        if (read_c) {
+                            const float old = ld_c(cbuf, cc * BM + r);
+                            out = (pr.lower_only && row < n0 + col0 + j)
+                                      ? old
+                                      : __fadd_rn(a, __fmul_rn(p.beta, old));
                         }
+                        st_c(cbuf, cc * BM + r, out);
                     }
+                }
+                // chunk complete: hand it to the TMA unit, then release it
+                ptx::fence_proxy_async_smem();
+                ptx::named_bar_sync(1, 128);
+                if (is_leader) {
+                    ptx::tma_store_3d(&p.map_c, cbuf, m0, n0 + h * CW, pr.c_tile);
+                    ptx::bulk_commit();
+                    ptx::bulk_wait_read0();
+                    ptx::mbar_arrive(cempty);
                 }
             }
             ptx::tc_fence_before();
@@ -238,6 +281,7 @@ __global__ void __launch_bounds__(256, 1) gemm_f16_tc_kernel(const __grid_consta
                 acc_phase ^= 1;
             }
         }
+        if (is_leader) ptx::bulk_wait0();
     }
     __syncthreads();
     if (warp == 2) {
@@ -267,19 +311,26 @@ EncodeFn get_encode() {
     return fn;
 }
 
-// 3-D map over [d2 tiles][d1][d0] 16-bit elements; d0 contiguous.
-void make_map(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
-              uint64_t ld_elems, uint64_t tile_stride_elems, uint32_t box0, uint32_t box1) {
-    const cuuint64_t dims[3] = {d0, d1, d2};
-    const cuuint64_t strides[2] = {ld_elems * 2, tile_stride_elems * 2};
+// 3-D map over [d2 tiles][d1][d0] elements; d0 contiguous.
+void make_map(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int esize, uint64_t d0,
+              uint64_t d1, uint64_t d2, uint64_t ld_elems, uint64_t tile_stride_elems,
+              uint32_t box0, uint32_t box1, CUtensorMapSwizzle swz) {
+    const cuuint64_t dims[3] = {d0, d1, d2 < 1 ? 1 : d2};
+    const cuuint64_t strides[2] = {ld_elems * esize,
+                                   (tile_stride_elems ? tile_stride_elems : ld_elems * d1) * esize};
     const cuuint32_t box[3] = {box0, box1, 1};
     const cuuint32_t estr[3] = {1, 1, 1};
-    const CUresult r = get_encode()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3,
-                                    const_cast<void*>(base), dims, strides, box, estr,
-                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+    const CUresult r = get_encode()(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(MP_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+}
+
+void make_op_map(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                 uint64_t ld, uint64_t ts, uint32_t box1) {
+    make_map(map, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, d0, d1, d2, ld, ts, 64, box1,
+             CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 template <bool A_MN, bool B_MN, typename TC>
@@ -300,59 +351,61 @@ void launch_kernel(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total) {
 }  // namespace tc
 
 bool tc_gemm_supported(const TcGemm& g) {
-    // TMA: 16-byte aligned bases and leading strides.
+    // TMA: 16-byte aligned bases and leading strides for A, B and C.
     auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
-    if (!al(g.A) || !al(g.B)) return false;
-    if ((g.lda * 2) % 16 || (g.ldb * 2) % 16) return false;
+    if (!al(g.A) || !al(g.B) || !al(g.C) || (g.B2 && !al(g.B2))) return false;
+    if ((g.lda * 2) % 16 || (g.ldb * 2) % 16 || (g.ldc * elem_bytes(g.pc)) % 16) return false;
     if (g.m < 1 || g.n < 1 || g.k < 1) return false;
     if (g.m >= (1ll << 31) || g.n >= (1ll << 31) || g.k >= (1ll << 31)) return false;
-    return true;
+    return g.pc == MP_HALF || g.pc == MP_SINGLE;
 }
 
 void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
     using namespace tc;
     Params p;
-    memset(&p, 0, sizeof(p));
+    std::memset(&p, 0, sizeof(p));
     const bool a_mn = !g.ta, b_mn = g.tb;
     // op(A): m x k.  MN-major: storage m x k (ld lda).  K-major: storage k x m.
     if (a_mn)
-        make_map(&p.map_a, g.A, g.m, g.k, g.a_tiles, g.lda, g.a_tile_stride, 64, 64);
+        make_op_map(&p.map_a, g.A, g.m, g.k, g.a_tiles, g.lda, g.a_tile_stride, 64);
     else
-        make_map(&p.map_a, g.A, g.k, g.m, g.a_tiles, g.lda, g.a_tile_stride, 64, BM);
+        make_op_map(&p.map_a, g.A, g.k, g.m, g.a_tiles, g.lda, g.a_tile_stride, BM);
     if (b_mn)
-        make_map(&p.map_b, g.B, g.n, g.k, g.b_tiles, g.ldb, g.b_tile_stride, 64, 64);
+        make_op_map(&p.map_b, g.B, g.n, g.k, g.b_tiles, g.ldb, g.b_tile_stride, 64);
     else
-        make_map(&p.map_b, g.B, g.k, g.n, g.b_tiles, g.ldb, g.b_tile_stride, 64, BN);
+        make_op_map(&p.map_b, g.B, g.k, g.n, g.b_tiles, g.ldb, g.b_tile_stride, BN);
+    if (g.B2) {
+        if (b_mn)
+            make_op_map(&p.map_b2, g.B2, g.n, g.k, g.b_tiles, g.ldb, g.b_tile_stride, 64);
+        else
+            make_op_map(&p.map_b2, g.B2, g.k, g.n, g.b_tiles, g.ldb, g.b_tile_stride, BN);
+    } else {
+        p.map_b2 = p.map_b;
+    }
+    // C: [c_tiles][n][m] with chunks of 128 rows x 256 bytes
+    const bool half_c = g.pc == MP_HALF;
+    make_map(&p.map_c, g.C, half_c ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+             half_c ? 2 : 4, g.m, g.n, g.c_tiles, g.ldc, g.c_tile_stride, BM, half_c ? 128 : 64,
+             CU_TENSOR_MAP_SWIZZLE_NONE);
     p.problems = g.problems;
-    p.single = TcProblem{0, 0, g.lower_only ? 1 : 0, 0, g.C};
+    p.single = TcProblem{0, 0, 0, g.lower_only ? 1 : 0};
     p.nprob = g.problems ? static_cast<int32_t>(g.count) : 1;
     p.M = static_cast<int32_t>(g.m);
     p.N = static_cast<int32_t>(g.n);
     p.K = static_cast<int32_t>(g.k);
-    p.ldc = g.ldc;
     p.alpha = static_cast<float>(g.alpha);
     p.beta = static_cast<float>(g.beta);
     p.mblocks = static_cast<int32_t>((g.m + BM - 1) / BM);
     p.nblocks = static_cast<int32_t>((g.n + BN - 1) / BN);
     p.kblocks1 = static_cast<int32_t>((g.k + BK - 1) / BK);
-    p.kblocks = p.kblocks1;
-    if (g.B2) {
-        // second K segment: same shape and layout as B
-        if (b_mn)
-            make_map(&p.map_b2, g.B2, g.n, g.k, g.b_tiles, g.ldb, g.b_tile_stride, 64, 64);
-        else
-            make_map(&p.map_b2, g.B2, g.k, g.n, g.b_tiles, g.ldb, g.b_tile_stride, 64, BN);
-        p.kblocks = 2 * p.kblocks1;
-    } else {
-        p.map_b2 = p.map_b;
-    }
+    p.kblocks = g.B2 ? 2 * p.kblocks1 : p.kblocks1;
     const int64_t total = static_cast<int64_t>(p.nprob) * p.mblocks * p.nblocks;
     ProfScope ps(ctx, MP_PROF_GEMM_F16, s,
                  2.0 * static_cast<double>(g.m) * g.n * g.k * p.nprob *
                      (g.lower_only ? 0.5 : 1.0));
 #define MP_TC(AM, BMJ)                                                            \
     if (a_mn == AM && b_mn == BMJ) {                                              \
-        if (g.pc == MP_HALF)                                                      \
+        if (half_c)                                                               \
             launch_kernel<AM, BMJ, uint16_t>(ctx, s, p, total);                   \
         else                                                                      \
             launch_kernel<AM, BMJ, float>(ctx, s, p, total);                      \

@@ -7,19 +7,18 @@
 
 namespace mpcr {
 
-// One problem of a grouped launch: operand tiles are indices into the
-// operand slabs' third TMA dimension; C is a direct pointer.
+// One problem of a grouped launch: tiles are indices into the third TMA
+// dimension of the A, B and C slabs.
 struct TcProblem {
     int32_t a_tile;
     int32_t b_tile;
-    int32_t lower_only;
-    int32_t pad;
-    void* C;
+    int32_t c_tile;
+    int32_t lower_only;  // skip / keep C strictly above the diagonal
 };
 
 // C <- alpha op(A) op(B) + beta C with FP16 A, B and half/single C.
-// Dense: a_tiles = b_tiles = 1, problems = nullptr.  Grouped: A and B are
-// slabs of `*_tiles` column-major tiles `*_tile_stride` elements apart.
+// Dense: *_tiles = 1, problems = nullptr.  Grouped: A, B and C are slabs of
+// `*_tiles` column-major tiles `*_tile_stride` elements apart.
 struct TcGemm {
     mp_precision pc = MP_HALF;
     bool ta = false, tb = false;
@@ -30,7 +29,7 @@ struct TcGemm {
     const void* B = nullptr;
     int64_t ldb = 0, b_tiles = 1, b_tile_stride = 0;
     void* C = nullptr;
-    int64_t ldc = 0;
+    int64_t ldc = 0, c_tiles = 1, c_tile_stride = 0;
     bool lower_only = false;
     const TcProblem* problems = nullptr;
     int64_t count = 0;

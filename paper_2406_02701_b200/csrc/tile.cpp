@@ -143,8 +143,9 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             const mp_precision q = t.p(i, k);
             L.need_linv[q] = true;
             if (q == MP_HALF && tc_ok)
-                trsm_tc.push_back(TcProblem{static_cast<int32_t>(t.slot[k * NT + i]), 0, 0, 0,
-                                            t.panel_ptr(MP_HALF, i)});
+                // A = matrix tile (i,k) in the FP16 slab, C = panel16[i]
+                trsm_tc.push_back(TcProblem{static_cast<int32_t>(t.slot[k * NT + i]), 0,
+                                            static_cast<int32_t>(i), 0});
             else
                 trsm_p[q].push_back(TileProblem{t.ptr(i, k), linv[q], t.panel_ptr(q, i), 0, 0});
             wb[q].push_back(CopyItem{t.panel_ptr(q, i), t.ptr(i, k)});
@@ -159,7 +160,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 const mp_precision q = t.p(i, j);
                 const int32_t lo = (i == j) ? 1 : 0;
                 if (q == MP_HALF && tc_ok)
-                    up_tc.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j), lo, 0, t.ptr(i, j)});
+                    up_tc.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
+                                              static_cast<int32_t>(t.slot[j * NT + i]), lo});
                 else
                     up_p[q].push_back(TileProblem{t.panel_ptr(q, i), t.panel_ptr(q, j), t.ptr(i, j), lo, 0});
             }
@@ -274,7 +276,10 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             g.ldb = nb;
             g.b_tiles = 1;
             g.b_tile_stride = tt;
+            g.C = t.panel[MP_HALF];
             g.ldc = nb;
+            g.c_tiles = NT;
+            g.c_tile_stride = tt;
             g.problems = reinterpret_cast<const TcProblem*>(dl + L.trsm_tc);
             g.count = L.n_trsm_tc;
             launch_tc_gemm(c, s, g);
@@ -323,7 +328,10 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             g.ldb = nb;
             g.b_tiles = NT;
             g.b_tile_stride = tt;
+            g.C = t.slab[MP_HALF];
             g.ldc = nb;
+            g.c_tiles = t.nslot[MP_HALF];
+            g.c_tile_stride = tt;
             g.problems = reinterpret_cast<const TcProblem*>(dl + L.up_tc);
             g.count = L.n_up_tc;
             launch_tc_gemm(c, s, g);
