@@ -109,10 +109,92 @@ __global__ void split_f16_kernel(const double* __restrict__ x, uint16_t* __restr
     }
 }
 
+__device__ __forceinline__ float to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+
+// 3xTF32 operand split: hi = tf32(x), lo = tf32(x - hi) (x - hi is exact).
+// One 32x32 block per CTA (blockDim 32x8); with `trans` the packed outputs
+// hold the transpose (cols x rows, ld = cols) so the operand is K-major for
+// kind::tf32 (which reads 128B-swizzled 32-bit data K-major only).
+template <typename TI>
+__device__ __forceinline__ void split_block(const TI* __restrict__ src, int64_t lds, int64_t rows,
+                                            int64_t cols, float* __restrict__ hi,
+                                            float* __restrict__ lo, bool trans,
+                                            float (*th)[33], float (*tl)[33]) {
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32, j0 = static_cast<int64_t>(blockIdx.y) * 32;
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        const int64_t i = i0 + threadIdx.x, j = j0 + r;
+        if (i < rows && j < cols) {
+            const float x = load_as<float>(src, j * lds + i);
+            const float h = to_tf32(x);
+            const float l = to_tf32(x - h);
+            if (!trans) {
+                hi[j * rows + i] = h;
+                lo[j * rows + i] = l;
+            } else {
+                th[r][threadIdx.x] = h;
+                tl[r][threadIdx.x] = l;
+            }
+        }
+    }
+    if (!trans) return;
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        const int64_t oj = i0 + r, oi = j0 + threadIdx.x;  // output (oi, oj) = input (oj, oi)
+        if (oj < rows && oi < cols) {
+            hi[oj * cols + oi] = th[threadIdx.x][r];
+            lo[oj * cols + oi] = tl[threadIdx.x][r];
+        }
+    }
+}
+
+template <typename TI>
+__global__ void split_tf32_2d_kernel(const TI* __restrict__ src, int64_t lds, int64_t rows,
+                                     int64_t cols, float* __restrict__ hi, float* __restrict__ lo,
+                                     bool trans) {
+    __shared__ float th[32][33], tl[32][33];
+    split_block(src, lds, rows, cols, hi, lo, trans, th, tl);
+}
+
+__global__ void batched_split_tf32_kernel(const SplitItem* __restrict__ items, int64_t nb) {
+    __shared__ float th[32][33], tl[32][33];
+    const SplitItem it = items[blockIdx.z];
+    split_block(static_cast<const float*>(it.src), nb, nb, nb, static_cast<float*>(it.hi),
+                static_cast<float*>(it.lo), true, th, tl);
+}
+
 template <int P>
 using ST = typename Storage<P>::T;
 
 }  // namespace
+
+void launch_split_tf32(Ctx* ctx, cudaStream_t s, mp_precision pin, const void* src, int64_t lds,
+                       int64_t rows, int64_t cols, float* hi, float* lo, bool trans) {
+    if (rows == 0 || cols == 0) return;
+    const dim3 grid(static_cast<unsigned>((rows + 31) / 32), static_cast<unsigned>((cols + 31) / 32));
+    const dim3 block(32, 8);
+    if (pin == MP_HALF)
+        split_tf32_2d_kernel<<<grid, block, 0, s>>>(static_cast<const uint16_t*>(src), lds, rows, cols, hi, lo, trans);
+    else if (pin == MP_SINGLE)
+        split_tf32_2d_kernel<<<grid, block, 0, s>>>(static_cast<const float*>(src), lds, rows, cols, hi, lo, trans);
+    else
+        fail(MP_INVALID_PARAM, "split_tf32: double input");
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+void launch_batched_split_tf32_t(Ctx* ctx, cudaStream_t s, const SplitItem* dev_items, int64_t count,
+                                 int64_t nb) {
+    if (count == 0) return;
+    const dim3 grid(static_cast<unsigned>((nb + 31) / 32), static_cast<unsigned>((nb + 31) / 32),
+                    static_cast<unsigned>(count));
+    batched_split_tf32_kernel<<<grid, dim3(32, 8), 0, s>>>(dev_items, nb);
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
 
 void launch_split_f16(Ctx* ctx, cudaStream_t s, const double* x, uint16_t* hi, uint16_t* lo,
                       int64_t n) {

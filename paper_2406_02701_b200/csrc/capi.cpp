@@ -15,8 +15,8 @@ namespace mpcr {
 thread_local std::string g_last_error;
 
 void* Ctx::ensure_scratch(size_t bytes, int which) {
-    void*& p = which == 0 ? scratch : scratch2;
-    size_t& cap = which == 0 ? scratch_bytes : scratch2_bytes;
+    void*& p = scr[which];
+    size_t& cap = scr_bytes[which];
     if (bytes <= cap) return p;
     if (p) {
         MP_CUDA(cudaStreamSynchronize(stream));
@@ -53,12 +53,17 @@ ProfScope::~ProfScope() {
     }
     if (cudaEventRecord(b, s) != cudaSuccess) return;
     ctx->prof.pending.push_back({a, b, cls, work});
-    if (ctx->prof.pending.size() > 4096) prof_collect(ctx);
+    if (ctx->prof.pending.size() > 8192) prof_collect(ctx, false);
 }
 
-void prof_collect(Ctx* ctx) {
+// Fold finished event pairs into the totals.  Non-blocking mode only takes
+// pairs that already completed (in order) so profiling never stalls the host.
+void prof_collect(Ctx* ctx, bool blocking) {
+    size_t done = 0;
     for (auto& r : ctx->prof.pending) {
+        if (!blocking && cudaEventQuery(r.b) != cudaSuccess) break;
         MP_CUDA(cudaEventSynchronize(r.b));
+        ++done;
         float ms = 0.f;
         MP_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
         ctx->prof.ms[r.cls] += ms;
@@ -67,7 +72,7 @@ void prof_collect(Ctx* ctx) {
         ctx->prof.pool.push_back(r.a);
         ctx->prof.pool.push_back(r.b);
     }
-    ctx->prof.pending.clear();
+    ctx->prof.pending.erase(ctx->prof.pending.begin(), ctx->prof.pending.begin() + done);
 }
 
 // Host restatement of encode_f16 rounding for scalars (precision.cpp:49-93),
@@ -212,8 +217,8 @@ mp_status mp_ctx_destroy(mp_ctx ctx) {
         cudaEventDestroy(r.b);
     }
     for (auto e : ctx->prof.pool) cudaEventDestroy(e);
-    if (ctx->scratch) cudaFree(ctx->scratch);
-    if (ctx->scratch2) cudaFree(ctx->scratch2);
+    for (void* p : ctx->scr)
+        if (p) cudaFree(p);
     for (auto& s : ctx->aux) cudaStreamDestroy(s);
     cudaStreamDestroy(ctx->hi);
     cudaStreamDestroy(ctx->own_stream);

@@ -35,17 +35,18 @@
 namespace mpcr {
 namespace tc {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_STAGE = BM * BK * 2;  // 16 KB
-constexpr int B_STAGE = BN * BK * 2;  // 32 KB
+// Every stage holds 128 bytes of K per row for either operand kind:
+// 64 FP16 (kind::f16) or 32 FP32 (kind::tf32) elements.
+constexpr int BM = 128, BN = 256, STAGES = 4;
+constexpr int A_STAGE = BM * 128;  // 16 KB
+constexpr int B_STAGE = BN * 128;  // 32 KB
 constexpr int C_CHUNK = BM * 256;     // 32 KB: 128 rows x 256 bytes
 constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + C_CHUNK + 1024 /*align*/ + 256;
 constexpr int TMEM_COLS = 512;
 
 struct Params {
-    CUtensorMap map_a;
-    CUtensorMap map_b;
-    CUtensorMap map_b2;  // second K segment's B (== map_b when unused)
+    CUtensorMap map_a[2];  // A, A_lo
+    CUtensorMap map_b[2];  // B, B_lo
     CUtensorMap map_c;
     const TcProblem* problems;  // nullptr -> use `single`
     TcProblem single;
@@ -53,7 +54,8 @@ struct Params {
     int32_t M, N, K;
     float alpha, beta;
     int32_t mblocks, nblocks, kblocks;
-    int32_t kblocks1;  // K blocks of the first segment (== kblocks without B2)
+    int32_t kblocks1;  // K blocks per segment; kblocks = nseg * kblocks1
+    int32_t seg_a[3], seg_b[3];  // K segment s multiplies map_a[seg_a[s]] by map_b[seg_b[s]]
 };
 
 __device__ __forceinline__ bool skip_tile(const TcProblem& pr, int m0, int n0) {
@@ -65,8 +67,15 @@ __device__ __forceinline__ float ld_c(const float* c, int i) { return c[i]; }
 __device__ __forceinline__ void st_c(uint16_t* c, int i, float v) { c[i] = f2h(v); }
 __device__ __forceinline__ void st_c(float* c, int i, float v) { c[i] = v; }
 
-template <bool A_MN, bool B_MN, typename TC>
-__global__ void __launch_bounds__(256, 1) gemm_f16_tc_kernel(const __grid_constant__ Params p) {
+// KIND 0: kind::f16 (FP16 operands), KIND 1: kind::tf32 (FP32 storage).
+template <int KIND, bool A_MN, bool B_MN, typename TC>
+__global__ void __launch_bounds__(256, 1) gemm_tc_kernel(const __grid_constant__ Params p) {
+    constexpr int ES = KIND == 0 ? 2 : 4;      // operand element bytes
+    constexpr int BK = 128 / ES;               // K elements per stage
+    constexpr int BW = 128 / ES;               // MN elements per 128B swizzle row
+    constexpr int BOX = BW * BK * ES;          // bytes of one MN-major TMA box
+    constexpr int KSTEP_MN = (32 / ES) * 128;  // UMMA K (32 bytes of K) in MN-major rows
+    constexpr uint32_t FMT = KIND == 0 ? 0u : 2u;
     constexpr int CW = 256 / sizeof(TC);  // chunk width in columns (128 half / 64 float)
     constexpr int NCHUNK = BN / CW;
     extern __shared__ uint8_t smem_raw[];
@@ -85,9 +94,10 @@ __global__ void __launch_bounds__(256, 1) gemm_f16_tc_kernel(const __grid_consta
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (warp == 0 && lane == 0) {
-        ptx::tma_prefetch_desc(&p.map_a);
-        ptx::tma_prefetch_desc(&p.map_b);
-        ptx::tma_prefetch_desc(&p.map_b2);
+        ptx::tma_prefetch_desc(&p.map_a[0]);
+        ptx::tma_prefetch_desc(&p.map_a[1]);
+        ptx::tma_prefetch_desc(&p.map_b[0]);
+        ptx::tma_prefetch_desc(&p.map_b[1]);
         ptx::tma_prefetch_desc(&p.map_c);
         for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(&full[s], 1);
@@ -134,22 +144,23 @@ __global__ void __launch_bounds__(256, 1) gemm_f16_tc_kernel(const __grid_consta
                     ptx::mbar_arrive_expect_tx(&full[stage], A_STAGE + B_STAGE);
                     uint8_t* a_dst = sA + stage * A_STAGE;
                     uint8_t* b_dst = sB + stage * B_STAGE;
-                    // K-concatenated second operand: A reused against B2
-                    const bool second = kb >= p.kblocks1;
-                    const int kk = (second ? kb - p.kblocks1 : kb) * BK;
-                    const CUtensorMap* mb = second ? &p.map_b2 : &p.map_b;
+                    // K segments: (A|A_lo) x (B|B_lo) products into one accumulator
+                    const int sg = kb / p.kblocks1;
+                    const int kk = (kb - sg * p.kblocks1) * BK;
+                    const CUtensorMap* ma = &p.map_a[p.seg_a[sg]];
+                    const CUtensorMap* mb = &p.map_b[p.seg_b[sg]];
                     if (A_MN) {
 #pragma unroll
-                        for (int j = 0; j < BM / 64; ++j)
-                            ptx::tma_load_3d(a_dst + j * 8192, &p.map_a, &full[stage], m0 + j * 64,
-                                             kk, pr.a_tile);
+                        for (int j = 0; j < BM / BW; ++j)
+                            ptx::tma_load_3d(a_dst + j * BOX, ma, &full[stage], m0 + j * BW, kk,
+                                             pr.a_tile);
                     } else {
-                        ptx::tma_load_3d(a_dst, &p.map_a, &full[stage], kk, m0, pr.a_tile);
+                        ptx::tma_load_3d(a_dst, ma, &full[stage], kk, m0, pr.a_tile);
                     }
                     if (B_MN) {
 #pragma unroll
-                        for (int j = 0; j < BN / 64; ++j)
-                            ptx::tma_load_3d(b_dst + j * 8192, mb, &full[stage], n0 + j * 64, kk,
+                        for (int j = 0; j < BN / BW; ++j)
+                            ptx::tma_load_3d(b_dst + j * BOX, mb, &full[stage], n0 + j * BW, kk,
                                              pr.b_tile);
                     } else {
                         ptx::tma_load_3d(b_dst, mb, &full[stage], kk, n0, pr.b_tile);
@@ -164,7 +175,7 @@ __global__ void __launch_bounds__(256, 1) gemm_f16_tc_kernel(const __grid_consta
     } else if (warp == 1) {
         // ===== MMA issuer =====
         if (lane == 0) {
-            constexpr uint32_t idesc = ptx::umma_idesc(BM, BN, A_MN, B_MN, 0);
+            constexpr uint32_t idesc = ptx::umma_idesc(BM, BN, A_MN, B_MN, FMT);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -183,12 +194,15 @@ __global__ void __launch_bounds__(256, 1) gemm_f16_tc_kernel(const __grid_consta
                     const uint32_t a_base = ptx::smem_u32(sA + stage * A_STAGE);
                     const uint32_t b_base = ptx::smem_u32(sB + stage * B_STAGE);
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k) {
-                        const uint64_t ad = A_MN ? ptx::umma_desc_sw128(a_base + k * 2048, 8192, 1024)
+                    for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K per stage
+                        const uint64_t ad = A_MN ? ptx::umma_desc_sw128(a_base + k * KSTEP_MN, BOX, 1024)
                                                  : ptx::umma_desc_sw128(a_base + k * 32, 0, 1024);
-                        const uint64_t bd = B_MN ? ptx::umma_desc_sw128(b_base + k * 2048, 8192, 1024)
+                        const uint64_t bd = B_MN ? ptx::umma_desc_sw128(b_base + k * KSTEP_MN, BOX, 1024)
                                                  : ptx::umma_desc_sw128(b_base + k * 32, 0, 1024);
-                        ptx::mma_f16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                        if (KIND == 0)
+                            ptx::mma_f16_ss(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                        else
+                            ptx::mma_tf32_ss(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
                     }
                     ptx::mma_commit(&empty[stage]);
                     if (++stage == STAGES) {
@@ -327,15 +341,17 @@ void make_map(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int es
     if (r != CUDA_SUCCESS) fail(MP_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
-void make_op_map(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
-                 uint64_t ld, uint64_t ts, uint32_t box1) {
-    make_map(map, base, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, d0, d1, d2, ld, ts, 64, box1,
-             CU_TENSOR_MAP_SWIZZLE_128B);
+// Operand map: 128-byte swizzled boxes of 128 bytes x box1 rows.
+void make_op_map(CUtensorMap* map, int kind, const void* base, uint64_t d0, uint64_t d1,
+                 uint64_t d2, uint64_t ld, uint64_t ts, uint32_t box1) {
+    const int es = kind == 0 ? 2 : 4;
+    make_map(map, base, kind == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+             es, d0, d1, d2, ld, ts, 128 / es, box1, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-template <bool A_MN, bool B_MN, typename TC>
+template <int KIND, bool A_MN, bool B_MN, typename TC>
 void launch_kernel(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total) {
-    auto kern = gemm_f16_tc_kernel<A_MN, B_MN, TC>;
+    auto kern = gemm_tc_kernel<KIND, A_MN, B_MN, TC>;
     static bool configured = false;
     if (!configured) {
         MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
@@ -353,10 +369,12 @@ void launch_kernel(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total) {
 bool tc_gemm_supported(const TcGemm& g) {
     // TMA: 16-byte aligned bases and leading strides for A, B and C.
     auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
-    if (!al(g.A) || !al(g.B) || !al(g.C) || (g.B2 && !al(g.B2))) return false;
-    if ((g.lda * 2) % 16 || (g.ldb * 2) % 16 || (g.ldc * elem_bytes(g.pc)) % 16) return false;
+    const int es = g.kind == 0 ? 2 : 4;
+    if (!al(g.A) || !al(g.B) || !al(g.C) || (g.A2 && !al(g.A2)) || (g.B2 && !al(g.B2))) return false;
+    if ((g.lda * es) % 16 || (g.ldb * es) % 16 || (g.ldc * elem_bytes(g.pc)) % 16) return false;
     if (g.m < 1 || g.n < 1 || g.k < 1) return false;
     if (g.m >= (1ll << 31) || g.n >= (1ll << 31) || g.k >= (1ll << 31)) return false;
+    if (g.kind == 1 && g.pc != MP_SINGLE) return false;
     return g.pc == MP_HALF || g.pc == MP_SINGLE;
 }
 
@@ -365,28 +383,42 @@ void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
     Params p;
     std::memset(&p, 0, sizeof(p));
     const bool a_mn = !g.ta, b_mn = g.tb;
-    // op(A): m x k.  MN-major: storage m x k (ld lda).  K-major: storage k x m.
-    if (a_mn)
-        make_op_map(&p.map_a, g.A, g.m, g.k, g.a_tiles, g.lda, g.a_tile_stride, 64);
-    else
-        make_op_map(&p.map_a, g.A, g.k, g.m, g.a_tiles, g.lda, g.a_tile_stride, BM);
-    if (b_mn)
-        make_op_map(&p.map_b, g.B, g.n, g.k, g.b_tiles, g.ldb, g.b_tile_stride, 64);
-    else
-        make_op_map(&p.map_b, g.B, g.k, g.n, g.b_tiles, g.ldb, g.b_tile_stride, BN);
-    if (g.B2) {
-        if (b_mn)
-            make_op_map(&p.map_b2, g.B2, g.n, g.k, g.b_tiles, g.ldb, g.b_tile_stride, 64);
+    const int kind = g.kind;
+    const uint32_t rows_a = a_mn ? 0 : BM, rows_b = b_mn ? 0 : BN;
+    const void* As[2] = {g.A, g.A2 ? g.A2 : g.A};
+    const void* Bs[2] = {g.B, g.B2 ? g.B2 : g.B};
+    for (int i = 0; i < 2; ++i) {
+        // op(A): m x k.  MN-major: storage m x k (ld lda).  K-major: storage k x m.
+        if (a_mn)
+            make_op_map(&p.map_a[i], kind, As[i], g.m, g.k, g.a_tiles, g.lda, g.a_tile_stride, 128 / (kind ? 4 : 2));
         else
-            make_op_map(&p.map_b2, g.B2, g.k, g.n, g.b_tiles, g.ldb, g.b_tile_stride, BN);
-    } else {
-        p.map_b2 = p.map_b;
+            make_op_map(&p.map_a[i], kind, As[i], g.k, g.m, g.a_tiles, g.lda, g.a_tile_stride, rows_a);
+        if (b_mn)
+            make_op_map(&p.map_b[i], kind, Bs[i], g.n, g.k, g.b_tiles, g.ldb, g.b_tile_stride, 128 / (kind ? 4 : 2));
+        else
+            make_op_map(&p.map_b[i], kind, Bs[i], g.k, g.n, g.b_tiles, g.ldb, g.b_tile_stride, rows_b);
     }
     // C: [c_tiles][n][m] with chunks of 128 rows x 256 bytes
     const bool half_c = g.pc == MP_HALF;
     make_map(&p.map_c, g.C, half_c ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
              half_c ? 2 : 4, g.m, g.n, g.c_tiles, g.ldc, g.c_tile_stride, BM, half_c ? 128 : 64,
              CU_TENSOR_MAP_SWIZZLE_NONE);
+    // K segments
+    int nseg = 1;
+    p.seg_a[0] = p.seg_b[0] = 0;
+    // The tensor core's FP32 accumulator truncates on every MMA, so the error
+    // grows with the accumulator's magnitude: the small lo segments go first
+    // and hi*hi last.
+    if (kind == 1 && g.A2 && g.B2) {  // 3xTF32: hi*lo + lo*hi + hi*hi
+        nseg = 3;
+        p.seg_a[0] = 0; p.seg_b[0] = 1;
+        p.seg_a[1] = 1; p.seg_b[1] = 0;
+        p.seg_a[2] = 0; p.seg_b[2] = 0;
+    } else if (g.B2) {  // A * B_lo + A * B
+        nseg = 2;
+        p.seg_a[0] = 0; p.seg_b[0] = 1;
+        p.seg_a[1] = 0; p.seg_b[1] = 0;
+    }
     p.problems = g.problems;
     p.single = TcProblem{0, 0, 0, g.lower_only ? 1 : 0};
     p.nprob = g.problems ? static_cast<int32_t>(g.count) : 1;
@@ -397,18 +429,21 @@ void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
     p.beta = static_cast<float>(g.beta);
     p.mblocks = static_cast<int32_t>((g.m + BM - 1) / BM);
     p.nblocks = static_cast<int32_t>((g.n + BN - 1) / BN);
-    p.kblocks1 = static_cast<int32_t>((g.k + BK - 1) / BK);
-    p.kblocks = g.B2 ? 2 * p.kblocks1 : p.kblocks1;
+    const int bk = kind == 0 ? 64 : 32;
+    p.kblocks1 = static_cast<int32_t>((g.k + bk - 1) / bk);
+    p.kblocks = nseg * p.kblocks1;
     const int64_t total = static_cast<int64_t>(p.nprob) * p.mblocks * p.nblocks;
-    ProfScope ps(ctx, MP_PROF_GEMM_F16, s,
+    ProfScope ps(ctx, kind == 0 ? MP_PROF_GEMM_F16 : MP_PROF_GEMM_F32, s,
                  2.0 * static_cast<double>(g.m) * g.n * g.k * p.nprob *
                      (g.lower_only ? 0.5 : 1.0));
 #define MP_TC(AM, BMJ)                                                            \
     if (a_mn == AM && b_mn == BMJ) {                                              \
-        if (half_c)                                                               \
-            launch_kernel<AM, BMJ, uint16_t>(ctx, s, p, total);                   \
+        if (kind == 1)                                                            \
+            launch_kernel<1, AM, BMJ, float>(ctx, s, p, total);                   \
+        else if (half_c)                                                          \
+            launch_kernel<0, AM, BMJ, uint16_t>(ctx, s, p, total);                \
         else                                                                      \
-            launch_kernel<AM, BMJ, float>(ctx, s, p, total);                      \
+            launch_kernel<0, AM, BMJ, float>(ctx, s, p, total);                   \
         return;                                                                   \
     }
     MP_TC(true, true)

@@ -16,10 +16,12 @@ struct TcProblem {
     int32_t lower_only;  // skip / keep C strictly above the diagonal
 };
 
-// C <- alpha op(A) op(B) + beta C with FP16 A, B and half/single C.
+// C <- alpha op(A) op(B) + beta C with FP16 A, B and half/single C, or
+// 3xTF32-split FP32 A, B and single C.
 // Dense: *_tiles = 1, problems = nullptr.  Grouped: A, B and C are slabs of
 // `*_tiles` column-major tiles `*_tile_stride` elements apart.
 struct TcGemm {
+    int kind = 0;  // 0: FP16 operands (kind::f16), 1: FP32 operands via TF32 (kind::tf32)
     mp_precision pc = MP_HALF;
     bool ta = false, tb = false;
     int64_t m = 0, n = 0, k = 0;
@@ -33,9 +35,11 @@ struct TcGemm {
     bool lower_only = false;
     const TcProblem* problems = nullptr;
     int64_t count = 0;
-    // Optional second B operand concatenated along K with A reused:
-    // C = alpha (A op(B) + A op(B2)) + beta C, both in one FP32 accumulator
-    // (the hi + lo split of an FP64 inverse, see tile.cpp TRSM).
+    // Optional lo parts, concatenated along K into one FP32 accumulator:
+    //   kind 0, B2 only : C = alpha A (B + B2) + beta C   (split FP64 inverse)
+    //   kind 1, A2 + B2 : 3xTF32, C = alpha (A B + A B2 + A2 B) + beta C
+    // (A2/B2 share the layout, tiles and strides of A/B).
+    const void* A2 = nullptr;
     const void* B2 = nullptr;
 };
 

@@ -68,10 +68,10 @@ struct Ctx {
     int64_t launches = 0;            // kernels launched by this library
     Prof prof;
     // Scratch device memory (grown on demand, freed with the context).
-    void* scratch = nullptr;
-    size_t scratch_bytes = 0;
-    void* scratch2 = nullptr;
-    size_t scratch2_bytes = 0;
+    // slot 0: op-level work buffers, 1: staging / POTRF barriers, 2: GEMM
+    // operand splits (3xTF32), 3: spare
+    void* scr[4] = {nullptr, nullptr, nullptr, nullptr};
+    size_t scr_bytes[4] = {0, 0, 0, 0};
     void* ensure_scratch(size_t bytes, int which = 0);
 };
 
@@ -97,7 +97,8 @@ struct ProfScope {
     ~ProfScope();
 };
 
-void prof_collect(Ctx* ctx);  // drain pending event pairs (syncs them)
+// Fold finished event pairs into the totals (blocking: wait for all).
+void prof_collect(Ctx* ctx, bool blocking = true);
 
 // ---- kernels (each returns after enqueueing on stream s) -----------------
 // casts: cast.cu
@@ -160,12 +161,20 @@ void launch_grouped_gemm(Ctx* ctx, cudaStream_t s, const GroupedGemm& g);
 // Cholesky / triangular kernels: potrf.cu, trsm.cu
 // In-place lower Cholesky of a column-major n x n matrix (compute in the
 // compute precision of p); writes the failing column (or -1) to dev_info.
+// FP64 only: when linv_diag is given, the inverses of the 64x64 diagonal
+// blocks of L are written onto the diagonal blocks of linv_diag (ld ldi).
 void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64_t lda,
-                        int64_t n, int64_t* dev_info, int64_t info_offset);
+                        int64_t n, int64_t* dev_info, int64_t info_offset,
+                        double* linv_diag = nullptr, int64_t ldi = 0);
 // Inverse of a lower triangular FP64 matrix, out of place.  The strictly
 // upper part of Linv is written with zeros.
 void launch_trtri_lower(Ctx* ctx, cudaStream_t s, const double* L, int64_t ldl, double* Linv,
                         int64_t ldi, int64_t n);
+struct TrtriPlan;
+TrtriPlan* trtri_plan_create(Ctx* ctx, cudaStream_t s, const double* L, int64_t ldl, double* Linv,
+                             int64_t ldi, int64_t n);
+void trtri_plan_destroy(TrtriPlan* P);
+void launch_trtri_plan(Ctx* ctx, cudaStream_t s, TrtriPlan* P, bool leaves_done);
 // General triangular solve (linalg.cpp:130-159 semantics): op(T) X = B for
 // every column of B (in place), computing in compute type of pb.
 void launch_tri_solve(Ctx* ctx, cudaStream_t s, mp_precision pt, const void* T, int64_t ldt,

@@ -86,18 +86,16 @@ __device__ __forceinline__ void block_nt(T (&acc)[4][4], const T* P, int64_t ldp
 template <typename T>
 __global__ void __launch_bounds__(PT) potrf_coop_kernel(T* A, int64_t lda, int n, T* dinv,
                                                         int64_t* info, int64_t info_off,
-                                                        GridBar* bar, int* abort_flag) {
-    // phase 1 (diagonal block) and phases 2/3 (panel blocks) never overlap
-    __shared__ union {
-        T d[PB][PB + 1];
-        struct {
-            T p[16][PB + 1];
-            T q[16][PB + 1];
-        } pq;
-    } sm;
-    auto& D = sm.d;
-    auto& Ps = sm.pq.p;
-    auto& Qs = sm.pq.q;
+                                                        GridBar* bar, int* abort_flag,
+                                                        T* linv_diag, int64_t ldi) {
+    // dynamic smem: phase 1 uses D (the diagonal block) and X (its inverse);
+    // phases 2/3 reuse the same bytes for the 16-deep operand slabs.
+    extern __shared__ __align__(16) unsigned char psm[];
+    T (*D)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(psm);
+    T (*X)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(psm + sizeof(T) * PB * (PB + 1));
+    T (*Ps)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(psm);
+    T (*Qs)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(psm + sizeof(T) * 16 * (PB + 1));
+    __shared__ T sdiag[PB];
     __shared__ int s_fail;
     const int nblk = (n + PB - 1) / PB;
     const unsigned int G = gridDim.x;
@@ -114,52 +112,73 @@ __global__ void __launch_bounds__(PT) potrf_coop_kernel(T* A, int64_t lda, int n
                 D[r][c] = (r < bb && c < bb && r >= c) ? A[(int64_t)(k0 + c) * lda + k0 + r] : T(0);
             }
             __syncthreads();
+            // Right-looking unblocked factorization; thread t owns column
+            // c = t % 64 and rows r = t / 64 + 4q (q < 16) of the block, so
+            // the rank-1 update has no index arithmetic in the loop.
+            const int oc = threadIdx.x % PB, orow = threadIdx.x / PB;
             for (int j = 0; j < bb; ++j) {
-                // pivot (every thread reads the same value)
+                // pivot: every thread reads the same value (chol_kernel's
+                // `!(d > 0)` test, linalg.cpp:121); D[j][j] itself is never
+                // rewritten inside the loop, the square root goes to sdiag.
                 const T d = D[j][j];
                 if (!(d > T(0))) {
                     if (threadIdx.x == 0) s_fail = j;
-                    __syncthreads();
                     break;
                 }
                 const T sd = sqrt(d);
+                if (threadIdx.x == 0) sdiag[j] = sd;
+                if (threadIdx.x > j && threadIdx.x < bb) D[threadIdx.x][j] = D[threadIdx.x][j] / sd;
                 __syncthreads();
-                if (threadIdx.x == 0) D[j][j] = sd;
-                for (int i = j + 1 + threadIdx.x; i < bb; i += PT) D[i][j] = D[i][j] / sd;
-                __syncthreads();
-                // rank-1 update of the trailing lower triangle
-                const int rem = bb - j - 1;
-                for (int idx = threadIdx.x; idx < rem * rem; idx += PT) {
-                    const int i = j + 1 + idx % rem, l = j + 1 + idx / rem;
-                    if (i >= l) D[i][l] -= D[i][j] * D[l][j];
+                if (oc > j) {
+                    const T lc = D[oc][j];
+#pragma unroll
+                    for (int q = 0; q < PB / 4; ++q) {
+                        const int r = orow + 4 * q;
+                        if (r >= oc && r < bb) D[r][oc] -= D[r][j] * lc;
+                    }
                 }
                 __syncthreads();
             }
+            __syncthreads();
             if (s_fail >= 0) {
                 if (threadIdx.x == 0) {
                     if (*info < 0) *info = info_off + k0 + s_fail;
                     atomicExch(abort_flag, 1);
                 }
             } else {
+                for (int j = threadIdx.x; j < bb; j += PT) D[j][j] = sdiag[j];
+                __syncthreads();
                 // write L_kk back (lower part only)
                 for (int idx = threadIdx.x; idx < bb * bb; idx += PT) {
                     const int r = idx % bb, c = idx / bb;
                     if (r >= c) A[(int64_t)(k0 + c) * lda + k0 + r] = D[r][c];
                 }
-                // inverse of the lower-triangular block: column c by forward
-                // substitution (one thread per column), into dinv[kb] (64x64).
-                T* Di = dinv + (int64_t)kb * PB * PB;
-                if (threadIdx.x < PB) {
-                    const int c = threadIdx.x;
+                // inverse X = D^-1, row by row: X[i][c] = (delta_ic -
+                // sum_{c<=k<i} D[i][k] X[k][c]) / D[i][i]; 4 threads per column
+                // split the sum and combine it with warp shuffles.
+                {
+                    const int c = threadIdx.x / 4, part = threadIdx.x % 4;
                     for (int i = 0; i < PB; ++i) {
-                        T x = T(0);
-                        if (c < bb && i < bb && i >= c) {
-                            T s = (i == c) ? T(1) : T(0);
-                            for (int k = c; k < i; ++k) s -= D[i][k] * Di[c * PB + k];
-                            x = s / D[i][i];
+                        T s = T(0);
+                        if (c < i && i < bb)
+                            for (int k = c + part; k < i; k += 4) s += D[i][k] * X[k][c];
+                        s += __shfl_xor_sync(0xffffffffu, s, 1);
+                        s += __shfl_xor_sync(0xffffffffu, s, 2);
+                        if (part == 0) {
+                            T x = T(0);
+                            if (i < bb && c <= i) x = ((i == c) ? T(1) - s : -s) / D[i][i];
+                            X[i][c] = x;
                         }
-                        Di[c * PB + i] = x;
+                        __syncthreads();
                     }
+                }
+                __syncthreads();
+                T* Di = dinv + (int64_t)kb * PB * PB;
+                for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
+                    const int r = idx % PB, c = idx / PB;
+                    Di[c * PB + r] = X[r][c];
+                    if (linv_diag && r < bb && c < bb)
+                        linv_diag[(int64_t)(k0 + c) * ldi + k0 + r] = X[r][c];
                 }
             }
         }
@@ -266,7 +285,8 @@ void dispatch_p(mp_precision p, F&& f) {
 }  // namespace
 
 void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64_t lda,
-                        int64_t n, int64_t* dev_info, int64_t info_offset) {
+                        int64_t n, int64_t* dev_info, int64_t info_offset, double* linv_diag,
+                        int64_t ldi) {
     if (p == MP_HALF) fail(MP_INVALID_PARAM, "potrf: half storage must be widened first");
     if (n == 0) return;
     const int nblk = static_cast<int>((n + PB - 1) / PB);
@@ -284,71 +304,132 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
     int ni = static_cast<int>(n);
     ProfScope ps(ctx, MP_PROF_POTRF, s, static_cast<double>(n) * n * n / 3.0);
     if (p == MP_DOUBLE) {
+        static bool cfg = false;
+        const size_t shm = 2 * sizeof(double) * PB * (PB + 1);
+        if (!cfg) {
+            MP_CUDA(cudaFuncSetAttribute((void*)potrf_coop_kernel<double>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+            cfg = true;
+        }
         double* a = static_cast<double*>(A);
         double* d = static_cast<double*>(dinv);
-        void* args[] = {&a, &lda, &ni, &d, &dev_info, &info_offset, &bar, &abort_flag};
-        MP_CUDA(cudaLaunchCooperativeKernel((void*)potrf_coop_kernel<double>, grid, PT, args, 0, s));
+        void* args[] = {&a, &lda, &ni, &d, &dev_info, &info_offset, &bar, &abort_flag, &linv_diag, &ldi};
+        MP_CUDA(cudaLaunchCooperativeKernel((void*)potrf_coop_kernel<double>, grid, PT, args, shm, s));
     } else {
+        const size_t shm = 2 * sizeof(float) * PB * (PB + 1);
         float* a = static_cast<float*>(A);
         float* d = static_cast<float*>(dinv);
-        void* args[] = {&a, &lda, &ni, &d, &dev_info, &info_offset, &bar, &abort_flag};
-        MP_CUDA(cudaLaunchCooperativeKernel((void*)potrf_coop_kernel<float>, grid, PT, args, 0, s));
+        float* ld_null = nullptr;
+        void* args[] = {&a, &lda, &ni, &d, &dev_info, &info_offset, &bar, &abort_flag, &ld_null, &ldi};
+        MP_CUDA(cudaLaunchCooperativeKernel((void*)potrf_coop_kernel<float>, grid, PT, args, shm, s));
     }
     count_launch(ctx);
 }
 
-// Inverse of a lower-triangular FP64 matrix: leaf inverses, then the
-// recursive 2x2 block formula level by level (grouped FP64 GEMMs).
-void launch_trtri_lower(Ctx* ctx, cudaStream_t s, const double* L, int64_t ldl, double* Linv,
-                        int64_t ldi, int64_t n) {
-    launch_fill(ctx, s, MP_DOUBLE, Linv, ldi, n, n, 0.0);
-    launch_leaf_inverse(ctx, s, L, ldl, n, Linv, ldi);
-    // T workspace: up to n/2 x n/2 per level problem set; sized n*n/2 total.
-    double* T = static_cast<double*>(ctx->ensure_scratch(static_cast<size_t>(n) * n * sizeof(double), 0));
-    std::vector<TileProblem> p1, p2;
-    TileProblem* dprob = reinterpret_cast<TileProblem*>(T + static_cast<size_t>(n) * n / 2 + 64);
-    for (int64_t sz = 2 * PB; sz / 2 < n; sz *= 2) {
-        const int64_t h = sz / 2;
-        p1.clear();
-        p2.clear();
-        int64_t toff = 0;
-        // uniform problems (full h x h lower-right) and one ragged tail
-        struct Rag {
-            int64_t r, rows2;
-        };
+// TRTRI plan: the recursive 2x2 block inverse inv([[A,0],[B,C]]) =
+// [[A^-1,0],[-C^-1 B A^-1, C^-1]] level by level (grouped FP64 GEMMs), with
+// every level's problem list uploaded once so a factorization issues its
+// TRTRIs without host synchronisation.
+struct TrtriPlan {
+    const double* L;
+    int64_t ldl;
+    double* Linv;
+    int64_t ldi, n;
+    double* T = nullptr;           // workspace (n^2/2 doubles)
+    TileProblem* dev = nullptr;    // device problem lists
+    struct Rag {
+        int64_t r, rows2;
+    };
+    struct Level {
+        int64_t h, cnt;
+        size_t off1, off2;
         std::vector<Rag> rag;
+    };
+    std::vector<Level> levels;
+};
+
+TrtriPlan* trtri_plan_create(Ctx* ctx, cudaStream_t s, const double* L, int64_t ldl, double* Linv,
+                             int64_t ldi, int64_t n) {
+    auto* P = new TrtriPlan{L, ldl, Linv, ldi, n};
+    std::vector<TileProblem> all;
+    MP_CUDA(cudaMalloc(&P->T, static_cast<size_t>(n) * n / 2 * sizeof(double) + 256));
+    for (int64_t sz = 2 * PB; sz / 2 < n; sz *= 2) {
+        TrtriPlan::Level lv;
+        lv.h = sz / 2;
+        const int64_t h = lv.h;
+        std::vector<TileProblem> p1, p2;
+        int64_t toff = 0;
         for (int64_t r = 0; r + h < n; r += sz) {
             const int64_t rows2 = (n - r - h) < h ? (n - r - h) : h;
             if (rows2 == h) {
                 // T = B * Ainv (h x h), Linv21 = -Cinv * T
-                p1.push_back(TileProblem{L + r * ldl + r + h, Linv + r * ldi + r, T + toff, 0, 0});
-                p2.push_back(TileProblem{Linv + (r + h) * ldi + r + h, T + toff, Linv + r * ldi + r + h, 0, 0});
+                p1.push_back(TileProblem{L + r * ldl + r + h, Linv + r * ldi + r, P->T + toff, 0, 0});
+                p2.push_back(TileProblem{Linv + (r + h) * ldi + r + h, P->T + toff, Linv + r * ldi + r + h, 0, 0});
                 toff += h * h;
             } else {
-                rag.push_back({r, rows2});
+                lv.rag.push_back({r, rows2});
             }
         }
-        if (!p1.empty()) {
-            const int64_t cnt = static_cast<int64_t>(p1.size());
-            MP_CUDA(cudaMemcpyAsync(dprob, p1.data(), cnt * sizeof(TileProblem), cudaMemcpyHostToDevice, s));
-            MP_CUDA(cudaMemcpyAsync(dprob + cnt, p2.data(), cnt * sizeof(TileProblem), cudaMemcpyHostToDevice, s));
-            GroupedGemm g1{MP_DOUBLE, MP_DOUBLE, false, h, h, h, ldl, ldi, h, 1.0, 0.0, dprob, cnt};
+        lv.cnt = static_cast<int64_t>(p1.size());
+        lv.off1 = all.size();
+        all.insert(all.end(), p1.begin(), p1.end());
+        lv.off2 = all.size();
+        all.insert(all.end(), p2.begin(), p2.end());
+        P->levels.push_back(lv);
+    }
+    if (!all.empty()) {
+        MP_CUDA(cudaMalloc(&P->dev, all.size() * sizeof(TileProblem)));
+        MP_CUDA(cudaMemcpyAsync(P->dev, all.data(), all.size() * sizeof(TileProblem),
+                                cudaMemcpyHostToDevice, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+    }
+    return P;
+}
+
+void trtri_plan_destroy(TrtriPlan* P) {
+    if (!P) return;
+    if (P->T) cudaFree(P->T);
+    if (P->dev) cudaFree(P->dev);
+    delete P;
+}
+
+// Linv's strictly-upper part must already be zero; `leaves_done` means the
+// 64x64 diagonal inverses were written by the POTRF that produced L.
+void launch_trtri_plan(Ctx* ctx, cudaStream_t s, TrtriPlan* P, bool leaves_done) {
+    const double* L = P->L;
+    double* Linv = P->Linv;
+    const int64_t ldl = P->ldl, ldi = P->ldi, n = P->n;
+    if (!leaves_done) launch_leaf_inverse(ctx, s, L, ldl, n, Linv, ldi);
+    for (const auto& lv : P->levels) {
+        const int64_t h = lv.h;
+        if (lv.cnt) {
+            GroupedGemm g1{MP_DOUBLE, MP_DOUBLE, false, h, h, h, ldl, ldi, h, 1.0, 0.0,
+                           P->dev + lv.off1, lv.cnt};
             launch_grouped_gemm(ctx, s, g1);
-            GroupedGemm g2{MP_DOUBLE, MP_DOUBLE, false, h, h, h, ldi, h, ldi, -1.0, 0.0, dprob + cnt, cnt};
+            GroupedGemm g2{MP_DOUBLE, MP_DOUBLE, false, h, h, h, ldi, h, ldi, -1.0, 0.0,
+                           P->dev + lv.off2, lv.cnt};
             launch_grouped_gemm(ctx, s, g2);
-            // host vectors must outlive the async copies
-            MP_CUDA(cudaStreamSynchronize(s));
         }
-        for (const Rag& rg : rag) {
+        for (const auto& rg : lv.rag) {
             const int64_t r = rg.r, rows2 = rg.rows2;
             GemmDesc g1{MP_DOUBLE, MP_DOUBLE, MP_DOUBLE, false, false, rows2, h, h, 1.0, 0.0,
-                        L + r * ldl + r + h, ldl, Linv + r * ldi + r, ldi, T, rows2};
+                        L + r * ldl + r + h, ldl, Linv + r * ldi + r, ldi, P->T, rows2};
             launch_gemm(ctx, s, g1);
             GemmDesc g2{MP_DOUBLE, MP_DOUBLE, MP_DOUBLE, false, false, rows2, h, rows2, -1.0, 0.0,
-                        Linv + (r + h) * ldi + r + h, ldi, T, rows2, Linv + r * ldi + r + h, ldi};
+                        Linv + (r + h) * ldi + r + h, ldi, P->T, rows2, Linv + r * ldi + r + h, ldi};
             launch_gemm(ctx, s, g2);
         }
     }
+}
+
+// One-shot inverse (zeroes Linv first).
+void launch_trtri_lower(Ctx* ctx, cudaStream_t s, const double* L, int64_t ldl, double* Linv,
+                        int64_t ldi, int64_t n) {
+    launch_fill(ctx, s, MP_DOUBLE, Linv, ldi, n, n, 0.0);
+    TrtriPlan* P = trtri_plan_create(ctx, s, L, ldl, Linv, ldi, n);
+    launch_trtri_plan(ctx, s, P, false);
+    MP_CUDA(cudaStreamSynchronize(s));
+    trtri_plan_destroy(P);
 }
 
 void launch_tri_solve(Ctx* ctx, cudaStream_t s, mp_precision pt, const void* T, int64_t ldt,

@@ -39,9 +39,11 @@ struct mp_tile_s {
     int64_t nslot[3] = {0, 0, 0};
     // scheduler workspace (grown on demand)
     void* panel[3] = {nullptr, nullptr, nullptr};
+    void* split32[2] = {nullptr, nullptr};  // 3xTF32 hi/lo of the FP32 panel
     void* work = nullptr;  // FP64 nb x nb x 2 + FP32 nb x nb + Linv{H,S}
     void* lists = nullptr;
     size_t lists_bytes = 0;
+    TrtriPlan* trtri = nullptr;  // FP64 inverse plan over work (built on first chol)
 
     int64_t tt() const { return br * bc; }
     mp_precision p(int64_t i, int64_t j) const { return prec[j * tr + i]; }
@@ -57,8 +59,11 @@ struct mp_tile_s {
             if (slab[q]) cudaFree(slab[q]);
             if (panel[q]) cudaFree(panel[q]);
         }
+        for (void* p : split32)
+            if (p) cudaFree(p);
         if (work) cudaFree(work);
         if (lists) cudaFree(lists);
+        trtri_plan_destroy(trtri);
     }
 };
 
@@ -86,6 +91,8 @@ void ensure_panels(mp_tile_s& t) {
     for (int q = 0; q < 3; ++q)
         if (!t.panel[q])
             MP_CUDA(cudaMalloc(&t.panel[q], static_cast<size_t>(t.tr) * t.tt() * elem_bytes((mp_precision)q)));
+    for (auto& p : t.split32)
+        if (!p) MP_CUDA(cudaMalloc(&p, static_cast<size_t>(t.tr) * t.tt() * 4));
     if (!t.work) {
         const size_t nn = static_cast<size_t>(t.br) * t.br;
         // FP64 work, FP64 Linv, FP32 work, FP32 LinvS, FP16 LinvH hi + lo, info
@@ -108,8 +115,8 @@ struct StepLists {
     int64_t n_wb[3] = {0, 0, 0};
     size_t cv[3][3] = {};
     int64_t n_cv[3][3] = {};
-    size_t up_tc = 0, up_h_simt = 0, up_s = 0, up_d = 0;
-    int64_t n_up_tc = 0, n_up_h_simt = 0, n_up_s = 0, n_up_d = 0;
+    size_t up_tc = 0, up_h_simt = 0, up_s = 0, up_d = 0, up_tc32 = 0, split32 = 0;
+    int64_t n_up_tc = 0, n_up_h_simt = 0, n_up_s = 0, n_up_d = 0, n_up_tc32 = 0, n_split32 = 0;
     bool need_linv[3] = {false, false, false};
 };
 
@@ -134,7 +141,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         std::vector<TileProblem> trsm_p[3];
         std::vector<CopyItem> wb[3];
         std::vector<CopyItem> cv[3][3];
-        std::vector<TcProblem> up_tc;
+        std::vector<TcProblem> up_tc, up_tc32;
+        std::vector<SplitItem> split32;
         std::vector<TileProblem> up_p[3];
         char* linv_base = static_cast<char*>(t.work);
         const size_t nn = static_cast<size_t>(nb) * nb;
@@ -154,6 +162,10 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             for (int64_t m = i; m < NT; ++m) need[t.p(m, i)] = true;      // B operand of column i
             for (int r = 0; r < 3; ++r)
                 if (need[r] && r != q) cv[q][r].push_back(CopyItem{t.panel_ptr(q, i), t.panel_ptr((mp_precision)r, i)});
+            if (tc_ok && need[MP_SINGLE])  // FP32 consumers run 3xTF32 on hi/lo splits
+                split32.push_back(SplitItem{t.panel_ptr(MP_SINGLE, i),
+                                            static_cast<char*>(t.split32[0]) + i * tt * 4,
+                                            static_cast<char*>(t.split32[1]) + i * tt * 4});
         }
         for (int64_t j = k + 1; j < NT; ++j)
             for (int64_t i = j; i < NT; ++i) {
@@ -163,7 +175,11 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                     up_tc.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
                                               static_cast<int32_t>(t.slot[j * NT + i]), lo});
                 else
-                    up_p[q].push_back(TileProblem{t.panel_ptr(q, i), t.panel_ptr(q, j), t.ptr(i, j), lo, 0});
+                    if (q == MP_SINGLE && tc_ok)
+                        up_tc32.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
+                                                    static_cast<int32_t>(t.slot[j * NT + i]), lo});
+                    else
+                        up_p[q].push_back(TileProblem{t.panel_ptr(q, i), t.panel_ptr(q, j), t.ptr(i, j), lo, 0});
             }
         append(buf, trsm_tc, L.trsm_tc);
         L.n_trsm_tc = trsm_tc.size();
@@ -183,6 +199,10 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         }
         append(buf, up_tc, L.up_tc);
         L.n_up_tc = up_tc.size();
+        append(buf, up_tc32, L.up_tc32);
+        L.n_up_tc32 = up_tc32.size();
+        append(buf, split32, L.split32);
+        L.n_split32 = split32.size();
         append(buf, up_p[MP_HALF], L.up_h_simt);
         L.n_up_h_simt = up_p[MP_HALF].size();
         append(buf, up_p[MP_SINGLE], L.up_s);
@@ -220,6 +240,11 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     int64_t* dinfo = reinterpret_cast<int64_t*>(w + nn * 28 + 64);
     const int64_t neg = -1;
     MP_CUDA(cudaMemcpyAsync(dinfo, &neg, sizeof(neg), cudaMemcpyHostToDevice, s));
+    // Linv's strictly upper part stays zero for the whole factorization; the
+    // TRTRI plan (FP64 inverse of dwork) is built once.
+    MP_CUDA(cudaMemsetAsync(linv64, 0, nn * sizeof(double), s));
+    if (!t.trtri) t.trtri = trtri_plan_create(c, s, dwork, nb, linv64, nb, nb);
+    TrtriPlan* trtri = t.trtri;
 
     for (int64_t k = 0; k < NT; ++k) {
         const StepLists& L = steps[k];
@@ -227,8 +252,12 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         const mp_precision pk = t.p(k, k);
         void* akk = t.ptr(k, k);
         if (pk == MP_DOUBLE) {
-            launch_potrf_lower(c, s, MP_DOUBLE, akk, nb, nb, dinfo, k * nb);
-            if (k + 1 < NT) launch_trtri_lower(c, s, static_cast<double*>(akk), nb, linv64, nb, nb);
+            // POTRF in place, its 64x64 block inverses straight into Linv
+            launch_potrf_lower(c, s, MP_DOUBLE, akk, nb, nb, dinfo, k * nb, linv64, nb);
+            if (k + 1 < NT) {
+                MP_CUDA(cudaMemcpyAsync(dwork, akk, nn * sizeof(double), cudaMemcpyDeviceToDevice, s));
+                launch_trtri_plan(c, s, trtri, true);
+            }
         } else {
             if (pk == MP_SINGLE) {
                 launch_potrf_lower(c, s, MP_SINGLE, akk, nb, nb, dinfo, k * nb);
@@ -237,9 +266,9 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 launch_potrf_lower(c, s, MP_SINGLE, swork, nb, nb, dinfo, k * nb);
                 launch_convert(c, s, MP_SINGLE, swork, nb, MP_HALF, akk, nb, nb, nb);
             }
-            if (k + 1 < NT) {
+            if (k + 1 < NT) {  // inverse of the stored (rounded) factor, in FP64
                 launch_convert(c, s, pk, akk, nb, MP_DOUBLE, dwork, nb, nb, nb);
-                launch_trtri_lower(c, s, dwork, nb, linv64, nb, nb);
+                launch_trtri_plan(c, s, trtri, false);
             }
         }
         if (k + 1 == NT) break;
@@ -309,7 +338,38 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                     launch_batched_convert(c, s, (mp_precision)q, (mp_precision)r,
                                            reinterpret_cast<const CopyItem*>(dl + L.cv[q][r]),
                                            L.n_cv[q][r], tt);
+        // hi/lo TF32 splits of the FP32 panel, stored transposed (K-major)
+        if (L.n_split32)
+            launch_batched_split_tf32_t(c, s, reinterpret_cast<const SplitItem*>(dl + L.split32),
+                                        L.n_split32, nb);
         // 5. trailing update
+        if (L.n_up_tc32) {  // FP32 tiles: 3xTF32 on tcgen05, C -= (L_ik^T)^T (L_jk^T)
+            TcGemm g;
+            g.kind = 1;
+            g.pc = MP_SINGLE;
+            g.ta = true;
+            g.tb = false;
+            g.m = g.n = g.k = nb;
+            g.alpha = -1.0;
+            g.beta = 1.0;
+            g.A = t.split32[0];
+            g.A2 = t.split32[1];
+            g.lda = nb;
+            g.a_tiles = NT;
+            g.a_tile_stride = tt;
+            g.B = t.split32[0];
+            g.B2 = t.split32[1];
+            g.ldb = nb;
+            g.b_tiles = NT;
+            g.b_tile_stride = tt;
+            g.C = t.slab[MP_SINGLE];
+            g.ldc = nb;
+            g.c_tiles = t.nslot[MP_SINGLE];
+            g.c_tile_stride = tt;
+            g.problems = reinterpret_cast<const TcProblem*>(dl + L.up_tc32);
+            g.count = L.n_up_tc32;
+            launch_tc_gemm(c, s, g);
+        }
         if (L.n_up_tc) {
             TcGemm g;
             g.pc = MP_HALF;

@@ -70,6 +70,27 @@ def test_gemm_fp16_tensor_core(ctx, ref, rng, ta, tb, pc):
         assert err <= gemm_tol(k, pc), (m, n, k, err)
 
 
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+def test_gemm_single_3xtf32(ctx, ref, rng, ta, tb):
+    """Single C with half/single operands runs 3xTF32 on tcgen05; it must stay
+    within the FP32 tolerance of the reference's float GEMM."""
+    import paper_2406_02701_b200 as mp
+
+    for (m, n, k) in ((256, 256, 64), (384, 512, 320), (200, 300, 136), (1024, 512, 1000)):
+        for pa, pb in ((S, S), (H, S), (S, H)):
+            A = mk(rng, (k, m) if ta else (m, k), pa) - 0.5
+            B = mk(rng, (n, k) if tb else (k, n), pb) - 0.5
+            Cm = mk(rng, (m, n), S)
+            da = mp.MPArray.from_numpy(A, mp.Precision(pa), ctx)
+            db = mp.MPArray.from_numpy(B, mp.Precision(pb), ctx)
+            dc = mp.MPArray.from_numpy(Cm, mp.Precision.Single, ctx)
+            mp.linalg.gemm(da, db, dc, ta, tb, 0.5, -1.0)
+            want = ref.gemm(pa, pb, S, A, B, Cm, ta, tb, 0.5, -1.0)
+            err = rel(dc.to_numpy(), want)
+            assert err <= gemm_tol(k, S), (m, n, k, pa, pb, err)
+
+
 def test_gemm_fp16_large_vs_fp64(ctx, rng):
     """n=2048 half GEMM against an exact FP64 product of the same halves."""
     import paper_2406_02701_b200 as mp
@@ -92,7 +113,9 @@ def test_gemm_fp16_large_vs_fp64(ctx, rng):
 
 
 def test_gemm_exact_cases(ctx, rng):
-    """test_linalg.cpp:152-183: A*I = A exactly, beta-only, PrecisionMismatch."""
+    """test_linalg.cpp:152-183: A*I = A exactly (double; half on the FP16
+    tensor cores is exact too; single runs 3xTF32 and is exact to ~2^-22),
+    beta-only, PrecisionMismatch."""
     import paper_2406_02701_b200 as mp
 
     for p in (H, S, D):
@@ -101,7 +124,10 @@ def test_gemm_exact_cases(ctx, rng):
         eye = mp.MPArray.from_numpy(np.eye(256), mp.Precision(p), ctx)
         dc = mp.MPArray.zeros_matrix(256, 256, mp.Precision(p), ctx)
         mp.linalg.gemm(da, eye, dc)
-        np.testing.assert_array_equal(dc.to_numpy(), A)
+        if p == S:
+            np.testing.assert_allclose(dc.to_numpy(), A, rtol=2.0 ** -21, atol=0)
+        else:
+            np.testing.assert_array_equal(dc.to_numpy(), A)
     a = mp.MPArray.from_numpy(mk(rng, (3, 3), D), mp.Precision.Double, ctx)
     zero = mp.MPArray.zeros_matrix(3, 3, mp.Precision.Double, ctx)
     ones = mp.MPArray.from_numpy(np.ones((3, 3)), mp.Precision.Double, ctx)
