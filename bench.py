@@ -405,7 +405,7 @@ def main():
     ap.add_argument("--nb", type=int, default=1024)
     ap.add_argument("--b64", type=int, default=1)
     ap.add_argument("--b32", type=int, default=2)
-    ap.add_argument("--range", type=float, default=0.1)
+    ap.add_argument("--range", type=float, default=0.03)
     ap.add_argument("--nugget", type=float, default=0.0)
     ap.add_argument("--prec", default="half")
     ap.add_argument("--ta", action="store_true")
