@@ -3,6 +3,7 @@
 //   A, B half and C half/single  -> tcgen05 FP16 tensor cores (gemm_tc.cu)
 //   everything else              -> SIMT in C's compute type (gemm_simt.cu)
 #include "batch.hpp"
+#include "gemm_dmma.hpp"
 #include "gemm_simt.hpp"
 #include "gemm_tc.hpp"
 #include "internal.hpp"
@@ -76,6 +77,13 @@ void launch_gemm(Ctx* ctx, cudaStream_t s, const GemmDesc& g) {
             return;
         }
     }
+    if (g.pa == MP_DOUBLE && g.pb == MP_DOUBLE && g.pc == MP_DOUBLE) {
+        DmmaArgs d{g.ta, g.tb, g.m, g.n, g.k, g.alpha, g.beta, g.A, g.lda,
+                   g.B, g.ldb, g.C, g.ldc, g.lower_only, nullptr};
+        ProfScope ps(ctx, MP_PROF_GEMM_F64, s, 2.0 * g.m * g.n * g.k * (g.lower_only ? 0.5 : 1.0));
+        launch_dmma_gemm(ctx, s, d, 1);
+        return;
+    }
     SimtArgs a{g.pa, g.pb, g.pc, g.ta, g.tb, g.m, g.n, g.k, g.alpha, g.beta, g.A, g.lda,
                g.B, g.ldb, g.C, g.ldc, g.lower_only, nullptr};
     const int cls = g.pc == MP_DOUBLE ? MP_PROF_GEMM_F64
@@ -87,6 +95,13 @@ void launch_gemm(Ctx* ctx, cudaStream_t s, const GemmDesc& g) {
 
 void launch_grouped_gemm(Ctx* ctx, cudaStream_t s, const GroupedGemm& g) {
     if (g.count == 0) return;
+    if (g.pab == MP_DOUBLE && g.pc == MP_DOUBLE) {
+        DmmaArgs d{false, g.tb, g.m, g.n, g.k, g.alpha, g.beta, nullptr, g.lda,
+                   nullptr, g.ldb, nullptr, g.ldc, false, g.problems};
+        ProfScope ps(ctx, MP_PROF_GEMM_F64, s, 2.0 * g.m * g.n * g.k * g.count);
+        launch_dmma_gemm(ctx, s, d, g.count);
+        return;
+    }
     SimtArgs a{g.pab, g.pab, g.pc, false, g.tb, g.m, g.n, g.k, g.alpha, g.beta, nullptr, g.lda,
                nullptr, g.ldb, nullptr, g.ldc, false, g.problems};
     const int cls = g.pc == MP_DOUBLE ? MP_PROF_GEMM_F64

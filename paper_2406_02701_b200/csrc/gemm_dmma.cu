@@ -1,0 +1,209 @@
+// FP64 GEMM on the FP64 tensor path (DMMA, mma.sync m16n8k8 .f64).
+//
+// tcgen05 has no f64 kind, so FP64 tiles (the diagonal band of the
+// mixed-precision Cholesky, its TRTRI, and linalg::gemm with a double C,
+// linalg.cpp:349-356) run here.  Measured on B200: DMMA and DFMA both peak
+// at 37.1 TFLOP/s (tools/micro/fp64_peak.cu); the SIMT kernel reached 15.5.
+//
+// CTA tile 128x128, K slab 16, 3-stage cp.async ring in shared memory;
+// 8 warps as 2 (m) x 4 (n), warp tile 64x32 = 4 x 4 fragments of 16x8
+// (64 FP64 accumulators per thread).  Shared layouts follow global
+// contiguity so every cp.async is 16 bytes; the padded strides make the
+// fragment reads conflict-free (2 wavefronts per 256-byte warp load).
+// blockIdx.z indexes the problem of a grouped launch; lower_only skips CTA
+// tiles strictly above the diagonal and masks the rest (SYRK).
+#include "gemm_dmma.hpp"
+#include "device.cuh"
+#include "internal.hpp"
+
+namespace mpcr {
+namespace {
+
+constexpr int BMd = 128, BNd = 128, BKd = 16, NST = 3, NTHR = 256;
+constexpr int SM_ = BMd + 8;  // stride (doubles) of MN-contiguous slabs  [k][mn]
+constexpr int SK_ = BKd + 4;  // stride (doubles) of K-contiguous slabs   [mn][k]
+constexpr int SLAB = BMd * SK_ > BKd * SM_ ? BMd * SK_ : BKd * SM_;  // doubles per operand stage
+constexpr int SMEM_D = NST * 2 * SLAB * 8;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int n = valid ? 16 : 0;  // src-size 0 zero-fills
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    const int n = valid ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void dmma_k8(double (&d)[4], const double (&a)[4], const double (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+        : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+// Load one K slab [k0, k0+16) of op(X) rows [r0, r0+128) into smem.
+//   mn_contig: X stored with the M/N index contiguous (ld between k) -> [k][mn]
+//   else     : K contiguous (ld between m/n)                           -> [mn][k]
+__device__ __forceinline__ void load_slab(double* sm, const double* X, int64_t ldx, bool mn_contig,
+                                          int64_t r0, int64_t rmax, int64_t k0, int64_t kmax,
+                                          bool vec) {
+    const int t = threadIdx.x;
+    if (mn_contig) {
+        // 16 k-rows x 128 mn = 1024 x 16B chunks (2 doubles): 4 per thread
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c = t + q * NTHR;
+            const int kk = c / 64, mm = (c % 64) * 2;
+            const int64_t gk = k0 + kk, gm = r0 + mm;
+            double* dst = sm + kk * SM_ + mm;
+            if (vec) {
+                const bool ok = gk < kmax && gm < rmax;  // rmax even when vec
+                cp_async16(dst, ok ? X + gk * ldx + gm : X, ok);
+            } else {
+                for (int e = 0; e < 2; ++e) {
+                    const bool ok = gk < kmax && gm + e < rmax;
+                    cp_async8(dst + e, ok ? X + gk * ldx + gm + e : X, ok);
+                }
+            }
+        }
+    } else {
+        // 128 mn rows x 16 k = 1024 x 16B chunks: 4 per thread
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c = t + q * NTHR;
+            const int mm = c / 8, kk = (c % 8) * 2;
+            const int64_t gm = r0 + mm, gk = k0 + kk;
+            double* dst = sm + mm * SK_ + kk;
+            if (vec) {
+                const bool ok = gm < rmax && gk < kmax;  // kmax even when vec
+                cp_async16(dst, ok ? X + gm * ldx + gk : X, ok);
+            } else {
+                for (int e = 0; e < 2; ++e) {
+                    const bool ok = gm < rmax && gk + e < kmax;
+                    cp_async8(dst + e, ok ? X + gm * ldx + gk + e : X, ok);
+                }
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ double sm_get(const double* sm, bool mn_contig, int mn, int k) {
+    return mn_contig ? sm[k * SM_ + mn] : sm[mn * SK_ + k];
+}
+
+__global__ void __launch_bounds__(NTHR, 1) dmma_gemm_kernel(DmmaArgs g) {
+    extern __shared__ __align__(16) double dsm[];
+    const TileProblem pr = g.problems ? g.problems[blockIdx.z]
+                                      : TileProblem{g.A, g.B, g.C, g.lower_only ? 1 : 0, 0};
+    const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BMd;
+    const int64_t n0 = static_cast<int64_t>(blockIdx.y) * BNd;
+    if (pr.lower_only && m0 + BMd - 1 < n0) return;
+    const double* __restrict__ A = static_cast<const double*>(pr.A);
+    const double* __restrict__ B = static_cast<const double*>(pr.B);
+    double* __restrict__ C = static_cast<double*>(pr.C);
+    const bool a_mn = !g.ta;  // op(A) = A: M contiguous
+    const bool b_mn = g.tb;   // op(B) = B^T: N contiguous
+    // 16-byte copies need even strides/offsets and even extents along the contiguous index
+    const bool va = (g.lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
+                    (a_mn ? g.m % 2 == 0 : g.k % 2 == 0);
+    const bool vb = (g.ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0) &&
+                    (b_mn ? g.n % 2 == 0 : g.k % 2 == 0);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int wm = (warp / 4) * 64, wn = (warp % 4) * 32;
+    const int gq = lane / 4, tq = lane % 4;
+    double acc[4][4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
+
+    const int nk = static_cast<int>((g.k + BKd - 1) / BKd);
+    auto stage_a = [&](int s) { return dsm + s * 2 * SLAB; };
+    auto stage_b = [&](int s) { return dsm + s * 2 * SLAB + SLAB; };
+    auto issue = [&](int kb) {
+        const int s = kb % NST;
+        load_slab(stage_a(s), A, g.lda, a_mn, m0, g.m, static_cast<int64_t>(kb) * BKd, g.k, va);
+        load_slab(stage_b(s), B, g.ldb, b_mn, n0, g.n, static_cast<int64_t>(kb) * BKd, g.k, vb);
+    };
+#pragma unroll
+    for (int s = 0; s < NST - 1; ++s) {
+        if (s < nk) issue(s);
+        cp_commit();
+    }
+    for (int kb = 0; kb < nk; ++kb) {
+        cp_wait<NST - 2>();
+        __syncthreads();
+        if (kb + NST - 1 < nk) issue(kb + NST - 1);
+        cp_commit();
+        const double* sa = stage_a(kb % NST);
+        const double* sb = stage_b(kb % NST);
+#pragma unroll
+        for (int ks = 0; ks < BKd; ks += 8) {
+            double af[4][4], bf[4][2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int mr = wm + i * 16 + gq;
+#pragma unroll
+                for (int v = 0; v < 4; ++v)  // a[v0 + 2 v1] = A[g + 8 v0][t + 4 v1]
+                    af[i][v] = sm_get(sa, a_mn, mr + 8 * (v & 1), ks + tq + 4 * (v >> 1));
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int nc = wn + j * 8 + gq;
+#pragma unroll
+                for (int v = 0; v < 2; ++v)  // b[v] = B[k = t + 4 v][n = g]
+                    bf[j][v] = sm_get(sb, b_mn, nc, ks + tq + 4 * v);
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma_k8(acc[i][j], af[i], bf[j]);
+        }
+    }
+    cp_wait<0>();
+    // epilogue: c[v0 + 2 v1] at (g + 8 v1, 2 t + v0)
+    const double alpha = g.alpha, beta = g.beta;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int64_t gm = m0 + wm + i * 16 + gq + 8 * (v >> 1);
+                const int64_t gn = n0 + wn + j * 8 + 2 * tq + (v & 1);
+                if (gm < g.m && gn < g.n && !(pr.lower_only && gm < gn)) {
+                    double* p = C + gn * g.ldc + gm;
+                    double r = alpha * acc[i][j][v];
+                    if (beta != 0.0) r += beta * *p;
+                    *p = r;
+                }
+            }
+}
+
+}  // namespace
+
+void launch_dmma_gemm(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count) {
+    if (g.m == 0 || g.n == 0) return;
+    static bool configured = false;
+    if (!configured) {
+        MP_CUDA(cudaFuncSetAttribute(dmma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_D));
+        configured = true;
+    }
+    const dim3 grid(static_cast<unsigned>((g.m + BMd - 1) / BMd),
+                    static_cast<unsigned>((g.n + BNd - 1) / BNd),
+                    static_cast<unsigned>(g.problems ? count : 1));
+    dmma_gemm_kernel<<<grid, NTHR, SMEM_D, s>>>(g);
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+}  // namespace mpcr

@@ -1,0 +1,25 @@
+// Host interface of the FP64 DMMA GEMM (gemm_dmma.cu).
+#pragma once
+
+#include "internal.hpp"
+
+namespace mpcr {
+
+// C <- alpha op(A) op(B) + beta C, all FP64, column-major (dense or grouped).
+struct DmmaArgs {
+    bool ta, tb;
+    int64_t m, n, k;
+    double alpha, beta;
+    const void* A;
+    int64_t lda;
+    const void* B;
+    int64_t ldb;
+    void* C;
+    int64_t ldc;
+    bool lower_only;
+    const TileProblem* problems;  // grouped launch when non-null
+};
+
+void launch_dmma_gemm(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count);
+
+}  // namespace mpcr

@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 
 #include <type_traits>
+#include <cstdlib>
 #include <vector>
 
 #include "batch.hpp"
@@ -33,6 +34,21 @@ struct GridBar {
     unsigned int count;
     unsigned int gen;
 };
+
+// Optional per-step clock trace of CTA 0 (MPCR_POTRF_TRACE=1, diagnostics).
+__device__ int g_trace_on = 0;
+__device__ long long g_trace[64 * 6];
+__device__ long long g_trace2[64 * 6];
+#define PTRACE2(kb, slot)                                                            \
+    do {                                                                             \
+        if (g_trace_on && blockIdx.x == 0 && threadIdx.x == 0 && (kb) < 64)          \
+            g_trace2[(kb) * 6 + (slot)] = clock64();                                 \
+    } while (0)
+#define PTRACE(kb, slot)                                                             \
+    do {                                                                             \
+        if (g_trace_on && blockIdx.x == 0 && threadIdx.x == 0 && (kb) < 64)          \
+            g_trace[(kb) * 6 + (slot)] = clock64();                                  \
+    } while (0)
 
 __device__ __forceinline__ void grid_sync(GridBar* bar, unsigned int nblocks) {
     __syncthreads();
@@ -83,113 +99,242 @@ __device__ __forceinline__ void block_nt(T (&acc)[4][4], const T* P, int64_t ldp
     }
 }
 
+// ---- diagonal-block kernels (one CTA, 256 threads, D in shared memory) ----
+
+// Factor the bb x bb lower block D in place (64 = 4 x 16 column panels):
+// each 16x16 diagonal piece by one warp in registers with shuffles, the 16
+// columns below it by row-parallel substitution, then a rank-16 update of
+// the trailing lower triangle.  Pivot test as chol_kernel (`!(d > 0)`,
+// linalg.cpp:121).  Returns the failing local column or -1 (block-uniform).
+template <typename T>
+__device__ int factor_block(T (*D)[PB + 1], int bb, int* s_fail, T* s_inv) {
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    if (tid == 0) *s_fail = -1;
+    __syncthreads();
+    for (int c0 = 0; c0 < bb; c0 += 16) {
+        const int w = min(16, bb - c0);
+        // (i) 16 x 16 diagonal piece: lane l holds row c0 + l in registers
+        if (warp == 0) {
+            T r[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) r[j] = (lane < w && j <= lane) ? D[c0 + lane][c0 + j] : T(0);
+            int fail = -1;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                if (j < w && fail < 0) {
+                    const T djj = __shfl_sync(0xffffffffu, r[j], j);
+                    if (!(djj > T(0))) {
+                        fail = j;
+                    } else {
+                        // one reciprocal per pivot instead of a divide per element
+                        const T inv = rsqrt(djj);  // MUFU seed + Newton, ~1 ulp
+                        const T sd = djj * inv;
+                        if (lane > j) r[j] = r[j] * inv;
+                        if (lane == j) {
+                            r[j] = sd;
+                            s_inv[c0 + j] = inv;
+                        }
+#pragma unroll
+                        for (int l = j + 1; l < 16; ++l) {
+                            const T v = __shfl_sync(0xffffffffu, r[j], l);  // L[l][j]
+                            if (lane >= l) r[l] -= r[j] * v;
+                        }
+                    }
+                }
+            }
+            if (lane < w) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (j <= lane) D[c0 + lane][c0 + j] = r[j];
+            }
+            if (lane == 0 && fail >= 0) *s_fail = c0 + fail;
+        }
+        __syncthreads();
+        if (*s_fail >= 0) return *s_fail;
+        // (ii) rows below: x * L_ss^T = D[i][c0..c0+w) by forward substitution
+        // (4 threads per row, each an interleaved quarter of every dot product)
+        {
+            const int part = tid % 4;
+            for (int i = c0 + w + tid / 4; i < bb; i += PT / 4) {
+                T x[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    if (j < w) {
+                        T s = T(0);
+#pragma unroll
+                        for (int t = 0; t < j; ++t)
+                            if ((t & 3) == part) s += x[t] * D[c0 + j][c0 + t];
+                        s += __shfl_xor_sync(0xffffffffu, s, 1);
+                        s += __shfl_xor_sync(0xffffffffu, s, 2);
+                        x[j] = (D[i][c0 + j] - s) * s_inv[c0 + j];
+                    } else {
+                        x[j] = T(0);
+                    }
+                }
+                if (part == 0)
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (j < w) D[i][c0 + j] = x[j];
+            }
+        }
+        __syncthreads();
+        // (iii) rank-w update of the trailing lower triangle; thread owns
+        // column oc and rows orow + 4q
+        const int oc = tid % PB, orow = tid / PB;
+        if (oc >= c0 + w && oc < bb) {
+            T lc[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) lc[t] = t < w ? D[oc][c0 + t] : T(0);
+#pragma unroll 4
+            for (int q = 0; q < PB / 4; ++q) {
+                const int r = orow + 4 * q;
+                if (r >= oc && r < bb) {
+                    T s = D[r][oc];
+#pragma unroll
+                    for (int t = 0; t < 16; ++t) s -= D[r][c0 + t] * lc[t];
+                    D[r][oc] = s;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    return -1;
+}
+
+// X = D^-1 for the bb x bb lower block (zeros above the diagonal):
+// 16x16 diagonal inverses per warp, then off-diagonal 16-blocks by distance,
+// X_ij = -X_ii * sum_{j<=t<i} D_it X_tj.  Uses Tm (16 x 16 x 3 scratch).
+template <typename T>
+__device__ void invert_block(const T (*D)[PB + 1], T (*X)[PB + 1], T* Tm, int bb, const T* s_inv) {
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    for (int idx = tid; idx < PB * PB; idx += PT) X[idx % PB][idx / PB] = T(0);
+    __syncthreads();
+    const int nsb = (bb + 15) / 16;
+    if (warp < nsb && lane < 16) {
+        const int b0 = warp * 16, w = min(16, bb - b0);
+        const int c = lane;  // column of the 16 x 16 inverse
+        T x[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            T v = T(0);
+            if (i < w && c < w && i >= c) {
+                T s = (i == c) ? T(1) : T(0);
+#pragma unroll
+                for (int t = 0; t < i; ++t)
+                    if (t >= c) s -= D[b0 + i][b0 + t] * x[t];
+                v = s * s_inv[b0 + i];
+            }
+            x[i] = v;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            if (i < w && c < w) X[b0 + i][b0 + c] = x[i];
+    }
+    __syncthreads();
+    for (int d = 1; d < nsb; ++d) {
+        const int nblk = nsb - d;  // blocks (i, i - d)
+        // T_b = sum_{t=j}^{i-1} D_it X_tj   (16 x 16 each)
+        for (int e = tid; e < nblk * 256; e += PT) {
+            const int b = e / 256, r = (e % 256) % 16, cc = (e % 256) / 16;
+            const int bi = b + d, bj = b;
+            const int row = bi * 16 + r, col = bj * 16 + cc;
+            T s = T(0);
+            if (row < bb && col < bb)
+                for (int t = bj * 16; t < bi * 16; ++t) s += D[row][t] * X[t][col];
+            Tm[e] = s;
+        }
+        __syncthreads();
+        for (int e = tid; e < nblk * 256; e += PT) {
+            const int b = e / 256, r = (e % 256) % 16, cc = (e % 256) / 16;
+            const int bi = b + d, bj = b;
+            const int row = bi * 16 + r, col = bj * 16 + cc;
+            if (row < bb && col < bb) {
+                T s = T(0);
+                for (int t = 0; t < 16; ++t) s += X[row][bi * 16 + t] * Tm[b * 256 + cc * 16 + t];
+                X[row][col] = -s;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Factor diagonal block kb (already fully updated) held in global A: load,
+// factor, invert; write L_kk back, Dinv to `dinv` (and to linv_diag).
+template <typename T>
+__device__ void diag_step(T* A, int64_t lda, int n, int kb, T* dinv, T* linv_diag, int64_t ldi,
+                          int64_t* info, int64_t info_off, int* abort_flag, T (*D)[PB + 1],
+                          T (*X)[PB + 1], T* Tm, int* s_fail) {
+    const int k0 = kb * PB, bb = min(PB, n - k0);
+    PTRACE2(kb, 0);
+    for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
+        const int r = idx % PB, c = idx / PB;
+        D[r][c] = (r < bb && c < bb && r >= c) ? A[(int64_t)(k0 + c) * lda + k0 + r] : T(0);
+    }
+    __syncthreads();
+    PTRACE2(kb, 1);
+    __shared__ T s_inv[PB];  // reciprocals of the pivots
+    const int fail = factor_block(D, bb, s_fail, s_inv);
+    PTRACE2(kb, 2);
+    if (fail >= 0) {
+        if (threadIdx.x == 0) {
+            if (*info < 0) *info = info_off + k0 + fail;
+            atomicExch(abort_flag, 1);
+        }
+        return;
+    }
+    for (int idx = threadIdx.x; idx < bb * bb; idx += PT) {
+        const int r = idx % bb, c = idx / bb;
+        if (r >= c) A[(int64_t)(k0 + c) * lda + k0 + r] = D[r][c];
+    }
+    PTRACE2(kb, 3);
+    invert_block<T>(D, X, Tm, bb, s_inv);
+    PTRACE2(kb, 4);
+    T* Di = dinv + (int64_t)kb * PB * PB;
+    for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
+        const int r = idx % PB, c = idx / PB;
+        Di[c * PB + r] = X[r][c];
+        if (linv_diag && r < bb && c < bb) linv_diag[(int64_t)(k0 + c) * ldi + k0 + r] = X[r][c];
+    }
+}
+
+// Cooperative blocked right-looking POTRF.  Per 64-block step kb:
+//   phase 2  all CTAs: panel X_ib = A_ib,kb * Dinv_kb^T
+//   barrier
+//   phase 3  CTA 0 updates block (kb+1, kb+1) and factors + inverts it
+//            (the next step's diagonal work), the other CTAs update the
+//            rest of the trailing lower triangle
+//   barrier
+// so the diagonal factorization overlaps the trailing update.
 template <typename T>
 __global__ void __launch_bounds__(PT) potrf_coop_kernel(T* A, int64_t lda, int n, T* dinv,
                                                         int64_t* info, int64_t info_off,
                                                         GridBar* bar, int* abort_flag,
                                                         T* linv_diag, int64_t ldi) {
-    // dynamic smem: phase 1 uses D (the diagonal block) and X (its inverse);
-    // phases 2/3 reuse the same bytes for the 16-deep operand slabs.
     extern __shared__ __align__(16) unsigned char psm[];
     T (*D)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(psm);
     T (*X)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(psm + sizeof(T) * PB * (PB + 1));
-    T (*Ps)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(psm);
-    T (*Qs)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(psm + sizeof(T) * 16 * (PB + 1));
-    __shared__ T sdiag[PB];
+    T (*Ps)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(psm + 2 * sizeof(T) * PB * (PB + 1));
+    T (*Qs)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(psm + 2 * sizeof(T) * PB * (PB + 1) +
+                                                      sizeof(T) * 16 * (PB + 1));
+    T* Tm = reinterpret_cast<T*>(psm + 2 * sizeof(T) * PB * (PB + 1) + 2 * sizeof(T) * 16 * (PB + 1));
     __shared__ int s_fail;
     const int nblk = (n + PB - 1) / PB;
     const unsigned int G = gridDim.x;
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
 
+    if (blockIdx.x == 0)
+        diag_step(A, lda, n, 0, dinv, linv_diag, ldi, info, info_off, abort_flag, D, X, Tm, &s_fail);
+    grid_sync(bar, G);
+    if (*(volatile int*)abort_flag) return;
     for (int kb = 0; kb < nblk; ++kb) {
         const int k0 = kb * PB;
         const int bb = min(PB, n - k0);
-        // ---- phase 1: diagonal block -----------------------------------
-        if (blockIdx.x == 0) {
-            if (threadIdx.x == 0) s_fail = -1;
-            for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
-                const int r = idx % PB, c = idx / PB;
-                D[r][c] = (r < bb && c < bb && r >= c) ? A[(int64_t)(k0 + c) * lda + k0 + r] : T(0);
-            }
-            __syncthreads();
-            // Right-looking unblocked factorization; thread t owns column
-            // c = t % 64 and rows r = t / 64 + 4q (q < 16) of the block, so
-            // the rank-1 update has no index arithmetic in the loop.
-            const int oc = threadIdx.x % PB, orow = threadIdx.x / PB;
-            for (int j = 0; j < bb; ++j) {
-                // pivot: every thread reads the same value (chol_kernel's
-                // `!(d > 0)` test, linalg.cpp:121); D[j][j] itself is never
-                // rewritten inside the loop, the square root goes to sdiag.
-                const T d = D[j][j];
-                if (!(d > T(0))) {
-                    if (threadIdx.x == 0) s_fail = j;
-                    break;
-                }
-                const T sd = sqrt(d);
-                if (threadIdx.x == 0) sdiag[j] = sd;
-                if (threadIdx.x > j && threadIdx.x < bb) D[threadIdx.x][j] = D[threadIdx.x][j] / sd;
-                __syncthreads();
-                if (oc > j) {
-                    const T lc = D[oc][j];
-#pragma unroll
-                    for (int q = 0; q < PB / 4; ++q) {
-                        const int r = orow + 4 * q;
-                        if (r >= oc && r < bb) D[r][oc] -= D[r][j] * lc;
-                    }
-                }
-                __syncthreads();
-            }
-            __syncthreads();
-            if (s_fail >= 0) {
-                if (threadIdx.x == 0) {
-                    if (*info < 0) *info = info_off + k0 + s_fail;
-                    atomicExch(abort_flag, 1);
-                }
-            } else {
-                for (int j = threadIdx.x; j < bb; j += PT) D[j][j] = sdiag[j];
-                __syncthreads();
-                // write L_kk back (lower part only)
-                for (int idx = threadIdx.x; idx < bb * bb; idx += PT) {
-                    const int r = idx % bb, c = idx / bb;
-                    if (r >= c) A[(int64_t)(k0 + c) * lda + k0 + r] = D[r][c];
-                }
-                // inverse X = D^-1, row by row: X[i][c] = (delta_ic -
-                // sum_{c<=k<i} D[i][k] X[k][c]) / D[i][i]; 4 threads per column
-                // split the sum and combine it with warp shuffles.
-                {
-                    const int c = threadIdx.x / 4, part = threadIdx.x % 4;
-                    for (int i = 0; i < PB; ++i) {
-                        T s = T(0);
-                        if (c < i && i < bb)
-                            for (int k = c + part; k < i; k += 4) s += D[i][k] * X[k][c];
-                        s += __shfl_xor_sync(0xffffffffu, s, 1);
-                        s += __shfl_xor_sync(0xffffffffu, s, 2);
-                        if (part == 0) {
-                            T x = T(0);
-                            if (i < bb && c <= i) x = ((i == c) ? T(1) - s : -s) / D[i][i];
-                            X[i][c] = x;
-                        }
-                        __syncthreads();
-                    }
-                }
-                __syncthreads();
-                T* Di = dinv + (int64_t)kb * PB * PB;
-                for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
-                    const int r = idx % PB, c = idx / PB;
-                    Di[c * PB + r] = X[r][c];
-                    if (linv_diag && r < bb && c < bb)
-                        linv_diag[(int64_t)(k0 + c) * ldi + k0 + r] = X[r][c];
-                }
-            }
-        }
-        grid_sync(bar, G);
-        if (*(volatile int*)abort_flag) return;
         // ---- phase 2: panel X = A_panel * Dinv^T ------------------------
         const T* Di = dinv + (int64_t)kb * PB * PB;
+        PTRACE(kb, 0);
         for (int ib = kb + 1 + blockIdx.x; ib < nblk; ib += G) {
             const int r0 = ib * PB, rb = min(PB, n - r0);
             T acc[4][4] = {};
-            // acc = P (rb x bb) * Di^T where Di is bb x bb (ld PB)
             block_nt(acc, A + (int64_t)k0 * lda + r0, lda, rb, Di, PB, bb, bb, Ps, Qs);
 #pragma unroll
             for (int i = 0; i < 4; ++i)
@@ -200,12 +345,14 @@ __global__ void __launch_bounds__(PT) potrf_coop_kernel(T* A, int64_t lda, int n
                 }
             __syncthreads();
         }
+        if (kb + 1 == nblk) break;
+        PTRACE(kb, 1);
         grid_sync(bar, G);
-        // ---- phase 3: trailing update, lower triangle ---------------------
+        PTRACE(kb, 2);
+        // ---- phase 3: trailing update; CTA 0 does the next diagonal ----
         const int rest = nblk - kb - 1;
         const int items = rest * (rest + 1) / 2;
-        for (int it = blockIdx.x; it < items; it += G) {
-            // map it -> (ib >= jb) over the trailing blocks
+        auto update_item = [&](int it) {
             int jj = 0, rem = it;
             while (rem >= rest - jj) {
                 rem -= rest - jj;
@@ -215,8 +362,8 @@ __global__ void __launch_bounds__(PT) potrf_coop_kernel(T* A, int64_t lda, int n
             const int r0 = ib * PB, c0 = jb * PB;
             const int rb = min(PB, n - r0), cb = min(PB, n - c0);
             T acc[4][4] = {};
-            block_nt(acc, A + (int64_t)k0 * lda + r0, lda, rb, A + (int64_t)k0 * lda + c0, lda,
-                     cb, bb, Ps, Qs);
+            block_nt(acc, A + (int64_t)k0 * lda + r0, lda, rb, A + (int64_t)k0 * lda + c0, lda, cb,
+                     bb, Ps, Qs);
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -228,8 +375,23 @@ __global__ void __launch_bounds__(PT) potrf_coop_kernel(T* A, int64_t lda, int n
                     }
                 }
             __syncthreads();
+        };
+        if (blockIdx.x == 0) {
+            update_item(0);  // item 0 is (kb+1, kb+1)
+            PTRACE(kb, 3);
+            __threadfence_block();
+            diag_step(A, lda, n, kb + 1, dinv, linv_diag, ldi, info, info_off, abort_flag, D, X, Tm,
+                      &s_fail);
+            PTRACE(kb, 4);
+        } else {
+            for (int it = blockIdx.x; it < items; it += G - 1 > 0 ? G - 1 : 1) {
+                if (it == 0) continue;
+                update_item(it);
+            }
         }
         grid_sync(bar, G);
+        PTRACE(kb, 5);
+        if (*(volatile int*)abort_flag) return;
     }
 }
 
@@ -298,14 +460,22 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
     GridBar* bar = reinterpret_cast<GridBar*>(scr);
     int* abort_flag = reinterpret_cast<int*>(scr + 64);
     void* dinv = scr + 256;
+    // Few CTAs: the step is latency-bound (diagonal work on CTA 0 overlaps
+    // the trailing update of the others); fewer CTAs make the grid barrier
+    // cheaper.  MPCR_POTRF_CTAS overrides for tuning.
+    static const int cap = [] {
+        const char* e = getenv("MPCR_POTRF_CTAS");
+        return e ? atoi(e) : 32;
+    }();
     int grid = nblk * (nblk + 1) / 2;
+    if (grid > cap) grid = cap;
     if (grid > ctx->sm_count) grid = ctx->sm_count;
     if (grid < 1) grid = 1;
     int ni = static_cast<int>(n);
     ProfScope ps(ctx, MP_PROF_POTRF, s, static_cast<double>(n) * n * n / 3.0);
     if (p == MP_DOUBLE) {
         static bool cfg = false;
-        const size_t shm = 2 * sizeof(double) * PB * (PB + 1);
+        const size_t shm = (2 * PB * (PB + 1) + 2 * 16 * (PB + 1) + 3 * 256) * sizeof(double);
         if (!cfg) {
             MP_CUDA(cudaFuncSetAttribute((void*)potrf_coop_kernel<double>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
@@ -314,9 +484,31 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
         double* a = static_cast<double*>(A);
         double* d = static_cast<double*>(dinv);
         void* args[] = {&a, &lda, &ni, &d, &dev_info, &info_offset, &bar, &abort_flag, &linv_diag, &ldi};
+        static const bool trace = getenv("MPCR_POTRF_TRACE") != nullptr;
+        if (trace) {
+            const int on = 1;
+            MP_CUDA(cudaMemcpyToSymbolAsync(g_trace_on, &on, sizeof(on), 0, cudaMemcpyHostToDevice, s));
+        }
         MP_CUDA(cudaLaunchCooperativeKernel((void*)potrf_coop_kernel<double>, grid, PT, args, shm, s));
+        if (trace) {
+            long long tr[64 * 6];
+            MP_CUDA(cudaMemcpyFromSymbolAsync(tr, g_trace, sizeof(tr), 0, cudaMemcpyDeviceToHost, s));
+            MP_CUDA(cudaStreamSynchronize(s));
+            double acc[5] = {};
+            for (int kb = 0; kb + 1 < nblk && kb < 64; ++kb)
+                for (int q = 0; q < 5; ++q) acc[q] += static_cast<double>(tr[kb * 6 + q + 1] - tr[kb * 6 + q]);
+            long long t2[64 * 6];
+            MP_CUDA(cudaMemcpyFromSymbolAsync(t2, g_trace2, sizeof(t2), 0, cudaMemcpyDeviceToHost, s));
+            MP_CUDA(cudaStreamSynchronize(s));
+            double a2[4] = {};
+            for (int kb = 1; kb < nblk && kb < 64; ++kb)
+                for (int q = 0; q < 4; ++q) a2[q] += static_cast<double>(t2[kb * 6 + q + 1] - t2[kb * 6 + q]);
+            fprintf(stderr, "  diag: load %.0f factor %.0f writeL %.0f invert %.0f\n", a2[0], a2[1], a2[2], a2[3]);
+            fprintf(stderr, "potrf trace (cycles, summed over %d steps): panel %.0f bar1 %.0f update %.0f diag %.0f bar2 %.0f\n",
+                    nblk - 1, acc[0], acc[1], acc[2], acc[3], acc[4]);
+        }
     } else {
-        const size_t shm = 2 * sizeof(float) * PB * (PB + 1);
+        const size_t shm = (2 * PB * (PB + 1) + 2 * 16 * (PB + 1) + 3 * 256) * sizeof(float);
         float* a = static_cast<float*>(A);
         float* d = static_cast<float*>(dinv);
         float* ld_null = nullptr;
