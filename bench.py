@@ -394,13 +394,53 @@ def run_gemm(args, world, rank, local):
                       "clocks": clk.summary()}))
 
 
+def run_cast(args, world, rank, local):
+    """Config 2 cast line: MPArray::converted bandwidth (n x n, pin -> pout)."""
+    import torch
+
+    import paper_2406_02701_b200 as mp
+
+    ctx = mp.Context(local)
+    n = args.n
+    pin, pout = (mp.parse_precision(p) for p in args.cast.split(":"))
+    a = mp.MPArray.zeros_matrix(n, n, pin, ctx)
+    b = mp.MPArray.zeros_matrix(n, n, pout, ctx)
+    lib, C = mp.lib(), __import__("ctypes")
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
+    for _ in range(args.warmup):
+        lib.mp_convert(ctx.h, a.h, b.h)
+    ctx.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            lib.mp_convert(ctx.h, a.h, b.h)
+        e1.record(stream)
+        ctx.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    es = {0: 2, 1: 4, 2: 8}
+    byts = n * n * (es[int(pin)] + es[int(pout)])
+    gbs = byts / (ms * 1e-3) / 1e9
+    pk, src = peaks()
+    print(json.dumps({"metric": f"cast {args.cast} GB/s", "value": gbs, "unit": "GB/s",
+                      "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                      "higher_is_better": True,
+                      "config": {"workload": f"MPArray::converted {n}x{n} {args.cast}",
+                                 "bytes_per_step": byts},
+                      "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"],
+                                   "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
+                                   "peak_source": src},
+                      "clocks": clk.summary()}))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="chol", choices=["chol", "gemm"])
+    ap.add_argument("--workload", default="chol", choices=["chol", "gemm", "cast"])
+    ap.add_argument("--cast", default="double:half")
     ap.add_argument("--n", type=int, default=65536)
     ap.add_argument("--nb", type=int, default=1024)
     ap.add_argument("--b64", type=int, default=1)
@@ -421,6 +461,8 @@ def main():
         run_reference_arm(args, world, rank)
     elif args.workload == "gemm":
         run_gemm(args, world, rank, local)
+    elif args.workload == "cast":
+        run_cast(args, world, rank, local)
     else:
         run_chol(args, world, rank, local)
     if world > 1:

@@ -6,8 +6,8 @@
 // at 37.1 TFLOP/s (tools/micro/fp64_peak.cu); the SIMT kernel reached 15.5.
 //
 // CTA tile 128x128, K slab 16, 3-stage cp.async ring in shared memory;
-// 8 warps as 2 (m) x 4 (n), warp tile 64x32 = 4 x 4 fragments of 16x8
-// (64 FP64 accumulators per thread).  Shared layouts follow global
+// 16 warps as 4 (m) x 4 (n), warp tile 32x32 = 2 x 4 fragments of 16x8
+// (32 FP64 accumulators per thread, 4 warps per scheduler).  Shared layouts follow global
 // contiguity so every cp.async is 16 bytes; the padded strides make the
 // fragment reads conflict-free (2 wavefronts per 256-byte warp load).
 // blockIdx.z indexes the problem of a grouped launch; lower_only skips CTA
@@ -19,7 +19,7 @@
 namespace mpcr {
 namespace {
 
-constexpr int BMd = 128, BNd = 128, BKd = 16, NST = 3, NTHR = 256;
+constexpr int BMd = 128, BNd = 128, BKd = 16, NST = 3, NTHR = 512;
 constexpr int SM_ = BMd + 8;  // stride (doubles) of MN-contiguous slabs  [k][mn]
 constexpr int SK_ = BKd + 4;  // stride (doubles) of K-contiguous slabs   [mn][k]
 constexpr int SLAB = BMd * SK_ > BKd * SM_ ? BMd * SK_ : BKd * SM_;  // doubles per operand stage
@@ -55,9 +55,9 @@ __device__ __forceinline__ void load_slab(double* sm, const double* X, int64_t l
                                           bool vec) {
     const int t = threadIdx.x;
     if (mn_contig) {
-        // 16 k-rows x 128 mn = 1024 x 16B chunks (2 doubles): 4 per thread
+        // 16 k-rows x 128 mn = 1024 x 16B chunks (2 doubles)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 1024 / NTHR; ++q) {
             const int c = t + q * NTHR;
             const int kk = c / 64, mm = (c % 64) * 2;
             const int64_t gk = k0 + kk, gm = r0 + mm;
@@ -73,9 +73,9 @@ __device__ __forceinline__ void load_slab(double* sm, const double* X, int64_t l
             }
         }
     } else {
-        // 128 mn rows x 16 k = 1024 x 16B chunks: 4 per thread
+        // 128 mn rows x 16 k = 1024 x 16B chunks
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 1024 / NTHR; ++q) {
             const int c = t + q * NTHR;
             const int mm = c / 8, kk = (c % 8) * 2;
             const int64_t gm = r0 + mm, gk = k0 + kk;
@@ -116,11 +116,11 @@ __global__ void __launch_bounds__(NTHR, 1) dmma_gemm_kernel(DmmaArgs g) {
                     (b_mn ? g.n % 2 == 0 : g.k % 2 == 0);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int wm = (warp / 4) * 64, wn = (warp % 4) * 32;
+    const int wm = (warp / 4) * 32, wn = (warp % 4) * 32;
     const int gq = lane / 4, tq = lane % 4;
-    double acc[4][4][4];
+    double acc[2][4][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -148,9 +148,9 @@ __global__ void __launch_bounds__(NTHR, 1) dmma_gemm_kernel(DmmaArgs g) {
         const double* sb = stage_b(kb % NST);
 #pragma unroll
         for (int ks = 0; ks < BKd; ks += 8) {
-            double af[4][4], bf[4][2];
+            double af[2][4], bf[4][2];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < 2; ++i) {
                 const int mr = wm + i * 16 + gq;
 #pragma unroll
                 for (int v = 0; v < 4; ++v)  // a[v0 + 2 v1] = A[g + 8 v0][t + 4 v1]
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(NTHR, 1) dmma_gemm_kernel(DmmaArgs g) {
                     bf[j][v] = sm_get(sb, b_mn, nc, ks + tq + 4 * v);
             }
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 2; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) dmma_k8(acc[i][j], af[i], bf[j]);
         }
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(NTHR, 1) dmma_gemm_kernel(DmmaArgs g) {
     // epilogue: c[v0 + 2 v1] at (g + 8 v1, 2 t + v0)
     const double alpha = g.alpha, beta = g.beta;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll

@@ -154,8 +154,11 @@ __device__ int factor_block(T (*D)[PB + 1], int bb, int* s_fail, T* s_inv) {
         // (ii) rows below: x * L_ss^T = D[i][c0..c0+w) by forward substitution
         // (4 threads per row, each an interleaved quarter of every dot product)
         {
+            // warp-uniform trip count: every lane takes part in the shuffles
             const int part = tid % 4;
-            for (int i = c0 + w + tid / 4; i < bb; i += PT / 4) {
+            for (int base = c0 + w + (tid / 32) * 8; base < bb; base += PT / 4) {
+                const int i = base + (tid % 32) / 4;
+                const bool ok = i < bb;
                 T x[16];
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
@@ -166,12 +169,12 @@ __device__ int factor_block(T (*D)[PB + 1], int bb, int* s_fail, T* s_inv) {
                             if ((t & 3) == part) s += x[t] * D[c0 + j][c0 + t];
                         s += __shfl_xor_sync(0xffffffffu, s, 1);
                         s += __shfl_xor_sync(0xffffffffu, s, 2);
-                        x[j] = (D[i][c0 + j] - s) * s_inv[c0 + j];
+                        x[j] = ok ? (D[i][c0 + j] - s) * s_inv[c0 + j] : T(0);
                     } else {
                         x[j] = T(0);
                     }
                 }
-                if (part == 0)
+                if (ok && part == 0)
 #pragma unroll
                     for (int j = 0; j < 16; ++j)
                         if (j < w) D[i][c0 + j] = x[j];
