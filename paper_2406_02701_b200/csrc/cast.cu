@@ -3,6 +3,8 @@
 // at_linear per element (see device.cuh); 8 elements per thread per
 // iteration with 16-byte loads and stores, grid-stride over a grid sized to
 // the SM count.
+#include <type_traits>
+
 #include "device.cuh"
 #include "internal.hpp"
 
@@ -51,18 +53,73 @@ template <> __device__ __forceinline__ uint16_t cvt1<double, uint16_t>(double x)
 template <> __device__ __forceinline__ float cvt1<double, float>(double x) { return d2f(x); }
 template <> __device__ __forceinline__ double cvt1<double, double>(double x) { return x; }
 
+// Same-width and narrowing casts: 8 elements per thread per iteration
+// (U groups loaded before any is converted and stored; U = 1 measured best).
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(256) convert_vec_kernel(const TI* __restrict__ in,
                                                           TO* __restrict__ out, int64_t n8) {
+    constexpr int U = 1;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n8;
-         t += stride) {
+    int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (; t + (U - 1) * stride < n8; t += U * stride) {
+        TI a[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) load8(in, (t + u * stride) * 8, a[u]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            TO b[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) b[k] = cvt1<TI, TO>(a[u][k]);
+            store8(out, (t + u * stride) * 8, b);
+        }
+    }
+    for (; t < n8; t += stride) {
         TI a[8];
         TO b[8];
         load8(in, t * 8, a);
 #pragma unroll
         for (int k = 0; k < 8; ++k) b[k] = cvt1<TI, TO>(a[k]);
         store8(out, t * 8, b);
+    }
+}
+
+// Widening casts (output wider than input) are write-bound: each thread
+// stores one coalesced 16-byte output chunk per group (E = 16 / sizeof(TO)
+// elements) from one narrow vector load, 4 groups in flight per thread.
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256) convert_widen_kernel(const TI* __restrict__ in,
+                                                            TO* __restrict__ out, int64_t nq) {
+    constexpr int E = 16 / sizeof(TO);
+    constexpr int U = 4;
+    using VIn = typename std::conditional<E * sizeof(TI) == 4, uint32_t, uint2>::type;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (; t + (U - 1) * stride < nq; t += U * stride) {
+        VIn v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcs(reinterpret_cast<const VIn*>(in) + t + u * stride);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            TI a[E];
+            memcpy(a, &v[u], sizeof(a));
+            TO b[E];
+#pragma unroll
+            for (int k = 0; k < E; ++k) b[k] = cvt1<TI, TO>(a[k]);
+            uint4 o;
+            memcpy(&o, b, sizeof(o));
+            __stcs(reinterpret_cast<uint4*>(out) + t + u * stride, o);
+        }
+    }
+    for (; t < nq; t += stride) {
+        const VIn v = __ldcs(reinterpret_cast<const VIn*>(in) + t);
+        TI a[E];
+        memcpy(a, &v, sizeof(a));
+        TO b[E];
+#pragma unroll
+        for (int k = 0; k < E; ++k) b[k] = cvt1<TI, TO>(a[k]);
+        uint4 o;
+        memcpy(&o, b, sizeof(o));
+        __stcs(reinterpret_cast<uint4*>(out) + t, o);
     }
 }
 
@@ -90,7 +147,21 @@ void run_convert(Ctx* ctx, cudaStream_t s, const void* src, int64_t lds, void* d
     const bool contiguous = (lds == rows && ldd == rows) || cols == 1;
     const bool aligned = (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-    if (contiguous && aligned) {
+    if (contiguous && aligned && sizeof(TO) == 8 && sizeof(TI) < 8) {
+        constexpr int E = 16 / sizeof(TO);
+        const int64_t nq = n / E;
+        if (nq > 0) {
+            convert_widen_kernel<TI, TO><<<grid_for(nq, 256, ctx->sm_count, 8), 256, 0, s>>>(
+                in, out, nq);
+            count_launch(ctx);
+        }
+        const int64_t done = nq * E;
+        if (done < n) {
+            convert_2d_kernel<TI, TO><<<1, 256, 0, s>>>(in + done, n - done, out + done,
+                                                         n - done, n - done, 1);
+            count_launch(ctx);
+        }
+    } else if (contiguous && aligned) {
         const int64_t n8 = n / 8;
         if (n8 > 0) {
             convert_vec_kernel<TI, TO><<<grid_for(n8, 256, ctx->sm_count, 4), 256, 0, s>>>(
