@@ -220,6 +220,17 @@ mp_status mp_tile_fill_matern_points(mp_ctx ctx, mp_tile t, const double* host_x
                                      double variance, double nugget);
 /* Device copy of all tile values (identical grids and precisions). */
 mp_status mp_tile_copy(mp_ctx ctx, mp_tile dst, mp_tile src);
+/* gaussian_nll (workloads.cpp:74-87) of host vector z under the covariance
+ * held in `cov`, which is factored in place (lower L):
+ *   chol_with_jitter (workloads.cpp:54-70): when jitter > 0 it is added to
+ *   the diagonal first and multiplied by 10 after every NotPositiveDefinite
+ *   failure while <= max_jitter (the input is restored between attempts);
+ *   logdet = 2 sum log L_ii; w = L^{-1} z (FP64 vector, tiles widened);
+ *   nll = 0.5 w'w + 0.5 logdet + 0.5 n log(2 pi).
+ * Any of the outputs may be NULL.  jitter_used receives the final jitter. */
+mp_status mp_tile_gaussian_nll(mp_ctx ctx, mp_tile cov, const double* host_z, double jitter,
+                               double max_jitter, double* nll, double* logdet, double* quad,
+                               double* jitter_used);
 
 #ifdef __cplusplus
 }

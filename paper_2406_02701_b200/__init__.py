@@ -20,6 +20,7 @@ from .mpcr import (  # noqa: F401
     ew_binary,
     ew_scalar,
     ew_unary,
+    gaussian_nll,
     linalg,
     parse_precision,
     promote,
@@ -32,7 +33,7 @@ from .mpcr import (  # noqa: F401
 
 __all__ = [
     "BinaryOp", "Context", "MPArray", "MPCRTile", "MPError", "Precision", "ReduceOp", "Side",
-    "UnaryOp", "default_context", "diag", "ew_binary", "ew_scalar", "ew_unary", "linalg",
+    "UnaryOp", "default_context", "diag", "ew_binary", "ew_scalar", "ew_unary", "gaussian_nll", "linalg",
     "parse_precision", "promote", "reduce", "tile_chol", "tile_gemm", "tile_trsm", "transpose",
     "lib", "LIB_PATH",
 ]

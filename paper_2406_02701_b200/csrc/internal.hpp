@@ -206,6 +206,19 @@ void launch_matern_points(Ctx* ctx, cudaStream_t s, mp_precision p, void* dst, i
                           const double* y, double nu, double range, double variance,
                           double nugget);
 
+// nll.cu: tiled forward solve pieces (FP64 right-hand side)
+struct TrsvItem {
+    const void* L;  // tile (j, i), nb x nb column-major
+    double* r;      // r_j
+};
+void launch_tile_trsv(Ctx* ctx, cudaStream_t s, mp_precision p, const void* L, int64_t ld, int nb,
+                      double* r);
+void launch_tile_gemv(Ctx* ctx, cudaStream_t s, mp_precision p, const void* dev_items,
+                      int64_t count, int nb, const double* w);
+void launch_square_sum(Ctx* ctx, cudaStream_t s, const double* w, int64_t n, double* out);
+void launch_add_diag(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64_t ld, int n,
+                     double v);
+
 inline void count_launch(Ctx* ctx, int n = 1) { ctx->launches += n; }
 
 extern thread_local std::string g_last_error;

@@ -770,6 +770,97 @@ mp_status mp_tile_fill_matern_points(mp_ctx ctx, mp_tile t, const double* host_x
     MP_API_END
 }
 
+mp_status mp_tile_gaussian_nll(mp_ctx ctx, mp_tile cov, const double* host_z, double jitter,
+                               double max_jitter, double* nll, double* logdet, double* quad,
+                               double* jitter_used) {
+    MP_API_BEGIN
+    mp_tile_s& t = T_(cov);
+    Ctx* c = ctx;
+    if (!c || !host_z) fail(MP_INVALID_PARAM, "null argument");
+    if (t.rows != t.cols || t.br != t.bc) fail(MP_SHAPE_MISMATCH, "nll: square MPCRTile required");
+    cudaStream_t s = c->stream;
+    const int64_t n = t.rows, nb = t.br, NT = t.tr;
+    // backup of the input for jitter escalation (workloads.cpp:63-67)
+    void* backup[3] = {nullptr, nullptr, nullptr};
+    struct Free {
+        void** b;
+        ~Free() {
+            for (int q = 0; q < 3; ++q)
+                if (b[q]) cudaFree(b[q]);
+        }
+    } free_backup{backup};
+    auto slab_bytes = [&](int q) {
+        return static_cast<size_t>(t.nslot[q]) * t.tt() * elem_bytes((mp_precision)q);
+    };
+    if (jitter > 0.0)
+        for (int q = 0; q < 3; ++q)
+            if (t.nslot[q]) {
+                MP_CUDA(cudaMalloc(&backup[q], slab_bytes(q)));
+                MP_CUDA(cudaMemcpyAsync(backup[q], t.slab[q], slab_bytes(q), cudaMemcpyDeviceToDevice, s));
+            }
+    double jit = jitter > 0.0 ? jitter : 0.0;
+    for (;;) {
+        if (jit > 0.0)
+            for (int64_t d = 0; d < NT; ++d)
+                launch_add_diag(c, s, t.p(d, d), t.ptr(d, d), nb, static_cast<int>(nb), jit);
+        const int64_t inf = tile_chol_inplace(c, t);
+        if (inf < 0) break;
+        if (jit <= 0.0 || jit * 10.0 > max_jitter)
+            throw Error(MP_NOT_POSITIVE_DEFINITE,
+                        "matrix is not positive definite at pivot column " + std::to_string(inf), inf);
+        jit *= 10.0;
+        for (int q = 0; q < 3; ++q)
+            if (t.nslot[q])
+                MP_CUDA(cudaMemcpyAsync(t.slab[q], backup[q], slab_bytes(q), cudaMemcpyDeviceToDevice, s));
+    }
+    // forward solve w = L^{-1} z, tile row by tile row
+    double* r = static_cast<double*>(c->ensure_scratch((n + 64) * sizeof(double), 3));
+    double* dsum = r + n;
+    MP_CUDA(cudaMemcpyAsync(r, host_z, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    std::vector<TrsvItem> items;
+    std::vector<size_t> off(NT * 3 + 1, 0);
+    std::vector<int64_t> cnt(NT * 3, 0);
+    for (int64_t i = 0; i < NT; ++i)
+        for (int q = 0; q < 3; ++q) {
+            off[i * 3 + q] = items.size();
+            for (int64_t j = i + 1; j < NT; ++j)
+                if (t.p(j, i) == q) items.push_back(TrsvItem{t.ptr(j, i), r + j * nb});
+            cnt[i * 3 + q] = static_cast<int64_t>(items.size() - off[i * 3 + q]);
+        }
+    TrsvItem* ditems = nullptr;
+    struct FreeItems {
+        TrsvItem** p;
+        ~FreeItems() {
+            if (*p) cudaFree(*p);
+        }
+    } free_items{&ditems};
+    if (!items.empty()) {
+        MP_CUDA(cudaMalloc(&ditems, items.size() * sizeof(TrsvItem)));
+        MP_CUDA(cudaMemcpyAsync(ditems, items.data(), items.size() * sizeof(TrsvItem),
+                                cudaMemcpyHostToDevice, s));
+    }
+    for (int64_t i = 0; i < NT; ++i) {
+        launch_tile_trsv(c, s, t.p(i, i), t.ptr(i, i), nb, static_cast<int>(nb), r + i * nb);
+        for (int q = 0; q < 3; ++q)
+            if (cnt[i * 3 + q])
+                launch_tile_gemv(c, s, (mp_precision)q, ditems + off[i * 3 + q], cnt[i * 3 + q],
+                                 static_cast<int>(nb), r + i * nb);
+    }
+    launch_square_sum(c, s, r, n, dsum);
+    MP_CUDA(cudaMemsetAsync(dsum + 1, 0, sizeof(double), s));
+    for (int64_t d = 0; d < NT; ++d)
+        launch_logdiag_sum(c, s, t.p(d, d), t.ptr(d, d), nb, nb, dsum + 1);
+    double h[2];
+    MP_CUDA(cudaMemcpyAsync(h, dsum, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    const double ld = 2.0 * h[1];
+    if (quad) *quad = h[0];
+    if (logdet) *logdet = ld;
+    if (nll) *nll = 0.5 * h[0] + 0.5 * ld + 0.5 * static_cast<double>(n) * std::log(2.0 * M_PI);
+    if (jitter_used) *jitter_used = jit;
+    MP_API_END
+}
+
 mp_status mp_tile_copy(mp_ctx ctx, mp_tile dst, mp_tile src) {
     MP_API_BEGIN
     mp_tile_s &d = T_(dst), &s = T_(src);

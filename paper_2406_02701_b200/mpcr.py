@@ -464,6 +464,18 @@ def tile_chol(x: MPCRTile, overwrite_input: bool = True, num_threads: int = 1) -
     return MPCRTile(0, 0, 0, 0, ctx=x.ctx, _handle=out)
 
 
+def gaussian_nll(z, cov: MPCRTile, jitter: float = 1e-6, max_jitter: float = 1e-3) -> dict:
+    """gaussian_nll (workloads.cpp:74-87) on a mixed-precision MPCRTile; `cov`
+    is factored in place.  jitter <= 0 disables chol_with_jitter (the
+    reference uses 1e-6 .. 1e-3 whenever the factor is not all-double)."""
+    z = np.ascontiguousarray(np.asarray(z, dtype=np.float64).ravel())
+    out = [C.c_double() for _ in range(4)]
+    check(lib().mp_tile_gaussian_nll(cov.ctx.h, cov.h, z.ctypes.data_as(C.c_void_p),
+                                     float(jitter), float(max_jitter),
+                                     *[C.byref(o) for o in out]))
+    return dict(zip(("nll", "logdet", "quad", "jitter"), (o.value for o in out)))
+
+
 def tile_trsm(a: MPCRTile, b: MPCRTile, side: str = "L", upper_triangle: bool = False,
               transpose: bool = False, alpha: float = 1.0) -> None:
     """MPCRTile.trsm: b overwritten with X."""
