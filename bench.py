@@ -3,7 +3,7 @@
 
 Default workload (BASELINE.json configs[2], the N=1 config the metric is
 quoted on): n = 65536, tile 1024, exponential (Matern nu=0.5) covariance of
-the first n points of a 256x256 unit grid, range 0.1; tile precision by band
+the first n points of a 256x256 unit grid, range 0.03; tile precision by band
 |i-j|: < b64 -> FP64, < b32 -> FP32, else FP16 (default b64=1, b32=2).
 
 A step is one full factorization chol(A) of the resident matrix (n^3/3
@@ -16,9 +16,11 @@ C ABI from host buffers: host point coordinates -> device Matern generation
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
     python bench.py --workload gemm --prec half --n 8192     (config 2 lines)
 
-Multi-GPU (torchrun): every rank factors its own replica (replicas only;
-the 2D block-cyclic distributed factorization is future work), the time is
-the max over ranks, value = total flops of all ranks / that time.
+Multi-GPU (torchrun, N > 1): BASELINE.json configs[3] — ONE n = 131072
+matrix (default; --n overrides) 2D block-cyclic over a P x Q process grid
+(P = largest divisor of N <= sqrt(N)), panel tiles broadcast by NCCL
+(csrc/dist.cpp); strong scaling: value = n^3/3 / (max over ranks of the
+step time).
 """
 from __future__ import annotations
 
@@ -238,12 +240,22 @@ def run_chol(args, world, rank, local):
     import paper_2406_02701_b200 as mp
 
     ctx = mp.Context(local)
-    n, nb = args.n, args.nb
+    n = args.n or (65536 if world == 1 else 131072)
+    nb = args.nb
     nt = n // nb
     g = band_map(nt, args.b64, args.b32)
     x, y, side = grid_points(n)
-    A0 = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
-    A = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+    grid = None
+    if world > 1:
+        import torch.distributed as tdist
+
+        P = max(d for d in range(1, int(world ** 0.5) + 1) if world % d == 0)
+        Q = world // P
+        obj = [mp.nccl_unique_id() if rank == 0 else None]
+        tdist.broadcast_object_list(obj, src=0)
+        grid = mp.ProcessGrid(rank, world, P, Q, obj[0], ctx)
+    A0 = mp.MPCRTile(n, n, nb, nb, None, g, ctx, grid=grid)
+    A = mp.MPCRTile(n, n, nb, nb, None, g, ctx, grid=grid)
     A0.fill_matern_points(x, y, 0.5, args.range, 1.0, args.nugget)
     ctx.synchronize()
 
@@ -322,20 +334,23 @@ def run_chol(args, world, rank, local):
     nominal = {"fp16": pk["bf16_tflops_sustained"], "fp32_simt": 74.0, "fp64": 37.0}
     tmin = fp[0] / (nominal["fp16"] * 1e12) + fp[1] / (nominal["fp32_simt"] * 1e12) + \
         fp[2] / (nominal["fp64"] * 1e12)
-    value = world * flops / (ms_max * 1e-3) / 1e12
+    value = flops / (ms_max * 1e-3) / 1e12  # one matrix over all ranks (strong scaling)
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "mixed(f64/f32/f16-storage; f16 tcgen05 f32-acc, f32/f64 SIMT)",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "mixed(f64/f32/f16 storage; f16 tcgen05 f32-acc, f32 3xTF32 tcgen05, f64 DMMA)",
         "data": "synthetic",
-        "config": {"workload": f"MPCRTile mixed-precision Cholesky n={n}, tile {nb}, 1 replica/GPU",
+        "config": {"workload": f"MPCRTile mixed-precision Cholesky n={n}, tile {nb}" +
+                               (f", 2D block-cyclic {grid.P}x{grid.Q}" if grid else ", 1 GPU"),
                    "n": n, "nb": nb, "precision_map": f"|i-j|<{args.b64}:FP64, <{args.b32}:FP32, else FP16",
                    "tiles_by_precision": {p: int((g == i).sum()) for i, p in enumerate(["f16", "f32", "f64"])},
                    "covariance": f"Matern nu=0.5 range {args.range} sigma2 1 nugget {args.nugget}, "
                                  f"first {n} points of a {side}x{side} unit grid",
-                   "fp32_method": "SIMT", "l2": "inputs 8+ GB >> 126 MB L2 (no flush needed)",
-                   "parallelism": f"replicas x{world}"},
+                   "fp32_method": "3xTF32 (tcgen05 kind::tf32)",
+                   "l2": "inputs 8+ GB >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"2D block-cyclic {grid.P}x{grid.Q}, NCCL panel broadcast"
+                                  if grid else "single GPU"},
         "roofline": roof,
         "blended_roofline": {"t_min_ms": tmin * 1e3, "frac": tmin / (ms_max * 1e-3),
                              "flops_by_dest_precision": {"f16": fp[0], "f32": fp[1], "f64": fp[2]},
@@ -348,7 +363,7 @@ def run_chol(args, world, rank, local):
         "clocks": clk.summary(),
     }
     if e2e_ms is not None:
-        line["e2e"] = {"value": world * flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+        line["e2e"] = {"value": flops / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                        "h2d_bytes_per_step": 2 * n * 8, "d2h_bytes_per_step": 8,
                        "ms_per_step": e2e_ms,
                        "path": "host (x,y) -> mp_tile_fill_matern_points -> mp_tile_chol -> mp_tile_logdet"}
@@ -366,7 +381,7 @@ def run_gemm(args, world, rank, local):
     import paper_2406_02701_b200 as mp
 
     ctx = mp.Context(local)
-    n = args.n
+    n = args.n or 8192
     p = mp.parse_precision(args.prec)
     rng = np.random.default_rng(1000 + n)
     A = mp.MPArray.from_numpy(rng.random((n, n)), p, ctx)
@@ -401,7 +416,7 @@ def run_cast(args, world, rank, local):
     import paper_2406_02701_b200 as mp
 
     ctx = mp.Context(local)
-    n = args.n
+    n = args.n or 32768
     pin, pout = (mp.parse_precision(p) for p in args.cast.split(":"))
     a = mp.MPArray.zeros_matrix(n, n, pin, ctx)
     b = mp.MPArray.zeros_matrix(n, n, pout, ctx)
@@ -441,7 +456,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="chol", choices=["chol", "gemm", "cast"])
     ap.add_argument("--cast", default="double:half")
-    ap.add_argument("--n", type=int, default=65536)
+    ap.add_argument("--n", type=int, default=None,
+                    help="matrix order (default 65536 at N=1, 131072 at N>1)")
     ap.add_argument("--nb", type=int, default=1024)
     ap.add_argument("--b64", type=int, default=1)
     ap.add_argument("--b32", type=int, default=2)

@@ -232,6 +232,34 @@ mp_status mp_tile_gaussian_nll(mp_ctx ctx, mp_tile cov, const double* host_z, do
                                double max_jitter, double* nll, double* logdet, double* quad,
                                double* jitter_used);
 
+/* ------------------------------------------------------------------------- */
+/* Multi-GPU: 2D block-cyclic MPCRTile over a P x Q process grid (one process */
+/* per GPU).  Tile (i, j), i >= j, lives on rank (i mod P) * Q + (j mod Q);   */
+/* panel tiles and the diagonal inverse are broadcast with NCCL over NVLink.  */
+/* ------------------------------------------------------------------------- */
+typedef struct mp_dist_s* mp_dist;
+/* 128-byte ncclUniqueId, made on one rank and shared by the caller (e.g.
+ * torch.distributed); NCCL is resolved with dlopen at first use. */
+mp_status mp_nccl_unique_id(unsigned char* out128);
+mp_status mp_dist_create(mp_ctx ctx, int rank, int world, int P, int Q,
+                         const unsigned char* uid128, mp_dist* out);
+mp_status mp_dist_destroy(mp_dist d);
+/* Owner rank of tile (i, j). */
+int mp_dist_owner(int64_t i, int64_t j, int P, int Q);
+/* The per-rank action list the distributed chol executes, as int32 records
+ * {op, k, i, j, root, prec} (op: 1 POTRF, 2 BCAST_DIAG, 3 TRSM, 4
+ * BCAST_PANEL, 5 UPDATE).  actions may be NULL to query *count. */
+mp_status mp_dist_schedule(int rank, int P, int Q, int64_t tiles, const int* precisions,
+                           int32_t* actions, int64_t capacity, int64_t* count);
+/* MPCRTile whose lower-triangle tiles are distributed; this rank stores only
+ * the tiles it owns (rows must equal cols).  mp_tile_chol on it runs the
+ * distributed factorization; mp_tile_logdet / mp_tile_gaussian_nll reduce
+ * over the ranks; get/set/fill touch owned tiles only. */
+mp_status mp_tile_create_dist(mp_ctx ctx, mp_dist dist, int64_t n, int64_t tile,
+                              const int* precisions, mp_tile* out);
+/* 1 if this rank stores tile (i, j). */
+int mp_tile_owns(mp_tile t, int64_t i, int64_t j);
+
 #ifdef __cplusplus
 }
 #endif

@@ -12,16 +12,20 @@ from .mpcr import (  # noqa: F401
     MPArray,
     MPCRTile,
     Precision,
+    ProcessGrid,
     ReduceOp,
     Side,
     UnaryOp,
     default_context,
     diag,
+    dist_owner,
+    dist_schedule,
     ew_binary,
     ew_scalar,
     ew_unary,
     gaussian_nll,
     linalg,
+    nccl_unique_id,
     parse_precision,
     promote,
     reduce,
@@ -32,8 +36,8 @@ from .mpcr import (  # noqa: F401
 )
 
 __all__ = [
-    "BinaryOp", "Context", "MPArray", "MPCRTile", "MPError", "Precision", "ReduceOp", "Side",
-    "UnaryOp", "default_context", "diag", "ew_binary", "ew_scalar", "ew_unary", "gaussian_nll", "linalg",
+    "BinaryOp", "Context", "MPArray", "MPCRTile", "MPError", "Precision", "ProcessGrid", "ReduceOp", "Side",
+    "UnaryOp", "default_context", "diag", "dist_owner", "dist_schedule", "nccl_unique_id", "ew_binary", "ew_scalar", "ew_unary", "gaussian_nll", "linalg",
     "parse_precision", "promote", "reduce", "tile_chol", "tile_gemm", "tile_trsm", "transpose",
     "lib", "LIB_PATH",
 ]

@@ -89,6 +89,15 @@ SIGNATURES = {
     "mp_tile_gaussian_nll": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_double,
                                        C.POINTER(C.c_double), C.POINTER(C.c_double),
                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    # multi-GPU (2D block-cyclic MPCRTile)
+    "mp_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "mp_dist_create": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(_vp)]),
+    "mp_dist_destroy": (C.c_int, [_vp]),
+    "mp_dist_owner": (C.c_int, [_i64, _i64, C.c_int, C.c_int]),
+    "mp_dist_schedule": (C.c_int, [C.c_int, C.c_int, C.c_int, _i64, C.POINTER(C.c_int),
+                                   C.POINTER(C.c_int32), _i64, _ip]),
+    "mp_tile_create_dist": (C.c_int, [_vp, _vp, _i64, _i64, C.POINTER(C.c_int), C.POINTER(_vp)]),
+    "mp_tile_owns": (C.c_int, [_vp, _i64, _i64]),
 }
 
 

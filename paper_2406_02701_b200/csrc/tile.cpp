@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "batch.hpp"
+#include "dist.hpp"
 #include "gemm_tc.hpp"
 #include "internal.hpp"
 
@@ -32,6 +33,7 @@ using namespace mpcr;
 
 struct mp_tile_s {
     Ctx* ctx = nullptr;
+    mp_dist_s* dist = nullptr;  // distributed over a process grid (null: single GPU)
     int64_t rows = 0, cols = 0, br = 0, bc = 0, tr = 0, tc = 0;
     std::vector<mp_precision> prec;  // tile (i, j) at j * tr + i
     std::vector<int64_t> slot;
@@ -47,10 +49,13 @@ struct mp_tile_s {
 
     int64_t tt() const { return br * bc; }
     mp_precision p(int64_t i, int64_t j) const { return prec[j * tr + i]; }
+    bool has(int64_t i, int64_t j) const { return slot[j * tr + i] >= 0; }
     void* ptr(int64_t i, int64_t j) const {
         const mp_precision q = p(i, j);
+        if (!has(i, j)) return nullptr;
         return static_cast<char*>(slab[q]) + slot[j * tr + i] * tt() * elem_bytes(q);
     }
+    int rank() const { return dist ? dist->rank : 0; }
     void* panel_ptr(mp_precision q, int64_t i) const {
         return static_cast<char*>(panel[q]) + i * tt() * elem_bytes(q);
     }
@@ -132,89 +137,121 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     ensure_panels(t);
     const bool tc_ok = (nb % 8) == 0;  // TMA stride alignment for FP16 tiles
 
-    // ---- host plan ----------------------------------------------------------
-    std::vector<char> buf;
-    std::vector<StepLists> steps(NT);
-    for (int64_t k = 0; k < NT; ++k) {
-        StepLists& L = steps[k];
-        std::vector<TcProblem> trsm_tc;
-        std::vector<TileProblem> trsm_p[3];
-        std::vector<CopyItem> wb[3];
-        std::vector<CopyItem> cv[3][3];
-        std::vector<TcProblem> up_tc, up_tc32;
+    // ---- host plan: the rank's action list (dist.hpp) turned into grouped
+    //      per-step work lists (single GPU: P = Q = 1, no broadcasts) --------
+    const int P = t.dist ? t.dist->P : 1, Q = t.dist ? t.dist->Q : 1, rank = t.rank();
+    std::vector<int> pgrid(t.prec.begin(), t.prec.end());
+    const auto sched = dist_schedule(rank, P, Q, NT, pgrid.data());
+    struct StepAcc {
+        bool potrf = false;
+        std::vector<TcProblem> trsm_tc, up_tc, up_tc32;
+        std::vector<TileProblem> trsm_p[3], up_p[3];
+        std::vector<CopyItem> wb[3], cv[3][3];
         std::vector<SplitItem> split32;
-        std::vector<TileProblem> up_p[3];
-        char* linv_base = static_cast<char*>(t.work);
-        const size_t nn = static_cast<size_t>(nb) * nb;
-        const void* linv[3] = {linv_base + nn * 24, linv_base + nn * 20, linv_base + nn * 8};
-        for (int64_t i = k + 1; i < NT; ++i) {
-            const mp_precision q = t.p(i, k);
-            L.need_linv[q] = true;
-            if (q == MP_HALF && tc_ok)
-                // A = matrix tile (i,k) in the FP16 slab, C = panel16[i]
-                trsm_tc.push_back(TcProblem{static_cast<int32_t>(t.slot[k * NT + i]), 0,
-                                            static_cast<int32_t>(i), 0});
-            else
-                trsm_p[q].push_back(TileProblem{t.ptr(i, k), linv[q], t.panel_ptr(q, i), 0, 0});
-            wb[q].push_back(CopyItem{t.panel_ptr(q, i), t.ptr(i, k)});
-            bool need[3] = {false, false, false};
-            for (int64_t j = k + 1; j <= i; ++j) need[t.p(i, j)] = true;  // A operand of row i
-            for (int64_t m = i; m < NT; ++m) need[t.p(m, i)] = true;      // B operand of column i
-            for (int r = 0; r < 3; ++r)
-                if (need[r] && r != q) cv[q][r].push_back(CopyItem{t.panel_ptr(q, i), t.panel_ptr((mp_precision)r, i)});
-            if (tc_ok && need[MP_SINGLE])  // FP32 consumers run 3xTF32 on hi/lo splits
-                split32.push_back(SplitItem{t.panel_ptr(MP_SINGLE, i),
-                                            static_cast<char*>(t.split32[0]) + i * tt * 4,
-                                            static_cast<char*>(t.split32[1]) + i * tt * 4});
-        }
-        for (int64_t j = k + 1; j < NT; ++j)
-            for (int64_t i = j; i < NT; ++i) {
-                const mp_precision q = t.p(i, j);
+        bool need_linv[3] = {false, false, false};
+    };
+    std::vector<StepAcc> acc(NT);
+    std::vector<std::vector<std::pair<int, int>>> bcasts(NT);  // (i, root) per step
+    const size_t nn0 = static_cast<size_t>(nb) * nb;
+    char* linv_base = static_cast<char*>(t.work);
+    const void* linv[3] = {linv_base + nn0 * 24, linv_base + nn0 * 20, linv_base + nn0 * 8};
+    auto consumers = [&](int64_t k, int64_t i, StepAcc& A) {
+        // every rank receives every panel tile: convert it once to each
+        // precision the rank's own consumers (A_ij.converted(p) operands) need
+        const mp_precision q = t.p(i, k);
+        bool need[3] = {false, false, false};
+        for (int64_t j = k + 1; j <= i; ++j)  // A operand of (owned) row-i updates
+            if (t.has(i, j)) need[t.p(i, j)] = true;
+        for (int64_t m = i; m < NT; ++m)  // B operand of (owned) column-i updates
+            if (t.has(m, i)) need[t.p(m, i)] = true;
+        for (int r = 0; r < 3; ++r)
+            if (need[r] && r != q) A.cv[q][r].push_back(CopyItem{t.panel_ptr(q, i), t.panel_ptr((mp_precision)r, i)});
+        if (tc_ok && need[MP_SINGLE])  // FP32 consumers run 3xTF32 on hi/lo splits
+            A.split32.push_back(SplitItem{t.panel_ptr(MP_SINGLE, i),
+                                          static_cast<char*>(t.split32[0]) + i * tt * 4,
+                                          static_cast<char*>(t.split32[1]) + i * tt * 4});
+    };
+    for (const DistAction& a : sched) {
+        StepAcc& A = acc[a.k];
+        const int64_t k = a.k, i = a.i, j = a.j;
+        const mp_precision q = static_cast<mp_precision>(a.prec);
+        switch (a.op) {
+            case DA_POTRF:
+                A.potrf = true;
+                break;
+            case DA_TRSM:
+                A.need_linv[q] = true;
+                if (q == MP_HALF && tc_ok)
+                    // A = matrix tile (i,k) in the FP16 slab, C = panel16[i]
+                    A.trsm_tc.push_back(TcProblem{static_cast<int32_t>(t.slot[k * NT + i]), 0,
+                                                  static_cast<int32_t>(i), 0});
+                else
+                    A.trsm_p[q].push_back(TileProblem{t.ptr(i, k), linv[q], t.panel_ptr(q, i), 0, 0});
+                A.wb[q].push_back(CopyItem{t.panel_ptr(q, i), t.ptr(i, k)});
+                if (P * Q == 1) consumers(k, i, A);
+                break;
+            case DA_BCAST_PANEL:
+                bcasts[k].push_back({static_cast<int>(i), a.root});
+                consumers(k, i, A);
+                break;
+            case DA_UPDATE: {
                 const int32_t lo = (i == j) ? 1 : 0;
                 if (q == MP_HALF && tc_ok)
-                    up_tc.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
-                                              static_cast<int32_t>(t.slot[j * NT + i]), lo});
+                    A.up_tc.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
+                                                static_cast<int32_t>(t.slot[j * NT + i]), lo});
+                else if (q == MP_SINGLE && tc_ok)
+                    A.up_tc32.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
+                                                  static_cast<int32_t>(t.slot[j * NT + i]), lo});
                 else
-                    if (q == MP_SINGLE && tc_ok)
-                        up_tc32.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
-                                                    static_cast<int32_t>(t.slot[j * NT + i]), lo});
-                    else
-                        up_p[q].push_back(TileProblem{t.panel_ptr(q, i), t.panel_ptr(q, j), t.ptr(i, j), lo, 0});
+                    A.up_p[q].push_back(TileProblem{t.panel_ptr(q, i), t.panel_ptr(q, j), t.ptr(i, j), lo, 0});
+                break;
             }
-        append(buf, trsm_tc, L.trsm_tc);
-        L.n_trsm_tc = trsm_tc.size();
-        append(buf, trsm_p[MP_HALF], L.trsm_h_simt);
-        L.n_trsm_h_simt = trsm_p[MP_HALF].size();
-        append(buf, trsm_p[MP_SINGLE], L.trsm_s);
-        L.n_trsm_s = trsm_p[MP_SINGLE].size();
-        append(buf, trsm_p[MP_DOUBLE], L.trsm_d);
-        L.n_trsm_d = trsm_p[MP_DOUBLE].size();
+            default:
+                break;
+        }
+    }
+    std::vector<char> buf;
+    std::vector<StepLists> steps(NT);
+    std::vector<bool> do_potrf(NT, false);
+    for (int64_t k = 0; k < NT; ++k) {
+        StepLists& L = steps[k];
+        StepAcc& A = acc[k];
+        do_potrf[k] = A.potrf;
+        for (int q = 0; q < 3; ++q) L.need_linv[q] = A.need_linv[q];
+        append(buf, A.trsm_tc, L.trsm_tc);
+        L.n_trsm_tc = A.trsm_tc.size();
+        append(buf, A.trsm_p[MP_HALF], L.trsm_h_simt);
+        L.n_trsm_h_simt = A.trsm_p[MP_HALF].size();
+        append(buf, A.trsm_p[MP_SINGLE], L.trsm_s);
+        L.n_trsm_s = A.trsm_p[MP_SINGLE].size();
+        append(buf, A.trsm_p[MP_DOUBLE], L.trsm_d);
+        L.n_trsm_d = A.trsm_p[MP_DOUBLE].size();
         for (int q = 0; q < 3; ++q) {
-            append(buf, wb[q], L.wb[q]);
-            L.n_wb[q] = wb[q].size();
+            append(buf, A.wb[q], L.wb[q]);
+            L.n_wb[q] = A.wb[q].size();
             for (int r = 0; r < 3; ++r) {
-                append(buf, cv[q][r], L.cv[q][r]);
-                L.n_cv[q][r] = cv[q][r].size();
+                append(buf, A.cv[q][r], L.cv[q][r]);
+                L.n_cv[q][r] = A.cv[q][r].size();
             }
         }
-        append(buf, up_tc, L.up_tc);
-        L.n_up_tc = up_tc.size();
-        append(buf, up_tc32, L.up_tc32);
-        L.n_up_tc32 = up_tc32.size();
-        append(buf, split32, L.split32);
-        L.n_split32 = split32.size();
-        append(buf, up_p[MP_HALF], L.up_h_simt);
-        L.n_up_h_simt = up_p[MP_HALF].size();
-        append(buf, up_p[MP_SINGLE], L.up_s);
-        L.n_up_s = up_p[MP_SINGLE].size();
-        append(buf, up_p[MP_DOUBLE], L.up_d);
-        L.n_up_d = up_p[MP_DOUBLE].size();
+        append(buf, A.up_tc, L.up_tc);
+        L.n_up_tc = A.up_tc.size();
+        append(buf, A.up_tc32, L.up_tc32);
+        L.n_up_tc32 = A.up_tc32.size();
+        append(buf, A.split32, L.split32);
+        L.n_split32 = A.split32.size();
+        append(buf, A.up_p[MP_HALF], L.up_h_simt);
+        L.n_up_h_simt = A.up_p[MP_HALF].size();
+        append(buf, A.up_p[MP_SINGLE], L.up_s);
+        L.n_up_s = A.up_p[MP_SINGLE].size();
+        append(buf, A.up_p[MP_DOUBLE], L.up_d);
+        L.n_up_d = A.up_p[MP_DOUBLE].size();
     }
     // final clean-up lists: upper part of diagonal tiles, strictly-upper tiles
     std::vector<void*> diag_ptrs[3], upper_ptrs[3];
     for (int64_t j = 0; j < NT; ++j)
         for (int64_t i = 0; i <= j; ++i)
-            (i == j ? diag_ptrs : upper_ptrs)[t.p(i, j)].push_back(t.ptr(i, j));
+            if (t.has(i, j)) (i == j ? diag_ptrs : upper_ptrs)[t.p(i, j)].push_back(t.ptr(i, j));
     size_t off_diag[3], off_upper[3];
     for (int q = 0; q < 3; ++q) {
         append(buf, diag_ptrs[q], off_diag[q]);
@@ -248,10 +285,12 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
 
     for (int64_t k = 0; k < NT; ++k) {
         const StepLists& L = steps[k];
-        // 1. diagonal factor + FP64 inverse of the stored factor
+        // 1. diagonal factor + FP64 inverse of the stored factor (owner only)
         const mp_precision pk = t.p(k, k);
         void* akk = t.ptr(k, k);
-        if (pk == MP_DOUBLE) {
+        if (!do_potrf[k]) {
+            // not the owner: nothing to factor
+        } else if (pk == MP_DOUBLE) {
             // POTRF in place, its 64x64 block inverses straight into Linv
             launch_potrf_lower(c, s, MP_DOUBLE, akk, nb, nb, dinfo, k * nb, linv64, nb);
             if (k + 1 < NT) {
@@ -272,6 +311,9 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             }
         }
         if (k + 1 == NT) break;
+        // distributed: the FP64 inverse of L_kk travels from its owner
+        if (t.dist && t.dist->world > 1)
+            dist_bcast(t.dist, linv64, nn * sizeof(double), dist_owner(k, k, P, Q), s);
         // 2. Linv rounded to the panel precisions (the reference rounds U_kk
         //    to p_ik before trsm: U_kk.converted(p_ik))
         // FP16 panels apply the inverse as hi + lo FP16 halves accumulated in
@@ -331,6 +373,15 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             if (L.n_wb[q])
                 launch_batched_convert(c, s, (mp_precision)q, (mp_precision)q,
                                        reinterpret_cast<const CopyItem*>(dl + L.wb[q]), L.n_wb[q], tt);
+        // distributed: every panel tile travels from its owner to all ranks
+        if (!bcasts[k].empty()) {
+            dist_group_start(t.dist);
+            for (const auto& br : bcasts[k]) {
+                const mp_precision q = t.p(br.first, k);
+                dist_bcast(t.dist, t.panel_ptr(q, br.first), tt * elem_bytes(q), br.second, s);
+            }
+            dist_group_end(t.dist);
+        }
         // 4. consumer-precision copies of the panel
         for (int q = 0; q < 3; ++q)
             for (int r = 0; r < 3; ++r)
@@ -419,6 +470,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             launch_batched_zero(c, s, (mp_precision)q, reinterpret_cast<void* const*>(dl + off_upper[q]),
                                 upper_ptrs[q].size(), tt, false, nb);
     }
+    // first failing column over all ranks (-1 as uint64 is the largest value)
+    if (t.dist && t.dist->world > 1) dist_allreduce_min_u64(t.dist, dinfo, s);
     int64_t info = -1;
     MP_CUDA(cudaMemcpyAsync(&info, dinfo, sizeof(info), cudaMemcpyDeviceToHost, s));
     MP_CUDA(cudaStreamSynchronize(s));
@@ -427,18 +480,19 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
 
 }  // namespace mpcr
 
-extern "C" {
+namespace {
 
-mp_status mp_tile_create(mp_ctx ctx, int64_t rows, int64_t cols, int64_t rpt, int64_t cpt,
-                         const int* precisions, mp_tile* out) {
-    MP_API_BEGIN
-    if (!ctx || !out || !precisions) fail(MP_INVALID_PARAM, "null argument");
+// Shared by mp_tile_create / mp_tile_create_dist: with `dist`, only the
+// lower-triangle tiles this rank owns get storage (slot -1 elsewhere).
+mp_tile_s* tile_new(Ctx* ctx, mp_dist_s* dist, int64_t rows, int64_t cols, int64_t rpt, int64_t cpt,
+                    const int* precisions) {
     if (rows < 1 || cols < 1 || rpt < 1 || cpt < 1)
         fail(MP_INVALID_PARAM, "MPCRTile: sizes must be >= 1");
     if (rows % rpt || cols % cpt)
         fail(MP_SHAPE_MISMATCH, "MPCRTile: tile size must divide the matrix size");
     auto* t = new mp_tile_s();
     t->ctx = ctx;
+    t->dist = dist;
     t->rows = rows;
     t->cols = cols;
     t->br = rpt;
@@ -454,7 +508,9 @@ mp_status mp_tile_create(mp_ctx ctx, int64_t rows, int64_t cols, int64_t rpt, in
             fail(MP_INVALID_PARAM, "MPCRTile: unknown precision code");
         }
         t->prec[q] = static_cast<mp_precision>(precisions[q]);
-        t->slot[q] = t->nslot[precisions[q]]++;
+        const int64_t i = q % t->tr, j = q / t->tr;
+        const bool stored = !dist || (i >= j && dist_owner(i, j, dist->P, dist->Q) == dist->rank);
+        t->slot[q] = stored ? t->nslot[precisions[q]]++ : -1;
     }
     try {
         for (int q = 0; q < 3; ++q)
@@ -467,8 +523,35 @@ mp_status mp_tile_create(mp_ctx ctx, int64_t rows, int64_t cols, int64_t rpt, in
         delete t;
         throw;
     }
-    *out = t;
+    return t;
+}
+
+}  // namespace
+
+extern "C" {
+
+mp_status mp_tile_create(mp_ctx ctx, int64_t rows, int64_t cols, int64_t rpt, int64_t cpt,
+                         const int* precisions, mp_tile* out) {
+    MP_API_BEGIN
+    if (!ctx || !out || !precisions) fail(MP_INVALID_PARAM, "null argument");
+    *out = tile_new(ctx, nullptr, rows, cols, rpt, cpt, precisions);
     MP_API_END
+}
+
+// 2D block-cyclic MPCRTile: tile (i, j), i >= j, stored on rank
+// (i mod P) * Q + (j mod Q) only.
+mp_status mp_tile_create_dist(mp_ctx ctx, mp_dist dist, int64_t n, int64_t tile, const int* precisions,
+                              mp_tile* out) {
+    MP_API_BEGIN
+    if (!ctx || !dist || !out || !precisions) fail(MP_INVALID_PARAM, "null argument");
+    if (dist->ctx != static_cast<Ctx*>(ctx)) fail(MP_INVALID_PARAM, "dist belongs to another context");
+    *out = tile_new(ctx, dist, n, n, tile, tile, precisions);
+    MP_API_END
+}
+
+int mp_tile_owns(mp_tile t, int64_t i, int64_t j) {
+    if (!t || i < 0 || j < 0 || i >= t->tr || j >= t->tc) return 0;
+    return t->has(i, j) ? 1 : 0;
 }
 
 mp_status mp_tile_destroy(mp_tile t) {
@@ -496,8 +579,9 @@ mp_status mp_tile_set_values_device(mp_tile t, const double* dev, int64_t ld) {
     Ctx* c = x.ctx;
     for (int64_t j = 0; j < x.tc; ++j)
         for (int64_t i = 0; i < x.tr; ++i)
-            launch_convert(c, c->stream, MP_DOUBLE, dev + (j * x.bc) * ld + i * x.br, ld, x.p(i, j),
-                           x.ptr(i, j), x.br, x.br, x.bc);
+            if (x.has(i, j))
+                launch_convert(c, c->stream, MP_DOUBLE, dev + (j * x.bc) * ld + i * x.br, ld, x.p(i, j),
+                               x.ptr(i, j), x.br, x.br, x.bc);
     MP_API_END
 }
 
@@ -512,8 +596,9 @@ mp_status mp_tile_set_values(mp_tile t, const double* host) {
         MP_CUDA(cudaMemcpyAsync(tmp, host + j * x.bc * x.rows, panel * sizeof(double),
                                 cudaMemcpyHostToDevice, c->stream));
         for (int64_t i = 0; i < x.tr; ++i)
-            launch_convert(c, c->stream, MP_DOUBLE, tmp + i * x.br, x.rows, x.p(i, j), x.ptr(i, j),
-                           x.br, x.br, x.bc);
+            if (x.has(i, j))
+                launch_convert(c, c->stream, MP_DOUBLE, tmp + i * x.br, x.rows, x.p(i, j), x.ptr(i, j),
+                               x.br, x.br, x.bc);
         MP_CUDA(cudaStreamSynchronize(c->stream));
     }
     MP_API_END
@@ -526,9 +611,12 @@ mp_status mp_tile_get_values(mp_tile t, double* host) {
     const size_t panel = static_cast<size_t>(x.rows) * x.bc;
     double* tmp = static_cast<double*>(c->ensure_scratch(panel * sizeof(double), 1));
     for (int64_t j = 0; j < x.tc; ++j) {
+        // distributed tiles: tiles held by other ranks read as zeros
+        if (x.dist) MP_CUDA(cudaMemsetAsync(tmp, 0, panel * sizeof(double), c->stream));
         for (int64_t i = 0; i < x.tr; ++i)
-            launch_convert(c, c->stream, x.p(i, j), x.ptr(i, j), x.br, MP_DOUBLE, tmp + i * x.br,
-                           x.rows, x.br, x.bc);
+            if (x.has(i, j))
+                launch_convert(c, c->stream, x.p(i, j), x.ptr(i, j), x.br, MP_DOUBLE, tmp + i * x.br,
+                               x.rows, x.br, x.bc);
         MP_CUDA(cudaMemcpyAsync(host + j * x.bc * x.rows, tmp, panel * sizeof(double),
                                 cudaMemcpyDeviceToHost, c->stream));
         MP_CUDA(cudaStreamSynchronize(c->stream));
@@ -541,6 +629,7 @@ mp_status mp_tile_get_tile(mp_tile t, int64_t i, int64_t j, mp_array* view) {
     mp_tile_s& x = T_(t);
     if (i < 0 || j < 0 || i >= x.tr || j >= x.tc)
         fail(MP_INDEX_OUT_OF_RANGE, "GetTile: tile index out of range");
+    if (!x.has(i, j)) fail(MP_INVALID_PARAM, "GetTile: tile is stored on another rank");
     return mp_array_wrap(static_cast<mp_ctx>(x.ctx), x.p(i, j), x.br, x.bc, x.br, x.ptr(i, j), view);
     MP_API_END
 }
@@ -565,9 +654,7 @@ mp_status mp_tile_chol(mp_ctx ctx, mp_tile a, int overwrite_input, mp_tile* out,
     if (!overwrite_input) {
         if (!out) fail(MP_INVALID_PARAM, "chol: out is required when overwrite_input is false");
         std::vector<int> pr(x.prec.begin(), x.prec.end());
-        mp_tile nt = nullptr;
-        const mp_status st = mp_tile_create(ctx, x.rows, x.cols, x.br, x.bc, pr.data(), &nt);
-        if (st != MP_OK) return st;
+        mp_tile nt = tile_new(ctx, x.dist, x.rows, x.cols, x.br, x.bc, pr.data());
         for (int q = 0; q < 3; ++q)
             if (x.nslot[q])
                 MP_CUDA(cudaMemcpyAsync(nt->slab[q], x.slab[q],
@@ -593,6 +680,7 @@ mp_status mp_tile_gemm(mp_ctx ctx, mp_tile a, mp_tile b, mp_tile cc, int ta, int
     mp_tile_s &A = T_(a), &B = T_(b), &C = T_(cc);
     Ctx* c = ctx;
     if (!c) fail(MP_INVALID_PARAM, "null context");
+    if (A.dist || B.dist || C.dist) fail(MP_INVALID_PARAM, "tile gemm: distributed MPCRTile not supported");
     const int64_t kt = ta ? A.tr : A.tc, kb = tb ? B.tc : B.tr;
     const int64_t mt = ta ? A.tc : A.tr, ntl = tb ? B.tr : B.tc;
     const int64_t abr = ta ? A.bc : A.br, abk = ta ? A.br : A.bc;
@@ -636,6 +724,7 @@ mp_status mp_tile_trsm(mp_ctx ctx, mp_tile a, mp_tile b, mp_side side, int upper
     mp_tile_s &A = T_(a), &B = T_(b);
     Ctx* c = ctx;
     if (!c) fail(MP_INVALID_PARAM, "null context");
+    if (A.dist || B.dist) fail(MP_INVALID_PARAM, "tile trsm: distributed MPCRTile not supported");
     if (A.rows != A.cols || A.br != A.bc) fail(MP_SHAPE_MISMATCH, "tile trsm: A must be square");
     const int64_t nt = A.tr, nb = A.br;
     const bool right = side == MP_RIGHT;
@@ -722,7 +811,8 @@ mp_status mp_tile_logdet(mp_ctx ctx, mp_tile l, double* logdet) {
     double* acc = static_cast<double*>(c->ensure_scratch(64, 1));
     MP_CUDA(cudaMemsetAsync(acc, 0, sizeof(double), c->stream));
     for (int64_t d = 0; d < x.tr; ++d)
-        launch_logdiag_sum(c, c->stream, x.p(d, d), x.ptr(d, d), x.br, x.br, acc);
+        if (x.has(d, d)) launch_logdiag_sum(c, c->stream, x.p(d, d), x.ptr(d, d), x.br, x.br, acc);
+    if (x.dist) dist_allreduce_sum_f64(x.dist, acc, 1, c->stream);
     double h = 0;
     MP_CUDA(cudaMemcpyAsync(&h, acc, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     MP_CUDA(cudaStreamSynchronize(c->stream));
@@ -744,7 +834,8 @@ mp_status mp_tile_fill_matern(mp_ctx ctx, mp_tile t, int64_t side, double nu, do
     if (nu != 0.5 && nu != 1.5 && nu != 2.5) fail(MP_INVALID_PARAM, "matern_cov: nu must be 0.5, 1.5, or 2.5");
     for (int64_t j = 0; j < x.tc; ++j)
         for (int64_t i = 0; i < x.tr; ++i)
-            launch_matern_tile(c, c->stream, x.p(i, j), x.ptr(i, j), x.br, i * x.br, j * x.bc, x.br,
+            if (x.has(i, j))
+                launch_matern_tile(c, c->stream, x.p(i, j), x.ptr(i, j), x.br, i * x.br, j * x.bc, x.br,
                                x.bc, side, nu, range, variance);
     MP_API_END
 }
@@ -765,7 +856,8 @@ mp_status mp_tile_fill_matern_points(mp_ctx ctx, mp_tile t, const double* host_x
     MP_CUDA(cudaMemcpyAsync(xy + n, host_y, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     for (int64_t j = 0; j < x.tc; ++j)
         for (int64_t i = 0; i < x.tr; ++i)
-            launch_matern_points(c, c->stream, x.p(i, j), x.ptr(i, j), x.br, i * x.br, j * x.bc,
+            if (x.has(i, j))
+                launch_matern_points(c, c->stream, x.p(i, j), x.ptr(i, j), x.br, i * x.br, j * x.bc,
                                  x.br, x.bc, xy, xy + n, nu, range, variance, nugget);
     MP_API_END
 }
@@ -802,7 +894,7 @@ mp_status mp_tile_gaussian_nll(mp_ctx ctx, mp_tile cov, const double* host_z, do
     for (;;) {
         if (jit > 0.0)
             for (int64_t d = 0; d < NT; ++d)
-                launch_add_diag(c, s, t.p(d, d), t.ptr(d, d), nb, static_cast<int>(nb), jit);
+                if (t.has(d, d)) launch_add_diag(c, s, t.p(d, d), t.ptr(d, d), nb, static_cast<int>(nb), jit);
         const int64_t inf = tile_chol_inplace(c, t);
         if (inf < 0) break;
         if (jit <= 0.0 || jit * 10.0 > max_jitter)
@@ -813,10 +905,17 @@ mp_status mp_tile_gaussian_nll(mp_ctx ctx, mp_tile cov, const double* host_z, do
             if (t.nslot[q])
                 MP_CUDA(cudaMemcpyAsync(t.slab[q], backup[q], slab_bytes(q), cudaMemcpyDeviceToDevice, s));
     }
-    // forward solve w = L^{-1} z, tile row by tile row
+    // forward solve w = L^{-1} z, tile row by tile row.  Distributed: every
+    // rank accumulates its own tiles' contributions to r (rank 0 starts from
+    // z, the others from 0); segment i is summed over ranks just before the
+    // owner of L_ii solves it, and w_i then travels back to every rank.
+    Dist* D = (t.dist && t.dist->world > 1) ? t.dist : nullptr;
     double* r = static_cast<double*>(c->ensure_scratch((n + 64) * sizeof(double), 3));
     double* dsum = r + n;
-    MP_CUDA(cudaMemcpyAsync(r, host_z, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (D && D->rank != 0)
+        MP_CUDA(cudaMemsetAsync(r, 0, n * sizeof(double), s));
+    else
+        MP_CUDA(cudaMemcpyAsync(r, host_z, n * sizeof(double), cudaMemcpyHostToDevice, s));
     std::vector<TrsvItem> items;
     std::vector<size_t> off(NT * 3 + 1, 0);
     std::vector<int64_t> cnt(NT * 3, 0);
@@ -824,7 +923,7 @@ mp_status mp_tile_gaussian_nll(mp_ctx ctx, mp_tile cov, const double* host_z, do
         for (int q = 0; q < 3; ++q) {
             off[i * 3 + q] = items.size();
             for (int64_t j = i + 1; j < NT; ++j)
-                if (t.p(j, i) == q) items.push_back(TrsvItem{t.ptr(j, i), r + j * nb});
+                if (t.has(j, i) && t.p(j, i) == q) items.push_back(TrsvItem{t.ptr(j, i), r + j * nb});
             cnt[i * 3 + q] = static_cast<int64_t>(items.size() - off[i * 3 + q]);
         }
     TrsvItem* ditems = nullptr;
@@ -840,7 +939,9 @@ mp_status mp_tile_gaussian_nll(mp_ctx ctx, mp_tile cov, const double* host_z, do
                                 cudaMemcpyHostToDevice, s));
     }
     for (int64_t i = 0; i < NT; ++i) {
-        launch_tile_trsv(c, s, t.p(i, i), t.ptr(i, i), nb, static_cast<int>(nb), r + i * nb);
+        if (D) dist_allreduce_sum_f64(D, r + i * nb, nb, s);
+        if (t.has(i, i)) launch_tile_trsv(c, s, t.p(i, i), t.ptr(i, i), nb, static_cast<int>(nb), r + i * nb);
+        if (D) dist_bcast(D, r + i * nb, nb * sizeof(double), dist_owner(i, i, D->P, D->Q), s);
         for (int q = 0; q < 3; ++q)
             if (cnt[i * 3 + q])
                 launch_tile_gemv(c, s, (mp_precision)q, ditems + off[i * 3 + q], cnt[i * 3 + q],
@@ -849,7 +950,8 @@ mp_status mp_tile_gaussian_nll(mp_ctx ctx, mp_tile cov, const double* host_z, do
     launch_square_sum(c, s, r, n, dsum);
     MP_CUDA(cudaMemsetAsync(dsum + 1, 0, sizeof(double), s));
     for (int64_t d = 0; d < NT; ++d)
-        launch_logdiag_sum(c, s, t.p(d, d), t.ptr(d, d), nb, nb, dsum + 1);
+        if (t.has(d, d)) launch_logdiag_sum(c, s, t.p(d, d), t.ptr(d, d), nb, nb, dsum + 1);
+    if (D) dist_allreduce_sum_f64(D, dsum + 1, 1, s);
     double h[2];
     MP_CUDA(cudaMemcpyAsync(h, dsum, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
     MP_CUDA(cudaStreamSynchronize(s));
@@ -867,6 +969,7 @@ mp_status mp_tile_copy(mp_ctx ctx, mp_tile dst, mp_tile src) {
     if (!ctx) fail(MP_INVALID_PARAM, "null context");
     if (d.rows != s.rows || d.cols != s.cols || d.br != s.br || d.bc != s.bc || d.prec != s.prec)
         fail(MP_SHAPE_MISMATCH, "tile copy: grids differ");
+    if (d.slot != s.slot) fail(MP_SHAPE_MISMATCH, "tile copy: tiles distributed differently");
     for (int q = 0; q < 3; ++q)
         if (s.nslot[q])
             MP_CUDA(cudaMemcpyAsync(d.slab[q], s.slab[q],

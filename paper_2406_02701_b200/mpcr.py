@@ -368,8 +368,10 @@ class MPCRTile:
     """
 
     def __init__(self, rows: int, cols: int, rows_per_tile: int, cols_per_tile: int,
-                 values=None, precisions=None, ctx: Context | None = None, _handle=None):
-        self.ctx = ctx or default_context()
+                 values=None, precisions=None, ctx: Context | None = None, _handle=None,
+                 grid: "ProcessGrid | None" = None):
+        self.ctx = ctx or (grid.ctx if grid is not None else default_context())
+        self.grid = grid
         if _handle is not None:
             self.h = _handle
         else:
@@ -381,8 +383,14 @@ class MPCRTile:
                                                                               dtype=object))])
             pcol = np.asfortranarray(pg, dtype=np.int32).ravel(order="F")
             h = C.c_void_p()
-            check(lib().mp_tile_create(self.ctx.h, rows, cols, rows_per_tile, cols_per_tile,
-                                       pcol.ctypes.data_as(C.POINTER(C.c_int)), C.byref(h)))
+            if grid is not None:
+                if rows != cols or rows_per_tile != cols_per_tile:
+                    raise ValueError("distributed MPCRTile: square matrix with square tiles")
+                check(lib().mp_tile_create_dist(self.ctx.h, grid.h, rows, rows_per_tile,
+                                                pcol.ctypes.data_as(C.POINTER(C.c_int)), C.byref(h)))
+            else:
+                check(lib().mp_tile_create(self.ctx.h, rows, cols, rows_per_tile, cols_per_tile,
+                                           pcol.ctypes.data_as(C.POINTER(C.c_int)), C.byref(h)))
             self.h = h
             if values is not None:
                 self.set_values(values)
@@ -413,6 +421,10 @@ class MPCRTile:
         out = np.empty((rows, cols), order="F")
         check(lib().mp_tile_get_values(self.h, out.ctypes.data_as(C.c_void_p)))
         return out
+
+    def owns(self, i: int, j: int) -> bool:
+        """True if tile (i, j) (0-based) is stored by this rank."""
+        return bool(lib().mp_tile_owns(self.h, i, j))
 
     def GetTile(self, rowidx: int, colidx: int) -> MPArray:
         """MPCRTile.GetTile: 1-based, a view of the tile."""
@@ -482,3 +494,63 @@ def tile_trsm(a: MPCRTile, b: MPCRTile, side: str = "L", upper_triangle: bool = 
     s = {"L": Side.Left, "R": Side.Right}[side]
     check(lib().mp_tile_trsm(a.ctx.h, a.h, b.h, int(s), int(upper_triangle), int(transpose),
                              float(alpha)))
+
+
+# ---- multi-GPU: 2D block-cyclic process grid -----------------
+
+DIST_OPS = {1: "potrf", 2: "bcast_diag", 3: "trsm", 4: "bcast_panel", 5: "update"}
+
+
+def dist_owner(i: int, j: int, P: int, Q: int) -> int:
+    """Rank holding tile (i, j) of a P x Q block-cyclic grid."""
+    return int(lib().mp_dist_owner(i, j, P, Q))
+
+
+def dist_schedule(rank: int, P: int, Q: int, tiles: int, precisions=None) -> np.ndarray:
+    """The rank's action list of the distributed tiled Cholesky, as an
+    (count, 6) int32 array of (op, k, i, j, root, precision) rows — the same
+    plan the GPU executor runs (csrc/dist.cpp)."""
+    if precisions is None:
+        precisions = np.full((tiles, tiles), 2)
+    pcol = np.asfortranarray(np.asarray(precisions, dtype=np.int32)).ravel(order="F")
+    cnt = C.c_int64()
+    pp = pcol.ctypes.data_as(C.POINTER(C.c_int))
+    check(lib().mp_dist_schedule(rank, P, Q, tiles, pp, None, 0, C.byref(cnt)))
+    out = np.zeros((cnt.value, 6), dtype=np.int32)
+    check(lib().mp_dist_schedule(rank, P, Q, tiles, pp, out.ctypes.data_as(C.POINTER(C.c_int32)),
+                                 cnt.value, C.byref(cnt)))
+    return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().mp_nccl_unique_id(buf))
+    return buf.raw
+
+
+class ProcessGrid:
+    """P x Q process grid over NCCL (one process per GPU).  Rank 0 makes the
+    id with ``nccl_unique_id()`` and shares it (e.g. torch.distributed
+    broadcast_object_list); world == 1 needs none."""
+
+    def __init__(self, rank: int, world: int, P: int, Q: int, uid: bytes | None = None,
+                 ctx: Context | None = None):
+        self.ctx = ctx or default_context()
+        self.rank, self.world, self.P, self.Q = rank, world, P, Q
+        h = C.c_void_p()
+        check(lib().mp_dist_create(self.ctx.h, rank, world, P, Q, uid, C.byref(h)))
+        self.h = h
+
+    def owner(self, i: int, j: int) -> int:
+        return dist_owner(i, j, self.P, self.Q)
+
+    def close(self):
+        if self.h:
+            lib().mp_dist_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

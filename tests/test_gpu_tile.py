@@ -207,3 +207,30 @@ def test_get_tile_view(ctx):
     np.testing.assert_array_equal(v.to_numpy(), M[4:8, 0:4])
     with pytest.raises(mp.MPError):
         t.GetTile(3, 1)
+
+
+def test_dist_world1_matches_single(ctx, ref):
+    """The distributed executor on a 1 x 1 process grid runs the same plan as
+    the single-GPU path: identical factor, logdet and nll; NCCL resolves."""
+    import paper_2406_02701_b200 as mp
+
+    assert len(mp.nccl_unique_id()) == 128
+    n, nb = 1024, 128
+    side = 32
+    nt = n // nb
+    i, j = np.indices((nt, nt))
+    g = np.where(i == j, 2, np.where(abs(i - j) == 1, 1, 0))
+    grid = mp.ProcessGrid(0, 1, 1, 1, ctx=ctx)
+    a = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+    b = mp.MPCRTile(n, n, nb, nb, None, g, grid=grid)
+    assert b.owns(3, 1) and b.owns(2, 2) and not b.owns(1, 3)
+    for t in (a, b):
+        t.fill_matern(side, 0.5, 0.03, 1.0)
+    mp.tile_chol(a)
+    mp.tile_chol(b)
+    La, Lb = a.to_numpy(), b.to_numpy()
+    assert np.array_equal(La, Lb)
+    assert a.logdet() == b.logdet()
+    want = ref.tile_chol(n, nb, g, ref.grid_matern(side, n, 0.5, 0.03, 1.0, 2))
+    assert np.abs(Lb - want).max() < 1e-2
+
