@@ -46,6 +46,7 @@ struct mp_tile_s {
     void* lists = nullptr;
     size_t lists_bytes = 0;
     TrtriPlan* trtri = nullptr;  // FP64 inverse plan over work (built on first chol)
+    std::vector<cudaEvent_t> events;  // lookahead stream ordering (built on first chol)
 
     int64_t tt() const { return br * bc; }
     mp_precision p(int64_t i, int64_t j) const { return prec[j * tr + i]; }
@@ -56,9 +57,6 @@ struct mp_tile_s {
         return static_cast<char*>(slab[q]) + slot[j * tr + i] * tt() * elem_bytes(q);
     }
     int rank() const { return dist ? dist->rank : 0; }
-    void* panel_ptr(mp_precision q, int64_t i) const {
-        return static_cast<char*>(panel[q]) + i * tt() * elem_bytes(q);
-    }
     ~mp_tile_s() {
         for (int q = 0; q < 3; ++q) {
             if (slab[q]) cudaFree(slab[q]);
@@ -69,6 +67,7 @@ struct mp_tile_s {
         if (work) cudaFree(work);
         if (lists) cudaFree(lists);
         trtri_plan_destroy(trtri);
+        for (cudaEvent_t e : events) cudaEventDestroy(e);
     }
 };
 
@@ -93,15 +92,21 @@ mp_tile_s& T_(mp_tile t) {
 }
 
 void ensure_panels(mp_tile_s& t) {
+    // two panel generations (step parity): the lookahead panel of step k+1 is
+    // produced while the trailing update of step k still reads panel k
     for (int q = 0; q < 3; ++q)
         if (!t.panel[q])
-            MP_CUDA(cudaMalloc(&t.panel[q], static_cast<size_t>(t.tr) * t.tt() * elem_bytes((mp_precision)q)));
+            MP_CUDA(cudaMalloc(&t.panel[q], 2 * static_cast<size_t>(t.tr) * t.tt() * elem_bytes((mp_precision)q)));
     for (auto& p : t.split32)
-        if (!p) MP_CUDA(cudaMalloc(&p, static_cast<size_t>(t.tr) * t.tt() * 4));
+        if (!p) MP_CUDA(cudaMalloc(&p, 2 * static_cast<size_t>(t.tr) * t.tt() * 4));
     if (!t.work) {
         const size_t nn = static_cast<size_t>(t.br) * t.br;
         // FP64 work, FP64 Linv, FP32 work, FP32 LinvS, FP16 LinvH hi + lo, info
         MP_CUDA(cudaMalloc(&t.work, nn * (8 + 8 + 4 + 4 + 2 + 2) + 256));
+    }
+    if (t.events.empty()) {
+        t.events.resize(2 * t.tr + 4);
+        for (auto& e : t.events) MP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
 }
 
@@ -112,17 +117,26 @@ void append(std::vector<char>& buf, const std::vector<V>& v, size_t& off) {
     if (!v.empty()) std::memcpy(buf.data() + off, v.data(), v.size() * sizeof(V));
 }
 
+// Device work lists of one trailing-update part (offsets into the list
+// buffer + counts): tcgen05 FP16, tcgen05 3xTF32, SIMT/DMMA per precision.
+struct UpLists {
+    size_t tc = 0, tc32 = 0, p[3] = {0, 0, 0};
+    int64_t n_tc = 0, n_tc32 = 0, n_p[3] = {0, 0, 0};
+};
+
 struct StepLists {
-    // offsets into the device list buffer and counts
-    size_t trsm_tc = 0, trsm_s = 0, trsm_d = 0, trsm_h_simt = 0;
-    int64_t n_trsm_tc = 0, n_trsm_s = 0, n_trsm_d = 0, n_trsm_h_simt = 0;
+    bool potrf = false;
+    bool need_linv[3] = {false, false, false};
+    size_t trsm_tc = 0, trsm_p[3] = {0, 0, 0};
+    int64_t n_trsm_tc = 0, n_trsm_p[3] = {0, 0, 0};
     size_t wb[3] = {0, 0, 0};
     int64_t n_wb[3] = {0, 0, 0};
     size_t cv[3][3] = {};
     int64_t n_cv[3][3] = {};
-    size_t up_tc = 0, up_h_simt = 0, up_s = 0, up_d = 0, up_tc32 = 0, split32 = 0;
-    int64_t n_up_tc = 0, n_up_h_simt = 0, n_up_s = 0, n_up_d = 0, n_up_tc32 = 0, n_split32 = 0;
-    bool need_linv[3] = {false, false, false};
+    size_t split32 = 0;
+    int64_t n_split32 = 0;
+    UpLists up[2];                            // 0: tile column k+1 (lookahead), 1: the rest
+    std::vector<std::pair<int, int>> bcasts;  // (i, root) panel broadcasts
 };
 
 }  // namespace
@@ -131,27 +145,49 @@ namespace mpcr {
 
 // Tiled Cholesky of an MPCRTile in place.  Returns the global failing column
 // (or -1); the caller maps it to MP_NOT_POSITIVE_DEFINITE.
+//
+// Lookahead (depth 1) on two streams: the critical path — update of tile
+// column k+1 with panel k, then POTRF/TRTRI/TRSM/conversions of panel k+1 —
+// runs on the high-priority stream while the bulk of step k's trailing update
+// runs on the context stream.  Panels alternate between two buffers by step
+// parity.  MPCR_LOOKAHEAD=0 serialises everything on one stream.
 int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     cudaStream_t s = c->stream;
     const int64_t nb = t.br, NT = t.tr, tt = t.tt();
     ensure_panels(t);
     const bool tc_ok = (nb % 8) == 0;  // TMA stride alignment for FP16 tiles
+    static const bool lookahead_env = [] {
+        const char* e = getenv("MPCR_LOOKAHEAD");
+        return !(e && e[0] == '0');
+    }();
+    const bool la = lookahead_env && NT > 1;
+    cudaStream_t sl = la ? c->hi : s;  // critical-path stream
+
+    auto pan = [&](mp_precision q, int64_t i, int64_t k) -> void* {
+        return static_cast<char*>(t.panel[q]) + ((k & 1) * NT + i) * tt * elem_bytes(q);
+    };
+    auto spl = [&](int h, int64_t i, int64_t k) -> void* {
+        return static_cast<char*>(t.split32[h]) + ((k & 1) * NT + i) * tt * 4;
+    };
 
     // ---- host plan: the rank's action list (dist.hpp) turned into grouped
     //      per-step work lists (single GPU: P = Q = 1, no broadcasts) --------
     const int P = t.dist ? t.dist->P : 1, Q = t.dist ? t.dist->Q : 1, rank = t.rank();
     std::vector<int> pgrid(t.prec.begin(), t.prec.end());
     const auto sched = dist_schedule(rank, P, Q, NT, pgrid.data());
+    struct UpAcc {
+        std::vector<TcProblem> tc, tc32;
+        std::vector<TileProblem> p[3];
+    };
     struct StepAcc {
-        bool potrf = false;
-        std::vector<TcProblem> trsm_tc, up_tc, up_tc32;
-        std::vector<TileProblem> trsm_p[3], up_p[3];
+        std::vector<TcProblem> trsm_tc;
+        std::vector<TileProblem> trsm_p[3];
         std::vector<CopyItem> wb[3], cv[3][3];
         std::vector<SplitItem> split32;
-        bool need_linv[3] = {false, false, false};
+        UpAcc up[2];
     };
     std::vector<StepAcc> acc(NT);
-    std::vector<std::vector<std::pair<int, int>>> bcasts(NT);  // (i, root) per step
+    std::vector<StepLists> steps(NT);
     const size_t nn0 = static_cast<size_t>(nb) * nb;
     char* linv_base = static_cast<char*>(t.work);
     const void* linv[3] = {linv_base + nn0 * 24, linv_base + nn0 * 20, linv_base + nn0 * 8};
@@ -165,45 +201,45 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         for (int64_t m = i; m < NT; ++m)  // B operand of (owned) column-i updates
             if (t.has(m, i)) need[t.p(m, i)] = true;
         for (int r = 0; r < 3; ++r)
-            if (need[r] && r != q) A.cv[q][r].push_back(CopyItem{t.panel_ptr(q, i), t.panel_ptr((mp_precision)r, i)});
+            if (need[r] && r != q) A.cv[q][r].push_back(CopyItem{pan(q, i, k), pan((mp_precision)r, i, k)});
         if (tc_ok && need[MP_SINGLE])  // FP32 consumers run 3xTF32 on hi/lo splits
-            A.split32.push_back(SplitItem{t.panel_ptr(MP_SINGLE, i),
-                                          static_cast<char*>(t.split32[0]) + i * tt * 4,
-                                          static_cast<char*>(t.split32[1]) + i * tt * 4});
+            A.split32.push_back(SplitItem{pan(MP_SINGLE, i, k), spl(0, i, k), spl(1, i, k)});
     };
     for (const DistAction& a : sched) {
         StepAcc& A = acc[a.k];
+        StepLists& L = steps[a.k];
         const int64_t k = a.k, i = a.i, j = a.j;
         const mp_precision q = static_cast<mp_precision>(a.prec);
         switch (a.op) {
             case DA_POTRF:
-                A.potrf = true;
+                L.potrf = true;
                 break;
             case DA_TRSM:
-                A.need_linv[q] = true;
+                L.need_linv[q] = true;
                 if (q == MP_HALF && tc_ok)
                     // A = matrix tile (i,k) in the FP16 slab, C = panel16[i]
                     A.trsm_tc.push_back(TcProblem{static_cast<int32_t>(t.slot[k * NT + i]), 0,
                                                   static_cast<int32_t>(i), 0});
                 else
-                    A.trsm_p[q].push_back(TileProblem{t.ptr(i, k), linv[q], t.panel_ptr(q, i), 0, 0});
-                A.wb[q].push_back(CopyItem{t.panel_ptr(q, i), t.ptr(i, k)});
+                    A.trsm_p[q].push_back(TileProblem{t.ptr(i, k), linv[q], pan(q, i, k), 0, 0});
+                A.wb[q].push_back(CopyItem{pan(q, i, k), t.ptr(i, k)});
                 if (P * Q == 1) consumers(k, i, A);
                 break;
             case DA_BCAST_PANEL:
-                bcasts[k].push_back({static_cast<int>(i), a.root});
+                L.bcasts.push_back({static_cast<int>(i), a.root});
                 consumers(k, i, A);
                 break;
             case DA_UPDATE: {
+                UpAcc& U = A.up[j == k + 1 ? 0 : 1];
                 const int32_t lo = (i == j) ? 1 : 0;
                 if (q == MP_HALF && tc_ok)
-                    A.up_tc.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
-                                                static_cast<int32_t>(t.slot[j * NT + i]), lo});
+                    U.tc.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
+                                             static_cast<int32_t>(t.slot[j * NT + i]), lo});
                 else if (q == MP_SINGLE && tc_ok)
-                    A.up_tc32.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
-                                                  static_cast<int32_t>(t.slot[j * NT + i]), lo});
+                    U.tc32.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
+                                               static_cast<int32_t>(t.slot[j * NT + i]), lo});
                 else
-                    A.up_p[q].push_back(TileProblem{t.panel_ptr(q, i), t.panel_ptr(q, j), t.ptr(i, j), lo, 0});
+                    U.p[q].push_back(TileProblem{pan(q, i, k), pan(q, j, k), t.ptr(i, j), lo, 0});
                 break;
             }
             default:
@@ -211,22 +247,14 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         }
     }
     std::vector<char> buf;
-    std::vector<StepLists> steps(NT);
-    std::vector<bool> do_potrf(NT, false);
     for (int64_t k = 0; k < NT; ++k) {
         StepLists& L = steps[k];
         StepAcc& A = acc[k];
-        do_potrf[k] = A.potrf;
-        for (int q = 0; q < 3; ++q) L.need_linv[q] = A.need_linv[q];
         append(buf, A.trsm_tc, L.trsm_tc);
         L.n_trsm_tc = A.trsm_tc.size();
-        append(buf, A.trsm_p[MP_HALF], L.trsm_h_simt);
-        L.n_trsm_h_simt = A.trsm_p[MP_HALF].size();
-        append(buf, A.trsm_p[MP_SINGLE], L.trsm_s);
-        L.n_trsm_s = A.trsm_p[MP_SINGLE].size();
-        append(buf, A.trsm_p[MP_DOUBLE], L.trsm_d);
-        L.n_trsm_d = A.trsm_p[MP_DOUBLE].size();
         for (int q = 0; q < 3; ++q) {
+            append(buf, A.trsm_p[q], L.trsm_p[q]);
+            L.n_trsm_p[q] = A.trsm_p[q].size();
             append(buf, A.wb[q], L.wb[q]);
             L.n_wb[q] = A.wb[q].size();
             for (int r = 0; r < 3; ++r) {
@@ -234,18 +262,18 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 L.n_cv[q][r] = A.cv[q][r].size();
             }
         }
-        append(buf, A.up_tc, L.up_tc);
-        L.n_up_tc = A.up_tc.size();
-        append(buf, A.up_tc32, L.up_tc32);
-        L.n_up_tc32 = A.up_tc32.size();
         append(buf, A.split32, L.split32);
         L.n_split32 = A.split32.size();
-        append(buf, A.up_p[MP_HALF], L.up_h_simt);
-        L.n_up_h_simt = A.up_p[MP_HALF].size();
-        append(buf, A.up_p[MP_SINGLE], L.up_s);
-        L.n_up_s = A.up_p[MP_SINGLE].size();
-        append(buf, A.up_p[MP_DOUBLE], L.up_d);
-        L.n_up_d = A.up_p[MP_DOUBLE].size();
+        for (int w = 0; w < 2; ++w) {
+            append(buf, A.up[w].tc, L.up[w].tc);
+            L.up[w].n_tc = A.up[w].tc.size();
+            append(buf, A.up[w].tc32, L.up[w].tc32);
+            L.up[w].n_tc32 = A.up[w].tc32.size();
+            for (int q = 0; q < 3; ++q) {
+                append(buf, A.up[w].p[q], L.up[w].p[q]);
+                L.up[w].n_p[q] = A.up[w].p[q].size();
+            }
+        }
     }
     // final clean-up lists: upper part of diagonal tiles, strictly-upper tiles
     std::vector<void*> diag_ptrs[3], upper_ptrs[3];
@@ -283,59 +311,58 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     if (!t.trtri) t.trtri = trtri_plan_create(c, s, dwork, nb, linv64, nb, nb);
     TrtriPlan* trtri = t.trtri;
 
-    for (int64_t k = 0; k < NT; ++k) {
+    // ---- panel k: factor A_kk, invert, TRSM the tile column, distribute and
+    //      convert the panel for its consumers ---------------------------------
+    auto panel_phase = [&](int64_t k, cudaStream_t st) {
         const StepLists& L = steps[k];
-        // 1. diagonal factor + FP64 inverse of the stored factor (owner only)
         const mp_precision pk = t.p(k, k);
         void* akk = t.ptr(k, k);
-        if (!do_potrf[k]) {
+        if (!L.potrf) {
             // not the owner: nothing to factor
         } else if (pk == MP_DOUBLE) {
             // POTRF in place, its 64x64 block inverses straight into Linv
-            launch_potrf_lower(c, s, MP_DOUBLE, akk, nb, nb, dinfo, k * nb, linv64, nb);
+            launch_potrf_lower(c, st, MP_DOUBLE, akk, nb, nb, dinfo, k * nb, linv64, nb);
             if (k + 1 < NT) {
-                MP_CUDA(cudaMemcpyAsync(dwork, akk, nn * sizeof(double), cudaMemcpyDeviceToDevice, s));
-                launch_trtri_plan(c, s, trtri, true);
+                MP_CUDA(cudaMemcpyAsync(dwork, akk, nn * sizeof(double), cudaMemcpyDeviceToDevice, st));
+                launch_trtri_plan(c, st, trtri, true);
             }
         } else {
             if (pk == MP_SINGLE) {
-                launch_potrf_lower(c, s, MP_SINGLE, akk, nb, nb, dinfo, k * nb);
+                launch_potrf_lower(c, st, MP_SINGLE, akk, nb, nb, dinfo, k * nb);
             } else {
-                launch_convert(c, s, MP_HALF, akk, nb, MP_SINGLE, swork, nb, nb, nb);
-                launch_potrf_lower(c, s, MP_SINGLE, swork, nb, nb, dinfo, k * nb);
-                launch_convert(c, s, MP_SINGLE, swork, nb, MP_HALF, akk, nb, nb, nb);
+                launch_convert(c, st, MP_HALF, akk, nb, MP_SINGLE, swork, nb, nb, nb);
+                launch_potrf_lower(c, st, MP_SINGLE, swork, nb, nb, dinfo, k * nb);
+                launch_convert(c, st, MP_SINGLE, swork, nb, MP_HALF, akk, nb, nb, nb);
             }
             if (k + 1 < NT) {  // inverse of the stored (rounded) factor, in FP64
-                launch_convert(c, s, pk, akk, nb, MP_DOUBLE, dwork, nb, nb, nb);
-                launch_trtri_plan(c, s, trtri, false);
+                launch_convert(c, st, pk, akk, nb, MP_DOUBLE, dwork, nb, nb, nb);
+                launch_trtri_plan(c, st, trtri, false);
             }
         }
-        if (k + 1 == NT) break;
+        if (k + 1 == NT) return;
         // distributed: the FP64 inverse of L_kk travels from its owner
         if (t.dist && t.dist->world > 1)
-            dist_bcast(t.dist, linv64, nn * sizeof(double), dist_owner(k, k, P, Q), s);
-        // 2. Linv rounded to the panel precisions (the reference rounds U_kk
-        //    to p_ik before trsm: U_kk.converted(p_ik))
-        // FP16 panels apply the inverse as hi + lo FP16 halves accumulated in
-        // one FP32 accumulator: an explicit inverse rounded to FP16 alone has
-        // a backward error ~cond(L_kk) * 2^-11 and loses definiteness where
-        // the reference's substitution does not.
+            dist_bcast(t.dist, linv64, nn * sizeof(double), dist_owner(k, k, P, Q), st);
+        // Linv rounded to the panel precisions (the reference rounds U_kk to
+        // p_ik before trsm: U_kk.converted(p_ik)).  FP16 panels apply the
+        // inverse as hi + lo FP16 halves accumulated in one FP32 accumulator:
+        // an explicit inverse rounded to FP16 alone has a backward error
+        // ~cond(L_kk) * 2^-11 and loses definiteness where the reference's
+        // substitution does not.
         if (L.need_linv[MP_HALF]) {
             if (L.n_trsm_tc)
-                launch_split_f16(c, s, linv64, linvH, linvHlo, static_cast<int64_t>(nn));
+                launch_split_f16(c, st, linv64, linvH, linvHlo, static_cast<int64_t>(nn));
             else
-                launch_convert(c, s, MP_DOUBLE, linv64, nb, MP_HALF, linvH, nb, nb, nb);
+                launch_convert(c, st, MP_DOUBLE, linv64, nb, MP_HALF, linvH, nb, nb, nb);
         }
-        if (L.need_linv[MP_SINGLE]) launch_convert(c, s, MP_DOUBLE, linv64, nb, MP_SINGLE, linvS, nb, nb, nb);
-        // 3. TRSM as GEMM: panel_q[i] = A_ik * Linv_q^T
+        if (L.need_linv[MP_SINGLE]) launch_convert(c, st, MP_DOUBLE, linv64, nb, MP_SINGLE, linvS, nb, nb, nb);
+        // TRSM as GEMM: panel_q[i] = A_ik * Linv_q^T
         if (L.n_trsm_tc) {
             TcGemm g;
             g.pc = MP_HALF;
             g.ta = false;
             g.tb = true;
-            g.m = nb;
-            g.n = nb;
-            g.k = nb;
+            g.m = g.n = g.k = nb;
             g.alpha = 1.0;
             g.beta = 0.0;
             g.A = t.slab[MP_HALF];
@@ -347,54 +374,51 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             g.ldb = nb;
             g.b_tiles = 1;
             g.b_tile_stride = tt;
-            g.C = t.panel[MP_HALF];
+            g.C = pan(MP_HALF, 0, k);
             g.ldc = nb;
             g.c_tiles = NT;
             g.c_tile_stride = tt;
             g.problems = reinterpret_cast<const TcProblem*>(dl + L.trsm_tc);
             g.count = L.n_trsm_tc;
-            launch_tc_gemm(c, s, g);
+            launch_tc_gemm(c, st, g);
         }
-        const struct {
-            int64_t n;
-            size_t off;
-            mp_precision q;
-        } tr_simt[3] = {{L.n_trsm_h_simt, L.trsm_h_simt, MP_HALF},
-                        {L.n_trsm_s, L.trsm_s, MP_SINGLE},
-                        {L.n_trsm_d, L.trsm_d, MP_DOUBLE}};
-        for (const auto& e : tr_simt)
-            if (e.n) {
-                GroupedGemm g{e.q, e.q, true, nb, nb, nb, nb, nb, nb, 1.0, 0.0,
-                              reinterpret_cast<const TileProblem*>(dl + e.off), e.n};
-                launch_grouped_gemm(c, s, g);
+        for (int q = 0; q < 3; ++q)
+            if (L.n_trsm_p[q]) {
+                GroupedGemm g{(mp_precision)q, (mp_precision)q, true, nb, nb, nb, nb, nb, nb, 1.0, 0.0,
+                              reinterpret_cast<const TileProblem*>(dl + L.trsm_p[q]), L.n_trsm_p[q]};
+                launch_grouped_gemm(c, st, g);
             }
         // write the factor back into the tiles
         for (int q = 0; q < 3; ++q)
             if (L.n_wb[q])
-                launch_batched_convert(c, s, (mp_precision)q, (mp_precision)q,
+                launch_batched_convert(c, st, (mp_precision)q, (mp_precision)q,
                                        reinterpret_cast<const CopyItem*>(dl + L.wb[q]), L.n_wb[q], tt);
         // distributed: every panel tile travels from its owner to all ranks
-        if (!bcasts[k].empty()) {
+        if (!L.bcasts.empty()) {
             dist_group_start(t.dist);
-            for (const auto& br : bcasts[k]) {
+            for (const auto& br : L.bcasts) {
                 const mp_precision q = t.p(br.first, k);
-                dist_bcast(t.dist, t.panel_ptr(q, br.first), tt * elem_bytes(q), br.second, s);
+                dist_bcast(t.dist, pan(q, br.first, k), tt * elem_bytes(q), br.second, st);
             }
             dist_group_end(t.dist);
         }
-        // 4. consumer-precision copies of the panel
+        // consumer-precision copies of the panel
         for (int q = 0; q < 3; ++q)
             for (int r = 0; r < 3; ++r)
                 if (L.n_cv[q][r])
-                    launch_batched_convert(c, s, (mp_precision)q, (mp_precision)r,
+                    launch_batched_convert(c, st, (mp_precision)q, (mp_precision)r,
                                            reinterpret_cast<const CopyItem*>(dl + L.cv[q][r]),
                                            L.n_cv[q][r], tt);
         // hi/lo TF32 splits of the FP32 panel, stored transposed (K-major)
         if (L.n_split32)
-            launch_batched_split_tf32_t(c, s, reinterpret_cast<const SplitItem*>(dl + L.split32),
+            launch_batched_split_tf32_t(c, st, reinterpret_cast<const SplitItem*>(dl + L.split32),
                                         L.n_split32, nb);
-        // 5. trailing update
-        if (L.n_up_tc32) {  // FP32 tiles: 3xTF32 on tcgen05, C -= (L_ik^T)^T (L_jk^T)
+    };
+
+    // ---- trailing update A_ij -= L_ik L_jk^T of one part of step k ------------
+    auto update_phase = [&](int64_t k, int part, cudaStream_t st) {
+        const UpLists& U = steps[k].up[part];
+        if (U.n_tc32) {  // FP32 tiles: 3xTF32 on tcgen05, C -= (L_ik^T)^T (L_jk^T)
             TcGemm g;
             g.kind = 1;
             g.pc = MP_SINGLE;
@@ -403,63 +427,72 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             g.m = g.n = g.k = nb;
             g.alpha = -1.0;
             g.beta = 1.0;
-            g.A = t.split32[0];
-            g.A2 = t.split32[1];
-            g.lda = nb;
-            g.a_tiles = NT;
-            g.a_tile_stride = tt;
-            g.B = t.split32[0];
-            g.B2 = t.split32[1];
-            g.ldb = nb;
-            g.b_tiles = NT;
-            g.b_tile_stride = tt;
+            g.A = g.B = spl(0, 0, k);
+            g.A2 = g.B2 = spl(1, 0, k);
+            g.lda = g.ldb = nb;
+            g.a_tiles = g.b_tiles = NT;
+            g.a_tile_stride = g.b_tile_stride = tt;
             g.C = t.slab[MP_SINGLE];
             g.ldc = nb;
             g.c_tiles = t.nslot[MP_SINGLE];
             g.c_tile_stride = tt;
-            g.problems = reinterpret_cast<const TcProblem*>(dl + L.up_tc32);
-            g.count = L.n_up_tc32;
-            launch_tc_gemm(c, s, g);
+            g.problems = reinterpret_cast<const TcProblem*>(dl + U.tc32);
+            g.count = U.n_tc32;
+            launch_tc_gemm(c, st, g);
         }
-        if (L.n_up_tc) {
+        if (U.n_tc) {
             TcGemm g;
             g.pc = MP_HALF;
             g.ta = false;
             g.tb = true;
-            g.m = nb;
-            g.n = nb;
-            g.k = nb;
+            g.m = g.n = g.k = nb;
             g.alpha = -1.0;
             g.beta = 1.0;
-            g.A = t.panel[MP_HALF];
-            g.lda = nb;
-            g.a_tiles = NT;
-            g.a_tile_stride = tt;
-            g.B = t.panel[MP_HALF];
-            g.ldb = nb;
-            g.b_tiles = NT;
-            g.b_tile_stride = tt;
+            g.A = g.B = pan(MP_HALF, 0, k);
+            g.lda = g.ldb = nb;
+            g.a_tiles = g.b_tiles = NT;
+            g.a_tile_stride = g.b_tile_stride = tt;
             g.C = t.slab[MP_HALF];
             g.ldc = nb;
             g.c_tiles = t.nslot[MP_HALF];
             g.c_tile_stride = tt;
-            g.problems = reinterpret_cast<const TcProblem*>(dl + L.up_tc);
-            g.count = L.n_up_tc;
-            launch_tc_gemm(c, s, g);
+            g.problems = reinterpret_cast<const TcProblem*>(dl + U.tc);
+            g.count = U.n_tc;
+            launch_tc_gemm(c, st, g);
         }
-        const struct {
-            int64_t n;
-            size_t off;
-            mp_precision q;
-        } up_simt[3] = {{L.n_up_h_simt, L.up_h_simt, MP_HALF},
-                        {L.n_up_s, L.up_s, MP_SINGLE},
-                        {L.n_up_d, L.up_d, MP_DOUBLE}};
-        for (const auto& e : up_simt)
-            if (e.n) {
-                GroupedGemm g{e.q, e.q, true, nb, nb, nb, nb, nb, nb, -1.0, 1.0,
-                              reinterpret_cast<const TileProblem*>(dl + e.off), e.n};
-                launch_grouped_gemm(c, s, g);
+        for (int q = 0; q < 3; ++q)
+            if (U.n_p[q]) {
+                GroupedGemm g{(mp_precision)q, (mp_precision)q, true, nb, nb, nb, nb, nb, nb, -1.0, 1.0,
+                              reinterpret_cast<const TileProblem*>(dl + U.p[q]), U.n_p[q]};
+                launch_grouped_gemm(c, st, g);
             }
+    };
+
+    // ---- issue: panel k+1 (column-(k+1) update first) on the critical-path
+    //      stream overlaps the rest of step k's update on the main stream ------
+    cudaEvent_t* ev_panel = t.events.data();       // NT
+    cudaEvent_t* ev_rest = t.events.data() + NT;   // NT
+    cudaEvent_t ev_join = t.events[2 * NT + 1];
+    if (la) {
+        MP_CUDA(cudaEventRecord(ev_join, s));
+        MP_CUDA(cudaStreamWaitEvent(sl, ev_join, 0));
+    }
+    panel_phase(0, sl);
+    if (la) MP_CUDA(cudaEventRecord(ev_panel[0], sl));
+    for (int64_t k = 0; k < NT; ++k) {
+        if (la) MP_CUDA(cudaStreamWaitEvent(s, ev_panel[k], 0));
+        update_phase(k, 1, s);
+        if (la) MP_CUDA(cudaEventRecord(ev_rest[k], s));
+        if (k + 1 < NT) {
+            if (la && k >= 1) MP_CUDA(cudaStreamWaitEvent(sl, ev_rest[k - 1], 0));
+            update_phase(k, 0, sl);
+            panel_phase(k + 1, sl);
+            if (la) MP_CUDA(cudaEventRecord(ev_panel[k + 1], sl));
+        }
+    }
+    if (la) {
+        MP_CUDA(cudaEventRecord(ev_join, sl));
+        MP_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
     }
     // ---- zero everything above the diagonal (lower L output) ------------------
     for (int q = 0; q < 3; ++q) {
