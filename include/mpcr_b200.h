@@ -93,6 +93,11 @@ typedef enum {
 mp_status mp_prof_enable(mp_ctx ctx, int enable);
 mp_status mp_prof_reset(mp_ctx ctx);
 mp_status mp_prof_query(mp_ctx ctx, int cls, double* ms, int64_t* launches, double* work);
+/* Timeline capture (profiling must be enabled): every timed launch's start
+ * and end in ms relative to the moment tracing was enabled, with its stream
+ * (0 = context stream, 1 = critical-path stream); dumped as CSV. */
+mp_status mp_prof_trace(mp_ctx ctx, int enable);
+mp_status mp_prof_trace_dump(mp_ctx ctx, const char* path);
 /* Number of this library's kernels launched since context creation. */
 mp_status mp_launch_count(mp_ctx ctx, int64_t* launches);
 

@@ -2,6 +2,7 @@
 // points (include/mpcr_b200.h).  Argument checks mirror the reference's
 // exception behaviour (array.cpp, linalg.cpp) and run before any device work.
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -52,7 +53,7 @@ ProfScope::~ProfScope() {
         ctx->prof.pool.pop_back();
     }
     if (cudaEventRecord(b, s) != cudaSuccess) return;
-    ctx->prof.pending.push_back({a, b, cls, work});
+    ctx->prof.pending.push_back({a, b, cls, work, s});
     if (ctx->prof.pending.size() > 8192) prof_collect(ctx, false);
 }
 
@@ -69,6 +70,12 @@ void prof_collect(Ctx* ctx, bool blocking) {
         ctx->prof.ms[r.cls] += ms;
         ctx->prof.launches[r.cls] += 1;
         ctx->prof.work[r.cls] += r.work;
+        if (ctx->prof.trace && ctx->prof.base) {
+            float t0 = 0.f, t1 = 0.f;
+            MP_CUDA(cudaEventElapsedTime(&t0, ctx->prof.base, r.a));
+            MP_CUDA(cudaEventElapsedTime(&t1, ctx->prof.base, r.b));
+            ctx->prof.spans.push_back({r.cls, r.s == ctx->hi ? 1 : r.s == ctx->hi2 ? 2 : 0, t0, t1});
+        }
         ctx->prof.pool.push_back(r.a);
         ctx->prof.pool.push_back(r.b);
     }
@@ -202,6 +209,7 @@ mp_status mp_ctx_create(int device, mp_ctx* out) {
     int lo = 0, hi = 0;
     MP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     MP_CUDA(cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, hi));
+    MP_CUDA(cudaStreamCreateWithPriority(&c->hi2, cudaStreamNonBlocking, hi));
     for (auto& s : c->aux) MP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     *out = c;
     MP_API_END
@@ -221,6 +229,7 @@ mp_status mp_ctx_destroy(mp_ctx ctx) {
         if (p) cudaFree(p);
     for (auto& s : ctx->aux) cudaStreamDestroy(s);
     cudaStreamDestroy(ctx->hi);
+    cudaStreamDestroy(ctx->hi2);
     cudaStreamDestroy(ctx->own_stream);
     delete ctx;
     MP_API_END
@@ -274,6 +283,31 @@ mp_status mp_prof_query(mp_ctx ctx, int cls, double* ms, int64_t* launches, doub
     if (ms) *ms = c->prof.ms[cls];
     if (launches) *launches = c->prof.launches[cls];
     if (work) *work = c->prof.work[cls];
+    MP_API_END
+}
+
+mp_status mp_prof_trace(mp_ctx ctx, int enable) {
+    MP_API_BEGIN
+    Ctx* c = C_(ctx);
+    prof_collect(c);
+    c->prof.spans.clear();
+    c->prof.trace = enable != 0;
+    if (enable) {
+        if (!c->prof.base) MP_CUDA(cudaEventCreate(&c->prof.base));
+        MP_CUDA(cudaEventRecord(c->prof.base, c->stream));
+    }
+    MP_API_END
+}
+
+mp_status mp_prof_trace_dump(mp_ctx ctx, const char* path) {
+    MP_API_BEGIN
+    Ctx* c = C_(ctx);
+    prof_collect(c);
+    FILE* f = std::fopen(path, "w");
+    if (!f) fail(MP_IO_ERROR, std::string("cannot open ") + path);
+    std::fprintf(f, "cls,stream,start_ms,end_ms\n");
+    for (const auto& sp : c->prof.spans) std::fprintf(f, "%d,%d,%.4f,%.4f\n", sp.cls, sp.stream, sp.t0, sp.t1);
+    std::fclose(f);
     MP_API_END
 }
 

@@ -22,6 +22,7 @@
 // A^T K-major; op(B) = B is K-major, B^T MN-major.  All three matrices are
 // addressed by 3-D TMA maps [tile][col][row], so a grouped launch can take any
 // tiles of a slab by index.
+#include <algorithm>
 #include <cuda.h>
 
 #include <cstring>
@@ -350,15 +351,16 @@ void make_op_map(CUtensorMap* map, int kind, const void* base, uint64_t d0, uint
 }
 
 template <int KIND, bool A_MN, bool B_MN, typename TC>
-void launch_kernel(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total) {
+void launch_kernel(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total, int tiles_per_cta) {
     auto kern = gemm_tc_kernel<KIND, A_MN, B_MN, TC>;
     static bool configured = false;
     if (!configured) {
         MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
         configured = true;
     }
-    int grid = static_cast<int>(total < ctx->sm_count ? total : ctx->sm_count);
-    if (grid < 1) grid = 1;
+    int64_t g = total < ctx->sm_count ? total : ctx->sm_count;
+    if (tiles_per_cta > 0) g = std::max<int64_t>(g, (total + tiles_per_cta - 1) / tiles_per_cta);
+    int grid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(g, 1), 1 << 30));
     kern<<<grid, 256, SMEM_BYTES, s>>>(p);
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());
@@ -436,15 +438,15 @@ void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
     ProfScope ps(ctx, kind == 0 ? MP_PROF_GEMM_F16 : MP_PROF_GEMM_F32, s,
                  2.0 * static_cast<double>(g.m) * g.n * g.k * p.nprob *
                      (g.lower_only ? 0.5 : 1.0));
-#define MP_TC(AM, BMJ)                                                            \
-    if (a_mn == AM && b_mn == BMJ) {                                              \
-        if (kind == 1)                                                            \
-            launch_kernel<1, AM, BMJ, float>(ctx, s, p, total);                   \
-        else if (half_c)                                                          \
-            launch_kernel<0, AM, BMJ, uint16_t>(ctx, s, p, total);                \
-        else                                                                      \
-            launch_kernel<0, AM, BMJ, float>(ctx, s, p, total);                   \
-        return;                                                                   \
+#define MP_TC(AM, BMJ)                                                                  \
+    if (a_mn == AM && b_mn == BMJ) {                                                    \
+        if (kind == 1)                                                                  \
+            launch_kernel<1, AM, BMJ, float>(ctx, s, p, total, g.tiles_per_cta);        \
+        else if (half_c)                                                                \
+            launch_kernel<0, AM, BMJ, uint16_t>(ctx, s, p, total, g.tiles_per_cta);     \
+        else                                                                            \
+            launch_kernel<0, AM, BMJ, float>(ctx, s, p, total, g.tiles_per_cta);        \
+        return;                                                                         \
     }
     MP_TC(true, true)
     MP_TC(true, false)

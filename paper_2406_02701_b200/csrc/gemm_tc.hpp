@@ -41,6 +41,10 @@ struct TcGemm {
     // (A2/B2 share the layout, tiles and strides of A/B).
     const void* A2 = nullptr;
     const void* B2 = nullptr;
+    // 0: fully persistent (one CTA per SM).  > 0: at most this many output
+    // tiles per CTA, so SMs are handed back at that granularity and kernels
+    // of a higher-priority stream (the Cholesky critical path) get in.
+    int tiles_per_cta = 0;
 };
 
 bool tc_gemm_supported(const TcGemm& g);

@@ -50,8 +50,17 @@ struct Prof {
         cudaEvent_t a, b;
         int cls;
         double work;
+        cudaStream_t s;
     };
     std::vector<Rec> pending;
+    // optional timeline (mp_prof_trace): per-launch start/end relative to base
+    bool trace = false;
+    cudaEvent_t base = nullptr;
+    struct Span {
+        int cls, stream;
+        float t0, t1;
+    };
+    std::vector<Span> spans;
     std::vector<cudaEvent_t> pool;
     double ms[MP_PROF_NUM_CLASSES] = {};
     int64_t launches[MP_PROF_NUM_CLASSES] = {};
@@ -65,6 +74,7 @@ struct Ctx {
     cudaStream_t stream = nullptr;   // current (own or external)
     cudaStream_t aux[4] = {};        // scheduler side streams
     cudaStream_t hi = nullptr;       // high-priority critical-path stream
+    cudaStream_t hi2 = nullptr;      // second high-priority stream (lookahead side work)
     int64_t launches = 0;            // kernels launched by this library
     Prof prof;
     // Scratch device memory (grown on demand, freed with the context).

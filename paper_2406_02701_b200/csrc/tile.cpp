@@ -105,7 +105,7 @@ void ensure_panels(mp_tile_s& t) {
         MP_CUDA(cudaMalloc(&t.work, nn * (8 + 8 + 4 + 4 + 2 + 2) + 256));
     }
     if (t.events.empty()) {
-        t.events.resize(2 * t.tr + 4);
+        t.events.resize(3 * t.tr + 4);
         for (auto& e : t.events) MP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
 }
@@ -135,7 +135,7 @@ struct StepLists {
     int64_t n_cv[3][3] = {};
     size_t split32 = 0;
     int64_t n_split32 = 0;
-    UpLists up[2];                            // 0: tile column k+1 (lookahead), 1: the rest
+    UpLists up[3];  // 0: tile column k+1 below the diagonal, 1: the rest, 2: tile (k+1, k+1)
     std::vector<std::pair<int, int>> bcasts;  // (i, root) panel broadcasts
 };
 
@@ -184,7 +184,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         std::vector<TileProblem> trsm_p[3];
         std::vector<CopyItem> wb[3], cv[3][3];
         std::vector<SplitItem> split32;
-        UpAcc up[2];
+        UpAcc up[3];
     };
     std::vector<StepAcc> acc(NT);
     std::vector<StepLists> steps(NT);
@@ -230,7 +230,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 consumers(k, i, A);
                 break;
             case DA_UPDATE: {
-                UpAcc& U = A.up[j == k + 1 ? 0 : 1];
+                UpAcc& U = A.up[j != k + 1 ? 1 : i == j ? 2 : 0];
                 const int32_t lo = (i == j) ? 1 : 0;
                 if (q == MP_HALF && tc_ok)
                     U.tc.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
@@ -264,7 +264,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         }
         append(buf, A.split32, L.split32);
         L.n_split32 = A.split32.size();
-        for (int w = 0; w < 2; ++w) {
+        for (int w = 0; w < 3; ++w) {
             append(buf, A.up[w].tc, L.up[w].tc);
             L.up[w].n_tc = A.up[w].tc.size();
             append(buf, A.up[w].tc32, L.up[w].tc32);
@@ -313,7 +313,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
 
     // ---- panel k: factor A_kk, invert, TRSM the tile column, distribute and
     //      convert the panel for its consumers ---------------------------------
-    auto panel_phase = [&](int64_t k, cudaStream_t st) {
+    auto panel_phase = [&](int64_t k, cudaStream_t st, cudaEvent_t before_trsm) {
         const StepLists& L = steps[k];
         const mp_precision pk = t.p(k, k);
         void* akk = t.ptr(k, k);
@@ -356,7 +356,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 launch_convert(c, st, MP_DOUBLE, linv64, nb, MP_HALF, linvH, nb, nb, nb);
         }
         if (L.need_linv[MP_SINGLE]) launch_convert(c, st, MP_DOUBLE, linv64, nb, MP_SINGLE, linvS, nb, nb, nb);
-        // TRSM as GEMM: panel_q[i] = A_ik * Linv_q^T
+        // TRSM as GEMM: panel_q[i] = A_ik * Linv_q^T (tile column k complete)
+        if (before_trsm) MP_CUDA(cudaStreamWaitEvent(st, before_trsm, 0));
         if (L.n_trsm_tc) {
             TcGemm g;
             g.pc = MP_HALF;
@@ -382,12 +383,21 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             g.count = L.n_trsm_tc;
             launch_tc_gemm(c, st, g);
         }
-        for (int q = 0; q < 3; ++q)
-            if (L.n_trsm_p[q]) {
-                GroupedGemm g{(mp_precision)q, (mp_precision)q, true, nb, nb, nb, nb, nb, nb, 1.0, 0.0,
-                              reinterpret_cast<const TileProblem*>(dl + L.trsm_p[q]), L.n_trsm_p[q]};
-                launch_grouped_gemm(c, st, g);
+        for (int q = 0; q < 3; ++q) {
+            if (!L.n_trsm_p[q]) continue;
+            if (q == MP_SINGLE && tc_ok) {
+                // the few FP32 panel tiles: 3xTF32 tcgen05 GEMM per tile
+                for (const TileProblem& pr : acc[k].trsm_p[q]) {
+                    GemmDesc g{MP_SINGLE, MP_SINGLE, MP_SINGLE, false, true, nb, nb, nb, 1.0, 0.0,
+                               pr.A, nb, pr.B, nb, pr.C, nb};
+                    launch_gemm(c, st, g);
+                }
+                continue;
             }
+            GroupedGemm g{(mp_precision)q, (mp_precision)q, true, nb, nb, nb, nb, nb, nb, 1.0, 0.0,
+                          reinterpret_cast<const TileProblem*>(dl + L.trsm_p[q]), L.n_trsm_p[q]};
+            launch_grouped_gemm(c, st, g);
+        }
         // write the factor back into the tiles
         for (int q = 0; q < 3; ++q)
             if (L.n_wb[q])
@@ -416,7 +426,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     };
 
     // ---- trailing update A_ij -= L_ik L_jk^T of one part of step k ------------
-    auto update_phase = [&](int64_t k, int part, cudaStream_t st) {
+    auto update_phase = [&](int64_t k, int part, cudaStream_t st, int tiles_per_cta) {
         const UpLists& U = steps[k].up[part];
         if (U.n_tc32) {  // FP32 tiles: 3xTF32 on tcgen05, C -= (L_ik^T)^T (L_jk^T)
             TcGemm g;
@@ -438,6 +448,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             g.c_tile_stride = tt;
             g.problems = reinterpret_cast<const TcProblem*>(dl + U.tc32);
             g.count = U.n_tc32;
+            g.tiles_per_cta = tiles_per_cta;
             launch_tc_gemm(c, st, g);
         }
         if (U.n_tc) {
@@ -458,6 +469,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             g.c_tile_stride = tt;
             g.problems = reinterpret_cast<const TcProblem*>(dl + U.tc);
             g.count = U.n_tc;
+            g.tiles_per_cta = tiles_per_cta;
             launch_tc_gemm(c, st, g);
         }
         for (int q = 0; q < 3; ++q)
@@ -468,31 +480,52 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             }
     };
 
-    // ---- issue: panel k+1 (column-(k+1) update first) on the critical-path
-    //      stream overlaps the rest of step k's update on the main stream ------
-    cudaEvent_t* ev_panel = t.events.data();       // NT
-    cudaEvent_t* ev_rest = t.events.data() + NT;   // NT
-    cudaEvent_t ev_join = t.events[2 * NT + 1];
+    // ---- issue.  Per step k, three streams:
+    //   s   : wait panel k; update of everything but tile column k+1 (bulk)
+    //   sl2 : wait panel k and bulk k-1; update of column k+1 below the diagonal
+    //   sl  : wait bulk k-1; SYRK of A_{k+1,k+1}; POTRF + TRTRI of panel k+1;
+    //         wait sl2; TRSM + conversions of panel k+1
+    //   The chain POTRF -> TRSM -> SYRK -> POTRF is the critical path; the
+    //   bulk GEMMs hand SMs back every few tiles so it is never starved.
+    static const int tpc_env = [] {
+        const char* e = getenv("MPCR_TILES_PER_CTA");
+        return e ? atoi(e) : 4;
+    }();
+    const int bulk_tpc = la ? tpc_env : 0;
+    cudaStream_t sl2 = la ? c->hi2 : s;
+    cudaEvent_t* ev_panel = t.events.data();          // NT
+    cudaEvent_t* ev_rest = t.events.data() + NT;      // NT
+    cudaEvent_t* ev_next = t.events.data() + 2 * NT;  // NT
+    cudaEvent_t ev_join = t.events[3 * NT + 1], ev_join2 = t.events[3 * NT + 2];
     if (la) {
         MP_CUDA(cudaEventRecord(ev_join, s));
         MP_CUDA(cudaStreamWaitEvent(sl, ev_join, 0));
+        MP_CUDA(cudaStreamWaitEvent(sl2, ev_join, 0));
     }
-    panel_phase(0, sl);
+    panel_phase(0, sl, nullptr);
     if (la) MP_CUDA(cudaEventRecord(ev_panel[0], sl));
     for (int64_t k = 0; k < NT; ++k) {
         if (la) MP_CUDA(cudaStreamWaitEvent(s, ev_panel[k], 0));
-        update_phase(k, 1, s);
+        update_phase(k, 1, s, bulk_tpc);
         if (la) MP_CUDA(cudaEventRecord(ev_rest[k], s));
         if (k + 1 < NT) {
+            if (la) {
+                MP_CUDA(cudaStreamWaitEvent(sl2, ev_panel[k], 0));
+                if (k >= 1) MP_CUDA(cudaStreamWaitEvent(sl2, ev_rest[k - 1], 0));
+            }
+            update_phase(k, 0, sl2, 0);
+            if (la) MP_CUDA(cudaEventRecord(ev_next[k], sl2));
             if (la && k >= 1) MP_CUDA(cudaStreamWaitEvent(sl, ev_rest[k - 1], 0));
-            update_phase(k, 0, sl);
-            panel_phase(k + 1, sl);
+            update_phase(k, 2, sl, 0);
+            panel_phase(k + 1, sl, la ? ev_next[k] : nullptr);
             if (la) MP_CUDA(cudaEventRecord(ev_panel[k + 1], sl));
         }
     }
     if (la) {
         MP_CUDA(cudaEventRecord(ev_join, sl));
+        MP_CUDA(cudaEventRecord(ev_join2, sl2));
         MP_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+        MP_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));
     }
     // ---- zero everything above the diagonal (lower L output) ------------------
     for (int q = 0; q < 3; ++q) {

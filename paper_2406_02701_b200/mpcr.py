@@ -105,6 +105,13 @@ class Context:
     def prof_reset(self):
         check(lib().mp_prof_reset(self.h))
 
+    def prof_trace(self, enable: bool = True):
+        """Record a per-launch timeline (needs prof_enable)."""
+        check(lib().mp_prof_trace(self.h, int(enable)))
+
+    def prof_trace_dump(self, path: str):
+        check(lib().mp_prof_trace_dump(self.h, path.encode()))
+
     def prof_query(self, cls: int):
         ms, n, w = C.c_double(), C.c_int64(), C.c_double()
         check(lib().mp_prof_query(self.h, cls, C.byref(ms), C.byref(n), C.byref(w)))
