@@ -95,9 +95,9 @@ void launch_gemm(Ctx* ctx, cudaStream_t s, const GemmDesc& g) {
 
 void launch_grouped_gemm(Ctx* ctx, cudaStream_t s, const GroupedGemm& g) {
     if (g.count == 0) return;
-    if (g.pab == MP_DOUBLE && g.pc == MP_DOUBLE) {
+    if (g.pc == MP_DOUBLE) {  // FP64 output: DMMA, narrow operands widened on load
         DmmaArgs d{false, g.tb, g.m, g.n, g.k, g.alpha, g.beta, nullptr, g.lda,
-                   nullptr, g.ldb, nullptr, g.ldc, false, g.problems};
+                   nullptr, g.ldb, nullptr, g.ldc, false, g.problems, g.pab};
         ProfScope ps(ctx, MP_PROF_GEMM_F64, s, 2.0 * g.m * g.n * g.k * g.count);
         launch_dmma_gemm(ctx, s, d, g.count);
         return;

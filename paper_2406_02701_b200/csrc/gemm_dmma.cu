@@ -7,11 +7,16 @@
 //
 // CTA tile 128x128, K slab 16, 3-stage cp.async ring in shared memory;
 // 16 warps as 4 (m) x 4 (n), warp tile 32x32 = 2 x 4 fragments of 16x8
-// (32 FP64 accumulators per thread, 4 warps per scheduler).  Shared layouts follow global
+// (32 FP64 accumulators per thread, 4 warps per scheduler).  Launches that
+// would not fill the machine with 128x128 tiles (one SYRK tile on the
+// Cholesky critical path, the TRTRI levels) use a 64x64 / 4-warp variant,
+// several CTAs per SM.  Shared layouts follow global
 // contiguity so every cp.async is 16 bytes; the padded strides make the
 // fragment reads conflict-free (2 wavefronts per 256-byte warp load).
 // blockIdx.z indexes the problem of a grouped launch; lower_only skips CTA
 // tiles strictly above the diagonal and masks the rest (SYRK).
+#include <type_traits>
+
 #include "gemm_dmma.hpp"
 #include "device.cuh"
 #include "internal.hpp"
@@ -19,11 +24,15 @@
 namespace mpcr {
 namespace {
 
-constexpr int BMd = 128, BNd = 128, BKd = 16, NST = 3, NTHR = 512;
-constexpr int SM_ = BMd + 8;  // stride (doubles) of MN-contiguous slabs  [k][mn]
+constexpr int BKd = 16, NST = 3;
 constexpr int SK_ = BKd + 4;  // stride (doubles) of K-contiguous slabs   [mn][k]
-constexpr int SLAB = BMd * SK_ > BKd * SM_ ? BMd * SK_ : BKd * SM_;  // doubles per operand stage
-constexpr int SMEM_D = NST * 2 * SLAB * 8;
+template <int BT>
+struct DCfg {
+    static constexpr int BM = BT, NTHR = BT * BT / 32;  // warp tile 32x32
+    static constexpr int SM_ = BT + 8;                   // stride of MN-contiguous slabs [k][mn]
+    static constexpr int SLAB = BT * SK_ > BKd * SM_ ? BT * SK_ : BKd * SM_;  // doubles per operand stage
+    static constexpr int SMEM = NST * 2 * SLAB * 8;
+};
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
@@ -50,16 +59,19 @@ __device__ __forceinline__ void dmma_k8(double (&d)[4], const double (&a)[4], co
 // Load one K slab [k0, k0+16) of op(X) rows [r0, r0+128) into smem.
 //   mn_contig: X stored with the M/N index contiguous (ld between k) -> [k][mn]
 //   else     : K contiguous (ld between m/n)                           -> [mn][k]
+template <int BT>
 __device__ __forceinline__ void load_slab(double* sm, const double* X, int64_t ldx, bool mn_contig,
                                           int64_t r0, int64_t rmax, int64_t k0, int64_t kmax,
                                           bool vec) {
+    using CF = DCfg<BT>;
+    constexpr int NTHR = CF::NTHR, SM_ = CF::SM_, CH = BT * BKd / 2;  // 16-byte chunks
     const int t = threadIdx.x;
     if (mn_contig) {
-        // 16 k-rows x 128 mn = 1024 x 16B chunks (2 doubles)
+        // 16 k-rows x BT mn
 #pragma unroll
-        for (int q = 0; q < 1024 / NTHR; ++q) {
+        for (int q = 0; q < CH / NTHR; ++q) {
             const int c = t + q * NTHR;
-            const int kk = c / 64, mm = (c % 64) * 2;
+            const int kk = c / (BT / 2), mm = (c % (BT / 2)) * 2;
             const int64_t gk = k0 + kk, gm = r0 + mm;
             double* dst = sm + kk * SM_ + mm;
             if (vec) {
@@ -73,9 +85,9 @@ __device__ __forceinline__ void load_slab(double* sm, const double* X, int64_t l
             }
         }
     } else {
-        // 128 mn rows x 16 k = 1024 x 16B chunks
+        // BT mn rows x 16 k
 #pragma unroll
-        for (int q = 0; q < 1024 / NTHR; ++q) {
+        for (int q = 0; q < CH / NTHR; ++q) {
             const int c = t + q * NTHR;
             const int mm = c / 8, kk = (c % 8) * 2;
             const int64_t gm = r0 + mm, gk = k0 + kk;
@@ -93,30 +105,106 @@ __device__ __forceinline__ void load_slab(double* sm, const double* X, int64_t l
     }
 }
 
+// Narrow-storage operands (FP16 bits / FP32) are widened to FP64 on the way
+// into shared memory (exact), so FP16/FP32 panel tiles feed the FP64 SYRK
+// without a converted copy in HBM.  Register-staged: the next slab's global
+// loads are in flight while the current slab is multiplied.
+template <typename TI>
+struct Stage4 {
+    TI v[4];
+};
+__device__ __forceinline__ double widen(uint16_t h) { return h2d(h); }
+__device__ __forceinline__ double widen(float f) { return static_cast<double>(f); }
+
+template <int BT, typename TI>
+struct NarrowSlab {
+    static constexpr int NTHR = DCfg<BT>::NTHR, SM_ = DCfg<BT>::SM_;
+    static constexpr int CH = BT * BKd / 4;  // 4-element chunks per slab
+    static constexpr int PER = CH / NTHR;     // chunks per thread
+    Stage4<TI> r[PER];
+
+    __device__ __forceinline__ void load(const TI* X, int64_t ldx, bool mn_contig, int64_t r0,
+                                         int64_t rmax, int64_t k0, int64_t kmax, bool vec) {
+        const int t = threadIdx.x;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int c = t + q * NTHR;
+            int mm, kk;
+            if (mn_contig) {
+                kk = c / (BT / 4);
+                mm = (c % (BT / 4)) * 4;
+            } else {
+                mm = c / 4;
+                kk = (c % 4) * 4;
+            }
+            const int64_t gm = r0 + mm, gk = k0 + kk;
+            const TI* src = mn_contig ? X + gk * ldx + gm : X + gm * ldx + gk;
+            const bool full = mn_contig ? (gk < kmax && gm + 3 < rmax) : (gm < rmax && gk + 3 < kmax);
+            if (vec && full) {
+                r[q] = *reinterpret_cast<const Stage4<TI>*>(src);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const bool ok = mn_contig ? (gk < kmax && gm + e < rmax) : (gm < rmax && gk + e < kmax);
+                    r[q].v[e] = ok ? src[e] : TI(0);
+                }
+            }
+        }
+    }
+    __device__ __forceinline__ void store(double* sm, bool mn_contig) const {
+        const int t = threadIdx.x;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int c = t + q * NTHR;
+            double d[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) d[e] = widen(r[q].v[e]);
+            if (mn_contig) {
+                const int kk = c / (BT / 4), mm = (c % (BT / 4)) * 4;
+                double2* dst = reinterpret_cast<double2*>(sm + kk * SM_ + mm);
+                dst[0] = make_double2(d[0], d[1]);
+                dst[1] = make_double2(d[2], d[3]);
+            } else {
+                const int mm = c / 4, kk = (c % 4) * 4;
+                double2* dst = reinterpret_cast<double2*>(sm + mm * SK_ + kk);
+                dst[0] = make_double2(d[0], d[1]);
+                dst[1] = make_double2(d[2], d[3]);
+            }
+        }
+    }
+};
+
+template <int BT>
 __device__ __forceinline__ double sm_get(const double* sm, bool mn_contig, int mn, int k) {
-    return mn_contig ? sm[k * SM_ + mn] : sm[mn * SK_ + k];
+    return mn_contig ? sm[k * DCfg<BT>::SM_ + mn] : sm[mn * SK_ + k];
 }
 
-__global__ void __launch_bounds__(NTHR, 1) dmma_gemm_kernel(DmmaArgs g) {
+template <int BT, typename TI>
+__global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 3 : 1) dmma_gemm_kernel(DmmaArgs g) {
+    using CF = DCfg<BT>;
+    constexpr int BMd = BT, BNd = BT, SLAB = CF::SLAB, WN = BT / 32;
     extern __shared__ __align__(16) double dsm[];
     const TileProblem pr = g.problems ? g.problems[blockIdx.z]
                                       : TileProblem{g.A, g.B, g.C, g.lower_only ? 1 : 0, 0};
     const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BMd;
     const int64_t n0 = static_cast<int64_t>(blockIdx.y) * BNd;
     if (pr.lower_only && m0 + BMd - 1 < n0) return;
-    const double* __restrict__ A = static_cast<const double*>(pr.A);
-    const double* __restrict__ B = static_cast<const double*>(pr.B);
+    constexpr bool WIDE = std::is_same<TI, double>::value;
+    const TI* __restrict__ A = static_cast<const TI*>(pr.A);
+    const TI* __restrict__ B = static_cast<const TI*>(pr.B);
     double* __restrict__ C = static_cast<double*>(pr.C);
     const bool a_mn = !g.ta;  // op(A) = A: M contiguous
     const bool b_mn = g.tb;   // op(B) = B^T: N contiguous
-    // 16-byte copies need even strides/offsets and even extents along the contiguous index
-    const bool va = (g.lda % 2 == 0) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0) &&
-                    (a_mn ? g.m % 2 == 0 : g.k % 2 == 0);
-    const bool vb = (g.ldb % 2 == 0) && ((reinterpret_cast<uintptr_t>(B) & 15) == 0) &&
-                    (b_mn ? g.n % 2 == 0 : g.k % 2 == 0);
+    // vector copies (16 bytes of FP64, 4 narrow elements) need aligned
+    // strides/offsets and extents along the contiguous index
+    constexpr int VE = WIDE ? 2 : 4;
+    const bool va = (g.lda % VE == 0) && ((reinterpret_cast<uintptr_t>(A) & (VE * sizeof(TI) - 1)) == 0) &&
+                    (a_mn ? g.m % VE == 0 : g.k % VE == 0);
+    const bool vb = (g.ldb % VE == 0) && ((reinterpret_cast<uintptr_t>(B) & (VE * sizeof(TI) - 1)) == 0) &&
+                    (b_mn ? g.n % VE == 0 : g.k % VE == 0);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int wm = (warp / 4) * 32, wn = (warp % 4) * 32;
+    const int wm = (warp / WN) * 32, wn = (warp % WN) * 32;
     const int gq = lane / 4, tq = lane % 4;
     double acc[2][4][4];
 #pragma unroll
@@ -129,21 +217,39 @@ __global__ void __launch_bounds__(NTHR, 1) dmma_gemm_kernel(DmmaArgs g) {
     const int nk = static_cast<int>((g.k + BKd - 1) / BKd);
     auto stage_a = [&](int s) { return dsm + s * 2 * SLAB; };
     auto stage_b = [&](int s) { return dsm + s * 2 * SLAB + SLAB; };
+    [[maybe_unused]] NarrowSlab<BT, TI> ra, rb;
     auto issue = [&](int kb) {
         const int s = kb % NST;
-        load_slab(stage_a(s), A, g.lda, a_mn, m0, g.m, static_cast<int64_t>(kb) * BKd, g.k, va);
-        load_slab(stage_b(s), B, g.ldb, b_mn, n0, g.n, static_cast<int64_t>(kb) * BKd, g.k, vb);
+        if constexpr (WIDE) {
+            load_slab<BT>(stage_a(s), reinterpret_cast<const double*>(A), g.lda, a_mn, m0, g.m,
+                          static_cast<int64_t>(kb) * BKd, g.k, va);
+            load_slab<BT>(stage_b(s), reinterpret_cast<const double*>(B), g.ldb, b_mn, n0, g.n,
+                          static_cast<int64_t>(kb) * BKd, g.k, vb);
+        } else {
+            ra.load(A, g.lda, a_mn, m0, g.m, static_cast<int64_t>(kb) * BKd, g.k, va);
+            rb.load(B, g.ldb, b_mn, n0, g.n, static_cast<int64_t>(kb) * BKd, g.k, vb);
+        }
+    };
+    auto land = [&](int kb) {  // narrow path: registers -> shared (FP64)
+        if constexpr (!WIDE) {
+            ra.store(stage_a(kb % NST), a_mn);
+            rb.store(stage_b(kb % NST), b_mn);
+        }
     };
 #pragma unroll
     for (int s = 0; s < NST - 1; ++s) {
-        if (s < nk) issue(s);
-        cp_commit();
+        if (s < nk) {
+            issue(s);
+            land(s);
+        }
+        if constexpr (WIDE) cp_commit();
     }
     for (int kb = 0; kb < nk; ++kb) {
-        cp_wait<NST - 2>();
+        if constexpr (WIDE) cp_wait<NST - 2>();
         __syncthreads();
-        if (kb + NST - 1 < nk) issue(kb + NST - 1);
-        cp_commit();
+        const bool next = kb + NST - 1 < nk;
+        if (next) issue(kb + NST - 1);
+        if constexpr (WIDE) cp_commit();
         const double* sa = stage_a(kb % NST);
         const double* sb = stage_b(kb % NST);
 #pragma unroll
@@ -154,22 +260,23 @@ __global__ void __launch_bounds__(NTHR, 1) dmma_gemm_kernel(DmmaArgs g) {
                 const int mr = wm + i * 16 + gq;
 #pragma unroll
                 for (int v = 0; v < 4; ++v)  // a[v0 + 2 v1] = A[g + 8 v0][t + 4 v1]
-                    af[i][v] = sm_get(sa, a_mn, mr + 8 * (v & 1), ks + tq + 4 * (v >> 1));
+                    af[i][v] = sm_get<BT>(sa, a_mn, mr + 8 * (v & 1), ks + tq + 4 * (v >> 1));
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int nc = wn + j * 8 + gq;
 #pragma unroll
                 for (int v = 0; v < 2; ++v)  // b[v] = B[k = t + 4 v][n = g]
-                    bf[j][v] = sm_get(sb, b_mn, nc, ks + tq + 4 * v);
+                    bf[j][v] = sm_get<BT>(sb, b_mn, nc, ks + tq + 4 * v);
             }
 #pragma unroll
             for (int i = 0; i < 2; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) dmma_k8(acc[i][j], af[i], bf[j]);
         }
+        if (next) land(kb + NST - 1);
     }
-    cp_wait<0>();
+    if constexpr (WIDE) cp_wait<0>();
     // epilogue: c[v0 + 2 v1] at (g + 8 v1, 2 t + v0)
     const double alpha = g.alpha, beta = g.beta;
 #pragma unroll
@@ -189,19 +296,44 @@ __global__ void __launch_bounds__(NTHR, 1) dmma_gemm_kernel(DmmaArgs g) {
             }
 }
 
+
+template <int BT, typename TI>
+void launch_bt(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count) {
+    using CF = DCfg<BT>;
+    static bool configured = false;
+    if (!configured) {
+        MP_CUDA(cudaFuncSetAttribute(dmma_gemm_kernel<BT, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     CF::SMEM));
+        configured = true;
+    }
+    const dim3 grid(static_cast<unsigned>((g.m + BT - 1) / BT), static_cast<unsigned>((g.n + BT - 1) / BT),
+                    static_cast<unsigned>(g.problems ? count : 1));
+    dmma_gemm_kernel<BT, TI><<<grid, CF::NTHR, CF::SMEM, s>>>(g);
+}
+
+template <typename TI>
+void launch_ti(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count, bool small) {
+    if (small)
+        launch_bt<64, TI>(ctx, s, g, count);
+    else
+        launch_bt<128, TI>(ctx, s, g, count);
+}
+
 }  // namespace
 
 void launch_dmma_gemm(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count) {
     if (g.m == 0 || g.n == 0) return;
-    static bool configured = false;
-    if (!configured) {
-        MP_CUDA(cudaFuncSetAttribute(dmma_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_D));
-        configured = true;
-    }
-    const dim3 grid(static_cast<unsigned>((g.m + BMd - 1) / BMd),
-                    static_cast<unsigned>((g.n + BNd - 1) / BNd),
-                    static_cast<unsigned>(g.problems ? count : 1));
-    dmma_gemm_kernel<<<grid, NTHR, SMEM_D, s>>>(g);
+    // CTAs (at/below the diagonal for SYRK) a 128x128 launch would have
+    const int64_t nprob = g.problems ? count : 1;
+    const int64_t tm = (g.m + 127) / 128, tn = (g.n + 127) / 128;
+    const int64_t ctas = nprob * (g.lower_only ? tm * (tn + 1) / 2 : tm * tn);  // lists live on the device
+    const bool small = ctas < ctx->sm_count;
+    if (g.pin == MP_HALF)
+        launch_ti<uint16_t>(ctx, s, g, count, small);
+    else if (g.pin == MP_SINGLE)
+        launch_ti<float>(ctx, s, g, count, small);
+    else
+        launch_ti<double>(ctx, s, g, count, small);
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());
 }

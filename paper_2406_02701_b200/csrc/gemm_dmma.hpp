@@ -5,7 +5,8 @@
 
 namespace mpcr {
 
-// C <- alpha op(A) op(B) + beta C, all FP64, column-major (dense or grouped).
+// C <- alpha op(A) op(B) + beta C in FP64, column-major (dense or grouped).
+// A and B are FP64, or FP16 / FP32 storage widened exactly on load (pin).
 struct DmmaArgs {
     bool ta, tb;
     int64_t m, n, k;
@@ -18,6 +19,7 @@ struct DmmaArgs {
     int64_t ldc;
     bool lower_only;
     const TileProblem* problems;  // grouped launch when non-null
+    mp_precision pin = MP_DOUBLE;  // operand storage precision
 };
 
 void launch_dmma_gemm(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count);

@@ -19,6 +19,8 @@
 // All per-step work lists are built on the host once per factorization and
 // uploaded in one copy; the step loop is launch-only (no host sync).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -47,6 +49,12 @@ struct mp_tile_s {
     size_t lists_bytes = 0;
     TrtriPlan* trtri = nullptr;  // FP64 inverse plan over work (built on first chol)
     std::vector<cudaEvent_t> events;  // lookahead stream ordering (built on first chol)
+    // the whole factorization as one CUDA graph (captured on the second
+    // chol of this tile, replayed afterwards)
+    cudaGraphExec_t graph = nullptr;
+    int64_t graph_launches = 0;
+    int chol_runs = 0;
+    bool graph_failed = false;
 
     int64_t tt() const { return br * bc; }
     mp_precision p(int64_t i, int64_t j) const { return prec[j * tr + i]; }
@@ -68,6 +76,7 @@ struct mp_tile_s {
         if (lists) cudaFree(lists);
         trtri_plan_destroy(trtri);
         for (cudaEvent_t e : events) cudaEventDestroy(e);
+        if (graph) cudaGraphExecDestroy(graph);
     }
 };
 
@@ -120,8 +129,8 @@ void append(std::vector<char>& buf, const std::vector<V>& v, size_t& off) {
 // Device work lists of one trailing-update part (offsets into the list
 // buffer + counts): tcgen05 FP16, tcgen05 3xTF32, SIMT/DMMA per precision.
 struct UpLists {
-    size_t tc = 0, tc32 = 0, p[3] = {0, 0, 0};
-    int64_t n_tc = 0, n_tc32 = 0, n_p[3] = {0, 0, 0};
+    size_t tc = 0, tc16s = 0, tc32 = 0, p[3] = {0, 0, 0}, pn[2] = {0, 0};
+    int64_t n_tc = 0, n_tc16s = 0, n_tc32 = 0, n_p[3] = {0, 0, 0}, n_pn[2] = {0, 0};
 };
 
 struct StepLists {
@@ -131,10 +140,12 @@ struct StepLists {
     int64_t n_trsm_tc = 0, n_trsm_p[3] = {0, 0, 0};
     size_t wb[3] = {0, 0, 0};
     int64_t n_wb[3] = {0, 0, 0};
-    size_t cv[3][3] = {};
-    int64_t n_cv[3][3] = {};
-    size_t split32 = 0;
-    int64_t n_split32 = 0;
+    // panel conversions, [0]: tiles k+1, k+2 (needed by the lookahead
+    // updates, critical path), [1]: the rest (needed by the bulk update only)
+    size_t cv[2][3][3] = {};
+    int64_t n_cv[2][3][3] = {};
+    size_t split32[2] = {0, 0};
+    int64_t n_split32[2] = {0, 0};
     UpLists up[3];  // 0: tile column k+1 below the diagonal, 1: the rest, 2: tile (k+1, k+1)
     std::vector<std::pair<int, int>> bcasts;  // (i, root) panel broadcasts
 };
@@ -155,6 +166,27 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     cudaStream_t s = c->stream;
     const int64_t nb = t.br, NT = t.tr, tt = t.tt();
     ensure_panels(t);
+    const size_t nn = static_cast<size_t>(nb) * nb;
+    int64_t* dinfo = reinterpret_cast<int64_t*>(static_cast<char*>(t.work) + nn * 28 + 64);
+    auto read_info = [&]() {
+        int64_t info = -1;
+        MP_CUDA(cudaMemcpyAsync(&info, dinfo, sizeof(info), cudaMemcpyDeviceToHost, s));
+        MP_CUDA(cudaStreamSynchronize(s));
+        return info;
+    };
+    // Graph replay: the factorization of this tile was captured once (lists,
+    // pointers and streams do not change over the tile's life).  Profiling
+    // and multi-rank runs stay eager.  MPCR_GRAPH=0 disables graphs.
+    static const bool graph_env = [] {
+        const char* e = getenv("MPCR_GRAPH");
+        return !(e && e[0] == '0');
+    }();
+    const bool want_graph = graph_env && !c->prof.enabled && !(t.dist && t.dist->world > 1);
+    if (want_graph && t.graph) {
+        MP_CUDA(cudaGraphLaunch(t.graph, s));
+        c->launches += t.graph_launches;
+        return read_info();
+    }
     const bool tc_ok = (nb % 8) == 0;  // TMA stride alignment for FP16 tiles
     static const bool lookahead_env = [] {
         const char* e = getenv("MPCR_LOOKAHEAD");
@@ -176,14 +208,26 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     std::vector<int> pgrid(t.prec.begin(), t.prec.end());
     const auto sched = dist_schedule(rank, P, Q, NT, pgrid.data());
     struct UpAcc {
-        std::vector<TcProblem> tc, tc32;
+        std::vector<TcProblem> tc, tc16s, tc32;
         std::vector<TileProblem> p[3];
+        std::vector<TileProblem> pn[2];  // FP64 tiles fed by FP16 / FP32 panels directly
+    };
+    // FP32 tiles whose two panel tiles are both FP16: the FP16 tensor-core
+    // GEMM with an FP32 accumulator/output (exact products; what 3xTF32
+    // reduces to when the low halves are zero)
+    auto half_into_single = [&](int64_t i, int64_t j, int64_t k) {
+        return tc_ok && t.p(i, k) == MP_HALF && t.p(j, k) == MP_HALF;
+    };
+    // FP64 updates whose two panel tiles share a narrower precision read them
+    // natively (widened exactly inside the DMMA kernel) instead of via copies
+    auto native64 = [&](int64_t i, int64_t j, int64_t k) {
+        return t.p(i, k) == t.p(j, k) && t.p(i, k) != MP_DOUBLE;
     };
     struct StepAcc {
         std::vector<TcProblem> trsm_tc;
         std::vector<TileProblem> trsm_p[3];
-        std::vector<CopyItem> wb[3], cv[3][3];
-        std::vector<SplitItem> split32;
+        std::vector<CopyItem> wb[3], cv[2][3][3];
+        std::vector<SplitItem> split32[2];
         UpAcc up[3];
     };
     std::vector<StepAcc> acc(NT);
@@ -193,17 +237,27 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     const void* linv[3] = {linv_base + nn0 * 24, linv_base + nn0 * 20, linv_base + nn0 * 8};
     auto consumers = [&](int64_t k, int64_t i, StepAcc& A) {
         // every rank receives every panel tile: convert it once to each
-        // precision the rank's own consumers (A_ij.converted(p) operands) need
+        // precision the rank's own consumers (A_ij.converted(p) operands)
+        // need.  Copies read by the lookahead updates (tile column k+1) are
+        // made on the critical path ([0]); the rest with the bulk update ([1]).
         const mp_precision q = t.p(i, k);
-        bool need[3] = {false, false, false};
+        bool need[2][3] = {{false, false, false}, {false, false, false}};
         for (int64_t j = k + 1; j <= i; ++j)  // A operand of (owned) row-i updates
-            if (t.has(i, j)) need[t.p(i, j)] = true;
+            if (t.has(i, j) && !(t.p(i, j) == MP_DOUBLE && native64(i, j, k)) &&
+                !(t.p(i, j) == MP_SINGLE && half_into_single(i, j, k)))
+                need[j == k + 1 ? 0 : 1][t.p(i, j)] = true;
         for (int64_t m = i; m < NT; ++m)  // B operand of (owned) column-i updates
-            if (t.has(m, i)) need[t.p(m, i)] = true;
-        for (int r = 0; r < 3; ++r)
-            if (need[r] && r != q) A.cv[q][r].push_back(CopyItem{pan(q, i, k), pan((mp_precision)r, i, k)});
-        if (tc_ok && need[MP_SINGLE])  // FP32 consumers run 3xTF32 on hi/lo splits
-            A.split32.push_back(SplitItem{pan(MP_SINGLE, i, k), spl(0, i, k), spl(1, i, k)});
+            if (t.has(m, i) && !(t.p(m, i) == MP_DOUBLE && native64(m, i, k)) &&
+                !(t.p(m, i) == MP_SINGLE && half_into_single(m, i, k)))
+                need[i == k + 1 ? 0 : 1][t.p(m, i)] = true;
+        for (int r = 0; r < 3; ++r) {
+            if (r == q) continue;
+            const int h = need[0][r] ? 0 : need[1][r] ? 1 : -1;
+            if (h >= 0) A.cv[h][q][r].push_back(CopyItem{pan(q, i, k), pan((mp_precision)r, i, k)});
+        }
+        const int h32 = need[0][MP_SINGLE] ? 0 : need[1][MP_SINGLE] ? 1 : -1;
+        if (tc_ok && h32 >= 0)  // FP32 consumers run 3xTF32 on hi/lo splits
+            A.split32[h32].push_back(SplitItem{pan(MP_SINGLE, i, k), spl(0, i, k), spl(1, i, k)});
     };
     for (const DistAction& a : sched) {
         StepAcc& A = acc[a.k];
@@ -235,10 +289,16 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 if (q == MP_HALF && tc_ok)
                     U.tc.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
                                              static_cast<int32_t>(t.slot[j * NT + i]), lo});
+                else if (q == MP_SINGLE && half_into_single(i, j, k))
+                    U.tc16s.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
+                                                static_cast<int32_t>(t.slot[j * NT + i]), lo});
                 else if (q == MP_SINGLE && tc_ok)
                     U.tc32.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
                                                static_cast<int32_t>(t.slot[j * NT + i]), lo});
-                else
+                else if (q == MP_DOUBLE && native64(i, j, k)) {
+                    const mp_precision pp = t.p(i, k);
+                    U.pn[pp].push_back(TileProblem{pan(pp, i, k), pan(pp, j, k), t.ptr(i, j), lo, 0});
+                } else
                     U.p[q].push_back(TileProblem{pan(q, i, k), pan(q, j, k), t.ptr(i, j), lo, 0});
                 break;
             }
@@ -257,21 +317,30 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             L.n_trsm_p[q] = A.trsm_p[q].size();
             append(buf, A.wb[q], L.wb[q]);
             L.n_wb[q] = A.wb[q].size();
-            for (int r = 0; r < 3; ++r) {
-                append(buf, A.cv[q][r], L.cv[q][r]);
-                L.n_cv[q][r] = A.cv[q][r].size();
-            }
+            for (int r = 0; r < 3; ++r)
+                for (int h = 0; h < 2; ++h) {
+                    append(buf, A.cv[h][q][r], L.cv[h][q][r]);
+                    L.n_cv[h][q][r] = A.cv[h][q][r].size();
+                }
         }
-        append(buf, A.split32, L.split32);
-        L.n_split32 = A.split32.size();
+        for (int h = 0; h < 2; ++h) {
+            append(buf, A.split32[h], L.split32[h]);
+            L.n_split32[h] = A.split32[h].size();
+        }
         for (int w = 0; w < 3; ++w) {
             append(buf, A.up[w].tc, L.up[w].tc);
             L.up[w].n_tc = A.up[w].tc.size();
+            append(buf, A.up[w].tc16s, L.up[w].tc16s);
+            L.up[w].n_tc16s = A.up[w].tc16s.size();
             append(buf, A.up[w].tc32, L.up[w].tc32);
             L.up[w].n_tc32 = A.up[w].tc32.size();
             for (int q = 0; q < 3; ++q) {
                 append(buf, A.up[w].p[q], L.up[w].p[q]);
                 L.up[w].n_p[q] = A.up[w].p[q].size();
+            }
+            for (int q = 0; q < 2; ++q) {
+                append(buf, A.up[w].pn[q], L.up[w].pn[q]);
+                L.up[w].n_pn[q] = A.up[w].pn[q].size();
             }
         }
     }
@@ -294,7 +363,6 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     MP_CUDA(cudaMemcpyAsync(dl, buf.data(), buf.size(), cudaMemcpyHostToDevice, s));
 
     // ---- workspace ------------------------------------------------------------
-    const size_t nn = static_cast<size_t>(nb) * nb;
     char* w = static_cast<char*>(t.work);
     double* dwork = reinterpret_cast<double*>(w);
     double* linv64 = reinterpret_cast<double*>(w + nn * 8);
@@ -302,17 +370,35 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     float* linvS = reinterpret_cast<float*>(w + nn * 20);
     uint16_t* linvH = reinterpret_cast<uint16_t*>(w + nn * 24);
     uint16_t* linvHlo = reinterpret_cast<uint16_t*>(w + nn * 26);
-    int64_t* dinfo = reinterpret_cast<int64_t*>(w + nn * 28 + 64);
-    const int64_t neg = -1;
-    MP_CUDA(cudaMemcpyAsync(dinfo, &neg, sizeof(neg), cudaMemcpyHostToDevice, s));
-    // Linv's strictly upper part stays zero for the whole factorization; the
-    // TRTRI plan (FP64 inverse of dwork) is built once.
-    MP_CUDA(cudaMemsetAsync(linv64, 0, nn * sizeof(double), s));
+    // the TRTRI plan (FP64 inverse of dwork) is built once
     if (!t.trtri) t.trtri = trtri_plan_create(c, s, dwork, nb, linv64, nb, nb);
     TrtriPlan* trtri = t.trtri;
 
     // ---- panel k: factor A_kk, invert, TRSM the tile column, distribute and
     //      convert the panel for its consumers ---------------------------------
+    // consumer-precision copies of panel k ([0] lookahead tiles, [1] bulk) and
+    // the hi/lo TF32 splits of its FP32 tiles, stored transposed (K-major)
+    auto convert_panel = [&](int64_t k, int h, cudaStream_t st) {
+        const StepLists& L = steps[k];
+        for (int q = 0; q < 3; ++q)
+            for (int r = 0; r < 3; ++r)
+                if (L.n_cv[h][q][r])
+                    launch_batched_convert(c, st, (mp_precision)q, (mp_precision)r,
+                                           reinterpret_cast<const CopyItem*>(dl + L.cv[h][q][r]),
+                                           L.n_cv[h][q][r], tt);
+        if (L.n_split32[h])
+            launch_batched_split_tf32_t(c, st, reinterpret_cast<const SplitItem*>(dl + L.split32[h]),
+                                        L.n_split32[h], nb);
+    };
+    // write the factor of tile column k back from the panel into the tiles
+    auto write_back = [&](int64_t k, cudaStream_t st) {
+        const StepLists& L = steps[k];
+        for (int q = 0; q < 3; ++q)
+            if (L.n_wb[q])
+                launch_batched_convert(c, st, (mp_precision)q, (mp_precision)q,
+                                       reinterpret_cast<const CopyItem*>(dl + L.wb[q]), L.n_wb[q], tt);
+    };
+
     auto panel_phase = [&](int64_t k, cudaStream_t st, cudaEvent_t before_trsm) {
         const StepLists& L = steps[k];
         const mp_precision pk = t.p(k, k);
@@ -398,11 +484,6 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                           reinterpret_cast<const TileProblem*>(dl + L.trsm_p[q]), L.n_trsm_p[q]};
             launch_grouped_gemm(c, st, g);
         }
-        // write the factor back into the tiles
-        for (int q = 0; q < 3; ++q)
-            if (L.n_wb[q])
-                launch_batched_convert(c, st, (mp_precision)q, (mp_precision)q,
-                                       reinterpret_cast<const CopyItem*>(dl + L.wb[q]), L.n_wb[q], tt);
         // distributed: every panel tile travels from its owner to all ranks
         if (!L.bcasts.empty()) {
             dist_group_start(t.dist);
@@ -412,17 +493,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             }
             dist_group_end(t.dist);
         }
-        // consumer-precision copies of the panel
-        for (int q = 0; q < 3; ++q)
-            for (int r = 0; r < 3; ++r)
-                if (L.n_cv[q][r])
-                    launch_batched_convert(c, st, (mp_precision)q, (mp_precision)r,
-                                           reinterpret_cast<const CopyItem*>(dl + L.cv[q][r]),
-                                           L.n_cv[q][r], tt);
-        // hi/lo TF32 splits of the FP32 panel, stored transposed (K-major)
-        if (L.n_split32)
-            launch_batched_split_tf32_t(c, st, reinterpret_cast<const SplitItem*>(dl + L.split32),
-                                        L.n_split32, nb);
+        convert_panel(k, 0, st);
     };
 
     // ---- trailing update A_ij -= L_ik L_jk^T of one part of step k ------------
@@ -448,6 +519,27 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             g.c_tile_stride = tt;
             g.problems = reinterpret_cast<const TcProblem*>(dl + U.tc32);
             g.count = U.n_tc32;
+            g.tiles_per_cta = tiles_per_cta;
+            launch_tc_gemm(c, st, g);
+        }
+        if (U.n_tc16s) {  // FP32 tiles from FP16 panels
+            TcGemm g;
+            g.pc = MP_SINGLE;
+            g.ta = false;
+            g.tb = true;
+            g.m = g.n = g.k = nb;
+            g.alpha = -1.0;
+            g.beta = 1.0;
+            g.A = g.B = pan(MP_HALF, 0, k);
+            g.lda = g.ldb = nb;
+            g.a_tiles = g.b_tiles = NT;
+            g.a_tile_stride = g.b_tile_stride = tt;
+            g.C = t.slab[MP_SINGLE];
+            g.ldc = nb;
+            g.c_tiles = t.nslot[MP_SINGLE];
+            g.c_tile_stride = tt;
+            g.problems = reinterpret_cast<const TcProblem*>(dl + U.tc16s);
+            g.count = U.n_tc16s;
             g.tiles_per_cta = tiles_per_cta;
             launch_tc_gemm(c, st, g);
         }
@@ -478,70 +570,121 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                               reinterpret_cast<const TileProblem*>(dl + U.p[q]), U.n_p[q]};
                 launch_grouped_gemm(c, st, g);
             }
+        for (int q = 0; q < 2; ++q)
+            if (U.n_pn[q]) {
+                GroupedGemm g{(mp_precision)q, MP_DOUBLE, true, nb, nb, nb, nb, nb, nb, -1.0, 1.0,
+                              reinterpret_cast<const TileProblem*>(dl + U.pn[q]), U.n_pn[q]};
+                launch_grouped_gemm(c, st, g);
+            }
     };
 
-    // ---- issue.  Per step k, three streams:
-    //   s   : wait panel k; update of everything but tile column k+1 (bulk)
-    //   sl2 : wait panel k and bulk k-1; update of column k+1 below the diagonal
-    //   sl  : wait bulk k-1; SYRK of A_{k+1,k+1}; POTRF + TRTRI of panel k+1;
-    //         wait sl2; TRSM + conversions of panel k+1
-    //   The chain POTRF -> TRSM -> SYRK -> POTRF is the critical path; the
-    //   bulk GEMMs hand SMs back every few tiles so it is never starved.
-    static const int tpc_env = [] {
-        const char* e = getenv("MPCR_TILES_PER_CTA");
-        return e ? atoi(e) : 4;
-    }();
-    const int bulk_tpc = la ? tpc_env : 0;
-    cudaStream_t sl2 = la ? c->hi2 : s;
-    cudaEvent_t* ev_panel = t.events.data();          // NT
-    cudaEvent_t* ev_rest = t.events.data() + NT;      // NT
-    cudaEvent_t* ev_next = t.events.data() + 2 * NT;  // NT
-    cudaEvent_t ev_join = t.events[3 * NT + 1], ev_join2 = t.events[3 * NT + 2];
-    if (la) {
-        MP_CUDA(cudaEventRecord(ev_join, s));
-        MP_CUDA(cudaStreamWaitEvent(sl, ev_join, 0));
-        MP_CUDA(cudaStreamWaitEvent(sl2, ev_join, 0));
-    }
-    panel_phase(0, sl, nullptr);
-    if (la) MP_CUDA(cudaEventRecord(ev_panel[0], sl));
-    for (int64_t k = 0; k < NT; ++k) {
-        if (la) MP_CUDA(cudaStreamWaitEvent(s, ev_panel[k], 0));
-        update_phase(k, 1, s, bulk_tpc);
-        if (la) MP_CUDA(cudaEventRecord(ev_rest[k], s));
-        if (k + 1 < NT) {
-            if (la) {
-                MP_CUDA(cudaStreamWaitEvent(sl2, ev_panel[k], 0));
-                if (k >= 1) MP_CUDA(cudaStreamWaitEvent(sl2, ev_rest[k - 1], 0));
-            }
-            update_phase(k, 0, sl2, 0);
-            if (la) MP_CUDA(cudaEventRecord(ev_next[k], sl2));
-            if (la && k >= 1) MP_CUDA(cudaStreamWaitEvent(sl, ev_rest[k - 1], 0));
-            update_phase(k, 2, sl, 0);
-            panel_phase(k + 1, sl, la ? ev_next[k] : nullptr);
-            if (la) MP_CUDA(cudaEventRecord(ev_panel[k + 1], sl));
+    auto issue_all = [&]() {
+        MP_CUDA(cudaMemsetAsync(dinfo, 0xFF, sizeof(int64_t), s));  // -1: no failure
+        // Linv's strictly upper part stays zero for the whole factorization
+        MP_CUDA(cudaMemsetAsync(linv64, 0, nn * sizeof(double), s));
+        // ---- issue.  Per step k, three streams:
+        //   s   : wait panel k; bulk conversions of panel k; update of everything
+        //         but tile column k+1 (bulk); write tile column k back
+        //   sl2 : wait panel k and bulk k-1; update of column k+1 below the diagonal
+        //   sl  : wait bulk k-1; SYRK of A_{k+1,k+1}; POTRF + TRTRI of panel k+1;
+        //         wait sl2; TRSM + conversions of panel k+1
+        //   The chain POTRF -> TRSM -> SYRK -> POTRF is the critical path; the
+        //   bulk GEMMs hand SMs back every few tiles so it is never starved.
+        static const int tpc_env = [] {
+            const char* e = getenv("MPCR_TILES_PER_CTA");
+            return e ? atoi(e) : 16;
+        }();
+        const int bulk_tpc = la ? tpc_env : 0;
+        cudaStream_t sl2 = la ? c->hi2 : s;
+        cudaEvent_t* ev_panel = t.events.data();          // NT
+        cudaEvent_t* ev_rest = t.events.data() + NT;      // NT
+        cudaEvent_t* ev_next = t.events.data() + 2 * NT;  // NT
+        cudaEvent_t ev_join = t.events[3 * NT + 1], ev_join2 = t.events[3 * NT + 2];
+        if (la) {
+            MP_CUDA(cudaEventRecord(ev_join, s));
+            MP_CUDA(cudaStreamWaitEvent(sl, ev_join, 0));
+            MP_CUDA(cudaStreamWaitEvent(sl2, ev_join, 0));
         }
+        static const bool dbg_host = getenv("MPCR_DEBUG_HOST") != nullptr;
+        const auto th0 = std::chrono::steady_clock::now();
+        std::vector<double> th;
+        panel_phase(0, sl, nullptr);
+        if (la) MP_CUDA(cudaEventRecord(ev_panel[0], sl));
+        for (int64_t k = 0; k < NT; ++k) {
+            if (la) MP_CUDA(cudaStreamWaitEvent(s, ev_panel[k], 0));
+            convert_panel(k, 1, s);
+            update_phase(k, 1, s, bulk_tpc);
+            write_back(k, s);
+            if (la) MP_CUDA(cudaEventRecord(ev_rest[k], s));
+            if (k + 1 < NT) {
+                if (la) {
+                    MP_CUDA(cudaStreamWaitEvent(sl2, ev_panel[k], 0));
+                    if (k >= 1) MP_CUDA(cudaStreamWaitEvent(sl2, ev_rest[k - 1], 0));
+                }
+                update_phase(k, 0, sl2, 0);
+                if (la) MP_CUDA(cudaEventRecord(ev_next[k], sl2));
+                if (la && k >= 1) MP_CUDA(cudaStreamWaitEvent(sl, ev_rest[k - 1], 0));
+                update_phase(k, 2, sl, 0);
+                panel_phase(k + 1, sl, la ? ev_next[k] : nullptr);
+                if (la) MP_CUDA(cudaEventRecord(ev_panel[k + 1], sl));
+            }
+            if (dbg_host)
+                th.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count());
+        }
+        if (dbg_host) {
+            std::fprintf(stderr, "[mpcr] host issue per step (ms):");
+            for (size_t q = 0; q < th.size(); q += 4) std::fprintf(stderr, " %zu:%.2f", q, th[q]);
+            std::fprintf(stderr, "\n");
+        }
+        if (la) {
+            MP_CUDA(cudaEventRecord(ev_join, sl));
+            MP_CUDA(cudaEventRecord(ev_join2, sl2));
+            MP_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
+            MP_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));
+        }
+        // ---- zero everything above the diagonal (lower L output) ------------------
+        for (int q = 0; q < 3; ++q) {
+            if (!diag_ptrs[q].empty())
+                launch_batched_zero(c, s, (mp_precision)q, reinterpret_cast<void* const*>(dl + off_diag[q]),
+                                    diag_ptrs[q].size(), tt, true, nb);
+            if (!upper_ptrs[q].empty())
+                launch_batched_zero(c, s, (mp_precision)q, reinterpret_cast<void* const*>(dl + off_upper[q]),
+                                    upper_ptrs[q].size(), tt, false, nb);
+        }
+    };
+    const bool capture = want_graph && t.chol_runs > 0 && !t.graph_failed;
+    if (capture) {
+        const int64_t l0 = c->launches;
+        cudaGraph_t g = nullptr;
+        MP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeRelaxed));
+        bool ok = true;
+        try {
+            issue_all();
+        } catch (const Error&) {
+            ok = false;
+        }
+        if (cudaStreamEndCapture(s, &g) != cudaSuccess) ok = false;
+        if (ok && cudaGraphInstantiate(&t.graph, g, 0) != cudaSuccess) {
+            ok = false;
+            t.graph = nullptr;
+        }
+        if (g) cudaGraphDestroy(g);
+        if (ok) {
+            t.graph_launches = c->launches - l0;
+            MP_CUDA(cudaGraphLaunch(t.graph, s));
+        } else {  // not capturable here: stay eager for this tile
+            (void)cudaGetLastError();
+            t.graph_failed = true;
+            c->launches = l0;
+            issue_all();
+        }
+    } else {
+        issue_all();
     }
-    if (la) {
-        MP_CUDA(cudaEventRecord(ev_join, sl));
-        MP_CUDA(cudaEventRecord(ev_join2, sl2));
-        MP_CUDA(cudaStreamWaitEvent(s, ev_join, 0));
-        MP_CUDA(cudaStreamWaitEvent(s, ev_join2, 0));
-    }
-    // ---- zero everything above the diagonal (lower L output) ------------------
-    for (int q = 0; q < 3; ++q) {
-        if (!diag_ptrs[q].empty())
-            launch_batched_zero(c, s, (mp_precision)q, reinterpret_cast<void* const*>(dl + off_diag[q]),
-                                diag_ptrs[q].size(), tt, true, nb);
-        if (!upper_ptrs[q].empty())
-            launch_batched_zero(c, s, (mp_precision)q, reinterpret_cast<void* const*>(dl + off_upper[q]),
-                                upper_ptrs[q].size(), tt, false, nb);
-    }
+    ++t.chol_runs;
     // first failing column over all ranks (-1 as uint64 is the largest value)
     if (t.dist && t.dist->world > 1) dist_allreduce_min_u64(t.dist, dinfo, s);
-    int64_t info = -1;
-    MP_CUDA(cudaMemcpyAsync(&info, dinfo, sizeof(info), cudaMemcpyDeviceToHost, s));
-    MP_CUDA(cudaStreamSynchronize(s));
-    return info;
+    return read_info();
 }
 
 }  // namespace mpcr

@@ -234,3 +234,27 @@ def test_dist_world1_matches_single(ctx, ref):
     want = ref.tile_chol(n, nb, g, ref.grid_matern(side, n, 0.5, 0.03, 1.0, 2))
     assert np.abs(Lb - want).max() < 1e-2
 
+
+
+def test_tile_chol_graph_replay_bitwise(ctx):
+    """First chol runs eagerly, the second is captured as a CUDA graph, later
+    ones replay it: all factors identical bit for bit, launches counted."""
+    import paper_2406_02701_b200 as mp
+
+    n, nb = 2048, 256
+    nt = n // nb
+    i, j = np.indices((nt, nt))
+    g = np.where(i == j, 2, np.where(abs(i - j) == 1, 1, 0))
+    A0 = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+    A0.fill_matern(64, 0.5, 0.03, 1.0)
+    A = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+    outs, counts = [], []
+    for _ in range(4):
+        A.copy_from(A0)
+        l0 = ctx.launch_count()
+        mp.tile_chol(A)
+        counts.append(ctx.launch_count() - l0)
+        outs.append(A.to_numpy())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    assert counts[2] == counts[3] > 0
