@@ -1,14 +1,71 @@
 // GEMM dispatch: picks the kernel family from the precisions
 // (linalg.cpp:340 branches on compute_precision(prec(C))).
 //   A, B half and C half/single  -> tcgen05 FP16 tensor cores (gemm_tc.cu)
+//   C single, A/B not double     -> 3xTF32 on tcgen05
+//   A, B half and C double       -> exact INT8 digit products (ozaki.cu)
+//   all double                   -> DMMA (gemm_dmma.cu)
 //   everything else              -> SIMT in C's compute type (gemm_simt.cu)
+#include <algorithm>
+#include <cstdlib>
+
 #include "batch.hpp"
 #include "gemm_dmma.hpp"
 #include "gemm_simt.hpp"
 #include "gemm_tc.hpp"
 #include "internal.hpp"
+#include "ozaki.hpp"
 
 namespace mpcr {
+
+bool ozaki_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("MPCR_OZAKI");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+// FP16 x FP16 -> FP64: exact 7-bit digit slicing + INT8 tensor cores (ozaki.cu).
+static void launch_gemm_ozaki(Ctx* ctx, cudaStream_t s, const GemmDesc& g) {
+    const int64_t kpad = (g.k + 15) / 16 * 16;
+    const size_t sa = static_cast<size_t>(g.m) * kpad, sb = static_cast<size_t>(g.n) * kpad;
+    const size_t dig = OZ_SLICES * (sa + sb);
+    const size_t items_off = (dig + 255) / 256 * 256;
+    const size_t rexp_off = items_off + 256;
+    char* w = static_cast<char*>(ctx->ensure_scratch(rexp_off + (g.m + g.n + 2) * 4 + 256, 2));
+    int8_t* da = reinterpret_cast<int8_t*>(w);
+    int8_t* db = da + OZ_SLICES * sa;
+    int32_t* ea = reinterpret_cast<int32_t*>(w + rexp_off);
+    int32_t* eb = ea + g.m;
+    int32_t* nd = eb + g.n;  // digits needed by A and B
+    MP_CUDA(cudaMemsetAsync(nd, 0, 2 * sizeof(int32_t), s));
+    // op(A)(r = m, c = k); op(B)^T(r = n, c = k).  trans: element (r, c) at x[r * ld + c]
+    OzSliceItem it[2] = {
+        {g.A, da, ea, nd, g.lda, g.m, g.k, kpad, static_cast<int64_t>(sa), g.ta ? 1 : 0, 0},
+        {g.B, db, eb, nd + 1, g.ldb, g.n, g.k, kpad, static_cast<int64_t>(sb), g.tb ? 0 : 1, 0}};
+    OzSliceItem* dit = reinterpret_cast<OzSliceItem*>(w + items_off);
+    MP_CUDA(cudaMemcpyAsync(dit, it, sizeof(it), cudaMemcpyHostToDevice, s));
+    launch_oz_slices(ctx, s, dit, 2, std::max(g.m, g.n), kpad);
+    OzGemm o;
+    o.A = da;
+    o.B = db;
+    o.a_slice_stride = static_cast<int64_t>(sa);
+    o.b_slice_stride = static_cast<int64_t>(sb);
+    o.kpad = kpad;
+    o.m = g.m;
+    o.n = g.n;
+    o.k = g.k;
+    o.C = g.C;
+    o.ldc = g.ldc;
+    o.alpha = g.alpha;
+    o.beta = g.beta;
+    o.lower_only = g.lower_only;
+    o.rexp_a = ea;
+    o.rexp_b = eb;
+    o.ndig_a = nd;
+    o.ndig_b = nd + 1;
+    launch_oz_gemm(ctx, s, o);
+}
 
 void launch_gemm(Ctx* ctx, cudaStream_t s, const GemmDesc& g) {
     if (g.m == 0 || g.n == 0) return;
@@ -76,6 +133,11 @@ void launch_gemm(Ctx* ctx, cudaStream_t s, const GemmDesc& g) {
             launch_tc_gemm(ctx, s, t);
             return;
         }
+    }
+    if (g.pa == MP_HALF && g.pb == MP_HALF && g.pc == MP_DOUBLE && g.k > 0 && g.k < (1 << 30) &&
+        ozaki_enabled()) {
+        launch_gemm_ozaki(ctx, s, g);
+        return;
     }
     if (g.pa == MP_DOUBLE && g.pb == MP_DOUBLE && g.pc == MP_DOUBLE) {
         DmmaArgs d{g.ta, g.tb, g.m, g.n, g.k, g.alpha, g.beta, g.A, g.lda,

@@ -342,6 +342,16 @@ void make_map(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int es
     if (r != CUDA_SUCCESS) fail(MP_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
 }
 
+}  // namespace tc
+
+void tma_map_3d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int esize, uint64_t d0,
+                uint64_t d1, uint64_t d2, uint64_t ld_elems, uint64_t tile_stride_elems, uint32_t box0,
+                uint32_t box1, CUtensorMapSwizzle swz) {
+    tc::make_map(map, base, dt, esize, d0, d1, d2, ld_elems, tile_stride_elems, box0, box1, swz);
+}
+
+namespace tc {
+
 // Operand map: 128-byte swizzled boxes of 128 bytes x box1 rows.
 void make_op_map(CUtensorMap* map, int kind, const void* base, uint64_t d0, uint64_t d1,
                  uint64_t d2, uint64_t ld, uint64_t ts, uint32_t box1) {

@@ -1,6 +1,8 @@
 // Host interface of the tcgen05 FP16 GEMM (gemm_tc.cu).
 #pragma once
 
+#include <cuda.h>
+
 #include <cstdint>
 
 #include "internal.hpp"
@@ -48,6 +50,12 @@ struct TcGemm {
 };
 
 bool tc_gemm_supported(const TcGemm& g);
+
+// 3-D TMA map over [d2][d1][d0] elements (d0 contiguous, rows ld_elems
+// apart, d2 slices tile_stride_elems apart), boxes of box0 x box1.
+void tma_map_3d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int esize, uint64_t d0,
+                uint64_t d1, uint64_t d2, uint64_t ld_elems, uint64_t tile_stride_elems, uint32_t box0,
+                uint32_t box1, CUtensorMapSwizzle swz);
 void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g);
 
 }  // namespace mpcr

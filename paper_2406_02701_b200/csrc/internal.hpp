@@ -144,6 +144,7 @@ struct GemmDesc {
     bool lower_only = false;
 };
 void launch_gemm(Ctx* ctx, cudaStream_t s, const GemmDesc& g);
+bool ozaki_enabled();  // MPCR_OZAKI=0 turns the INT8 FP64 path off
 
 // Grouped tile GEMM used by the MPCRTile scheduler: every problem is
 // C_p <- alpha A_p op(B_p) + beta C_p with identical shapes.

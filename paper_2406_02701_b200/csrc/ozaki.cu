@@ -1,0 +1,493 @@
+// FP64 GEMM of FP16-valued operands on the INT8 tensor cores (Ozaki scheme,
+// exact digit slicing).
+//
+// Where it serves: the FP64 tiles of the mixed-precision Cholesky are updated
+// with panel tiles that are stored in FP16 (the reference converts them to
+// double and calls an FP64 GEMM, linalg.cpp:349-356), and linalg::gemm with
+// FP16 operands and a double C.  B200 runs FP64 at 37 TFLOP/s but INT8 MMA at
+// ~4.5 POPS, so the FP64 product is rebuilt from INT8 products:
+//
+//   every row r of an operand is scaled by 2^-e_r (e_r: exponent of its
+//   largest magnitude) and split into S = 6 signed 7-bit digits
+//     x = 2^e_r * sum_p d_p 2^(-6-7(p-1)),  d_p in [-64, 64]  (int8).
+//   An FP16 row spans at most 40 significant bits below its maximum (2^5 ..
+//   2^-24 plus 11 significand bits), and 6 digits hold 41, so the split is
+//   EXACT.  All S^2 = 36 digit products d_p d_q^T are computed (int32 sums
+//   are exact: |sum| <= 6 * K * 64^2 < 2^31 for K <= 8192 per group) and
+//   combined in FP64 with one rounding per group: the result is as accurate
+//   as a correctly-ordered FP64 dot product, usually better.
+//
+// Kernel: persistent, warp-specialised, 128 x 128 output tiles.
+//   warp 0      TMA producer: 6-stage ring of {A 128x128, B 128x128} int8 digit
+//               tiles (128B swizzle).
+//   warp 1      TMEM allocator + MMA issuer: tcgen05.mma kind::i8 (M=128,
+//               N=128, K=32) into a double-buffered int32 accumulator; the 36
+//               digit pairs are issued grouped by t = p + q (11 groups, all
+//               pairs of a group share the scale 2^(-12-7(t-2)) and one
+//               accumulator), smallest magnitude first.
+//   warps 2-9   epilogue: each thread owns one tile row and 64 columns of
+//               FP64 running sums in registers; per group it adds
+//               2^(-12-7(t-2)) * acc, then C = alpha * 2^(e_r+e_c) * sum
+//               + beta * C (lower triangle only for SYRK tiles).
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "device.cuh"
+#include "gemm_tc.hpp"
+#include "internal.hpp"
+#include "ozaki.hpp"
+#include "tc_ptx.cuh"
+
+namespace mpcr {
+namespace oz {
+
+constexpr int S = OZ_SLICES;  // digits per value
+constexpr int BM = 128, BN = 128, BK = 128, STAGES = 6;
+constexpr int A_STAGE = BM * BK, B_STAGE = BN * BK;  // 16 KB each
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 + 256;
+constexpr int TMEM_COLS = 256;  // 2 x 128 int32 accumulators
+constexpr int NTHREADS = 320;   // 10 warps
+constexpr int ROWEXP_NONFINITE = 0x7fffffff;
+
+struct Params {
+    CUtensorMap map_a, map_b;  // [tiles * S][rows][K] int8
+    const OzProblem* problems;
+    OzProblem single;
+    int32_t nprob;
+    int32_t M, N, K;
+    int32_t mblocks, nblocks, kblocks;
+    int64_t ldc;
+    double alpha, beta;
+    const int32_t* rexp_a;  // row exponents of A tile t at rexp_a + t * rexp_stride_a
+    const int32_t* rexp_b;
+    int64_t rexp_stride_a, rexp_stride_b;
+    const int32_t* ndig_a;  // digits per tile (nullptr: all S)
+    const int32_t* ndig_b;
+};
+
+// Digit counts of a problem: pairs (dp, dq) with dp <= sa, dq <= sb; groups
+// g = sa + sb .. 2.
+__device__ __forceinline__ void digits_of(const Params& p, const OzProblem& pr, int& sa, int& sb) {
+    sa = p.ndig_a ? max(1, min(S, p.ndig_a[pr.a_tile])) : S;
+    sb = p.ndig_b ? max(1, min(S, p.ndig_b[pr.b_tile])) : S;
+}
+
+__device__ __forceinline__ void mma_i8_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// kind::i8 instruction descriptor: S32 accumulator, signed 8-bit A and B,
+// both K-major.
+__host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
+    return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) |
+           (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ bool skip_tile(const OzProblem& pr, int m0, int n0) {
+    return pr.lower_only && (m0 + BM - 1 < n0);
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_constant__ Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~static_cast<uintptr_t>(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_STAGE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&p.map_a);
+        ptx::tma_prefetch_desc(&p.map_b);
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            ptx::mbar_init(&tfull[s], 1);
+            ptx::mbar_init(&tempty[s], 256);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int tiles_per_prob = p.mblocks * p.nblocks;
+    const int64_t total = static_cast<int64_t>(p.nprob) * tiles_per_prob;
+    auto decode = [&](int64_t t, OzProblem& pr, int& m0, int& n0) {
+        const int64_t pi = t / tiles_per_prob;
+        const int r = static_cast<int>(t - pi * tiles_per_prob);
+        pr = p.problems ? p.problems[pi] : p.single;
+        m0 = (r % p.mblocks) * BM;
+        n0 = (r / p.mblocks) * BN;
+    };
+
+    if (warp == 0) {
+        // ===== TMA producer: groups t = 2S .. 2 (small magnitudes first) =====
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+                OzProblem pr;
+                int m0, n0;
+                decode(t, pr, m0, n0);
+                if (skip_tile(pr, m0, n0)) continue;
+                int sa, sb;
+                digits_of(p, pr, sa, sb);
+                for (int g = sa + sb; g >= 2; --g)
+                    for (int dp = max(1, g - sb); dp <= min(sa, g - 1); ++dp) {
+                        const int dq = g - dp;
+                        const int za = pr.a_tile * S + dp - 1, zb = pr.b_tile * S + dq - 1;
+                        for (int kb = 0; kb < p.kblocks; ++kb) {
+                            ptx::mbar_wait(&empty[stage], phase ^ 1);
+                            ptx::mbar_arrive_expect_tx(&full[stage], A_STAGE + B_STAGE);
+                            ptx::tma_load_3d(sA + stage * A_STAGE, &p.map_a, &full[stage], kb * BK, m0, za);
+                            ptx::tma_load_3d(sB + stage * B_STAGE, &p.map_b, &full[stage], kb * BK, n0, zb);
+                            if (++stage == STAGES) {
+                                stage = 0;
+                                phase ^= 1;
+                            }
+                        }
+                    }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer: one accumulator per digit group =====
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_i8(BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+                OzProblem pr;
+                int m0, n0;
+                decode(t, pr, m0, n0);
+                if (skip_tile(pr, m0, n0)) continue;
+                int sa, sb;
+                digits_of(p, pr, sa, sb);
+                for (int g = sa + sb; g >= 2; --g) {
+                    ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                    ptx::tc_fence_after();
+                    const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+                    bool first = true;
+                    for (int dp = max(1, g - sb); dp <= min(sa, g - 1); ++dp)
+                        for (int kb = 0; kb < p.kblocks; ++kb) {
+                            ptx::mbar_wait(&full[stage], phase);
+                            ptx::tc_fence_after();
+                            const uint32_t a_base = ptx::smem_u32(sA + stage * A_STAGE);
+                            const uint32_t b_base = ptx::smem_u32(sB + stage * B_STAGE);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K per stage
+                                const uint64_t ad = ptx::umma_desc_sw128(a_base + k * 32, 0, 1024);
+                                const uint64_t bd = ptx::umma_desc_sw128(b_base + k * 32, 0, 1024);
+                                mma_i8_ss(d_tmem, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
+                            }
+                            first = false;
+                            ptx::mma_commit(&empty[stage]);
+                            if (++stage == STAGES) {
+                                stage = 0;
+                                phase ^= 1;
+                            }
+                        }
+                    ptx::mma_commit(&tfull[acc]);
+                    if (++acc == 2) {
+                        acc = 0;
+                        acc_phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else {
+        // ===== epilogue: warps 2..9 =====
+        const int lg = warp & 3;            // TMEM lane group this warp may access
+        const int ch = (warp - 2) >> 2;     // column half: 0 -> cols 0..63, 1 -> 64..127
+        const int r = lg * 32 + lane;       // tile row (TMEM lane)
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+            OzProblem pr;
+            int m0, n0;
+            decode(t, pr, m0, n0);
+            if (skip_tile(pr, m0, n0)) continue;
+            int sa, sb;
+            digits_of(p, pr, sa, sb);
+            double sum[64];
+#pragma unroll
+            for (int j = 0; j < 64; ++j) sum[j] = 0.0;
+            for (int g = sa + sb; g >= 2; --g) {
+                ptx::mbar_wait(&tfull[acc], acc_phase);
+                ptx::tc_fence_after();
+                const double w = __longlong_as_double(static_cast<long long>(1023 - 12 - 7 * (g - 2)) << 52);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    uint32_t v[16];
+                    ptx::tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(lg * 32) << 16) +
+                                                static_cast<uint32_t>(acc * BN + ch * 64 + c * 16),
+                                            v);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        sum[c * 16 + j] = fma(w, static_cast<double>(static_cast<int32_t>(v[j])), sum[c * 16 + j]);
+                }
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&tempty[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+            // C = alpha * 2^(e_r + e_c) * sum + beta * C
+            const int row = m0 + r;
+            if (row < p.M) {
+                const int er = p.rexp_a[static_cast<int64_t>(pr.a_tile) * p.rexp_stride_a + row];
+                double* C = static_cast<double*>(pr.c);
+                const int32_t* ecol = p.rexp_b + static_cast<int64_t>(pr.b_tile) * p.rexp_stride_b;
+#pragma unroll
+                for (int j = 0; j < 64; ++j) {
+                    const int col = n0 + ch * 64 + j;
+                    if (col >= p.N || (pr.lower_only && row < col)) continue;
+                    const int ec = __ldg(ecol + col);
+                    double v;
+                    if (er == ROWEXP_NONFINITE || ec == ROWEXP_NONFINITE)
+                        v = __longlong_as_double(0x7ff8000000000000ll);
+                    else
+                        v = ldexp(sum[j], er + ec);
+                    double* cp = C + static_cast<int64_t>(col) * p.ldc + row;
+                    double out = p.alpha * v;
+                    if (p.beta != 0.0) out = fma(p.beta, *cp, out);
+                    *cp = out;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
+    }
+}
+
+// ---- digit slicing -------------------------------------------------------------
+
+// One CTA per 32-row stripe of one matrix: (1) row exponent e_r with
+// |x| < 2^e_r for the whole row (frexp of the row max; rows holding Inf/NaN
+// get ROWEXP_NONFINITE, their products become NaN), (2) the digits, one
+// 32 x 128 block at a time, each thread writing 16 consecutive digits of one
+// row per plane (16-byte stores).
+__global__ void __launch_bounds__(256) oz_slice_kernel(const OzSliceItem* items) {
+    const OzSliceItem it = items[blockIdx.y];
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
+    if (r0 >= it.rows) return;
+    const uint16_t* x = static_cast<const uint16_t*>(it.x);
+    __shared__ uint16_t sx[32][128 + 2];
+    __shared__ uint32_t smax[8][33];
+    __shared__ int sexp[32];
+    auto at = [&](int64_t r, int64_t c) -> uint16_t {
+        return it.trans ? x[r * it.ld + c] : x[c * it.ld + r];
+    };
+    // column-major stripes of 32 full rows, 16-byte aligned: 8 rows per load
+    const bool vec = !it.trans && r0 + 32 <= it.rows && (it.ld % 8) == 0 &&
+                     (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    if (vec) {
+        if (threadIdx.x < 32) {
+            smax[0][threadIdx.x] = 0;
+            smax[1][threadIdx.x] = 31;
+        }
+        __syncthreads();
+        const int rg = threadIdx.x % 4;  // rows rg*8 .. rg*8+7
+        uint32_t mx[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        uint32_t mn[8] = {31, 31, 31, 31, 31, 31, 31, 31};  // min exponent field of nonzeros
+#pragma unroll 4
+        for (int64_t c = threadIdx.x / 4; c < it.cols; c += 64) {
+            const uint4 v = *reinterpret_cast<const uint4*>(x + c * it.ld + r0 + rg * 8);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t lo = w[q] & 0x7fffu, hi = (w[q] >> 16) & 0x7fffu;
+                mx[2 * q] = max(mx[2 * q], lo);
+                mx[2 * q + 1] = max(mx[2 * q + 1], hi);
+                if (lo) mn[2 * q] = min(mn[2 * q], max(lo >> 10, 1u));
+                if (hi) mn[2 * q + 1] = min(mn[2 * q + 1], max(hi >> 10, 1u));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            atomicMax(&smax[0][rg * 8 + j], mx[j]);
+            atomicMin(&smax[1][rg * 8 + j], mn[j]);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const uint32_t m = smax[0][threadIdx.x];
+            int e = 0, need = 0;
+            if (m >= 0x7c00u) {
+                e = ROWEXP_NONFINITE;
+            } else if (m != 0) {
+                frexp(h2d(static_cast<uint16_t>(m)), &e);
+                // lowest set bit of the row is >= 2^(minexp - 25); digits reach
+                // 2^(e - 6 - 7 (S - 1))
+                const int lsb = static_cast<int>(smax[1][threadIdx.x]) - 25;
+                need = 1 + (max(0, e - 6 - lsb) + 6) / 7;
+            }
+            sexp[threadIdx.x] = e;
+            it.rexp[r0 + threadIdx.x] = e;
+            if (it.ndig) {
+                for (int o = 16; o; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
+                if (threadIdx.x == 0) atomicMax(it.ndig, min(need, S));
+            }
+        }
+        __syncthreads();
+    } else {
+        // (1) row max of |x| as FP16 magnitude bits (monotone in the value)
+        int lr, cs;
+        if (!it.trans) {  // warp = 32 consecutive rows of one column
+            lr = threadIdx.x % 32;
+            cs = threadIdx.x / 32;
+        } else {  // warp = 32 consecutive columns of ... 8 threads per row chunk
+            lr = threadIdx.x / 8;
+            cs = threadIdx.x % 8;
+        }
+        const int64_t r = r0 + lr;
+        uint32_t mx = 0;
+        if (r < it.rows)
+            for (int64_t c = cs; c < it.cols; c += 8) mx = max(mx, static_cast<uint32_t>(at(r, c) & 0x7fff));
+        smax[cs][lr] = mx;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            uint32_t m = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) m = max(m, smax[q][threadIdx.x]);
+            int e = 0;
+            if (m >= 0x7c00u)
+                e = ROWEXP_NONFINITE;
+            else if (m != 0)
+                frexp(h2d(static_cast<uint16_t>(m)), &e);
+            sexp[threadIdx.x] = e;
+            if (r0 + threadIdx.x < it.rows) it.rexp[r0 + threadIdx.x] = e;
+            if (it.ndig && threadIdx.x == 0) atomicMax(it.ndig, S);  // no digit analysis here
+        }
+        __syncthreads();
+    }
+    // (2) digits
+    const int lr = threadIdx.x / 8, cg = (threadIdx.x % 8) * 16;
+    const int64_t gr = r0 + lr;
+    const int er = sexp[lr];
+    const bool zero = er == ROWEXP_NONFINITE;
+    for (int64_t c0 = 0; c0 < it.kpad; c0 += 128) {
+        if (vec) {
+            for (int e = threadIdx.x; e < 128 * 4; e += 256) {  // 128 columns x 4 row groups
+                const int b = e / 4, rg = e % 4;
+                const int64_t cc = c0 + b;
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (cc < it.cols) v = *reinterpret_cast<const uint4*>(x + cc * it.ld + r0 + rg * 8);
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    sx[rg * 8 + 2 * q][b] = static_cast<uint16_t>(w[q] & 0xffffu);
+                    sx[rg * 8 + 2 * q + 1][b] = static_cast<uint16_t>(w[q] >> 16);
+                }
+            }
+        } else
+        for (int e = threadIdx.x; e < 32 * 128; e += 256) {
+            int a, b;
+            if (!it.trans) {
+                a = e % 32;
+                b = e / 32;
+            } else {
+                b = e % 128;
+                a = e / 128;
+            }
+            const int64_t rr = r0 + a, cc = c0 + b;
+            sx[a][b] = (rr < it.rows && cc < it.cols) ? at(rr, cc) : static_cast<uint16_t>(0);
+        }
+        __syncthreads();
+        if (gr < it.rows && c0 + cg < it.kpad) {
+            alignas(16) int8_t dig[S][16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                double y = zero ? 0.0 : ldexp(h2d(sx[lr][cg + j]), 6 - er);  // |y| < 64, exact
+#pragma unroll
+                for (int d = 0; d < S; ++d) {
+                    const double q = rint(y);
+                    dig[d][j] = static_cast<int8_t>(q);
+                    y = (y - q) * 128.0;  // exact: y - q in [-1/2, 1/2], at most 41 bits
+                }
+            }
+            int8_t* out = static_cast<int8_t*>(it.out) + gr * it.kpad + c0 + cg;
+#pragma unroll
+            for (int d = 0; d < S; ++d)
+                *reinterpret_cast<int4*>(out + d * it.slice_stride) = *reinterpret_cast<const int4*>(dig[d]);
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace oz
+
+void launch_oz_slices(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_t count, int64_t max_rows,
+                      int64_t /*max_cols*/) {
+    if (count == 0) return;
+    ProfScope ps(ctx, MP_PROF_CAST, s, 0.0);
+    oz::oz_slice_kernel<<<dim3(static_cast<unsigned>((max_rows + 31) / 32), static_cast<unsigned>(count)), 256,
+                          0, s>>>(items);
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+void launch_oz_gemm(Ctx* ctx, cudaStream_t s, const OzGemm& g) {
+    using namespace oz;
+    Params p;
+    std::memset(&p, 0, sizeof(p));
+    // [tiles * S][rows][K] int8 digits, rows kpad bytes apart
+    tma_map_3d(&p.map_a, g.A, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.k, g.m, g.a_tiles * S, g.kpad,
+               g.a_slice_stride, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+    tma_map_3d(&p.map_b, g.B, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.k, g.n, g.b_tiles * S, g.kpad,
+               g.b_slice_stride, BK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+    p.problems = g.problems;
+    p.single = OzProblem{0, 0, g.C, g.lower_only ? 1 : 0};
+    p.nprob = g.problems ? static_cast<int32_t>(g.count) : 1;
+    p.M = static_cast<int32_t>(g.m);
+    p.N = static_cast<int32_t>(g.n);
+    p.K = static_cast<int32_t>(g.k);
+    p.mblocks = static_cast<int32_t>((g.m + BM - 1) / BM);
+    p.nblocks = static_cast<int32_t>((g.n + BN - 1) / BN);
+    p.kblocks = static_cast<int32_t>((g.k + BK - 1) / BK);
+    p.ldc = g.ldc;
+    p.alpha = g.alpha;
+    p.beta = g.beta;
+    p.rexp_a = g.rexp_a;
+    p.rexp_b = g.rexp_b;
+    p.rexp_stride_a = g.rexp_stride_a;
+    p.rexp_stride_b = g.rexp_stride_b;
+    p.ndig_a = g.ndig_a;
+    p.ndig_b = g.ndig_b;
+    const int64_t total = static_cast<int64_t>(p.nprob) * p.mblocks * p.nblocks;
+    ProfScope ps(ctx, MP_PROF_GEMM_F64, s,
+                 2.0 * static_cast<double>(g.m) * g.n * g.k * p.nprob * (g.lower_only ? 0.5 : 1.0));
+    static bool configured = false;
+    if (!configured) {
+        MP_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        configured = true;
+    }
+    int64_t grid = std::min<int64_t>(total, ctx->sm_count);
+    if (g.tiles_per_cta > 0) grid = std::max<int64_t>(grid, (total + g.tiles_per_cta - 1) / g.tiles_per_cta);
+    oz_gemm_kernel<<<static_cast<unsigned>(std::max<int64_t>(grid, 1)), NTHREADS, SMEM_BYTES, s>>>(p);
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+}  // namespace mpcr

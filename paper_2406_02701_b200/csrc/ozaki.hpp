@@ -1,0 +1,65 @@
+// Host interface of the FP64-from-INT8 (Ozaki) GEMM for FP16-valued operands
+// (ozaki.cu).
+#pragma once
+
+#include <cstdint>
+
+#include "internal.hpp"
+
+namespace mpcr {
+
+constexpr int OZ_SLICES = 6;  // 6 x 7-bit digits: exact for any FP16 row
+
+// One problem of a grouped launch: digit tiles of A and B (indices into the
+// slabs), the FP64 C tile, lower triangle only (SYRK).
+struct OzProblem {
+    int32_t a_tile;
+    int32_t b_tile;
+    void* c;
+    int32_t lower_only;
+    int32_t pad;
+};
+
+// Slice one FP16 matrix (rows x cols, element (r, c) at x[c * ld + r], or
+// x[r * ld + c] when trans) into OZ_SLICES int8 digit planes [S][rows][kpad]
+// (planes slice_stride bytes apart) and per-row exponents rexp[rows].  The
+// number of planes that are not all zero (exactness needs only those) is
+// max-reduced into *ndig.
+struct OzSliceItem {
+    const void* x;
+    void* out;
+    int32_t* rexp;
+    int32_t* ndig;  // optional: atomicMax of the digits this matrix needs (pre-zeroed)
+    int64_t ld, rows, cols, kpad, slice_stride;
+    int32_t trans;
+    int32_t pad;
+};
+
+// C = alpha * A B^T + beta * C with A (m x k), B (n x k) given as digit slabs
+// [tiles][S][rows][kpad] and row exponents; C FP64 column-major (ldc).
+struct OzGemm {
+    const void* A = nullptr;
+    const void* B = nullptr;
+    int64_t a_tiles = 1, b_tiles = 1;
+    int64_t a_slice_stride = 0, b_slice_stride = 0;  // bytes between digit planes
+    int64_t kpad = 0;
+    int64_t m = 0, n = 0, k = 0;
+    void* C = nullptr;
+    int64_t ldc = 0;
+    double alpha = 1.0, beta = 0.0;
+    bool lower_only = false;
+    const OzProblem* problems = nullptr;  // device array (grouped) or nullptr
+    int64_t count = 0;
+    const int32_t* rexp_a = nullptr;
+    const int32_t* rexp_b = nullptr;
+    const int32_t* ndig_a = nullptr;  // optional digits needed per tile (<= OZ_SLICES)
+    const int32_t* ndig_b = nullptr;
+    int64_t rexp_stride_a = 0, rexp_stride_b = 0;  // between tiles
+    int tiles_per_cta = 0;
+};
+
+void launch_oz_slices(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_t count, int64_t max_rows,
+                      int64_t max_cols);
+void launch_oz_gemm(Ctx* ctx, cudaStream_t s, const OzGemm& g);
+
+}  // namespace mpcr

@@ -29,6 +29,7 @@
 #include "batch.hpp"
 #include "dist.hpp"
 #include "gemm_tc.hpp"
+#include "ozaki.hpp"
 #include "internal.hpp"
 
 using namespace mpcr;
@@ -44,6 +45,9 @@ struct mp_tile_s {
     // scheduler workspace (grown on demand)
     void* panel[3] = {nullptr, nullptr, nullptr};
     void* split32[2] = {nullptr, nullptr};  // 3xTF32 hi/lo of the FP32 panel
+    void* digits = nullptr;  // INT8 digit planes of FP16 panel tiles [2][tr][S][br][br]
+    int32_t* rexp = nullptr;  // their row exponents [2][tr][br]
+    int32_t* ndig = nullptr;  // digits each of them needs [2][tr]
     void* work = nullptr;  // FP64 nb x nb x 2 + FP32 nb x nb + Linv{H,S}
     void* lists = nullptr;
     size_t lists_bytes = 0;
@@ -72,6 +76,9 @@ struct mp_tile_s {
         }
         for (void* p : split32)
             if (p) cudaFree(p);
+        if (digits) cudaFree(digits);
+        if (rexp) cudaFree(rexp);
+        if (ndig) cudaFree(ndig);
         if (work) cudaFree(work);
         if (lists) cudaFree(lists);
         trtri_plan_destroy(trtri);
@@ -108,6 +115,11 @@ void ensure_panels(mp_tile_s& t) {
             MP_CUDA(cudaMalloc(&t.panel[q], 2 * static_cast<size_t>(t.tr) * t.tt() * elem_bytes((mp_precision)q)));
     for (auto& p : t.split32)
         if (!p) MP_CUDA(cudaMalloc(&p, 2 * static_cast<size_t>(t.tr) * t.tt() * 4));
+    if (!t.digits && ozaki_enabled()) {
+        MP_CUDA(cudaMalloc(&t.digits, 2 * static_cast<size_t>(t.tr) * OZ_SLICES * t.tt()));
+        MP_CUDA(cudaMalloc(&t.rexp, 2 * static_cast<size_t>(t.tr) * t.br * sizeof(int32_t)));
+        MP_CUDA(cudaMalloc(&t.ndig, 2 * static_cast<size_t>(t.tr) * sizeof(int32_t)));
+    }
     if (!t.work) {
         const size_t nn = static_cast<size_t>(t.br) * t.br;
         // FP64 work, FP64 Linv, FP32 work, FP32 LinvS, FP16 LinvH hi + lo, info
@@ -129,8 +141,8 @@ void append(std::vector<char>& buf, const std::vector<V>& v, size_t& off) {
 // Device work lists of one trailing-update part (offsets into the list
 // buffer + counts): tcgen05 FP16, tcgen05 3xTF32, SIMT/DMMA per precision.
 struct UpLists {
-    size_t tc = 0, tc16s = 0, tc32 = 0, p[3] = {0, 0, 0}, pn[2] = {0, 0};
-    int64_t n_tc = 0, n_tc16s = 0, n_tc32 = 0, n_p[3] = {0, 0, 0}, n_pn[2] = {0, 0};
+    size_t tc = 0, tc16s = 0, tc32 = 0, p[3] = {0, 0, 0}, pn[2] = {0, 0}, oz = 0;
+    int64_t n_tc = 0, n_tc16s = 0, n_tc32 = 0, n_p[3] = {0, 0, 0}, n_pn[2] = {0, 0}, n_oz = 0;
 };
 
 struct StepLists {
@@ -146,6 +158,8 @@ struct StepLists {
     int64_t n_cv[2][3][3] = {};
     size_t split32[2] = {0, 0};
     int64_t n_split32[2] = {0, 0};
+    size_t digits[2] = {0, 0};  // INT8 digit slicing of FP16 panel tiles (same split)
+    int64_t n_digits[2] = {0, 0};
     UpLists up[3];  // 0: tile column k+1 below the diagonal, 1: the rest, 2: tile (k+1, k+1)
     std::vector<std::pair<int, int>> bcasts;  // (i, root) panel broadcasts
 };
@@ -211,6 +225,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         std::vector<TcProblem> tc, tc16s, tc32;
         std::vector<TileProblem> p[3];
         std::vector<TileProblem> pn[2];  // FP64 tiles fed by FP16 / FP32 panels directly
+        std::vector<OzProblem> oz;       // FP64 tiles fed by FP16 panels: INT8 digit products
     };
     // FP32 tiles whose two panel tiles are both FP16: the FP16 tensor-core
     // GEMM with an FP32 accumulator/output (exact products; what 3xTF32
@@ -223,11 +238,23 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     auto native64 = [&](int64_t i, int64_t j, int64_t k) {
         return t.p(i, k) == t.p(j, k) && t.p(i, k) != MP_DOUBLE;
     };
+    // ... and when both are FP16, on the INT8 tensor cores (exact digits)
+    const bool oz_ok = tc_ok && (nb % 16) == 0 && ozaki_enabled();
+    auto ozaki64 = [&](int64_t i, int64_t j, int64_t k) {
+        return oz_ok && t.p(i, k) == MP_HALF && t.p(j, k) == MP_HALF;
+    };
+    const int64_t dig_tile = OZ_SLICES * tt;  // bytes of one tile's digit planes
+    auto dig = [&](int64_t i, int64_t k) -> int8_t* {
+        return static_cast<int8_t*>(t.digits) + ((k & 1) * NT + i) * dig_tile;
+    };
+    auto rex = [&](int64_t i, int64_t k) -> int32_t* { return t.rexp + ((k & 1) * NT + i) * nb; };
+    auto ndg = [&](int64_t i, int64_t k) -> int32_t* { return t.ndig + (k & 1) * NT + i; };
     struct StepAcc {
         std::vector<TcProblem> trsm_tc;
         std::vector<TileProblem> trsm_p[3];
         std::vector<CopyItem> wb[3], cv[2][3][3];
         std::vector<SplitItem> split32[2];
+        std::vector<OzSliceItem> digits[2];
         UpAcc up[3];
     };
     std::vector<StepAcc> acc(NT);
@@ -255,6 +282,15 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             const int h = need[0][r] ? 0 : need[1][r] ? 1 : -1;
             if (h >= 0) A.cv[h][q][r].push_back(CopyItem{pan(q, i, k), pan((mp_precision)r, i, k)});
         }
+        bool need_dig[2] = {false, false};
+        for (int64_t j = k + 1; j <= i; ++j)
+            if (t.has(i, j) && t.p(i, j) == MP_DOUBLE && ozaki64(i, j, k)) need_dig[j == k + 1 ? 0 : 1] = true;
+        for (int64_t m = i; m < NT; ++m)
+            if (t.has(m, i) && t.p(m, i) == MP_DOUBLE && ozaki64(m, i, k)) need_dig[i == k + 1 ? 0 : 1] = true;
+        const int hd = need_dig[0] ? 0 : need_dig[1] ? 1 : -1;
+        if (hd >= 0)
+            A.digits[hd].push_back(
+                OzSliceItem{pan(MP_HALF, i, k), dig(i, k), rex(i, k), ndg(i, k), nb, nb, nb, nb, tt, 0, 0});
         const int h32 = need[0][MP_SINGLE] ? 0 : need[1][MP_SINGLE] ? 1 : -1;
         if (tc_ok && h32 >= 0)  // FP32 consumers run 3xTF32 on hi/lo splits
             A.split32[h32].push_back(SplitItem{pan(MP_SINGLE, i, k), spl(0, i, k), spl(1, i, k)});
@@ -295,6 +331,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 else if (q == MP_SINGLE && tc_ok)
                     U.tc32.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
                                                static_cast<int32_t>(t.slot[j * NT + i]), lo});
+                else if (q == MP_DOUBLE && ozaki64(i, j, k))
+                    U.oz.push_back(OzProblem{static_cast<int32_t>(i), static_cast<int32_t>(j), t.ptr(i, j), lo, 0});
                 else if (q == MP_DOUBLE && native64(i, j, k)) {
                     const mp_precision pp = t.p(i, k);
                     U.pn[pp].push_back(TileProblem{pan(pp, i, k), pan(pp, j, k), t.ptr(i, j), lo, 0});
@@ -326,6 +364,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         for (int h = 0; h < 2; ++h) {
             append(buf, A.split32[h], L.split32[h]);
             L.n_split32[h] = A.split32[h].size();
+            append(buf, A.digits[h], L.digits[h]);
+            L.n_digits[h] = A.digits[h].size();
         }
         for (int w = 0; w < 3; ++w) {
             append(buf, A.up[w].tc, L.up[w].tc);
@@ -338,6 +378,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 append(buf, A.up[w].p[q], L.up[w].p[q]);
                 L.up[w].n_p[q] = A.up[w].p[q].size();
             }
+            append(buf, A.up[w].oz, L.up[w].oz);
+            L.up[w].n_oz = A.up[w].oz.size();
             for (int q = 0; q < 2; ++q) {
                 append(buf, A.up[w].pn[q], L.up[w].pn[q]);
                 L.up[w].n_pn[q] = A.up[w].pn[q].size();
@@ -389,6 +431,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         if (L.n_split32[h])
             launch_batched_split_tf32_t(c, st, reinterpret_cast<const SplitItem*>(dl + L.split32[h]),
                                         L.n_split32[h], nb);
+        if (L.n_digits[h])
+            launch_oz_slices(c, st, reinterpret_cast<const OzSliceItem*>(dl + L.digits[h]), L.n_digits[h], nb, nb);
     };
     // write the factor of tile column k back from the panel into the tiles
     auto write_back = [&](int64_t k, cudaStream_t st) {
@@ -401,6 +445,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
 
     auto panel_phase = [&](int64_t k, cudaStream_t st, cudaEvent_t before_trsm) {
         const StepLists& L = steps[k];
+        if (L.n_digits[0] + L.n_digits[1])  // digit counts of panel k are max-reduced
+            MP_CUDA(cudaMemsetAsync(ndg(0, k), 0, NT * sizeof(int32_t), st));
         const mp_precision pk = t.p(k, k);
         void* akk = t.ptr(k, k);
         if (!L.potrf) {
@@ -570,6 +616,24 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                               reinterpret_cast<const TileProblem*>(dl + U.p[q]), U.n_p[q]};
                 launch_grouped_gemm(c, st, g);
             }
+        if (U.n_oz) {  // FP64 tiles from FP16 panels: exact INT8 digit products
+            OzGemm o;
+            o.A = o.B = dig(0, k);
+            o.a_tiles = o.b_tiles = NT;
+            o.a_slice_stride = o.b_slice_stride = tt;
+            o.kpad = nb;
+            o.m = o.n = o.k = nb;
+            o.ldc = nb;
+            o.alpha = -1.0;
+            o.beta = 1.0;
+            o.problems = reinterpret_cast<const OzProblem*>(dl + U.oz);
+            o.count = U.n_oz;
+            o.rexp_a = o.rexp_b = rex(0, k);
+            o.ndig_a = o.ndig_b = ndg(0, k);
+            o.rexp_stride_a = o.rexp_stride_b = nb;
+            o.tiles_per_cta = tiles_per_cta;
+            launch_oz_gemm(c, st, o);
+        }
         for (int q = 0; q < 2; ++q)
             if (U.n_pn[q]) {
                 GroupedGemm g{(mp_precision)q, MP_DOUBLE, true, nb, nb, nb, nb, nb, nb, -1.0, 1.0,

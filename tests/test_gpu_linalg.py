@@ -288,3 +288,50 @@ def test_trsm_singular_and_solves(ctx, ref, rng):
             du = mp.MPArray.from_numpy(Lr.T.copy(), mp.Precision(pt), ctx)
             g = mp.linalg.backsolve(du, db)
             assert rel(g.to_numpy(), ref.trisolve(True, pt, pb, Lr.T, Br)) < 1e-5
+
+
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+def test_gemm_half_to_double_int8_digits(ctx, rng, ta, tb):
+    """FP16 x FP16 -> FP64 runs on the INT8 tensor cores with exact 7-bit
+    digit slicing (ozaki.cu): every digit product is exact, so against an
+    extended-precision sum of the exact FP16 products the error is a few FP64
+    roundings of the result, over a 2^-24 .. 2^14 dynamic range."""
+    import paper_2406_02701_b200 as mp
+    from oracle.oracle import round_to
+
+    for (m, n, k) in ((256, 256, 1024), (300, 200, 700), (67, 45, 33)):
+        def wide(shape):
+            v = rng.standard_normal(shape) * np.exp2(rng.integers(-20, 12, size=shape))
+            return round_to(v, H)
+        A = wide((k, m) if ta else (m, k))
+        B = wide((n, k) if tb else (k, n))
+        Cm = rng.standard_normal((m, n))
+        opA = A.T if ta else A
+        opB = B.T if tb else B
+        exact = opA.astype(np.longdouble) @ opB.astype(np.longdouble)
+        want = (-1.0 * exact + Cm.astype(np.longdouble))
+        da = mp.MPArray.from_numpy(A, mp.Precision.Half, ctx)
+        db = mp.MPArray.from_numpy(B, mp.Precision.Half, ctx)
+        dc = mp.MPArray.from_numpy(Cm, mp.Precision.Double, ctx)
+        mp.linalg.gemm(da, db, dc, ta, tb, -1.0, 1.0)
+        got = dc.to_numpy()
+        scale = np.abs(opA) @ np.abs(opB) + np.abs(Cm)
+        err = np.abs(got.astype(np.longdouble) - want) / scale
+        assert err.max() <= 16 * 2.0 ** -53, (m, n, k, float(err.max()))
+
+
+def test_gemm_half_to_double_nonfinite(ctx):
+    """Inf/NaN in an FP16 operand row propagate as NaN to that output row."""
+    import paper_2406_02701_b200 as mp
+
+    A = np.ones((128, 64))
+    A[5, 3] = np.inf
+    B = np.ones((64, 128))
+    da = mp.MPArray.from_numpy(A, mp.Precision.Half, ctx)
+    db = mp.MPArray.from_numpy(B, mp.Precision.Half, ctx)
+    dc = mp.MPArray.from_numpy(np.zeros((128, 128)), mp.Precision.Double, ctx)
+    mp.linalg.gemm(da, db, dc)
+    got = dc.to_numpy()
+    assert np.isnan(got[5]).all() or np.isinf(got[5]).all()
+    assert np.all(got[np.arange(128) != 5] == 64.0)
