@@ -39,6 +39,7 @@ struct GridBar {
 __device__ int g_trace_on = 0;
 __device__ long long g_trace[64 * 6];
 __device__ long long g_trace2[64 * 6];
+
 #define PTRACE2(kb, slot)                                                            \
     do {                                                                             \
         if (g_trace_on && blockIdx.x == 0 && threadIdx.x == 0 && (kb) < 64)          \
@@ -69,20 +70,41 @@ __device__ __forceinline__ void grid_sync(GridBar* bar, unsigned int nblocks) {
 }
 
 // acc(64x64 per CTA, 4x4 per thread) += P (64 x kk, ldp) * Q (64 x kk, ldq)^T
-// with P/Q rows limited to pr/qr valid rows.
+// with P/Q rows limited to pr/qr valid rows.  16-wide K slabs; the next
+// slab's global loads are in flight (registers) while the current one is
+// multiplied from shared memory.
 template <typename T>
 __device__ __forceinline__ void block_nt(T (&acc)[4][4], const T* P, int64_t ldp, int pr,
                                          const T* Q, int64_t ldq, int qr, int kk,
                                          T (*Ps)[PB + 1], T (*Qs)[PB + 1]) {
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-    for (int k0 = 0; k0 < kk; k0 += 16) {
-        for (int idx = threadIdx.x; idx < 16 * PB; idx += PT) {
-            const int r = idx % PB, c = idx / PB;
-            const int k = k0 + c;
-            Ps[c][r] = (r < pr && k < kk) ? P[k * ldp + r] : T(0);
-            Qs[c][r] = (r < qr && k < kk) ? Q[k * ldq + r] : T(0);
+    constexpr int PER = 16 * PB / PT;  // elements of each operand per thread and slab
+    T pa[PER], qa[PER];
+    auto gload = [&](int k0) {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int idx = threadIdx.x + q * PT;
+            const int r = idx % PB, k = k0 + idx / PB;
+            pa[q] = (r < pr && k < kk) ? P[k * ldp + r] : T(0);
+            qa[q] = (r < qr && k < kk) ? Q[k * ldq + r] : T(0);
         }
-        __syncthreads();
+    };
+    auto sstore = [&]() {
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int idx = threadIdx.x + q * PT;
+            Ps[idx / PB][idx % PB] = pa[q];
+            Qs[idx / PB][idx % PB] = qa[q];
+        }
+    };
+    const int nk = (kk + 15) / 16;
+    if (nk == 0) return;
+    gload(0);
+    sstore();
+    __syncthreads();
+    for (int sl = 0; sl < nk; ++sl) {
+        const bool more = sl + 1 < nk;
+        if (more) gload((sl + 1) * 16);
 #pragma unroll
         for (int c = 0; c < 16; ++c) {
             T a[4], b[4];
@@ -96,170 +118,14 @@ __device__ __forceinline__ void block_nt(T (&acc)[4][4], const T* P, int64_t ldp
                 for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
         }
         __syncthreads();
+        if (more) {
+            sstore();
+            __syncthreads();
+        }
     }
 }
 
-// ---- diagonal-block kernels (one CTA, 256 threads, D in shared memory) ----
-
-// Factor the bb x bb lower block D in place (64 = 4 x 16 column panels):
-// each 16x16 diagonal piece by one warp in registers with shuffles, the 16
-// columns below it by row-parallel substitution, then a rank-16 update of
-// the trailing lower triangle.  Pivot test as chol_kernel (`!(d > 0)`,
-// linalg.cpp:121).  Returns the failing local column or -1 (block-uniform).
-template <typename T>
-__device__ int factor_block(T (*D)[PB + 1], int bb, int* s_fail, T* s_inv) {
-    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-    if (tid == 0) *s_fail = -1;
-    __syncthreads();
-    for (int c0 = 0; c0 < bb; c0 += 16) {
-        const int w = min(16, bb - c0);
-        // (i) 16 x 16 diagonal piece: lane l holds row c0 + l in registers
-        if (warp == 0) {
-            T r[16];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) r[j] = (lane < w && j <= lane) ? D[c0 + lane][c0 + j] : T(0);
-            int fail = -1;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                if (j < w && fail < 0) {
-                    const T djj = __shfl_sync(0xffffffffu, r[j], j);
-                    if (!(djj > T(0))) {
-                        fail = j;
-                    } else {
-                        // one reciprocal per pivot instead of a divide per element
-                        const T inv = rsqrt(djj);  // MUFU seed + Newton, ~1 ulp
-                        const T sd = djj * inv;
-                        if (lane > j) r[j] = r[j] * inv;
-                        if (lane == j) {
-                            r[j] = sd;
-                            s_inv[c0 + j] = inv;
-                        }
-#pragma unroll
-                        for (int l = j + 1; l < 16; ++l) {
-                            const T v = __shfl_sync(0xffffffffu, r[j], l);  // L[l][j]
-                            if (lane >= l) r[l] -= r[j] * v;
-                        }
-                    }
-                }
-            }
-            if (lane < w) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    if (j <= lane) D[c0 + lane][c0 + j] = r[j];
-            }
-            if (lane == 0 && fail >= 0) *s_fail = c0 + fail;
-        }
-        __syncthreads();
-        if (*s_fail >= 0) return *s_fail;
-        // (ii) rows below: x * L_ss^T = D[i][c0..c0+w) by forward substitution
-        // (4 threads per row, each an interleaved quarter of every dot product)
-        {
-            // warp-uniform trip count: every lane takes part in the shuffles
-            const int part = tid % 4;
-            for (int base = c0 + w + (tid / 32) * 8; base < bb; base += PT / 4) {
-                const int i = base + (tid % 32) / 4;
-                const bool ok = i < bb;
-                T x[16];
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    if (j < w) {
-                        T s = T(0);
-#pragma unroll
-                        for (int t = 0; t < j; ++t)
-                            if ((t & 3) == part) s += x[t] * D[c0 + j][c0 + t];
-                        s += __shfl_xor_sync(0xffffffffu, s, 1);
-                        s += __shfl_xor_sync(0xffffffffu, s, 2);
-                        x[j] = ok ? (D[i][c0 + j] - s) * s_inv[c0 + j] : T(0);
-                    } else {
-                        x[j] = T(0);
-                    }
-                }
-                if (ok && part == 0)
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        if (j < w) D[i][c0 + j] = x[j];
-            }
-        }
-        __syncthreads();
-        // (iii) rank-w update of the trailing lower triangle; thread owns
-        // column oc and rows orow + 4q
-        const int oc = tid % PB, orow = tid / PB;
-        if (oc >= c0 + w && oc < bb) {
-            T lc[16];
-#pragma unroll
-            for (int t = 0; t < 16; ++t) lc[t] = t < w ? D[oc][c0 + t] : T(0);
-#pragma unroll 4
-            for (int q = 0; q < PB / 4; ++q) {
-                const int r = orow + 4 * q;
-                if (r >= oc && r < bb) {
-                    T s = D[r][oc];
-#pragma unroll
-                    for (int t = 0; t < 16; ++t) s -= D[r][c0 + t] * lc[t];
-                    D[r][oc] = s;
-                }
-            }
-        }
-        __syncthreads();
-    }
-    return -1;
-}
-
-// X = D^-1 for the bb x bb lower block (zeros above the diagonal):
-// 16x16 diagonal inverses per warp, then off-diagonal 16-blocks by distance,
-// X_ij = -X_ii * sum_{j<=t<i} D_it X_tj.  Uses Tm (16 x 16 x 3 scratch).
-template <typename T>
-__device__ void invert_block(const T (*D)[PB + 1], T (*X)[PB + 1], T* Tm, int bb, const T* s_inv) {
-    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-    for (int idx = tid; idx < PB * PB; idx += PT) X[idx % PB][idx / PB] = T(0);
-    __syncthreads();
-    const int nsb = (bb + 15) / 16;
-    if (warp < nsb && lane < 16) {
-        const int b0 = warp * 16, w = min(16, bb - b0);
-        const int c = lane;  // column of the 16 x 16 inverse
-        T x[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            T v = T(0);
-            if (i < w && c < w && i >= c) {
-                T s = (i == c) ? T(1) : T(0);
-#pragma unroll
-                for (int t = 0; t < i; ++t)
-                    if (t >= c) s -= D[b0 + i][b0 + t] * x[t];
-                v = s * s_inv[b0 + i];
-            }
-            x[i] = v;
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-            if (i < w && c < w) X[b0 + i][b0 + c] = x[i];
-    }
-    __syncthreads();
-    for (int d = 1; d < nsb; ++d) {
-        const int nblk = nsb - d;  // blocks (i, i - d)
-        // T_b = sum_{t=j}^{i-1} D_it X_tj   (16 x 16 each)
-        for (int e = tid; e < nblk * 256; e += PT) {
-            const int b = e / 256, r = (e % 256) % 16, cc = (e % 256) / 16;
-            const int bi = b + d, bj = b;
-            const int row = bi * 16 + r, col = bj * 16 + cc;
-            T s = T(0);
-            if (row < bb && col < bb)
-                for (int t = bj * 16; t < bi * 16; ++t) s += D[row][t] * X[t][col];
-            Tm[e] = s;
-        }
-        __syncthreads();
-        for (int e = tid; e < nblk * 256; e += PT) {
-            const int b = e / 256, r = (e % 256) % 16, cc = (e % 256) / 16;
-            const int bi = b + d, bj = b;
-            const int row = bi * 16 + r, col = bj * 16 + cc;
-            if (row < bb && col < bb) {
-                T s = T(0);
-                for (int t = 0; t < 16; ++t) s += X[row][bi * 16 + t] * Tm[b * 256 + cc * 16 + t];
-                X[row][col] = -s;
-            }
-        }
-        __syncthreads();
-    }
-}
+#include "potrf_block.cuh"
 
 // Factor diagonal block kb (already fully updated) held in global A: load,
 // factor, invert; write L_kk back, Dinv to `dinv` (and to linv_diag).
@@ -276,7 +142,7 @@ __device__ void diag_step(T* A, int64_t lda, int n, int kb, T* dinv, T* linv_dia
     __syncthreads();
     PTRACE2(kb, 1);
     __shared__ T s_inv[PB];  // reciprocals of the pivots
-    const int fail = factor_block(D, bb, s_fail, s_inv);
+    const int fail = factor_block(D, X, bb, s_fail, s_inv);
     PTRACE2(kb, 2);
     if (fail >= 0) {
         if (threadIdx.x == 0) {
