@@ -368,9 +368,7 @@ void launch_kernel(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total, int
         MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
         configured = true;
     }
-    int64_t g = total < ctx->sm_count ? total : ctx->sm_count;
-    if (tiles_per_cta > 0) g = std::max<int64_t>(g, (total + tiles_per_cta - 1) / tiles_per_cta);
-    int grid = static_cast<int>(std::min<int64_t>(std::max<int64_t>(g, 1), 1 << 30));
+    const int grid = static_cast<int>(std::min<int64_t>(persistent_grid(total, ctx->sm_count, tiles_per_cta), 1 << 30));
     kern<<<grid, 256, SMEM_BYTES, s>>>(p);
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());

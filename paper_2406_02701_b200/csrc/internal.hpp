@@ -144,6 +144,18 @@ struct GemmDesc {
     bool lower_only = false;
 };
 void launch_gemm(Ctx* ctx, cudaStream_t s, const GemmDesc& g);
+// Grid of a persistent tile kernel (one CTA per SM resident): fully
+// persistent when tiles_per_cta <= 0, else whole waves of SMs with at most
+// ~tiles_per_cta tiles per CTA (so SMs are handed back at that granularity
+// without a ragged last wave).
+inline int64_t persistent_grid(int64_t total, int sms, int tiles_per_cta) {
+    if (total <= sms) return total < 1 ? 1 : total;
+    if (tiles_per_cta <= 0) return sms;
+    const int64_t waves = (total + static_cast<int64_t>(sms) * tiles_per_cta - 1) /
+                          (static_cast<int64_t>(sms) * tiles_per_cta);
+    const int64_t g = waves * sms;
+    return g < total ? g : total;
+}
 bool ozaki_enabled();  // MPCR_OZAKI=0 turns the INT8 FP64 path off
 
 // Grouped tile GEMM used by the MPCRTile scheduler: every problem is

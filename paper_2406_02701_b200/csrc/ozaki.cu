@@ -21,7 +21,7 @@
 //   warp 0      TMA producer: 6-stage ring of {A 128x128, B 128x128} int8 digit
 //               tiles (128B swizzle).
 //   warp 1      TMEM allocator + MMA issuer: tcgen05.mma kind::i8 (M=128,
-//               N=128, K=32) into a double-buffered int32 accumulator; the 36
+//               N=128, K=32) into 4 rotating int32 TMEM accumulators; the 36
 //               digit pairs are issued grouped by t = p + q (11 groups, all
 //               pairs of a group share the scale 2^(-12-7(t-2)) and one
 //               accumulator), smallest magnitude first.
@@ -46,8 +46,9 @@ namespace oz {
 constexpr int S = OZ_SLICES;  // digits per value
 constexpr int BM = 128, BN = 128, BK = 128, STAGES = 6;
 constexpr int A_STAGE = BM * BK, B_STAGE = BN * BK;  // 16 KB each
-constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 + 256;
-constexpr int TMEM_COLS = 256;  // 2 x 128 int32 accumulators
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 + 256;  // + barriers
+constexpr int NACC = 4;          // int32 accumulators in flight (MMA runs NACC groups ahead)
+constexpr int TMEM_COLS = 512;  // NACC x 128 columns
 constexpr int NTHREADS = 320;   // 10 warps
 constexpr int ROWEXP_NONFINITE = 0x7fffffff;
 
@@ -103,8 +104,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tempty = tfull + NACC;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (warp == 0 && lane == 0) {
@@ -114,7 +115,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], 1);
         }
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < NACC; ++s) {
             ptx::mbar_init(&tfull[s], 1);
             ptx::mbar_init(&tempty[s], 256);
         }
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                             }
                         }
                     ptx::mma_commit(&tfull[acc]);
-                    if (++acc == 2) {
+                    if (++acc == NACC) {
                         acc = 0;
                         acc_phase ^= 1;
                     }
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                 }
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&tempty[acc]);
-                if (++acc == 2) {
+                if (++acc == NACC) {
                     acc = 0;
                     acc_phase ^= 1;
                 }
@@ -483,8 +484,7 @@ void launch_oz_gemm(Ctx* ctx, cudaStream_t s, const OzGemm& g) {
         MP_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
         configured = true;
     }
-    int64_t grid = std::min<int64_t>(total, ctx->sm_count);
-    if (g.tiles_per_cta > 0) grid = std::max<int64_t>(grid, (total + g.tiles_per_cta - 1) / g.tiles_per_cta);
+    const int64_t grid = persistent_grid(total, ctx->sm_count, g.tiles_per_cta);
     oz_gemm_kernel<<<static_cast<unsigned>(std::max<int64_t>(grid, 1)), NTHREADS, SMEM_BYTES, s>>>(p);
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());

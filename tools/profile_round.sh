@@ -1,11 +1,17 @@
 #!/bin/bash
-# Runs on the GPU box: plain bench, then the ncu launch list of the same
-# command, then one full capture of the dominant kernel.  Outputs in gpurun_out/.
+# Runs on the GPU box: the default bench line, then (same command, plain run
+# first) the ncu launch list, then one full capture each of the two dominant
+# kernels (FP16 trailing update, INT8-digit FP64 SYRK).  Outputs in gpurun_out/.
 set -u
 OUT=gpurun_out
-CMD="python bench.py --steps 1 --warmup 1 --no-cpu --no-e2e"
+mkdir -p $OUT
+python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err
+CMD="python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e"
 $CMD > $OUT/prof_plain.log 2>&1 || { echo "plain run failed"; exit 1; }
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launch.log 2>&1
-$CMD > $OUT/prof_plain2.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:gemm_tc_kernel -s 40 -c 1 -o $OUT/tc_full $CMD > $OUT/ncu_full.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD \
+    > $OUT/ncu_launch.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:'gemm_tc_kernel<0' -s 200 -c 1 \
+    -o $OUT/tc_full $CMD > $OUT/ncu_full_tc.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:oz_gemm_kernel -s 20 -c 1 \
+    -o $OUT/oz_full $CMD > $OUT/ncu_full_oz.log 2>&1
 echo done
