@@ -24,6 +24,7 @@
 // tiles of a slab by index.
 #include <algorithm>
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include <cstring>
 #include <mutex>
@@ -63,14 +64,21 @@ __device__ __forceinline__ bool skip_tile(const TcProblem& pr, int m0, int n0) {
     return pr.lower_only && (m0 + BM - 1 < n0);
 }
 
-__device__ __forceinline__ float ld_c(const uint16_t* c, int i) { return h2f(c[i]); }
+// Epilogue conversions use the hardware cvt (round-to-nearest-even, IEEE
+// subnormals and overflow to Inf — the reference's encode_f16 for every
+// non-NaN value); the bit-exact software path (device.cuh) is kept for the
+// cast kernels, where NaN payloads must match the reference too.
+__device__ __forceinline__ float ld_c(const uint16_t* c, int i) { return __half2float(__ushort_as_half(c[i])); }
 __device__ __forceinline__ float ld_c(const float* c, int i) { return c[i]; }
-__device__ __forceinline__ void st_c(uint16_t* c, int i, float v) { c[i] = f2h(v); }
+__device__ __forceinline__ void st_c(uint16_t* c, int i, float v) { c[i] = __half_as_ushort(__float2half_rn(v)); }
 __device__ __forceinline__ void st_c(float* c, int i, float v) { c[i] = v; }
 
 // KIND 0: kind::f16 (FP16 operands), KIND 1: kind::tf32 (FP32 storage).
+constexpr int NTHREADS = 256;  // 4 role warps + 4 epilogue warps
+constexpr int EPI_THREADS = 128;
+
 template <int KIND, bool A_MN, bool B_MN, typename TC>
-__global__ void __launch_bounds__(256, 1) gemm_tc_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_constant__ Params p) {
     constexpr int ES = KIND == 0 ? 2 : 4;      // operand element bytes
     constexpr int BK = 128 / ES;               // K elements per stage
     constexpr int BW = 128 / ES;               // MN elements per 128B swizzle row
@@ -106,7 +114,7 @@ __global__ void __launch_bounds__(256, 1) gemm_tc_kernel(const __grid_constant__
         }
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&tfull[s], 1);
-            ptx::mbar_init(&tempty[s], 128);
+            ptx::mbar_init(&tempty[s], EPI_THREADS);
         }
         ptx::mbar_init(cfull, 1);
         ptx::mbar_init(cempty, 1);
@@ -241,7 +249,7 @@ __global__ void __launch_bounds__(256, 1) gemm_tc_kernel(const __grid_constant__
         }
     } else if (warp >= 4) {
         // ===== epilogue =====
-        const int q = warp - 4;
+        const int q = warp - 4;  // TMEM lane group this warp may access
         const int r = q * 32 + lane;  // tile row owned by this thread (TMEM lane)
         const bool is_leader = threadIdx.x == 128;
         int acc = 0;
@@ -281,7 +289,7 @@ __global__ void __launch_bounds__(256, 1) gemm_tc_kernel(const __grid_constant__
                 }
                 // chunk complete: hand it to the TMA unit, then release it
                 ptx::fence_proxy_async_smem();
-                ptx::named_bar_sync(1, 128);
+                ptx::named_bar_sync(1, EPI_THREADS);
                 if (is_leader) {
                     ptx::tma_store_3d(&p.map_c, cbuf, m0, n0 + h * CW, pr.c_tile);
                     ptx::bulk_commit();
@@ -369,7 +377,7 @@ void launch_kernel(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total, int
         configured = true;
     }
     const int grid = static_cast<int>(std::min<int64_t>(persistent_grid(total, ctx->sm_count, tiles_per_cta), 1 << 30));
-    kern<<<grid, 256, SMEM_BYTES, s>>>(p);
+    kern<<<grid, NTHREADS, SMEM_BYTES, s>>>(p);
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());
 }
