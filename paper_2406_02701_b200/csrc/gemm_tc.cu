@@ -88,8 +88,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
     constexpr int CW = 256 / sizeof(TC);  // chunk width in columns (128 half / 64 float)
     constexpr int NCHUNK = BN / CW;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~static_cast<uintptr_t>(1023));
+    // 1024-byte alignment (128B swizzle atoms) by an offset from the shared
+    // array itself, so the compiler keeps shared-space addressing (LDS/STS)
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_STAGE;
     TC* cbuf = reinterpret_cast<TC*>(sB + STAGES * B_STAGE);  // [CW cols][BM rows]
