@@ -270,6 +270,63 @@ __global__ void matern_points_kernel(ST<P>* __restrict__ dst, int64_t ld, int64_
     }
 }
 
+// Batched symmetric generation for MPCRTile: one launch over the lower tiles
+// (i >= j); a CTA computes a 32 x 32 block of tile (i, j) once and stores it
+// to (i, j) and, transposed through shared memory, to (j, i) (each in its own
+// precision, rounded from the double value as set_linear does).
+struct MaternItem {
+    void* lo;        // tile (i, j), column-major, ld = rows
+    void* up;        // tile (j, i) or nullptr (diagonal / not stored here)
+    int32_t p_lo, p_up;
+    int64_t row0, col0;  // global row of tile row 0 / column of tile column 0
+};
+
+__device__ __forceinline__ void store_any(void* base, int p, int64_t i, double v) {
+    if (p == MP_HALF) store_from(static_cast<uint16_t*>(base), i, v);
+    else if (p == MP_SINGLE) store_from(static_cast<float*>(base), i, v);
+    else static_cast<double*>(base)[i] = v;
+}
+
+template <bool GRID>
+__global__ void __launch_bounds__(256) matern_tiles_kernel(const MaternItem* __restrict__ items, int64_t nb,
+                                                           const double* __restrict__ x,
+                                                           const double* __restrict__ y, int64_t side,
+                                                           double nu, double range, double var,
+                                                           double nugget) {
+    const MaternItem it = items[blockIdx.y];
+    const int64_t bpr = nb / 32;  // 32 x 32 blocks per tile row
+    const int64_t bi = blockIdx.x % bpr, bj = blockIdx.x / bpr;
+    __shared__ double sv[32][33];
+    const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 8 row-groups of 32 lanes
+    const double den = static_cast<double>(side - 1);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int lj = ty + 8 * q;                    // column within the block
+        const int64_t i = bi * 32 + tx, j = bj * 32 + lj;  // within the tile
+        const int64_t pi = it.row0 + i, pj = it.col0 + j;
+        double v;
+        if (GRID) {
+            const double dx = static_cast<double>(pi % side) / den - static_cast<double>(pj % side) / den;
+            const double dy = static_cast<double>(pi / side) / den - static_cast<double>(pj / side) / den;
+            v = matern_value(hypot(dx, dy), nu, range, var);
+        } else {
+            v = matern_value(hypot(x[pi] - x[pj], y[pi] - y[pj]), nu, range, var);
+            if (pi == pj) v += nugget;
+        }
+        store_any(it.lo, it.p_lo, j * nb + i, v);
+        sv[lj][tx] = v;
+    }
+    if (!it.up) return;
+    __syncthreads();
+    // (j, i) tile: element (row = global col pj, col = global row pi) = same value
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int li = ty + 8 * q;  // becomes the column of the transposed block
+        const int64_t r = bj * 32 + tx, c = bi * 32 + li;
+        store_any(it.up, it.p_up, c * nb + r, sv[tx][li]);
+    }
+}
+
 template <typename F>
 void dispatch_p(mp_precision p, F&& f) {
     if (p == MP_HALF) f(std::integral_constant<int, 0>{});
@@ -443,6 +500,26 @@ void launch_matern_tile(Ctx* ctx, cudaStream_t s, mp_precision p, void* dst, int
 }  // namespace mpcr
 
 namespace mpcr {
+void launch_matern_tiles(Ctx* ctx, cudaStream_t s, const void* items, int64_t count, int64_t nb,
+                         const double* x, const double* y, int64_t side, double nu, double range,
+                         double variance, double nugget) {
+    if (count == 0) return;
+    if (nb % 32) fail(MP_INVALID_PARAM, "matern: batched generation needs tiles of a multiple of 32");
+    const dim3 g(static_cast<unsigned>((nb / 32) * (nb / 32)), static_cast<unsigned>(count));
+    const auto* it = static_cast<const MaternItem*>(items);
+    if (x)
+        matern_tiles_kernel<false><<<g, 256, 0, s>>>(it, nb, x, y, side, nu, range, variance, nugget);
+    else
+        matern_tiles_kernel<true><<<g, 256, 0, s>>>(it, nb, x, y, side, nu, range, variance, nugget);
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+size_t matern_item_bytes() { return sizeof(MaternItem); }
+void matern_item_fill(void* dst, void* lo, void* up, int p_lo, int p_up, int64_t row0, int64_t col0) {
+    *static_cast<MaternItem*>(dst) = MaternItem{lo, up, p_lo, p_up, row0, col0};
+}
+
 void launch_matern_points(Ctx* ctx, cudaStream_t s, mp_precision p, void* dst, int64_t ld,
                           int64_t row0, int64_t col0, int64_t rows, int64_t cols, const double* x,
                           const double* y, double nu, double range, double variance,

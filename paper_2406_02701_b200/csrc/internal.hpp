@@ -224,6 +224,13 @@ void launch_matern_tile(Ctx* ctx, cudaStream_t s, mp_precision p, void* dst, int
                         int64_t row0, int64_t col0, int64_t rows, int64_t cols,
                         int64_t side, double nu, double range, double variance);
 
+// Batched symmetric Matern fill of square nb-tiles (items built with
+// matern_item_fill); x == nullptr selects the unit grid of `side` points.
+void launch_matern_tiles(Ctx* ctx, cudaStream_t s, const void* items, int64_t count, int64_t nb,
+                         const double* x, const double* y, int64_t side, double nu, double range,
+                         double variance, double nugget);
+size_t matern_item_bytes();
+void matern_item_fill(void* dst, void* lo, void* up, int p_lo, int p_up, int64_t row0, int64_t col0);
 void launch_matern_points(Ctx* ctx, cudaStream_t s, mp_precision p, void* dst, int64_t ld,
                           int64_t row0, int64_t col0, int64_t rows, int64_t cols, const double* x,
                           const double* y, double nu, double range, double variance,

@@ -755,6 +755,36 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
 
 namespace {
 
+// Whole-matrix Matern fill in one launch (square tiles, nb % 32 == 0): each
+// lower tile (i, j) is computed once and also written, transposed, to (j, i).
+bool fill_matern_batched(Ctx* c, mp_tile_s& x, const double* dx, const double* dy, int64_t side, double nu,
+                         double range, double variance, double nugget) {
+    if (x.rows != x.cols || x.br != x.bc || x.br % 32) return false;
+    const size_t isz = matern_item_bytes();
+    std::vector<char> items;
+    for (int64_t j = 0; j < x.tc; ++j)
+        for (int64_t i = j; i < x.tr; ++i) {
+            void* lo = x.has(i, j) ? x.ptr(i, j) : nullptr;
+            void* up = (i != j && x.has(j, i)) ? x.ptr(j, i) : nullptr;
+            if (!lo && !up) continue;
+            if (!lo) {  // only the upper tile is stored here: generate it as the "lower" of (j, i)
+                items.resize(items.size() + isz);
+                matern_item_fill(items.data() + items.size() - isz, up, nullptr, x.p(j, i), 0, j * x.br,
+                                 i * x.br);
+                continue;
+            }
+            items.resize(items.size() + isz);
+            matern_item_fill(items.data() + items.size() - isz, lo, up, x.p(i, j), up ? x.p(j, i) : 0,
+                             i * x.br, j * x.br);
+        }
+    const int64_t count = static_cast<int64_t>(items.size() / isz);
+    if (count == 0) return true;
+    void* d = c->ensure_scratch(items.size(), 0);
+    MP_CUDA(cudaMemcpyAsync(d, items.data(), items.size(), cudaMemcpyHostToDevice, c->stream));
+    launch_matern_tiles(c, c->stream, d, count, x.br, dx, dy, side, nu, range, variance, nugget);
+    return true;
+}
+
 // Shared by mp_tile_create / mp_tile_create_dist: with `dist`, only the
 // lower-triangle tiles this rank owns get storage (slot -1 elsewhere).
 mp_tile_s* tile_new(Ctx* ctx, mp_dist_s* dist, int64_t rows, int64_t cols, int64_t rpt, int64_t cpt,
@@ -1105,11 +1135,12 @@ mp_status mp_tile_fill_matern(mp_ctx ctx, mp_tile t, int64_t side, double nu, do
     if (range <= 0.0 || variance <= 0.0)
         fail(MP_INVALID_PARAM, "matern_cov: range and variance must be positive");
     if (nu != 0.5 && nu != 1.5 && nu != 2.5) fail(MP_INVALID_PARAM, "matern_cov: nu must be 0.5, 1.5, or 2.5");
-    for (int64_t j = 0; j < x.tc; ++j)
-        for (int64_t i = 0; i < x.tr; ++i)
-            if (x.has(i, j))
-                launch_matern_tile(c, c->stream, x.p(i, j), x.ptr(i, j), x.br, i * x.br, j * x.bc, x.br,
-                               x.bc, side, nu, range, variance);
+    if (!fill_matern_batched(c, x, nullptr, nullptr, side, nu, range, variance, 0.0))
+        for (int64_t j = 0; j < x.tc; ++j)
+            for (int64_t i = 0; i < x.tr; ++i)
+                if (x.has(i, j))
+                    launch_matern_tile(c, c->stream, x.p(i, j), x.ptr(i, j), x.br, i * x.br, j * x.bc,
+                                       x.br, x.bc, side, nu, range, variance);
     MP_API_END
 }
 
@@ -1127,11 +1158,12 @@ mp_status mp_tile_fill_matern_points(mp_ctx ctx, mp_tile t, const double* host_x
     double* xy = static_cast<double*>(c->ensure_scratch(2 * n * sizeof(double), 1));
     MP_CUDA(cudaMemcpyAsync(xy, host_x, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     MP_CUDA(cudaMemcpyAsync(xy + n, host_y, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    for (int64_t j = 0; j < x.tc; ++j)
-        for (int64_t i = 0; i < x.tr; ++i)
-            if (x.has(i, j))
-                launch_matern_points(c, c->stream, x.p(i, j), x.ptr(i, j), x.br, i * x.br, j * x.bc,
-                                 x.br, x.bc, xy, xy + n, nu, range, variance, nugget);
+    if (!fill_matern_batched(c, x, xy, xy + n, 0, nu, range, variance, nugget))
+        for (int64_t j = 0; j < x.tc; ++j)
+            for (int64_t i = 0; i < x.tr; ++i)
+                if (x.has(i, j))
+                    launch_matern_points(c, c->stream, x.p(i, j), x.ptr(i, j), x.br, i * x.br, j * x.bc,
+                                         x.br, x.bc, xy, xy + n, nu, range, variance, nugget);
     MP_API_END
 }
 

@@ -7,6 +7,7 @@
 namespace bench {
 __device__ long long g_fb[8];
 __device__ long long g_last;
+#ifdef FB_TRACE
 #define FB_MARK(slot)                                   \
     do {                                                \
         if (threadIdx.x == 0) {                         \
@@ -15,6 +16,7 @@ __device__ long long g_last;
             g_last = now_;                              \
         }                                               \
     } while (0)
+#endif
 constexpr int PB = 64, PT = 256;
 #include "potrf_block.cuh"
 
