@@ -253,26 +253,38 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                     acc_phase ^= 1;
                 }
             }
-            // C = alpha * 2^(e_r + e_c) * sum + beta * C
+            // C = alpha * 2^(e_r + e_c) * sum + beta * C, 8 columns at a time:
+            // all loads of a chunk are issued before its stores (a store may
+            // alias a later load, so interleaving would serialise the misses)
             const int row = m0 + r;
             if (row < p.M) {
                 const int er = p.rexp_a[static_cast<int64_t>(pr.a_tile) * p.rexp_stride_a + row];
                 double* C = static_cast<double*>(pr.c);
                 const int32_t* ecol = p.rexp_b + static_cast<int64_t>(pr.b_tile) * p.rexp_stride_b;
 #pragma unroll
-                for (int j = 0; j < 64; ++j) {
-                    const int col = n0 + ch * 64 + j;
-                    if (col >= p.N || (pr.lower_only && row < col)) continue;
-                    const int ec = __ldg(ecol + col);
-                    double v;
-                    if (er == ROWEXP_NONFINITE || ec == ROWEXP_NONFINITE)
-                        v = __longlong_as_double(0x7ff8000000000000ll);
-                    else
-                        v = ldexp(sum[j], er + ec);
-                    double* cp = C + static_cast<int64_t>(col) * p.ldc + row;
-                    double out = p.alpha * v;
-                    if (p.beta != 0.0) out = fma(p.beta, *cp, out);
-                    *cp = out;
+                for (int jb = 0; jb < 64; jb += 8) {
+                    double cv[8];
+                    int ec[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int col = n0 + ch * 64 + jb + u;
+                        const bool ok = col < p.N && !(pr.lower_only && row < col);
+                        ec[u] = ok ? __ldg(ecol + col) : 0;
+                        cv[u] = (ok && p.beta != 0.0) ? C[static_cast<int64_t>(col) * p.ldc + row] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int col = n0 + ch * 64 + jb + u;
+                        if (col >= p.N || (pr.lower_only && row < col)) continue;
+                        double v;
+                        if (er == ROWEXP_NONFINITE || ec[u] == ROWEXP_NONFINITE)
+                            v = __longlong_as_double(0x7ff8000000000000ll);
+                        else
+                            v = ldexp(sum[jb + u], er + ec[u]);
+                        double out = p.alpha * v;
+                        if (p.beta != 0.0) out = fma(p.beta, cv[u], out);
+                        C[static_cast<int64_t>(col) * p.ldc + row] = out;
+                    }
                 }
             }
         }
