@@ -277,10 +277,22 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 3 : 1) dmma_gemm_ke
         if (next) land(kb + NST - 1);
     }
     if constexpr (WIDE) cp_wait<0>();
-    // epilogue: c[v0 + 2 v1] at (g + 8 v1, 2 t + v0)
+    // epilogue: c[v0 + 2 v1] at (g + 8 v1, 2 t + v0).  Per 16-row fragment
+    // row i, the 16 C loads are issued before any store (a store may alias a
+    // later load, so interleaving them would serialise the misses).
     const double alpha = g.alpha, beta = g.beta;
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 2; ++i) {
+        double cold[4][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int64_t gm = m0 + wm + i * 16 + gq + 8 * (v >> 1);
+                const int64_t gn = n0 + wn + j * 8 + 2 * tq + (v & 1);
+                const bool ok = gm < g.m && gn < g.n && !(pr.lower_only && gm < gn);
+                cold[j][v] = (ok && beta != 0.0) ? C[gn * g.ldc + gm] : 0.0;
+            }
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -288,12 +300,12 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 3 : 1) dmma_gemm_ke
                 const int64_t gm = m0 + wm + i * 16 + gq + 8 * (v >> 1);
                 const int64_t gn = n0 + wn + j * 8 + 2 * tq + (v & 1);
                 if (gm < g.m && gn < g.n && !(pr.lower_only && gm < gn)) {
-                    double* p = C + gn * g.ldc + gm;
                     double r = alpha * acc[i][j][v];
-                    if (beta != 0.0) r += beta * *p;
-                    *p = r;
+                    if (beta != 0.0) r += beta * cold[j][v];
+                    C[gn * g.ldc + gm] = r;
                 }
             }
+    }
 }
 
 
