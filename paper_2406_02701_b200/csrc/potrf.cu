@@ -230,6 +230,16 @@ __global__ void __launch_bounds__(PT) potrf_coop_kernel(T* A, int64_t lda, int n
             const int jb = kb + 1 + jj, ib = jb + rem;
             const int r0 = ib * PB, c0 = jb * PB;
             const int rb = min(PB, n - r0), cb = min(PB, n - c0);
+            // the block's old values are loaded while block_nt runs (no aliasing
+            // with its reads: different columns), all before any store
+            T old[4][4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int r = tx + 16 * i, c = ty + 16 * j;
+                    old[i][j] = (r < rb && c < cb) ? A[(int64_t)(c0 + c) * lda + r0 + r] : T(0);
+                }
             T acc[4][4] = {};
             block_nt(acc, A + (int64_t)k0 * lda + r0, lda, rb, A + (int64_t)k0 * lda + c0, lda, cb,
                      bb, Ps, Qs);
@@ -238,10 +248,8 @@ __global__ void __launch_bounds__(PT) potrf_coop_kernel(T* A, int64_t lda, int n
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int r = tx + 16 * i, c = ty + 16 * j;
-                    if (r < rb && c < cb && (ib != jb || r >= c)) {
-                        T* p = A + (int64_t)(c0 + c) * lda + r0 + r;
-                        *p = *p - acc[i][j];
-                    }
+                    if (r < rb && c < cb && (ib != jb || r >= c))
+                        A[(int64_t)(c0 + c) * lda + r0 + r] = old[i][j] - acc[i][j];
                 }
             __syncthreads();
         };
