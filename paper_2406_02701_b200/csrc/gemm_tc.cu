@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cuda_fp16.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -314,6 +315,247 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
     }
 }
 
+
+// ---- 2-CTA pair kernel (cta_group::2): 256 x 256 output tile per CTA pair ----
+// Same warp roles; each CTA of the pair loads its 128 rows of A and its 128
+// rows (half) of B per stage, so a CTA's shared-memory ingress per K step is
+// 32 KB instead of 48 KB for the same FLOPs.  The even CTA issues the pair
+// MMA (M=256, N=256); stage "full" barriers live in the even CTA, "empty"
+// barriers in both (multicast commit); each CTA's epilogue reads its own 128
+// TMEM lanes and signals the even CTA's tmem-empty barrier.
+constexpr int STAGES2 = 6;
+constexpr int B2_STAGE = (BN / 2) * 128;  // 16 KB
+constexpr int SMEM2_BYTES = STAGES2 * (A_STAGE + B2_STAGE) + C_CHUNK + 1024 + 256;
+
+template <bool A_MN, bool B_MN, typename TC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ Params p) {
+    constexpr int ES = 2, BK = 64, BW = 64;
+    constexpr int BOX = BW * BK * ES;          // 8 KB MN-major box
+    constexpr int KSTEP_MN = (32 / ES) * 128;  // UMMA K (32 bytes) in MN-major rows
+    constexpr int CW = 256 / sizeof(TC);
+    constexpr int NCHUNK = BN / CW;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES2 * A_STAGE;
+    TC* cbuf = reinterpret_cast<TC*>(sB + STAGES2 * B2_STAGE);
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(cbuf) + C_CHUNK);
+    uint64_t* empty = full + STAGES2;
+    uint64_t* tfull = empty + STAGES2;
+    uint64_t* tempty = tfull + 2;
+    uint64_t* cfull = tempty + 2;
+    uint64_t* cempty = cfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 1);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = ptx::cluster_ctarank();
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&p.map_a[0]);
+        ptx::tma_prefetch_desc(&p.map_a[1]);
+        ptx::tma_prefetch_desc(&p.map_b[0]);
+        ptx::tma_prefetch_desc(&p.map_b[1]);
+        ptx::tma_prefetch_desc(&p.map_c);
+        for (int s = 0; s < STAGES2; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            ptx::mbar_init(&tfull[s], 1);
+            ptx::mbar_init(&tempty[s], 2);  // one arrival per CTA of the pair
+        }
+        ptx::mbar_init(cfull, 1);
+        ptx::mbar_init(cempty, 1);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
+    ptx::tc_fence_before();
+    ptx::cluster_sync_all();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int mpairs = (p.mblocks + 1) / 2;  // an odd last block pairs with an out-of-range one
+    const int tiles_per_prob = mpairs * p.nblocks;
+    const int64_t total = static_cast<int64_t>(p.nprob) * tiles_per_prob;
+    const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const bool read_c = p.beta != 0.0f;
+    auto decode = [&](int64_t t, TcProblem& pr, int& m0, int& n0) {
+        const int64_t pi = t / tiles_per_prob;
+        const int r = static_cast<int>(t - pi * tiles_per_prob);
+        pr = p.problems ? p.problems[pi] : p.single;
+        m0 = (r % mpairs) * (2 * BM) + static_cast<int>(rank) * BM;
+        n0 = (r / mpairs) * BN;
+    };
+
+    if (warp == 0) {
+        // ===== TMA producer (both CTAs): own A rows, own half of B =====
+        if (lane == 0) {
+            const uint32_t full0 = ptx::mapa_shared(ptx::smem_u32(full), 0);  // even CTA's barriers
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = cid; t < total; t += ncl) {
+                TcProblem pr;
+                int m0, n0;
+                decode(t, pr, m0, n0);
+                const int nb0 = n0 + static_cast<int>(rank) * (BN / 2);
+                for (int kb = 0; kb < p.kblocks; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (A_STAGE + B2_STAGE));
+                    const uint32_t fb = full0 + stage * 8;
+                    uint8_t* a_dst = sA + stage * A_STAGE;
+                    uint8_t* b_dst = sB + stage * B2_STAGE;
+                    const int sg = kb / p.kblocks1;
+                    const int kk = (kb - sg * p.kblocks1) * BK;
+                    const CUtensorMap* ma = &p.map_a[p.seg_a[sg]];
+                    const CUtensorMap* mb = &p.map_b[p.seg_b[sg]];
+                    if (A_MN) {
+#pragma unroll
+                        for (int j = 0; j < BM / BW; ++j)
+                            ptx::tma_load_3d_2sm(a_dst + j * BOX, ma, fb, m0 + j * BW, kk, pr.a_tile);
+                    } else {
+                        ptx::tma_load_3d_2sm(a_dst, ma, fb, kk, m0, pr.a_tile);
+                    }
+                    if (B_MN) {
+#pragma unroll
+                        for (int j = 0; j < (BN / 2) / BW; ++j)
+                            ptx::tma_load_3d_2sm(b_dst + j * BOX, mb, fb, nb0 + j * BW, kk, pr.b_tile);
+                    } else {
+                        ptx::tma_load_3d_2sm(b_dst, mb, fb, kk, nb0, pr.b_tile);
+                    }
+                    if (++stage == STAGES2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== pair MMA issuer (even CTA only) =====
+        if (rank == 0 && lane == 0) {
+            constexpr uint32_t idesc = ptx::umma_idesc(2 * BM, BN, A_MN, B_MN, 0u);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t t = cid; t < total; t += ncl) {
+                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+                for (int kb = 0; kb < p.kblocks; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a_base = ptx::smem_u32(sA + stage * A_STAGE);
+                    const uint32_t b_base = ptx::smem_u32(sB + stage * B2_STAGE);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint64_t ad = A_MN ? ptx::umma_desc_sw128(a_base + k * KSTEP_MN, BOX, 1024)
+                                                 : ptx::umma_desc_sw128(a_base + k * 32, 0, 1024);
+                        const uint64_t bd = B_MN ? ptx::umma_desc_sw128(b_base + k * KSTEP_MN, BOX, 1024)
+                                                 : ptx::umma_desc_sw128(b_base + k * 32, 0, 1024);
+                        ptx::mma_f16_ss_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+                    }
+                    ptx::mma_commit_2sm_mc(&empty[stage], 0x3);
+                    if (++stage == STAGES2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                ptx::mma_commit_2sm_mc(&tfull[acc], 0x3);
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 3) {
+        // ===== C loader (both CTAs, own rows) =====
+        if (lane == 0) {
+            uint32_t cphase = 0;
+            for (int64_t t = cid; t < total; t += ncl) {
+                TcProblem pr;
+                int m0, n0;
+                decode(t, pr, m0, n0);
+                for (int h = 0; h < NCHUNK; ++h) {
+                    ptx::mbar_wait(cempty, cphase ^ 1);
+                    if (read_c) {
+                        ptx::mbar_arrive_expect_tx(cfull, C_CHUNK);
+                        ptx::tma_load_3d(cbuf, &p.map_c, cfull, m0, n0 + h * CW, pr.c_tile);
+                    } else {
+                        ptx::mbar_arrive(cfull);
+                    }
+                    cphase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== epilogue (both CTAs, own 128 TMEM lanes) =====
+        const int q = warp - 4;
+        const int r = q * 32 + lane;
+        const bool is_leader = threadIdx.x == 128;
+        const uint32_t tempty0 = ptx::mapa_shared(ptx::smem_u32(tempty), 0);
+        int acc = 0;
+        uint32_t acc_phase = 0, cphase = 0;
+        for (int64_t t = cid; t < total; t += ncl) {
+            TcProblem pr;
+            int m0, n0;
+            decode(t, pr, m0, n0);
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            const int row = m0 + r;
+#pragma unroll 1
+            for (int h = 0; h < NCHUNK; ++h) {
+                ptx::mbar_wait(cfull, cphase);
+                cphase ^= 1;
+#pragma unroll 1
+                for (int c = 0; c < CW / 32; ++c) {
+                    uint32_t v[32];
+                    const int col0 = h * CW + c * 32;
+                    ptx::tmem_ld_32x32b_x32(
+                        tmem_base + (static_cast<uint32_t>(q * 32) << 16) + acc * BN + col0, v);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int cc = c * 32 + j;
+                        const float a = __fmul_rn(p.alpha, __uint_as_float(v[j]));
+                        float out = a;
+                        if (read_c) {
+                            const float old = ld_c(cbuf, cc * BM + r);
+                            out = (pr.lower_only && row < n0 + col0 + j)
+                                      ? old
+                                      : __fadd_rn(a, __fmul_rn(p.beta, old));
+                        }
+                        st_c(cbuf, cc * BM + r, out);
+                    }
+                }
+                ptx::fence_proxy_async_smem();
+                ptx::named_bar_sync(1, EPI_THREADS);
+                if (is_leader) {
+                    ptx::tma_store_3d(&p.map_c, cbuf, m0, n0 + h * CW, pr.c_tile);
+                    ptx::bulk_commit();
+                    ptx::bulk_wait_read0();
+                    ptx::mbar_arrive(cempty);
+                }
+            }
+            // this CTA is done with accumulator `acc`: one arrival on the even CTA
+            ptx::tc_fence_before();
+            ptx::named_bar_sync(2, EPI_THREADS);
+            if (is_leader) ptx::mbar_arrive_cluster(tempty0 + acc * 8);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+        if (is_leader) ptx::bulk_wait0();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync_all();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_2sm<TMEM_COLS>(tmem_base);
+    }
+}
+
 // ---- host side ---------------------------------------------------------------
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -383,6 +625,26 @@ void launch_kernel(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total, int
     MP_CUDA(cudaGetLastError());
 }
 
+
+template <bool A_MN, bool B_MN, typename TC>
+void launch_kernel2(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total_pairs, int tiles_per_cta) {
+    auto kern = gemm_tc2_kernel<A_MN, B_MN, TC>;
+    static bool configured = false;
+    if (!configured) {
+        MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
+        configured = true;
+    }
+    const int64_t clusters = persistent_grid(total_pairs, ctx->sm_count / 2, tiles_per_cta);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * clusters));
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = SMEM2_BYTES;
+    cfg.stream = s;
+    MP_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
 }  // namespace tc
 
 bool tc_gemm_supported(const TcGemm& g) {
@@ -403,7 +665,12 @@ void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
     std::memset(&p, 0, sizeof(p));
     const bool a_mn = !g.ta, b_mn = g.tb;
     const int kind = g.kind;
-    const uint32_t rows_a = a_mn ? 0 : BM, rows_b = b_mn ? 0 : BN;
+    static const bool tc2_env = [] {
+        const char* e = getenv("MPCR_TC2");
+        return !(e && e[0] == '0');
+    }();
+    const bool pair = kind == 0 && tc2_env;  // FP16: 2-CTA pair kernel
+    const uint32_t rows_a = a_mn ? 0 : BM, rows_b = b_mn ? 0 : (pair ? BN / 2 : BN);
     const void* As[2] = {g.A, g.A2 ? g.A2 : g.A};
     const void* Bs[2] = {g.B, g.B2 ? g.B2 : g.B};
     for (int i = 0; i < 2; ++i) {
@@ -455,6 +722,22 @@ void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
     ProfScope ps(ctx, kind == 0 ? MP_PROF_GEMM_F16 : MP_PROF_GEMM_F32, s,
                  2.0 * static_cast<double>(g.m) * g.n * g.k * p.nprob *
                      (g.lower_only ? 0.5 : 1.0));
+    if (pair) {
+        const int64_t pairs = static_cast<int64_t>(p.nprob) * ((p.mblocks + 1) / 2) * p.nblocks;
+#define MP_TC2(AM, BMJ)                                                                 \
+        if (a_mn == AM && b_mn == BMJ) {                                                \
+            if (half_c)                                                                 \
+                launch_kernel2<AM, BMJ, uint16_t>(ctx, s, p, pairs, g.tiles_per_cta);   \
+            else                                                                        \
+                launch_kernel2<AM, BMJ, float>(ctx, s, p, pairs, g.tiles_per_cta);      \
+            return;                                                                     \
+        }
+        MP_TC2(true, true)
+        MP_TC2(true, false)
+        MP_TC2(false, true)
+        MP_TC2(false, false)
+#undef MP_TC2
+    }
 #define MP_TC(AM, BMJ)                                                                  \
     if (a_mn == AM && b_mn == BMJ) {                                                    \
         if (kind == 1)                                                                  \
