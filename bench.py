@@ -336,9 +336,18 @@ def run_chol(args, world, rank, local):
         # dominant kernel: tcgen05 FP16 GEMM; algorithmic flops / its event time
         ach = f16["rate"]
         peak = pk["bf16_tflops_sustained"]
+        traffic, tnote = None, None
+        try:
+            with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+                tj = json.load(f)
+            traffic = tj["traffic_bytes_per_launch"]
+            tnote = (f"dram read+write of one captured bulk launch ({tj['duration_us']} us), "
+                     f"algorithmic {tj['algorithmic_bytes_per_launch']:.3g} B; {tj['summary']}")
+        except (OSError, KeyError, ValueError):
+            pass
         roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                "frac": ach / peak, "traffic": None,
-                "kernel": "gemm_f16_tc_kernel (tcgen05 kind::f16, grouped trailing update + panel TRSM)",
+                "frac": ach / peak, "traffic": traffic, "traffic_note": tnote,
+                "kernel": "gemm_tc2_kernel (tcgen05 kind::f16 cta_group::2, grouped trailing update + panel TRSM)",
                 "peak_source": f"{src} bf16_tflops_sustained (FP16 = BF16 tensor rate)",
                 "share_of_step": f16["ms"] / prof_step_ms}
     # Blended roofline: every flop at the tensor-core peak of its destination
