@@ -430,16 +430,29 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(const OzSliceItem* items)
         }
         __syncthreads();
         if (gr < it.rows && c0 + cg < it.kpad) {
+            // Integer digit extraction: Y = x * 2^(41 - e_r) is an integer with
+            // |Y| < 2^41 (an FP16 x = m 2^E with E >= e_r - 40 in its row), then
+            // balanced base-2^7 digits, most significant first (weights 2^35 .. 2^0).
             alignas(16) int8_t dig[S][16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-                double y = zero ? 0.0 : ldexp(h2d(sx[lr][cg + j]), 6 - er);  // |y| < 64, exact
-#pragma unroll
-                for (int d = 0; d < S; ++d) {
-                    const double q = rint(y);
-                    dig[d][j] = static_cast<int8_t>(q);
-                    y = (y - q) * 128.0;  // exact: y - q in [-1/2, 1/2], at most 41 bits
+                const uint32_t h = sx[lr][cg + j];
+                const uint32_t mag = h & 0x7fffu, ef = mag >> 10;
+                long long Y = 0;
+                if (!zero && mag != 0) {
+                    const long long m = ef ? ((mag & 0x3ffu) | 0x400u) : mag;
+                    const int shift = (ef ? static_cast<int>(ef) : 1) - 25 + 41 - er;  // in [1, 41]
+                    Y = m << shift;
+                    if (h & 0x8000u) Y = -Y;
                 }
+#pragma unroll
+                for (int d = 0; d < S - 1; ++d) {
+                    const int w = 35 - 7 * d;
+                    const long long q = (Y + (1ll << (w - 1))) >> w;  // round half up: q in [-64, 64]
+                    dig[d][j] = static_cast<int8_t>(q);
+                    Y -= q << w;
+                }
+                dig[S - 1][j] = static_cast<int8_t>(Y);  // |Y| <= 64 remains, weight 2^0
             }
             int8_t* out = static_cast<int8_t*>(it.out) + gr * it.kpad + c0 + cg;
 #pragma unroll
