@@ -342,7 +342,7 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
     // cheaper.  MPCR_POTRF_CTAS overrides for tuning.
     static const int cap = [] {
         const char* e = getenv("MPCR_POTRF_CTAS");
-        return e ? atoi(e) : 32;
+        return e ? atoi(e) : 16;
     }();
     int grid = nblk * (nblk + 1) / 2;
     if (grid > cap) grid = cap;
