@@ -431,8 +431,20 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         if (L.n_split32[h])
             launch_batched_split_tf32_t(c, st, reinterpret_cast<const SplitItem*>(dl + L.split32[h]),
                                         L.n_split32[h], nb);
-        if (L.n_digits[h])
+        if (L.n_digits[h]) {
             launch_oz_slices(c, st, reinterpret_cast<const OzSliceItem*>(dl + L.digits[h]), L.n_digits[h], nb, nb);
+            static const bool dbg = getenv("MPCR_DEBUG_NDIG") != nullptr;  // diagnostics (eager runs only)
+            if (dbg && h == 1) {
+                std::vector<int32_t> nd(NT);
+                MP_CUDA(cudaMemcpyAsync(nd.data(), ndg(0, k), NT * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+                MP_CUDA(cudaStreamSynchronize(st));
+                int hist[8] = {};
+                for (int64_t i = k + 1; i < NT; ++i) hist[std::min(7, std::max(0, nd[i]))]++;
+                std::fprintf(stderr, "[mpcr] step %lld digits:", static_cast<long long>(k));
+                for (int q = 0; q < 8; ++q) std::fprintf(stderr, " %d", hist[q]);
+                std::fprintf(stderr, "\n");
+            }
+        }
     };
     // write the factor of tile column k back from the panel into the tiles
     auto write_back = [&](int64_t k, cudaStream_t st) {
