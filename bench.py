@@ -443,6 +443,62 @@ def run_gemm(args, world, rank, local):
                       "clocks": clk.summary()}))
 
 
+def run_nll(args, world, rank, local):
+    """BASELINE.json configs[4]: Gaussian log-likelihood of a Matern GP at the
+    given locations: host (x, y, z) -> device covariance -> jittered tiled
+    Cholesky -> forward solve -> logdet + quadratic form -> nll to the host
+    (workloads.cpp:56-87).  One step = one likelihood evaluation."""
+    import torch
+
+    import paper_2406_02701_b200 as mp
+
+    ctx = mp.Context(local)
+    n = args.n or 65536
+    nb = args.nb
+    g = band_map(n // nb, args.b64, args.b32)
+    x, y, side = grid_points(n)
+    z = np.random.default_rng(5).standard_normal(n)
+    A = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+    st = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
+
+    def step():
+        A.fill_matern_points(x, y, 0.5, args.range, 1.0, args.nugget)
+        return mp.gaussian_nll(z, A, jitter=1e-6, max_jitter=1e-3)
+
+    for _ in range(args.warmup):
+        r = step()
+    ctx.synchronize()
+    l0 = ctx.launch_count()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record(st)
+            r = step()  # returns after the nll is on the host
+            e1.record(st)
+            ctx.synchronize()
+            times.append((e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3))
+    ms = float(np.mean([t[0] for t in times]))
+    wall = float(np.mean([t[1] for t in times]))
+    flops = n ** 3 / 3
+    line = {
+        "metric": "Gaussian log-likelihood evaluation (Matern -> tiled chol -> solve -> logdet) TFLOP/s",
+        "value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "mixed(f64/f32/f16 tiles)", "data": "synthetic",
+        "config": {"workload": f"gaussian_nll n={n}, tile {nb}, Matern nu=0.5 range {args.range}, "
+                               f"jitter 1e-6 (x10 up to 1e-3)",
+                   "n": n, "nb": nb, "precision_map": f"|i-j|<{args.b64}:FP64, <{args.b32}:FP32, else FP16"},
+        "nll": r["nll"], "logdet": r["logdet"], "jitter_used": r["jitter"],
+        "gpu_launches": ctx.launch_count() - l0,
+        "e2e": {"value": flops / (wall * 1e-3) / 1e12, "unit": "TFLOP/s",
+                "h2d_bytes_per_step": 3 * n * 8, "d2h_bytes_per_step": 32, "ms_per_step": wall},
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+
+
 def run_cast(args, world, rank, local):
     """Config 2 cast line: MPArray::converted bandwidth (n x n, pin -> pout)."""
     import torch
@@ -488,7 +544,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="chol", choices=["chol", "gemm", "cast"])
+    ap.add_argument("--workload", default="chol", choices=["chol", "gemm", "cast", "nll"])
     ap.add_argument("--cast", default="double:half")
     ap.add_argument("--n", type=int, default=None,
                     help="matrix order (default 65536 at N=1, 131072 at N>1)")
@@ -513,6 +569,8 @@ def main():
         run_gemm(args, world, rank, local)
     elif args.workload == "cast":
         run_cast(args, world, rank, local)
+    elif args.workload == "nll":
+        run_nll(args, world, rank, local)
     else:
         run_chol(args, world, rank, local)
     if world > 1:

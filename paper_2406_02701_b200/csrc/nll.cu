@@ -16,60 +16,110 @@ namespace {
 template <int P>
 using ST = typename Storage<P>::T;
 
-// In-place lower-triangular solve of one nb x nb tile against r (FP64).
+// In-place lower-triangular solve of one nb x nb tile against r (FP64),
+// left-looking over 32-row blocks: the block's rows first take the dot
+// products with all solved entries (8 threads per row, all loads of a thread
+// independent), then warp 0 substitutes down the 32 x 32 diagonal block (one
+// multiply, one shuffle and one FMA on the chain per column).
 template <int P>
 __global__ void __launch_bounds__(256) tile_trsv_kernel(const ST<P>* __restrict__ L, int64_t ld,
                                                         int nb, double* __restrict__ r) {
-    __shared__ double wb[32];
+    extern __shared__ double wsol[];  // solved entries w[0 .. nb)
+    __shared__ double rb[32];
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     for (int b0 = 0; b0 < nb; b0 += 32) {
         const int w = min(32, nb - b0);
+        // (1) rb[row] = r[row] - sum_{c < b0} L[row][c] w[c]; thread = (row, part)
+        {
+            const int row = tid % 32, part = tid / 32;  // 8 parts over the columns
+            double s0 = 0.0, s1 = 0.0;
+            if (row < w) {
+                const int64_t gr = b0 + row;
+                int c = part;
+                for (; c + 8 < b0; c += 16) {
+                    s0 = fma(load_as<double>(L, (int64_t)c * ld + gr), wsol[c], s0);
+                    s1 = fma(load_as<double>(L, (int64_t)(c + 8) * ld + gr), wsol[c + 8], s1);
+                }
+                for (; c < b0; c += 8) s0 = fma(load_as<double>(L, (int64_t)c * ld + gr), wsol[c], s0);
+            }
+            double sum = s0 + s1;
+            // reduce the 8 parts (threads row, row+32, ..., row+224) through shared memory
+            __shared__ double part_sum[8][33];
+            part_sum[part][row] = sum;
+            __syncthreads();
+            if (tid < 32 && tid < w) {
+                double t = 0.0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) t += part_sum[q][tid];
+                rb[tid] = r[b0 + tid] - t;
+            }
+            __syncthreads();
+        }
+        // (2) warp 0: substitution down the diagonal block
         if (warp == 0) {
-            // lane i owns row b0 + i; substitution down the 32 x 32 block
-            double x = lane < w ? r[b0 + lane] : 0.0;
-            for (int j = 0; j < w; ++j) {
-                const double lj = lane < w ? load_as<double>(L, (int64_t)(b0 + j) * ld + b0 + lane) : 0.0;
-                const double xj = __shfl_sync(0xffffffffu, x, j) / __shfl_sync(0xffffffffu, lj, j);
-                if (lane == j) x = xj;
-                if (lane > j) x -= lj * xj;
+            double lrow[32];  // L[b0 + lane][b0 + j]
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                lrow[j] = (lane < w && j < w && j <= lane) ? load_as<double>(L, (int64_t)(b0 + j) * ld + b0 + lane)
+                                                           : 0.0;
+            double x = lane < w ? rb[lane] : 0.0;
+            double dg = 1.0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (j == lane && lane < w) dg = lrow[j];
+            const double inv = 1.0 / dg;  // one division per lane
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                if (j < w) {
+                    if (lane == j) x *= inv;
+                    const double xj = __shfl_sync(0xffffffffu, x, j);
+                    if (lane > j) x = fma(-lrow[j], xj, x);
+                }
             }
             if (lane < w) {
                 r[b0 + lane] = x;
-                wb[lane] = x;
+                wsol[b0 + lane] = x;
             }
-        }
-        __syncthreads();
-        for (int i = b0 + w + tid; i < nb; i += blockDim.x) {
-            double s = 0.0;
-            for (int c = 0; c < w; ++c) s += load_as<double>(L, (int64_t)(b0 + c) * ld + i) * wb[c];
-            r[i] -= s;
         }
         __syncthreads();
     }
 }
 
 // r_j[rows] -= L_ji[rows, :] * w_i for a list of tiles (blockIdx.y = tile,
-// blockIdx.x = 256-row chunk); thread = row, columns streamed coalesced.
+// blockIdx.x = 32-row chunk): lane = row (coalesced), the 8 warps split the
+// columns, partial sums reduced in shared memory (deterministic order).
 using GemvItem = TrsvItem;
 
 template <int P>
 __global__ void __launch_bounds__(256) tile_gemv_kernel(const GemvItem* __restrict__ items, int nb,
                                                         const double* __restrict__ w) {
     __shared__ double ws[1024];
+    __shared__ double part_sum[8][33];
     const GemvItem it = items[blockIdx.y];
     const ST<P>* __restrict__ L = static_cast<const ST<P>*>(it.L);
     for (int c = threadIdx.x; c < nb && c < 1024; c += blockDim.x) ws[c] = w[c];
     __syncthreads();
-    const int row = blockIdx.x * blockDim.x + threadIdx.x;
-    if (row >= nb) return;
-    double s0 = 0.0, s1 = 0.0;
-    int c = 0;
-    for (; c + 1 < nb; c += 2) {
-        s0 += load_as<double>(L, (int64_t)c * nb + row) * ws[c];
-        s1 += load_as<double>(L, (int64_t)(c + 1) * nb + row) * ws[c + 1];
+    const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+    const int row = blockIdx.x * 32 + lane;
+    const int chunk = (nb + 7) / 8, c0 = warp * chunk, c1 = min(nb, c0 + chunk);
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (row < nb) {
+        int c = c0;
+        for (; c + 8 <= c1; c += 8) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                acc[u] = fma(load_as<double>(L, (int64_t)(c + u) * nb + row), ws[c + u], acc[u]);
+        }
+        for (; c < c1; ++c) acc[0] = fma(load_as<double>(L, (int64_t)c * nb + row), ws[c], acc[0]);
     }
-    if (c < nb) s0 += load_as<double>(L, (int64_t)c * nb + row) * ws[c];
-    it.r[row] -= s0 + s1;
+    part_sum[warp][lane] = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    __syncthreads();
+    if (warp == 0 && row < nb) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t += part_sum[q][lane];
+        it.r[row] -= t;
+    }
 }
 
 __global__ void square_sum_kernel(const double* __restrict__ w, int64_t n, double* out) {
@@ -106,7 +156,7 @@ void launch_tile_trsv(Ctx* ctx, cudaStream_t s, mp_precision p, const void* L, i
                       double* r) {
     dispatch_p(p, [&](auto pp) {
         constexpr int P = decltype(pp)::value;
-        tile_trsv_kernel<P><<<1, 256, 0, s>>>(static_cast<const ST<P>*>(L), ld, nb, r);
+        tile_trsv_kernel<P><<<1, 256, nb * sizeof(double), s>>>(static_cast<const ST<P>*>(L), ld, nb, r);
     });
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());
@@ -116,7 +166,7 @@ void launch_tile_gemv(Ctx* ctx, cudaStream_t s, mp_precision p, const void* dev_
                       int64_t count, int nb, const double* w) {
     if (count == 0) return;
     if (nb > 1024) fail(MP_INVALID_PARAM, "tile gemv: tile size above 1024");
-    const dim3 grid(static_cast<unsigned>((nb + 255) / 256), static_cast<unsigned>(count));
+    const dim3 grid(static_cast<unsigned>((nb + 31) / 32), static_cast<unsigned>(count));
     dispatch_p(p, [&](auto pp) {
         constexpr int P = decltype(pp)::value;
         tile_gemv_kernel<P><<<grid, 256, 0, s>>>(static_cast<const GemvItem*>(dev_items), nb, w);

@@ -48,6 +48,7 @@ struct mp_tile_s {
     void* digits = nullptr;  // INT8 digit planes of FP16 panel tiles [2][tr][S][br][br]
     int32_t* rexp = nullptr;  // their row exponents [2][tr][br]
     int32_t* ndig = nullptr;  // digits each of them needs [2][tr]
+    void* backup[3] = {nullptr, nullptr, nullptr};  // jittered-NLL copy of the input slabs
     void* work = nullptr;  // FP64 nb x nb x 2 + FP32 nb x nb + Linv{H,S}
     void* lists = nullptr;
     size_t lists_bytes = 0;
@@ -79,6 +80,8 @@ struct mp_tile_s {
         if (digits) cudaFree(digits);
         if (rexp) cudaFree(rexp);
         if (ndig) cudaFree(ndig);
+        for (void* b : backup)
+            if (b) cudaFree(b);
         if (work) cudaFree(work);
         if (lists) cudaFree(lists);
         trtri_plan_destroy(trtri);
@@ -1189,22 +1192,16 @@ mp_status mp_tile_gaussian_nll(mp_ctx ctx, mp_tile cov, const double* host_z, do
     if (t.rows != t.cols || t.br != t.bc) fail(MP_SHAPE_MISMATCH, "nll: square MPCRTile required");
     cudaStream_t s = c->stream;
     const int64_t n = t.rows, nb = t.br, NT = t.tr;
-    // backup of the input for jitter escalation (workloads.cpp:63-67)
-    void* backup[3] = {nullptr, nullptr, nullptr};
-    struct Free {
-        void** b;
-        ~Free() {
-            for (int q = 0; q < 3; ++q)
-                if (b[q]) cudaFree(b[q]);
-        }
-    } free_backup{backup};
+    // backup of the input for jitter escalation (workloads.cpp:63-67); the
+    // buffers stay with the tile (a likelihood is usually evaluated many times)
+    void** backup = t.backup;
     auto slab_bytes = [&](int q) {
         return static_cast<size_t>(t.nslot[q]) * t.tt() * elem_bytes((mp_precision)q);
     };
     if (jitter > 0.0)
         for (int q = 0; q < 3; ++q)
             if (t.nslot[q]) {
-                MP_CUDA(cudaMalloc(&backup[q], slab_bytes(q)));
+                if (!backup[q]) MP_CUDA(cudaMalloc(&backup[q], slab_bytes(q)));
                 MP_CUDA(cudaMemcpyAsync(backup[q], t.slab[q], slab_bytes(q), cudaMemcpyDeviceToDevice, s));
             }
     double jit = jitter > 0.0 ? jitter : 0.0;
@@ -1221,6 +1218,12 @@ mp_status mp_tile_gaussian_nll(mp_ctx ctx, mp_tile cov, const double* host_z, do
         for (int q = 0; q < 3; ++q)
             if (t.nslot[q])
                 MP_CUDA(cudaMemcpyAsync(t.slab[q], backup[q], slab_bytes(q), cudaMemcpyDeviceToDevice, s));
+    }
+    static const bool dbg_nll = getenv("MPCR_DEBUG_NLL") != nullptr;  // phase timings (diagnostics)
+    cudaEvent_t dbg_ev[3] = {nullptr, nullptr, nullptr};
+    if (dbg_nll) {
+        for (auto& e : dbg_ev) MP_CUDA(cudaEventCreate(&e));
+        MP_CUDA(cudaEventRecord(dbg_ev[0], s));
     }
     // forward solve w = L^{-1} z, tile row by tile row.  Distributed: every
     // rank accumulates its own tiles' contributions to r (rank 0 starts from
@@ -1244,14 +1247,8 @@ mp_status mp_tile_gaussian_nll(mp_ctx ctx, mp_tile cov, const double* host_z, do
             cnt[i * 3 + q] = static_cast<int64_t>(items.size() - off[i * 3 + q]);
         }
     TrsvItem* ditems = nullptr;
-    struct FreeItems {
-        TrsvItem** p;
-        ~FreeItems() {
-            if (*p) cudaFree(*p);
-        }
-    } free_items{&ditems};
     if (!items.empty()) {
-        MP_CUDA(cudaMalloc(&ditems, items.size() * sizeof(TrsvItem)));
+        ditems = static_cast<TrsvItem*>(c->ensure_scratch(items.size() * sizeof(TrsvItem), 0));
         MP_CUDA(cudaMemcpyAsync(ditems, items.data(), items.size() * sizeof(TrsvItem),
                                 cudaMemcpyHostToDevice, s));
     }
@@ -1264,6 +1261,7 @@ mp_status mp_tile_gaussian_nll(mp_ctx ctx, mp_tile cov, const double* host_z, do
                 launch_tile_gemv(c, s, (mp_precision)q, ditems + off[i * 3 + q], cnt[i * 3 + q],
                                  static_cast<int>(nb), r + i * nb);
     }
+    if (dbg_nll) MP_CUDA(cudaEventRecord(dbg_ev[1], s));
     launch_square_sum(c, s, r, n, dsum);
     MP_CUDA(cudaMemsetAsync(dsum + 1, 0, sizeof(double), s));
     for (int64_t d = 0; d < NT; ++d)
@@ -1271,7 +1269,15 @@ mp_status mp_tile_gaussian_nll(mp_ctx ctx, mp_tile cov, const double* host_z, do
     if (D) dist_allreduce_sum_f64(D, dsum + 1, 1, s);
     double h[2];
     MP_CUDA(cudaMemcpyAsync(h, dsum, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (dbg_nll) MP_CUDA(cudaEventRecord(dbg_ev[2], s));
     MP_CUDA(cudaStreamSynchronize(s));
+    if (dbg_nll) {
+        float a = 0, b = 0;
+        MP_CUDA(cudaEventElapsedTime(&a, dbg_ev[0], dbg_ev[1]));
+        MP_CUDA(cudaEventElapsedTime(&b, dbg_ev[1], dbg_ev[2]));
+        std::fprintf(stderr, "[mpcr] nll: forward solve %.3f ms, sums %.3f ms\n", a, b);
+        for (auto e : dbg_ev) cudaEventDestroy(e);
+    }
     const double ld = 2.0 * h[1];
     if (quad) *quad = h[0];
     if (logdet) *logdet = ld;
