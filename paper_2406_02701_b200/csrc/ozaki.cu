@@ -91,6 +91,11 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
            (static_cast<uint32_t>(M >> 4) << 24);
 }
 
+// 2^e for |e| <= 1022 (built from the exponent bits; exact)
+__device__ __forceinline__ double pow2(int e) {
+    return __longlong_as_double(static_cast<long long>(1023 + e) << 52);
+}
+
 __device__ __forceinline__ bool skip_tile(const OzProblem& pr, int m0, int n0) {
     return pr.lower_only && (m0 + BM - 1 < n0);
 }
@@ -259,6 +264,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
             const int row = m0 + r;
             if (row < p.M) {
                 const int er = p.rexp_a[static_cast<int64_t>(pr.a_tile) * p.rexp_stride_a + row];
+                const double sr = pow2(er == ROWEXP_NONFINITE ? 0 : er);
                 double* C = static_cast<double*>(pr.c);
                 const int32_t* ecol = p.rexp_b + static_cast<int64_t>(pr.b_tile) * p.rexp_stride_b;
 #pragma unroll
@@ -279,8 +285,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                         double v;
                         if (er == ROWEXP_NONFINITE || ec[u] == ROWEXP_NONFINITE)
                             v = __longlong_as_double(0x7ff8000000000000ll);
-                        else
-                            v = ldexp(sum[jb + u], er + ec[u]);
+                        else  // exact power-of-two scalings (FP16 rows: |e| <= 40)
+                            v = sum[jb + u] * sr * pow2(ec[u]);
                         double out = p.alpha * v;
                         if (p.beta != 0.0) out = fma(p.beta, cv[u], out);
                         C[static_cast<int64_t>(col) * p.ldc + row] = out;
