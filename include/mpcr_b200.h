@@ -237,6 +237,18 @@ mp_status mp_tile_gaussian_nll(mp_ctx ctx, mp_tile cov, const double* host_z, do
                                double max_jitter, double* nll, double* logdet, double* quad,
                                double* jitter_used);
 
+/* matern_mle (workloads.cpp:89-110, optimize.cpp:9-95): Nelder-Mead over
+ * (log range, log sigma2) of a Matern(nu) Gaussian process at the host
+ * points (x, y) with observations z; every objective evaluation regenerates
+ * the covariance into `cov` on the device and evaluates mp_tile_gaussian_nll
+ * (jitter policy as given).  max_iter / tol as NelderMeadConfig (the
+ * reference's matern_mle default: 200 / 1e-4). */
+mp_status mp_tile_matern_mle(mp_ctx ctx, mp_tile cov, const double* host_x, const double* host_y,
+                             const double* host_z, int64_t n, double nu, double init_log_range,
+                             double init_log_sigma2, int max_iter, double tol, double jitter,
+                             double max_jitter, double* range_hat, double* sigma2_hat, double* nll,
+                             int* iterations, int* converged);
+
 /* ------------------------------------------------------------------------- */
 /* Multi-GPU: 2D block-cyclic MPCRTile over a P x Q process grid (one process */
 /* per GPU).  Tile (i, j), i >= j, lives on rank (i mod P) * Q + (j mod Q);   */

@@ -269,6 +269,17 @@ class Ref(_Base):
                                            C.c_uint64(seed), _ptr(out)))
         return out
 
+    def matern_mle(self, prec, side, z, init_log_range, init_log_sigma2, max_iter=200, tol=1e-4):
+        """matern_mle (workloads.cpp:89-110) on the first len(z) points of the side x side grid."""
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        out = [C.c_double(), C.c_double(), C.c_double(), C.c_int()]
+        self._check(self.lib.ref_matern_mle(C.c_int(prec), _i64(side), _i64(z.size), _ptr(z),
+                                            C.c_double(init_log_range), C.c_double(init_log_sigma2),
+                                            C.c_int(max_iter), C.c_double(tol), C.byref(out[0]),
+                                            C.byref(out[1]), C.byref(out[2]), C.byref(out[3])))
+        return {"range": out[0].value, "sigma2": out[1].value, "nll": out[2].value,
+                "iterations": out[3].value}
+
     def tile_gemm(self, A, ptA, nbA, B, ptB, nbB, Cm, ptC, nbC, ta=False, tb=False,
                   alpha=1.0, beta=0.0):
         """nbX = (rows_per_tile, cols_per_tile); ptX = tile-precision grid."""

@@ -305,6 +305,28 @@ int ref_gaussian_nll(int prec, std::int64_t n, const double* z, const double* co
     });
 }
 
+// matern_mle (workloads.cpp:89-110): Nelder-Mead over (log range, log sigma2)
+// on the unit-grid distances of `side`, first n points.
+int ref_matern_mle(int prec, std::int64_t side, std::int64_t n, const double* z, double init_log_range,
+                   double init_log_sigma2, int max_iter, double tol, double* range_hat, double* sigma2_hat,
+                   double* nll, int* iterations) {
+    return guard([&] {
+        const auto g = stats::grid_locations(static_cast<std::size_t>(side));
+        MPArray d = MPArray::zeros_matrix(n, n, Precision::Double);
+        for (std::int64_t j = 0; j < n; ++j)
+            for (std::int64_t i = 0; i < n; ++i) d.set(i, j, g.distances.get(i, j));
+        const MPArray zz = MPArray::vector_from_doubles(std::vector<double>(z, z + n), Precision::Double);
+        stats::NelderMeadConfig cfg;
+        cfg.max_iter = max_iter;
+        cfg.tol = tol;
+        const auto r = stats::matern_mle(zz, d, P(prec), init_log_range, init_log_sigma2, cfg);
+        *range_hat = r.range_hat;
+        *sigma2_hat = r.sigma2_hat;
+        *nll = r.nll;
+        *iterations = r.iterations;
+    });
+}
+
 // sample_gp (workloads.cpp:41-49).
 int ref_sample_gp(std::int64_t n, const double* cov, std::uint64_t seed, double* out) {
     return guard([&] {

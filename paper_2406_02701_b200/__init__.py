@@ -25,6 +25,7 @@ from .mpcr import (  # noqa: F401
     ew_unary,
     gaussian_nll,
     linalg,
+    matern_mle,
     nccl_unique_id,
     parse_precision,
     promote,
@@ -37,7 +38,7 @@ from .mpcr import (  # noqa: F401
 
 __all__ = [
     "BinaryOp", "Context", "MPArray", "MPCRTile", "MPError", "Precision", "ProcessGrid", "ReduceOp", "Side",
-    "UnaryOp", "default_context", "diag", "dist_owner", "dist_schedule", "nccl_unique_id", "ew_binary", "ew_scalar", "ew_unary", "gaussian_nll", "linalg",
+    "UnaryOp", "default_context", "diag", "dist_owner", "dist_schedule", "nccl_unique_id", "ew_binary", "ew_scalar", "ew_unary", "gaussian_nll", "linalg", "matern_mle",
     "parse_precision", "promote", "reduce", "tile_chol", "tile_gemm", "tile_trsm", "transpose",
     "lib", "LIB_PATH",
 ]

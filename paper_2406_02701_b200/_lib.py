@@ -91,6 +91,10 @@ SIGNATURES = {
     "mp_tile_gaussian_nll": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_double,
                                        C.POINTER(C.c_double), C.POINTER(C.c_double),
                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "mp_tile_matern_mle": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, C.c_double, C.c_double, C.c_double,
+                                     C.c_int, C.c_double, C.c_double, C.c_double,
+                                     C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                     C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     # multi-GPU (2D block-cyclic MPCRTile)
     "mp_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "mp_dist_create": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(_vp)]),

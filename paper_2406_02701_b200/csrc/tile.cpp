@@ -19,6 +19,7 @@
 // All per-step work lists are built on the host once per factorization and
 // uploaded in one copy; the step loop is launch-only (no host sync).
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdio>
 #include <cmath>
@@ -800,6 +801,107 @@ bool fill_matern_batched(Ctx* c, mp_tile_s& x, const double* dx, const double* d
     return true;
 }
 
+// Gaussian negative log-likelihood of z under the covariance held in t
+// (factored in place).  z may be host or device memory.
+void tile_nll(Ctx* c, mp_tile_s& t, const double* host_z, double jitter, double max_jitter, double* nll,
+              double* logdet, double* quad, double* jitter_used) {
+    if (!c || !host_z) fail(MP_INVALID_PARAM, "null argument");
+    if (t.rows != t.cols || t.br != t.bc) fail(MP_SHAPE_MISMATCH, "nll: square MPCRTile required");
+    cudaStream_t s = c->stream;
+    const int64_t n = t.rows, nb = t.br, NT = t.tr;
+    // backup of the input for jitter escalation (workloads.cpp:63-67); the
+    // buffers stay with the tile (a likelihood is usually evaluated many times)
+    void** backup = t.backup;
+    auto slab_bytes = [&](int q) {
+        return static_cast<size_t>(t.nslot[q]) * t.tt() * elem_bytes((mp_precision)q);
+    };
+    if (jitter > 0.0)
+        for (int q = 0; q < 3; ++q)
+            if (t.nslot[q]) {
+                if (!backup[q]) MP_CUDA(cudaMalloc(&backup[q], slab_bytes(q)));
+                MP_CUDA(cudaMemcpyAsync(backup[q], t.slab[q], slab_bytes(q), cudaMemcpyDeviceToDevice, s));
+            }
+    double jit = jitter > 0.0 ? jitter : 0.0;
+    for (;;) {
+        if (jit > 0.0)
+            for (int64_t d = 0; d < NT; ++d)
+                if (t.has(d, d)) launch_add_diag(c, s, t.p(d, d), t.ptr(d, d), nb, static_cast<int>(nb), jit);
+        const int64_t inf = tile_chol_inplace(c, t);
+        if (inf < 0) break;
+        if (jit <= 0.0 || jit * 10.0 > max_jitter)
+            throw Error(MP_NOT_POSITIVE_DEFINITE,
+                        "matrix is not positive definite at pivot column " + std::to_string(inf), inf);
+        jit *= 10.0;
+        for (int q = 0; q < 3; ++q)
+            if (t.nslot[q])
+                MP_CUDA(cudaMemcpyAsync(t.slab[q], backup[q], slab_bytes(q), cudaMemcpyDeviceToDevice, s));
+    }
+    static const bool dbg_nll = getenv("MPCR_DEBUG_NLL") != nullptr;  // phase timings (diagnostics)
+    cudaEvent_t dbg_ev[3] = {nullptr, nullptr, nullptr};
+    if (dbg_nll) {
+        for (auto& e : dbg_ev) MP_CUDA(cudaEventCreate(&e));
+        MP_CUDA(cudaEventRecord(dbg_ev[0], s));
+    }
+    // forward solve w = L^{-1} z, tile row by tile row.  Distributed: every
+    // rank accumulates its own tiles' contributions to r (rank 0 starts from
+    // z, the others from 0); segment i is summed over ranks just before the
+    // owner of L_ii solves it, and w_i then travels back to every rank.
+    Dist* D = (t.dist && t.dist->world > 1) ? t.dist : nullptr;
+    double* r = static_cast<double*>(c->ensure_scratch((n + 64) * sizeof(double), 3));
+    double* dsum = r + n;
+    if (D && D->rank != 0)
+        MP_CUDA(cudaMemsetAsync(r, 0, n * sizeof(double), s));
+    else
+        MP_CUDA(cudaMemcpyAsync(r, host_z, n * sizeof(double), cudaMemcpyDefault, s));
+    std::vector<TrsvItem> items;
+    std::vector<size_t> off(NT * 3 + 1, 0);
+    std::vector<int64_t> cnt(NT * 3, 0);
+    for (int64_t i = 0; i < NT; ++i)
+        for (int q = 0; q < 3; ++q) {
+            off[i * 3 + q] = items.size();
+            for (int64_t j = i + 1; j < NT; ++j)
+                if (t.has(j, i) && t.p(j, i) == q) items.push_back(TrsvItem{t.ptr(j, i), r + j * nb});
+            cnt[i * 3 + q] = static_cast<int64_t>(items.size() - off[i * 3 + q]);
+        }
+    TrsvItem* ditems = nullptr;
+    if (!items.empty()) {
+        ditems = static_cast<TrsvItem*>(c->ensure_scratch(items.size() * sizeof(TrsvItem), 0));
+        MP_CUDA(cudaMemcpyAsync(ditems, items.data(), items.size() * sizeof(TrsvItem),
+                                cudaMemcpyHostToDevice, s));
+    }
+    for (int64_t i = 0; i < NT; ++i) {
+        if (D) dist_allreduce_sum_f64(D, r + i * nb, nb, s);
+        if (t.has(i, i)) launch_tile_trsv(c, s, t.p(i, i), t.ptr(i, i), nb, static_cast<int>(nb), r + i * nb);
+        if (D) dist_bcast(D, r + i * nb, nb * sizeof(double), dist_owner(i, i, D->P, D->Q), s);
+        for (int q = 0; q < 3; ++q)
+            if (cnt[i * 3 + q])
+                launch_tile_gemv(c, s, (mp_precision)q, ditems + off[i * 3 + q], cnt[i * 3 + q],
+                                 static_cast<int>(nb), r + i * nb);
+    }
+    if (dbg_nll) MP_CUDA(cudaEventRecord(dbg_ev[1], s));
+    launch_square_sum(c, s, r, n, dsum);
+    MP_CUDA(cudaMemsetAsync(dsum + 1, 0, sizeof(double), s));
+    for (int64_t d = 0; d < NT; ++d)
+        if (t.has(d, d)) launch_logdiag_sum(c, s, t.p(d, d), t.ptr(d, d), nb, nb, dsum + 1);
+    if (D) dist_allreduce_sum_f64(D, dsum + 1, 1, s);
+    double h[2];
+    MP_CUDA(cudaMemcpyAsync(h, dsum, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (dbg_nll) MP_CUDA(cudaEventRecord(dbg_ev[2], s));
+    MP_CUDA(cudaStreamSynchronize(s));
+    if (dbg_nll) {
+        float a = 0, b = 0;
+        MP_CUDA(cudaEventElapsedTime(&a, dbg_ev[0], dbg_ev[1]));
+        MP_CUDA(cudaEventElapsedTime(&b, dbg_ev[1], dbg_ev[2]));
+        std::fprintf(stderr, "[mpcr] nll: forward solve %.3f ms, sums %.3f ms\n", a, b);
+        for (auto e : dbg_ev) cudaEventDestroy(e);
+    }
+    const double ld = 2.0 * h[1];
+    if (quad) *quad = h[0];
+    if (logdet) *logdet = ld;
+    if (nll) *nll = 0.5 * h[0] + 0.5 * ld + 0.5 * static_cast<double>(n) * std::log(2.0 * M_PI);
+    if (jitter_used) *jitter_used = jit;
+}
+
 // Shared by mp_tile_create / mp_tile_create_dist: with `dist`, only the
 // lower-triangle tiles this rank owns get storage (slot -1 elsewhere).
 mp_tile_s* tile_new(Ctx* ctx, mp_dist_s* dist, int64_t rows, int64_t cols, int64_t rpt, int64_t cpt,
@@ -1186,103 +1288,137 @@ mp_status mp_tile_gaussian_nll(mp_ctx ctx, mp_tile cov, const double* host_z, do
                                double max_jitter, double* nll, double* logdet, double* quad,
                                double* jitter_used) {
     MP_API_BEGIN
+    tile_nll(ctx, T_(cov), host_z, jitter, max_jitter, nll, logdet, quad, jitter_used);
+    MP_API_END
+}
+
+// matern_mle (workloads.cpp:89-110) with the likelihood on the device.  The
+// simplex search restates stats::nelder_mead (optimize.cpp:9-95): start
+// simplex x0 and x0 + 5 % (2.5e-4 for a zero coordinate) per axis, vertices
+// kept sorted by value (stable), stop when the population standard deviation
+// of the vertex values is below tol; reflection -1, expansion -2, outside /
+// inside contraction -1/2 / +1/2 about the centroid of all but the worst,
+// shrink 1/2 toward the best.  Every evaluation regenerates the Matern
+// covariance for (range, sigma2) = exp(params) on the device and factors it.
+mp_status mp_tile_matern_mle(mp_ctx ctx, mp_tile cov, const double* host_x, const double* host_y,
+                             const double* host_z, int64_t n, double nu, double init_log_range,
+                             double init_log_sigma2, int max_iter, double tol, double jitter,
+                             double max_jitter, double* range_hat, double* sigma2_hat, double* nll,
+                             int* iterations, int* converged) {
+    MP_API_BEGIN
     mp_tile_s& t = T_(cov);
     Ctx* c = ctx;
-    if (!c || !host_z) fail(MP_INVALID_PARAM, "null argument");
-    if (t.rows != t.cols || t.br != t.bc) fail(MP_SHAPE_MISMATCH, "nll: square MPCRTile required");
-    cudaStream_t s = c->stream;
-    const int64_t n = t.rows, nb = t.br, NT = t.tr;
-    // backup of the input for jitter escalation (workloads.cpp:63-67); the
-    // buffers stay with the tile (a likelihood is usually evaluated many times)
-    void** backup = t.backup;
-    auto slab_bytes = [&](int q) {
-        return static_cast<size_t>(t.nslot[q]) * t.tt() * elem_bytes((mp_precision)q);
-    };
-    if (jitter > 0.0)
-        for (int q = 0; q < 3; ++q)
-            if (t.nslot[q]) {
-                if (!backup[q]) MP_CUDA(cudaMalloc(&backup[q], slab_bytes(q)));
-                MP_CUDA(cudaMemcpyAsync(backup[q], t.slab[q], slab_bytes(q), cudaMemcpyDeviceToDevice, s));
-            }
-    double jit = jitter > 0.0 ? jitter : 0.0;
-    for (;;) {
-        if (jit > 0.0)
-            for (int64_t d = 0; d < NT; ++d)
-                if (t.has(d, d)) launch_add_diag(c, s, t.p(d, d), t.ptr(d, d), nb, static_cast<int>(nb), jit);
-        const int64_t inf = tile_chol_inplace(c, t);
-        if (inf < 0) break;
-        if (jit <= 0.0 || jit * 10.0 > max_jitter)
-            throw Error(MP_NOT_POSITIVE_DEFINITE,
-                        "matrix is not positive definite at pivot column " + std::to_string(inf), inf);
-        jit *= 10.0;
-        for (int q = 0; q < 3; ++q)
-            if (t.nslot[q])
-                MP_CUDA(cudaMemcpyAsync(t.slab[q], backup[q], slab_bytes(q), cudaMemcpyDeviceToDevice, s));
-    }
-    static const bool dbg_nll = getenv("MPCR_DEBUG_NLL") != nullptr;  // phase timings (diagnostics)
-    cudaEvent_t dbg_ev[3] = {nullptr, nullptr, nullptr};
-    if (dbg_nll) {
-        for (auto& e : dbg_ev) MP_CUDA(cudaEventCreate(&e));
-        MP_CUDA(cudaEventRecord(dbg_ev[0], s));
-    }
-    // forward solve w = L^{-1} z, tile row by tile row.  Distributed: every
-    // rank accumulates its own tiles' contributions to r (rank 0 starts from
-    // z, the others from 0); segment i is summed over ranks just before the
-    // owner of L_ii solves it, and w_i then travels back to every rank.
-    Dist* D = (t.dist && t.dist->world > 1) ? t.dist : nullptr;
-    double* r = static_cast<double*>(c->ensure_scratch((n + 64) * sizeof(double), 3));
-    double* dsum = r + n;
-    if (D && D->rank != 0)
-        MP_CUDA(cudaMemsetAsync(r, 0, n * sizeof(double), s));
-    else
-        MP_CUDA(cudaMemcpyAsync(r, host_z, n * sizeof(double), cudaMemcpyHostToDevice, s));
-    std::vector<TrsvItem> items;
-    std::vector<size_t> off(NT * 3 + 1, 0);
-    std::vector<int64_t> cnt(NT * 3, 0);
-    for (int64_t i = 0; i < NT; ++i)
-        for (int q = 0; q < 3; ++q) {
-            off[i * 3 + q] = items.size();
-            for (int64_t j = i + 1; j < NT; ++j)
-                if (t.has(j, i) && t.p(j, i) == q) items.push_back(TrsvItem{t.ptr(j, i), r + j * nb});
-            cnt[i * 3 + q] = static_cast<int64_t>(items.size() - off[i * 3 + q]);
+    if (!c || !host_x || !host_y || !host_z) fail(MP_INVALID_PARAM, "null argument");
+    if (n != t.rows || n != t.cols || t.br != t.bc) fail(MP_SHAPE_MISMATCH, "mle: n x n MPCRTile with square tiles");
+    if (nu != 0.5 && nu != 1.5 && nu != 2.5) fail(MP_INVALID_PARAM, "matern_cov: nu must be 0.5, 1.5, or 2.5");
+    if (max_iter < 0) fail(MP_INVALID_PARAM, "mle: max_iter must be >= 0");
+    // points and observations stay on the device for the whole search
+    double* d = nullptr;
+    MP_CUDA(cudaMalloc(&d, 3 * n * sizeof(double)));
+    struct Free {
+        double* p;
+        ~Free() {
+            if (p) cudaFree(p);
         }
-    TrsvItem* ditems = nullptr;
-    if (!items.empty()) {
-        ditems = static_cast<TrsvItem*>(c->ensure_scratch(items.size() * sizeof(TrsvItem), 0));
-        MP_CUDA(cudaMemcpyAsync(ditems, items.data(), items.size() * sizeof(TrsvItem),
-                                cudaMemcpyHostToDevice, s));
+    } free_d{d};
+    MP_CUDA(cudaMemcpyAsync(d, host_x, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    MP_CUDA(cudaMemcpyAsync(d + n, host_y, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    MP_CUDA(cudaMemcpyAsync(d + 2 * n, host_z, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    using Pt = std::array<double, 2>;
+    auto objective = [&](const Pt& q) {
+        const double range = std::exp(q[0]), sigma2 = std::exp(q[1]);
+        if (!(range > 0.0) || !(sigma2 > 0.0) || !std::isfinite(range) || !std::isfinite(sigma2))
+            fail(MP_INVALID_PARAM, "matern_cov: range and variance must be positive");
+        if (!fill_matern_batched(c, t, d, d + n, 0, nu, range, sigma2, 0.0))
+            for (int64_t j = 0; j < t.tc; ++j)
+                for (int64_t i = 0; i < t.tr; ++i)
+                    if (t.has(i, j))
+                        launch_matern_points(c, c->stream, t.p(i, j), t.ptr(i, j), t.br, i * t.br, j * t.bc, t.br,
+                                             t.bc, d, d + n, nu, range, sigma2, 0.0);
+        double v = 0.0;
+        tile_nll(c, t, d + 2 * n, jitter, max_jitter, &v, nullptr, nullptr, nullptr);
+        return v;
+    };
+    constexpr int K = 2;
+    std::array<Pt, K + 1> vx;
+    std::array<double, K + 1> vf;
+    const Pt x0 = {init_log_range, init_log_sigma2};
+    for (int v = 0; v <= K; ++v) vx[v] = x0;
+    for (int i = 0; i < K; ++i) vx[i + 1][i] += x0[i] != 0.0 ? 0.05 * x0[i] : 0.00025;
+    for (int v = 0; v <= K; ++v) vf[v] = objective(vx[v]);
+    auto spread = [&] {  // population standard deviation of the vertex values
+        double mean = 0.0;
+        for (double f : vf) mean += f;
+        mean /= static_cast<double>(K + 1);
+        double acc = 0.0;
+        for (double f : vf) acc += (f - mean) * (f - mean);
+        return std::sqrt(acc / static_cast<double>(K + 1));
+    };
+    int it = 0;
+    bool done = false;
+    for (; it < max_iter; ++it) {
+        std::array<int, K + 1> ord;
+        for (int v = 0; v <= K; ++v) ord[v] = v;
+        std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return vf[a] < vf[b]; });
+        const auto ox = vx;
+        const auto of = vf;
+        for (int v = 0; v <= K; ++v) {
+            vx[v] = ox[ord[v]];
+            vf[v] = of[ord[v]];
+        }
+        if (spread() < tol) {
+            done = true;
+            break;
+        }
+        Pt cen = {0.0, 0.0};
+        for (int i = 0; i < K; ++i) {
+            for (int v = 0; v < K; ++v) cen[i] += vx[v][i];
+            cen[i] /= static_cast<double>(K);
+        }
+        auto along = [&](double coef) {
+            Pt q;
+            for (int i = 0; i < K; ++i) q[i] = cen[i] + coef * (vx[K][i] - cen[i]);
+            return q;
+        };
+        const Pt xr = along(-1.0);
+        const double fr = objective(xr);
+        if (fr < vf[0]) {
+            const Pt xe = along(-2.0);
+            const double fe = objective(xe);
+            if (fe < fr) {
+                vx[K] = xe;
+                vf[K] = fe;
+            } else {
+                vx[K] = xr;
+                vf[K] = fr;
+            }
+        } else if (fr < vf[K - 1]) {
+            vx[K] = xr;
+            vf[K] = fr;
+        } else {
+            const bool outside = fr < vf[K];
+            const Pt xc = along(outside ? -0.5 : 0.5);
+            const double fc = objective(xc);
+            if (fc < (outside ? fr : vf[K])) {
+                vx[K] = xc;
+                vf[K] = fc;
+            } else {
+                for (int v = 1; v <= K; ++v) {
+                    for (int i = 0; i < K; ++i) vx[v][i] = vx[0][i] + 0.5 * (vx[v][i] - vx[0][i]);
+                    vf[v] = objective(vx[v]);
+                }
+            }
+        }
     }
-    for (int64_t i = 0; i < NT; ++i) {
-        if (D) dist_allreduce_sum_f64(D, r + i * nb, nb, s);
-        if (t.has(i, i)) launch_tile_trsv(c, s, t.p(i, i), t.ptr(i, i), nb, static_cast<int>(nb), r + i * nb);
-        if (D) dist_bcast(D, r + i * nb, nb * sizeof(double), dist_owner(i, i, D->P, D->Q), s);
-        for (int q = 0; q < 3; ++q)
-            if (cnt[i * 3 + q])
-                launch_tile_gemv(c, s, (mp_precision)q, ditems + off[i * 3 + q], cnt[i * 3 + q],
-                                 static_cast<int>(nb), r + i * nb);
-    }
-    if (dbg_nll) MP_CUDA(cudaEventRecord(dbg_ev[1], s));
-    launch_square_sum(c, s, r, n, dsum);
-    MP_CUDA(cudaMemsetAsync(dsum + 1, 0, sizeof(double), s));
-    for (int64_t d = 0; d < NT; ++d)
-        if (t.has(d, d)) launch_logdiag_sum(c, s, t.p(d, d), t.ptr(d, d), nb, nb, dsum + 1);
-    if (D) dist_allreduce_sum_f64(D, dsum + 1, 1, s);
-    double h[2];
-    MP_CUDA(cudaMemcpyAsync(h, dsum, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    if (dbg_nll) MP_CUDA(cudaEventRecord(dbg_ev[2], s));
-    MP_CUDA(cudaStreamSynchronize(s));
-    if (dbg_nll) {
-        float a = 0, b = 0;
-        MP_CUDA(cudaEventElapsedTime(&a, dbg_ev[0], dbg_ev[1]));
-        MP_CUDA(cudaEventElapsedTime(&b, dbg_ev[1], dbg_ev[2]));
-        std::fprintf(stderr, "[mpcr] nll: forward solve %.3f ms, sums %.3f ms\n", a, b);
-        for (auto e : dbg_ev) cudaEventDestroy(e);
-    }
-    const double ld = 2.0 * h[1];
-    if (quad) *quad = h[0];
-    if (logdet) *logdet = ld;
-    if (nll) *nll = 0.5 * h[0] + 0.5 * ld + 0.5 * static_cast<double>(n) * std::log(2.0 * M_PI);
-    if (jitter_used) *jitter_used = jit;
+    int best = 0;
+    if (!done)
+        for (int v = 1; v <= K; ++v)
+            if (vf[v] < vf[best]) best = v;
+    if (range_hat) *range_hat = std::exp(vx[best][0]);
+    if (sigma2_hat) *sigma2_hat = std::exp(vx[best][1]);
+    if (nll) *nll = vf[best];
+    if (iterations) *iterations = it;
+    if (converged) *converged = done ? 1 : 0;
     MP_API_END
 }
 

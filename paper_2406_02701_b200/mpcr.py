@@ -495,6 +495,24 @@ def gaussian_nll(z, cov: MPCRTile, jitter: float = 1e-6, max_jitter: float = 1e-
     return dict(zip(("nll", "logdet", "quad", "jitter"), (o.value for o in out)))
 
 
+def matern_mle(cov: MPCRTile, x, y, z, init_log_range: float, init_log_sigma2: float, nu: float = 0.5,
+               max_iter: int = 200, tol: float = 1e-4, jitter: float = 1e-6,
+               max_jitter: float = 1e-3) -> dict:
+    """matern_mle (workloads.cpp:89-110): Nelder-Mead over (log range,
+    log sigma2) with every likelihood evaluated on the GPU in `cov`."""
+    n = cov.info()[0]
+    xs, ys, zs = (np.ascontiguousarray(np.asarray(v, dtype=np.float64).ravel()) for v in (x, y, z))
+    if not (xs.size == ys.size == zs.size == n):
+        raise MPError(1, "matern_mle: x, y and z must have n entries")
+    out = [C.c_double(), C.c_double(), C.c_double(), C.c_int(), C.c_int()]
+    check(lib().mp_tile_matern_mle(cov.ctx.h, cov.h, xs.ctypes.data_as(C.c_void_p),
+                                   ys.ctypes.data_as(C.c_void_p), zs.ctypes.data_as(C.c_void_p), n,
+                                   float(nu), float(init_log_range), float(init_log_sigma2), int(max_iter),
+                                   float(tol), float(jitter), float(max_jitter), *[C.byref(o) for o in out]))
+    return {"range": out[0].value, "sigma2": out[1].value, "nll": out[2].value,
+            "iterations": out[3].value, "converged": bool(out[4].value)}
+
+
 def tile_trsm(a: MPCRTile, b: MPCRTile, side: str = "L", upper_triangle: bool = False,
               transpose: bool = False, alpha: float = 1.0) -> None:
     """MPCRTile.trsm: b overwritten with X."""

@@ -83,3 +83,43 @@ def test_nll_jitter_escalation(ctx):
     with pytest.raises(mp.MPError) as e:
         mp.gaussian_nll(np.ones(n), t2, jitter=0.0)
     assert e.value.kind == "NotPositiveDefinite"
+
+
+def test_matern_mle_matches_reference(ctx, ref):
+    """matern_mle (workloads.cpp:89-110): the same Nelder-Mead path as the
+    reference (identical iteration count) with every likelihood on the GPU;
+    all-FP64 tiles against the reference's Double run (no jitter)."""
+    import paper_2406_02701_b200 as mp
+
+    side, n, nb = 20, 400, 100
+    x, y, _ = grid(n)
+    cov = ref.grid_matern(side, n, 0.5, 0.1, 1.0, 2)
+    z = ref.sample_gp(cov, 4)
+    want = ref.matern_mle(2, side, z, np.log(0.05), np.log(0.5), 200, 1e-4)
+    t = mp.MPCRTile(n, n, nb, nb, None, np.full((4, 4), 2), ctx)
+    got = mp.matern_mle(t, x, y, z, np.log(0.05), np.log(0.5), max_iter=200, tol=1e-4, jitter=0.0)
+    assert got["converged"]
+    assert got["iterations"] == want["iterations"], (got, want)
+    assert abs(got["range"] - want["range"]) <= 1e-8 * want["range"], (got, want)
+    assert abs(got["sigma2"] - want["sigma2"]) <= 1e-8 * want["sigma2"], (got, want)
+    assert abs(got["nll"] - want["nll"]) <= 1e-10 * abs(want["nll"]), (got, want)
+
+
+def test_matern_mle_mixed_precision_close(ctx, ref):
+    """A mixed FP64/FP32/FP16 tile map reaches the FP64 optimum to the
+    precision the FP16 tiles allow."""
+    import paper_2406_02701_b200 as mp
+
+    side, n, nb = 32, 1024, 128
+    x, y, _ = grid(n)
+    z = ref.sample_gp(ref.grid_matern(side, n, 0.5, 0.05, 1.0, 2), 4)
+    nt = n // nb
+    i, j = np.indices((nt, nt))
+    g = np.where(i == j, 2, np.where(abs(i - j) == 1, 1, 0))
+    t64 = mp.MPCRTile(n, n, nb, nb, None, np.full((nt, nt), 2), ctx)
+    tmx = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+    a = mp.matern_mle(t64, x, y, z, np.log(0.03), np.log(0.7), jitter=0.0)
+    b = mp.matern_mle(tmx, x, y, z, np.log(0.03), np.log(0.7), jitter=1e-6)
+    assert a["converged"] and b["converged"]
+    assert abs(b["range"] - a["range"]) <= 2e-2 * a["range"], (a, b)
+    assert abs(b["sigma2"] - a["sigma2"]) <= 2e-2 * a["sigma2"], (a, b)
