@@ -499,6 +499,39 @@ def run_nll(args, world, rank, local):
     print(json.dumps(line))
 
 
+def run_mle(args, world, rank, local):
+    """matern_mle (workloads.cpp:89-110) with every likelihood
+    evaluated on the GPU: Nelder-Mead (host, deterministic) over (log range,
+    log sigma2), start log(range/2), log(0.5).  One step = one full fit."""
+    import torch  # noqa: F401
+
+    import paper_2406_02701_b200 as mp
+
+    ctx = mp.Context(local)
+    n = args.n or 65536
+    nb = args.nb
+    g = band_map(n // nb, args.b64, args.b32)
+    x, y, side = grid_points(n)
+    z = np.random.default_rng(5).standard_normal(n)  # white-noise observations (synthetic)
+    A = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+    fits = []
+    for _ in range(max(1, args.steps)):
+        ctx.synchronize()
+        t0 = time.perf_counter()
+        r = mp.matern_mle(A, x, y, z, np.log(args.range / 2), np.log(0.5), max_iter=200, tol=1e-4)
+        fits.append((time.perf_counter() - t0, r))
+    secs = float(np.median([f[0] for f in fits]))
+    r = fits[-1][1]
+    print(json.dumps({
+        "metric": "matern_mle fit time (Nelder-Mead, GPU likelihood)", "value": secs, "unit": "s",
+        "n_gpus": 1, "steps": len(fits), "warmup": 0, "ms_per_step": secs * 1e3, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "mixed(f64/f32/f16 tiles)", "data": "synthetic",
+        "config": {"workload": f"matern_mle n={n}, tile {nb}, nu=0.5", "n": n, "nb": nb,
+                   "precision_map": f"|i-j|<{args.b64}:FP64, <{args.b32}:FP32, else FP16"},
+        "result": r,
+    }))
+
+
 def run_cast(args, world, rank, local):
     """Config 2 cast line: MPArray::converted bandwidth (n x n, pin -> pout)."""
     import torch
@@ -544,7 +577,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="chol", choices=["chol", "gemm", "cast", "nll"])
+    ap.add_argument("--workload", default="chol", choices=["chol", "gemm", "cast", "nll", "mle"])
     ap.add_argument("--cast", default="double:half")
     ap.add_argument("--n", type=int, default=None,
                     help="matrix order (default 65536 at N=1, 131072 at N>1)")
@@ -571,6 +604,8 @@ def main():
         run_cast(args, world, rank, local)
     elif args.workload == "nll":
         run_nll(args, world, rank, local)
+    elif args.workload == "mle":
+        run_mle(args, world, rank, local)
     else:
         run_chol(args, world, rank, local)
     if world > 1:
