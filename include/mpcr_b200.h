@@ -178,6 +178,14 @@ mp_status mp_trsm(mp_ctx ctx, mp_array a, mp_array b, mp_side side, int upper, i
 /* forwardsolve / backsolve (linalg.cpp:490-496): out precision promote. */
 mp_status mp_forwardsolve(mp_ctx ctx, mp_array l, mp_array b, mp_array out);
 mp_status mp_backsolve(mp_ctx ctx, mp_array u, mp_array b, mp_array out);
+/* solve(a, b) (linalg.cpp:551-575): exactly symmetric a -> Cholesky path,
+ * otherwise / not positive definite -> LU with partial pivoting (lu_kernel,
+ * linalg.cpp:163-193); out = a^-1 b in promote(a, b); zero pivot ->
+ * MP_SINGULAR_MATRIX. */
+mp_status mp_solve(mp_ctx ctx, mp_array a, mp_array b, mp_array out);
+/* chol2inv(u) (linalg.cpp:383-408, 481-488): (U^T U)^-1 from the upper
+ * factor, exactly symmetric, in u's precision. */
+mp_status mp_chol2inv(mp_ctx ctx, mp_array u, mp_array out);
 
 /* ------------------------------------------------------------------------- */
 /* MPCRTile                                                */

@@ -189,6 +189,19 @@ class Ref(_Base):
                                         _i64(B.shape[1]), _ptr(A), _ptr(B), _ptr(out)))
         return out
 
+    def solve(self, pa, pb, A, B):
+        A, B = _f(A), _f(B)
+        out = np.zeros_like(B, order="F")
+        self._check(self.lib.ref_solve(C.c_int(pa), C.c_int(pb), _i64(A.shape[0]), _i64(B.shape[1]),
+                                       _ptr(A), _ptr(B), _ptr(out)))
+        return out
+
+    def chol2inv(self, p, U):
+        U = _f(U)
+        out = np.zeros_like(U, order="F")
+        self._check(self.lib.ref_chol2inv(C.c_int(p), _i64(U.shape[0]), _ptr(U), _ptr(out)))
+        return out
+
     def trisolve(self, upper, pt, pb, T, B):
         T, B = _f(T), _f(B)
         out = np.zeros_like(B, order="F")

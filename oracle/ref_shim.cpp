@@ -236,6 +236,16 @@ int ref_trisolve(int upper, int pt, int pb, std::int64_t n, std::int64_t tn,
     });
 }
 
+// linalg::solve (linalg.cpp:551-575) and chol2inv (linalg.cpp:481-488).
+int ref_solve(int pa, int pb, std::int64_t n, std::int64_t bc, const double* A, const double* B,
+              double* out) {
+    return guard([&] { out_doubles(linalg::solve(mat(A, n, n, pa), mat(B, n, bc, pb)), out); });
+}
+
+int ref_chol2inv(int p, std::int64_t n, const double* U, double* out) {
+    return guard([&] { out_doubles(linalg::chol2inv(mat(U, n, n, p)), out); });
+}
+
 // ew_binary / ew_scalar / ew_unary (array.cpp:252-322).
 int ref_ew_binary(int op, int pa, int pb, std::int64_t r, std::int64_t c, std::int64_t r2,
                   std::int64_t c2, const double* A, const double* B, double* out) {

@@ -72,6 +72,8 @@ SIGNATURES = {
     "mp_trsm": (C.c_int, [_vp, _vp, _vp, C.c_int, C.c_int, C.c_int, C.c_double]),
     "mp_forwardsolve": (C.c_int, [_vp, _vp, _vp, _vp]),
     "mp_backsolve": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "mp_solve": (C.c_int, [_vp, _vp, _vp, _vp]),
+    "mp_chol2inv": (C.c_int, [_vp, _vp, _vp]),
     "mp_tile_create": (C.c_int, [_vp, _i64, _i64, _i64, _i64, C.POINTER(C.c_int), C.POINTER(_vp)]),
     "mp_tile_destroy": (C.c_int, [_vp]),
     "mp_tile_info": (C.c_int, [_vp, _ip, _ip, _ip, _ip, _ip, _ip]),

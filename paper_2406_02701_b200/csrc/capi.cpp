@@ -780,4 +780,97 @@ mp_status mp_backsolve(mp_ctx ctx, mp_array u, mp_array b, mp_array out) {
     return tri_solve_api(ctx, u, b, out, true, "backsolve");
 }
 
+
+// chol2inv (linalg.cpp:383-408): (U^T U)^-1 for the upper factor U, exactly
+// symmetric.  X = U^-1 = (L^-1)^T with L = U^T inverted by the FP64 TRTRI,
+// then X X^T = Linv^T Linv (lower half computed once, mirrored), rounded to
+// U's precision.  Exact zero diagonal -> SingularMatrix.
+mp_status mp_chol2inv(mp_ctx ctx, mp_array u, mp_array out) {
+    MP_API_BEGIN
+    Ctx* c = C_(ctx);
+    Array &x = A_(u, "chol2inv"), &o = A_(out, "chol2inv");
+    require_matrix(x, "chol2inv");
+    if (x.rows != x.cols) fail(MP_SHAPE_MISMATCH, "chol2inv: matrix is not square");
+    require_shape(o, x.rows, x.cols, "chol2inv");
+    require_prec(o, x.prec, "chol2inv");
+    const int64_t n = x.rows;
+    if (n == 0) return MP_OK;
+    const int64_t z = find_zero_diag(c, c->stream, x.prec, x.data, x.ld, n, compute_precision(x.prec));
+    if (z >= 0) fail(MP_SINGULAR_MATRIX, "chol2inv: zero diagonal at index " + std::to_string(z));
+    const size_t nn = static_cast<size_t>(n) * n;
+    double* w = static_cast<double*>(c->ensure_scratch(3 * nn * sizeof(double), 0));
+    double *wu = w, *wl = w + nn, *wi = w + 2 * nn;
+    launch_convert(c, c->stream, x.prec, x.data, x.ld, MP_DOUBLE, wu, n, n, n);
+    launch_zero_triangle(c, c->stream, MP_DOUBLE, wu, n, n, /*upper=*/false);  // U's lower part is unused
+    launch_transpose_raw(c, c->stream, MP_DOUBLE, wu, n, n, n, wl, n);          // L = U^T
+    launch_trtri_lower(c, c->stream, wl, n, wi, n, n);                          // Linv
+    GemmDesc g{MP_DOUBLE, MP_DOUBLE, MP_DOUBLE, true, false, n, n, n, 1.0, 0.0, wi, n, wi, n, wu, n, true};
+    launch_gemm(c, c->stream, g);  // lower of Linv^T Linv
+    launch_mirror_lower(c, c->stream, MP_DOUBLE, wu, n, n);
+    launch_convert(c, c->stream, MP_DOUBLE, wu, n, o.prec, o.data, o.ld, n, n);
+    MP_API_END
+}
+
+// solve(a, b) (linalg.cpp:551-575): out = a^-1 b in promote(a, b).  Exactly
+// symmetric a: chol(a.converted(out_prec)), forwardsolve(U^T), backsolve(U);
+// otherwise (or not positive definite) LU with partial pivoting in the
+// compute precision (lu_solve_impl, :451-476).  Zero pivot -> SingularMatrix.
+mp_status mp_solve(mp_ctx ctx, mp_array a, mp_array b, mp_array out) {
+    MP_API_BEGIN
+    Ctx* c = C_(ctx);
+    Array &x = A_(a, "solve"), &y = A_(b, "solve"), &o = A_(out, "solve");
+    require_matrix(x, "solve");
+    if (x.rows != x.cols) fail(MP_SHAPE_MISMATCH, "solve: matrix is not square");
+    if (y.rows != x.rows)
+        fail(MP_SHAPE_MISMATCH, "solve: rhs has " + std::to_string(y.rows) + " rows, expected " +
+                                    std::to_string(x.rows));
+    require_shape(o, y.rows, y.cols, "solve");
+    const mp_precision po = promote(x.prec, y.prec);
+    require_prec(o, po, "solve");
+    const int64_t n = x.rows;
+    if (n == 0 || y.cols == 0) return MP_OK;
+    if (device_exactly_symmetric(c, c->stream, x.prec, x.data, x.ld, n)) {
+        // SPD fast path through the public entry points (same semantics as the reference)
+        mp_array ac = nullptr, uu = nullptr, lt = nullptr, yy = nullptr;
+        auto cleanup = [&] {
+            for (mp_array h : {ac, uu, lt, yy})
+                if (h) mp_array_destroy(h);
+        };
+        bool ok = mp_array_create(ctx, po, n, n, 1, &ac) == MP_OK && mp_array_create(ctx, po, n, n, 1, &uu) == MP_OK &&
+                  mp_array_create(ctx, po, n, n, 1, &lt) == MP_OK &&
+                  mp_array_create(ctx, po, y.rows, y.cols, 1, &yy) == MP_OK;
+        if (!ok) {
+            cleanup();
+            fail(MP_OUT_OF_MEMORY, "solve: workspace");
+        }
+        mp_status st = mp_convert(ctx, a, ac);
+        int64_t info = -1;
+        if (st == MP_OK) st = mp_chol(ctx, ac, uu, &info);
+        if (st == MP_OK) {
+            st = mp_transpose(ctx, uu, lt);
+            if (st == MP_OK) st = mp_forwardsolve(ctx, lt, b, yy);
+            if (st == MP_OK) st = mp_backsolve(ctx, uu, yy, out);
+            cleanup();
+            if (st != MP_OK) throw Error(st, g_last_error);
+            return MP_OK;
+        }
+        cleanup();
+        if (st != MP_NOT_POSITIVE_DEFINITE) throw Error(st, g_last_error);
+        // not positive definite: fall through to LU
+    }
+    const mp_precision cp = compute_precision(po);
+    const size_t es = elem_bytes(cp);
+    const size_t nn = static_cast<size_t>(n) * n, nb = static_cast<size_t>(y.rows) * y.cols;
+    char* w = static_cast<char*>(c->ensure_scratch((nn + 2 * nb) * es + 512, 0));
+    void* wa = w;
+    void* wb = w + ((nn * es + 255) / 256) * 256;
+    void* wx = static_cast<char*>(wb) + ((nb * es + 255) / 256) * 256;
+    launch_convert(c, c->stream, x.prec, x.data, x.ld, cp, wa, n, n, n);
+    launch_convert(c, c->stream, y.prec, y.data, y.ld, cp, wb, y.rows, y.rows, y.cols);
+    const int64_t zp = lu_solve_device(c, c->stream, cp, wa, n, wb, y.rows, wx, y.rows, y.cols);
+    if (zp >= 0) fail(MP_SINGULAR_MATRIX, "solve: zero pivot at column " + std::to_string(zp));
+    launch_convert(c, c->stream, cp, wx, y.rows, o.prec, o.data, o.ld, y.rows, y.cols);
+    MP_API_END
+}
+
 }  // extern "C"

@@ -144,6 +144,10 @@ struct GemmDesc {
     bool lower_only = false;
 };
 void launch_gemm(Ctx* ctx, cudaStream_t s, const GemmDesc& g);
+// solve.cu: exact symmetry test and LU (partial pivoting) solve
+bool device_exactly_symmetric(Ctx* ctx, cudaStream_t s, mp_precision p, const void* a, int64_t lda, int64_t n);
+int64_t lu_solve_device(Ctx* ctx, cudaStream_t s, mp_precision cp, void* w, int64_t n, const void* b,
+                        int64_t ldb, void* x, int64_t ldx, int64_t ncols);
 // Grid of a persistent tile kernel (one CTA per SM resident): fully
 // persistent when tiles_per_cta <= 0, else whole waves of SMs with at most
 // ~tiles_per_cta tiles per CTA (so SMs are handed back at that granularity

@@ -366,6 +366,22 @@ class linalg:
         check(lib().mp_backsolve(u.ctx.h, u.h, b.h, out.h))
         return out
 
+    @staticmethod
+    def solve(a: MPArray, b: MPArray | None = None) -> MPArray:
+        """solve(a[, b]) (linalg.cpp:544-575); without b, the inverse."""
+        if b is None:
+            b = MPArray.from_numpy(np.eye(a.rows()), a.precision(), a.ctx)
+        out = _like(b, promote(a.precision(), b.precision()))
+        check(lib().mp_solve(a.ctx.h, a.h, b.h, out.h))
+        return out
+
+    @staticmethod
+    def chol2inv(u: MPArray) -> MPArray:
+        """chol2inv (linalg.cpp:481-488): (U^T U)^-1 from the upper factor."""
+        out = MPArray.zeros_matrix(u.rows(), u.cols(), u.precision(), u.ctx)
+        check(lib().mp_chol2inv(u.ctx.h, u.h, out.h))
+        return out
+
 
 class MPCRTile:
     """MPCRTile: per-tile precisions, tiles on the device.

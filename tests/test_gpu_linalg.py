@@ -335,3 +335,81 @@ def test_gemm_half_to_double_nonfinite(ctx):
     got = dc.to_numpy()
     assert np.isnan(got[5]).all() or np.isinf(got[5]).all()
     assert np.all(got[np.arange(128) != 5] == 64.0)
+
+
+@pytest.mark.parametrize("p", [S, D])
+def test_solve_spd_and_lu_paths(ctx, ref, rng, p):
+    """solve(a, b) (linalg.cpp:551-575): exactly symmetric SPD a takes the
+    Cholesky path, a general a the LU path (partial pivoting); both against
+    the reference's solve in the same precisions."""
+    import paper_2406_02701_b200 as mp
+    from oracle.oracle import round_to
+
+    n, k = 200, 7
+    X = rng.standard_normal((n, n))
+    spd = round_to(X @ X.T / n + np.eye(n), p)
+    gen = round_to(rng.standard_normal((n, n)) + 0.1 * np.eye(n), p)  # pivoting happens
+    B = round_to(rng.standard_normal((n, k)), p)
+    for A in (spd, gen):
+        da = mp.MPArray.from_numpy(A, mp.Precision(p), ctx)
+        db = mp.MPArray.from_numpy(B, mp.Precision(p), ctx)
+        got = mp.linalg.solve(da, db).to_numpy()
+        want = ref.solve(p, p, A, B)
+        cond = np.linalg.cond(A)
+        tol = 16 * n * U[p] * cond
+        assert rel(got, want) <= tol, (p, rel(got, want), tol)
+    # inverse (b omitted) of the general matrix
+    inv = mp.linalg.solve(mp.MPArray.from_numpy(gen, mp.Precision(p), ctx)).to_numpy()
+    assert rel(inv, ref.solve(p, p, gen, np.eye(n))) <= 16 * n * U[p] * np.linalg.cond(gen)
+
+
+def test_solve_lu_bit_exact_factors(ctx, ref, rng):
+    """The LU path follows lu_kernel's operation order (first maximal pivot,
+    IEEE division, separate multiply and subtract): on a small matrix with
+    many ties and a permutation-heavy pattern the FP64 solution equals the
+    reference's to the last bit or within a few ulps (substitution order)."""
+    import paper_2406_02701_b200 as mp
+
+    n = 48
+    A = np.round(rng.standard_normal((n, n)) * 4) / 4  # many equal magnitudes (ties)
+    A += np.diag(np.where(np.arange(n) % 3 == 0, 0.0, 0.5))
+    B = rng.standard_normal((n, 2))
+    got = mp.linalg.solve(mp.MPArray.from_numpy(A, mp.Precision.Double, ctx),
+                          mp.MPArray.from_numpy(B, mp.Precision.Double, ctx)).to_numpy()
+    want = ref.solve(D, D, A, B)
+    assert np.max(np.abs(got - want) / np.maximum(np.abs(want), 1e-300)) <= 1e-12
+
+
+def test_solve_errors(ctx):
+    import paper_2406_02701_b200 as mp
+
+    sing = np.ones((8, 8))
+    with pytest.raises(mp.MPError) as e:
+        mp.linalg.solve(mp.MPArray.from_numpy(sing, mp.Precision.Double, ctx),
+                        mp.MPArray.from_numpy(np.ones((8, 1)), mp.Precision.Double, ctx))
+    assert e.value.kind == "SingularMatrix"
+    with pytest.raises(mp.MPError) as e:
+        mp.linalg.solve(mp.MPArray.from_numpy(np.eye(8), mp.Precision.Double, ctx),
+                        mp.MPArray.from_numpy(np.ones((7, 1)), mp.Precision.Double, ctx))
+    assert e.value.kind == "ShapeMismatch"
+
+
+@pytest.mark.parametrize("p", [S, D])
+def test_chol2inv(ctx, ref, rng, p):
+    """chol2inv (linalg.cpp:383-408): exactly symmetric (U^T U)^-1."""
+    import paper_2406_02701_b200 as mp
+    from oracle.oracle import round_to
+
+    n = 160
+    X = rng.standard_normal((n, n))
+    A = X @ X.T / n + np.eye(n)
+    Uf = round_to(ref.chol(p, round_to(A, p)), p)
+    got = mp.linalg.chol2inv(mp.MPArray.from_numpy(Uf, mp.Precision(p), ctx)).to_numpy()
+    want = ref.chol2inv(p, Uf)
+    assert np.array_equal(got, got.T)
+    assert rel(got, want) <= 16 * n * U[p] * np.linalg.cond(A), rel(got, want)
+    with pytest.raises(mp.MPError) as e:
+        Z = Uf.copy()
+        Z[5, 5] = 0.0
+        mp.linalg.chol2inv(mp.MPArray.from_numpy(Z, mp.Precision(p), ctx))
+    assert e.value.kind == "SingularMatrix"
