@@ -41,6 +41,27 @@ PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
+def write_results(path, records, fmt=None):
+    """BenchRecord-compatible results (io.hpp:11-20, io.cpp:97-126): CSV header
+    op,n,precision,placement,reps,median_seconds,rel_frob_err with %.17g
+    numbers, or a JSON array of the same objects (extra keys carry the
+    roofline fields).  rel_frob_err is NaN / null where it was not measured."""
+    fmt = fmt or ("json" if path.endswith(".json") else "csv")
+    keys = ["op", "n", "precision", "placement", "reps", "median_seconds", "rel_frob_err"]
+    if fmt == "csv":
+        with open(path, "w") as f:
+            f.write(",".join(keys) + "\n")
+            for r in records:
+                def num(v):
+                    return "nan" if v is None else "%.17g" % v
+                f.write(f"{r['op']},{r['n']},{r['precision']},{r['placement']},{r['reps']},"
+                        f"{num(r['median_seconds'])},{num(r.get('rel_frob_err'))}\n")
+    else:
+        with open(path, "w") as f:
+            json.dump(records, f, indent=2)
+            f.write("\n")
+
+
 def peaks():
     try:
         with open(PEAKS_FILE) as f:
@@ -405,6 +426,14 @@ def run_chol(args, world, rank, local):
         line["cpu_baseline"], _ = cpu_reference_chol(args)
     if rank == 0:
         print(json.dumps(line))
+        if args.results:
+            steps_s = sorted(a.elapsed_time(b) * 1e-3 for a, b in ev)
+            write_results(args.results, [{
+                "op": "tile_chol", "n": n, "precision": f"mixed(b64={args.b64},b32={args.b32})",
+                "placement": f"gpu:{world}", "reps": args.steps,
+                "median_seconds": steps_s[len(steps_s) // 2], "rel_frob_err": None,
+                "tflops": value, "blended_roofline_frac": line["blended_roofline"]["frac"],
+                "e2e_tflops": line.get("e2e", {}).get("value")}])
     ctx.synchronize()
 
 
@@ -594,6 +623,8 @@ def main():
     ap.add_argument("--cpu-nb", type=int, default=256)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--results", default=None,
+                    help="also write a BenchRecord CSV/JSON (io.hpp:11-20) to this path")
     args = ap.parse_args()
     world, rank, local = dist_setup()
     if args.impl == "reference":
