@@ -429,7 +429,7 @@ def run_chol(args, world, rank, local):
         if args.results:
             steps_s = sorted(a.elapsed_time(b) * 1e-3 for a, b in ev)
             write_results(args.results, [{
-                "op": "tile_chol", "n": n, "precision": f"mixed(b64={args.b64},b32={args.b32})",
+                "op": "tile_chol", "n": n, "precision": f"mixed(b64={args.b64};b32={args.b32})",
                 "placement": f"gpu:{world}", "reps": args.steps,
                 "median_seconds": steps_s[len(steps_s) // 2], "rel_frob_err": None,
                 "tflops": value, "blended_roofline_frac": line["blended_roofline"]["frac"],

@@ -12,13 +12,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 def test_results_csv_and_json(tmp_path):
     import bench
 
-    rec = {"op": "tile_chol", "n": 65536, "precision": "mixed(b64=1,b32=2)", "placement": "gpu:1",
+    rec = {"op": "tile_chol", "n": 65536, "precision": "mixed(b64=1;b32=2)", "placement": "gpu:1",
            "reps": 3, "median_seconds": 0.1425, "rel_frob_err": 1.25e-7, "tflops": 640.0}
     p = tmp_path / "r.csv"
     bench.write_results(str(p), [rec])
     rows = list(csv.reader(open(p)))
     assert rows[0] == ["op", "n", "precision", "placement", "reps", "median_seconds", "rel_frob_err"]
-    assert rows[1][:5] == ["tile_chol", "65536", "mixed(b64=1,b32=2)", "gpu:1", "3"]
+    assert rows[1][:5] == ["tile_chol", "65536", "mixed(b64=1;b32=2)", "gpu:1", "3"]
     assert float(rows[1][5]) == 0.1425 and float(rows[1][6]) == 1.25e-7
     q = tmp_path / "r.json"
     bench.write_results(str(q), [rec])
