@@ -16,6 +16,8 @@
 // tensor-core GEMM with this inverse (see tile.cpp).
 #include <cooperative_groups.h>
 
+#include <algorithm>
+
 #include <type_traits>
 #include <cstdlib>
 #include <vector>
@@ -352,7 +354,15 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
     ProfScope ps(ctx, MP_PROF_POTRF, s, static_cast<double>(n) * n * n / 3.0);
     if (p == MP_DOUBLE) {
         static bool cfg = false;
-        const size_t shm = (2 * PB * (PB + 1) + 2 * 16 * (PB + 1) + 3 * 256) * sizeof(double);
+        // The factorization is latency-bound: by default each CTA reserves
+        // most of its SM's shared memory so no other kernel's CTAs share the
+        // SM with it (MPCR_POTRF_EXCLUSIVE=0 turns this off).
+        static const bool exclusive = [] {
+            const char* e = getenv("MPCR_POTRF_EXCLUSIVE");
+            return !(e && e[0] == '0');
+        }();
+        const size_t shm_need = (2 * PB * (PB + 1) + 2 * 16 * (PB + 1) + 3 * 256) * sizeof(double);
+        const size_t shm = exclusive ? std::max<size_t>(shm_need, 160 * 1024) : shm_need;
         if (!cfg) {
             MP_CUDA(cudaFuncSetAttribute((void*)potrf_coop_kernel<double>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
