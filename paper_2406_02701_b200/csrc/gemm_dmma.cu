@@ -15,6 +15,7 @@
 // fragment reads conflict-free (2 wavefronts per 256-byte warp load).
 // blockIdx.z indexes the problem of a grouped launch; lower_only skips CTA
 // tiles strictly above the diagonal and masks the rest (SYRK).
+#include <algorithm>
 #include <type_traits>
 
 #include "gemm_dmma.hpp"
@@ -315,12 +316,13 @@ void launch_bt(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count) {
     static bool configured = false;
     if (!configured) {
         MP_CUDA(cudaFuncSetAttribute(dmma_gemm_kernel<BT, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     CF::SMEM));
+                                     std::max(CF::SMEM, 160 * 1024)));
         configured = true;
     }
     const dim3 grid(static_cast<unsigned>((g.m + BT - 1) / BT), static_cast<unsigned>((g.n + BT - 1) / BT),
                     static_cast<unsigned>(g.problems ? count : 1));
-    dmma_gemm_kernel<BT, TI><<<grid, CF::NTHR, CF::SMEM, s>>>(g);
+    const int smem = g.exclusive ? std::max(CF::SMEM, 160 * 1024) : CF::SMEM;
+    dmma_gemm_kernel<BT, TI><<<grid, CF::NTHR, smem, s>>>(g);
 }
 
 template <typename TI>

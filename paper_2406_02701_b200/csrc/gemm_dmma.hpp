@@ -20,6 +20,7 @@ struct DmmaArgs {
     bool lower_only;
     const TileProblem* problems;  // grouped launch when non-null
     mp_precision pin = MP_DOUBLE;  // operand storage precision
+    bool exclusive = false;        // reserve the SM (latency-critical launches)
 };
 
 void launch_dmma_gemm(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count);

@@ -182,6 +182,8 @@ struct GroupedGemm {
     // Optional: all operand tiles are slices of one slab (enables TMA maps).
     const void* slab = nullptr;
     int64_t slab_tiles = 0;
+    // Critical-path launch: each CTA reserves its SM (no co-resident CTAs).
+    bool exclusive = false;
 };
 void launch_grouped_gemm(Ctx* ctx, cudaStream_t s, const GroupedGemm& g);
 

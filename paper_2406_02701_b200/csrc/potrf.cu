@@ -484,9 +484,11 @@ void launch_trtri_plan(Ctx* ctx, cudaStream_t s, TrtriPlan* P, bool leaves_done)
         if (lv.cnt) {
             GroupedGemm g1{MP_DOUBLE, MP_DOUBLE, false, h, h, h, ldl, ldi, h, 1.0, 0.0,
                            P->dev + lv.off1, lv.cnt};
+            g1.exclusive = true;  // TRTRI sits on the Cholesky critical path
             launch_grouped_gemm(ctx, s, g1);
             GroupedGemm g2{MP_DOUBLE, MP_DOUBLE, false, h, h, h, ldi, h, ldi, -1.0, 0.0,
                            P->dev + lv.off2, lv.cnt};
+            g2.exclusive = true;
             launch_grouped_gemm(ctx, s, g2);
         }
         for (const auto& rg : lv.rag) {

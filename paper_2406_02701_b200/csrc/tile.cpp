@@ -654,6 +654,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             if (U.n_pn[q]) {
                 GroupedGemm g{(mp_precision)q, MP_DOUBLE, true, nb, nb, nb, nb, nb, nb, -1.0, 1.0,
                               reinterpret_cast<const TileProblem*>(dl + U.pn[q]), U.n_pn[q]};
+                g.exclusive = part == 2;  // the diagonal SYRK feeding the next POTRF
                 launch_grouped_gemm(c, st, g);
             }
     };
