@@ -673,7 +673,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         //   bulk GEMMs hand SMs back every few tiles so it is never starved.
         static const int tpc_env = [] {
             const char* e = getenv("MPCR_TILES_PER_CTA");
-            return e ? atoi(e) : 16;
+            return e ? atoi(e) : 24;
         }();
         const int bulk_tpc = la ? tpc_env : 0;
         cudaStream_t sl2 = la ? c->hi2 : s;
