@@ -464,11 +464,16 @@ def run_gemm(args, world, rank, local):
     ms = e0.elapsed_time(e1) / args.steps
     tf = 2 * n ** 3 / (ms * 1e-3) / 1e12
     pk, src = peaks()
+    # FP16: tcgen05 kind::f16 at the measured burst rate; FP32: 3xTF32 (3 TF32
+    # MMAs per product, TF32 = half the FP16 rate); FP64: measured DMMA peak
+    peak, peak_src = {0: (pk["bf16_tflops"], f"{src} bf16_tflops (burst)"),
+                      1: (pk["bf16_tflops"] / 6, f"{src} bf16_tflops / 2 / 3 (3xTF32)"),
+                      2: (37.1, "measured DMMA peak, tools/micro/fp64_peak.cu")}[int(p)]
     print(json.dumps({"metric": f"{args.prec} GEMM TFLOP/s", "value": tf, "unit": "TFLOP/s",
                       "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                       "higher_is_better": True, "config": {"workload": f"GEMM {n}^3 {args.prec}"},
-                      "roofline": {"bound": "tensor", "achieved": tf, "peak": pk["bf16_tflops"],
-                                   "unit": "TFLOP/s", "frac": tf / pk["bf16_tflops"]} if p == 0 else None,
+                      "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
+                                   "frac": tf / peak, "peak_source": peak_src},
                       "clocks": clk.summary()}))
 
 
