@@ -123,6 +123,48 @@ __global__ void __launch_bounds__(256) convert_widen_kernel(const TI* __restrict
     }
 }
 
+// Widening (sizeof(TO) > sizeof(TI)) with both streams at full width: each
+// lane loads 16 bytes (16 / sizeof(TI) elements), converts into its warp's
+// shared buffer, and the warp writes the R = sizeof(TO) / sizeof(TI) output
+// rows of 512 contiguous bytes each (lane-consecutive 16-byte stores).
+// Measured half -> double at 32768^2: 6.1 TB/s vs 5.3-5.5 output-centric.
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256) convert_widen_smem_kernel(const TI* __restrict__ in,
+                                                                 TO* __restrict__ out, int64_t n16) {
+    constexpr int EIN = 16 / sizeof(TI);           // input elements per lane
+    constexpr int R = sizeof(TO) / sizeof(TI);     // 16-byte output chunks per lane
+    __shared__ uint4 buf[8][32 * R + 1];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * 8;
+    for (int64_t wc = static_cast<int64_t>(blockIdx.x) * 8 + warp; wc * 32 < n16; wc += nwarps) {
+        const int64_t t = wc * 32 + lane;
+        if (t < n16) {
+            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(in) + t);
+            TI a[EIN];
+            memcpy(a, &v, sizeof(a));
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                TO b[16 / sizeof(TO)];
+#pragma unroll
+                for (int k = 0; k < 16 / static_cast<int>(sizeof(TO)); ++k)
+                    b[k] = cvt1<TI, TO>(a[q * (16 / sizeof(TO)) + k]);
+                uint4 o;
+                memcpy(&o, b, sizeof(o));
+                buf[warp][lane * R + q] = o;
+            }
+        }
+        __syncwarp();
+        uint4* o = reinterpret_cast<uint4*>(out) + wc * 32 * R;
+        const int64_t lim = n16 * R - wc * 32 * R;  // chunks left from this warp's base
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            const int idx = q * 32 + lane;
+            if (idx < lim) __stcs(o + idx, buf[warp][idx]);
+        }
+        __syncwarp();
+    }
+}
+
 // Strided / tail path: one element per thread over a rows x cols block.
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(256) convert_2d_kernel(const TI* __restrict__ in, int64_t ldi,
@@ -148,6 +190,19 @@ void run_convert(Ctx* ctx, cudaStream_t s, const void* src, int64_t lds, void* d
     const bool aligned = (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(out) % 16 == 0);
     if (contiguous && aligned && sizeof(TO) == 8 && sizeof(TI) < 8) {
+        constexpr int EIN = 16 / sizeof(TI);
+        const int64_t n16 = n / EIN;
+        if (n16 > 0) {
+            convert_widen_smem_kernel<TI, TO><<<4 * ctx->sm_count, 256, 0, s>>>(in, out, n16);
+            count_launch(ctx);
+        }
+        const int64_t done = n16 * EIN;
+        if (done < n) {
+            convert_2d_kernel<TI, TO><<<1, 256, 0, s>>>(in + done, n - done, out + done,
+                                                         n - done, n - done, 1);
+            count_launch(ctx);
+        }
+    } else if (false) {  // output-centric widening, superseded by the shared-memory staged kernel
         constexpr int E = 16 / sizeof(TO);
         const int64_t nq = n / E;
         if (nq > 0) {
