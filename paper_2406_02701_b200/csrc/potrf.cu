@@ -130,7 +130,8 @@ __device__ __forceinline__ void block_nt(T (&acc)[4][4], const T* P, int64_t ldp
 #include "potrf_block.cuh"
 
 // Factor diagonal block kb (already fully updated) held in global A: load,
-// factor, invert; write L_kk back, Dinv to `dinv` (and to linv_diag).
+// factor + invert (potrf_block.cuh); write L_kk back, Dinv to `dinv` (and to
+// linv_diag).
 template <typename T>
 __device__ void diag_step(T* A, int64_t lda, int n, int kb, T* dinv, T* linv_diag, int64_t ldi,
                           int64_t* info, int64_t info_off, int* abort_flag, T (*D)[PB + 1],
@@ -139,14 +140,16 @@ __device__ void diag_step(T* A, int64_t lda, int n, int kb, T* dinv, T* linv_dia
     PTRACE2(kb, 0);
     for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
         const int r = idx % PB, c = idx / PB;
-        D[r][c] = (r < bb && c < bb && r >= c) ? A[(int64_t)(k0 + c) * lda + k0 + r] : T(0);
+        // lower triangle, zeros above, identity padding past the matrix edge
+        D[r][c] = (r < bb && c < bb) ? (r >= c ? A[(int64_t)(k0 + c) * lda + k0 + r] : T(0))
+                                     : (r == c ? T(1) : T(0));
     }
     __syncthreads();
     PTRACE2(kb, 1);
     __shared__ T s_inv[PB];  // reciprocals of the pivots
-    const int fail = factor_block(D, X, bb, s_fail, s_inv);
+    const int fail = factor_invert_block(D, X, Tm, s_fail, s_inv);
     PTRACE2(kb, 2);
-    if (fail >= 0) {
+    if (fail >= 0 && fail < bb) {
         if (threadIdx.x == 0) {
             if (*info < 0) *info = info_off + k0 + fail;
             atomicExch(abort_flag, 1);
@@ -158,14 +161,14 @@ __device__ void diag_step(T* A, int64_t lda, int n, int kb, T* dinv, T* linv_dia
         if (r >= c) A[(int64_t)(k0 + c) * lda + k0 + r] = D[r][c];
     }
     PTRACE2(kb, 3);
-    invert_block<T>(D, X, Tm, bb, s_inv);
-    PTRACE2(kb, 4);
     T* Di = dinv + (int64_t)kb * PB * PB;
     for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
         const int r = idx % PB, c = idx / PB;
-        Di[c * PB + r] = X[r][c];
-        if (linv_diag && r < bb && c < bb) linv_diag[(int64_t)(k0 + c) * ldi + k0 + r] = X[r][c];
+        const T v = (r < bb && c < bb) ? X[r][c] : T(0);
+        Di[c * PB + r] = v;
+        if (linv_diag && r < bb && c < bb) linv_diag[(int64_t)(k0 + c) * ldi + k0 + r] = v;
     }
+    PTRACE2(kb, 4);
 }
 
 // Cooperative blocked right-looking POTRF.  Per 64-block step kb:
@@ -177,7 +180,7 @@ __device__ void diag_step(T* A, int64_t lda, int n, int kb, T* dinv, T* linv_dia
 //   barrier
 // so the diagonal factorization overlaps the trailing update.
 template <typename T>
-__global__ void __launch_bounds__(PT) potrf_coop_kernel(T* A, int64_t lda, int n, T* dinv,
+__global__ void __launch_bounds__(PT, 1) potrf_coop_kernel(T* A, int64_t lda, int n, T* dinv,
                                                         int64_t* info, int64_t info_off,
                                                         GridBar* bar, int* abort_flag,
                                                         T* linv_diag, int64_t ldi) {
@@ -390,7 +393,7 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
             double a2[4] = {};
             for (int kb = 1; kb < nblk && kb < 64; ++kb)
                 for (int q = 0; q < 4; ++q) a2[q] += static_cast<double>(t2[kb * 6 + q + 1] - t2[kb * 6 + q]);
-            fprintf(stderr, "  diag: load %.0f factor %.0f writeL %.0f invert %.0f\n", a2[0], a2[1], a2[2], a2[3]);
+            fprintf(stderr, "  diag: load %.0f factor+invert %.0f writeL %.0f writeDinv %.0f\n", a2[0], a2[1], a2[2], a2[3]);
             fprintf(stderr, "potrf trace (cycles, summed over %d steps): panel %.0f bar1 %.0f update %.0f diag %.0f bar2 %.0f\n",
                     nblk - 1, acc[0], acc[1], acc[2], acc[3], acc[4]);
         }
