@@ -40,13 +40,7 @@ struct GridBar {
 // Optional per-step clock trace of CTA 0 (MPCR_POTRF_TRACE=1, diagnostics).
 __device__ int g_trace_on = 0;
 __device__ long long g_trace[64 * 6];
-__device__ long long g_trace2[64 * 6];
 
-#define PTRACE2(kb, slot)                                                            \
-    do {                                                                             \
-        if (g_trace_on && blockIdx.x == 0 && threadIdx.x == 0 && (kb) < 64)          \
-            g_trace2[(kb) * 6 + (slot)] = clock64();                                 \
-    } while (0)
 #define PTRACE(kb, slot)                                                             \
     do {                                                                             \
         if (g_trace_on && blockIdx.x == 0 && threadIdx.x == 0 && (kb) < 64)          \
@@ -69,6 +63,20 @@ __device__ __forceinline__ void grid_sync(GridBar* bar, unsigned int nblocks) {
         __threadfence();
     }
     __syncthreads();
+}
+
+// Arrive at a grid barrier without waiting for it (the CTA's prior global
+// stores are published first).
+__device__ __forceinline__ void grid_arrive(GridBar* bar, unsigned int nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&bar->count, 1u) == nblocks - 1) {
+            atomicExch(&bar->count, 0u);
+            __threadfence();
+            atomicAdd(&bar->gen, 1u);
+        }
+    }
 }
 
 // acc(64x64 per CTA, 4x4 per thread) += P (64 x kk, ldp) * Q (64 x kk, ldq)^T
@@ -129,26 +137,16 @@ __device__ __forceinline__ void block_nt(T (&acc)[4][4], const T* P, int64_t ldp
 
 #include "potrf_block.cuh"
 
-// Factor diagonal block kb (already fully updated) held in global A: load,
-// factor + invert (potrf_block.cuh); write L_kk back, Dinv to `dinv` (and to
-// linv_diag).
+// Factor the diagonal block kb held in D (lower, zeros above, identity
+// padding) and invert it (potrf_block.cuh); write L_kk to A and Dinv to
+// `dinv` (and to linv_diag).  X keeps Dinv for the CTA's next panel block.
 template <typename T>
-__device__ void diag_step(T* A, int64_t lda, int n, int kb, T* dinv, T* linv_diag, int64_t ldi,
-                          int64_t* info, int64_t info_off, int* abort_flag, T (*D)[PB + 1],
-                          T (*X)[PB + 1], T* Tm, int* s_fail) {
+__device__ void diag_factor_store(T* A, int64_t lda, int n, int kb, T* dinv, T* linv_diag, int64_t ldi,
+                                  int64_t* info, int64_t info_off, int* abort_flag, T (*D)[PB + 1],
+                                  T (*X)[PB + 1], T* Tm, int* s_fail) {
     const int k0 = kb * PB, bb = min(PB, n - k0);
-    PTRACE2(kb, 0);
-    for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
-        const int r = idx % PB, c = idx / PB;
-        // lower triangle, zeros above, identity padding past the matrix edge
-        D[r][c] = (r < bb && c < bb) ? (r >= c ? A[(int64_t)(k0 + c) * lda + k0 + r] : T(0))
-                                     : (r == c ? T(1) : T(0));
-    }
-    __syncthreads();
-    PTRACE2(kb, 1);
     __shared__ T s_inv[PB];  // reciprocals of the pivots
     const int fail = factor_invert_block(D, X, Tm, s_fail, s_inv);
-    PTRACE2(kb, 2);
     if (fail >= 0 && fail < bb) {
         if (threadIdx.x == 0) {
             if (*info < 0) *info = info_off + k0 + fail;
@@ -160,7 +158,6 @@ __device__ void diag_step(T* A, int64_t lda, int n, int kb, T* dinv, T* linv_dia
         const int r = idx % bb, c = idx / bb;
         if (r >= c) A[(int64_t)(k0 + c) * lda + k0 + r] = D[r][c];
     }
-    PTRACE2(kb, 3);
     T* Di = dinv + (int64_t)kb * PB * PB;
     for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
         const int r = idx % PB, c = idx / PB;
@@ -168,21 +165,21 @@ __device__ void diag_step(T* A, int64_t lda, int n, int kb, T* dinv, T* linv_dia
         Di[c * PB + r] = v;
         if (linv_diag && r < bb && c < bb) linv_diag[(int64_t)(k0 + c) * ldi + k0 + r] = v;
     }
-    PTRACE2(kb, 4);
 }
 
 // Cooperative blocked right-looking POTRF.  Per 64-block step kb:
-//   phase 2  all CTAs: panel X_ib = A_ib,kb * Dinv_kb^T
-//   barrier
-//   phase 3  CTA 0 updates block (kb+1, kb+1) and factors + inverts it
-//            (the next step's diagonal work), the other CTAs update the
-//            rest of the trailing lower triangle
-//   barrier
-// so the diagonal factorization overlaps the trailing update.
+//   CTA 0     panel block kb+1 = A_{kb+1,kb} Dinv_kb^T (Dinv still in shared
+//             memory), published with a non-waiting arrive at barrier 1;
+//             then A_{kb+1,kb+1} -= P P^T from shared memory and the factor +
+//             inverse of that block: the next step's diagonal work never
+//             waits for the other CTAs' panels
+//   others    panel blocks kb+2.., barrier 1, trailing update of the lower
+//             triangle except block (kb+1, kb+1)
+//   barrier 2 (all)
 template <typename T>
 __global__ void __launch_bounds__(PT, 1) potrf_coop_kernel(T* A, int64_t lda, int n, T* dinv,
                                                         int64_t* info, int64_t info_off,
-                                                        GridBar* bar, int* abort_flag,
+                                                        GridBar* bar, GridBar* bar1, int* abort_flag,
                                                         T* linv_diag, int64_t ldi) {
     extern __shared__ __align__(16) unsigned char psm[];
     T (*D)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(psm);
@@ -193,86 +190,143 @@ __global__ void __launch_bounds__(PT, 1) potrf_coop_kernel(T* A, int64_t lda, in
     T* Tm = reinterpret_cast<T*>(psm + 2 * sizeof(T) * PB * (PB + 1) + 2 * sizeof(T) * 16 * (PB + 1));
     __shared__ int s_fail;
     const int nblk = (n + PB - 1) / PB;
-    const unsigned int G = gridDim.x;
+    const unsigned int G = gridDim.x;  // >= 2 whenever nblk >= 2
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
 
-    if (blockIdx.x == 0)
-        diag_step(A, lda, n, 0, dinv, linv_diag, ldi, info, info_off, abort_flag, D, X, Tm, &s_fail);
+    if (blockIdx.x == 0) {
+        const int bb = min(PB, n);
+        for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
+            const int r = idx % PB, c = idx / PB;
+            D[r][c] = (r < bb && c < bb) ? (r >= c ? A[(int64_t)c * lda + r] : T(0)) : (r == c ? T(1) : T(0));
+        }
+        __syncthreads();
+        diag_factor_store(A, lda, n, 0, dinv, linv_diag, ldi, info, info_off, abort_flag, D, X, Tm, &s_fail);
+    }
     grid_sync(bar, G);
     if (*(volatile int*)abort_flag) return;
-    for (int kb = 0; kb < nblk; ++kb) {
-        const int k0 = kb * PB;
-        const int bb = min(PB, n - k0);
-        // ---- phase 2: panel X = A_panel * Dinv^T ------------------------
-        const T* Di = dinv + (int64_t)kb * PB * PB;
-        PTRACE(kb, 0);
-        for (int ib = kb + 1 + blockIdx.x; ib < nblk; ib += G) {
-            const int r0 = ib * PB, rb = min(PB, n - r0);
-            T acc[4][4] = {};
-            block_nt(acc, A + (int64_t)k0 * lda + r0, lda, rb, Di, PB, bb, bb, Ps, Qs);
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int r = tx + 16 * i, c = ty + 16 * j;
-                    if (r < rb && c < bb) A[(int64_t)(k0 + c) * lda + r0 + r] = acc[i][j];
-                }
-            __syncthreads();
-        }
-        if (kb + 1 == nblk) break;
-        PTRACE(kb, 1);
-        grid_sync(bar, G);
-        PTRACE(kb, 2);
-        // ---- phase 3: trailing update; CTA 0 does the next diagonal ----
+    for (int kb = 0; kb + 1 < nblk; ++kb) {
+        const int k0 = kb * PB;  // a full block (not the last one)
         const int rest = nblk - kb - 1;
-        const int items = rest * (rest + 1) / 2;
-        auto update_item = [&](int it) {
-            int jj = 0, rem = it;
-            while (rem >= rest - jj) {
-                rem -= rest - jj;
-                ++jj;
-            }
-            const int jb = kb + 1 + jj, ib = jb + rem;
-            const int r0 = ib * PB, c0 = jb * PB;
-            const int rb = min(PB, n - r0), cb = min(PB, n - c0);
-            // the block's old values are loaded while block_nt runs (no aliasing
-            // with its reads: different columns), all before any store
-            T old[4][4];
+        PTRACE(kb, 0);
+        if (blockIdx.x == 0) {
+            const int r0 = k0 + PB, rb = min(PB, n - r0);
+            T old[4][4];  // block (kb+1, kb+1), loaded early
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int r = tx + 16 * i, c = ty + 16 * j;
-                    old[i][j] = (r < rb && c < cb) ? A[(int64_t)(c0 + c) * lda + r0 + r] : T(0);
+                    old[i][j] = (r < rb && c < rb && r >= c) ? A[(int64_t)(r0 + c) * lda + r0 + r] : T(0);
                 }
+            for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
+                const int r = idx % PB, c = idx / PB;
+                D[r][c] = r < rb ? A[(int64_t)(k0 + c) * lda + r0 + r] : T(0);
+            }
+            __syncthreads();
             T acc[4][4] = {};
-            block_nt(acc, A + (int64_t)k0 * lda + r0, lda, rb, A + (int64_t)k0 * lda + c0, lda, cb,
-                     bb, Ps, Qs);
+#pragma unroll 4
+            for (int k = 0; k < PB; ++k) {
+                T a[4], b[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = D[tx + 16 * i][k];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) b[j] = X[ty + 16 * j][k];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+            }
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const int r = tx + 16 * i, c = ty + 16 * j;
-                    if (r < rb && c < cb && (ib != jb || r >= c))
-                        A[(int64_t)(c0 + c) * lda + r0 + r] = old[i][j] - acc[i][j];
+                    if (r < rb) A[(int64_t)(k0 + c) * lda + r0 + r] = acc[i][j];
                 }
             __syncthreads();
-        };
-        if (blockIdx.x == 0) {
-            update_item(0);  // item 0 is (kb+1, kb+1)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) D[tx + 16 * i][ty + 16 * j] = acc[i][j];
+            grid_arrive(bar1, G);  // also orders the D stores before the reads below
+            PTRACE(kb, 1);
+#pragma unroll 4
+            for (int k = 0; k < PB; ++k) {
+                T a[4], b[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = D[tx + 16 * i][k];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) b[j] = D[ty + 16 * j][k];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) old[i][j] = fma(-a[i], b[j], old[i][j]);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const int r = tx + 16 * i, c = ty + 16 * j;
+                    D[r][c] = (r < rb && c < rb) ? (r >= c ? old[i][j] : T(0)) : (r == c ? T(1) : T(0));
+                }
+            __syncthreads();
+            PTRACE(kb, 2);
+            diag_factor_store(A, lda, n, kb + 1, dinv, linv_diag, ldi, info, info_off, abort_flag, D, X, Tm,
+                              &s_fail);
             PTRACE(kb, 3);
-            __threadfence_block();
-            diag_step(A, lda, n, kb + 1, dinv, linv_diag, ldi, info, info_off, abort_flag, D, X, Tm,
-                      &s_fail);
-            PTRACE(kb, 4);
         } else {
-            for (int it = blockIdx.x; it < items; it += G - 1 > 0 ? G - 1 : 1) {
-                if (it == 0) continue;
-                update_item(it);
+            const T* Di = dinv + (int64_t)kb * PB * PB;
+            for (int ib = kb + 1 + blockIdx.x; ib < nblk; ib += G - 1) {
+                const int r0 = ib * PB, rb = min(PB, n - r0);
+                T acc[4][4] = {};
+                block_nt(acc, A + (int64_t)k0 * lda + r0, lda, rb, Di, PB, PB, PB, Ps, Qs);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int r = tx + 16 * i, c = ty + 16 * j;
+                        if (r < rb) A[(int64_t)(k0 + c) * lda + r0 + r] = acc[i][j];
+                    }
+                __syncthreads();
+            }
+            grid_sync(bar1, G);
+            const int items = rest * (rest + 1) / 2;  // item 0 is (kb+1, kb+1): CTA 0's
+            for (int it = blockIdx.x; it < items; it += G - 1) {
+                int jj = 0, rem = it;
+                while (rem >= rest - jj) {
+                    rem -= rest - jj;
+                    ++jj;
+                }
+                const int jb = kb + 1 + jj, ib = jb + rem;
+                const int r0 = ib * PB, c0 = jb * PB;
+                const int rb = min(PB, n - r0), cb = min(PB, n - c0);
+                // the block's old values are loaded while block_nt runs (no aliasing
+                // with its reads: different columns), all before any store
+                T old[4][4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int r = tx + 16 * i, c = ty + 16 * j;
+                        old[i][j] = (r < rb && c < cb) ? A[(int64_t)(c0 + c) * lda + r0 + r] : T(0);
+                    }
+                T acc[4][4] = {};
+                block_nt(acc, A + (int64_t)k0 * lda + r0, lda, rb, A + (int64_t)k0 * lda + c0, lda, cb, PB, Ps,
+                         Qs);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int r = tx + 16 * i, c = ty + 16 * j;
+                        if (r < rb && c < cb && (ib != jb || r >= c))
+                            A[(int64_t)(c0 + c) * lda + r0 + r] = old[i][j] - acc[i][j];
+                    }
+                __syncthreads();
             }
         }
         grid_sync(bar, G);
-        PTRACE(kb, 5);
+        PTRACE(kb, 4);
         if (*(volatile int*)abort_flag) return;
     }
 }
@@ -340,6 +394,7 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
     char* scr = static_cast<char*>(ctx->ensure_scratch(256 + dinv_bytes, 1));
     MP_CUDA(cudaMemsetAsync(scr, 0, 256, s));
     GridBar* bar = reinterpret_cast<GridBar*>(scr);
+    GridBar* bar1 = reinterpret_cast<GridBar*>(scr + 128);
     int* abort_flag = reinterpret_cast<int*>(scr + 64);
     void* dinv = scr + 256;
     // Few CTAs: the step is latency-bound (diagonal work on CTA 0 overlaps
@@ -347,12 +402,12 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
     // cheaper.  MPCR_POTRF_CTAS overrides for tuning.
     static const int cap = [] {
         const char* e = getenv("MPCR_POTRF_CTAS");
-        return e ? atoi(e) : 16;
+        return e ? atoi(e) : 24;
     }();
     int grid = nblk * (nblk + 1) / 2;
     if (grid > cap) grid = cap;
     if (grid > ctx->sm_count) grid = ctx->sm_count;
-    if (grid < 1) grid = 1;
+    if (grid < 2) grid = nblk >= 2 ? 2 : 1;  // CTA 0's diagonal path needs a partner
     int ni = static_cast<int>(n);
     ProfScope ps(ctx, MP_PROF_POTRF, s, static_cast<double>(n) * n * n / 3.0);
     if (p == MP_DOUBLE) {
@@ -373,7 +428,7 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
         }
         double* a = static_cast<double*>(A);
         double* d = static_cast<double*>(dinv);
-        void* args[] = {&a, &lda, &ni, &d, &dev_info, &info_offset, &bar, &abort_flag, &linv_diag, &ldi};
+        void* args[] = {&a, &lda, &ni, &d, &dev_info, &info_offset, &bar, &bar1, &abort_flag, &linv_diag, &ldi};
         static const bool trace = getenv("MPCR_POTRF_TRACE") != nullptr;
         if (trace) {
             const int on = 1;
@@ -384,25 +439,18 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
             long long tr[64 * 6];
             MP_CUDA(cudaMemcpyFromSymbolAsync(tr, g_trace, sizeof(tr), 0, cudaMemcpyDeviceToHost, s));
             MP_CUDA(cudaStreamSynchronize(s));
-            double acc[5] = {};
+            double acc[4] = {};
             for (int kb = 0; kb + 1 < nblk && kb < 64; ++kb)
-                for (int q = 0; q < 5; ++q) acc[q] += static_cast<double>(tr[kb * 6 + q + 1] - tr[kb * 6 + q]);
-            long long t2[64 * 6];
-            MP_CUDA(cudaMemcpyFromSymbolAsync(t2, g_trace2, sizeof(t2), 0, cudaMemcpyDeviceToHost, s));
-            MP_CUDA(cudaStreamSynchronize(s));
-            double a2[4] = {};
-            for (int kb = 1; kb < nblk && kb < 64; ++kb)
-                for (int q = 0; q < 4; ++q) a2[q] += static_cast<double>(t2[kb * 6 + q + 1] - t2[kb * 6 + q]);
-            fprintf(stderr, "  diag: load %.0f factor+invert %.0f writeL %.0f writeDinv %.0f\n", a2[0], a2[1], a2[2], a2[3]);
-            fprintf(stderr, "potrf trace (cycles, summed over %d steps): panel %.0f bar1 %.0f update %.0f diag %.0f bar2 %.0f\n",
-                    nblk - 1, acc[0], acc[1], acc[2], acc[3], acc[4]);
+                for (int q = 0; q < 4; ++q) acc[q] += static_cast<double>(tr[kb * 6 + q + 1] - tr[kb * 6 + q]);
+            fprintf(stderr, "potrf trace, CTA 0 (cycles, summed over %d steps): panel block %.0f syrk %.0f "
+                    "factor+inverse %.0f barrier %.0f\n", nblk - 1, acc[0], acc[1], acc[2], acc[3]);
         }
     } else {
         const size_t shm = (2 * PB * (PB + 1) + 2 * 16 * (PB + 1) + 3 * 256) * sizeof(float);
         float* a = static_cast<float*>(A);
         float* d = static_cast<float*>(dinv);
         float* ld_null = nullptr;
-        void* args[] = {&a, &lda, &ni, &d, &dev_info, &info_offset, &bar, &abort_flag, &ld_null, &ldi};
+        void* args[] = {&a, &lda, &ni, &d, &dev_info, &info_offset, &bar, &bar1, &abort_flag, &ld_null, &ldi};
         MP_CUDA(cudaLaunchCooperativeKernel((void*)potrf_coop_kernel<float>, grid, PT, args, shm, s));
     }
     count_launch(ctx);
