@@ -137,57 +137,202 @@ __device__ __forceinline__ void block_nt(T (&acc)[4][4], const T* P, int64_t ldp
 
 #include "potrf_block.cuh"
 
+// ---- FP64 trailing-update block on DMMA (mma.sync m16n8k8 .f64) ----
+constexpr int US = 68;  // stride of the [k][row] operand slabs: conflict-free fragment loads
+
+__device__ __forceinline__ void pcp_async16(void* smem, const void* gmem, bool valid) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void pcp_async8(void* smem, const void* gmem, bool valid) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0)
+                 : "memory");
+}
+
+// Stage rows [r0, r0 + 64) x columns [k0, k0 + 64) of column-major A into
+// U[k][row] (zero past `rows`), asynchronously.
+__device__ __forceinline__ void stage_panel(double* U, const double* A, int64_t lda, int r0, int rows, int k0,
+                                            bool vec) {
+    for (int q = threadIdx.x; q < PB * (PB / 2); q += PT) {
+        const int k = q / (PB / 2), rp = 2 * (q % (PB / 2));
+        const double* src = A + (int64_t)(k0 + k) * lda + r0 + rp;
+        double* dst = U + k * US + rp;
+        if (vec && rp + 1 < rows) {
+            pcp_async16(dst, src, true);
+        } else {
+            pcp_async8(dst, src, rp < rows);
+            pcp_async8(dst + 1, src + 1, rp + 1 < rows);
+        }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// C(r0.., c0..) -= P_i P_j^T for the 64 x 64 block (lower triangle only when
+// ib == jb), P_i / P_j the panel blocks of rows r0 / c0 in columns k0...
+// 8 warps, each a 32 x 16 tile of 2 x 2 m16n8k8 fragments.
+__device__ void update_block_dmma(double* A, int64_t lda, int n, int k0, int ib, int jb, double* Us) {
+    const int r0 = ib * PB, c0 = jb * PB, rb = min(PB, n - r0), cb = min(PB, n - c0);
+    const bool vec = (lda % 2) == 0;
+    double* Pi = Us;
+    double* Pj = Us + PB * US;
+    stage_panel(Pi, A, lda, r0, rb, k0, vec);
+    stage_panel(Pj, A, lda, c0, cb, k0, vec);
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane / 4, t = lane % 4;
+    const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+    // old values of this thread's fragment elements, loaded while the slabs land
+    double old[2][2][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int r = wm + 16 * i + g + 8 * (v >> 1), c = wn + 8 * j + 2 * t + (v & 1);
+                const bool ok = r < rb && c < cb && (ib != jb || r >= c);
+                old[i][j][v] = ok ? A[(int64_t)(c0 + c) * lda + r0 + r] : 0.0;
+            }
+    double acc[2][2][4] = {};
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < PB; ks += 8) {
+        double af[2][4], bf[2][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int v = 0; v < 4; ++v)  // a[v0 + 2 v1] = P_i[g + 8 v0][t + 4 v1]
+                af[i][v] = Pi[(ks + t + 4 * (v >> 1)) * US + wm + 16 * i + g + 8 * (v & 1)];
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v)  // b[v] = P_j[n = g][k = t + 4 v]
+                bf[j][v] = Pj[(ks + t + 4 * v) * US + wn + 8 * j + g];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+                asm volatile(
+                    "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                    "{%0,%1,%2,%3};"
+                    : "+d"(acc[i][j][0]), "+d"(acc[i][j][1]), "+d"(acc[i][j][2]), "+d"(acc[i][j][3])
+                    : "d"(af[i][0]), "d"(af[i][1]), "d"(af[i][2]), "d"(af[i][3]), "d"(bf[j][0]), "d"(bf[j][1]));
+    }
+    // c[v0 + 2 v1] at (g + 8 v1, 2 t + v0)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int r = wm + 16 * i + g + 8 * (v >> 1), c = wn + 8 * j + 2 * t + (v & 1);
+                if (r < rb && c < cb && (ib != jb || r >= c))
+                    A[(int64_t)(c0 + c) * lda + r0 + r] = old[i][j][v] - acc[i][j][v];
+            }
+    __syncthreads();  // the slabs are reused by the next block
+}
+
 // Factor the diagonal block kb held in D (lower, zeros above, identity
-// padding) and invert it (potrf_block.cuh); write L_kk to A and Dinv to
-// `dinv` (and to linv_diag).  X keeps Dinv for the CTA's next panel block.
+// padding; potrf_block.cuh): L_kk stays in D and goes to A, the inverses of
+// its 16 x 16 diagonal pieces stay in Xs and go to xd (the other CTAs' panel
+// solves read them).  Returns false (after flagging) on a failed pivot.
 template <typename T>
-__device__ void diag_factor_store(T* A, int64_t lda, int n, int kb, T* dinv, T* linv_diag, int64_t ldi,
-                                  int64_t* info, int64_t info_off, int* abort_flag, T (*D)[PB + 1],
-                                  T (*X)[PB + 1], T* Tm, int* s_fail) {
+__device__ bool diag_factor_store(T* A, int64_t lda, int n, int kb, T* xd, int64_t* info, int64_t info_off,
+                                  int* abort_flag, T (*D)[PB + 1], T* Xs, int* s_fail) {
     const int k0 = kb * PB, bb = min(PB, n - k0);
     __shared__ T s_inv[PB];  // reciprocals of the pivots
-    const int fail = factor_invert_block(D, X, Tm, s_fail, s_inv);
+    const int fail = factor_block_diag(D, Xs, s_fail, s_inv);
     if (fail >= 0 && fail < bb) {
         if (threadIdx.x == 0) {
             if (*info < 0) *info = info_off + k0 + fail;
             atomicExch(abort_flag, 1);
         }
-        return;
+        return false;
     }
     for (int idx = threadIdx.x; idx < bb * bb; idx += PT) {
         const int r = idx % bb, c = idx / bb;
         if (r >= c) A[(int64_t)(k0 + c) * lda + k0 + r] = D[r][c];
     }
-    T* Di = dinv + (int64_t)kb * PB * PB;
+    T* xk = xd + (int64_t)kb * 4 * 256;
+    for (int idx = threadIdx.x; idx < 4 * 256; idx += PT) xk[idx] = Xs[idx];
+    return true;
+}
+
+// Load L_kk (lower, zeros above) into Ls and its diagonal-piece inverses into Xs.
+template <typename T>
+__device__ void load_lkk(const T* A, int64_t lda, int n, int kb, const T* xd, T (*Ls)[PB + 1], T* Xs) {
+    const int k0 = kb * PB, bb = min(PB, n - k0);
     for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
         const int r = idx % PB, c = idx / PB;
-        const T v = (r < bb && c < bb) ? X[r][c] : T(0);
-        Di[c * PB + r] = v;
-        if (linv_diag && r < bb && c < bb) linv_diag[(int64_t)(k0 + c) * ldi + k0 + r] = v;
+        Ls[r][c] = (r < bb && c < bb) ? (r >= c ? A[(int64_t)(k0 + c) * lda + k0 + r] : T(0)) : (r == c ? T(1) : T(0));
+    }
+    const T* xk = xd + (int64_t)kb * 4 * 256;
+    for (int idx = threadIdx.x; idx < 4 * 256; idx += PT) Xs[idx] = xk[idx];
+    __syncthreads();
+}
+
+// Panel block: As = A_{ib,kb} (rows r0.., zero padded), solved in place
+// against L_kk (Ls, Xs) and written back.
+template <typename T>
+__device__ void panel_block(T* A, int64_t lda, int n, int kb, int ib, T (*As)[PB + 1], const T (*Ls)[PB + 1],
+                            const T* Xs) {
+    const int k0 = kb * PB, r0 = ib * PB, rb = min(PB, n - r0);
+    for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
+        const int r = idx % PB, c = idx / PB;
+        As[r][c] = r < rb ? A[(int64_t)(k0 + c) * lda + r0 + r] : T(0);
+    }
+    __syncthreads();
+    trsm_block(As, Ls, Xs);
+    for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
+        const int r = idx % PB, c = idx / PB;
+        if (r < rb) A[(int64_t)(k0 + c) * lda + r0 + r] = As[r][c];
     }
 }
 
+// Full inverse of L_kk (for the TRTRI leaves) into linv_diag.
+template <typename T>
+__device__ void leaf_inverse(const T* A, int64_t lda, int n, int kb, const T* xd, T* linv_diag, int64_t ldi,
+                             T (*Ls)[PB + 1], T* Xs, T (*Xf)[PB + 1], T* Tm) {
+    load_lkk(A, lda, n, kb, xd, Ls, Xs);
+    dinv_block(Ls, Xs, Xf, Tm);
+    const int k0 = kb * PB, bb = min(PB, n - k0);
+    for (int idx = threadIdx.x; idx < bb * bb; idx += PT) {
+        const int r = idx % bb, c = idx / bb;
+        linv_diag[(int64_t)(k0 + c) * ldi + k0 + r] = Xf[r][c];
+    }
+    __syncthreads();
+}
+
+// Shared memory of potrf_coop_kernel, in elements of T.
+constexpr int POTRF_SMEM_ELEMS = 2 * PB * (PB + 1) + 4 * 256 + 3 * 256 + 2 * 16 * (PB + 1);
+
 // Cooperative blocked right-looking POTRF.  Per 64-block step kb:
-//   CTA 0     panel block kb+1 = A_{kb+1,kb} Dinv_kb^T (Dinv still in shared
-//             memory), published with a non-waiting arrive at barrier 1;
-//             then A_{kb+1,kb+1} -= P P^T from shared memory and the factor +
-//             inverse of that block: the next step's diagonal work never
-//             waits for the other CTAs' panels
-//   others    panel blocks kb+2.., barrier 1, trailing update of the lower
-//             triangle except block (kb+1, kb+1)
+//   CTA 0     panel block kb+1 = A_{kb+1,kb} L_kk^-T (L_kk and its diagonal
+//             piece inverses still in shared memory), published with a
+//             non-waiting arrive at barrier 1; then A_{kb+1,kb+1} -= P P^T
+//             from shared memory and the factorization of that block: the
+//             next step's diagonal work never waits for the other CTAs
+//   others    panel blocks kb+2.. (same blocked solve), barrier 1, trailing
+//             update of the lower triangle except block (kb+1, kb+1)
 //   barrier 2 (all)
 template <typename T>
-__global__ void __launch_bounds__(PT, 1) potrf_coop_kernel(T* A, int64_t lda, int n, T* dinv,
+__global__ void __launch_bounds__(PT, 1) potrf_coop_kernel(T* A, int64_t lda, int n, T* xd,
                                                         int64_t* info, int64_t info_off,
-                                                        GridBar* bar, GridBar* bar1, int* abort_flag,
-                                                        T* linv_diag, int64_t ldi) {
+                                                        GridBar* bar, GridBar* bar1, int* abort_flag) {
     extern __shared__ __align__(16) unsigned char psm[];
-    T (*D)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(psm);
-    T (*X)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(psm + sizeof(T) * PB * (PB + 1));
-    T (*Ps)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(psm + 2 * sizeof(T) * PB * (PB + 1));
-    T (*Qs)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(psm + 2 * sizeof(T) * PB * (PB + 1) +
-                                                      sizeof(T) * 16 * (PB + 1));
-    T* Tm = reinterpret_cast<T*>(psm + 2 * sizeof(T) * PB * (PB + 1) + 2 * sizeof(T) * 16 * (PB + 1));
+    T* base = reinterpret_cast<T*>(psm);
+    T (*D)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(base);
+    T (*As)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(base + PB * (PB + 1));
+    T* Xs = base + 2 * PB * (PB + 1);
+    T* Tm = Xs + 4 * 256;
+    T (*Ps)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(Tm + 3 * 256);
+    T (*Qs)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(Tm + 3 * 256 + 16 * (PB + 1));
+    // DMMA slabs of the trailing update (double only): 2 x 64 x US elements over
+    // D, As and Xs, which the non-zero CTAs only use before barrier 1
+    double* Us = reinterpret_cast<double*>(base);
+    static_assert(2 * PB * US <= 2 * PB * (PB + 1) + 4 * 256, "update slabs exceed D + As + Xs");
+
     __shared__ int s_fail;
     const int nblk = (n + PB - 1) / PB;
     const unsigned int G = gridDim.x;  // >= 2 whenever nblk >= 2
@@ -200,7 +345,7 @@ __global__ void __launch_bounds__(PT, 1) potrf_coop_kernel(T* A, int64_t lda, in
             D[r][c] = (r < bb && c < bb) ? (r >= c ? A[(int64_t)c * lda + r] : T(0)) : (r == c ? T(1) : T(0));
         }
         __syncthreads();
-        diag_factor_store(A, lda, n, 0, dinv, linv_diag, ldi, info, info_off, abort_flag, D, X, Tm, &s_fail);
+        diag_factor_store(A, lda, n, 0, xd, info, info_off, abort_flag, D, Xs, &s_fail);
     }
     grid_sync(bar, G);
     if (*(volatile int*)abort_flag) return;
@@ -218,51 +363,21 @@ __global__ void __launch_bounds__(PT, 1) potrf_coop_kernel(T* A, int64_t lda, in
                     const int r = tx + 16 * i, c = ty + 16 * j;
                     old[i][j] = (r < rb && c < rb && r >= c) ? A[(int64_t)(r0 + c) * lda + r0 + r] : T(0);
                 }
-            for (int idx = threadIdx.x; idx < PB * PB; idx += PT) {
-                const int r = idx % PB, c = idx / PB;
-                D[r][c] = r < rb ? A[(int64_t)(k0 + c) * lda + r0 + r] : T(0);
-            }
-            __syncthreads();
-            T acc[4][4] = {};
-#pragma unroll 4
-            for (int k = 0; k < PB; ++k) {
-                T a[4], b[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) a[i] = D[tx + 16 * i][k];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) b[j] = X[ty + 16 * j][k];
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-            }
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int r = tx + 16 * i, c = ty + 16 * j;
-                    if (r < rb) A[(int64_t)(k0 + c) * lda + r0 + r] = acc[i][j];
-                }
-            __syncthreads();
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) D[tx + 16 * i][ty + 16 * j] = acc[i][j];
-            grid_arrive(bar1, G);  // also orders the D stores before the reads below
+            panel_block(A, lda, n, kb, kb + 1, As, D, Xs);
+            grid_arrive(bar1, G);  // also orders the panel in As before the reads below
             PTRACE(kb, 1);
 #pragma unroll 4
             for (int k = 0; k < PB; ++k) {
                 T a[4], b[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) a[i] = D[tx + 16 * i][k];
+                for (int i = 0; i < 4; ++i) a[i] = As[tx + 16 * i][k];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) b[j] = D[ty + 16 * j][k];
+                for (int j = 0; j < 4; ++j) b[j] = As[ty + 16 * j][k];
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) old[i][j] = fma(-a[i], b[j], old[i][j]);
+                    for (int j = 0; j <= i; ++j) old[i][j] = fma(-a[i], b[j], old[i][j]);  // lower only
             }
-            __syncthreads();
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -272,23 +387,15 @@ __global__ void __launch_bounds__(PT, 1) potrf_coop_kernel(T* A, int64_t lda, in
                 }
             __syncthreads();
             PTRACE(kb, 2);
-            diag_factor_store(A, lda, n, kb + 1, dinv, linv_diag, ldi, info, info_off, abort_flag, D, X, Tm,
-                              &s_fail);
+            diag_factor_store(A, lda, n, kb + 1, xd, info, info_off, abort_flag, D, Xs, &s_fail);
             PTRACE(kb, 3);
         } else {
-            const T* Di = dinv + (int64_t)kb * PB * PB;
-            for (int ib = kb + 1 + blockIdx.x; ib < nblk; ib += G - 1) {
-                const int r0 = ib * PB, rb = min(PB, n - r0);
-                T acc[4][4] = {};
-                block_nt(acc, A + (int64_t)k0 * lda + r0, lda, rb, Di, PB, PB, PB, Ps, Qs);
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int r = tx + 16 * i, c = ty + 16 * j;
-                        if (r < rb) A[(int64_t)(k0 + c) * lda + r0 + r] = acc[i][j];
-                    }
-                __syncthreads();
+            if (kb + 1 + (int)blockIdx.x < nblk) {
+                load_lkk(A, lda, n, kb, xd, D, Xs);
+                for (int ib = kb + 1 + blockIdx.x; ib < nblk; ib += G - 1) {
+                    panel_block(A, lda, n, kb, ib, As, D, Xs);
+                    __syncthreads();
+                }
             }
             grid_sync(bar1, G);
             const int items = rest * (rest + 1) / 2;  // item 0 is (kb+1, kb+1): CTA 0's
@@ -301,34 +408,51 @@ __global__ void __launch_bounds__(PT, 1) potrf_coop_kernel(T* A, int64_t lda, in
                 const int jb = kb + 1 + jj, ib = jb + rem;
                 const int r0 = ib * PB, c0 = jb * PB;
                 const int rb = min(PB, n - r0), cb = min(PB, n - c0);
-                // the block's old values are loaded while block_nt runs (no aliasing
-                // with its reads: different columns), all before any store
-                T old[4][4];
+                if constexpr (std::is_same<T, double>::value) {
+                    update_block_dmma(A, lda, n, k0, ib, jb, Us);
+                } else {
+                    // the block's old values are loaded while block_nt runs (no aliasing
+                    // with its reads: different columns), all before any store
+                    T old[4][4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                    for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int r = tx + 16 * i, c = ty + 16 * j;
-                        old[i][j] = (r < rb && c < cb) ? A[(int64_t)(c0 + c) * lda + r0 + r] : T(0);
-                    }
-                T acc[4][4] = {};
-                block_nt(acc, A + (int64_t)k0 * lda + r0, lda, rb, A + (int64_t)k0 * lda + c0, lda, cb, PB, Ps,
-                         Qs);
+                        for (int j = 0; j < 4; ++j) {
+                            const int r = tx + 16 * i, c = ty + 16 * j;
+                            old[i][j] = (r < rb && c < cb) ? A[(int64_t)(c0 + c) * lda + r0 + r] : T(0);
+                        }
+                    T acc[4][4] = {};
+                    block_nt(acc, A + (int64_t)k0 * lda + r0, lda, rb, A + (int64_t)k0 * lda + c0, lda, cb, PB, Ps,
+                             Qs);
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                    for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int r = tx + 16 * i, c = ty + 16 * j;
-                        if (r < rb && c < cb && (ib != jb || r >= c))
-                            A[(int64_t)(c0 + c) * lda + r0 + r] = old[i][j] - acc[i][j];
-                    }
-                __syncthreads();
+                        for (int j = 0; j < 4; ++j) {
+                            const int r = tx + 16 * i, c = ty + 16 * j;
+                            if (r < rb && c < cb && (ib != jb || r >= c))
+                                A[(int64_t)(c0 + c) * lda + r0 + r] = old[i][j] - acc[i][j];
+                        }
+                    __syncthreads();
+                }
             }
         }
         grid_sync(bar, G);
         PTRACE(kb, 4);
         if (*(volatile int*)abort_flag) return;
     }
+}
+
+// The full inverses of the diagonal blocks (TRTRI leaves), one CTA per block,
+// from L and the diagonal-piece inverses the factorization left in xd.
+__global__ void __launch_bounds__(PT, 1) leaf_inverse_kernel(const double* A, int64_t lda, int n, const double* xd,
+                                                             double* linv_diag, int64_t ldi) {
+    extern __shared__ __align__(16) unsigned char psm[];
+    double* base = reinterpret_cast<double*>(psm);
+    double (*Ls)[PB + 1] = reinterpret_cast<double (*)[PB + 1]>(base);
+    double (*Xf)[PB + 1] = reinterpret_cast<double (*)[PB + 1]>(base + PB * (PB + 1));
+    double* Xs = base + 2 * PB * (PB + 1);
+    double* Tm = Xs + 4 * 256;
+    leaf_inverse(A, lda, n, blockIdx.x, xd, linv_diag, ldi, Ls, Xs, Xf, Tm);
 }
 
 // ---- triangular solve (linalg.cpp:130-159), one thread per RHS vector ----
@@ -419,7 +543,7 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
             const char* e = getenv("MPCR_POTRF_EXCLUSIVE");
             return !(e && e[0] == '0');
         }();
-        const size_t shm_need = (2 * PB * (PB + 1) + 2 * 16 * (PB + 1) + 3 * 256) * sizeof(double);
+        const size_t shm_need = POTRF_SMEM_ELEMS * sizeof(double);
         const size_t shm = exclusive ? std::max<size_t>(shm_need, 160 * 1024) : shm_need;
         if (!cfg) {
             MP_CUDA(cudaFuncSetAttribute((void*)potrf_coop_kernel<double>,
@@ -428,13 +552,24 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
         }
         double* a = static_cast<double*>(A);
         double* d = static_cast<double*>(dinv);
-        void* args[] = {&a, &lda, &ni, &d, &dev_info, &info_offset, &bar, &bar1, &abort_flag, &linv_diag, &ldi};
+        void* args[] = {&a, &lda, &ni, &d, &dev_info, &info_offset, &bar, &bar1, &abort_flag};
         static const bool trace = getenv("MPCR_POTRF_TRACE") != nullptr;
         if (trace) {
             const int on = 1;
             MP_CUDA(cudaMemcpyToSymbolAsync(g_trace_on, &on, sizeof(on), 0, cudaMemcpyHostToDevice, s));
         }
         MP_CUDA(cudaLaunchCooperativeKernel((void*)potrf_coop_kernel<double>, grid, PT, args, shm, s));
+        if (linv_diag) {
+            static bool cfg_l = false;
+            const size_t shm_l = (2 * PB * (PB + 1) + 4 * 256 + 3 * 256) * sizeof(double);
+            if (!cfg_l) {
+                MP_CUDA(cudaFuncSetAttribute((void*)leaf_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)shm_l));
+                cfg_l = true;
+            }
+            leaf_inverse_kernel<<<nblk, PT, shm_l, s>>>(a, lda, ni, d, linv_diag, ldi);
+            count_launch(ctx);
+        }
         if (trace) {
             long long tr[64 * 6];
             MP_CUDA(cudaMemcpyFromSymbolAsync(tr, g_trace, sizeof(tr), 0, cudaMemcpyDeviceToHost, s));
@@ -446,11 +581,16 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
                     "factor+inverse %.0f barrier %.0f\n", nblk - 1, acc[0], acc[1], acc[2], acc[3]);
         }
     } else {
-        const size_t shm = (2 * PB * (PB + 1) + 2 * 16 * (PB + 1) + 3 * 256) * sizeof(float);
+        const size_t shm = POTRF_SMEM_ELEMS * sizeof(float);
+        static bool cfg_f = false;
+        if (!cfg_f) {
+            MP_CUDA(cudaFuncSetAttribute((void*)potrf_coop_kernel<float>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+            cfg_f = true;
+        }
         float* a = static_cast<float*>(A);
         float* d = static_cast<float*>(dinv);
-        float* ld_null = nullptr;
-        void* args[] = {&a, &lda, &ni, &d, &dev_info, &info_offset, &bar, &bar1, &abort_flag, &ld_null, &ldi};
+        void* args[] = {&a, &lda, &ni, &d, &dev_info, &info_offset, &bar, &bar1, &abort_flag};
         MP_CUDA(cudaLaunchCooperativeKernel((void*)potrf_coop_kernel<float>, grid, PT, args, shm, s));
     }
     count_launch(ctx);

@@ -23,16 +23,18 @@ __device__ __forceinline__ float rsqrt_nr(float x) { return rsqrtf(x); }
 
 // Warp 0: factor the 64 x 16 panel at columns c0.. (rows >= c0 already
 // updated by the columns left of it) right-looking in registers.  Lane l
-// holds rows l and l + 32; the panel entries of each column are broadcast by
-// shuffles.  The lane holding the next pivot's row updates that pivot from
-// its own L entry first, so the pivot chain per column is one shuffle, the
-// reciprocal square root and two FP64 operations.
+// holds rows l and l + 32.  Per pivot only the pivot itself is shuffled: the
+// lane holding the next pivot's row updates that pivot from its own L entry
+// first (so the chain per column is one shuffle, the reciprocal square root
+// and two FP64 operations), and the column's 16 panel entries are broadcast
+// through shared memory (cb, 2 x 16 elements) for the rank-1 update.
 // Pivot test as chol_kernel (`!(d > 0)`, linalg.cpp:121).
 template <typename T>
-__device__ __forceinline__ void panel_factor(T (*D)[PB + 1], int c0, int* s_fail, T* s_inv) {
+__device__ __forceinline__ void panel_factor(T (*D)[PB + 1], int c0, int* s_fail, T* s_inv, T (*cb)[16]) {
     const int lane = threadIdx.x & 31;
     const bool hi = c0 >= 32;  // the panel's diagonal rows sit in the second slot
     const int r0 = lane, r1 = lane + 32;
+    const int pr = (hi ? r1 : r0) - c0;  // this lane's row within the panel's diagonal piece
     T v0[16], v1[16];
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
@@ -52,12 +54,16 @@ __device__ __forceinline__ void panel_factor(T (*D)[PB + 1], int c0, int* s_fail
         v0[j] = l0;
         v1[j] = l1;
         const T src = hi ? l1 : l0;
-        if (j + 1 < 16) dnext = (hi ? v1[j + 1] : v0[j + 1]) - src * src;
+        if (j + 1 < 16) {
+            dnext = (hi ? v1[j + 1] : v0[j + 1]) - src * src;
+            if (pr > j && pr < 16) cb[j & 1][pr] = src;  // L(c0 + pr, gj)
+            __syncwarp();
 #pragma unroll
-        for (int c = j + 1; c < 16; ++c) {
-            const T lc = __shfl_sync(0xFFFFFFFFu, src, (c0 + c) & 31);  // L(c0 + c, gj)
-            v0[c] -= l0 * lc;
-            v1[c] -= l1 * lc;
+            for (int c = j + 1; c < 16; ++c) {
+                const T lc = cb[j & 1][c];
+                v0[c] -= l0 * lc;
+                v1[c] -= l1 * lc;
+            }
         }
         if (lane == 0) s_inv[gj] = inv;
     }
@@ -69,105 +75,179 @@ __device__ __forceinline__ void panel_factor(T (*D)[PB + 1], int c0, int* s_fail
     if (lane == 0 && fail >= 0 && *s_fail < 0) *s_fail = fail;
 }
 
-// All threads: left-looking update of the panel at c0 by the columns left of it,
-// D(r, c) -= sum_{t < c0} D(r, t) D(c, t) for r >= c, c in [c0, c0 + 16).
-template <typename T>
-__device__ __forceinline__ void panel_update(T (*D)[PB + 1], int c0) {
-    for (int e = threadIdx.x; e < (PB - c0) * 16; e += PT) {
-        const int r = c0 + e / 16, c = c0 + e % 16;
-        if (r < c) continue;
-        T s0 = D[r][c], s1 = T(0);
-        for (int t = 0; t < c0; t += 2) {
-            s0 -= D[r][t] * D[c][t];
-            s1 -= D[r][t + 1] * D[c][t + 1];
-        }
-        D[r][c] = s0 + s1;
+// All threads: left-looking update of the panel at C0 by the columns left of
+// it, D(r, c) -= sum_{t < C0} D(r, t) D(c, t) for r >= c, c in [C0, C0 + 16).
+// Compile-time trip counts: the loads of all of a thread's elements are in
+// flight together.
+template <typename T, int C0>
+__device__ __forceinline__ void panel_update_t(T (*D)[PB + 1]) {
+    constexpr int NE = (PB - C0) * 16 / PT;  // elements per thread
+    int r[NE], c[NE];
+    T s0[NE], s1[NE];
+#pragma unroll
+    for (int q = 0; q < NE; ++q) {
+        const int e = threadIdx.x + q * PT;
+        r[q] = C0 + e / 16;
+        c[q] = C0 + e % 16;
+        s0[q] = D[r[q]][c[q]];
+        s1[q] = T(0);
     }
+#pragma unroll
+    for (int t = 0; t < C0; t += 2) {
+#pragma unroll
+        for (int q = 0; q < NE; ++q) {
+            s0[q] -= D[r[q]][t] * D[c[q]][t];
+            s1[q] -= D[r[q]][t + 1] * D[c[q]][t + 1];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < NE; ++q)
+        if (r[q] >= c[q]) D[r[q]][c[q]] = s0[q] + s1[q];
 }
 
-// Warps 1..7: row block ib (rows 16 ib ..) of X = L^-1, once L's row block ib
-// is final and X's row blocks above it are done:
-//   X_ii = inv(L_ii)                           (warp 1, one column per lane)
-//   T_j  = sum_{t = j}^{i-1} L_it X_tj, j < i  (warps 2..7, concurrently)
-//   X_ij = -X_ii T_j
 template <typename T>
-__device__ __forceinline__ void xrow_block(const T (*D)[PB + 1], T (*X)[PB + 1], T* Tm, int ib, const T* s_inv) {
-    const int tid = threadIdx.x - 32;  // 0..223
-    const int r0 = 16 * ib;
-    if (tid < 16) {
-        // column cc of inv(L_ii), right-looking: one multiply-add per row on the chain
-        const int cc = tid;
-        T x[16];
+__device__ __forceinline__ void panel_update(T (*D)[PB + 1], int c0) {
+    if (c0 == 16) panel_update_t<T, 16>(D);
+    else if (c0 == 32) panel_update_t<T, 32>(D);
+    else if (c0 == 48) panel_update_t<T, 48>(D);
+}
+
+// Warp 1, lanes 0..15: Xd_q = inv(L_qq) for the 16 x 16 diagonal piece q
+// (one column per lane, right-looking: one multiply-add per row on the
+// chain); Xd_q(r, c) at Xd[256 q + 16 r + c], zeros above the diagonal.
+template <typename T>
+__device__ __forceinline__ void diag_inverse16(const T (*D)[PB + 1], T* Xd, int q, const T* s_inv) {
+    const int cc = threadIdx.x & 15, r0 = 16 * q;
+    T x[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) x[i] = (i == cc) ? T(1) : T(0);
+    for (int i = 0; i < 16; ++i) x[i] = (i == cc) ? T(1) : T(0);
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-            x[t] *= s_inv[r0 + t];
+    for (int t = 0; t < 16; ++t) {
+        x[t] *= s_inv[r0 + t];
 #pragma unroll
-            for (int i = t + 1; i < 16; ++i) x[i] -= D[r0 + i][r0 + t] * x[t];
-        }
-#pragma unroll
-        for (int i = 0; i < 16; ++i) X[r0 + i][r0 + cc] = x[i];
-    } else if (tid >= 32) {
-        // 2 x 2 output patches of T_j (one patch per thread for ib <= 3)
-        for (int e = tid - 32; e < ib * 64; e += PT - 64) {
-            const int j = e / 64, pr = (e % 64) % 8, pc = (e % 64) / 8;
-            const int cj = 16 * j, rr = r0 + 2 * pr, cc = cj + 2 * pc;
-            T s00 = T(0), s01 = T(0), s10 = T(0), s11 = T(0);
-            for (int t = cj; t < r0; ++t) {
-                const T a0 = D[rr][t], a1 = D[rr + 1][t];
-                const T b0 = X[t][cc], b1 = X[t][cc + 1];
-                s00 += a0 * b0;
-                s01 += a0 * b1;
-                s10 += a1 * b0;
-                s11 += a1 * b1;
-            }
-            T* tj = Tm + j * 256;  // T_j(r, c) at c * 16 + r
-            tj[(2 * pc) * 16 + 2 * pr] = s00;
-            tj[(2 * pc + 1) * 16 + 2 * pr] = s01;
-            tj[(2 * pc) * 16 + 2 * pr + 1] = s10;
-            tj[(2 * pc + 1) * 16 + 2 * pr + 1] = s11;
-        }
+        for (int i = t + 1; i < 16; ++i) x[i] -= D[r0 + i][r0 + t] * x[t];
     }
-    asm volatile("bar.sync 1, 224;" ::: "memory");
-    for (int e = tid; e < ib * 256; e += PT - 32) {
-        const int j = e / 256, r = (e % 256) % 16, c = (e % 256) / 16;
-        T s = T(0);
 #pragma unroll
-        for (int t = 0; t < 16; ++t) s += X[r0 + r][r0 + t] * Tm[j * 256 + c * 16 + t];
-        X[r0 + r][16 * j + c] = -s;
-    }
+    for (int i = 0; i < 16; ++i) Xd[256 * q + 16 * i + cc] = x[i];
 }
 
 // Factor the SPD block in D (lower triangle valid, zeros above, padding rows
-// and columns set to the identity) in place into L, and write X = L^-1 (lower,
-// zeros above).  Left-looking over four 16-column panels: warp 0 factors
-// panel i while warps 1..7 build row block i-1 of the inverse.  Returns the
-// first failing column or -1; the pivot reciprocals go to s_inv.  Tm holds
-// 3 x 256 elements.
+// and columns set to the identity) in place into L, and write the inverses
+// of its four 16 x 16 diagonal pieces to Xd.  Left-looking over 16-column
+// panels: warp 0 factors panel i while warp 1 inverts the diagonal piece of
+// panel i-1.  Returns the first failing column or -1; the pivot reciprocals
+// go to s_inv.
 template <typename T>
-__device__ int factor_invert_block(T (*D)[PB + 1], T (*X)[PB + 1], T* Tm, int* s_fail, T* s_inv) {
+__device__ int factor_block_diag(T (*D)[PB + 1], T* Xd, int* s_fail, T* s_inv) {
     const int tid = threadIdx.x, warp = tid >> 5;
-    for (int idx = tid; idx < PB * (PB + 1); idx += PT) (&X[0][0])[idx] = T(0);
+    __shared__ T cb[2][16];
     if (tid == 0) *s_fail = -1;
     __syncthreads();
 #pragma unroll 1
     for (int pi = 0; pi <= PB / 16; ++pi) {
         const int c0 = 16 * pi;
-        FB_MARK(0);
         if (pi >= 1 && pi < PB / 16) {
             panel_update(D, c0);
             __syncthreads();
         }
-        FB_MARK(1);
+        FB_MARK(0);
         if (warp == 0) {
-            if (pi < PB / 16) panel_factor(D, c0, s_fail, s_inv);
-        } else if (pi >= 1) {
-            xrow_block<T>(D, X, Tm, pi - 1, s_inv);
+            if (pi < PB / 16) panel_factor(D, c0, s_fail, s_inv, cb);
+        } else if (warp == 1 && pi >= 1 && (tid & 31) < 16) {
+            diag_inverse16<T>(D, Xd, pi - 1, s_inv);
         }
-        FB_MARK(2);
+        FB_MARK(1);
         __syncthreads();
-        FB_MARK(3);
     }
     return *s_fail;
+}
+
+// In place X = A L^-T for the 64-row block in As, blocked by the 16-column
+// pieces of L (lower, in Ls) with their inverses Xd:
+//   Y_q = A_q - sum_{p < q} X_p L_qp^T,   X_q = Y_q Xd_q^T.
+// Thread (r = tid % 64, g = tid / 64) owns columns g, g+4, g+8, g+12 of each piece.
+template <typename T>
+__device__ __forceinline__ void trsm_block(T (*As)[PB + 1], const T (*Ls)[PB + 1], const T* Xd) {
+    const int r = threadIdx.x & 63, g = threadIdx.x >> 6;
+#pragma unroll
+    for (int q = 0; q < PB / 16; ++q) {
+        const int q0 = 16 * q;
+        T y[4], z[4] = {};
+#pragma unroll
+        for (int m = 0; m < 4; ++m) y[m] = As[r][q0 + g + 4 * m];
+#pragma unroll
+        for (int t = 0; t < q0; t += 2) {
+            const T a0 = As[r][t], a1 = As[r][t + 1];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                y[m] -= a0 * Ls[q0 + g + 4 * m][t];
+                z[m] -= a1 * Ls[q0 + g + 4 * m][t + 1];
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < 4; ++m) As[r][q0 + g + 4 * m] = y[m] + z[m];
+        __syncthreads();
+        T x[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+            const T* xr = Xd + 256 * q + 16 * (g + 4 * m);  // zeros above the diagonal
+            T s0 = T(0), s1 = T(0);
+#pragma unroll
+            for (int u = 0; u < 16; u += 2) {
+                s0 += As[r][q0 + u] * xr[u];
+                s1 += As[r][q0 + u + 1] * xr[u + 1];
+            }
+            x[m] = s0 + s1;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 4; ++m) As[r][q0 + g + 4 * m] = x[m];
+        __syncthreads();
+    }
+}
+
+// X = L^-1 (64 x 64, zeros above) from L (Ls) and the diagonal-piece
+// inverses Xd, row block by row block: X_ij = -Xd_i sum_{t=j}^{i-1} L_it X_tj.
+// Tm holds 3 x 256 elements.
+template <typename T>
+__device__ void dinv_block(const T (*Ls)[PB + 1], const T* Xd, T (*X)[PB + 1], T* Tm) {
+    const int tid = threadIdx.x;
+    for (int idx = tid; idx < PB * PB; idx += PT) {
+        const int r = idx % PB, c = idx / PB;
+        X[r][c] = (r / 16 == c / 16) ? Xd[256 * (r / 16) + 16 * (r % 16) + c % 16] : T(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 1; i < PB / 16; ++i) {
+        const int r0 = 16 * i;
+        // T_j = sum_{t < r0} L(r0 + rr, t) X(t, 16 j + c): X is zero above the
+        // diagonal, so the uniform range covers t in [16 j, r0)
+#pragma unroll
+        for (int q = 0; q < i; ++q) {
+            const int e = tid + q * PT;  // 256 i elements
+            const int j = e / 256, rr = e % 16, c = (e % 256) / 16;
+            T s0 = T(0), s1 = T(0);
+#pragma unroll
+            for (int t = 0; t < r0; t += 2) {
+                s0 += Ls[r0 + rr][t] * X[t][16 * j + c];
+                s1 += Ls[r0 + rr][t + 1] * X[t + 1][16 * j + c];
+            }
+            Tm[e] = s0 + s1;  // T_j(rr, c) at 256 j + 16 c + rr
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < i; ++q) {
+            const int e = tid + q * PT;
+            const int j = e / 256, rr = e % 16, c = (e % 256) / 16;
+            const T* xr = Xd + 256 * i + 16 * rr;  // zeros above the diagonal
+            T s0 = T(0), s1 = T(0);
+#pragma unroll
+            for (int u = 0; u < 16; u += 2) {
+                s0 += xr[u] * Tm[256 * j + 16 * c + u];
+                s1 += xr[u + 1] * Tm[256 * j + 16 * c + u + 1];
+            }
+            X[r0 + rr][16 * j + c] = -(s0 + s1);
+        }
+        __syncthreads();
+    }
 }
