@@ -1,14 +1,17 @@
 #!/usr/bin/env python
 """Benchmark: MPCRTile mixed-precision tiled Cholesky TFLOP/s on B200.
 
-Default workload (BASELINE.json configs[2], the N=1 config the metric is
-quoted on): n = 65536, tile 1024, exponential (Matern nu=0.5) covariance of
-the first n points of a 256x256 unit grid, range 0.03; tile precision by band
-|i-j|: < b64 -> FP64, < b32 -> FP32, else FP16 (default b64=1, b32=2).
+Default workload (north star: "n=131072 ... on 1 B200 with >=6x strong
+scaling at 8 GPUs"; BASELINE.json configs[3]): n = 131072, tile 1024,
+exponential (Matern nu=0.5) covariance of the first n points of a 363x363
+unit grid, range 0.03; tile precision by band |i-j|: < b64 -> FP64, < b32 ->
+FP32, else FP16 (default b64=1, b32=2).  The same n at every N, so the
+driver's per-N values measure strong scaling (fixed total work).
+configs[2] (n = 65536) is `--n 65536`.
 
 A step is one full factorization chol(A) of the resident matrix (n^3/3
 flops).  Inputs are restored from a pristine device copy before every step,
-outside the CUDA-event pair; the 8.8 GB of tiles are far larger than the
+outside the CUDA-event pair; the 35 GB of tiles are far larger than the
 126 MB L2, so no flush is needed.  e2e repeats the step through the public
 C ABI from host buffers: host point coordinates -> device Matern generation
 -> chol -> logdet read back.
@@ -17,7 +20,7 @@ C ABI from host buffers: host point coordinates -> device Matern generation
     python bench.py --workload gemm --prec half --n 8192     (config 2 lines)
 
 Multi-GPU (torchrun, N > 1): BASELINE.json configs[3] — ONE n = 131072
-matrix (default; --n overrides) 2D block-cyclic over a P x Q process grid
+matrix (--n overrides) 2D block-cyclic over a P x Q process grid
 (P = largest divisor of N <= sqrt(N)), panel tiles broadcast by NCCL
 (csrc/dist.cpp); strong scaling: value = n^3/3 / (max over ranks of the
 step time).
@@ -261,7 +264,7 @@ def run_chol(args, world, rank, local):
     import paper_2406_02701_b200 as mp
 
     ctx = mp.Context(local)
-    n = args.n or (65536 if world == 1 else 131072)
+    n = args.n or 131072
     nb = args.nb
     nt = n // nb
     g = band_map(nt, args.b64, args.b32)
@@ -614,7 +617,7 @@ def main():
     ap.add_argument("--workload", default="chol", choices=["chol", "gemm", "cast", "nll", "mle"])
     ap.add_argument("--cast", default="double:half")
     ap.add_argument("--n", type=int, default=None,
-                    help="matrix order (default 65536 at N=1, 131072 at N>1)")
+                    help="matrix order (default 131072 for the chol at every N; per-workload defaults otherwise)")
     ap.add_argument("--nb", type=int, default=1024)
     ap.add_argument("--b64", type=int, default=1)
     ap.add_argument("--b32", type=int, default=2)

@@ -9,7 +9,7 @@
 // 16 warps as 4 (m) x 4 (n), warp tile 32x32 = 2 x 4 fragments of 16x8
 // (32 FP64 accumulators per thread, 4 warps per scheduler).  Launches that
 // would not fill the machine with 128x128 tiles (one SYRK tile on the
-// Cholesky critical path, the TRTRI levels) use a 64x64 / 4-warp variant,
+// Cholesky critical path, the TRTRI levels) use a 64x64 / 8-warp variant,
 // several CTAs per SM.  Shared layouts follow global
 // contiguity so every cp.async is 16 bytes; the padded strides make the
 // fragment reads conflict-free (2 wavefronts per 256-byte warp load).
@@ -25,13 +25,17 @@
 namespace mpcr {
 namespace {
 
-constexpr int BKd = 16, NST = 3;
-constexpr int SK_ = BKd + 4;  // stride (doubles) of K-contiguous slabs   [mn][k]
 template <int BT>
 struct DCfg {
-    static constexpr int BM = BT, NTHR = BT * BT / 32;  // warp tile 32x32
-    static constexpr int SM_ = BT + 8;                   // stride of MN-contiguous slabs [k][mn]
-    static constexpr int SLAB = BT * SK_ > BKd * SM_ ? BT * SK_ : BKd * SM_;  // doubles per operand stage
+    // warp tile 32 x WTN: 32x32 for the 128 tile (16 warps); 32x16 for the 64
+    // tile (8 warps).  The 64 tile serves latency-bound launches (one CTA per
+    // SM): a 32-deep K slab keeps twice the bytes in flight per stage.
+    static constexpr int WTN = BT == 64 ? 16 : 32;
+    static constexpr int BM = BT, NTHR = BT * BT / WTN;
+    static constexpr int BK = BT == 64 ? 32 : 16, NST = 3;
+    static constexpr int SK_ = BK + 4;  // stride (doubles) of K-contiguous slabs [mn][k]
+    static constexpr int SM_ = BT + 4;  // stride of MN-contiguous slabs [k][mn] (== 4 mod 16: conflict-free)
+    static constexpr int SLAB = BT * SK_ > BK * SM_ ? BT * SK_ : BK * SM_;  // doubles per operand stage
     static constexpr int SMEM = NST * 2 * SLAB * 8;
 };
 
@@ -65,10 +69,10 @@ __device__ __forceinline__ void load_slab(double* sm, const double* X, int64_t l
                                           int64_t r0, int64_t rmax, int64_t k0, int64_t kmax,
                                           bool vec) {
     using CF = DCfg<BT>;
-    constexpr int NTHR = CF::NTHR, SM_ = CF::SM_, CH = BT * BKd / 2;  // 16-byte chunks
+    constexpr int NTHR = CF::NTHR, SM_ = CF::SM_, SK_ = CF::SK_, BKd = CF::BK, CH = BT * BKd / 2;  // 16-byte chunks
     const int t = threadIdx.x;
     if (mn_contig) {
-        // 16 k-rows x BT mn
+        // BK k-rows x BT mn
 #pragma unroll
         for (int q = 0; q < CH / NTHR; ++q) {
             const int c = t + q * NTHR;
@@ -86,11 +90,11 @@ __device__ __forceinline__ void load_slab(double* sm, const double* X, int64_t l
             }
         }
     } else {
-        // BT mn rows x 16 k
+        // BT mn rows x BK k
 #pragma unroll
         for (int q = 0; q < CH / NTHR; ++q) {
             const int c = t + q * NTHR;
-            const int mm = c / 8, kk = (c % 8) * 2;
+            const int mm = c / (BKd / 2), kk = (c % (BKd / 2)) * 2;
             const int64_t gm = r0 + mm, gk = k0 + kk;
             double* dst = sm + mm * SK_ + kk;
             if (vec) {
@@ -119,7 +123,7 @@ __device__ __forceinline__ double widen(float f) { return static_cast<double>(f)
 
 template <int BT, typename TI>
 struct NarrowSlab {
-    static constexpr int NTHR = DCfg<BT>::NTHR, SM_ = DCfg<BT>::SM_;
+    static constexpr int NTHR = DCfg<BT>::NTHR, SM_ = DCfg<BT>::SM_, SK_ = DCfg<BT>::SK_, BKd = DCfg<BT>::BK;
     static constexpr int CH = BT * BKd / 4;  // 4-element chunks per slab
     static constexpr int PER = CH / NTHR;     // chunks per thread
     Stage4<TI> r[PER];
@@ -135,8 +139,8 @@ struct NarrowSlab {
                 kk = c / (BT / 4);
                 mm = (c % (BT / 4)) * 4;
             } else {
-                mm = c / 4;
-                kk = (c % 4) * 4;
+                mm = c / (BKd / 4);
+                kk = (c % (BKd / 4)) * 4;
             }
             const int64_t gm = r0 + mm, gk = k0 + kk;
             const TI* src = mn_contig ? X + gk * ldx + gm : X + gm * ldx + gk;
@@ -166,7 +170,7 @@ struct NarrowSlab {
                 dst[0] = make_double2(d[0], d[1]);
                 dst[1] = make_double2(d[2], d[3]);
             } else {
-                const int mm = c / 4, kk = (c % 4) * 4;
+                const int mm = c / (BKd / 4), kk = (c % (BKd / 4)) * 4;
                 double2* dst = reinterpret_cast<double2*>(sm + mm * SK_ + kk);
                 dst[0] = make_double2(d[0], d[1]);
                 dst[1] = make_double2(d[2], d[3]);
@@ -177,19 +181,27 @@ struct NarrowSlab {
 
 template <int BT>
 __device__ __forceinline__ double sm_get(const double* sm, bool mn_contig, int mn, int k) {
-    return mn_contig ? sm[k * DCfg<BT>::SM_ + mn] : sm[mn * SK_ + k];
+    return mn_contig ? sm[k * DCfg<BT>::SM_ + mn] : sm[mn * DCfg<BT>::SK_ + k];
 }
 
 template <int BT, typename TI>
-__global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 3 : 1) dmma_gemm_kernel(DmmaArgs g) {
+__global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 2 : 1) dmma_gemm_kernel(DmmaArgs g) {
     using CF = DCfg<BT>;
-    constexpr int BMd = BT, BNd = BT, SLAB = CF::SLAB, WN = BT / 32;
+    constexpr int BMd = BT, BNd = BT, SLAB = CF::SLAB, WTN = CF::WTN, WN = BT / WTN, NJ = WTN / 8;
+    constexpr int BKd = CF::BK, NST = CF::NST;
     extern __shared__ __align__(16) double dsm[];
     const TileProblem pr = g.problems ? g.problems[blockIdx.z]
                                       : TileProblem{g.A, g.B, g.C, g.lower_only ? 1 : 0, 0};
-    const int64_t m0 = static_cast<int64_t>(blockIdx.x) * BMd;
+    // split K: the S CTAs of a cluster (consecutive blockIdx.x) share one C
+    // tile, each takes a K range, and the partial sums meet in the leader's
+    // shared memory in rank order (deterministic)
+    const int S = g.ksplit;
+    const int rank = S > 1 ? static_cast<int>(blockIdx.x % S) : 0;
+    const int64_t m0 = static_cast<int64_t>(S > 1 ? blockIdx.x / S : blockIdx.x) * BMd;
     const int64_t n0 = static_cast<int64_t>(blockIdx.y) * BNd;
-    if (pr.lower_only && m0 + BMd - 1 < n0) return;
+    if (pr.lower_only && m0 + BMd - 1 < n0) return;  // the whole cluster leaves together
+    const int64_t kchunk = S > 1 ? ((g.k + S - 1) / S + BKd - 1) / BKd * BKd : g.k;
+    const int64_t kbeg = rank * kchunk, kend = std::min<int64_t>(g.k, kbeg + kchunk);
     constexpr bool WIDE = std::is_same<TI, double>::value;
     const TI* __restrict__ A = static_cast<const TI*>(pr.A);
     const TI* __restrict__ B = static_cast<const TI*>(pr.B);
@@ -205,17 +217,17 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 3 : 1) dmma_gemm_ke
                     (b_mn ? g.n % VE == 0 : g.k % VE == 0);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int wm = (warp / WN) * 32, wn = (warp % WN) * 32;
+    const int wm = (warp / WN) * 32, wn = (warp % WN) * WTN;
     const int gq = lane / 4, tq = lane % 4;
-    double acc[2][4][4];
+    double acc[2][NJ][4];
 #pragma unroll
     for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < NJ; ++j)
 #pragma unroll
             for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
 
-    const int nk = static_cast<int>((g.k + BKd - 1) / BKd);
+    const int nk = kend > kbeg ? static_cast<int>((kend - kbeg + BKd - 1) / BKd) : 0;
     auto stage_a = [&](int s) { return dsm + s * 2 * SLAB; };
     auto stage_b = [&](int s) { return dsm + s * 2 * SLAB + SLAB; };
     [[maybe_unused]] NarrowSlab<BT, TI> ra, rb;
@@ -223,12 +235,12 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 3 : 1) dmma_gemm_ke
         const int s = kb % NST;
         if constexpr (WIDE) {
             load_slab<BT>(stage_a(s), reinterpret_cast<const double*>(A), g.lda, a_mn, m0, g.m,
-                          static_cast<int64_t>(kb) * BKd, g.k, va);
+                          kbeg + static_cast<int64_t>(kb) * BKd, kend, va);
             load_slab<BT>(stage_b(s), reinterpret_cast<const double*>(B), g.ldb, b_mn, n0, g.n,
-                          static_cast<int64_t>(kb) * BKd, g.k, vb);
+                          kbeg + static_cast<int64_t>(kb) * BKd, kend, vb);
         } else {
-            ra.load(A, g.lda, a_mn, m0, g.m, static_cast<int64_t>(kb) * BKd, g.k, va);
-            rb.load(B, g.ldb, b_mn, n0, g.n, static_cast<int64_t>(kb) * BKd, g.k, vb);
+            ra.load(A, g.lda, a_mn, m0, g.m, kbeg + static_cast<int64_t>(kb) * BKd, kend, va);
+            rb.load(B, g.ldb, b_mn, n0, g.n, kbeg + static_cast<int64_t>(kb) * BKd, kend, vb);
         }
     };
     auto land = [&](int kb) {  // narrow path: registers -> shared (FP64)
@@ -255,7 +267,7 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 3 : 1) dmma_gemm_ke
         const double* sb = stage_b(kb % NST);
 #pragma unroll
         for (int ks = 0; ks < BKd; ks += 8) {
-            double af[2][4], bf[4][2];
+            double af[2][4], bf[NJ][2];
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
                 const int mr = wm + i * 16 + gq;
@@ -264,7 +276,7 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 3 : 1) dmma_gemm_ke
                     af[i][v] = sm_get<BT>(sa, a_mn, mr + 8 * (v & 1), ks + tq + 4 * (v >> 1));
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < NJ; ++j) {
                 const int nc = wn + j * 8 + gq;
 #pragma unroll
                 for (int v = 0; v < 2; ++v)  // b[v] = B[k = t + 4 v][n = g]
@@ -273,20 +285,51 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 3 : 1) dmma_gemm_ke
 #pragma unroll
             for (int i = 0; i < 2; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma_k8(acc[i][j], af[i], bf[j]);
+                for (int j = 0; j < NJ; ++j) dmma_k8(acc[i][j], af[i], bf[j]);
         }
         if (next) land(kb + NST - 1);
     }
     if constexpr (WIDE) cp_wait<0>();
+    if (S > 1) {
+        // every CTA's stages are free once all have left the main loop
+        asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        constexpr int E = 2 * NJ * 4;  // accumulators per thread
+        if (rank != 0) {
+            const uint32_t local = static_cast<uint32_t>(
+                __cvta_generic_to_shared(dsm + ((rank - 1) * CF::NTHR + threadIdx.x) * E));
+            uint32_t remote;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(0));
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v)
+                        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote + 8 * ((i * NJ + j) * 4 + v)),
+                                     "d"(acc[i][j][v])
+                                     : "memory");
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (rank != 0) return;
+        for (int r = 1; r < S; ++r) {
+            const double* part = dsm + ((r - 1) * CF::NTHR + threadIdx.x) * E;
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < NJ; ++j)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) acc[i][j][v] += part[(i * NJ + j) * 4 + v];
+        }
+    }
     // epilogue: c[v0 + 2 v1] at (g + 8 v1, 2 t + v0).  Per 16-row fragment
     // row i, the 16 C loads are issued before any store (a store may alias a
     // later load, so interleaving them would serialise the misses).
     const double alpha = g.alpha, beta = g.beta;
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-        double cold[4][4];
+        double cold[NJ][4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < NJ; ++j)
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 const int64_t gm = m0 + wm + i * 16 + gq + 8 * (v >> 1);
@@ -295,7 +338,7 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 3 : 1) dmma_gemm_ke
                 cold[j][v] = (ok && beta != 0.0) ? C[gn * g.ldc + gm] : 0.0;
             }
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < NJ; ++j)
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
                 const int64_t gm = m0 + wm + i * 16 + gq + 8 * (v >> 1);
@@ -319,10 +362,27 @@ void launch_bt(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count) {
                                      std::max(CF::SMEM, 160 * 1024)));
         configured = true;
     }
-    const dim3 grid(static_cast<unsigned>((g.m + BT - 1) / BT), static_cast<unsigned>((g.n + BT - 1) / BT),
-                    static_cast<unsigned>(g.problems ? count : 1));
     const int smem = g.exclusive ? std::max(CF::SMEM, 160 * 1024) : CF::SMEM;
-    dmma_gemm_kernel<BT, TI><<<grid, CF::NTHR, smem, s>>>(g);
+    const unsigned S = static_cast<unsigned>(std::max(1, g.ksplit));
+    const dim3 grid(static_cast<unsigned>((g.m + BT - 1) / BT) * S, static_cast<unsigned>((g.n + BT - 1) / BT),
+                    static_cast<unsigned>(g.problems ? count : 1));
+    if (S == 1) {
+        dmma_gemm_kernel<BT, TI><<<grid, CF::NTHR, smem, s>>>(g);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(CF::NTHR);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = S;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    MP_CUDA(cudaLaunchKernelEx(&cfg, dmma_gemm_kernel<BT, TI>, g));
 }
 
 template <typename TI>
@@ -342,12 +402,25 @@ void launch_dmma_gemm(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count
     const int64_t tm = (g.m + 127) / 128, tn = (g.n + 127) / 128;
     const int64_t ctas = nprob * (g.lower_only ? tm * (tn + 1) / 2 : tm * tn);  // lists live on the device
     const bool small = ctas < ctx->sm_count;
+    DmmaArgs h = g;
+    h.ksplit = 1;
+    if (small) {
+        // latency-bound launches (TRTRI levels): split K over a cluster while
+        // the 64x64 tiles leave most SMs idle, keeping >= 2 slabs per CTA
+        const int64_t t64m = (g.m + 63) / 64, t64n = (g.n + 63) / 64;
+        const int64_t c64 = nprob * (g.lower_only ? t64m * (t64n + 1) / 2 : t64m * t64n);
+        for (int sp = 4; sp >= 2; sp /= 2)
+            if (c64 * sp <= ctx->sm_count && g.k >= 64LL * sp) {
+                h.ksplit = sp;
+                break;
+            }
+    }
     if (g.pin == MP_HALF)
-        launch_ti<uint16_t>(ctx, s, g, count, small);
+        launch_ti<uint16_t>(ctx, s, h, count, small);
     else if (g.pin == MP_SINGLE)
-        launch_ti<float>(ctx, s, g, count, small);
+        launch_ti<float>(ctx, s, h, count, small);
     else
-        launch_ti<double>(ctx, s, g, count, small);
+        launch_ti<double>(ctx, s, h, count, small);
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());
 }

@@ -21,6 +21,7 @@ struct DmmaArgs {
     const TileProblem* problems;  // grouped launch when non-null
     mp_precision pin = MP_DOUBLE;  // operand storage precision
     bool exclusive = false;        // reserve the SM (latency-critical launches)
+    int ksplit = 1;                // K split over a thread-block cluster (set by the launcher)
 };
 
 void launch_dmma_gemm(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count);
