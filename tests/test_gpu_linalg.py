@@ -413,3 +413,40 @@ def test_chol2inv(ctx, ref, rng, p):
         Z[5, 5] = 0.0
         mp.linalg.chol2inv(mp.MPArray.from_numpy(Z, mp.Precision(p), ctx))
     assert e.value.kind == "SingularMatrix"
+
+
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+def test_gemm_double_small_split_k(ctx, rng, ta, tb):
+    """FP64 DMMA launches that leave SMs idle split K over a cluster (2 or 4
+    CTAs, DSMEM reduction in rank order): ragged shapes, both layouts,
+    deterministic run to run."""
+    import paper_2406_02701_b200 as mp
+
+    for (m, n, k) in ((512, 512, 512), (130, 70, 1000), (64, 64, 4096), (200, 190, 130), (33, 17, 257)):
+        A = rng.random((k, m) if ta else (m, k)) - 0.5
+        B = rng.random((n, k) if tb else (k, n)) - 0.5
+        C0 = rng.random((m, n))
+        want = 0.5 * C0 - (A.T if ta else A) @ (B.T if tb else B)
+        outs = []
+        for _ in range(2):
+            dc = mp.MPArray.from_numpy(C0, mp.Precision.Double, ctx)
+            mp.linalg.gemm(mp.MPArray.from_numpy(A, mp.Precision.Double, ctx),
+                           mp.MPArray.from_numpy(B, mp.Precision.Double, ctx), dc, ta, tb, -1.0, 0.5)
+            outs.append(dc.to_numpy())
+        assert rel(outs[0], want) <= gemm_tol(k, D), (m, n, k)
+        np.testing.assert_array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("n,bad", [(300, 64), (300, 127), (300, 128), (300, 130), (1000, 999), (1024, 16)])
+def test_chol_failing_pivot_positions(ctx, n, bad):
+    """NotPositiveDefinite reports the first failing column (errors.hpp:25-31)
+    wherever it falls relative to the 64-blocks and 16-column panels."""
+    import paper_2406_02701_b200 as mp
+
+    M = np.eye(n) * 4.0
+    M[bad, bad] = -1.0
+    for p in (S, D):
+        with pytest.raises(mp.MPError) as e:
+            mp.linalg.chol(mp.MPArray.from_numpy(M, mp.Precision(p), ctx))
+        assert e.value.kind == "NotPositiveDefinite" and e.value.info == bad, (p, e.value.info)
