@@ -1,6 +1,7 @@
 // Elementwise, reduction and layout kernels (array.cpp:228-429) plus the
 // small helpers the factorizations need.  All HBM-streaming, grid-stride,
 // grid sized to a multiple of the SM count.
+#include <algorithm>
 #include <cfloat>
 
 #include "device.cuh"
@@ -287,6 +288,108 @@ __device__ __forceinline__ void store_any(void* base, int p, int64_t i, double v
     else static_cast<double*>(base)[i] = v;
 }
 
+// FP16 value of var * exp(-d / range) for an FP16 tile (nu = 1/2), equal to
+// the reference's double value rounded by encode_f16: d from a branch-free
+// FP64 reciprocal square root (relative error ~2^-46), an exact double range
+// reduction t = fl + f, 2^-f on the SFU in FP32 (relative error < 2^-21
+// overall), and the result accepted only when both v (1 +- 2^-19) round to
+// the same half -- no rounding midpoint within reach of the error.  The rare
+// rest falls back to the FP64 expression.  Returns false for a fallback.
+__device__ __forceinline__ bool matern_half_fast(double dx, double dy, double c_log2, float var32,
+                                                 uint16_t* h) {
+    const double s2 = fma(dx, dx, dy * dy);
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(s2));
+    r = r * fma(-0.5 * s2 * r, r, 1.5);  // one Newton step
+    const double t = s2 * r * c_log2;      // d / range * log2(e)
+    const double fl = floor(t);
+    if (!(fl <= 60.0)) return false;       // NaN, coincident points, or tiny values: FP64 path
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-static_cast<float>(t - fl)));
+    const float v = e * __int_as_float((127 - static_cast<int>(fl)) << 23) * var32;  // exact 2^-fl
+    if (!(fabsf(v) <= 6.0e4f)) return false;
+    const uint16_t h1 = __half_as_ushort(__float2half_rn(v * (1.0f + 0x1p-19f)));
+    const uint16_t h2 = __half_as_ushort(__float2half_rn(v * (1.0f - 0x1p-19f)));
+    *h = h1;
+    return h1 == h2;
+}
+
+// All-FP16 items (nu = 1/2): 32-bit indexing, the row point's coordinates
+// loaded once per block, two tiles (i, j) and (j, i) written through a shared
+// transpose of the half values.
+template <bool GRID>
+__device__ __forceinline__ void matern_half_tiles(const MaternItem& it, int nb, const double* __restrict__ x,
+                                                  const double* __restrict__ y, int64_t side, double range,
+                                                  double var, double nugget) {
+    const int bpr = nb / 32;
+    __shared__ uint16_t sh[32][34];
+    const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+    const double den = static_cast<double>(side - 1);
+    const double c_log2 = 1.4426950408889634 / range;
+    const float var32 = static_cast<float>(var);
+    const bool var_exact = static_cast<double>(var32) == var;
+    uint16_t* lo = static_cast<uint16_t*>(it.lo);
+    uint16_t* up = static_cast<uint16_t*>(it.up);
+    auto coords = [&](int64_t p, double& cx, double& cy) {
+        if (GRID) {
+            cx = static_cast<double>(p % side) / den;
+            cy = static_cast<double>(p / side) / den;
+        } else {
+            cx = x[p];
+            cy = y[p];
+        }
+    };
+    __shared__ int nfail;
+    __shared__ uint16_t flist[32 * 32];  // elements left to the FP64 path (rare)
+    __shared__ double cxs[32], cys[32];  // the block's column points
+    for (int blk = blockIdx.x; blk < bpr * bpr; blk += gridDim.x) {
+        const int bi = blk % bpr, bj = blk / bpr;
+        const int i = bi * 32 + tx;
+        const int64_t pi = it.row0 + i, pc0 = it.col0 + bj * 32;
+        double xi, yi;
+        coords(pi, xi, yi);
+        if (threadIdx.x < 32) coords(pc0 + threadIdx.x, cxs[threadIdx.x], cys[threadIdx.x]);
+        if (threadIdx.x == 0) nfail = 0;
+        __syncthreads();  // also: the previous block's transpose reads are done
+        uint16_t* lob = lo + static_cast<int64_t>(bj * 32) * nb + bi * 32 + tx;  // + lj * nb
+        const bool diag = pi >= pc0 && pi < pc0 + 32;  // this row meets the diagonal here
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int lj = ty + 8 * q;
+            uint16_t h;
+            if (var_exact && !(diag && pi == pc0 + lj) &&
+                matern_half_fast(xi - cxs[lj], yi - cys[lj], c_log2, var32, &h)) {
+                lob[static_cast<int64_t>(lj) * nb] = h;
+                sh[lj][tx] = h;
+            } else {
+                flist[atomicAdd(&nfail, 1)] = static_cast<uint16_t>(lj * 32 + tx);
+            }
+        }
+        __syncthreads();
+        // the failures, compacted: one element per thread on the FP64 path
+        for (int f = threadIdx.x; f < nfail; f += blockDim.x) {
+            const int e = flist[f], lj = e >> 5, li = e & 31;
+            const int ii = bi * 32 + li, j = bj * 32 + lj;
+            const int64_t pii = it.row0 + ii, pj = it.col0 + j;
+            double xa, ya;
+            coords(pii, xa, ya);
+            double v = matern_value(hypot(xa - cxs[lj], ya - cys[lj]), 0.5, range, var);
+            if (!GRID && pii == pj) v += nugget;
+            const uint16_t h = d2h(v);
+            lo[static_cast<int64_t>(j) * nb + ii] = h;
+            sh[lj][li] = h;
+        }
+        if (!up) continue;
+        __syncthreads();
+        uint16_t* upb = up + static_cast<int64_t>(bi * 32) * nb + bj * 32 + tx;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int li = ty + 8 * q;
+            upb[static_cast<int64_t>(li) * nb] = sh[tx][li];
+        }
+    }
+}
+
 template <bool GRID>
 __global__ void __launch_bounds__(256) matern_tiles_kernel(const MaternItem* __restrict__ items, int64_t nb,
                                                            const double* __restrict__ x,
@@ -294,29 +397,38 @@ __global__ void __launch_bounds__(256) matern_tiles_kernel(const MaternItem* __r
                                                            double nu, double range, double var,
                                                            double nugget) {
     const MaternItem it = items[blockIdx.y];
+    if (nu == 0.5 && it.p_lo == MP_HALF && (!it.up || it.p_up == MP_HALF)) {  // uniform per CTA
+        matern_half_tiles<GRID>(it, static_cast<int>(nb), x, y, side, range, var, nugget);
+        return;
+    }
     const int64_t bpr = nb / 32;  // 32 x 32 blocks per tile row
-    const int64_t bi = blockIdx.x % bpr, bj = blockIdx.x / bpr;
     __shared__ double sv[32][33];
     const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 8 row-groups of 32 lanes
     const double den = static_cast<double>(side - 1);
+    // a CTA walks several blocks of its tile (few, long-lived CTAs: the block
+    // scheduler, not the math, bounded the one-block-per-CTA version)
+    for (int64_t blk = blockIdx.x; blk < bpr * bpr; blk += gridDim.x) {
+    const int64_t bi = blk % bpr, bj = blk / bpr;
+    if (blk != blockIdx.x) __syncthreads();  // the transpose buffers are reused
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int lj = ty + 8 * q;                    // column within the block
         const int64_t i = bi * 32 + tx, j = bj * 32 + lj;  // within the tile
         const int64_t pi = it.row0 + i, pj = it.col0 + j;
-        double v;
+        double dx, dy;
         if (GRID) {
-            const double dx = static_cast<double>(pi % side) / den - static_cast<double>(pj % side) / den;
-            const double dy = static_cast<double>(pi / side) / den - static_cast<double>(pj / side) / den;
-            v = matern_value(hypot(dx, dy), nu, range, var);
+            dx = static_cast<double>(pi % side) / den - static_cast<double>(pj % side) / den;
+            dy = static_cast<double>(pi / side) / den - static_cast<double>(pj / side) / den;
         } else {
-            v = matern_value(hypot(x[pi] - x[pj], y[pi] - y[pj]), nu, range, var);
-            if (pi == pj) v += nugget;
+            dx = x[pi] - x[pj];
+            dy = y[pi] - y[pj];
         }
+        double v = matern_value(hypot(dx, dy), nu, range, var);
+        if (!GRID && pi == pj) v += nugget;
         store_any(it.lo, it.p_lo, j * nb + i, v);
         sv[lj][tx] = v;
     }
-    if (!it.up) return;
+    if (!it.up) continue;
     __syncthreads();
     // (j, i) tile: element (row = global col pj, col = global row pi) = same value
 #pragma unroll
@@ -324,6 +436,7 @@ __global__ void __launch_bounds__(256) matern_tiles_kernel(const MaternItem* __r
         const int li = ty + 8 * q;  // becomes the column of the transposed block
         const int64_t r = bj * 32 + tx, c = bi * 32 + li;
         store_any(it.up, it.p_up, c * nb + r, sv[tx][li]);
+    }
     }
 }
 
@@ -505,7 +618,10 @@ void launch_matern_tiles(Ctx* ctx, cudaStream_t s, const void* items, int64_t co
                          double variance, double nugget) {
     if (count == 0) return;
     if (nb % 32) fail(MP_INVALID_PARAM, "matern: batched generation needs tiles of a multiple of 32");
-    const dim3 g(static_cast<unsigned>((nb / 32) * (nb / 32)), static_cast<unsigned>(count));
+    // ~64 CTAs per SM over the launch (balanced tail), each walking several blocks
+    const int64_t blocks = (nb / 32) * (nb / 32);
+    const int64_t per_item = std::max<int64_t>(1, std::min<int64_t>(blocks, (64LL * ctx->sm_count + count - 1) / count));
+    const dim3 g(static_cast<unsigned>(per_item), static_cast<unsigned>(count));
     const auto* it = static_cast<const MaternItem*>(items);
     if (x)
         matern_tiles_kernel<false><<<g, 256, 0, s>>>(it, nb, x, y, side, nu, range, variance, nugget);

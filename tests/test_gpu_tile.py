@@ -258,3 +258,23 @@ def test_tile_chol_graph_replay_bitwise(ctx):
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
     assert counts[2] == counts[3] > 0
+
+
+def test_tile_fill_matern_points_half_bit_exact(ctx, ref):
+    """fill_matern_points on FP16 tiles: the FP32 fast exponential must give
+    exactly the reference's double value rounded by encode_f16 (covariance.cpp
+    + precision.cpp:49-93), nugget on the diagonal included."""
+    import paper_2406_02701_b200 as mp
+    from oracle.oracle import round_to
+
+    rng = np.random.default_rng(11)
+    n, nb = 512, 128
+    x = rng.random(n)
+    y = rng.random(n)
+    d = np.hypot(x[:, None] - x[None], y[:, None] - y[None])
+    for rng_a, var, nug in ((0.03, 1.0, 0.0), (0.1, 2.0, 0.25), (0.5, 0.75, 0.0)):
+        g = np.zeros((n // nb, n // nb), int)  # all FP16
+        t = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+        t.fill_matern_points(x, y, 0.5, rng_a, var, nug)
+        want = var * np.exp(-d / rng_a) + nug * np.eye(n)
+        np.testing.assert_array_equal(t.to_numpy(), round_to(want, 0))
