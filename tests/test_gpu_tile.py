@@ -268,7 +268,7 @@ def test_tile_fill_matern_points_half_bit_exact(ctx, ref):
     from oracle.oracle import round_to
 
     rng = np.random.default_rng(11)
-    n, nb = 512, 128
+    n, nb = 2048, 256  # 12.6 M half values over the three parameter sets
     x = rng.random(n)
     y = rng.random(n)
     d = np.hypot(x[:, None] - x[None], y[:, None] - y[None])
