@@ -304,15 +304,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
 
 // ---- digit slicing -------------------------------------------------------------
 
+// Digits of one FP16 value: Y = x * 2^(41 - e_r) is an integer |Y| < 2^41
+// with at most 11 significant bits, so it and every remainder Y - q 2^w (at
+// most 13 significant bits) are exact FP32 values; balanced base-2^7 digits
+// q = rint(Y 2^-w), most significant first (weights 2^35 .. 2^0), |q| <= 64.
+// The rounding uses the 1.5 * 2^23 bias (FP32 adds, round-to-nearest-even),
+// and q is read from the biased value's bits: no conversion-pipe ops.
+__device__ __forceinline__ void oz_digits(uint16_t h, float scale, int8_t (&dig)[S][16], int j) {
+    constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23
+    float Y = __half2float(__ushort_as_half(h)) * scale;
+#pragma unroll
+    for (int d = 0; d < S - 1; ++d) {
+        const float w = __int_as_float((127 + 35 - 7 * d) << 23), iw = __int_as_float((127 - 35 + 7 * d) << 23);
+        const float t = fmaf(Y, iw, MAGIC);  // rint(Y 2^-w) + 1.5 * 2^23, exact
+        dig[d][j] = static_cast<int8_t>(__float_as_int(t) - 0x4B400000);
+        Y = fmaf(-(t - MAGIC), w, Y);
+    }
+    dig[S - 1][j] = static_cast<int8_t>(__float_as_int(Y + MAGIC) - 0x4B400000);  // |Y| <= 64, weight 2^0
+}
+
 // One CTA per 32-row stripe of one matrix: (1) row exponent e_r with
 // |x| < 2^e_r for the whole row (frexp of the row max; rows holding Inf/NaN
 // get ROWEXP_NONFINITE, their products become NaN), (2) the digits, one
 // 32 x 128 block at a time, each thread writing 16 consecutive digits of one
 // row per plane (16-byte stores).
-__global__ void __launch_bounds__(256) oz_slice_kernel(const OzSliceItem* items) {
-    const OzSliceItem it = items[blockIdx.y];
-    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
-    if (r0 >= it.rows) return;
+__device__ __forceinline__ void oz_slice_generic(const OzSliceItem& it, int64_t r0) {
     const uint16_t* x = static_cast<const uint16_t*>(it.x);
     __shared__ uint16_t sx[32][128 + 2];
     __shared__ uint32_t smax[8][33];
@@ -436,30 +452,10 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(const OzSliceItem* items)
         }
         __syncthreads();
         if (gr < it.rows && c0 + cg < it.kpad) {
-            // Integer digit extraction: Y = x * 2^(41 - e_r) is an integer with
-            // |Y| < 2^41 (an FP16 x = m 2^E with E >= e_r - 40 in its row), then
-            // balanced base-2^7 digits, most significant first (weights 2^35 .. 2^0).
             alignas(16) int8_t dig[S][16];
+            const float scale = zero ? 0.0f : __int_as_float((127 + 41 - er) << 23);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const uint32_t h = sx[lr][cg + j];
-                const uint32_t mag = h & 0x7fffu, ef = mag >> 10;
-                long long Y = 0;
-                if (!zero && mag != 0) {
-                    const long long m = ef ? ((mag & 0x3ffu) | 0x400u) : mag;
-                    const int shift = (ef ? static_cast<int>(ef) : 1) - 25 + 41 - er;  // in [1, 41]
-                    Y = m << shift;
-                    if (h & 0x8000u) Y = -Y;
-                }
-#pragma unroll
-                for (int d = 0; d < S - 1; ++d) {
-                    const int w = 35 - 7 * d;
-                    const long long q = (Y + (1ll << (w - 1))) >> w;  // round half up: q in [-64, 64]
-                    dig[d][j] = static_cast<int8_t>(q);
-                    Y -= q << w;
-                }
-                dig[S - 1][j] = static_cast<int8_t>(Y);  // |Y| <= 64 remains, weight 2^0
-            }
+            for (int j = 0; j < 16; ++j) oz_digits(sx[lr][cg + j], scale, dig, j);
             int8_t* out = static_cast<int8_t*>(it.out) + gr * it.kpad + c0 + cg;
 #pragma unroll
             for (int d = 0; d < S; ++d)
@@ -469,14 +465,130 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(const OzSliceItem* items)
     }
 }
 
+
+__global__ void __launch_bounds__(256) oz_slice_kernel(const OzSliceItem* items) {
+    const OzSliceItem it = items[blockIdx.y];
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
+    if (r0 >= it.rows) return;
+    oz_slice_generic(it, r0);
+}
+
+// Tiles (K <= OZ_STRIPE_K): the whole 32-row stripe is staged in shared
+// memory by one round of 16-byte loads (all in flight at once), the row
+// exponents and digit counts come from the registers on the way, and the
+// digits are cut from shared memory -- one HBM read of the operand.
+constexpr int OZ_STRIPE_K = 1024;
+__global__ void __launch_bounds__(256) oz_slice_stripe_kernel(const OzSliceItem* items) {
+    const OzSliceItem it = items[blockIdx.y];
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
+    if (r0 >= it.rows) return;
+    const uint16_t* x = static_cast<const uint16_t*>(it.x);
+    const bool vec = !it.trans && r0 + 32 <= it.rows && (it.ld % 8) == 0 &&
+                     (reinterpret_cast<uintptr_t>(x) & 15) == 0 && it.kpad <= OZ_STRIPE_K;
+    if (!vec) {
+        oz_slice_generic(it, r0);
+        return;
+    }
+    extern __shared__ __align__(16) uint16_t sxf[];  // [32][KS]
+    const int KS = static_cast<int>(it.kpad) + 8;
+    __shared__ uint32_t smax[2][32];
+    __shared__ int sexp[32];
+    if (threadIdx.x < 32) {
+        smax[0][threadIdx.x] = 0;
+        smax[1][threadIdx.x] = 31;
+    }
+    const int rg = threadIdx.x % 4;  // rows rg*8 .. rg*8+7
+    uint32_t mx[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    uint32_t mn[8] = {31, 31, 31, 31, 31, 31, 31, 31};  // min exponent field of nonzeros
+    const int cols = static_cast<int>(it.cols), kp = static_cast<int>(it.kpad);
+    for (int c0 = threadIdx.x / 4; c0 < kp; c0 += 64 * 4) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // four independent loads in flight per thread
+            const int c = c0 + 64 * u;
+            v[u] = (c < cols) ? *reinterpret_cast<const uint4*>(x + static_cast<int64_t>(c) * it.ld + r0 + rg * 8)
+                              : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int c = c0 + 64 * u;
+            if (c >= kp) break;
+            const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t lo = w[q] & 0xffffu, hi = w[q] >> 16;
+                const uint32_t ml = lo & 0x7fffu, mh = hi & 0x7fffu;
+                mx[2 * q] = max(mx[2 * q], ml);
+                mx[2 * q + 1] = max(mx[2 * q + 1], mh);
+                if (ml) mn[2 * q] = min(mn[2 * q], max(ml >> 10, 1u));
+                if (mh) mn[2 * q + 1] = min(mn[2 * q + 1], max(mh >> 10, 1u));
+                sxf[(rg * 8 + 2 * q) * KS + c] = static_cast<uint16_t>(lo);
+                sxf[(rg * 8 + 2 * q + 1) * KS + c] = static_cast<uint16_t>(hi);
+            }
+        }
+    }
+    __syncthreads();  // smax initialised
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        atomicMax(&smax[0][rg * 8 + j], mx[j]);
+        atomicMin(&smax[1][rg * 8 + j], mn[j]);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const uint32_t m = smax[0][threadIdx.x];
+        int e = 0, need = 0;
+        if (m >= 0x7c00u) {
+            e = ROWEXP_NONFINITE;
+        } else if (m != 0) {
+            frexp(h2d(static_cast<uint16_t>(m)), &e);
+            const int lsb = static_cast<int>(smax[1][threadIdx.x]) - 25;
+            need = 1 + (max(0, e - 6 - lsb) + 6) / 7;
+        }
+        sexp[threadIdx.x] = e;
+        it.rexp[r0 + threadIdx.x] = e;
+        if (it.ndig) {
+            for (int o = 16; o; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
+            if (threadIdx.x == 0) atomicMax(it.ndig, min(need, S));
+        }
+    }
+    __syncthreads();
+    const int lr = threadIdx.x / 8, cg = (threadIdx.x % 8) * 16;
+    const int er = sexp[lr];
+    const float scale = er == ROWEXP_NONFINITE ? 0.0f : __int_as_float((127 + 41 - er) << 23);
+    const uint16_t* row = sxf + lr * KS;
+    int8_t* outr = static_cast<int8_t*>(it.out) + (r0 + lr) * it.kpad;
+    for (int c0 = cg; c0 < kp; c0 += 128) {
+        alignas(16) int8_t dig[S][16];
+        alignas(16) uint16_t hv[16];
+        *reinterpret_cast<uint4*>(hv) = *reinterpret_cast<const uint4*>(row + c0);
+        *reinterpret_cast<uint4*>(hv + 8) = *reinterpret_cast<const uint4*>(row + c0 + 8);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) oz_digits(hv[j], scale, dig, j);
+#pragma unroll
+        for (int d = 0; d < S; ++d)
+            *reinterpret_cast<int4*>(outr + d * it.slice_stride + c0) = *reinterpret_cast<const int4*>(dig[d]);
+    }
+}
 }  // namespace oz
 
 void launch_oz_slices(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_t count, int64_t max_rows,
-                      int64_t /*max_cols*/) {
+                      int64_t max_cols) {
     if (count == 0) return;
     ProfScope ps(ctx, MP_PROF_CAST, s, 0.0);
-    oz::oz_slice_kernel<<<dim3(static_cast<unsigned>((max_rows + 31) / 32), static_cast<unsigned>(count)), 256,
-                          0, s>>>(items);
+    const dim3 grid(static_cast<unsigned>((max_rows + 31) / 32), static_cast<unsigned>(count));
+    if (max_cols <= oz::OZ_STRIPE_K) {
+        const int kpad = static_cast<int>((max_cols + 15) / 16 * 16);
+        const int smem = 32 * (kpad + 8) * 2;
+        static bool cfg = false;
+        if (!cfg) {
+            MP_CUDA(cudaFuncSetAttribute(oz::oz_slice_stripe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         32 * (oz::OZ_STRIPE_K + 8) * 2));
+            cfg = true;
+        }
+        oz::oz_slice_stripe_kernel<<<grid, 256, smem, s>>>(items);
+    } else {
+        oz::oz_slice_kernel<<<grid, 256, 0, s>>>(items);
+    }
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());
 }
