@@ -323,9 +323,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
 // MMA (M=256, N=256); stage "full" barriers live in the even CTA, "empty"
 // barriers in both (multicast commit); each CTA's epilogue reads its own 128
 // TMEM lanes and signals the even CTA's tmem-empty barrier.
-constexpr int STAGES2 = 6;
+// 5 operand stages and two C chunk buffers: the C loader prefetches the next
+// chunk (also the next unit's first one) while the epilogue works on the
+// current, so the read-modify-write of C stays off the MMA's path.
+constexpr int STAGES2 = 5;
 constexpr int B2_STAGE = (BN / 2) * 128;  // 16 KB
-constexpr int SMEM2_BYTES = STAGES2 * (A_STAGE + B2_STAGE) + C_CHUNK + 1024 + 256;
+constexpr int SMEM2_BYTES = STAGES2 * (A_STAGE + B2_STAGE) + 2 * C_CHUNK + 1024 + 256;
 
 template <bool A_MN, bool B_MN, typename TC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
@@ -339,14 +342,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES2 * A_STAGE;
-    TC* cbuf = reinterpret_cast<TC*>(sB + STAGES2 * B2_STAGE);
-    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(cbuf) + C_CHUNK);
+    TC* cbuf0 = reinterpret_cast<TC*>(sB + STAGES2 * B2_STAGE);  // two chunks of C_CHUNK bytes
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(cbuf0) + 2 * C_CHUNK);
     uint64_t* empty = full + STAGES2;
     uint64_t* tfull = empty + STAGES2;
     uint64_t* tempty = tfull + 2;
-    uint64_t* cfull = tempty + 2;
-    uint64_t* cempty = cfull + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 1);
+    uint64_t* cfull = tempty + 2;  // [2]
+    uint64_t* cempty = cfull + 2;  // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
+    auto cbuf_of = [&](int b) { return reinterpret_cast<TC*>(reinterpret_cast<uint8_t*>(cbuf0) + b * C_CHUNK); };
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = ptx::cluster_ctarank();
@@ -363,9 +367,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&tfull[s], 1);
             ptx::mbar_init(&tempty[s], 2);  // one arrival per CTA of the pair
+            ptx::mbar_init(&cfull[s], 1);
+            ptx::mbar_init(&cempty[s], 1);
         }
-        ptx::mbar_init(cfull, 1);
-        ptx::mbar_init(cempty, 1);
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc_2sm<TMEM_COLS>(tmem_slot);
@@ -470,20 +474,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     } else if (warp == 3) {
         // ===== C loader (both CTAs, own rows) =====
         if (lane == 0) {
-            uint32_t cphase = 0;
+            uint32_t g = 0;  // running chunk count: buffer g & 1, phase (g >> 1) & 1
             for (int64_t t = cid; t < total; t += ncl) {
                 TcProblem pr;
                 int m0, n0;
                 decode(t, pr, m0, n0);
-                for (int h = 0; h < NCHUNK; ++h) {
-                    ptx::mbar_wait(cempty, cphase ^ 1);
+                for (int h = 0; h < NCHUNK; ++h, ++g) {
+                    const int b = g & 1;
+                    ptx::mbar_wait(&cempty[b], ((g >> 1) & 1) ^ 1);
                     if (read_c) {
-                        ptx::mbar_arrive_expect_tx(cfull, C_CHUNK);
-                        ptx::tma_load_3d(cbuf, &p.map_c, cfull, m0, n0 + h * CW, pr.c_tile);
+                        ptx::mbar_arrive_expect_tx(&cfull[b], C_CHUNK);
+                        ptx::tma_load_3d(cbuf_of(b), &p.map_c, &cfull[b], m0, n0 + h * CW, pr.c_tile);
                     } else {
-                        ptx::mbar_arrive(cfull);
+                        ptx::mbar_arrive(&cfull[b]);
                     }
-                    cphase ^= 1;
                 }
             }
         }
@@ -494,7 +498,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         const bool is_leader = threadIdx.x == 128;
         const uint32_t tempty0 = ptx::mapa_shared(ptx::smem_u32(tempty), 0);
         int acc = 0;
-        uint32_t acc_phase = 0, cphase = 0;
+        uint32_t acc_phase = 0, g = 0;
         for (int64_t t = cid; t < total; t += ncl) {
             TcProblem pr;
             int m0, n0;
@@ -503,9 +507,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             ptx::tc_fence_after();
             const int row = m0 + r;
 #pragma unroll 1
-            for (int h = 0; h < NCHUNK; ++h) {
-                ptx::mbar_wait(cfull, cphase);
-                cphase ^= 1;
+            for (int h = 0; h < NCHUNK; ++h, ++g) {
+                const int b = g & 1;
+                TC* cbuf = cbuf_of(b);
+                ptx::mbar_wait(&cfull[b], (g >> 1) & 1);
 #pragma unroll 1
                 for (int c = 0; c < CW / 32; ++c) {
                     uint32_t v[32];
@@ -533,7 +538,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     ptx::tma_store_3d(&p.map_c, cbuf, m0, n0 + h * CW, pr.c_tile);
                     ptx::bulk_commit();
                     ptx::bulk_wait_read0();
-                    ptx::mbar_arrive(cempty);
+                    ptx::mbar_arrive(&cempty[b]);
                 }
             }
             // this CTA is done with accumulator `acc`: one arrival on the even CTA
