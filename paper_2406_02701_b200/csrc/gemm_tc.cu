@@ -383,12 +383,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     const int64_t total = static_cast<int64_t>(p.nprob) * tiles_per_prob;
     const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
     const bool read_c = p.beta != 0.0f;
+    // Units of a problem in groups of up to 8 M-pairs, N-blocks within a group:
+    // the ~74 pairs in flight share 8 A and ~9 B slabs per K step, so large
+    // GEMMs stream each operand from HBM a few times instead of once per
+    // tile row (the Cholesky's 4 x 4-unit tiles keep the plain M-fastest order).
+    constexpr int GROUP_M = 8;
     auto decode = [&](int64_t t, TcProblem& pr, int& m0, int& n0) {
         const int64_t pi = t / tiles_per_prob;
         const int r = static_cast<int>(t - pi * tiles_per_prob);
         pr = p.problems ? p.problems[pi] : p.single;
-        m0 = (r % mpairs) * (2 * BM) + static_cast<int>(rank) * BM;
-        n0 = (r / mpairs) * BN;
+        const int per_group = GROUP_M * p.nblocks;
+        const int g = r / per_group, rem = r - g * per_group;
+        const int gm = min(GROUP_M, mpairs - g * GROUP_M);  // the last group may be narrower
+        m0 = (g * GROUP_M + rem % gm) * (2 * BM) + static_cast<int>(rank) * BM;
+        n0 = (rem / gm) * BN;
     };
 
     if (warp == 0) {
