@@ -132,12 +132,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
     const int64_t total = static_cast<int64_t>(p.nprob) * tiles_per_prob;
     const bool read_c = p.beta != 0.0f;
 
+    // grouped rasterization as in the pair kernel: 16 M-blocks per group
+    constexpr int GROUP_M1 = 16;
     auto decode = [&](int64_t t, TcProblem& pr, int& m0, int& n0) {
         const int64_t pi = t / tiles_per_prob;
         const int r = static_cast<int>(t - pi * tiles_per_prob);
         pr = p.problems ? p.problems[pi] : p.single;
-        m0 = (r % p.mblocks) * BM;
-        n0 = (r / p.mblocks) * BN;
+        const int per_group = GROUP_M1 * p.nblocks;
+        const int g = r / per_group, rem = r - g * per_group;
+        const int gm = min(GROUP_M1, p.mblocks - g * GROUP_M1);
+        m0 = (g * GROUP_M1 + rem % gm) * BM;
+        n0 = (rem / gm) * BN;
     };
 
     if (warp == 0) {
