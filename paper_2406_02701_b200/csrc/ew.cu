@@ -351,15 +351,16 @@ __device__ __forceinline__ void matern_half_tiles(const MaternItem& it, int nb, 
         if (threadIdx.x < 32) coords(pc0 + threadIdx.x, cxs[threadIdx.x], cys[threadIdx.x]);
         if (threadIdx.x == 0) nfail = 0;
         __syncthreads();  // also: the previous block's transpose reads are done
-        uint16_t* lob = lo + static_cast<int64_t>(bj * 32) * nb + bi * 32 + tx;  // + lj * nb
-        const bool diag = pi >= pc0 && pi < pc0 + 32;  // this row meets the diagonal here
+        uint16_t* lob = lo + static_cast<int64_t>(bj * 32 + ty) * nb + bi * 32 + tx;  // column ty, row tx
+        const int64_t step = 8 * static_cast<int64_t>(nb);
+        // local column of this row's diagonal element in the block, or -1
+        const int dcol = (pi >= pc0 && pi < pc0 + 32) ? static_cast<int>(pi - pc0) : -1;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int lj = ty + 8 * q;
             uint16_t h;
-            if (var_exact && !(diag && pi == pc0 + lj) &&
-                matern_half_fast(xi - cxs[lj], yi - cys[lj], c_log2, var32, &h)) {
-                lob[static_cast<int64_t>(lj) * nb] = h;
+            if (var_exact && lj != dcol && matern_half_fast(xi - cxs[lj], yi - cys[lj], c_log2, var32, &h)) {
+                lob[q * step] = h;
                 sh[lj][tx] = h;
             } else {
                 flist[atomicAdd(&nfail, 1)] = static_cast<uint16_t>(lj * 32 + tx);
