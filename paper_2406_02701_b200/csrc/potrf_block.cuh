@@ -29,39 +29,41 @@ __device__ __forceinline__ float rsqrt_nr(float x) { return rsqrtf(x); }
 // and two FP64 operations), and the column's 16 panel entries are broadcast
 // through shared memory (cb, 2 x 16 elements) for the rank-1 update.
 // Pivot test as chol_kernel (`!(d > 0)`, linalg.cpp:121).
-template <typename T>
-__device__ __forceinline__ void panel_factor(T (*D)[PB + 1], int c0, int* s_fail, T* s_inv, T (*cb)[16]) {
+template <typename T, bool HI>
+__device__ __forceinline__ void panel_factor_t(T (*D)[PB + 1], int c0, int* s_fail, T* s_inv, T (*cb)[16]) {
+    // HI: c0 >= 32, the panel's rows all sit in the second slot (rows 32..63)
+    // and the first slot is zero -- it is skipped
     const int lane = threadIdx.x & 31;
-    const bool hi = c0 >= 32;  // the panel's diagonal rows sit in the second slot
     const int r0 = lane, r1 = lane + 32;
-    const int pr = (hi ? r1 : r0) - c0;  // this lane's row within the panel's diagonal piece
+    const int pr = (HI ? r1 : r0) - c0;  // this lane's row within the panel's diagonal piece
     T v0[16], v1[16];
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
-        v0[c] = D[r0][c0 + c];  // entries above the diagonal are zero
+        v0[c] = HI ? T(0) : D[r0][c0 + c];  // entries above the diagonal are zero
         v1[c] = D[r1][c0 + c];
     }
     int fail = -1;
-    T dnext = hi ? v1[0] : v0[0];  // this lane's candidate for the next pivot
+    T dnext = HI ? v1[0] : v0[0];  // this lane's candidate for the next pivot
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
         const int gj = c0 + j;
         const T d = __shfl_sync(0xFFFFFFFFu, dnext, gj & 31);
         const T inv = rsqrt_nr(d);
         if (!(d > T(0)) && fail < 0) fail = gj;
-        const T l0 = r0 > gj ? v0[j] * inv : (r0 == gj ? d * inv : T(0));
+        T l0 = T(0);
+        if (!HI) l0 = r0 > gj ? v0[j] * inv : (r0 == gj ? d * inv : T(0));
         const T l1 = r1 > gj ? v1[j] * inv : (r1 == gj ? d * inv : T(0));
-        v0[j] = l0;
+        if (!HI) v0[j] = l0;
         v1[j] = l1;
-        const T src = hi ? l1 : l0;
+        const T src = HI ? l1 : l0;
         if (j + 1 < 16) {
-            dnext = (hi ? v1[j + 1] : v0[j + 1]) - src * src;
+            dnext = (HI ? v1[j + 1] : v0[j + 1]) - src * src;
             if (pr > j && pr < 16) cb[j & 1][pr] = src;  // L(c0 + pr, gj)
             __syncwarp();
 #pragma unroll
             for (int c = j + 1; c < 16; ++c) {
                 const T lc = cb[j & 1][c];
-                v0[c] -= l0 * lc;
+                if (!HI) v0[c] -= l0 * lc;
                 v1[c] -= l1 * lc;
             }
         }
@@ -69,10 +71,16 @@ __device__ __forceinline__ void panel_factor(T (*D)[PB + 1], int c0, int* s_fail
     }
 #pragma unroll
     for (int c = 0; c < 16; ++c) {
-        if (r0 >= c0 + c) D[r0][c0 + c] = v0[c];
+        if (!HI && r0 >= c0 + c) D[r0][c0 + c] = v0[c];
         if (r1 >= c0 + c) D[r1][c0 + c] = v1[c];
     }
     if (lane == 0 && fail >= 0 && *s_fail < 0) *s_fail = fail;
+}
+
+template <typename T>
+__device__ __forceinline__ void panel_factor(T (*D)[PB + 1], int c0, int* s_fail, T* s_inv, T (*cb)[16]) {
+    if (c0 >= 32) panel_factor_t<T, true>(D, c0, s_fail, s_inv, cb);
+    else panel_factor_t<T, false>(D, c0, s_fail, s_inv, cb);
 }
 
 // All threads: left-looking update of the panel at C0 by the columns left of
