@@ -130,7 +130,7 @@ void ensure_panels(mp_tile_s& t) {
         MP_CUDA(cudaMalloc(&t.work, nn * (8 + 8 + 4 + 4 + 2 + 2) + 256));
     }
     if (t.events.empty()) {
-        t.events.resize(3 * t.tr + 4);
+        t.events.resize(4 * t.tr + 4);
         for (auto& e : t.events) MP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
 }
@@ -152,18 +152,21 @@ struct UpLists {
 struct StepLists {
     bool potrf = false;
     bool need_linv[3] = {false, false, false};
-    size_t trsm_tc = 0, trsm_p[3] = {0, 0, 0};
-    int64_t n_trsm_tc = 0, n_trsm_p[3] = {0, 0, 0};
+    // panel TRSM lists, [0]: tile k+1 (the head: the next diagonal SYRK and
+    // the next column's first tile need it), [1]: the rest of the column
+    size_t trsm_tc[2] = {0, 0}, trsm_p[2][3] = {};
+    int64_t n_trsm_tc[2] = {0, 0}, n_trsm_p[2][3] = {};
     size_t wb[3] = {0, 0, 0};
     int64_t n_wb[3] = {0, 0, 0};
-    // panel conversions, [0]: tiles k+1, k+2 (needed by the lookahead
-    // updates, critical path), [1]: the rest (needed by the bulk update only)
-    size_t cv[2][3][3] = {};
-    int64_t n_cv[2][3][3] = {};
-    size_t split32[2] = {0, 0};
-    int64_t n_split32[2] = {0, 0};
-    size_t digits[2] = {0, 0};  // INT8 digit slicing of FP16 panel tiles (same split)
-    int64_t n_digits[2] = {0, 0};
+    // panel conversions, [0]: copies read by the lookahead updates (tile
+    // column k+1), [1]: the rest (read by the bulk update only), [2]: the
+    // head tile's share of [0], made on the critical path right after its TRSM
+    size_t cv[3][3][3] = {};
+    int64_t n_cv[3][3][3] = {};
+    size_t split32[3] = {0, 0, 0};
+    int64_t n_split32[3] = {0, 0, 0};
+    size_t digits[3] = {0, 0, 0};  // INT8 digit slicing of FP16 panel tiles (same split)
+    int64_t n_digits[3] = {0, 0, 0};
     UpLists up[3];  // 0: tile column k+1 below the diagonal, 1: the rest, 2: tile (k+1, k+1)
     std::vector<std::pair<int, int>> bcasts;  // (i, root) panel broadcasts
 };
@@ -254,13 +257,22 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     auto rex = [&](int64_t i, int64_t k) -> int32_t* { return t.rexp + ((k & 1) * NT + i) * nb; };
     auto ndg = [&](int64_t i, int64_t k) -> int32_t* { return t.ndig + (k & 1) * NT + i; };
     struct StepAcc {
-        std::vector<TcProblem> trsm_tc;
-        std::vector<TileProblem> trsm_p[3];
-        std::vector<CopyItem> wb[3], cv[2][3][3];
-        std::vector<SplitItem> split32[2];
-        std::vector<OzSliceItem> digits[2];
+        std::vector<TcProblem> trsm_tc[2];
+        std::vector<TileProblem> trsm_p[2][3];
+        std::vector<CopyItem> wb[3], cv[3][3][3];
+        std::vector<SplitItem> split32[3];
+        std::vector<OzSliceItem> digits[3];
         UpAcc up[3];
     };
+    // Head/tail split of the panel TRSM (single GPU with lookahead): the head
+    // tile runs on the critical-path stream, the rest of the column on the
+    // lookahead stream next to the column update it feeds.  MPCR_TRSM_SPLIT=0
+    // keeps the whole column on the critical path.
+    static const bool tsplit_env = [] {
+        const char* e = getenv("MPCR_TRSM_SPLIT");
+        return !(e && e[0] == '0');
+    }();
+    const bool tsplit = tsplit_env && la && P * Q == 1;
     std::vector<StepAcc> acc(NT);
     std::vector<StepLists> steps(NT);
     const size_t nn0 = static_cast<size_t>(nb) * nb;
@@ -281,9 +293,10 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             if (t.has(m, i) && !(t.p(m, i) == MP_DOUBLE && native64(m, i, k)) &&
                 !(t.p(m, i) == MP_SINGLE && half_into_single(m, i, k)))
                 need[i == k + 1 ? 0 : 1][t.p(m, i)] = true;
+        const int h0 = (tsplit && i == k + 1) ? 2 : 0;  // the head tile's part-0 work
         for (int r = 0; r < 3; ++r) {
             if (r == q) continue;
-            const int h = need[0][r] ? 0 : need[1][r] ? 1 : -1;
+            const int h = need[0][r] ? h0 : need[1][r] ? 1 : -1;
             if (h >= 0) A.cv[h][q][r].push_back(CopyItem{pan(q, i, k), pan((mp_precision)r, i, k)});
         }
         bool need_dig[2] = {false, false};
@@ -291,11 +304,11 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             if (t.has(i, j) && t.p(i, j) == MP_DOUBLE && ozaki64(i, j, k)) need_dig[j == k + 1 ? 0 : 1] = true;
         for (int64_t m = i; m < NT; ++m)
             if (t.has(m, i) && t.p(m, i) == MP_DOUBLE && ozaki64(m, i, k)) need_dig[i == k + 1 ? 0 : 1] = true;
-        const int hd = need_dig[0] ? 0 : need_dig[1] ? 1 : -1;
+        const int hd = need_dig[0] ? h0 : need_dig[1] ? 1 : -1;
         if (hd >= 0)
             A.digits[hd].push_back(
                 OzSliceItem{pan(MP_HALF, i, k), dig(i, k), rex(i, k), ndg(i, k), nb, nb, nb, nb, tt, 0, 0});
-        const int h32 = need[0][MP_SINGLE] ? 0 : need[1][MP_SINGLE] ? 1 : -1;
+        const int h32 = need[0][MP_SINGLE] ? h0 : need[1][MP_SINGLE] ? 1 : -1;
         if (tc_ok && h32 >= 0)  // FP32 consumers run 3xTF32 on hi/lo splits
             A.split32[h32].push_back(SplitItem{pan(MP_SINGLE, i, k), spl(0, i, k), spl(1, i, k)});
     };
@@ -308,17 +321,19 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             case DA_POTRF:
                 L.potrf = true;
                 break;
-            case DA_TRSM:
+            case DA_TRSM: {
                 L.need_linv[q] = true;
+                const int hb = (tsplit && i == k + 1) ? 0 : 1;
                 if (q == MP_HALF && tc_ok)
                     // A = matrix tile (i,k) in the FP16 slab, C = panel16[i]
-                    A.trsm_tc.push_back(TcProblem{static_cast<int32_t>(t.slot[k * NT + i]), 0,
-                                                  static_cast<int32_t>(i), 0});
+                    A.trsm_tc[hb].push_back(TcProblem{static_cast<int32_t>(t.slot[k * NT + i]), 0,
+                                                      static_cast<int32_t>(i), 0});
                 else
-                    A.trsm_p[q].push_back(TileProblem{t.ptr(i, k), linv[q], pan(q, i, k), 0, 0});
+                    A.trsm_p[hb][q].push_back(TileProblem{t.ptr(i, k), linv[q], pan(q, i, k), 0, 0});
                 A.wb[q].push_back(CopyItem{pan(q, i, k), t.ptr(i, k)});
                 if (P * Q == 1) consumers(k, i, A);
                 break;
+            }
             case DA_BCAST_PANEL:
                 L.bcasts.push_back({static_cast<int>(i), a.root});
                 consumers(k, i, A);
@@ -352,20 +367,24 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     for (int64_t k = 0; k < NT; ++k) {
         StepLists& L = steps[k];
         StepAcc& A = acc[k];
-        append(buf, A.trsm_tc, L.trsm_tc);
-        L.n_trsm_tc = A.trsm_tc.size();
+        for (int hb = 0; hb < 2; ++hb) {
+            append(buf, A.trsm_tc[hb], L.trsm_tc[hb]);
+            L.n_trsm_tc[hb] = A.trsm_tc[hb].size();
+            for (int q = 0; q < 3; ++q) {
+                append(buf, A.trsm_p[hb][q], L.trsm_p[hb][q]);
+                L.n_trsm_p[hb][q] = A.trsm_p[hb][q].size();
+            }
+        }
         for (int q = 0; q < 3; ++q) {
-            append(buf, A.trsm_p[q], L.trsm_p[q]);
-            L.n_trsm_p[q] = A.trsm_p[q].size();
             append(buf, A.wb[q], L.wb[q]);
             L.n_wb[q] = A.wb[q].size();
             for (int r = 0; r < 3; ++r)
-                for (int h = 0; h < 2; ++h) {
+                for (int h = 0; h < 3; ++h) {
                     append(buf, A.cv[h][q][r], L.cv[h][q][r]);
                     L.n_cv[h][q][r] = A.cv[h][q][r].size();
                 }
         }
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < 3; ++h) {
             append(buf, A.split32[h], L.split32[h]);
             L.n_split32[h] = A.split32[h].size();
             append(buf, A.digits[h], L.digits[h]);
@@ -459,9 +478,57 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                                        reinterpret_cast<const CopyItem*>(dl + L.wb[q]), L.n_wb[q], tt);
     };
 
-    auto panel_phase = [&](int64_t k, cudaStream_t st, cudaEvent_t before_trsm) {
+    // TRSM as GEMM of one part of the column: panel_q[i] = A_ik * Linv_q^T
+    auto trsm_part = [&](int64_t k, int hb, cudaStream_t st) {
         const StepLists& L = steps[k];
-        if (L.n_digits[0] + L.n_digits[1])  // digit counts of panel k are max-reduced
+        if (L.n_trsm_tc[hb]) {
+            TcGemm g;
+            g.pc = MP_HALF;
+            g.ta = false;
+            g.tb = true;
+            g.m = g.n = g.k = nb;
+            g.alpha = 1.0;
+            g.beta = 0.0;
+            g.A = t.slab[MP_HALF];
+            g.lda = nb;
+            g.a_tiles = t.nslot[MP_HALF];
+            g.a_tile_stride = tt;
+            g.B = linvH;
+            g.B2 = linvHlo;
+            g.ldb = nb;
+            g.b_tiles = 1;
+            g.b_tile_stride = tt;
+            g.C = pan(MP_HALF, 0, k);
+            g.ldc = nb;
+            g.c_tiles = NT;
+            g.c_tile_stride = tt;
+            g.problems = reinterpret_cast<const TcProblem*>(dl + L.trsm_tc[hb]);
+            g.count = L.n_trsm_tc[hb];
+            launch_tc_gemm(c, st, g);
+        }
+        for (int q = 0; q < 3; ++q) {
+            if (!L.n_trsm_p[hb][q]) continue;
+            if (q == MP_SINGLE && tc_ok) {
+                // the few FP32 panel tiles: 3xTF32 tcgen05 GEMM per tile
+                for (const TileProblem& pr : acc[k].trsm_p[hb][q]) {
+                    GemmDesc g{MP_SINGLE, MP_SINGLE, MP_SINGLE, false, true, nb, nb, nb, 1.0, 0.0,
+                               pr.A, nb, pr.B, nb, pr.C, nb};
+                    launch_gemm(c, st, g);
+                }
+                continue;
+            }
+            GroupedGemm g{(mp_precision)q, (mp_precision)q, true, nb, nb, nb, nb, nb, nb, 1.0, 0.0,
+                          reinterpret_cast<const TileProblem*>(dl + L.trsm_p[hb][q]), L.n_trsm_p[hb][q]};
+            launch_grouped_gemm(c, st, g);
+        }
+    };
+
+    // Panel k, critical part (stream st): factor A_kk, invert, round Linv to
+    // the panel precisions, TRSM of the head tile (k+1) and its lookahead
+    // conversions.  Without the head/tail split the whole column follows here.
+    auto panel_head = [&](int64_t k, cudaStream_t st, cudaEvent_t before_trsm) {
+        const StepLists& L = steps[k];
+        if (L.n_digits[0] + L.n_digits[1] + L.n_digits[2])  // digit counts of panel k are max-reduced
             MP_CUDA(cudaMemsetAsync(ndg(0, k), 0, NT * sizeof(int32_t), st));
         const mp_precision pk = t.p(k, k);
         void* akk = t.ptr(k, k);
@@ -498,54 +565,23 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         // ~cond(L_kk) * 2^-11 and loses definiteness where the reference's
         // substitution does not.
         if (L.need_linv[MP_HALF]) {
-            if (L.n_trsm_tc)
+            if (L.n_trsm_tc[0] + L.n_trsm_tc[1])
                 launch_split_f16(c, st, linv64, linvH, linvHlo, static_cast<int64_t>(nn));
             else
                 launch_convert(c, st, MP_DOUBLE, linv64, nb, MP_HALF, linvH, nb, nb, nb);
         }
         if (L.need_linv[MP_SINGLE]) launch_convert(c, st, MP_DOUBLE, linv64, nb, MP_SINGLE, linvS, nb, nb, nb);
-        // TRSM as GEMM: panel_q[i] = A_ik * Linv_q^T (tile column k complete)
+        // the tile column has its update from step k-1
         if (before_trsm) MP_CUDA(cudaStreamWaitEvent(st, before_trsm, 0));
-        if (L.n_trsm_tc) {
-            TcGemm g;
-            g.pc = MP_HALF;
-            g.ta = false;
-            g.tb = true;
-            g.m = g.n = g.k = nb;
-            g.alpha = 1.0;
-            g.beta = 0.0;
-            g.A = t.slab[MP_HALF];
-            g.lda = nb;
-            g.a_tiles = t.nslot[MP_HALF];
-            g.a_tile_stride = tt;
-            g.B = linvH;
-            g.B2 = linvHlo;
-            g.ldb = nb;
-            g.b_tiles = 1;
-            g.b_tile_stride = tt;
-            g.C = pan(MP_HALF, 0, k);
-            g.ldc = nb;
-            g.c_tiles = NT;
-            g.c_tile_stride = tt;
-            g.problems = reinterpret_cast<const TcProblem*>(dl + L.trsm_tc);
-            g.count = L.n_trsm_tc;
-            launch_tc_gemm(c, st, g);
-        }
-        for (int q = 0; q < 3; ++q) {
-            if (!L.n_trsm_p[q]) continue;
-            if (q == MP_SINGLE && tc_ok) {
-                // the few FP32 panel tiles: 3xTF32 tcgen05 GEMM per tile
-                for (const TileProblem& pr : acc[k].trsm_p[q]) {
-                    GemmDesc g{MP_SINGLE, MP_SINGLE, MP_SINGLE, false, true, nb, nb, nb, 1.0, 0.0,
-                               pr.A, nb, pr.B, nb, pr.C, nb};
-                    launch_gemm(c, st, g);
-                }
-                continue;
-            }
-            GroupedGemm g{(mp_precision)q, (mp_precision)q, true, nb, nb, nb, nb, nb, nb, 1.0, 0.0,
-                          reinterpret_cast<const TileProblem*>(dl + L.trsm_p[q]), L.n_trsm_p[q]};
-            launch_grouped_gemm(c, st, g);
-        }
+        trsm_part(k, 0, st);
+        convert_panel(k, 2, st);
+    };
+    // Panel k, the rest of the column (stream st): TRSM, broadcasts, lookahead
+    // conversions.
+    auto panel_tail = [&](int64_t k, cudaStream_t st) {
+        if (k + 1 == NT) return;
+        const StepLists& L = steps[k];
+        trsm_part(k, 1, st);
         // distributed: every panel tile travels from its owner to all ranks
         if (!L.bcasts.empty()) {
             dist_group_start(t.dist);
@@ -666,11 +702,13 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         // ---- issue.  Per step k, three streams:
         //   s   : wait panel k; bulk conversions of panel k; update of everything
         //         but tile column k+1 (bulk); write tile column k back
-        //   sl2 : wait panel k and bulk k-1; update of column k+1 below the diagonal
+        //   sl2 : wait panel k and bulk k-1; update of column k+1 below the diagonal;
+        //         then (head/tail split) wait the head of panel k+1, TRSM and
+        //         conversions of the rest of tile column k+1
         //   sl  : wait bulk k-1; SYRK of A_{k+1,k+1}; POTRF + TRTRI of panel k+1;
-        //         wait sl2; TRSM + conversions of panel k+1
-        //   The chain POTRF -> TRSM -> SYRK -> POTRF is the critical path; the
-        //   bulk GEMMs hand SMs back every few tiles so it is never starved.
+        //         wait sl2; TRSM + conversions of the head tile (k+2, k+1)
+        //   The chain POTRF -> TRSM(head) -> SYRK -> POTRF is the critical path;
+        //   the bulk GEMMs hand SMs back every few tiles so it is never starved.
         static const int tpc_env = [] {
             const char* e = getenv("MPCR_TILES_PER_CTA");
             return e ? atoi(e) : 24;
@@ -681,6 +719,20 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         cudaEvent_t* ev_rest = t.events.data() + NT;      // NT
         cudaEvent_t* ev_next = t.events.data() + 2 * NT;  // NT
         cudaEvent_t ev_join = t.events[3 * NT + 1], ev_join2 = t.events[3 * NT + 2];
+        cudaEvent_t* ev_head = t.events.data() + 3 * NT + 4;  // NT
+        // panel k: head on the critical-path stream, tail on the lookahead stream
+        auto panel_phase = [&](int64_t k, cudaEvent_t before_trsm) {
+            panel_head(k, sl, before_trsm);
+            if (tsplit) {
+                MP_CUDA(cudaEventRecord(ev_head[k], sl));
+                MP_CUDA(cudaStreamWaitEvent(sl2, ev_head[k], 0));
+                panel_tail(k, sl2);
+                MP_CUDA(cudaEventRecord(ev_panel[k], sl2));
+            } else {
+                panel_tail(k, sl);
+                if (la) MP_CUDA(cudaEventRecord(ev_panel[k], sl));
+            }
+        };
         if (la) {
             MP_CUDA(cudaEventRecord(ev_join, s));
             MP_CUDA(cudaStreamWaitEvent(sl, ev_join, 0));
@@ -689,8 +741,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         static const bool dbg_host = getenv("MPCR_DEBUG_HOST") != nullptr;
         const auto th0 = std::chrono::steady_clock::now();
         std::vector<double> th;
-        panel_phase(0, sl, nullptr);
-        if (la) MP_CUDA(cudaEventRecord(ev_panel[0], sl));
+        panel_phase(0, nullptr);
         for (int64_t k = 0; k < NT; ++k) {
             if (la) MP_CUDA(cudaStreamWaitEvent(s, ev_panel[k], 0));
             convert_panel(k, 1, s);
@@ -706,8 +757,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 if (la) MP_CUDA(cudaEventRecord(ev_next[k], sl2));
                 if (la && k >= 1) MP_CUDA(cudaStreamWaitEvent(sl, ev_rest[k - 1], 0));
                 update_phase(k, 2, sl, 0);
-                panel_phase(k + 1, sl, la ? ev_next[k] : nullptr);
-                if (la) MP_CUDA(cudaEventRecord(ev_panel[k + 1], sl));
+                panel_phase(k + 1, la ? ev_next[k] : nullptr);
             }
             if (dbg_host)
                 th.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count());
