@@ -166,19 +166,25 @@ __device__ __forceinline__ void stage_panel(double* U, const double* A, int64_t 
             pcp_async8(dst + 1, src + 1, rp + 1 < rows);
         }
     }
+}
+
+// Stage the two panel blocks of trailing-update block (ib, jb) into U (two
+// [k][row] slabs), asynchronously (one cp.async group).
+__device__ __forceinline__ void stage_item(const double* A, int64_t lda, int n, int k0, int ib, int jb, double* U) {
+    const bool vec = (lda % 2) == 0;
+    stage_panel(U, A, lda, ib * PB, min(PB, n - ib * PB), k0, vec);
+    stage_panel(U + PB * US, A, lda, jb * PB, min(PB, n - jb * PB), k0, vec);
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 // C(r0.., c0..) -= P_i P_j^T for the 64 x 64 block (lower triangle only when
-// ib == jb), P_i / P_j the panel blocks of rows r0 / c0 in columns k0...
-// 8 warps, each a 32 x 16 tile of 2 x 2 m16n8k8 fragments.
-__device__ void update_block_dmma(double* A, int64_t lda, int n, int k0, int ib, int jb, double* Us) {
+// ib == jb) from the slabs in U (staged by stage_item; `more`: one later
+// group is still in flight).  8 warps, each a 32 x 16 tile of 2 x 2
+// m16n8k8 fragments.
+__device__ void update_block_dmma(double* A, int64_t lda, int n, int ib, int jb, const double* U, bool more) {
     const int r0 = ib * PB, c0 = jb * PB, rb = min(PB, n - r0), cb = min(PB, n - c0);
-    const bool vec = (lda % 2) == 0;
-    double* Pi = Us;
-    double* Pj = Us + PB * US;
-    stage_panel(Pi, A, lda, r0, rb, k0, vec);
-    stage_panel(Pj, A, lda, c0, cb, k0, vec);
+    const double* Pi = U;
+    const double* Pj = U + PB * US;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, g = lane / 4, t = lane % 4;
     const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
     // old values of this thread's fragment elements, loaded while the slabs land
@@ -194,7 +200,10 @@ __device__ void update_block_dmma(double* A, int64_t lda, int n, int k0, int ib,
                 old[i][j][v] = ok ? A[(int64_t)(c0 + c) * lda + r0 + r] : 0.0;
             }
     double acc[2][2][4] = {};
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (more)
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
 #pragma unroll
     for (int ks = 0; ks < PB; ks += 8) {
@@ -230,7 +239,7 @@ __device__ void update_block_dmma(double* A, int64_t lda, int n, int k0, int ib,
                 if (r < rb && c < cb && (ib != jb || r >= c))
                     A[(int64_t)(c0 + c) * lda + r0 + r] = old[i][j][v] - acc[i][j][v];
             }
-    __syncthreads();  // the slabs are reused by the next block
+    __syncthreads();  // this buffer is restaged two blocks later
 }
 
 // Factor the diagonal block kb held in D (lower, zeros above, identity
@@ -306,6 +315,7 @@ __device__ void leaf_inverse(const T* A, int64_t lda, int n, int kb, const T* xd
 
 // Shared memory of potrf_coop_kernel, in elements of T.
 constexpr int POTRF_SMEM_ELEMS = 2 * PB * (PB + 1) + 4 * 256 + 3 * 256 + 2 * 16 * (PB + 1);
+constexpr int POTRF_UPD_ELEMS = 4 * PB * US;  // double-buffered DMMA update slabs (double only)
 
 // Cooperative blocked right-looking POTRF.  Per 64-block step kb:
 //   CTA 0     panel block kb+1 = A_{kb+1,kb} L_kk^-T (L_kk and its diagonal
@@ -328,10 +338,10 @@ __global__ void __launch_bounds__(PT, 1) potrf_coop_kernel(T* A, int64_t lda, in
     T* Tm = Xs + 4 * 256;
     T (*Ps)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(Tm + 3 * 256);
     T (*Qs)[PB + 1] = reinterpret_cast<T (*)[PB + 1]>(Tm + 3 * 256 + 16 * (PB + 1));
-    // DMMA slabs of the trailing update (double only): 2 x 64 x US elements over
-    // D, As and Xs, which the non-zero CTAs only use before barrier 1
+    // DMMA slabs of the trailing update (double only): two blocks' worth (2 x 2
+    // x 64 x US elements) over the whole shared area, which the non-zero CTAs
+    // only use for their panel solves before barrier 1
     double* Us = reinterpret_cast<double*>(base);
-    static_assert(2 * PB * US <= 2 * PB * (PB + 1) + 4 * 256, "update slabs exceed D + As + Xs");
 
     __shared__ int s_fail;
     const int nblk = (n + PB - 1) / PB;
@@ -399,18 +409,42 @@ __global__ void __launch_bounds__(PT, 1) potrf_coop_kernel(T* A, int64_t lda, in
             }
             grid_sync(bar1, G);
             const int items = rest * (rest + 1) / 2;  // item 0 is (kb+1, kb+1): CTA 0's
-            for (int it = blockIdx.x; it < items; it += G - 1) {
+            auto item_blocks = [&](int it, int& ib, int& jb) {
                 int jj = 0, rem = it;
                 while (rem >= rest - jj) {
                     rem -= rest - jj;
                     ++jj;
                 }
-                const int jb = kb + 1 + jj, ib = jb + rem;
+                jb = kb + 1 + jj;
+                ib = jb + rem;
+            };
+            if constexpr (std::is_same<T, double>::value) {
+                // DMMA blocks, the next block's slabs staged while this one runs
+                int q = 0;
+                if (static_cast<int>(blockIdx.x) < items) {
+                    int ib, jb;
+                    item_blocks(blockIdx.x, ib, jb);
+                    stage_item(A, lda, n, k0, ib, jb, Us);
+                }
+                for (int it = blockIdx.x; it < items; it += G - 1, ++q) {
+                    const int nx = it + G - 1;
+                    const bool more = nx < items;
+                    if (more) {
+                        int ib2, jb2;
+                        item_blocks(nx, ib2, jb2);
+                        stage_item(A, lda, n, k0, ib2, jb2, Us + ((q + 1) & 1) * 2 * PB * US);
+                    }
+                    int ib, jb;
+                    item_blocks(it, ib, jb);
+                    update_block_dmma(A, lda, n, ib, jb, Us + (q & 1) * 2 * PB * US, more);
+                }
+            }
+            for (int it = blockIdx.x; !std::is_same<T, double>::value && it < items; it += G - 1) {
+                int ib, jb;
+                item_blocks(it, ib, jb);
                 const int r0 = ib * PB, c0 = jb * PB;
                 const int rb = min(PB, n - r0), cb = min(PB, n - c0);
-                if constexpr (std::is_same<T, double>::value) {
-                    update_block_dmma(A, lda, n, k0, ib, jb, Us);
-                } else {
+                {
                     // the block's old values are loaded while block_nt runs (no aliasing
                     // with its reads: different columns), all before any store
                     T old[4][4];
@@ -543,7 +577,7 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
             const char* e = getenv("MPCR_POTRF_EXCLUSIVE");
             return !(e && e[0] == '0');
         }();
-        const size_t shm_need = POTRF_SMEM_ELEMS * sizeof(double);
+        const size_t shm_need = std::max(POTRF_SMEM_ELEMS, POTRF_UPD_ELEMS) * sizeof(double);
         const size_t shm = exclusive ? std::max<size_t>(shm_need, 160 * 1024) : shm_need;
         if (!cfg) {
             MP_CUDA(cudaFuncSetAttribute((void*)potrf_coop_kernel<double>,
