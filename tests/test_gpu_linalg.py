@@ -450,3 +450,21 @@ def test_chol_failing_pivot_positions(ctx, n, bad):
         with pytest.raises(mp.MPError) as e:
             mp.linalg.chol(mp.MPArray.from_numpy(M, mp.Precision(p), ctx))
         assert e.value.kind == "NotPositiveDefinite" and e.value.info == bad, (p, e.value.info)
+
+
+@pytest.mark.parametrize("prec", [H, S])
+def test_gemm_grouped_rasterization_ragged(ctx, rng, prec):
+    """Tile grids with more M-blocks than one rasterization group and a
+    narrower last group (FP16 pair kernel: 8 pairs of 256 rows; 3xTF32
+    single-CTA kernel: 16 blocks of 128 rows), ragged N and K."""
+    import paper_2406_02701_b200 as mp
+    from oracle.oracle import round_to
+
+    m, n, k = 4500, 700, 520
+    A = round_to(rng.random((m, k)) - 0.5, prec)
+    B = round_to(rng.random((n, k)) - 0.5, prec)
+    da = mp.MPArray.from_numpy(A, mp.Precision(prec), ctx)
+    db = mp.MPArray.from_numpy(B, mp.Precision(prec), ctx)
+    dc = mp.MPArray.zeros_matrix(m, n, mp.Precision.Single, ctx)
+    mp.linalg.gemm(da, db, dc, False, True, 1.0, 0.0)
+    assert rel(dc.to_numpy(), A @ B.T) < 4 * k * 2.0 ** -24
