@@ -24,25 +24,31 @@ template <> __device__ __forceinline__ uint16_t cv<double, uint16_t>(double x) {
 template <> __device__ __forceinline__ float cv<double, float>(double x) { return d2f(x); }
 template <> __device__ __forceinline__ double cv<double, double>(double x) { return x; }
 
+// Eight elements per thread and step through 16-byte vector loads and
+// stores when both tiles are 16-byte aligned (the scheduler's panel and
+// matrix tiles always are); scalar tail / fallback otherwise.
+template <typename T>
+struct alignas(16) Vec8 {
+    T v[8];
+};
+
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(256) batched_convert_kernel(const CopyItem* __restrict__ items,
                                                               int64_t n) {
     const CopyItem it = items[blockIdx.y];
     const TI* __restrict__ src = static_cast<const TI*>(it.src);
     TO* __restrict__ dst = static_cast<TO*>(it.dst);
-    const int64_t n4 = n / 4;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n4;
+    const bool vec = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+    const int64_t n8 = vec ? n / 8 : 0;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n8;
          t += (int64_t)gridDim.x * blockDim.x) {
-        TI a[4];
-        TO b[4];
+        const Vec8<TI> a = reinterpret_cast<const Vec8<TI>*>(src)[t];
+        Vec8<TO> b;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) a[k] = src[t * 4 + k];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) b[k] = cv<TI, TO>(a[k]);
-#pragma unroll
-        for (int k = 0; k < 4; ++k) dst[t * 4 + k] = b[k];
+        for (int k = 0; k < 8; ++k) b.v[k] = cv<TI, TO>(a.v[k]);
+        reinterpret_cast<Vec8<TO>*>(dst)[t] = b;
     }
-    for (int64_t t = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+    for (int64_t t = n8 * 8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
          t += (int64_t)gridDim.x * blockDim.x)
         dst[t] = cv<TI, TO>(src[t]);
 }
@@ -206,8 +212,8 @@ void launch_split_f16(Ctx* ctx, cudaStream_t s, const double* x, uint16_t* hi, u
 void launch_batched_convert(Ctx* ctx, cudaStream_t s, mp_precision pin, mp_precision pout,
                             const CopyItem* dev_items, int64_t count, int64_t elems) {
     if (count == 0 || elems == 0) return;
-    int gx = static_cast<int>((elems / 4 + 255) / 256);
-    const int cap = static_cast<int>(4 * ctx->sm_count / (count < 1 ? 1 : count)) + 1;
+    int gx = static_cast<int>((elems / 8 + 255) / 256);
+    const int cap = static_cast<int>(8 * ctx->sm_count / (count < 1 ? 1 : count)) + 1;
     if (gx > cap) gx = cap;
     if (gx < 1) gx = 1;
     const dim3 grid(gx, static_cast<unsigned>(count));
