@@ -44,9 +44,12 @@ namespace mpcr {
 namespace oz {
 
 constexpr int S = OZ_SLICES;  // digits per value
-constexpr int BM = 128, BN = 128, BK = 128, STAGES = 6;
+// A stage holds one A digit plane k-block and up to two B planes: the groups
+// are issued in pairs (g, g-1), whose pairs (p, g-p) and (p, g-1-p) share A_p,
+// so each A k-block feeds two MMAs (a quarter less operand ingress).
+constexpr int BM = 128, BN = 128, BK = 128, STAGES = 4;
 constexpr int A_STAGE = BM * BK, B_STAGE = BN * BK;  // 16 KB each
-constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) + 1024 + 256;  // + barriers
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + 2 * B_STAGE) + 1024 + 256;  // + barriers
 constexpr int NACC = 4;          // int32 accumulators in flight (MMA runs NACC groups ahead)
 constexpr int TMEM_COLS = 512;  // NACC x 128 columns
 constexpr int NTHREADS = 320;   // 10 warps
@@ -106,8 +109,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
     // array itself, so the compiler keeps shared-space addressing (LDS/STS)
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
-    uint8_t* sB = smem + STAGES * A_STAGE;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_STAGE);
+    uint8_t* sB = smem + STAGES * A_STAGE;  // [STAGES][2][B_STAGE]
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * 2 * B_STAGE);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + NACC;
@@ -155,21 +158,31 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                 if (skip_tile(pr, m0, n0)) continue;
                 int sa, sb;
                 digits_of(p, pr, sa, sb);
-                for (int g = sa + sb; g >= 2; --g)
-                    for (int dp = max(1, g - sb); dp <= min(sa, g - 1); ++dp) {
-                        const int dq = g - dp;
-                        const int za = pr.a_tile * S + dp - 1, zb = pr.b_tile * S + dq - 1;
+                for (int g = sa + sb; g >= 2; g -= 2) {
+                    const bool two = g - 1 >= 2;  // group g-1 rides along
+                    const int lo = max(1, (two ? g - 1 : g) - sb), hi = min(sa, g - 1);
+                    for (int dp = lo; dp <= hi; ++dp) {
+                        const bool v1 = dp >= max(1, g - sb);                 // pair (dp, g - dp)
+                        const bool v2 = two && dp <= min(sa, g - 2);          // pair (dp, g - 1 - dp)
+                        const int za = pr.a_tile * S + dp - 1;
                         for (int kb = 0; kb < p.kblocks; ++kb) {
                             ptx::mbar_wait(&empty[stage], phase ^ 1);
-                            ptx::mbar_arrive_expect_tx(&full[stage], A_STAGE + B_STAGE);
+                            ptx::mbar_arrive_expect_tx(&full[stage],
+                                                       A_STAGE + (v1 ? B_STAGE : 0) + (v2 ? B_STAGE : 0));
                             ptx::tma_load_3d(sA + stage * A_STAGE, &p.map_a, &full[stage], kb * BK, m0, za);
-                            ptx::tma_load_3d(sB + stage * B_STAGE, &p.map_b, &full[stage], kb * BK, n0, zb);
+                            if (v1)
+                                ptx::tma_load_3d(sB + (stage * 2) * B_STAGE, &p.map_b, &full[stage], kb * BK, n0,
+                                                 pr.b_tile * S + (g - dp) - 1);
+                            if (v2)
+                                ptx::tma_load_3d(sB + (stage * 2 + 1) * B_STAGE, &p.map_b, &full[stage], kb * BK,
+                                                 n0, pr.b_tile * S + (g - 1 - dp) - 1);
                             if (++stage == STAGES) {
                                 stage = 0;
                                 phase ^= 1;
                             }
                         }
                     }
+                }
             }
         }
     } else if (warp == 1) {
@@ -187,34 +200,57 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                 if (skip_tile(pr, m0, n0)) continue;
                 int sa, sb;
                 digits_of(p, pr, sa, sb);
-                for (int g = sa + sb; g >= 2; --g) {
+                for (int g = sa + sb; g >= 2; g -= 2) {
+                    const bool two = g - 1 >= 2;
+                    // accumulators of groups g and g-1 (the next one in the rotation)
+                    const int acc2 = acc + 1 == NACC ? 0 : acc + 1;
+                    const uint32_t ph2 = acc + 1 == NACC ? acc_phase ^ 1 : acc_phase;
                     ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                    if (two) ptx::mbar_wait(&tempty[acc2], ph2 ^ 1);
                     ptx::tc_fence_after();
-                    const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-                    bool first = true;
-                    for (int dp = max(1, g - sb); dp <= min(sa, g - 1); ++dp)
+                    const uint32_t d1 = tmem_base + static_cast<uint32_t>(acc * BN);
+                    const uint32_t d2 = tmem_base + static_cast<uint32_t>(acc2 * BN);
+                    bool first1 = true, first2 = true;
+                    const int lo = max(1, (two ? g - 1 : g) - sb), hi = min(sa, g - 1);
+                    for (int dp = lo; dp <= hi; ++dp) {
+                        const bool v1 = dp >= max(1, g - sb);
+                        const bool v2 = two && dp <= min(sa, g - 2);
                         for (int kb = 0; kb < p.kblocks; ++kb) {
                             ptx::mbar_wait(&full[stage], phase);
                             ptx::tc_fence_after();
                             const uint32_t a_base = ptx::smem_u32(sA + stage * A_STAGE);
-                            const uint32_t b_base = ptx::smem_u32(sB + stage * B_STAGE);
+                            const uint32_t b1 = ptx::smem_u32(sB + (stage * 2) * B_STAGE);
+                            const uint32_t b2 = ptx::smem_u32(sB + (stage * 2 + 1) * B_STAGE);
 #pragma unroll
                             for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K per stage
                                 const uint64_t ad = ptx::umma_desc_sw128(a_base + k * 32, 0, 1024);
-                                const uint64_t bd = ptx::umma_desc_sw128(b_base + k * 32, 0, 1024);
-                                mma_i8_ss(d_tmem, ad, bd, idesc, (first && k == 0) ? 0u : 1u);
+                                if (v1)
+                                    mma_i8_ss(d1, ad, ptx::umma_desc_sw128(b1 + k * 32, 0, 1024), idesc,
+                                              (first1 && k == 0) ? 0u : 1u);
+                                if (v2)
+                                    mma_i8_ss(d2, ad, ptx::umma_desc_sw128(b2 + k * 32, 0, 1024), idesc,
+                                              (first2 && k == 0) ? 0u : 1u);
                             }
-                            first = false;
+                            if (v1) first1 = false;
+                            if (v2) first2 = false;
                             ptx::mma_commit(&empty[stage]);
                             if (++stage == STAGES) {
                                 stage = 0;
                                 phase ^= 1;
                             }
                         }
+                    }
                     ptx::mma_commit(&tfull[acc]);
                     if (++acc == NACC) {
                         acc = 0;
                         acc_phase ^= 1;
+                    }
+                    if (two) {
+                        ptx::mma_commit(&tfull[acc]);
+                        if (++acc == NACC) {
+                            acc = 0;
+                            acc_phase ^= 1;
+                        }
                     }
                 }
             }
