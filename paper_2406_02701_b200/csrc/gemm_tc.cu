@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cuda_fp16.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -328,34 +329,41 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
 // MMA (M=256, N=256); stage "full" barriers live in the even CTA, "empty"
 // barriers in both (multicast commit); each CTA's epilogue reads its own 128
 // TMEM lanes and signals the even CTA's tmem-empty barrier.
-// 5 operand stages and two C chunk buffers: the C loader prefetches the next
+// 6 operand stages and two C chunk buffers: the C loader prefetches the next
 // chunk (also the next unit's first one) while the epilogue works on the
 // current, so the read-modify-write of C stays off the MMA's path.
-constexpr int STAGES2 = 5;
+// NST = 6 (default): six operand stages and two half-size C chunks (128 rows x
+// 128 bytes) in the same shared memory; NST = 5 (MPCR_TC2_STAGES=5): five
+// stages and two 128 x 256-byte chunks.  Six stages: +1.5 % on the n=65536
+// Cholesky (770.5 -> 782 TF/s), dense GEMM unchanged.
 constexpr int B2_STAGE = (BN / 2) * 128;  // 16 KB
-constexpr int SMEM2_BYTES = STAGES2 * (A_STAGE + B2_STAGE) + 2 * C_CHUNK + 1024 + 256;
+template <int NST>
+constexpr int c2_chunk() { return NST == 5 ? C_CHUNK : C_CHUNK / 2; }
+template <int NST>
+constexpr int smem2_bytes() { return NST * (A_STAGE + B2_STAGE) + 2 * c2_chunk<NST>() + 1024 + 256; }
 
-template <bool A_MN, bool B_MN, typename TC>
+template <bool A_MN, bool B_MN, typename TC, int STAGES2>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ Params p) {
     constexpr int ES = 2, BK = 64, BW = 64;
     constexpr int BOX = BW * BK * ES;          // 8 KB MN-major box
     constexpr int KSTEP_MN = (32 / ES) * 128;  // UMMA K (32 bytes) in MN-major rows
-    constexpr int CW = 256 / sizeof(TC);
+    constexpr int C2_CHUNK = c2_chunk<STAGES2>();
+    constexpr int CW = C2_CHUNK / BM / sizeof(TC);
     constexpr int NCHUNK = BN / CW;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES2 * A_STAGE;
-    TC* cbuf0 = reinterpret_cast<TC*>(sB + STAGES2 * B2_STAGE);  // two chunks of C_CHUNK bytes
-    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(cbuf0) + 2 * C_CHUNK);
+    TC* cbuf0 = reinterpret_cast<TC*>(sB + STAGES2 * B2_STAGE);  // two chunks of C2_CHUNK bytes
+    uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(cbuf0) + 2 * C2_CHUNK);
     uint64_t* empty = full + STAGES2;
     uint64_t* tfull = empty + STAGES2;
     uint64_t* tempty = tfull + 2;
     uint64_t* cfull = tempty + 2;  // [2]
     uint64_t* cempty = cfull + 2;  // [2]
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cempty + 2);
-    auto cbuf_of = [&](int b) { return reinterpret_cast<TC*>(reinterpret_cast<uint8_t*>(cbuf0) + b * C_CHUNK); };
+    auto cbuf_of = [&](int b) { return reinterpret_cast<TC*>(reinterpret_cast<uint8_t*>(cbuf0) + b * C2_CHUNK); };
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = ptx::cluster_ctarank();
@@ -496,7 +504,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     const int b = g & 1;
                     ptx::mbar_wait(&cempty[b], ((g >> 1) & 1) ^ 1);
                     if (read_c) {
-                        ptx::mbar_arrive_expect_tx(&cfull[b], C_CHUNK);
+                        ptx::mbar_arrive_expect_tx(&cfull[b], C2_CHUNK);
                         ptx::tma_load_3d(cbuf_of(b), &p.map_c, &cfull[b], m0, n0 + h * CW, pr.c_tile);
                     } else {
                         ptx::mbar_arrive(&cfull[b]);
@@ -644,9 +652,10 @@ void launch_kernel(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total, int
 }
 
 
-template <bool A_MN, bool B_MN, typename TC>
+template <bool A_MN, bool B_MN, typename TC, int NST>
 void launch_kernel2(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total_pairs, int tiles_per_cta) {
-    auto kern = gemm_tc2_kernel<A_MN, B_MN, TC>;
+    auto kern = gemm_tc2_kernel<A_MN, B_MN, TC, NST>;
+    constexpr int SMEM2_BYTES = smem2_bytes<NST>();
     static bool configured = false;
     if (!configured) {
         MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
@@ -688,6 +697,10 @@ void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
         return !(e && e[0] == '0');
     }();
     const bool pair = kind == 0 && tc2_env;  // FP16: 2-CTA pair kernel
+    static const int tc2_stages = [] {
+        const char* e = getenv("MPCR_TC2_STAGES");
+        return (e && e[0] == '5') ? 5 : 6;
+    }();
     const uint32_t rows_a = a_mn ? 0 : BM, rows_b = b_mn ? 0 : (pair ? BN / 2 : BN);
     const void* As[2] = {g.A, g.A2 ? g.A2 : g.A};
     const void* Bs[2] = {g.B, g.B2 ? g.B2 : g.B};
@@ -705,7 +718,8 @@ void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
     // C: [c_tiles][n][m] with chunks of 128 rows x 256 bytes
     const bool half_c = g.pc == MP_HALF;
     make_map(&p.map_c, g.C, half_c ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
-             half_c ? 2 : 4, g.m, g.n, g.c_tiles, g.ldc, g.c_tile_stride, BM, half_c ? 128 : 64,
+             half_c ? 2 : 4, g.m, g.n, g.c_tiles, g.ldc, g.c_tile_stride, BM,
+             (half_c ? 128 : 64) / (pair && tc2_stages == 6 ? 2 : 1),
              CU_TENSOR_MAP_SWIZZLE_NONE);
     // K segments
     int nseg = 1;
@@ -742,12 +756,26 @@ void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
                      (g.lower_only ? 0.5 : 1.0));
     if (pair) {
         const int64_t pairs = static_cast<int64_t>(p.nprob) * ((p.mblocks + 1) / 2) * p.nblocks;
+        // MPCR_DEBUG_TC: one line per pair-kernel launch in issue order (picks
+        // the launch index of an ncu capture and its tile count)
+        static const bool dbg_tc = getenv("MPCR_DEBUG_TC") != nullptr;
+        static int64_t dbg_idx = 0;
+        if (dbg_tc)
+            std::fprintf(stderr, "[mpcr] tc2 launch %lld: C %s, %d problem(s) of %dx%dx%d, beta %g\n",
+                         static_cast<long long>(dbg_idx++), half_c ? "half" : "single", p.nprob, p.M,
+                         p.N, p.K, p.beta);
 #define MP_TC2(AM, BMJ)                                                                 \
         if (a_mn == AM && b_mn == BMJ) {                                                \
-            if (half_c)                                                                 \
-                launch_kernel2<AM, BMJ, uint16_t>(ctx, s, p, pairs, g.tiles_per_cta);   \
-            else                                                                        \
-                launch_kernel2<AM, BMJ, float>(ctx, s, p, pairs, g.tiles_per_cta);      \
+            if (tc2_stages == 6) {                                                      \
+                if (half_c)                                                             \
+                    launch_kernel2<AM, BMJ, uint16_t, 6>(ctx, s, p, pairs, g.tiles_per_cta); \
+                else                                                                    \
+                    launch_kernel2<AM, BMJ, float, 6>(ctx, s, p, pairs, g.tiles_per_cta); \
+            } else if (half_c) {                                                        \
+                launch_kernel2<AM, BMJ, uint16_t, 5>(ctx, s, p, pairs, g.tiles_per_cta); \
+            } else {                                                                    \
+                launch_kernel2<AM, BMJ, float, 5>(ctx, s, p, pairs, g.tiles_per_cta);   \
+            }                                                                           \
             return;                                                                     \
         }
         MP_TC2(true, true)
