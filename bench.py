@@ -361,12 +361,17 @@ def run_chol(args, world, rank, local):
         ach = f16["rate"]
         peak = pk["bf16_tflops_sustained"]
         traffic, tnote = None, None
+        # the ncu capture of this n's bulk launch when one is committed
+        tpath = os.path.join(ROOT, "profiles", f"r01_ncu_traffic_n{n}.json")
+        if not os.path.exists(tpath):
+            tpath = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
         try:
-            with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as f:
+            with open(tpath) as f:
                 tj = json.load(f)
             traffic = tj["traffic_bytes_per_launch"]
-            tnote = (f"dram read+write of one captured bulk launch ({tj['duration_us']} us), "
-                     f"algorithmic {tj['algorithmic_bytes_per_launch']:.3g} B; {tj['summary']}")
+            tnote = (f"dram read+write of one captured bulk launch ({tj['duration_us']} us, "
+                     f"{tj.get('tiles', '?')} tiles), algorithmic "
+                     f"{tj['algorithmic_bytes_per_launch']:.3g} B; {os.path.basename(tpath)}")
         except (OSError, KeyError, ValueError):
             pass
         roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",

@@ -363,6 +363,24 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 break;
         }
     }
+    // FP16 update tiles of a step in groups of G tile columns, rows within a
+    // group, the group's columns within a row: each panel tile L_ik serves G
+    // consecutive tiles and the group's G tiles L_jk stay in L2, so the panel
+    // (256 MB at n=131072, twice the L2) is not re-read from HBM per column.
+    // Tiles of one step are independent, so the factor is unchanged.
+    static const int upd_group = [] {
+        const char* e = getenv("MPCR_UPDATE_GROUP");
+        return e ? std::max(1, atoi(e)) : 8;
+    }();
+    for (int64_t k = 0; k < NT; ++k)
+        for (int w = 0; w < 3; ++w)
+            std::stable_sort(acc[k].up[w].tc.begin(), acc[k].up[w].tc.end(),
+                             [](const TcProblem& x, const TcProblem& y) {
+                                 const int gx = x.b_tile / upd_group, gy = y.b_tile / upd_group;
+                                 if (gx != gy) return gx < gy;
+                                 if (x.a_tile != y.a_tile) return x.a_tile < y.a_tile;
+                                 return x.b_tile < y.b_tile;
+                             });
     std::vector<char> buf;
     for (int64_t k = 0; k < NT; ++k) {
         StepLists& L = steps[k];
