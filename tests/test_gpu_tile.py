@@ -278,3 +278,45 @@ def test_tile_fill_matern_points_half_bit_exact(ctx, ref):
         t.fill_matern_points(x, y, 0.5, rng_a, var, nug)
         want = var * np.exp(-d / rng_a) + nug * np.eye(n)
         np.testing.assert_array_equal(t.to_numpy(), round_to(want, 0))
+
+
+_ENV_PROBE = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2406_02701_b200 as mp
+ctx = mp.Context(0)
+n, nb = 4096, 256
+nt = n // nb
+i, j = np.indices((nt, nt))
+g = np.where(i == j, 2, np.where(abs(i - j) == 1, 1, 0))
+A = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+A.fill_matern(64, 0.5, 0.03, 1.0)
+mp.tile_chol(A)
+print(hashlib.sha256(np.ascontiguousarray(A.to_numpy()).tobytes()).hexdigest())
+"""
+
+
+@pytest.mark.parametrize("env", [{"MPCR_UPDATE_GROUP": "1"}, {"MPCR_UPDATE_GROUP": "3"},
+                                 {"MPCR_TC2_STAGES": "5"}, {"MPCR_LOOKAHEAD": "0"}])
+def test_tile_chol_schedule_knobs_bitwise(env):
+    """Update-tile order (MPCR_UPDATE_GROUP), the pair kernel's stage count and
+    the lookahead change only the schedule, never the arithmetic: the factor
+    is bit-identical to the default run (16 x 16 tiles, 2 update groups)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+    def run(extra):
+        e = dict(os.environ)
+        for k in ("MPCR_UPDATE_GROUP", "MPCR_TC2_STAGES", "MPCR_LOOKAHEAD"):
+            e.pop(k, None)
+        e.update(extra)
+        out = subprocess.run([sys.executable, "-c", _ENV_PROBE, root], env=e, capture_output=True,
+                             text=True, timeout=300)
+        assert out.returncode == 0, out.stderr[-2000:]
+        return out.stdout.strip().splitlines()[-1]
+
+    assert run(env) == run({})
