@@ -60,6 +60,12 @@ struct Params {
     int32_t mblocks, nblocks, kblocks;
     int32_t kblocks1;  // K blocks per segment; kblocks = nseg * kblocks1
     int32_t seg_a[3], seg_b[3];  // K segment s multiplies map_a[seg_a[s]] by map_b[seg_b[s]]
+    int32_t c_evict_first;       // pair kernel: C loads/stores marked L2 evict_first
+    // pair kernel unit assignment: cluster c takes units
+    // (c / lanes) * lanes * per + c % lanes + r * lanes, r < per, so the
+    // clusters resident together (one wave of `lanes`) work on neighbouring
+    // units through one contiguous chunk of the list instead of striding it
+    int32_t lanes, per;
 };
 
 __device__ __forceinline__ bool skip_tile(const TcProblem& pr, int m0, int n0) {
@@ -394,7 +400,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     const int mpairs = (p.mblocks + 1) / 2;  // an odd last block pairs with an out-of-range one
     const int tiles_per_prob = mpairs * p.nblocks;
     const int64_t total = static_cast<int64_t>(p.nprob) * tiles_per_prob;
-    const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const int64_t cid = blockIdx.x >> 1;
+    const int64_t wave0 = (cid / p.lanes) * static_cast<int64_t>(p.lanes) * p.per;
+    const int64_t t_first = wave0 + cid % p.lanes;
+    const int64_t t_end = min(total, wave0 + static_cast<int64_t>(p.lanes) * p.per);
+    const int64_t ncl = p.lanes;
     const bool read_c = p.beta != 0.0f;
     // Units of a problem in groups of up to 8 M-pairs, N-blocks within a group:
     // the ~74 pairs in flight share 8 A and ~9 B slabs per K step, so large
@@ -418,7 +428,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             const uint32_t full0 = ptx::mapa_shared(ptx::smem_u32(full), 0);  // even CTA's barriers
             int stage = 0;
             uint32_t phase = 0;
-            for (int64_t t = cid; t < total; t += ncl) {
+            for (int64_t t = t_first; t < t_end; t += ncl) {
                 TcProblem pr;
                 int m0, n0;
                 decode(t, pr, m0, n0);
@@ -462,7 +472,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int64_t t = cid; t < total; t += ncl) {
+            for (int64_t t = t_first; t < t_end; t += ncl) {
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
@@ -496,7 +506,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         // ===== C loader (both CTAs, own rows) =====
         if (lane == 0) {
             uint32_t g = 0;  // running chunk count: buffer g & 1, phase (g >> 1) & 1
-            for (int64_t t = cid; t < total; t += ncl) {
+            for (int64_t t = t_first; t < t_end; t += ncl) {
                 TcProblem pr;
                 int m0, n0;
                 decode(t, pr, m0, n0);
@@ -505,7 +515,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     ptx::mbar_wait(&cempty[b], ((g >> 1) & 1) ^ 1);
                     if (read_c) {
                         ptx::mbar_arrive_expect_tx(&cfull[b], C2_CHUNK);
-                        ptx::tma_load_3d(cbuf_of(b), &p.map_c, &cfull[b], m0, n0 + h * CW, pr.c_tile);
+                        if (p.c_evict_first)
+                            ptx::tma_load_3d_hint(cbuf_of(b), &p.map_c, &cfull[b], m0, n0 + h * CW, pr.c_tile,
+                                                  ptx::l2_policy_evict_first());
+                        else
+                            ptx::tma_load_3d(cbuf_of(b), &p.map_c, &cfull[b], m0, n0 + h * CW, pr.c_tile);
                     } else {
                         ptx::mbar_arrive(&cfull[b]);
                     }
@@ -520,7 +534,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         const uint32_t tempty0 = ptx::mapa_shared(ptx::smem_u32(tempty), 0);
         int acc = 0;
         uint32_t acc_phase = 0, g = 0;
-        for (int64_t t = cid; t < total; t += ncl) {
+        for (int64_t t = t_first; t < t_end; t += ncl) {
             TcProblem pr;
             int m0, n0;
             decode(t, pr, m0, n0);
@@ -556,7 +570,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                 ptx::fence_proxy_async_smem();
                 ptx::named_bar_sync(1, EPI_THREADS);
                 if (is_leader) {
-                    ptx::tma_store_3d(&p.map_c, cbuf, m0, n0 + h * CW, pr.c_tile);
+                    if (p.c_evict_first)
+                        ptx::tma_store_3d_hint(&p.map_c, cbuf, m0, n0 + h * CW, pr.c_tile,
+                                               ptx::l2_policy_evict_first());
+                    else
+                        ptx::tma_store_3d(&p.map_c, cbuf, m0, n0 + h * CW, pr.c_tile);
                     ptx::bulk_commit();
                     ptx::bulk_wait_read0();
                     ptx::mbar_arrive(&cempty[b]);
@@ -662,12 +680,23 @@ void launch_kernel2(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total_pai
         configured = true;
     }
     const int64_t clusters = persistent_grid(total_pairs, ctx->sm_count / 2, tiles_per_cta);
+    Params q = p;
+    q.lanes = static_cast<int32_t>(std::min<int64_t>(ctx->sm_count / 2, clusters));
+    q.per = static_cast<int32_t>((total_pairs + clusters - 1) / clusters);
+    static const bool strided = [] {  // MPCR_UNIT_STRIDED=1: classic grid-stride assignment
+        const char* e = getenv("MPCR_UNIT_STRIDED");
+        return e && e[0] == '1';
+    }();
+    if (strided) {
+        q.lanes = static_cast<int32_t>(clusters);
+        q.per = static_cast<int32_t>((total_pairs + clusters - 1) / clusters);
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(2 * clusters));
     cfg.blockDim = dim3(NTHREADS);
     cfg.dynamicSmemBytes = SMEM2_BYTES;
     cfg.stream = s;
-    MP_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+    MP_CUDA(cudaLaunchKernelEx(&cfg, kern, q));
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());
 }
@@ -737,6 +766,11 @@ void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
         p.seg_a[0] = 0; p.seg_b[0] = 1;
         p.seg_a[1] = 0; p.seg_b[1] = 0;
     }
+    static const int c_evict_first = [] {
+        const char* e = getenv("MPCR_C_EVICT_FIRST");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    p.c_evict_first = c_evict_first;
     p.problems = g.problems;
     p.single = TcProblem{0, 0, 0, g.lower_only ? 1 : 0};
     p.nprob = g.problems ? static_cast<int32_t>(g.count) : 1;

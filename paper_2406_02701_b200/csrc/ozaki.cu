@@ -32,6 +32,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "device.cuh"
@@ -69,6 +70,9 @@ struct Params {
     int64_t rexp_stride_a, rexp_stride_b;
     const int32_t* ndig_a;  // digits per tile (nullptr: all S)
     const int32_t* ndig_b;
+    // CTA c takes units (c / lanes) * lanes * per + c % lanes + r * lanes,
+    // r < per: the CTAs resident together sweep one contiguous chunk
+    int32_t lanes, per;
 };
 
 // Digit counts of a problem: pairs (dp, dq) with dp <= sa, dq <= sb; groups
@@ -138,6 +142,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
 
     const int tiles_per_prob = p.mblocks * p.nblocks;
     const int64_t total = static_cast<int64_t>(p.nprob) * tiles_per_prob;
+    const int64_t wave0 = (blockIdx.x / p.lanes) * static_cast<int64_t>(p.lanes) * p.per;
+    const int64_t t_first = wave0 + blockIdx.x % p.lanes;
+    const int64_t t_end = min(total, wave0 + static_cast<int64_t>(p.lanes) * p.per);
     auto decode = [&](int64_t t, OzProblem& pr, int& m0, int& n0) {
         const int64_t pi = t / tiles_per_prob;
         const int r = static_cast<int>(t - pi * tiles_per_prob);
@@ -151,7 +158,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+            for (int64_t t = t_first; t < t_end; t += p.lanes) {
                 OzProblem pr;
                 int m0, n0;
                 decode(t, pr, m0, n0);
@@ -193,7 +200,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+            for (int64_t t = t_first; t < t_end; t += p.lanes) {
                 OzProblem pr;
                 int m0, n0;
                 decode(t, pr, m0, n0);
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
         const int r = lg * 32 + lane;       // tile row (TMEM lane)
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+        for (int64_t t = t_first; t < t_end; t += p.lanes) {
             OzProblem pr;
             int m0, n0;
             decode(t, pr, m0, n0);
@@ -664,8 +671,14 @@ void launch_oz_gemm(Ctx* ctx, cudaStream_t s, const OzGemm& g) {
         MP_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
         configured = true;
     }
-    const int64_t grid = persistent_grid(total, ctx->sm_count, g.tiles_per_cta);
-    oz_gemm_kernel<<<static_cast<unsigned>(std::max<int64_t>(grid, 1)), NTHREADS, SMEM_BYTES, s>>>(p);
+    const int64_t grid = std::max<int64_t>(persistent_grid(total, ctx->sm_count, g.tiles_per_cta), 1);
+    static const bool strided = [] {  // MPCR_UNIT_STRIDED=1: classic grid-stride assignment
+        const char* e = getenv("MPCR_UNIT_STRIDED");
+        return e && e[0] == '1';
+    }();
+    p.lanes = static_cast<int32_t>(strided ? grid : std::min<int64_t>(ctx->sm_count, grid));
+    p.per = static_cast<int32_t>((std::max<int64_t>(total, 1) + grid - 1) / grid);
+    oz_gemm_kernel<<<static_cast<unsigned>(grid), NTHREADS, SMEM_BYTES, s>>>(p);
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());
 }
