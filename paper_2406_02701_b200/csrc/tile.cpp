@@ -760,11 +760,22 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         const auto th0 = std::chrono::steady_clock::now();
         std::vector<double> th;
         panel_phase(0, nullptr);
+        // MPCR_WB_ASYNC=1 (off by default: measured 0.5-0.8 % slower at n=65536 and 131072,
+        // the high-priority copy steals SMs from the bulk GEMM; tools/ab_wb_async.sh):
+        // write-back of tile column k off the bulk stream: on sl2 right after the tail of
+        // panel k+1 (ev_panel[k+1] is recorded before it, so bulk k+1 does not wait on it).
+        // The panel buffer (k & 1) is next written by panel k+2, whose head TRSM waits
+        // ev_next[k+1] (recorded on sl2 after this copy) and whose tail runs on sl2.
+        static const bool wb_env = [] {
+            const char* e = getenv("MPCR_WB_ASYNC");
+            return e && e[0] == '1';
+        }();
+        const bool wb_async = wb_env && tsplit;
         for (int64_t k = 0; k < NT; ++k) {
             if (la) MP_CUDA(cudaStreamWaitEvent(s, ev_panel[k], 0));
             convert_panel(k, 1, s);
             update_phase(k, 1, s, bulk_tpc);
-            write_back(k, s);
+            if (!wb_async || k + 1 >= NT) write_back(k, s);
             if (la) MP_CUDA(cudaEventRecord(ev_rest[k], s));
             if (k + 1 < NT) {
                 if (la) {
@@ -776,6 +787,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 if (la && k >= 1) MP_CUDA(cudaStreamWaitEvent(sl, ev_rest[k - 1], 0));
                 update_phase(k, 2, sl, 0);
                 panel_phase(k + 1, la ? ev_next[k] : nullptr);
+                if (wb_async) write_back(k, sl2);
             }
             if (dbg_host)
                 th.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count());
