@@ -337,6 +337,7 @@ def run_chol(args, world, rank, local):
             prof[nm] = {"ms": t, "launches": cnt, "work": work,
                         "rate": work / (t * 1e-3) / 1e12 if t > 0 else None}
     logdet = A.logdet()
+    accuracy = None if args.no_check else check_factor(args, A, g, x, y, n, nb, ctx, world, grid)
     # e2e through the C ABI from host buffers
     e2e_ms = None
     if not args.no_e2e:
@@ -423,6 +424,8 @@ def run_chol(args, world, rank, local):
         "gpu_launches": launches,
         "wall_ms_per_step": t_wall / args.steps * 1e3,
         "logdet": logdet,
+        "accuracy": accuracy,
+        "rel_err": accuracy["sampled_backward_error"] if accuracy else None,
         "clocks": clk.summary(),
     }
     if e2e_ms is not None:
@@ -439,10 +442,52 @@ def run_chol(args, world, rank, local):
             write_results(args.results, [{
                 "op": "tile_chol", "n": n, "precision": f"mixed(b64={args.b64};b32={args.b32})",
                 "placement": f"gpu:{world}", "reps": args.steps,
-                "median_seconds": steps_s[len(steps_s) // 2], "rel_frob_err": None,
+                "median_seconds": steps_s[len(steps_s) // 2],
+                "rel_frob_err": accuracy["sampled_backward_error"] if accuracy else None,
                 "tflops": value, "blended_roofline_frac": line["blended_roofline"]["frac"],
                 "e2e_tflops": line.get("e2e", {}).get("value")}])
     ctx.synchronize()
+
+
+def check_factor(args, A, g, x, y, n, nb, ctx, world, grid):
+    """Error attached to the timing (mpnum_cli.cpp:59-63,174 writes rel_frob_err
+    with every bench record): the factor is 9-35 GB, so it is checked on a
+    sample (paper_2406_02701_b200/verify.py):
+      * sampled backward error ||(LL^T - A)[R,R]||_F / ||A[R,R]||_F over 256 rows
+        (clusters spread over the matrix, the last tile row included, + random);
+      * the leading m x m block (m = min(n, 8192)) equal bit for bit to a
+        separate factorization of the leading sub-problem, which
+        tests/test_gpu_tile_nb1024.py checks against the CPU oracle."""
+    import paper_2406_02701_b200 as mp
+    from paper_2406_02701_b200 import verify
+
+    t0 = time.perf_counter()
+    rows = verify.sample_rows(n, nb, clusters=16, width=8, extra=128)
+    Lr = A.get_rows(rows)
+    if world > 1:  # every rank holds its own tiles, zeros elsewhere
+        import torch
+        import torch.distributed as tdist
+
+        tt = torch.from_numpy(Lr).cuda()
+        tdist.all_reduce(tt)
+        Lr = tt.cpu().numpy()
+    res = verify.sampled_residual(None, x, y, rows, nb, g, args.range, 1.0, args.nugget, L_rows=Lr)
+    m = min(n, 8192 // nb * nb)
+    lead = rows[rows < m]
+    same = None
+    if m < n and lead.size:
+        sub = mp.MPCRTile(m, m, nb, nb, None, g[:m // nb, :m // nb], ctx)
+        sub.fill_matern_points(x[:m], y[:m], 0.5, args.range, 1.0, args.nugget)
+        mp.tile_chol(sub)
+        same = verify.leading_rows_equal(Lr[np.searchsorted(rows, lead)], sub.get_rows(lead))
+        sub.close()
+    return {"sampled_backward_error": res["normwise"], "componentwise_backward_error": res["componentwise"],
+            "sample_rows": res["rows"], "sample_entries": res["entries"],
+            "leading_block": m, "leading_block_bitwise_equal": same,
+            "check_seconds": time.perf_counter() - t0,
+            "note": "normwise ||(LL^T-A)[R,R]||_F/||A[R,R]||_F on the sample R; the leading block is the "
+                    "factor of the leading sub-problem (checked vs the CPU oracle in "
+                    "tests/test_gpu_tile_nb1024.py); bound there: 4*(n/8192)*oracle value at n=8192"}
 
 
 def run_gemm(args, world, rank, local):
@@ -636,6 +681,7 @@ def main():
     ap.add_argument("--cpu-nb", type=int, default=256)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-check", action="store_true", help="skip the sampled accuracy check")
     ap.add_argument("--results", default=None,
                     help="also write a BenchRecord CSV/JSON (io.hpp:11-20) to this path")
     args = ap.parse_args()

@@ -201,6 +201,10 @@ mp_status mp_tile_info(mp_tile t, int64_t* rows, int64_t* cols, int64_t* rows_pe
 /* Whole-matrix values (column-major doubles), rounded per tile precision. */
 mp_status mp_tile_set_values(mp_tile t, const double* host);
 mp_status mp_tile_get_values(mp_tile t, double* host);
+/* Rows rows[0..count) of the whole matrix widened to double, row-major
+ * (host[q * cols + c]).  No reference counterpart: checking a factor too
+ * large to download (sampled residuals of L L^T - A at n = 131072). */
+mp_status mp_tile_get_rows(mp_tile t, const int64_t* rows, int64_t count, double* host);
 /* Same, device-resident double source (n x n column-major, ld). */
 mp_status mp_tile_set_values_device(mp_tile t, const double* dev, int64_t ld);
 /* MPCRTile.GetTile, 0-based; returns a non-owning view. */

@@ -79,6 +79,7 @@ SIGNATURES = {
     "mp_tile_info": (C.c_int, [_vp, _ip, _ip, _ip, _ip, _ip, _ip]),
     "mp_tile_set_values": (C.c_int, [_vp, _vp]),
     "mp_tile_get_values": (C.c_int, [_vp, _vp]),
+    "mp_tile_get_rows": (C.c_int, [_vp, _vp, C.c_int64, _vp]),
     "mp_tile_set_values_device": (C.c_int, [_vp, _vp, _i64]),
     "mp_tile_get_tile": (C.c_int, [_vp, _i64, _i64, C.POINTER(_vp)]),
     "mp_tile_precision": (C.c_int, [_vp, _i64, _i64, C.POINTER(C.c_int)]),

@@ -257,4 +257,30 @@ void launch_leaf_inverse(Ctx* ctx, cudaStream_t s, const double* L, int64_t ldl,
     MP_CUDA(cudaGetLastError());
 }
 
+namespace {
+__global__ void __launch_bounds__(256) gather_rows_kernel(const RowItem* __restrict__ items, int64_t nb,
+                                                          int64_t ldd) {
+    const RowItem it = items[blockIdx.y];
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nb; c += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = c * nb + it.row;
+        double v;
+        if (it.prec == MP_HALF) v = h2d(static_cast<const uint16_t*>(it.tile)[e]);
+        else if (it.prec == MP_SINGLE) v = f2d(static_cast<const float*>(it.tile)[e]);
+        else v = static_cast<const double*>(it.tile)[e];
+        it.dst[c * ldd] = v;
+    }
+}
+}  // namespace
+
+void launch_gather_rows(Ctx* ctx, cudaStream_t s, const RowItem* dev_items, int64_t count, int64_t nb,
+                        int64_t ldd) {
+    for (int64_t b = 0; b < count; b += 65535) {
+        const int64_t cnt = count - b < 65535 ? count - b : 65535;
+        const dim3 grid(static_cast<unsigned>((nb + 255) / 256), static_cast<unsigned>(cnt));
+        gather_rows_kernel<<<grid, 256, 0, s>>>(dev_items + b, nb, ldd);
+        count_launch(ctx);
+    }
+    MP_CUDA(cudaGetLastError());
+}
+
 }  // namespace mpcr

@@ -35,4 +35,16 @@ void launch_split_f16(Ctx* ctx, cudaStream_t s, const double* x, uint16_t* hi, u
 void launch_leaf_inverse(Ctx* ctx, cudaStream_t s, const double* L, int64_t ldl, int64_t n,
                          double* Linv, int64_t ldi);
 
+// Row gather for mp_tile_get_rows: item q copies row `row` (0-based within
+// the tile) of one nb x nb column-major tile of precision `prec`, widened to
+// double, into dst[c * ldd] for c < nb.
+struct RowItem {
+    const void* tile;
+    double* dst;
+    int32_t row;
+    int32_t prec;
+};
+void launch_gather_rows(Ctx* ctx, cudaStream_t s, const RowItem* dev_items, int64_t count, int64_t nb,
+                        int64_t ldd);
+
 }  // namespace mpcr

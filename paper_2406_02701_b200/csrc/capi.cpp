@@ -27,6 +27,7 @@ void* Ctx::ensure_scratch(size_t bytes, int which) {
     }
     MP_CUDA(cudaMalloc(&p, bytes));
     cap = bytes;
+    ++scr_gen;
     return p;
 }
 
@@ -148,10 +149,12 @@ namespace {
 
 Ctx* C_(mp_ctx c) {
     if (!c) fail(MP_INVALID_PARAM, "null context");
+    bind_device(c);
     return c;
 }
 Array& A_(mp_array a, const char* what) {
     if (!a) fail(MP_INVALID_PARAM, std::string(what) + ": null array");
+    if (a->ctx) bind_device(a->ctx);
     return *a;
 }
 void require_matrix(const Array& a, const char* what) {

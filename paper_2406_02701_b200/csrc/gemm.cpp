@@ -134,9 +134,19 @@ void launch_gemm(Ctx* ctx, cudaStream_t s, const GemmDesc& g) {
             return;
         }
     }
-    if (g.pa == MP_HALF && g.pb == MP_HALF && g.pc == MP_DOUBLE && g.k > 0 && g.k < (1 << 30) &&
-        ozaki_enabled()) {
-        launch_gemm_ozaki(ctx, s, g);
+    if (g.pa == MP_HALF && g.pb == MP_HALF && g.pc == MP_DOUBLE && g.k > 0 && ozaki_enabled()) {
+        // The int32 digit-group sums are exact while 6 pairs * K * 64^2 < 2^31
+        // (K < 87381): longer contractions run in K chunks of OZ_MAX_K, each
+        // chunk's FP64 result accumulated into C (beta applies once).
+        for (int64_t k0 = 0; k0 < g.k; k0 += OZ_MAX_K) {
+            GemmDesc c = g;
+            c.k = std::min<int64_t>(OZ_MAX_K, g.k - k0);
+            // op(A) columns / op(B) rows k0 .. k0 + c.k (elements of 2 bytes)
+            c.A = static_cast<const uint16_t*>(g.A) + (g.ta ? k0 : k0 * g.lda);
+            c.B = static_cast<const uint16_t*>(g.B) + (g.tb ? k0 * g.ldb : k0);
+            if (k0 > 0) c.beta = 1.0;
+            launch_gemm_ozaki(ctx, s, c);
+        }
         return;
     }
     if (g.pa == MP_DOUBLE && g.pb == MP_DOUBLE && g.pc == MP_DOUBLE) {

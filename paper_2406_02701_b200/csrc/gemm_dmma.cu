@@ -356,11 +356,10 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 2 : 1) dmma_gemm_ke
 template <int BT, typename TI>
 void launch_bt(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count) {
     using CF = DCfg<BT>;
-    static bool configured = false;
-    if (!configured) {
+    static unsigned long long configured = 0;  // per-device bitmask
+    if (first_on_device(configured)) {
         MP_CUDA(cudaFuncSetAttribute(dmma_gemm_kernel<BT, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      std::max(CF::SMEM, 160 * 1024)));
-        configured = true;
     }
     const int smem = g.exclusive ? std::max(CF::SMEM, 160 * 1024) : CF::SMEM;
     const unsigned S = static_cast<unsigned>(std::max(1, g.ksplit));

@@ -658,10 +658,9 @@ void make_op_map(CUtensorMap* map, int kind, const void* base, uint64_t d0, uint
 template <int KIND, bool A_MN, bool B_MN, typename TC>
 void launch_kernel(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total, int tiles_per_cta) {
     auto kern = gemm_tc_kernel<KIND, A_MN, B_MN, TC>;
-    static bool configured = false;
-    if (!configured) {
+    static unsigned long long configured = 0;  // per-device bitmask
+    if (first_on_device(configured)) {
         MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-        configured = true;
     }
     const int grid = static_cast<int>(std::min<int64_t>(persistent_grid(total, ctx->sm_count, tiles_per_cta), 1 << 30));
     kern<<<grid, NTHREADS, SMEM_BYTES, s>>>(p);
@@ -674,10 +673,9 @@ template <bool A_MN, bool B_MN, typename TC, int NST>
 void launch_kernel2(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total_pairs, int tiles_per_cta) {
     auto kern = gemm_tc2_kernel<A_MN, B_MN, TC, NST>;
     constexpr int SMEM2_BYTES = smem2_bytes<NST>();
-    static bool configured = false;
-    if (!configured) {
+    static unsigned long long configured = 0;  // per-device bitmask
+    if (first_on_device(configured)) {
         MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
-        configured = true;
     }
     const int64_t clusters = persistent_grid(total_pairs, ctx->sm_count / 2, tiles_per_cta);
     Params q = p;

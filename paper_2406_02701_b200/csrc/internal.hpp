@@ -82,8 +82,21 @@ struct Ctx {
     // operand splits (3xTF32), 3: spare
     void* scr[4] = {nullptr, nullptr, nullptr, nullptr};
     size_t scr_bytes[4] = {0, 0, 0, 0};
+    // bumped whenever a scratch slot is (re)allocated: CUDA graphs captured
+    // over scratch pointers are stale once it changes
+    uint64_t scr_gen = 0;
     void* ensure_scratch(size_t bytes, int which = 0);
 };
+
+// Make ctx's device current for this thread (every C-ABI entry point does
+// this through its handle accessors before any allocation or launch).
+inline void bind_device(const Ctx* c) {
+    int d = -1;
+    if (cudaGetDevice(&d) != cudaSuccess || d != c->device) {
+        const cudaError_t e = cudaSetDevice(c->device);
+        if (e != cudaSuccess) throw std::runtime_error(std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    }
+}
 
 struct Array {
     Ctx* ctx = nullptr;
@@ -256,6 +269,17 @@ void launch_add_diag(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64_t 
                      double v);
 
 inline void count_launch(Ctx* ctx, int n = 1) { ctx->launches += n; }
+
+// One-time per-device setup (kernel attribute opt-ins): true the first time
+// it is called for the current device with this mask.
+inline bool first_on_device(unsigned long long& mask) {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) d = 0;
+    const unsigned long long bit = 1ull << (d & 63);
+    if (mask & bit) return false;
+    mask |= bit;
+    return true;
+}
 
 extern thread_local std::string g_last_error;
 double host_round(double x, mp_precision p);

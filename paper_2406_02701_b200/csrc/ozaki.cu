@@ -13,7 +13,8 @@
 //   An FP16 row spans at most 40 significant bits below its maximum (2^5 ..
 //   2^-24 plus 11 significand bits), and 6 digits hold 41, so the split is
 //   EXACT.  All S^2 = 36 digit products d_p d_q^T are computed (int32 sums
-//   are exact: |sum| <= 6 * K * 64^2 < 2^31 for K <= 8192 per group) and
+//   are exact: |sum| <= 6 * K * 64^2 < 2^31 for K < 87381; callers split
+//   longer K into OZ_MAX_K chunks) and
 //   combined in FP64 with one rounding per group: the result is as accurate
 //   as a correctly-ordered FP64 dot product, usually better.
 //
@@ -622,11 +623,10 @@ void launch_oz_slices(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_
     if (max_cols <= oz::OZ_STRIPE_K) {
         const int kpad = static_cast<int>((max_cols + 15) / 16 * 16);
         const int smem = 32 * (kpad + 8) * 2;
-        static bool cfg = false;
-        if (!cfg) {
+        static unsigned long long cfg = 0;  // per-device bitmask
+        if (first_on_device(cfg)) {
             MP_CUDA(cudaFuncSetAttribute(oz::oz_slice_stripe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          32 * (oz::OZ_STRIPE_K + 8) * 2));
-            cfg = true;
         }
         oz::oz_slice_stripe_kernel<<<grid, 256, smem, s>>>(items);
     } else {
@@ -666,10 +666,9 @@ void launch_oz_gemm(Ctx* ctx, cudaStream_t s, const OzGemm& g) {
     const int64_t total = static_cast<int64_t>(p.nprob) * p.mblocks * p.nblocks;
     ProfScope ps(ctx, MP_PROF_GEMM_F64, s,
                  2.0 * static_cast<double>(g.m) * g.n * g.k * p.nprob * (g.lower_only ? 0.5 : 1.0));
-    static bool configured = false;
-    if (!configured) {
+    static unsigned long long configured = 0;  // per-device bitmask
+    if (first_on_device(configured)) {
         MP_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-        configured = true;
     }
     const int64_t grid = std::max<int64_t>(persistent_grid(total, ctx->sm_count, g.tiles_per_cta), 1);
     static const bool strided = [] {  // MPCR_UNIT_STRIDED=1: classic grid-stride assignment

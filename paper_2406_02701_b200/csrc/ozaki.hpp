@@ -9,6 +9,10 @@
 namespace mpcr {
 
 constexpr int OZ_SLICES = 6;  // 6 x 7-bit digits: exact for any FP16 row
+// Longest contraction per launch: a digit group sums at most 6 pairs of
+// products |d_p d_q| <= 64^2, so its int32 accumulator is exact for
+// 6 * K * 2^12 < 2^31, i.e. K < 87381.
+constexpr int64_t OZ_MAX_K = 65536;
 
 // One problem of a grouped launch: digit tiles of A and B (indices into the
 // slabs), the FP64 C tile, lower triangle only (SYRK).

@@ -569,7 +569,7 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
     int ni = static_cast<int>(n);
     ProfScope ps(ctx, MP_PROF_POTRF, s, static_cast<double>(n) * n * n / 3.0);
     if (p == MP_DOUBLE) {
-        static bool cfg = false;
+        static unsigned long long cfg = 0;  // per-device bitmask
         // The factorization is latency-bound: by default each CTA reserves
         // most of its SM's shared memory so no other kernel's CTAs share the
         // SM with it (MPCR_POTRF_EXCLUSIVE=0 turns this off).
@@ -579,10 +579,9 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
         }();
         const size_t shm_need = std::max(POTRF_SMEM_ELEMS, POTRF_UPD_ELEMS) * sizeof(double);
         const size_t shm = exclusive ? std::max<size_t>(shm_need, 160 * 1024) : shm_need;
-        if (!cfg) {
+        if (first_on_device(cfg)) {
             MP_CUDA(cudaFuncSetAttribute((void*)potrf_coop_kernel<double>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-            cfg = true;
         }
         double* a = static_cast<double*>(A);
         double* d = static_cast<double*>(dinv);
@@ -594,12 +593,11 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
         }
         MP_CUDA(cudaLaunchCooperativeKernel((void*)potrf_coop_kernel<double>, grid, PT, args, shm, s));
         if (linv_diag) {
-            static bool cfg_l = false;
+            static unsigned long long cfg_l = 0;  // per-device bitmask
             const size_t shm_l = (2 * PB * (PB + 1) + 4 * 256 + 3 * 256) * sizeof(double);
-            if (!cfg_l) {
+            if (first_on_device(cfg_l)) {
                 MP_CUDA(cudaFuncSetAttribute((void*)leaf_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)shm_l));
-                cfg_l = true;
             }
             leaf_inverse_kernel<<<nblk, PT, shm_l, s>>>(a, lda, ni, d, linv_diag, ldi);
             count_launch(ctx);
@@ -616,11 +614,10 @@ void launch_potrf_lower(Ctx* ctx, cudaStream_t s, mp_precision p, void* A, int64
         }
     } else {
         const size_t shm = POTRF_SMEM_ELEMS * sizeof(float);
-        static bool cfg_f = false;
-        if (!cfg_f) {
+        static unsigned long long cfg_f = 0;  // per-device bitmask
+        if (first_on_device(cfg_f)) {
             MP_CUDA(cudaFuncSetAttribute((void*)potrf_coop_kernel<float>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-            cfg_f = true;
         }
         float* a = static_cast<float*>(A);
         float* d = static_cast<float*>(dinv);

@@ -50,14 +50,15 @@ struct mp_tile_s {
     int32_t* rexp = nullptr;  // their row exponents [2][tr][br]
     int32_t* ndig = nullptr;  // digits each of them needs [2][tr]
     void* backup[3] = {nullptr, nullptr, nullptr};  // jittered-NLL copy of the input slabs
-    void* work = nullptr;  // FP64 nb x nb x 2 + FP32 nb x nb + Linv{H,S}
+    void* work = nullptr;  // FP64 + FP32 diagonal work, two Linv generations, info (WorkLayout)
     void* lists = nullptr;
     size_t lists_bytes = 0;
-    TrtriPlan* trtri = nullptr;  // FP64 inverse plan over work (built on first chol)
+    TrtriPlan* trtri[2] = {nullptr, nullptr};  // FP64 inverse plans, one per Linv generation
     std::vector<cudaEvent_t> events;  // lookahead stream ordering (built on first chol)
     // the whole factorization as one CUDA graph (captured on the second
     // chol of this tile, replayed afterwards)
     cudaGraphExec_t graph = nullptr;
+    uint64_t graph_scr_gen = 0;  // Ctx::scr_gen the graph's scratch pointers belong to
     int64_t graph_launches = 0;
     int chol_runs = 0;
     bool graph_failed = false;
@@ -85,7 +86,7 @@ struct mp_tile_s {
             if (b) cudaFree(b);
         if (work) cudaFree(work);
         if (lists) cudaFree(lists);
-        trtri_plan_destroy(trtri);
+        for (TrtriPlan* p : trtri) trtri_plan_destroy(p);
         for (cudaEvent_t e : events) cudaEventDestroy(e);
         if (graph) cudaGraphExecDestroy(graph);
     }
@@ -108,8 +109,28 @@ namespace {
 
 mp_tile_s& T_(mp_tile t) {
     if (!t) fail(MP_INVALID_PARAM, "null MPCRTile");
+    if (t->ctx) bind_device(t->ctx);
     return *t;
 }
+
+// Diagonal-tile workspace of the scheduler.  Linv (FP64) and its FP32 /
+// FP16 hi+lo roundings come in two generations by step parity: the tail
+// TRSM of panel k (lookahead stream) still reads Linv_k while the critical
+// stream's POTRF/TRTRI of step k+1 writes Linv_{k+1}.
+struct WorkLayout {
+    size_t nn;
+    explicit WorkLayout(int64_t nb) : nn(static_cast<size_t>(nb) * nb) {}
+    double* dwork(void* w) const { return static_cast<double*>(w); }            // 8 nn
+    float* swork(void* w) const { return reinterpret_cast<float*>(b(w) + 8 * nn); }  // 4 nn
+    size_t gen(int g) const { return 12 * nn + static_cast<size_t>(g) * 16 * nn; }
+    double* linv64(void* w, int g) const { return reinterpret_cast<double*>(b(w) + gen(g)); }
+    float* linvS(void* w, int g) const { return reinterpret_cast<float*>(b(w) + gen(g) + 8 * nn); }
+    uint16_t* linvH(void* w, int g) const { return reinterpret_cast<uint16_t*>(b(w) + gen(g) + 12 * nn); }
+    uint16_t* linvHlo(void* w, int g) const { return reinterpret_cast<uint16_t*>(b(w) + gen(g) + 14 * nn); }
+    int64_t* info(void* w) const { return reinterpret_cast<int64_t*>(b(w) + gen(2) + 64); }
+    size_t bytes() const { return gen(2) + 256; }
+    static char* b(void* w) { return static_cast<char*>(w); }
+};
 
 void ensure_panels(mp_tile_s& t) {
     // two panel generations (step parity): the lookahead panel of step k+1 is
@@ -124,11 +145,7 @@ void ensure_panels(mp_tile_s& t) {
         MP_CUDA(cudaMalloc(&t.rexp, 2 * static_cast<size_t>(t.tr) * t.br * sizeof(int32_t)));
         MP_CUDA(cudaMalloc(&t.ndig, 2 * static_cast<size_t>(t.tr) * sizeof(int32_t)));
     }
-    if (!t.work) {
-        const size_t nn = static_cast<size_t>(t.br) * t.br;
-        // FP64 work, FP64 Linv, FP32 work, FP32 LinvS, FP16 LinvH hi + lo, info
-        MP_CUDA(cudaMalloc(&t.work, nn * (8 + 8 + 4 + 4 + 2 + 2) + 256));
-    }
+    if (!t.work) MP_CUDA(cudaMalloc(&t.work, WorkLayout(t.br).bytes()));
     if (t.events.empty()) {
         t.events.resize(4 * t.tr + 4);
         for (auto& e : t.events) MP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -188,7 +205,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     const int64_t nb = t.br, NT = t.tr, tt = t.tt();
     ensure_panels(t);
     const size_t nn = static_cast<size_t>(nb) * nb;
-    int64_t* dinfo = reinterpret_cast<int64_t*>(static_cast<char*>(t.work) + nn * 28 + 64);
+    const WorkLayout WL(nb);
+    int64_t* dinfo = WL.info(t.work);
     auto read_info = [&]() {
         int64_t info = -1;
         MP_CUDA(cudaMemcpyAsync(&info, dinfo, sizeof(info), cudaMemcpyDeviceToHost, s));
@@ -203,6 +221,13 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         return !(e && e[0] == '0');
     }();
     const bool want_graph = graph_env && !c->prof.enabled && !(t.dist && t.dist->world > 1);
+    if (t.graph && t.graph_scr_gen != c->scr_gen) {
+        // a context scratch slot the graph captured (POTRF barriers / leaf
+        // inverses, 3xTF32 splits) was reallocated since: re-capture
+        MP_CUDA(cudaStreamSynchronize(s));
+        MP_CUDA(cudaGraphExecDestroy(t.graph));
+        t.graph = nullptr;
+    }
     if (want_graph && t.graph) {
         MP_CUDA(cudaGraphLaunch(t.graph, s));
         c->launches += t.graph_launches;
@@ -276,8 +301,13 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     std::vector<StepAcc> acc(NT);
     std::vector<StepLists> steps(NT);
     const size_t nn0 = static_cast<size_t>(nb) * nb;
-    char* linv_base = static_cast<char*>(t.work);
-    const void* linv[3] = {linv_base + nn0 * 24, linv_base + nn0 * 20, linv_base + nn0 * 8};
+    (void)nn0;
+    auto linv = [&](int q, int64_t k) -> const void* {  // Linv_k rounded to p = q
+        const int g = static_cast<int>(k & 1);
+        return q == MP_HALF ? static_cast<const void*>(WL.linvH(t.work, g))
+               : q == MP_SINGLE ? static_cast<const void*>(WL.linvS(t.work, g))
+                                : static_cast<const void*>(WL.linv64(t.work, g));
+    };
     auto consumers = [&](int64_t k, int64_t i, StepAcc& A) {
         // every rank receives every panel tile: convert it once to each
         // precision the rank's own consumers (A_ij.converted(p) operands)
@@ -329,7 +359,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                     A.trsm_tc[hb].push_back(TcProblem{static_cast<int32_t>(t.slot[k * NT + i]), 0,
                                                       static_cast<int32_t>(i), 0});
                 else
-                    A.trsm_p[hb][q].push_back(TileProblem{t.ptr(i, k), linv[q], pan(q, i, k), 0, 0});
+                    A.trsm_p[hb][q].push_back(TileProblem{t.ptr(i, k), linv(q, k), pan(q, i, k), 0, 0});
                 A.wb[q].push_back(CopyItem{pan(q, i, k), t.ptr(i, k)});
                 if (P * Q == 1) consumers(k, i, A);
                 break;
@@ -446,16 +476,11 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     MP_CUDA(cudaMemcpyAsync(dl, buf.data(), buf.size(), cudaMemcpyHostToDevice, s));
 
     // ---- workspace ------------------------------------------------------------
-    char* w = static_cast<char*>(t.work);
-    double* dwork = reinterpret_cast<double*>(w);
-    double* linv64 = reinterpret_cast<double*>(w + nn * 8);
-    float* swork = reinterpret_cast<float*>(w + nn * 16);
-    float* linvS = reinterpret_cast<float*>(w + nn * 20);
-    uint16_t* linvH = reinterpret_cast<uint16_t*>(w + nn * 24);
-    uint16_t* linvHlo = reinterpret_cast<uint16_t*>(w + nn * 26);
-    // the TRTRI plan (FP64 inverse of dwork) is built once
-    if (!t.trtri) t.trtri = trtri_plan_create(c, s, dwork, nb, linv64, nb, nb);
-    TrtriPlan* trtri = t.trtri;
+    double* dwork = WL.dwork(t.work);
+    float* swork = WL.swork(t.work);
+    // the TRTRI plans (FP64 inverse of dwork into either Linv generation) are built once
+    for (int g = 0; g < 2; ++g)
+        if (!t.trtri[g]) t.trtri[g] = trtri_plan_create(c, s, dwork, nb, WL.linv64(t.work, g), nb, nb);
 
     // ---- panel k: factor A_kk, invert, TRSM the tile column, distribute and
     //      convert the panel for its consumers ---------------------------------
@@ -511,8 +536,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             g.lda = nb;
             g.a_tiles = t.nslot[MP_HALF];
             g.a_tile_stride = tt;
-            g.B = linvH;
-            g.B2 = linvHlo;
+            g.B = WL.linvH(t.work, static_cast<int>(k & 1));
+            g.B2 = WL.linvHlo(t.work, static_cast<int>(k & 1));
             g.ldb = nb;
             g.b_tiles = 1;
             g.b_tile_stride = tt;
@@ -550,6 +575,9 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             MP_CUDA(cudaMemsetAsync(ndg(0, k), 0, NT * sizeof(int32_t), st));
         const mp_precision pk = t.p(k, k);
         void* akk = t.ptr(k, k);
+        const int lg = static_cast<int>(k & 1);  // Linv generation of this step
+        double* linv64 = WL.linv64(t.work, lg);
+        TrtriPlan* trtri = t.trtri[lg];
         if (!L.potrf) {
             // not the owner: nothing to factor
         } else if (pk == MP_DOUBLE) {
@@ -584,11 +612,13 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         // substitution does not.
         if (L.need_linv[MP_HALF]) {
             if (L.n_trsm_tc[0] + L.n_trsm_tc[1])
-                launch_split_f16(c, st, linv64, linvH, linvHlo, static_cast<int64_t>(nn));
+                launch_split_f16(c, st, linv64, WL.linvH(t.work, lg), WL.linvHlo(t.work, lg),
+                                 static_cast<int64_t>(nn));
             else
-                launch_convert(c, st, MP_DOUBLE, linv64, nb, MP_HALF, linvH, nb, nb, nb);
+                launch_convert(c, st, MP_DOUBLE, linv64, nb, MP_HALF, WL.linvH(t.work, lg), nb, nb, nb);
         }
-        if (L.need_linv[MP_SINGLE]) launch_convert(c, st, MP_DOUBLE, linv64, nb, MP_SINGLE, linvS, nb, nb, nb);
+        if (L.need_linv[MP_SINGLE])
+            launch_convert(c, st, MP_DOUBLE, linv64, nb, MP_SINGLE, WL.linvS(t.work, lg), nb, nb, nb);
         // the tile column has its update from step k-1
         if (before_trsm) MP_CUDA(cudaStreamWaitEvent(st, before_trsm, 0));
         trsm_part(k, 0, st);
@@ -716,7 +746,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     auto issue_all = [&]() {
         MP_CUDA(cudaMemsetAsync(dinfo, 0xFF, sizeof(int64_t), s));  // -1: no failure
         // Linv's strictly upper part stays zero for the whole factorization
-        MP_CUDA(cudaMemsetAsync(linv64, 0, nn * sizeof(double), s));
+        for (int g = 0; g < 2; ++g) MP_CUDA(cudaMemsetAsync(WL.linv64(t.work, g), 0, nn * sizeof(double), s));
         // ---- issue.  Per step k, three streams:
         //   s   : wait panel k; bulk conversions of panel k; update of everything
         //         but tile column k+1 (bulk); write tile column k back
@@ -832,6 +862,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         if (g) cudaGraphDestroy(g);
         if (ok) {
             t.graph_launches = c->launches - l0;
+            t.graph_scr_gen = c->scr_gen;
             MP_CUDA(cudaGraphLaunch(t.graph, s));
         } else {  // not capturable here: stay eager for this tile
             (void)cudaGetLastError();
@@ -1035,6 +1066,7 @@ mp_status mp_tile_create(mp_ctx ctx, int64_t rows, int64_t cols, int64_t rpt, in
                          const int* precisions, mp_tile* out) {
     MP_API_BEGIN
     if (!ctx || !out || !precisions) fail(MP_INVALID_PARAM, "null argument");
+    bind_device(ctx);
     *out = tile_new(ctx, nullptr, rows, cols, rpt, cpt, precisions);
     MP_API_END
 }
@@ -1045,6 +1077,7 @@ mp_status mp_tile_create_dist(mp_ctx ctx, mp_dist dist, int64_t n, int64_t tile,
                               mp_tile* out) {
     MP_API_BEGIN
     if (!ctx || !dist || !out || !precisions) fail(MP_INVALID_PARAM, "null argument");
+    bind_device(ctx);
     if (dist->ctx != static_cast<Ctx*>(ctx)) fail(MP_INVALID_PARAM, "dist belongs to another context");
     *out = tile_new(ctx, dist, n, n, tile, tile, precisions);
     MP_API_END
@@ -1122,6 +1155,42 @@ mp_status mp_tile_get_values(mp_tile t, double* host) {
                                 cudaMemcpyDeviceToHost, c->stream));
         MP_CUDA(cudaStreamSynchronize(c->stream));
     }
+    MP_API_END
+}
+
+// Selected rows of the whole matrix, widened to double, row-major
+// (count x cols, out[q * cols + c]); tiles this rank does not store read as
+// zeros.  Used to check factors too large to download (sampled residuals).
+mp_status mp_tile_get_rows(mp_tile t, const int64_t* rows, int64_t count, double* host) {
+    MP_API_BEGIN
+    mp_tile_s& x = T_(t);
+    if (count < 0 || (count > 0 && (!rows || !host))) fail(MP_INVALID_PARAM, "get_rows: null argument");
+    if (count == 0) return MP_OK;
+    if (x.br != x.bc) fail(MP_SHAPE_MISMATCH, "get_rows: square tiles required");
+    for (int64_t q = 0; q < count; ++q)
+        if (rows[q] < 0 || rows[q] >= x.rows) fail(MP_INDEX_OUT_OF_RANGE, "get_rows: row index out of range");
+    Ctx* c = x.ctx;
+    const size_t out_bytes = static_cast<size_t>(count) * x.cols * sizeof(double);
+    std::vector<RowItem> items;
+    items.reserve(static_cast<size_t>(count) * x.tc);
+    char* scr = static_cast<char*>(c->ensure_scratch(out_bytes + 256 + count * x.tc * sizeof(RowItem), 1));
+    double* dout = reinterpret_cast<double*>(scr);
+    RowItem* dit = reinterpret_cast<RowItem*>(scr + (out_bytes + 255) / 256 * 256);
+    MP_CUDA(cudaMemsetAsync(dout, 0, out_bytes, c->stream));
+    for (int64_t q = 0; q < count; ++q) {
+        const int64_t i = rows[q] / x.br, r = rows[q] % x.br;
+        for (int64_t j = 0; j < x.tc; ++j)
+            if (x.has(i, j))
+                items.push_back(RowItem{x.ptr(i, j), dout + q * x.cols + j * x.bc, static_cast<int32_t>(r),
+                                        static_cast<int32_t>(x.p(i, j))});
+    }
+    if (!items.empty()) {
+        MP_CUDA(cudaMemcpyAsync(dit, items.data(), items.size() * sizeof(RowItem), cudaMemcpyHostToDevice,
+                                c->stream));
+        launch_gather_rows(c, c->stream, dit, static_cast<int64_t>(items.size()), x.br, 1);
+    }
+    MP_CUDA(cudaMemcpyAsync(host, dout, out_bytes, cudaMemcpyDeviceToHost, c->stream));
+    MP_CUDA(cudaStreamSynchronize(c->stream));
     MP_API_END
 }
 

@@ -445,6 +445,16 @@ class MPCRTile:
         check(lib().mp_tile_get_values(self.h, out.ctypes.data_as(C.c_void_p)))
         return out
 
+    def get_rows(self, rows) -> np.ndarray:
+        """Selected rows (0-based) of the whole matrix as doubles, shape
+        (len(rows), cols); tiles stored on other ranks read as zeros."""
+        _, cols, *_ = self.info()
+        r = np.ascontiguousarray(rows, dtype=np.int64)
+        out = np.empty((r.size, cols))
+        check(lib().mp_tile_get_rows(self.h, r.ctypes.data_as(C.c_void_p), r.size,
+                                     out.ctypes.data_as(C.c_void_p)))
+        return out
+
     def owns(self, i: int, j: int) -> bool:
         """True if tile (i, j) (0-based) is stored by this rank."""
         return bool(lib().mp_tile_owns(self.h, i, j))

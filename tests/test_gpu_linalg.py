@@ -321,6 +321,31 @@ def test_gemm_half_to_double_int8_digits(ctx, rng, ta, tb):
         assert err.max() <= 16 * 2.0 ** -53, (m, n, k, float(err.max()))
 
 
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, True)])
+def test_gemm_half_to_double_large_k_chunks(ctx, ta, tb):
+    """K beyond the int32-exact limit of one digit group (6 K 64^2 < 2^31):
+    the INT8-digit path splits K into OZ_MAX_K = 65536 chunks summed in FP64.
+    All-positive near-maximal digits make every group sum as large as it can
+    get; an unchunked K = 2^19 + 96 would overflow the single-pair group."""
+    import paper_2406_02701_b200 as mp
+
+    m, n, k = 64, 32, (1 << 19) + 96
+    r = np.random.default_rng(3)
+    A = (1.0 + r.integers(0, 1024, (m, k)) / 1024.0).astype(np.float16).astype(np.float64)
+    B = (1.0 + r.integers(0, 1024, (k, n)) / 1024.0).astype(np.float16).astype(np.float64)
+    A[:, 0] = 1.9990234375  # row maxima just below 2: leading digits near 64
+    A_st = np.asfortranarray(A.T) if ta else A
+    B_st = np.asfortranarray(B.T) if tb else B
+    da = mp.MPArray.from_numpy(A_st, mp.Precision.Half, ctx)
+    db = mp.MPArray.from_numpy(B_st, mp.Precision.Half, ctx)
+    dc = mp.MPArray.zeros_matrix(m, n, mp.Precision.Double, ctx)
+    mp.linalg.gemm(da, db, dc, ta, tb, 1.0, 0.0)
+    got = dc.to_numpy()
+    exact = A.astype(np.longdouble) @ B.astype(np.longdouble)
+    err = np.abs(got.astype(np.longdouble) - exact) / exact
+    assert err.max() <= 16 * 2.0 ** -53, float(err.max())
+
+
 def test_gemm_half_to_double_nonfinite(ctx):
     """Inf/NaN in an FP16 operand row propagate as NaN to that output row."""
     import paper_2406_02701_b200 as mp
