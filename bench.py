@@ -481,7 +481,7 @@ def check_factor(args, A, g, x, y, n, nb, ctx, world, grid):
         mp.tile_chol(sub)
         same = verify.leading_rows_equal(Lr[np.searchsorted(rows, lead)], sub.get_rows(lead))
         sub.close()
-    return {"sampled_backward_error": res["normwise"], "componentwise_backward_error": res["componentwise"],
+    return {"sampled_backward_error": res["normwise"], "max_entry_backward_error": res["max_entry"],
             "sample_rows": res["rows"], "sample_entries": res["entries"],
             "leading_block": m, "leading_block_bitwise_equal": same,
             "check_seconds": time.perf_counter() - t0,

@@ -93,6 +93,10 @@ typedef enum {
 mp_status mp_prof_enable(mp_ctx ctx, int enable);
 mp_status mp_prof_reset(mp_ctx ctx);
 mp_status mp_prof_query(mp_ctx ctx, int cls, double* ms, int64_t* launches, double* work);
+/* While profiling: INT8 digit-pair MMAs the FP64-from-FP16 (Ozaki) kernel
+ * issued, summed over its 128 x 128 output tiles (pair_mmas / tiles = mean
+ * digit products per FP64 tile product), since the last mp_prof_reset. */
+mp_status mp_prof_digit_products(mp_ctx ctx, int64_t* pair_mmas, int64_t* tiles);
 /* Timeline capture (profiling must be enabled): every timed launch's start
  * and end in ms relative to the moment tracing was enabled, with its stream
  * (0 = context stream, 1 = critical-path stream); dumped as CSV. */

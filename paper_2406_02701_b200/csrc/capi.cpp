@@ -230,6 +230,7 @@ mp_status mp_ctx_destroy(mp_ctx ctx) {
     for (auto e : ctx->prof.pool) cudaEventDestroy(e);
     for (void* p : ctx->scr)
         if (p) cudaFree(p);
+    if (ctx->prof.dev_stats) cudaFree(ctx->prof.dev_stats);
     for (auto& s : ctx->aux) cudaStreamDestroy(s);
     cudaStreamDestroy(ctx->hi);
     cudaStreamDestroy(ctx->hi2);
@@ -262,7 +263,26 @@ mp_status mp_ctx_synchronize(mp_ctx ctx) {
 
 mp_status mp_prof_enable(mp_ctx ctx, int enable) {
     MP_API_BEGIN
-    C_(ctx)->prof.enabled = enable != 0;
+    Ctx* c = C_(ctx);
+    if (enable && !c->prof.dev_stats) {
+        MP_CUDA(cudaMalloc(&c->prof.dev_stats, 64));
+        MP_CUDA(cudaMemsetAsync(c->prof.dev_stats, 0, 64, c->stream));
+    }
+    c->prof.enabled = enable != 0;
+    MP_API_END
+}
+
+mp_status mp_prof_digit_products(mp_ctx ctx, int64_t* pair_mmas, int64_t* tiles) {
+    MP_API_BEGIN
+    Ctx* c = C_(ctx);
+    unsigned long long h[2] = {0, 0};
+    if (c->prof.dev_stats) {
+        MP_CUDA(cudaStreamSynchronize(c->stream));
+        MP_CUDA(cudaDeviceSynchronize());
+        MP_CUDA(cudaMemcpy(h, c->prof.dev_stats, sizeof(h), cudaMemcpyDeviceToHost));
+    }
+    if (pair_mmas) *pair_mmas = static_cast<int64_t>(h[0]);
+    if (tiles) *tiles = static_cast<int64_t>(h[1]);
     MP_API_END
 }
 
@@ -274,6 +294,10 @@ mp_status mp_prof_reset(mp_ctx ctx) {
         c->prof.ms[i] = 0;
         c->prof.launches[i] = 0;
         c->prof.work[i] = 0;
+    }
+    if (c->prof.dev_stats) {
+        MP_CUDA(cudaDeviceSynchronize());
+        MP_CUDA(cudaMemset(c->prof.dev_stats, 0, 64));
     }
     MP_API_END
 }

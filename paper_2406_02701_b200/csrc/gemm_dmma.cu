@@ -184,7 +184,7 @@ __device__ __forceinline__ double sm_get(const double* sm, bool mn_contig, int m
     return mn_contig ? sm[k * DCfg<BT>::SM_ + mn] : sm[mn * DCfg<BT>::SK_ + k];
 }
 
-template <int BT, typename TI>
+template <int BT, typename TA, typename TB, typename TC>
 __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 2 : 1) dmma_gemm_kernel(DmmaArgs g) {
     using CF = DCfg<BT>;
     constexpr int BMd = BT, BNd = BT, SLAB = CF::SLAB, WTN = CF::WTN, WN = BT / WTN, NJ = WTN / 8;
@@ -200,21 +200,23 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 2 : 1) dmma_gemm_ke
     const int64_t m0 = static_cast<int64_t>(S > 1 ? blockIdx.x / S : blockIdx.x) * BMd;
     const int64_t n0 = static_cast<int64_t>(blockIdx.y) * BNd;
     if (pr.lower_only && m0 + BMd - 1 < n0) return;  // the whole cluster leaves together
-    const int64_t kchunk = S > 1 ? ((g.k + S - 1) / S + BKd - 1) / BKd * BKd : g.k;
-    const int64_t kbeg = rank * kchunk, kend = std::min<int64_t>(g.k, kbeg + kchunk);
-    constexpr bool WIDE = std::is_same<TI, double>::value;
-    const TI* __restrict__ A = static_cast<const TI*>(pr.A);
-    const TI* __restrict__ B = static_cast<const TI*>(pr.B);
-    double* __restrict__ C = static_cast<double*>(pr.C);
+    const int64_t kext = g.k_tri ? std::min<int64_t>(g.k, n0 + BNd) : g.k;
+    const int64_t kchunk = S > 1 ? ((kext + S - 1) / S + BKd - 1) / BKd * BKd : kext;
+    const int64_t kbeg = rank * kchunk, kend = std::min<int64_t>(kext, kbeg + kchunk);
+    constexpr bool WA = std::is_same<TA, double>::value, WB = std::is_same<TB, double>::value;
+    constexpr bool ANY_WIDE = WA || WB;
+    const TA* __restrict__ A = static_cast<const TA*>(pr.A);
+    const TB* __restrict__ B = static_cast<const TB*>(pr.B);
+    TC* __restrict__ C = static_cast<TC*>(pr.C);
     const bool a_mn = !g.ta;  // op(A) = A: M contiguous
     const bool b_mn = g.tb;   // op(B) = B^T: N contiguous
     // vector copies (16 bytes of FP64, 4 narrow elements) need aligned
     // strides/offsets and extents along the contiguous index
-    constexpr int VE = WIDE ? 2 : 4;
-    const bool va = (g.lda % VE == 0) && ((reinterpret_cast<uintptr_t>(A) & (VE * sizeof(TI) - 1)) == 0) &&
-                    (a_mn ? g.m % VE == 0 : g.k % VE == 0);
-    const bool vb = (g.ldb % VE == 0) && ((reinterpret_cast<uintptr_t>(B) & (VE * sizeof(TI) - 1)) == 0) &&
-                    (b_mn ? g.n % VE == 0 : g.k % VE == 0);
+    constexpr int VA = WA ? 2 : 4, VB = WB ? 2 : 4;
+    const bool va = (g.lda % VA == 0) && ((reinterpret_cast<uintptr_t>(A) & (VA * sizeof(TA) - 1)) == 0) &&
+                    (a_mn ? g.m % VA == 0 : g.k % VA == 0);
+    const bool vb = (g.ldb % VB == 0) && ((reinterpret_cast<uintptr_t>(B) & (VB * sizeof(TB) - 1)) == 0) &&
+                    (b_mn ? g.n % VB == 0 : g.k % VB == 0);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int wm = (warp / WN) * 32, wn = (warp % WN) * WTN;
@@ -230,24 +232,23 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 2 : 1) dmma_gemm_ke
     const int nk = kend > kbeg ? static_cast<int>((kend - kbeg + BKd - 1) / BKd) : 0;
     auto stage_a = [&](int s) { return dsm + s * 2 * SLAB; };
     auto stage_b = [&](int s) { return dsm + s * 2 * SLAB + SLAB; };
-    [[maybe_unused]] NarrowSlab<BT, TI> ra, rb;
+    [[maybe_unused]] NarrowSlab<BT, TA> ra;
+    [[maybe_unused]] NarrowSlab<BT, TB> rb;
     auto issue = [&](int kb) {
         const int s = kb % NST;
-        if constexpr (WIDE) {
-            load_slab<BT>(stage_a(s), reinterpret_cast<const double*>(A), g.lda, a_mn, m0, g.m,
-                          kbeg + static_cast<int64_t>(kb) * BKd, kend, va);
-            load_slab<BT>(stage_b(s), reinterpret_cast<const double*>(B), g.ldb, b_mn, n0, g.n,
-                          kbeg + static_cast<int64_t>(kb) * BKd, kend, vb);
-        } else {
-            ra.load(A, g.lda, a_mn, m0, g.m, kbeg + static_cast<int64_t>(kb) * BKd, kend, va);
-            rb.load(B, g.ldb, b_mn, n0, g.n, kbeg + static_cast<int64_t>(kb) * BKd, kend, vb);
-        }
+        const int64_t k0 = kbeg + static_cast<int64_t>(kb) * BKd;
+        if constexpr (WA)
+            load_slab<BT>(stage_a(s), reinterpret_cast<const double*>(A), g.lda, a_mn, m0, g.m, k0, kend, va);
+        else
+            ra.load(A, g.lda, a_mn, m0, g.m, k0, kend, va);
+        if constexpr (WB)
+            load_slab<BT>(stage_b(s), reinterpret_cast<const double*>(B), g.ldb, b_mn, n0, g.n, k0, kend, vb);
+        else
+            rb.load(B, g.ldb, b_mn, n0, g.n, k0, kend, vb);
     };
-    auto land = [&](int kb) {  // narrow path: registers -> shared (FP64)
-        if constexpr (!WIDE) {
-            ra.store(stage_a(kb % NST), a_mn);
-            rb.store(stage_b(kb % NST), b_mn);
-        }
+    auto land = [&](int kb) {  // narrow operands: registers -> shared (FP64)
+        if constexpr (!WA) ra.store(stage_a(kb % NST), a_mn);
+        if constexpr (!WB) rb.store(stage_b(kb % NST), b_mn);
     };
 #pragma unroll
     for (int s = 0; s < NST - 1; ++s) {
@@ -255,14 +256,14 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 2 : 1) dmma_gemm_ke
             issue(s);
             land(s);
         }
-        if constexpr (WIDE) cp_commit();
+        if constexpr (ANY_WIDE) cp_commit();
     }
     for (int kb = 0; kb < nk; ++kb) {
-        if constexpr (WIDE) cp_wait<NST - 2>();
+        if constexpr (ANY_WIDE) cp_wait<NST - 2>();
         __syncthreads();
         const bool next = kb + NST - 1 < nk;
         if (next) issue(kb + NST - 1);
-        if constexpr (WIDE) cp_commit();
+        if constexpr (ANY_WIDE) cp_commit();
         const double* sa = stage_a(kb % NST);
         const double* sb = stage_b(kb % NST);
 #pragma unroll
@@ -289,7 +290,7 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 2 : 1) dmma_gemm_ke
         }
         if (next) land(kb + NST - 1);
     }
-    if constexpr (WIDE) cp_wait<0>();
+    if constexpr (ANY_WIDE) cp_wait<0>();
     if (S > 1) {
         // every CTA's stages are free once all have left the main loop
         asm volatile("barrier.cluster.arrive.release.aligned; barrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 2 : 1) dmma_gemm_ke
                 const int64_t gm = m0 + wm + i * 16 + gq + 8 * (v >> 1);
                 const int64_t gn = n0 + wn + j * 8 + 2 * tq + (v & 1);
                 const bool ok = gm < g.m && gn < g.n && !(pr.lower_only && gm < gn);
-                cold[j][v] = (ok && beta != 0.0) ? C[gn * g.ldc + gm] : 0.0;
+                cold[j][v] = (ok && beta != 0.0) ? static_cast<double>(C[gn * g.ldc + gm]) : 0.0;
             }
 #pragma unroll
         for (int j = 0; j < NJ; ++j)
@@ -346,19 +347,22 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 2 : 1) dmma_gemm_ke
                 if (gm < g.m && gn < g.n && !(pr.lower_only && gm < gn)) {
                     double r = alpha * acc[i][j][v];
                     if (beta != 0.0) r += beta * cold[j][v];
-                    C[gn * g.ldc + gm] = r;
+                    if constexpr (std::is_same<TC, double>::value)
+                        C[gn * g.ldc + gm] = r;
+                    else
+                        C[gn * g.ldc + gm] = d2f(r);  // one rounding of the FP64 result
                 }
             }
     }
 }
 
 
-template <int BT, typename TI>
+template <int BT, typename TA, typename TB, typename TC>
 void launch_bt(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count) {
     using CF = DCfg<BT>;
     static unsigned long long configured = 0;  // per-device bitmask
     if (first_on_device(configured)) {
-        MP_CUDA(cudaFuncSetAttribute(dmma_gemm_kernel<BT, TI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        MP_CUDA(cudaFuncSetAttribute(dmma_gemm_kernel<BT, TA, TB, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      std::max(CF::SMEM, 160 * 1024)));
     }
     const int smem = g.exclusive ? std::max(CF::SMEM, 160 * 1024) : CF::SMEM;
@@ -366,7 +370,7 @@ void launch_bt(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count) {
     const dim3 grid(static_cast<unsigned>((g.m + BT - 1) / BT) * S, static_cast<unsigned>((g.n + BT - 1) / BT),
                     static_cast<unsigned>(g.problems ? count : 1));
     if (S == 1) {
-        dmma_gemm_kernel<BT, TI><<<grid, CF::NTHR, smem, s>>>(g);
+        dmma_gemm_kernel<BT, TA, TB, TC><<<grid, CF::NTHR, smem, s>>>(g);
         return;
     }
     cudaLaunchConfig_t cfg = {};
@@ -381,15 +385,15 @@ void launch_bt(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    MP_CUDA(cudaLaunchKernelEx(&cfg, dmma_gemm_kernel<BT, TI>, g));
+    MP_CUDA(cudaLaunchKernelEx(&cfg, dmma_gemm_kernel<BT, TA, TB, TC>, g));
 }
 
-template <typename TI>
+template <typename TA, typename TB, typename TC>
 void launch_ti(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count, bool small) {
     if (small)
-        launch_bt<64, TI>(ctx, s, g, count);
+        launch_bt<64, TA, TB, TC>(ctx, s, g, count);
     else
-        launch_bt<128, TI>(ctx, s, g, count);
+        launch_bt<128, TA, TB, TC>(ctx, s, g, count);
 }
 
 }  // namespace
@@ -400,6 +404,7 @@ void launch_dmma_gemm(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count
     const int64_t nprob = g.problems ? count : 1;
     const int64_t tm = (g.m + 127) / 128, tn = (g.n + 127) / 128;
     const int64_t ctas = nprob * (g.lower_only ? tm * (tn + 1) / 2 : tm * tn);  // lists live on the device
+    // (k_tri: the K work per CTA shrinks, the CTA count does not)
     const bool small = ctas < ctx->sm_count;
     DmmaArgs h = g;
     h.ksplit = 1;
@@ -414,12 +419,16 @@ void launch_dmma_gemm(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count
                 break;
             }
     }
-    if (g.pin == MP_HALF)
-        launch_ti<uint16_t>(ctx, s, h, count, small);
+    if (g.b_wide && g.pin == MP_SINGLE && g.pout == MP_SINGLE)  // FP32 tile x FP64 Linv^T (TRSM)
+        launch_ti<float, double, float>(ctx, s, h, count, small);
+    else if (g.b_wide || g.pout != MP_DOUBLE)
+        fail(MP_INTERNAL_ERROR, "dmma: unsupported operand/output precision combination");
+    else if (g.pin == MP_HALF)
+        launch_ti<uint16_t, uint16_t, double>(ctx, s, h, count, small);
     else if (g.pin == MP_SINGLE)
-        launch_ti<float>(ctx, s, h, count, small);
+        launch_ti<float, float, double>(ctx, s, h, count, small);
     else
-        launch_ti<double>(ctx, s, h, count, small);
+        launch_ti<double, double, double>(ctx, s, h, count, small);
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());
 }

@@ -19,9 +19,14 @@ struct DmmaArgs {
     int64_t ldc;
     bool lower_only;
     const TileProblem* problems;  // grouped launch when non-null
-    mp_precision pin = MP_DOUBLE;  // operand storage precision
+    mp_precision pin = MP_DOUBLE;  // operand storage precision (A, and B unless b_wide)
     bool exclusive = false;        // reserve the SM (latency-critical launches)
     int ksplit = 1;                // K split over a thread-block cluster (set by the launcher)
+    bool b_wide = false;           // B is FP64 whatever pin is
+    mp_precision pout = MP_DOUBLE;  // C storage: FP64, or FP32 (rounded once, RNE)
+    // op(B)[k][n] == 0 for k > n (B = L^T of a lower-triangular L, the TRSM
+    // as X = A L^-T): each CTA stops its K loop at its last column
+    bool k_tri = false;
 };
 
 void launch_dmma_gemm(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count);

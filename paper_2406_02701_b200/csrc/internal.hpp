@@ -65,6 +65,9 @@ struct Prof {
     double ms[MP_PROF_NUM_CLASSES] = {};
     int64_t launches[MP_PROF_NUM_CLASSES] = {};
     double work[MP_PROF_NUM_CLASSES] = {};
+    // device counters while profiling: [0] INT8 digit-pair MMAs issued per
+    // 128-row k-extent, summed over output tiles; [1] those output tiles
+    unsigned long long* dev_stats = nullptr;
 };
 
 struct Ctx {

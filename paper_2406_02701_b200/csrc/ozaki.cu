@@ -74,6 +74,7 @@ struct Params {
     // CTA c takes units (c / lanes) * lanes * per + c % lanes + r * lanes,
     // r < per: the CTAs resident together sweep one contiguous chunk
     int32_t lanes, per;
+    unsigned long long* stats;  // profiling: [0] += sa*sb per output tile, [1] += 1 (or nullptr)
 };
 
 // Digit counts of a problem: pairs (dp, dq) with dp <= sa, dq <= sb; groups
@@ -208,6 +209,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                 if (skip_tile(pr, m0, n0)) continue;
                 int sa, sb;
                 digits_of(p, pr, sa, sb);
+                if (p.stats) {
+                    atomicAdd(p.stats, static_cast<unsigned long long>(sa * sb));
+                    atomicAdd(p.stats + 1, 1ull);
+                }
                 for (int g = sa + sb; g >= 2; g -= 2) {
                     const bool two = g - 1 >= 2;
                     // accumulators of groups g and g-1 (the next one in the rotation)
@@ -663,6 +668,7 @@ void launch_oz_gemm(Ctx* ctx, cudaStream_t s, const OzGemm& g) {
     p.rexp_stride_b = g.rexp_stride_b;
     p.ndig_a = g.ndig_a;
     p.ndig_b = g.ndig_b;
+    p.stats = ctx->prof.enabled ? ctx->prof.dev_stats : nullptr;
     const int64_t total = static_cast<int64_t>(p.nprob) * p.mblocks * p.nblocks;
     ProfScope ps(ctx, MP_PROF_GEMM_F64, s,
                  2.0 * static_cast<double>(g.m) * g.n * g.k * p.nprob * (g.lower_only ? 0.5 : 1.0));

@@ -29,6 +29,7 @@
 
 #include "batch.hpp"
 #include "dist.hpp"
+#include "gemm_dmma.hpp"
 #include "gemm_tc.hpp"
 #include "ozaki.hpp"
 #include "internal.hpp"
@@ -297,7 +298,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         const char* e = getenv("MPCR_TRSM_SPLIT");
         return !(e && e[0] == '0');
     }();
-    const bool tsplit = tsplit_env && la && P * Q == 1;
+    // (also without lookahead, on one stream: the same launches, serialised)
+    const bool tsplit = tsplit_env && NT > 1 && P * Q == 1;
     std::vector<StepAcc> acc(NT);
     std::vector<StepLists> steps(NT);
     const size_t nn0 = static_cast<size_t>(nb) * nb;
@@ -358,8 +360,9 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                     // A = matrix tile (i,k) in the FP16 slab, C = panel16[i]
                     A.trsm_tc[hb].push_back(TcProblem{static_cast<int32_t>(t.slot[k * NT + i]), 0,
                                                       static_cast<int32_t>(i), 0});
-                else
-                    A.trsm_p[hb][q].push_back(TileProblem{t.ptr(i, k), linv(q, k), pan(q, i, k), 0, 0});
+                else  // FP32 / FP64 tiles (and FP16 when nb % 8): the FP64 inverse
+                    A.trsm_p[hb][q].push_back(TileProblem{t.ptr(i, k), linv(q == MP_HALF ? MP_HALF : MP_DOUBLE, k),
+                                                          pan(q, i, k), 0, 0});
                 A.wb[q].push_back(CopyItem{pan(q, i, k), t.ptr(i, k)});
                 if (P * Q == 1) consumers(k, i, A);
                 break;
@@ -551,17 +554,25 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         }
         for (int q = 0; q < 3; ++q) {
             if (!L.n_trsm_p[hb][q]) continue;
-            if (q == MP_SINGLE && tc_ok) {
-                // the few FP32 panel tiles: 3xTF32 tcgen05 GEMM per tile
-                for (const TileProblem& pr : acc[k].trsm_p[hb][q]) {
-                    GemmDesc g{MP_SINGLE, MP_SINGLE, MP_SINGLE, false, true, nb, nb, nb, 1.0, 0.0,
-                               pr.A, nb, pr.B, nb, pr.C, nb};
-                    launch_gemm(c, st, g);
-                }
+            const auto* probs = reinterpret_cast<const TileProblem*>(dl + L.trsm_p[hb][q]);
+            if (q != MP_HALF) {
+                // FP32 / FP64 panel tiles: one grouped DMMA launch, A_ik (FP32
+                // widened exactly on load, or FP64) times the FP64 inverse, each
+                // CTA's K loop cut at the triangle; FP32 tiles rounded once from
+                // the FP64 result.  (An explicit inverse applied in TF32/FP32
+                // carries cond(L_kk) * u_32 into the panel; in FP64 it does not.)
+                DmmaArgs d{false, true, nb, nb, nb, 1.0, 0.0, nullptr, nb, nullptr, nb, nullptr, nb, false,
+                           probs, (mp_precision)q};
+                d.pout = (mp_precision)q;
+                d.k_tri = true;
+                d.b_wide = q == MP_SINGLE;
+                d.exclusive = hb == 0;  // the head tile is on the critical path
+                ProfScope ps(c, MP_PROF_TRSM, st, static_cast<double>(nb) * nb * nb * L.n_trsm_p[hb][q]);
+                launch_dmma_gemm(c, st, d, L.n_trsm_p[hb][q]);
                 continue;
             }
-            GroupedGemm g{(mp_precision)q, (mp_precision)q, true, nb, nb, nb, nb, nb, nb, 1.0, 0.0,
-                          reinterpret_cast<const TileProblem*>(dl + L.trsm_p[hb][q]), L.n_trsm_p[hb][q]};
+            GroupedGemm g{(mp_precision)q, (mp_precision)q, true, nb, nb, nb, nb, nb, nb, 1.0, 0.0, probs,
+                          L.n_trsm_p[hb][q]};
             launch_grouped_gemm(c, st, g);
         }
     };
@@ -617,8 +628,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             else
                 launch_convert(c, st, MP_DOUBLE, linv64, nb, MP_HALF, WL.linvH(t.work, lg), nb, nb, nb);
         }
-        if (L.need_linv[MP_SINGLE])
-            launch_convert(c, st, MP_DOUBLE, linv64, nb, MP_SINGLE, WL.linvS(t.work, lg), nb, nb, nb);
+
         // the tile column has its update from step k-1
         if (before_trsm) MP_CUDA(cudaStreamWaitEvent(st, before_trsm, 0));
         trsm_part(k, 0, st);

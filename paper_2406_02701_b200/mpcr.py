@@ -117,6 +117,13 @@ class Context:
         check(lib().mp_prof_query(self.h, cls, C.byref(ms), C.byref(n), C.byref(w)))
         return ms.value, n.value, w.value
 
+    def prof_digit_products(self):
+        """(INT8 digit-pair MMAs issued, FP64 output tiles) of the Ozaki kernel
+        since the last prof_reset (profiling runs only)."""
+        a, b = C.c_int64(), C.c_int64()
+        check(lib().mp_prof_digit_products(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def launch_count(self) -> int:
         n = C.c_int64()
         check(lib().mp_launch_count(self.h, C.byref(n)))
