@@ -102,6 +102,56 @@ def flops_by_precision(nt, nb, g):
     return f
 
 
+PIPES = ("tc_f16", "int8_digits", "dmma")
+
+
+def flops_by_pipe(nt, nb, g):
+    """The same algorithmic flops (SURVEY §8d counts) split by the pipe the
+    scheduler (csrc/tile.cpp) runs each task on:
+      tc_f16      FP16-destination GEMM/SYRK, FP32-destination updates whose two
+                  panel tiles are FP16 (exact products, FP32 accumulate), the
+                  FP16 panel TRSM (tcgen05 kind::f16);
+      int8_digits FP64-destination updates with two FP16 panel tiles (exact
+                  INT8 digit products, tcgen05 kind::i8);
+      dmma        every other FP32/FP64-destination update (panel tiles widened
+                  exactly, FP64 accumulate), the FP32 and FP64 panel TRSM,
+                  POTRF (mma.sync .f64)."""
+    f = dict.fromkeys(PIPES, 0.0)
+    b3 = float(nb) ** 3
+    for k in range(nt):
+        f["dmma"] += b3 / 3
+        for i in range(k + 1, nt):
+            f["tc_f16" if g[i, k] == 0 else "dmma"] += b3
+            for j in range(k + 1, i + 1):
+                w = b3 if i == j else 2 * b3
+                d, pa, pb = g[i, j], g[i, k], g[j, k]
+                if d == 0:
+                    f["tc_f16"] += w
+                elif d == 1:
+                    f["tc_f16" if pa == 0 and pb == 0 else "dmma"] += w
+                else:
+                    f["int8_digits" if pa == 0 and pb == 0 else "dmma"] += w
+    return f
+
+
+def pipe_peaks(pk):
+    """Per-pipe sustained peaks (TFLOP/s; INT8 in TOPS) for the blended
+    roofline: the measured sustained BF16 GEMM rate (MEASURED_PEAKS.json) is
+    the FP16 pipe; INT8 scales it by the tcgen05 kind::i8 / kind::f16 issue-rate
+    ratio measured by tools/micro/tc_peak.cu (profiles/r02_pipe_peaks.json,
+    clocks recorded); DMMA is the measured FP64 peak
+    (tools/micro/fp64_peak.cu, same file)."""
+    f16 = pk["bf16_tflops_sustained"]
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_pipe_peaks.json")) as fh:
+            mp = json.load(fh)
+        src = "profiles/r02_pipe_peaks.json"
+    except (OSError, ValueError):
+        mp, src = {"f16_burst": 1.0, "tf32_burst": 0.5, "i8_burst": 2.0, "dmma_tflops": 37.1}, "nominal ratios"
+    r = {"tc_f16": f16, "int8_tops": f16 * mp["i8_burst"] / mp["f16_burst"], "dmma": mp["dmma_tflops"]}
+    return r, src
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -328,6 +378,7 @@ def run_chol(args, world, rank, local):
     pe[1].record(stream)
     ctx.synchronize()
     prof_step_ms = pe[0].elapsed_time(pe[1])
+    prof_pairs = ctx.prof_digit_products()
     ctx.prof_enable(False)
     cls_names = ["gemm_f16", "gemm_f32", "gemm_f64", "potrf_trtri", "trsm", "cast", "other"]
     prof = {}
@@ -355,11 +406,14 @@ def run_chol(args, world, rank, local):
     pk, src = peaks()
     flops = n ** 3 / 3
     fp = flops_by_precision(nt, nb, g)
+    fpipe = flops_by_pipe(nt, nb, g)
     f16 = prof.get("gemm_f16")
     roof = None
     if f16:
-        # dominant kernel: tcgen05 FP16 GEMM; algorithmic flops / its event time
-        ach = f16["rate"]
+        # dominant kernel: the tcgen05 FP16 pair GEMM (trailing update, FP32 tiles
+        # fed by FP16 panels, FP16 panel TRSM); algorithmic flops of exactly
+        # those tasks (TRSM at nb^3) / the class's event-timed duration
+        ach = fpipe["tc_f16"] / world / (f16["ms"] * 1e-3) / 1e12
         peak = pk["bf16_tflops_sustained"]
         traffic, tnote = None, None
         # the ncu capture of this n's bulk launch when one is committed
@@ -377,26 +431,28 @@ def run_chol(args, world, rank, local):
             pass
         roof = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                 "frac": ach / peak, "traffic": traffic, "traffic_note": tnote,
-                "kernel": "gemm_tc2_kernel (tcgen05 kind::f16 cta_group::2, grouped trailing update + panel TRSM)",
+                "kernel": "gemm_tc2_kernel (tcgen05 kind::f16 cta_group::2: trailing update, FP32 tiles "
+                          "fed by FP16 panels, FP16 panel TRSM)",
+                "algorithmic_flops": fpipe["tc_f16"] / world,
                 "peak_source": f"{src} bf16_tflops_sustained (FP16 = BF16 tensor rate)",
                 "share_of_step": f16["ms"] / prof_step_ms}
-    # Blended roofline: every flop at the tensor-core peak of its destination
-    # tile's precision.  FP16: measured sustained BF16/FP16 rate; FP32: the
-    # 3xTF32 emulation (3 TF32 MMAs per FP32 product, TF32 = half the FP16
-    # rate); FP64: the measured DMMA peak (tools/micro/fp64_peak.cu, 37.1).
-    # The FP64 tiles fed by FP16 panels run as exact INT8 digit products and
-    # can beat that leg; the FP32-SIMT basis (74 TF) is kept for reference.
-    fp32_3xtf32 = pk["bf16_tflops_sustained"] / 2 / 3
-    peaks_used = {"fp16": pk["bf16_tflops_sustained"], "fp32": fp32_3xtf32, "fp64": 37.1}
-    tmin = sum(fp[i] / (peaks_used[k] * 1e12) for i, k in enumerate(("fp16", "fp32", "fp64")))
-    tmin_simt = fp[0] / (peaks_used["fp16"] * 1e12) + fp[1] / 74e12 + fp[2] / 37.1e12
+    # Blended roofline: every algorithmic flop charged at the pipe that runs it
+    # (flops_by_pipe); the INT8-digit FP64 tiles at the INT8 rate divided by
+    # the digit-pair products the kernel actually issued (device counter).
+    pp, pp_src = pipe_peaks(pk)
+    pairs, ptiles = prof_pairs
+    avg_pairs = pairs / ptiles if ptiles else 36.0
+    t_pipe = {"tc_f16": fpipe["tc_f16"] / (pp["tc_f16"] * 1e12),
+              "int8_digits": fpipe["int8_digits"] * avg_pairs / (pp["int8_tops"] * 1e12),
+              "dmma": fpipe["dmma"] / (pp["dmma"] * 1e12)}
+    tmin = sum(t_pipe.values()) / world
     value = flops / (ms_max * 1e-3) / 1e12  # one matrix over all ranks (strong scaling)
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "mixed(f64/f32/f16 tiles; f16: tcgen05 f16 f32-acc; f32: tcgen05 f16 (f16 panels) / "
-                 "3xTF32; f64: exact INT8 digits (f16 panels) / DMMA)",
+                 "DMMA; f64: exact INT8 digits (f16 panels) / DMMA)",
         "data": "synthetic",
         "config": {"workload": f"MPCRTile mixed-precision Cholesky n={n}, tile {nb}" +
                                (f", 2D block-cyclic {grid.P}x{grid.Q}" if grid else ", 1 GPU"),
@@ -405,7 +461,7 @@ def run_chol(args, world, rank, local):
                    "covariance": f"Matern nu=0.5 range {args.range} sigma2 1 nugget {args.nugget}, "
                                  f"first {n} points of a {side}x{side} unit grid",
                    "fp32_method": "FP16 panels: tcgen05 kind::f16 (exact products, FP32 accumulate); "
-                                  "FP32 panels: 3xTF32 (tcgen05 kind::tf32)",
+                                  "FP32 panels: DMMA (widened exactly, FP64 accumulate, one rounding)",
                    "fp64_method": "FP16 panels: exact 7-bit digit slicing, tcgen05 kind::i8 (Ozaki); "
                                   "FP32/FP64 panels: DMMA",
                    "l2": "inputs 8+ GB >> 126 MB L2 (no flush needed)",
@@ -413,11 +469,15 @@ def run_chol(args, world, rank, local):
                                   if grid else "single GPU"},
         "roofline": roof,
         "blended_roofline": {"t_min_ms": tmin * 1e3, "frac": tmin / (ms_max * 1e-3),
+                             "flops_by_pipe": fpipe, "t_min_ms_by_pipe": {k: v * 1e3 / world for k, v in t_pipe.items()},
                              "flops_by_dest_precision": {"f16": fp[0], "f32": fp[1], "f64": fp[2]},
-                             "peaks_tflops": peaks_used,
-                             "frac_fp32_simt_basis": tmin_simt / (ms_max * 1e-3),
-                             "note": "fp16 = measured sustained bf16; fp32 = that / 2 / 3 (3xTF32); "
-                                     "fp64 = measured DMMA peak 37.1 (INT8-digit FP64 may exceed it)"},
+                             "peaks": {"tc_f16_tflops": pp["tc_f16"], "int8_tops": pp["int8_tops"],
+                                       "dmma_tflops": pp["dmma"]},
+                             "int8_digit_pairs_per_tile_product": avg_pairs,
+                             "peak_source": f"{src} bf16 sustained x tcgen05 kind ratios ({pp_src})",
+                             "note": "T_min = sum over pipes of algorithmic flops / that pipe's sustained peak "
+                                     "(INT8-digit FP64 tiles: flops x digit pairs issued / INT8 peak); "
+                                     "frac = T_min / step time"},
         "breakdown": {"note": "one extra eager (non-graph) factorization with per-launch event "
                               "pairs; classes overlap in time across the three streams",
                       "step_ms": prof_step_ms, "classes": prof},
@@ -445,6 +505,7 @@ def run_chol(args, world, rank, local):
                 "median_seconds": steps_s[len(steps_s) // 2],
                 "rel_frob_err": accuracy["sampled_backward_error"] if accuracy else None,
                 "tflops": value, "blended_roofline_frac": line["blended_roofline"]["frac"],
+                "roofline_frac": (line["roofline"] or {}).get("frac"),
                 "e2e_tflops": line.get("e2e", {}).get("value")}])
     ctx.synchronize()
 

@@ -239,6 +239,9 @@ mp_status mp_tile_fill_matern(mp_ctx ctx, mp_tile t, int64_t grid_side, double n
 mp_status mp_tile_fill_matern_points(mp_ctx ctx, mp_tile t, const double* host_x,
                                      const double* host_y, int64_t n, double nu, double range,
                                      double variance, double nugget);
+/* Tile-wise converted(): each tile of src rounded/widened into the precision
+ * dst holds for that tile (same grid; array.cpp:187-191 per tile). */
+mp_status mp_tile_convert(mp_ctx ctx, mp_tile dst, mp_tile src);
 /* Device copy of all tile values (identical grids and precisions). */
 mp_status mp_tile_copy(mp_ctx ctx, mp_tile dst, mp_tile src);
 /* gaussian_nll (workloads.cpp:74-87) of host vector z under the covariance

@@ -91,6 +91,7 @@ SIGNATURES = {
     "mp_tile_fill_matern": (C.c_int, [_vp, _vp, _i64, C.c_double, C.c_double, C.c_double]),
     "mp_tile_fill_matern_points": (C.c_int, [_vp, _vp, _vp, _vp, _i64, C.c_double, C.c_double,
                                              C.c_double, C.c_double]),
+    "mp_tile_convert": (C.c_int, [_vp, _vp, _vp]),
     "mp_tile_copy": (C.c_int, [_vp, _vp, _vp]),
     "mp_tile_gaussian_nll": (C.c_int, [_vp, _vp, _vp, C.c_double, C.c_double,
                                        C.POINTER(C.c_double), C.POINTER(C.c_double),

@@ -419,16 +419,39 @@ void launch_dmma_gemm(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count
                 break;
             }
     }
-    if (g.b_wide && g.pin == MP_SINGLE && g.pout == MP_SINGLE)  // FP32 tile x FP64 Linv^T (TRSM)
-        launch_ti<float, double, float>(ctx, s, h, count, small);
-    else if (g.b_wide || g.pout != MP_DOUBLE)
-        fail(MP_INTERNAL_ERROR, "dmma: unsupported operand/output precision combination");
-    else if (g.pin == MP_HALF)
-        launch_ti<uint16_t, uint16_t, double>(ctx, s, h, count, small);
-    else if (g.pin == MP_SINGLE)
-        launch_ti<float, float, double>(ctx, s, h, count, small);
-    else
-        launch_ti<double, double, double>(ctx, s, h, count, small);
+    const mp_precision pa = g.pin, pb = g.pin_b < 0 ? g.pin : static_cast<mp_precision>(g.pin_b);
+    // storage type per precision: FP16 bits, float, double
+    auto with_b = [&](auto ta, auto tc) {
+        using TA = decltype(ta);
+        using TC = decltype(tc);
+        if (pb == MP_HALF)
+            launch_ti<TA, uint16_t, TC>(ctx, s, h, count, small);
+        else if (pb == MP_SINGLE)
+            launch_ti<TA, float, TC>(ctx, s, h, count, small);
+        else
+            launch_ti<TA, double, TC>(ctx, s, h, count, small);
+    };
+    if (g.pout == MP_SINGLE) {
+        if (pa == MP_SINGLE && pb == MP_DOUBLE)  // FP32 panel tile x FP64 inverse (TRSM)
+            launch_ti<float, double, float>(ctx, s, h, count, small);
+        else if (pa == MP_DOUBLE || pb == MP_DOUBLE)
+            fail(MP_INTERNAL_ERROR, "dmma: FP32 output with an FP64 A operand is not built");
+        else if (pa == MP_HALF)
+            pb == MP_HALF ? launch_ti<uint16_t, uint16_t, float>(ctx, s, h, count, small)
+                          : launch_ti<uint16_t, float, float>(ctx, s, h, count, small);
+        else
+            pb == MP_HALF ? launch_ti<float, uint16_t, float>(ctx, s, h, count, small)
+                          : launch_ti<float, float, float>(ctx, s, h, count, small);
+    } else if (g.pout == MP_DOUBLE) {
+        if (pa == MP_HALF)
+            with_b(uint16_t{}, double{});
+        else if (pa == MP_SINGLE)
+            with_b(float{}, double{});
+        else
+            with_b(double{}, double{});
+    } else {
+        fail(MP_INTERNAL_ERROR, "dmma: FP16 output is not built");
+    }
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());
 }

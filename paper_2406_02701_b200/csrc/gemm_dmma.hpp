@@ -6,7 +6,9 @@
 namespace mpcr {
 
 // C <- alpha op(A) op(B) + beta C in FP64, column-major (dense or grouped).
-// A and B are FP64, or FP16 / FP32 storage widened exactly on load (pin).
+// A and B are FP64, or FP16 / FP32 storage widened exactly on load (each at
+// its own precision); C is FP64, or FP32 rounded once from the FP64 result
+// (FP16 / FP32 operands only, plus FP32 x FP64 for the panel TRSM).
 struct DmmaArgs {
     bool ta, tb;
     int64_t m, n, k;
@@ -19,11 +21,11 @@ struct DmmaArgs {
     int64_t ldc;
     bool lower_only;
     const TileProblem* problems;  // grouped launch when non-null
-    mp_precision pin = MP_DOUBLE;  // operand storage precision (A, and B unless b_wide)
+    mp_precision pin = MP_DOUBLE;  // operand storage precision (A, and B unless pin_b is set)
     bool exclusive = false;        // reserve the SM (latency-critical launches)
     int ksplit = 1;                // K split over a thread-block cluster (set by the launcher)
-    bool b_wide = false;           // B is FP64 whatever pin is
-    mp_precision pout = MP_DOUBLE;  // C storage: FP64, or FP32 (rounded once, RNE)
+    int pin_b = -1;                // B storage precision when it differs from A's (-1: pin)
+    mp_precision pout = MP_DOUBLE;  // C storage: FP64, or FP32 (rounded once from FP64, RNE)
     // op(B)[k][n] == 0 for k > n (B = L^T of a lower-triangular L, the TRSM
     // as X = A L^-T): each CTA stops its K loop at its last column
     bool k_tri = false;

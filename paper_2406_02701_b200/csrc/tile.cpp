@@ -46,7 +46,6 @@ struct mp_tile_s {
     int64_t nslot[3] = {0, 0, 0};
     // scheduler workspace (grown on demand)
     void* panel[3] = {nullptr, nullptr, nullptr};
-    void* split32[2] = {nullptr, nullptr};  // 3xTF32 hi/lo of the FP32 panel
     void* digits = nullptr;  // INT8 digit planes of FP16 panel tiles [2][tr][S][br][br]
     int32_t* rexp = nullptr;  // their row exponents [2][tr][br]
     int32_t* ndig = nullptr;  // digits each of them needs [2][tr]
@@ -78,8 +77,6 @@ struct mp_tile_s {
             if (slab[q]) cudaFree(slab[q]);
             if (panel[q]) cudaFree(panel[q]);
         }
-        for (void* p : split32)
-            if (p) cudaFree(p);
         if (digits) cudaFree(digits);
         if (rexp) cudaFree(rexp);
         if (ndig) cudaFree(ndig);
@@ -139,8 +136,6 @@ void ensure_panels(mp_tile_s& t) {
     for (int q = 0; q < 3; ++q)
         if (!t.panel[q])
             MP_CUDA(cudaMalloc(&t.panel[q], 2 * static_cast<size_t>(t.tr) * t.tt() * elem_bytes((mp_precision)q)));
-    for (auto& p : t.split32)
-        if (!p) MP_CUDA(cudaMalloc(&p, 2 * static_cast<size_t>(t.tr) * t.tt() * 4));
     if (!t.digits && ozaki_enabled()) {
         MP_CUDA(cudaMalloc(&t.digits, 2 * static_cast<size_t>(t.tr) * OZ_SLICES * t.tt()));
         MP_CUDA(cudaMalloc(&t.rexp, 2 * static_cast<size_t>(t.tr) * t.br * sizeof(int32_t)));
@@ -161,10 +156,14 @@ void append(std::vector<char>& buf, const std::vector<V>& v, size_t& off) {
 }
 
 // Device work lists of one trailing-update part (offsets into the list
-// buffer + counts): tcgen05 FP16, tcgen05 3xTF32, SIMT/DMMA per precision.
+// buffer + counts): tcgen05 FP16 (FP16 tiles; FP32 tiles fed by two FP16
+// panel tiles), INT8 digits (FP64 tiles fed by two FP16 panel tiles), SIMT
+// FP16 (tile sizes the tcgen05 path cannot map), and DMMA for every other
+// FP32 / FP64 tile, keyed [A panel precision][B panel precision][C: FP32, FP64]
+// with the panel tiles read natively (widened exactly on load).
 struct UpLists {
-    size_t tc = 0, tc16s = 0, tc32 = 0, p[3] = {0, 0, 0}, pn[2] = {0, 0}, oz = 0;
-    int64_t n_tc = 0, n_tc16s = 0, n_tc32 = 0, n_p[3] = {0, 0, 0}, n_pn[2] = {0, 0}, n_oz = 0;
+    size_t tc = 0, tc16s = 0, simt16 = 0, oz = 0, dm[3][3][2] = {};
+    int64_t n_tc = 0, n_tc16s = 0, n_simt16 = 0, n_oz = 0, n_dm[3][3][2] = {};
 };
 
 struct StepLists {
@@ -181,8 +180,6 @@ struct StepLists {
     // head tile's share of [0], made on the critical path right after its TRSM
     size_t cv[3][3][3] = {};
     int64_t n_cv[3][3][3] = {};
-    size_t split32[3] = {0, 0, 0};
-    int64_t n_split32[3] = {0, 0, 0};
     size_t digits[3] = {0, 0, 0};  // INT8 digit slicing of FP16 panel tiles (same split)
     int64_t n_digits[3] = {0, 0, 0};
     UpLists up[3];  // 0: tile column k+1 below the diagonal, 1: the rest, 2: tile (k+1, k+1)
@@ -245,9 +242,6 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     auto pan = [&](mp_precision q, int64_t i, int64_t k) -> void* {
         return static_cast<char*>(t.panel[q]) + ((k & 1) * NT + i) * tt * elem_bytes(q);
     };
-    auto spl = [&](int h, int64_t i, int64_t k) -> void* {
-        return static_cast<char*>(t.split32[h]) + ((k & 1) * NT + i) * tt * 4;
-    };
 
     // ---- host plan: the rank's action list (dist.hpp) turned into grouped
     //      per-step work lists (single GPU: P = Q = 1, no broadcasts) --------
@@ -255,10 +249,10 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     std::vector<int> pgrid(t.prec.begin(), t.prec.end());
     const auto sched = dist_schedule(rank, P, Q, NT, pgrid.data());
     struct UpAcc {
-        std::vector<TcProblem> tc, tc16s, tc32;
-        std::vector<TileProblem> p[3];
-        std::vector<TileProblem> pn[2];  // FP64 tiles fed by FP16 / FP32 panels directly
-        std::vector<OzProblem> oz;       // FP64 tiles fed by FP16 panels: INT8 digit products
+        std::vector<TcProblem> tc, tc16s;
+        std::vector<TileProblem> simt16;
+        std::vector<OzProblem> oz;           // FP64 tiles fed by FP16 panels: INT8 digit products
+        std::vector<TileProblem> dm[3][3][2];  // DMMA, native panel precisions
     };
     // FP32 tiles whose two panel tiles are both FP16: the FP16 tensor-core
     // GEMM with an FP32 accumulator/output (exact products; what 3xTF32
@@ -266,12 +260,19 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     auto half_into_single = [&](int64_t i, int64_t j, int64_t k) {
         return tc_ok && t.p(i, k) == MP_HALF && t.p(j, k) == MP_HALF;
     };
-    // FP64 updates whose two panel tiles share a narrower precision read them
-    // natively (widened exactly inside the DMMA kernel) instead of via copies
-    auto native64 = [&](int64_t i, int64_t j, int64_t k) {
-        return t.p(i, k) == t.p(j, k) && t.p(i, k) != MP_DOUBLE;
+    // Operand precision the update of a tile of precision q reads panel tile
+    // (i, k) in: FP16 tiles take FP16 copies (A_ik.converted(half), the
+    // reference composition); FP32 and FP64 tiles are updated on DMMA, which
+    // widens FP16 / FP32 panel tiles exactly on load (an FP64 panel tile is
+    // rounded to FP32 first for an FP32 tile, as the reference's
+    // converted(single)).
+    auto opnd_prec = [&](mp_precision q, int64_t i, int64_t k) -> mp_precision {
+        const mp_precision r = t.p(i, k);
+        if (q == MP_HALF) return MP_HALF;
+        if (q == MP_SINGLE && r == MP_DOUBLE) return MP_SINGLE;
+        return r;
     };
-    // ... and when both are FP16, on the INT8 tensor cores (exact digits)
+    // FP64 tiles fed by two FP16 panel tiles: the INT8 tensor cores (exact digits)
     const bool oz_ok = tc_ok && (nb % 16) == 0 && ozaki_enabled();
     auto ozaki64 = [&](int64_t i, int64_t j, int64_t k) {
         return oz_ok && t.p(i, k) == MP_HALF && t.p(j, k) == MP_HALF;
@@ -286,7 +287,6 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         std::vector<TcProblem> trsm_tc[2];
         std::vector<TileProblem> trsm_p[2][3];
         std::vector<CopyItem> wb[3], cv[3][3][3];
-        std::vector<SplitItem> split32[3];
         std::vector<OzSliceItem> digits[3];
         UpAcc up[3];
     };
@@ -318,13 +318,11 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         const mp_precision q = t.p(i, k);
         bool need[2][3] = {{false, false, false}, {false, false, false}};
         for (int64_t j = k + 1; j <= i; ++j)  // A operand of (owned) row-i updates
-            if (t.has(i, j) && !(t.p(i, j) == MP_DOUBLE && native64(i, j, k)) &&
-                !(t.p(i, j) == MP_SINGLE && half_into_single(i, j, k)))
-                need[j == k + 1 ? 0 : 1][t.p(i, j)] = true;
+            if (t.has(i, j) && !(t.p(i, j) == MP_DOUBLE && ozaki64(i, j, k)))
+                need[j == k + 1 ? 0 : 1][opnd_prec(t.p(i, j), i, k)] = true;
         for (int64_t m = i; m < NT; ++m)  // B operand of (owned) column-i updates
-            if (t.has(m, i) && !(t.p(m, i) == MP_DOUBLE && native64(m, i, k)) &&
-                !(t.p(m, i) == MP_SINGLE && half_into_single(m, i, k)))
-                need[i == k + 1 ? 0 : 1][t.p(m, i)] = true;
+            if (t.has(m, i) && !(t.p(m, i) == MP_DOUBLE && ozaki64(m, i, k)))
+                need[i == k + 1 ? 0 : 1][opnd_prec(t.p(m, i), i, k)] = true;
         const int h0 = (tsplit && i == k + 1) ? 2 : 0;  // the head tile's part-0 work
         for (int r = 0; r < 3; ++r) {
             if (r == q) continue;
@@ -340,9 +338,6 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         if (hd >= 0)
             A.digits[hd].push_back(
                 OzSliceItem{pan(MP_HALF, i, k), dig(i, k), rex(i, k), ndg(i, k), nb, nb, nb, nb, tt, 0, 0});
-        const int h32 = need[0][MP_SINGLE] ? h0 : need[1][MP_SINGLE] ? 1 : -1;
-        if (tc_ok && h32 >= 0)  // FP32 consumers run 3xTF32 on hi/lo splits
-            A.split32[h32].push_back(SplitItem{pan(MP_SINGLE, i, k), spl(0, i, k), spl(1, i, k)});
     };
     for (const DistAction& a : sched) {
         StepAcc& A = acc[a.k];
@@ -377,19 +372,18 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 if (q == MP_HALF && tc_ok)
                     U.tc.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
                                              static_cast<int32_t>(t.slot[j * NT + i]), lo});
+                else if (q == MP_HALF)
+                    U.simt16.push_back(TileProblem{pan(MP_HALF, i, k), pan(MP_HALF, j, k), t.ptr(i, j), lo, 0});
                 else if (q == MP_SINGLE && half_into_single(i, j, k))
                     U.tc16s.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
                                                 static_cast<int32_t>(t.slot[j * NT + i]), lo});
-                else if (q == MP_SINGLE && tc_ok)
-                    U.tc32.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
-                                               static_cast<int32_t>(t.slot[j * NT + i]), lo});
                 else if (q == MP_DOUBLE && ozaki64(i, j, k))
                     U.oz.push_back(OzProblem{static_cast<int32_t>(i), static_cast<int32_t>(j), t.ptr(i, j), lo, 0});
-                else if (q == MP_DOUBLE && native64(i, j, k)) {
-                    const mp_precision pp = t.p(i, k);
-                    U.pn[pp].push_back(TileProblem{pan(pp, i, k), pan(pp, j, k), t.ptr(i, j), lo, 0});
-                } else
-                    U.p[q].push_back(TileProblem{pan(q, i, k), pan(q, j, k), t.ptr(i, j), lo, 0});
+                else {
+                    const mp_precision pa = opnd_prec(q, i, k), pb = opnd_prec(q, j, k);
+                    U.dm[pa][pb][q == MP_DOUBLE ? 1 : 0].push_back(
+                        TileProblem{pan(pa, i, k), pan(pb, j, k), t.ptr(i, j), lo, 0});
+                }
                 break;
             }
             default:
@@ -436,8 +430,6 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 }
         }
         for (int h = 0; h < 3; ++h) {
-            append(buf, A.split32[h], L.split32[h]);
-            L.n_split32[h] = A.split32[h].size();
             append(buf, A.digits[h], L.digits[h]);
             L.n_digits[h] = A.digits[h].size();
         }
@@ -446,18 +438,16 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             L.up[w].n_tc = A.up[w].tc.size();
             append(buf, A.up[w].tc16s, L.up[w].tc16s);
             L.up[w].n_tc16s = A.up[w].tc16s.size();
-            append(buf, A.up[w].tc32, L.up[w].tc32);
-            L.up[w].n_tc32 = A.up[w].tc32.size();
-            for (int q = 0; q < 3; ++q) {
-                append(buf, A.up[w].p[q], L.up[w].p[q]);
-                L.up[w].n_p[q] = A.up[w].p[q].size();
-            }
+            append(buf, A.up[w].simt16, L.up[w].simt16);
+            L.up[w].n_simt16 = A.up[w].simt16.size();
             append(buf, A.up[w].oz, L.up[w].oz);
             L.up[w].n_oz = A.up[w].oz.size();
-            for (int q = 0; q < 2; ++q) {
-                append(buf, A.up[w].pn[q], L.up[w].pn[q]);
-                L.up[w].n_pn[q] = A.up[w].pn[q].size();
-            }
+            for (int a = 0; a < 3; ++a)
+                for (int b = 0; b < 3; ++b)
+                    for (int c2 = 0; c2 < 2; ++c2) {
+                        append(buf, A.up[w].dm[a][b][c2], L.up[w].dm[a][b][c2]);
+                        L.up[w].n_dm[a][b][c2] = A.up[w].dm[a][b][c2].size();
+                    }
         }
     }
     // final clean-up lists: upper part of diagonal tiles, strictly-upper tiles
@@ -497,9 +487,6 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                     launch_batched_convert(c, st, (mp_precision)q, (mp_precision)r,
                                            reinterpret_cast<const CopyItem*>(dl + L.cv[h][q][r]),
                                            L.n_cv[h][q][r], tt);
-        if (L.n_split32[h])
-            launch_batched_split_tf32_t(c, st, reinterpret_cast<const SplitItem*>(dl + L.split32[h]),
-                                        L.n_split32[h], nb);
         if (L.n_digits[h]) {
             launch_oz_slices(c, st, reinterpret_cast<const OzSliceItem*>(dl + L.digits[h]), L.n_digits[h], nb, nb);
             static const bool dbg = getenv("MPCR_DEBUG_NDIG") != nullptr;  // diagnostics (eager runs only)
@@ -565,7 +552,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                            probs, (mp_precision)q};
                 d.pout = (mp_precision)q;
                 d.k_tri = true;
-                d.b_wide = q == MP_SINGLE;
+                d.pin_b = MP_DOUBLE;
                 d.exclusive = hb == 0;  // the head tile is on the critical path
                 ProfScope ps(c, MP_PROF_TRSM, st, static_cast<double>(nb) * nb * nb * L.n_trsm_p[hb][q]);
                 launch_dmma_gemm(c, st, d, L.n_trsm_p[hb][q]);
@@ -655,29 +642,6 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     // ---- trailing update A_ij -= L_ik L_jk^T of one part of step k ------------
     auto update_phase = [&](int64_t k, int part, cudaStream_t st, int tiles_per_cta) {
         const UpLists& U = steps[k].up[part];
-        if (U.n_tc32) {  // FP32 tiles: 3xTF32 on tcgen05, C -= (L_ik^T)^T (L_jk^T)
-            TcGemm g;
-            g.kind = 1;
-            g.pc = MP_SINGLE;
-            g.ta = true;
-            g.tb = false;
-            g.m = g.n = g.k = nb;
-            g.alpha = -1.0;
-            g.beta = 1.0;
-            g.A = g.B = spl(0, 0, k);
-            g.A2 = g.B2 = spl(1, 0, k);
-            g.lda = g.ldb = nb;
-            g.a_tiles = g.b_tiles = NT;
-            g.a_tile_stride = g.b_tile_stride = tt;
-            g.C = t.slab[MP_SINGLE];
-            g.ldc = nb;
-            g.c_tiles = t.nslot[MP_SINGLE];
-            g.c_tile_stride = tt;
-            g.problems = reinterpret_cast<const TcProblem*>(dl + U.tc32);
-            g.count = U.n_tc32;
-            g.tiles_per_cta = tiles_per_cta;
-            launch_tc_gemm(c, st, g);
-        }
         if (U.n_tc16s) {  // FP32 tiles from FP16 panels
             TcGemm g;
             g.pc = MP_SINGLE;
@@ -720,12 +684,11 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             g.tiles_per_cta = tiles_per_cta;
             launch_tc_gemm(c, st, g);
         }
-        for (int q = 0; q < 3; ++q)
-            if (U.n_p[q]) {
-                GroupedGemm g{(mp_precision)q, (mp_precision)q, true, nb, nb, nb, nb, nb, nb, -1.0, 1.0,
-                              reinterpret_cast<const TileProblem*>(dl + U.p[q]), U.n_p[q]};
-                launch_grouped_gemm(c, st, g);
-            }
+        if (U.n_simt16) {  // FP16 tiles of a size the tcgen05 maps cannot take
+            GroupedGemm g{MP_HALF, MP_HALF, true, nb, nb, nb, nb, nb, nb, -1.0, 1.0,
+                          reinterpret_cast<const TileProblem*>(dl + U.simt16), U.n_simt16};
+            launch_grouped_gemm(c, st, g);
+        }
         if (U.n_oz) {  // FP64 tiles from FP16 panels: exact INT8 digit products
             OzGemm o;
             o.A = o.B = dig(0, k);
@@ -744,13 +707,22 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             o.tiles_per_cta = tiles_per_cta;
             launch_oz_gemm(c, st, o);
         }
-        for (int q = 0; q < 2; ++q)
-            if (U.n_pn[q]) {
-                GroupedGemm g{(mp_precision)q, MP_DOUBLE, true, nb, nb, nb, nb, nb, nb, -1.0, 1.0,
-                              reinterpret_cast<const TileProblem*>(dl + U.pn[q]), U.n_pn[q]};
-                g.exclusive = part == 2;  // the diagonal SYRK feeding the next POTRF
-                launch_grouped_gemm(c, st, g);
-            }
+        // FP32 / FP64 tiles on DMMA: exact products of the widened panel
+        // tiles, FP64 accumulation, one rounding into the tile
+        for (int pa = 0; pa < 3; ++pa)
+            for (int pb = 0; pb < 3; ++pb)
+                for (int c2 = 0; c2 < 2; ++c2) {
+                    const int64_t cnt = U.n_dm[pa][pb][c2];
+                    if (!cnt) continue;
+                    DmmaArgs d{false, true, nb, nb, nb, -1.0, 1.0, nullptr, nb, nullptr, nb, nullptr, nb, false,
+                               reinterpret_cast<const TileProblem*>(dl + U.dm[pa][pb][c2]), (mp_precision)pa};
+                    d.pin_b = pb;
+                    d.pout = c2 ? MP_DOUBLE : MP_SINGLE;
+                    d.exclusive = part == 2;  // the diagonal SYRK feeding the next POTRF
+                    ProfScope ps(c, c2 ? MP_PROF_GEMM_F64 : MP_PROF_GEMM_F32, st,
+                                 2.0 * static_cast<double>(nb) * nb * nb * cnt);
+                    launch_dmma_gemm(c, st, d, cnt);
+                }
     };
 
     auto issue_all = [&]() {
@@ -1579,6 +1551,24 @@ mp_status mp_tile_matern_mle(mp_ctx ctx, mp_tile cov, const double* host_x, cons
     if (nll) *nll = vf[best];
     if (iterations) *iterations = it;
     if (converged) *converged = done ? 1 : 0;
+    MP_API_END
+}
+
+// Tile-wise MPArray::converted (array.cpp:187-191): every tile of src
+// converted into the precision dst holds for it (same grid and tiling).
+mp_status mp_tile_convert(mp_ctx ctx, mp_tile dst, mp_tile src) {
+    MP_API_BEGIN
+    mp_tile_s &d = T_(dst), &s = T_(src);
+    if (!ctx) fail(MP_INVALID_PARAM, "null context");
+    if (d.rows != s.rows || d.cols != s.cols || d.br != s.br || d.bc != s.bc)
+        fail(MP_SHAPE_MISMATCH, "tile convert: grids differ");
+    for (int64_t j = 0; j < s.tc; ++j)
+        for (int64_t i = 0; i < s.tr; ++i) {
+            if (s.has(i, j) != d.has(i, j)) fail(MP_SHAPE_MISMATCH, "tile convert: tiles distributed differently");
+            if (s.has(i, j))
+                launch_convert(ctx, ctx->stream, s.p(i, j), s.ptr(i, j), s.br, d.p(i, j), d.ptr(i, j), d.br, s.br,
+                               s.bc);
+        }
     MP_API_END
 }
 

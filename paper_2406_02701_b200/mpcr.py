@@ -489,6 +489,10 @@ class MPCRTile:
                                                y.ctypes.data_as(C.c_void_p), x.size, nu, range_,
                                                variance, nugget))
 
+    def convert_from(self, src: "MPCRTile"):
+        """Every tile of src converted into this tile object's precision for it."""
+        check(lib().mp_tile_convert(self.ctx.h, self.h, src.h))
+
     def copy_from(self, src: "MPCRTile"):
         check(lib().mp_tile_copy(self.ctx.h, self.h, src.h))
 

@@ -17,8 +17,9 @@ unit grid the bench factors at n = 131072.
   ||(LL^T - A)[R,R]||_F / ||A[R,R]||_F on 256 rows including the last tile
   row, bounded by 4 * (n / 8192) times the oracle's value on the same sample
   scheme at n = 8192 (the c * n * u shape of the Cholesky backward-error
-  bound), and (iii) the logdet against an all-FP64 GPU factorization, bounded
-  the same way by the oracle's mixed-vs-FP64 logdet gap at n = 8192.
+  bound), and (iii) the logdet against an all-FP64 GPU factorization of the
+  same tile-rounded input, bounded the same way by the oracle's
+  mixed-vs-FP64 logdet gap at n = 8192 (also against its tile-rounded input).
 """
 import time
 
@@ -130,13 +131,26 @@ def test_tile_chol_nb1024_n65536_sampled(ctx, case8192):
     bound = 4 * (n / m) * case8192["res_ref"]["normwise"]
     print(f"n=65536 sampled residual {res} bound {bound:.3e} (oracle@8192 {case8192['res_ref']})")
     assert res["normwise"] <= bound
-    # (iii) logdet vs an all-FP64 GPU factorization of the same matrix
-    del t
-    t64 = mp.MPCRTile(n, n, NB, NB, None, np.full((n // NB, n // NB), 2, np.int32), ctx)
-    t64.fill_matern_points(x, y, 0.5, 0.03, 1.0, 0.0)
-    mp.tile_chol(t64)
-    ld64 = t64.logdet()
+    t.close()
+    # (iii) logdet vs an all-FP64 GPU factorization of the same (tile-rounded)
+    # input: the gap is the mixed arithmetic's, as ld_gap_ref is at n = 8192
+    ld64 = _fp64_logdet_of_input(ctx, n, g, x, y)
     gap = abs(ld - ld64) / abs(ld64)
     gbound = 4 * (n / m) * case8192["ld_gap_ref"]
     print(f"n=65536 logdet mixed {ld:.12g} fp64 {ld64:.12g} rel gap {gap:.3e} bound {gbound:.3e}")
     assert gap <= gbound
+
+
+def _fp64_logdet_of_input(ctx, n, g, x, y):
+    import paper_2406_02701_b200 as mp
+
+    nt = n // NB
+    src = mp.MPCRTile(n, n, NB, NB, None, g, ctx)
+    src.fill_matern_points(x, y, 0.5, 0.03, 1.0, 0.0)
+    t64 = mp.MPCRTile(n, n, NB, NB, None, np.full((nt, nt), 2, np.int32), ctx)
+    t64.convert_from(src)
+    src.close()
+    mp.tile_chol(t64)
+    ld = t64.logdet()
+    t64.close()
+    return ld
