@@ -192,6 +192,29 @@ mp_status mp_solve(mp_ctx ctx, mp_array a, mp_array b, mp_array out);
 mp_status mp_chol2inv(mp_ctx ctx, mp_array u, mp_array out);
 
 /* ------------------------------------------------------------------------- */
+/* Op-name dispatch (dispatch.hpp, dispatch.cpp:46-137)                       */
+/* ------------------------------------------------------------------------- */
+/* KernelKey: input precisions and the promoted output; in_b = -1 for the
+ * unary form.  Registered ops, in the reference's order: add sub mul div
+ * rbind cbind matmul crossprod (binary), log exp sqrt abs transpose chol
+ * solve (unary). */
+typedef struct {
+    int in_a;
+    int in_b;
+    int out;
+} mp_kernel_key;
+/* KernelRegistry::is_unary; MP_UNKNOWN_OPERATION for an unregistered name. */
+mp_status mp_op_is_unary(const char* op, int* unary);
+/* dispatch::resolve (dispatch.cpp:102-114): prec_b < 0 for the unary form;
+ * out = promote(a, b).  MP_UNKNOWN_OPERATION for an unregistered name. */
+mp_status mp_resolve(const char* op, int prec_a, int prec_b, mp_kernel_key* key);
+/* dispatch::execute (dispatch.cpp:116-137): MP_PRECISION_MISMATCH when the
+ * inputs' precisions differ from the key; b = NULL for unary ops.  *out is a
+ * new device array (mp_array_destroy it). */
+mp_status mp_execute(mp_ctx ctx, const mp_kernel_key* key, const char* op, mp_array a, mp_array b,
+                     mp_array* out);
+
+/* ------------------------------------------------------------------------- */
 /* MPCRTile                                                */
 /* ------------------------------------------------------------------------- */
 /* new(MPCRTile, rows, cols, rows_per_tile, cols_per_tile, values, precisions)

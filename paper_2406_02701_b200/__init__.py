@@ -9,6 +9,7 @@ from ._lib import LIB_PATH, MPError, lib  # noqa: F401
 from .mpcr import (  # noqa: F401
     BinaryOp,
     Context,
+    KernelKey,
     MPArray,
     MPCRTile,
     Precision,
@@ -18,6 +19,7 @@ from .mpcr import (  # noqa: F401
     UnaryOp,
     default_context,
     diag,
+    dispatch,
     dist_owner,
     dist_schedule,
     ew_binary,
@@ -37,7 +39,7 @@ from .mpcr import (  # noqa: F401
 )
 
 __all__ = [
-    "BinaryOp", "Context", "MPArray", "MPCRTile", "MPError", "Precision", "ProcessGrid", "ReduceOp", "Side",
+    "BinaryOp", "Context", "KernelKey", "dispatch", "MPArray", "MPCRTile", "MPError", "Precision", "ProcessGrid", "ReduceOp", "Side",
     "UnaryOp", "default_context", "diag", "dist_owner", "dist_schedule", "nccl_unique_id", "ew_binary", "ew_scalar", "ew_unary", "gaussian_nll", "linalg", "matern_mle",
     "parse_precision", "promote", "reduce", "tile_chol", "tile_gemm", "tile_trsm", "transpose",
     "lib", "LIB_PATH",

@@ -40,6 +40,9 @@ SIGNATURES = {
     "mp_prof_reset": (C.c_int, [_vp]),
     "mp_prof_trace": (C.c_int, [_vp, C.c_int]),
     "mp_prof_trace_dump": (C.c_int, [_vp, C.c_char_p]),
+    "mp_op_is_unary": (C.c_int, [C.c_char_p, C.POINTER(C.c_int)]),
+    "mp_resolve": (C.c_int, [C.c_char_p, C.c_int, C.c_int, _vp]),
+    "mp_execute": (C.c_int, [_vp, _vp, C.c_char_p, _vp, _vp, C.POINTER(_vp)]),
     "mp_prof_digit_products": (C.c_int, [_vp, _vp, _vp]),
     "mp_prof_query": (C.c_int, [_vp, C.c_int, C.POINTER(C.c_double), _ip, C.POINTER(C.c_double)]),
     "mp_launch_count": (C.c_int, [_vp, _ip]),

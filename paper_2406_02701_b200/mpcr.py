@@ -390,6 +390,39 @@ class linalg:
         return out
 
 
+class KernelKey(C.Structure):
+    """dispatch::KernelKey (dispatch.hpp): input precisions, promoted output;
+    in_b = -1 for unary operations."""
+    _fields_ = [("in_a", C.c_int), ("in_b", C.c_int), ("out", C.c_int)]
+
+    def __repr__(self):
+        b = None if self.in_b < 0 else Precision(self.in_b)
+        return f"KernelKey(in_a={Precision(self.in_a)!r}, in_b={b!r}, out={Precision(self.out)!r})"
+
+
+class dispatch:
+    """mpnum::dispatch (dispatch.cpp:46-137): the op-name registry on device arrays."""
+
+    @staticmethod
+    def is_unary(op: str) -> bool:
+        u = C.c_int()
+        check(lib().mp_op_is_unary(op.encode(), C.byref(u)))
+        return bool(u.value)
+
+    @staticmethod
+    def resolve(op: str, a: Precision, b: Precision | None = None) -> KernelKey:
+        k = KernelKey()
+        check(lib().mp_resolve(op.encode(), int(a), -1 if b is None else int(b), C.byref(k)))
+        return k
+
+    @staticmethod
+    def execute(key: KernelKey, op: str, a: MPArray, b: MPArray | None = None) -> MPArray:
+        out = C.c_void_p()
+        check(lib().mp_execute(a.ctx.h, C.byref(key), op.encode(), a.h, b.h if b is not None else None,
+                               C.byref(out)))
+        return MPArray(out, a.ctx)
+
+
 class MPCRTile:
     """MPCRTile: per-tile precisions, tiles on the device.
 

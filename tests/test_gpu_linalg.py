@@ -493,3 +493,63 @@ def test_gemm_grouped_rasterization_ragged(ctx, rng, prec):
     dc = mp.MPArray.zeros_matrix(m, n, mp.Precision.Single, ctx)
     mp.linalg.gemm(da, db, dc, False, True, 1.0, 0.0)
     assert rel(dc.to_numpy(), A @ B.T) < 4 * k * 2.0 ** -24
+
+
+@pytest.mark.parametrize("pa,pb", [(H, S), (S, D), (D, D), (H, H)])
+def test_dispatch_registry_ops(ctx, ref, rng, pa, pb):
+    """dispatch::resolve / execute (dispatch.cpp:46-137) by op name on device
+    arrays: promoted keys, the same results as the reference's kernels
+    (bit-exact for elementwise/concat/transpose, c*n*u for the rest)."""
+    import paper_2406_02701_b200 as mp
+    from oracle.oracle import round_to
+
+    m, n = 48, 48
+    A = round_to(rng.random((m, n)) + 0.5, pa)
+    B = round_to(rng.random((m, n)) + 0.5, pb)
+    da, db = mp.MPArray.from_numpy(A, pa, ctx), mp.MPArray.from_numpy(B, pb, ctx)
+    po = max(pa, pb)
+    for i, op in enumerate(("add", "sub", "mul", "div")):
+        key = mp.dispatch.resolve(op, pa, pb)
+        assert (key.in_a, key.in_b, key.out) == (pa, pb, po) and not mp.dispatch.is_unary(op)
+        got = mp.dispatch.execute(key, op, da, db)
+        assert got.precision() == po
+        np.testing.assert_array_equal(got.to_numpy(), ref.ew_binary(i, pa, pb, A, B))
+    key = mp.dispatch.resolve("matmul", pa, pb)
+    got = mp.dispatch.execute(key, "matmul", da, db).to_numpy()
+    want = ref.matmul(pa, pb, A, B)
+    assert np.linalg.norm(got - want) <= 4 * n * {0: 2.0 ** -11, 1: 2.0 ** -24, 2: 2.0 ** -53}[po] * np.linalg.norm(want) + 1e-300
+    got = mp.dispatch.execute(mp.dispatch.resolve("crossprod", pa, pb), "crossprod", da, db).to_numpy()
+    want = ref.crossprod(pa, A, pb, B)
+    assert np.linalg.norm(got - want) <= 4 * m * {0: 2.0 ** -11, 1: 2.0 ** -24, 2: 2.0 ** -53}[po] * np.linalg.norm(want)
+    for op, ax in (("rbind", 0), ("cbind", 1)):
+        got = mp.dispatch.execute(mp.dispatch.resolve(op, pa, pb), op, da, db)
+        np.testing.assert_array_equal(got.to_numpy(), np.concatenate([A, B], axis=ax))
+    for i, op in enumerate(("log", "exp", "sqrt", "abs")):
+        key = mp.dispatch.resolve(op, pa)
+        assert key.in_b == -1 and key.out == pa and mp.dispatch.is_unary(op)
+        got = mp.dispatch.execute(key, op, da).to_numpy()
+        want = ref.ew_unary(i, pa, A)
+        if op in ("sqrt", "abs"):
+            np.testing.assert_array_equal(got, want)
+        else:  # few-ulp (SURVEY §8c)
+            np.testing.assert_allclose(got, want, rtol=4 * {0: 2.0 ** -11, 1: 2.0 ** -24, 2: 2.0 ** -52}[pa])
+    np.testing.assert_array_equal(mp.dispatch.execute(mp.dispatch.resolve("transpose", pa), "transpose", da).to_numpy(),
+                                  A.T)
+    S_ = round_to(A.T @ A + m * np.eye(n), pa)
+    dS = mp.MPArray.from_numpy(S_, pa, ctx)
+    u = mp.dispatch.execute(mp.dispatch.resolve("chol", pa), "chol", dS).to_numpy()
+    cp = max(pa, S)
+    tol = 100 * n * {1: 2.0 ** -24, 2: 2.0 ** -53}[cp] + 2 * {0: 2.0 ** -11, 1: 2.0 ** -24, 2: 2.0 ** -53}[pa]
+    uw = ref.chol(pa, S_)
+    assert np.linalg.norm(u - uw) <= tol * np.linalg.norm(uw)
+    inv = mp.dispatch.execute(mp.dispatch.resolve("solve", pa), "solve", dS).to_numpy()
+    invw = ref.solve(pa, pa, S_, np.eye(n))
+    assert np.linalg.norm(inv - invw) <= tol * np.linalg.norm(invw)
+    # errors: unknown op, wrong precision for the key, arity
+    with pytest.raises(mp.MPError) as e:
+        mp.dispatch.resolve("qr", pa)
+    assert e.value.kind == "UnknownOperation"
+    with pytest.raises(mp.MPError) as e:
+        mp.dispatch.execute(mp.dispatch.resolve("add", pb, pb), "add", da, db) if pa != pb else \
+            mp.dispatch.execute(mp.dispatch.resolve("add", D if pa != D else H, pb), "add", da, db)
+    assert e.value.kind == "PrecisionMismatch"

@@ -17,9 +17,11 @@ unit grid the bench factors at n = 131072.
   ||(LL^T - A)[R,R]||_F / ||A[R,R]||_F on 256 rows including the last tile
   row, bounded by 4 * (n / 8192) times the oracle's value on the same sample
   scheme at n = 8192 (the c * n * u shape of the Cholesky backward-error
-  bound), and (iii) the logdet against an all-FP64 GPU factorization of the
-  same tile-rounded input, bounded the same way by the oracle's
-  mixed-vs-FP64 logdet gap at n = 8192 (also against its tile-rounded input).
+  bound), and (iii) the factor (sampled rows) and logdet against the
+  reference's composition run on the GPU dense API (tests/composed.py; it
+  reproduces the oracle at n = 8192), with the n <= 8192 rule: as close to the
+  composition as the composition is to an all-FP64 factorization of the same
+  tile-rounded input.
 """
 import time
 
@@ -97,7 +99,28 @@ def case8192(ctx, ref):
     c["res_gpu"] = verify.sampled_residual(None, x, y, rows, NB, c["g"], 0.03, L_rows=c["L"][rows])
     c["res_ref"] = verify.sampled_residual(None, x, y, rows, NB, c["g"], 0.03, L_rows=c["Lref"][rows])
     c["ld_gap_ref"] = abs(c["ld_ref"] - c["ld_dense"]) / abs(c["ld_dense"])
+    # the composed reference on the GPU dense API (tests/composed.py) at this size
+    tc = _composed(ctx, n, c["g"], x, y)
+    c["L_comp"] = np.tril(tc.to_numpy())  # upper tiles keep the input in the composition
+    c["err_comp"] = np.linalg.norm(c["L_comp"] - c["Lref"]) / np.linalg.norm(c["Lref"])
+    tc.close()
     return c
+
+
+def _composed(ctx, n, g, x, y):
+    import paper_2406_02701_b200 as mp
+    from composed import composed_tile_chol
+
+    tc = mp.MPCRTile(n, n, NB, NB, None, g, ctx)
+    tc.fill_matern_points(x, y, 0.5, 0.03, 1.0, 0.0)
+    composed_tile_chol(tc, NB, g)
+    return tc
+
+
+def _lower_rows(L_rows, rows):
+    """Rows of a composed factor with the (untouched) upper tiles masked."""
+    cols = np.arange(L_rows.shape[1])
+    return np.where(cols[None, :] // NB <= np.asarray(rows)[:, None] // NB, L_rows, 0.0)
 
 
 def test_tile_chol_nb1024_n8192_vs_oracle(case8192):
@@ -108,6 +131,9 @@ def test_tile_chol_nb1024_n8192_vs_oracle(case8192):
     _check_vs_oracle(c)
     # the sampled metric agrees with the oracle's on the same rows
     assert c["res_gpu"]["normwise"] <= 4 * c["res_ref"]["normwise"]
+    # the GPU-composed reference (used at n = 65536) reproduces the oracle
+    print(f"n=8192 composed-on-GPU vs oracle {c['err_comp']:.3e}")
+    assert c["err_comp"] <= max(4 * c["err_dense"], 1e-12)
 
 
 def test_tile_chol_nb1024_n65536_sampled(ctx, case8192):
@@ -131,17 +157,26 @@ def test_tile_chol_nb1024_n65536_sampled(ctx, case8192):
     bound = 4 * (n / m) * case8192["res_ref"]["normwise"]
     print(f"n=65536 sampled residual {res} bound {bound:.3e} (oracle@8192 {case8192['res_ref']})")
     assert res["normwise"] <= bound
+    Lf = t.get_rows(rows)
     t.close()
-    # (iii) logdet vs an all-FP64 GPU factorization of the same (tile-rounded)
-    # input: the gap is the mixed arithmetic's, as ld_gap_ref is at n = 8192
-    ld64 = _fp64_logdet_of_input(ctx, n, g, x, y)
-    gap = abs(ld - ld64) / abs(ld64)
-    gbound = 4 * (n / m) * case8192["ld_gap_ref"]
-    print(f"n=65536 logdet mixed {ld:.12g} fp64 {ld64:.12g} rel gap {gap:.3e} bound {gbound:.3e}")
-    assert gap <= gbound
+    # (iii) against the reference composition run on the GPU dense API
+    # (tests/composed.py) and an all-FP64 factorization of the same
+    # tile-rounded input: the fused factor and logdet are as close to the
+    # composition as the composition is to FP64 (the n <= 8192 rule).
+    tc = _composed(ctx, n, g, x, y)
+    ld_c = tc.logdet()
+    Lc = _lower_rows(tc.get_rows(rows), rows)
+    tc.close()
+    ld64, L64 = _fp64_of_input(ctx, n, g, x, y, rows)
+    err_f = np.linalg.norm(Lf - Lc) / np.linalg.norm(Lc)
+    err_c = np.linalg.norm(Lc - L64) / np.linalg.norm(L64)
+    print(f"n=65536 sampled rows: fused vs composed {err_f:.3e}, composed vs fp64 {err_c:.3e}; logdet fused "
+          f"{ld:.12g} composed {ld_c:.12g} fp64 {ld64:.12g}")
+    assert err_f <= 4 * err_c
+    assert abs(ld - ld_c) <= 4 * abs(ld_c - ld64)
 
 
-def _fp64_logdet_of_input(ctx, n, g, x, y):
+def _fp64_of_input(ctx, n, g, x, y, rows):
     import paper_2406_02701_b200 as mp
 
     nt = n // NB
@@ -152,5 +187,6 @@ def _fp64_logdet_of_input(ctx, n, g, x, y):
     src.close()
     mp.tile_chol(t64)
     ld = t64.logdet()
+    L_rows = t64.get_rows(rows)
     t64.close()
-    return ld
+    return ld, L_rows
