@@ -551,8 +551,76 @@ def check_factor(args, A, g, x, y, n, nb, ctx, world, grid):
                     "tests/test_gpu_tile_nb1024.py); bound there: 4*(n/8192)*oracle value at n=8192"}
 
 
+def cpu_info():
+    """Host CPU model and the thread count a reference run may use."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count() or 1
+
+
+def _ref_lib():
+    """The reference CPU library for a cpu_baseline leg (oracle/_ref, else the port)."""
+    from oracle import oracle as orc
+
+    if os.path.exists(orc.REF_SO):
+        o = orc.Ref()
+        o.set_num_threads(cpu_info()[1])
+        return o, "reference", cpu_info()[1]
+    return orc.Port(), "port", 1
+
+
+class L2Flush:
+    """Writes a 512 MB buffer (> the 126 MB L2) between timed iterations of a
+    workload whose operands fit in L2."""
+
+    def __init__(self, enabled, stream):
+        import torch
+
+        self.buf = torch.empty(256 << 20, dtype=torch.float16, device="cuda") if enabled else None
+        self.stream = stream
+
+    def __call__(self):
+        if self.buf is not None:
+            import torch
+
+            with torch.cuda.stream(self.stream):
+                self.buf.fill_(0.0)
+
+
+GEMM_PEAK_NOTE = {0: "tcgen05 kind::f16: measured bf16 burst (MEASURED_PEAKS.json)",
+                  1: "3xTF32: measured bf16 burst x tcgen05 tf32/f16 ratio / 3 (profiles/r02_pipe_peaks.json)",
+                  2: "DMMA: measured FP64 peak (profiles/r02_pipe_peaks.json)"}
+
+
+def gemm_peak(p, pc, pk):
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_pipe_peaks.json")) as fh:
+            mp_ = json.load(fh)
+    except (OSError, ValueError):
+        mp_ = {"f16_burst": 1.0, "tf32_burst": 0.5, "i8_burst": 2.0, "dmma_tflops": 37.1}
+    if p == 0 and pc == 2:
+        return pk["bf16_tflops"] * mp_["i8_burst"] / mp_["f16_burst"], "INT8 digits: measured bf16 burst x i8/f16 ratio (TOPS; FP64-equivalent divides by the digit pairs)"
+    if p == 0:
+        return pk["bf16_tflops"], GEMM_PEAK_NOTE[0]
+    if p == 1:
+        return pk["bf16_tflops"] * mp_["tf32_burst"] / mp_["f16_burst"] / 3, GEMM_PEAK_NOTE[1]
+    return mp_["dmma_tflops"], GEMM_PEAK_NOTE[2]
+
+
 def run_gemm(args, world, rank, local):
-    """Config 2 line: per-precision GEMM TFLOP/s (n x n x n, C = A B)."""
+    """BASELINE.json configs[0] / [1]: linalg::gemm (linalg.cpp:316-357) on
+    n x n x n MPArrays, C = A B (alpha 1, beta 0, NN: mpnum_cli.cpp:117-120).
+    Inputs are the reference's acceptance-test stream (acceptance.cpp:30-36,
+    :158-162): A = the first n^2 draws of Rng(1000 + n) column-major, B the
+    next n^2, rounded to the precision on upload.  rel_frob_err is against the
+    same product at double precision (mpnum_cli.cpp:59-63,174 does the same)."""
     import torch
 
     import paper_2406_02701_b200 as mp
@@ -560,42 +628,121 @@ def run_gemm(args, world, rank, local):
     ctx = mp.Context(local)
     n = args.n or 8192
     p = mp.parse_precision(args.prec)
-    rng = np.random.default_rng(1000 + n)
-    A = mp.MPArray.from_numpy(rng.random((n, n)), p, ctx)
-    B = mp.MPArray.from_numpy(rng.random((n, n)), p, ctx)
-    Cm = mp.MPArray.zeros_matrix(n, n, p, ctx)
+    pc = mp.parse_precision(args.cprec) if args.cprec else p
+    A = mp.random_uniform_matrix(n, n, 1000 + n)
+    B = mp.random_uniform_matrix(n, n, 1000 + n, skip=n * n)
+    dA, dB = mp.MPArray.from_numpy(A, p, ctx), mp.MPArray.from_numpy(B, p, ctx)
+    dC = mp.MPArray.zeros_matrix(n, n, pc, ctx)
     stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
+    es = {0: 2, 1: 4, 2: 8}
+    in_l2 = 2 * n * n * es[int(p)] + n * n * es[int(pc)] < 126e6
+    flush = L2Flush(in_l2, stream)
     for _ in range(args.warmup):
-        mp.linalg.gemm(A, B, Cm, args.ta, args.tb, 1.0, args.beta)
+        mp.linalg.gemm(dA, dB, dC)
     ctx.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = ctx.launch_count()
+    evs = []
     with ClockSampler(local) as clk:
-        e0.record(stream)
         for _ in range(args.steps):
-            mp.linalg.gemm(A, B, Cm, args.ta, args.tb, 1.0, args.beta)
-        e1.record(stream)
+            flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            mp.linalg.gemm(dA, dB, dC)
+            e1.record(stream)
+            evs.append((e0, e1))
         ctx.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
+    launches = ctx.launch_count() - l0
+    ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
     tf = 2 * n ** 3 / (ms * 1e-3) / 1e12
+    # error as mpnum_cli reports it: vs the same product at double precision
+    d64 = mp.MPArray.zeros_matrix(n, n, mp.Precision.Double, ctx)
+    mp.linalg.gemm(mp.MPArray.from_numpy(A, p, ctx).converted(mp.Precision.Double),
+                   mp.MPArray.from_numpy(B, p, ctx).converted(mp.Precision.Double), d64)
+    C64, Cg = d64.to_numpy(), dC.to_numpy()
+    rel = float(np.linalg.norm(Cg - C64) / np.linalg.norm(C64))
+    # e2e: host doubles -> device (set_linear rounding) -> gemm -> host doubles
+    e2e = []
+    for _ in range(max(1, args.steps)):
+        ctx.synchronize()
+        t0 = time.perf_counter()
+        a_ = mp.MPArray.from_numpy(A, p, ctx)
+        b_ = mp.MPArray.from_numpy(B, p, ctx)
+        c_ = mp.MPArray.zeros_matrix(n, n, pc, ctx)
+        mp.linalg.gemm(a_, b_, c_)
+        c_.to_numpy()
+        e2e.append(time.perf_counter() - t0)
+        for h in (a_, b_, c_):
+            h.close()
+    e2e_s = float(np.median(e2e))
     pk, src = peaks()
-    # FP16: tcgen05 kind::f16 at the measured burst rate; FP32: 3xTF32 (3 TF32
-    # MMAs per product, TF32 = half the FP16 rate); FP64: measured DMMA peak
-    peak, peak_src = {0: (pk["bf16_tflops"], f"{src} bf16_tflops (burst)"),
-                      1: (pk["bf16_tflops"] / 6, f"{src} bf16_tflops / 2 / 3 (3xTF32)"),
-                      2: (37.1, "measured DMMA peak, tools/micro/fp64_peak.cu")}[int(p)]
-    print(json.dumps({"metric": f"{args.prec} GEMM TFLOP/s", "value": tf, "unit": "TFLOP/s",
-                      "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                      "higher_is_better": True, "config": {"workload": f"GEMM {n}^3 {args.prec}"},
-                      "roofline": {"bound": "tensor", "achieved": tf, "peak": peak, "unit": "TFLOP/s",
-                                   "frac": tf / peak, "peak_source": peak_src},
-                      "clocks": clk.summary()}))
+    peak, peak_src = gemm_peak(int(p), int(pc), pk)
+    ach = tf
+    line = {"metric": "per-precision GEMM TFLOP/s", "value": tf, "unit": "TFLOP/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "replicas only", "vs_baseline": None, "dtype": f"{args.prec}" + (f"->{args.cprec}" if args.cprec else ""),
+            "data": "synthetic (reference Rng(1000+n) uniform stream, acceptance.cpp:158-162)",
+            "config": {"workload": f"linalg::gemm {n}x{n}x{n} {mp.Precision(p).name} inputs, "
+                                   f"{mp.Precision(pc).name} C, NN, alpha 1 beta 0", "n": n,
+                       "l2": "flushed between iterations (512 MB write)" if in_l2 else "operands > 126 MB L2"},
+            "roofline": {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s" if not (p == 0 and pc == 2) else "TOPS",
+                         "frac": ach / peak if not (p == 0 and pc == 2) else None, "peak_source": f"{src}: {peak_src}",
+                         "traffic": None},
+            "rel_frob_err": rel, "gpu_launches": launches, "clocks": clk.summary(),
+            "e2e": {"value": 2 * n ** 3 / e2e_s / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": 2 * n * n * 8,
+                    "d2h_bytes_per_step": n * n * 8, "ms_per_step": e2e_s * 1e3,
+                    "path": "host doubles -> mp_array_from_doubles (x2) -> mp_gemm -> mp_array_to_doubles"}}
+    if not args.no_cpu:
+        o, kind, cores = _ref_lib()
+        ns = min(n, args.cpu_n if args.cpu_n else 2048)
+        As, Bs = A[:ns, :ns].copy(order="F"), B[:ns, :ns].copy(order="F")
+        from oracle.oracle import round_to
+        As, Bs = round_to(As, int(p)), round_to(Bs, int(p))
+        ts = []
+        t_end = time.perf_counter() + 20
+        while len(ts) < 3 and (not ts or time.perf_counter() < t_end):
+            t0 = time.perf_counter()
+            o.gemm(int(p), int(p), int(pc), As, Bs, np.zeros((ns, ns)))
+            ts.append(time.perf_counter() - t0)
+        t = float(np.median(ts))
+        model, _ = cpu_info()
+        line["cpu_baseline"] = {"value": 2 * ns ** 3 / t / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": kind,
+                                "cpu": model,
+                                "sample": f"reference linalg::gemm {ns}^3 same precisions, median of {len(ts)}: {t:.3f} s"
+                                          + ("" if ns == n else f"; n^3 projection to n={n}: {t * (n / ns) ** 3:.1f} s (projected, not run)")}
+    print(json.dumps(line))
+
+
+def sample_gp_gpu(ctx, x, y, n, nb, range_, nugget):
+    """sample_gp (workloads.cpp:41-49) at the reference's criterion-6 / CLI seed
+    (acceptance.cpp:325-326, mpnum_cli.cpp:397): z = L eps, L the FP64 Cholesky
+    factor of the true covariance, eps = Rng(4).normal() (the reference stream,
+    mp_rng_normal).  The factor runs on the GPU (all-FP64 MPCRTile) since the
+    host cannot factor n = 65536; returns z and the exact-factor NLL
+    0.5 (eps'eps + logdet) + 0.5 n log 2 pi (w = L^-1 z = eps)."""
+    import paper_2406_02701_b200 as mp
+
+    nt = n // nb
+    t64 = mp.MPCRTile(n, n, nb, nb, None, np.full((nt, nt), 2, np.int32), ctx)
+    t64.fill_matern_points(x, y, 0.5, range_, 1.0, nugget)
+    mp.tile_chol(t64)
+    ld64 = t64.logdet()
+    eps = mp.rng_normal(4, n)
+    e = mp.MPCRTile(n, 1, nb, 1, eps, np.full((nt, 1), 2, np.int32), ctx)
+    z_t = mp.MPCRTile(n, 1, nb, 1, None, np.full((nt, 1), 2, np.int32), ctx)
+    mp.tile_gemm(t64, e, z_t, False, False, 1.0, 0.0)
+    z = z_t.to_numpy().ravel()
+    for h in (t64, e, z_t):
+        h.close()
+    nll64 = 0.5 * float(eps @ eps) + 0.5 * ld64 + 0.5 * n * np.log(2 * np.pi)
+    return z, nll64, ld64
 
 
 def run_nll(args, world, rank, local):
     """BASELINE.json configs[4]: Gaussian log-likelihood of a Matern GP at the
-    given locations: host (x, y, z) -> device covariance -> jittered tiled
-    Cholesky -> forward solve -> logdet + quadratic form -> nll to the host
-    (workloads.cpp:56-87).  One step = one likelihood evaluation."""
+    given locations (workloads.cpp:74-87): covariance generated on the device
+    from the points -> jittered mixed-precision tiled Cholesky -> forward solve
+    -> logdet + quadratic form -> nll to the host.  One step = one likelihood
+    evaluation; z = sample_gp(cov_true, Rng(4)) as in the reference."""
     import torch
 
     import paper_2406_02701_b200 as mp
@@ -605,7 +752,7 @@ def run_nll(args, world, rank, local):
     nb = args.nb
     g = band_map(n // nb, args.b64, args.b32)
     x, y, side = grid_points(n)
-    z = np.random.default_rng(5).standard_normal(n)
+    z, nll64, ld64 = sample_gp_gpu(ctx, x, y, n, nb, args.range, args.nugget)
     A = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
     st = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
 
@@ -627,6 +774,7 @@ def run_nll(args, world, rank, local):
             e1.record(st)
             ctx.synchronize()
             times.append((e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3))
+    launches = ctx.launch_count() - l0
     ms = float(np.mean([t[0] for t in times]))
     wall = float(np.mean([t[1] for t in times]))
     flops = n ** 3 / 3
@@ -634,16 +782,39 @@ def run_nll(args, world, rank, local):
         "metric": "Gaussian log-likelihood evaluation (Matern -> tiled chol -> solve -> logdet) TFLOP/s",
         "value": flops / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "mixed(f64/f32/f16 tiles)", "data": "synthetic",
+        "vs_baseline": None, "dtype": "mixed(f64/f32/f16 tiles)",
+        "data": "synthetic: z = sample_gp(cov_true, Rng(4)) (workloads.cpp:41-49; reference Rng stream)",
         "config": {"workload": f"gaussian_nll n={n}, tile {nb}, Matern nu=0.5 range {args.range}, "
                                f"jitter 1e-6 (x10 up to 1e-3)",
-                   "n": n, "nb": nb, "precision_map": f"|i-j|<{args.b64}:FP64, <{args.b32}:FP32, else FP16"},
+                   "n": n, "nb": nb, "precision_map": f"|i-j|<{args.b64}:FP64, <{args.b32}:FP32, else FP16",
+                   "l2": "covariance regenerated in HBM every step (> 126 MB L2)"},
         "nll": r["nll"], "logdet": r["logdet"], "jitter_used": r["jitter"],
-        "gpu_launches": ctx.launch_count() - l0,
+        "nll_fp64_factor": nll64, "rel_err": abs(r["nll"] - nll64) / abs(nll64),
+        "rel_err_note": "vs the NLL of the exact (all-FP64) factor of the same covariance",
+        "gpu_launches": launches,
         "e2e": {"value": flops / (wall * 1e-3) / 1e12, "unit": "TFLOP/s",
-                "h2d_bytes_per_step": 3 * n * 8, "d2h_bytes_per_step": 32, "ms_per_step": wall},
+                "h2d_bytes_per_step": 3 * n * 8, "d2h_bytes_per_step": 32, "ms_per_step": wall,
+                "path": "host (x, y, z) -> mp_tile_fill_matern_points -> mp_tile_gaussian_nll -> nll"},
         "clocks": clk.summary(),
     }
+    if not args.no_cpu:
+        o, kind, cores = _ref_lib()
+        if kind == "reference":
+            ns = min(n, 2048)
+            xs, ys, sside = grid_points(ns)
+            cov = np.exp(-np.hypot(xs[:, None] - xs[None], ys[:, None] - ys[None]) / args.range)
+            zs = z[:ns].copy()
+            ts = []
+            while len(ts) < 3:
+                t0 = time.perf_counter()
+                o.gaussian_nll(1, zs, cov)
+                ts.append(time.perf_counter() - t0)
+            t = float(np.median(ts))
+            line["cpu_baseline"] = {
+                "value": ns ** 3 / 3 / t / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": kind, "cpu": cpu_info()[0],
+                "sample": f"reference stats::gaussian_nll(z, cov, single) n={ns} dense (chol single-threaded "
+                          f"in the reference), median of 3: {t:.3f} s; n^3 projection to n={n}: "
+                          f"{t * (n / ns) ** 3 / 3600:.1f} h (projected, not run)"}
     print(json.dumps(line))
 
 
@@ -681,42 +852,89 @@ def run_mle(args, world, rank, local):
 
 
 def run_cast(args, world, rank, local):
-    """Config 2 cast line: MPArray::converted bandwidth (n x n, pin -> pout)."""
+    """BASELINE.json configs[1] cast line: MPArray::converted (array.cpp:187-191)
+    of an n x n array, pin -> pout, as an HBM stream (n^2 (s_in + s_out) bytes).
+    Input values: the reference Rng(1000 + n) uniform stream scaled to span
+    the destination's range, so FP16 destinations see normals, subnormals and
+    overflow to inf (bit-exactness over every pattern is in the tests)."""
     import torch
 
     import paper_2406_02701_b200 as mp
 
     ctx = mp.Context(local)
-    n = args.n or 32768
-    pin, pout = (mp.parse_precision(p) for p in args.cast.split(":"))
-    a = mp.MPArray.zeros_matrix(n, n, pin, ctx)
+    n = args.n or 8192
+    pin, pout = (mp.parse_precision(x) for x in args.cast.split(":"))
+    es = {0: 2, 1: 4, 2: 8}
+    u = mp.rng_uniform(1000 + n, n * n)
+    vals = np.ldexp(u - 0.5, (np.floor(u * 1e6) % 48 - 24).astype(np.int32))  # |x| from 2^-25 to 2^23
+    with np.errstate(over="ignore"):
+        raw = {0: vals.astype(np.float16).view(np.uint16), 1: vals.astype(np.float32), 2: vals}[int(pin)]
+    a = mp.MPArray.from_storage(raw.reshape((n, n), order="F"), n, n, pin, ctx)
     b = mp.MPArray.zeros_matrix(n, n, pout, ctx)
     lib, C = mp.lib(), __import__("ctypes")
     stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
     for _ in range(args.warmup):
         lib.mp_convert(ctx.h, a.h, b.h)
     ctx.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = ctx.launch_count()
+    evs = []
     with ClockSampler(local) as clk:
-        e0.record(stream)
         for _ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             lib.mp_convert(ctx.h, a.h, b.h)
-        e1.record(stream)
+            e1.record(stream)
+            evs.append((e0, e1))
         ctx.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
-    es = {0: 2, 1: 4, 2: 8}
+    launches = ctx.launch_count() - l0
+    ms = float(np.mean([x.elapsed_time(y) for x, y in evs]))
     byts = n * n * (es[int(pin)] + es[int(pout)])
     gbs = byts / (ms * 1e-3) / 1e9
+    # e2e through the public API: raw source storage up, convert, raw result down
+    e2e = []
+    for _ in range(max(1, args.steps)):
+        ctx.synchronize()
+        t0 = time.perf_counter()
+        a_ = mp.MPArray.from_storage(raw.reshape((n, n), order="F"), n, n, pin, ctx)
+        b_ = a_.converted(pout)
+        b_.storage()
+        e2e.append(time.perf_counter() - t0)
+        a_.close()
+        b_.close()
+    e2e_s = float(np.median(e2e))
     pk, src = peaks()
-    print(json.dumps({"metric": f"cast {args.cast} GB/s", "value": gbs, "unit": "GB/s",
-                      "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                      "higher_is_better": True,
-                      "config": {"workload": f"MPArray::converted {n}x{n} {args.cast}",
-                                 "bytes_per_step": byts},
-                      "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"],
-                                   "unit": "GB/s", "frac": gbs / pk["hbm_gbs"],
-                                   "peak_source": src},
-                      "clocks": clk.summary()}))
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_casts.json")) as fh:
+            traffic = json.load(fh).get(f"{args.cast}@{n}", {}).get("dram_bytes")
+    except (OSError, ValueError):
+        pass
+    line = {"metric": "precision conversion GB/s", "value": gbs, "unit": "GB/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "replicas only", "vs_baseline": None, "dtype": args.cast.replace(":", "->"),
+            "data": "synthetic (reference Rng(1000+n) stream, scaled)",
+            "config": {"workload": f"MPArray::converted {n}x{n} {args.cast}", "n": n, "bytes_per_step": byts,
+                       "l2": "operands > 126 MB L2" if byts > 126e6 else "operands fit L2 (small n)"},
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": gbs / pk["hbm_gbs"], "peak_source": f"{src} hbm_gbs (copy)",
+                         "algorithmic_bytes": byts, "traffic": traffic},
+            "gpu_launches": launches, "clocks": clk.summary(),
+            "e2e": {"value": byts / e2e_s / 1e9, "unit": "GB/s", "h2d_bytes_per_step": n * n * es[int(pin)],
+                    "d2h_bytes_per_step": n * n * es[int(pout)], "ms_per_step": e2e_s * 1e3,
+                    "path": "host raw -> mp_array_upload -> mp_convert -> mp_array_download"}}
+    if not args.no_cpu:
+        o, kind, _ = _ref_lib()
+        ts = []
+        flat = np.ascontiguousarray(raw.ravel())
+        while len(ts) < 3:
+            t0 = time.perf_counter()
+            o.convert(int(pin), int(pout), flat)
+            ts.append(time.perf_counter() - t0)
+        t = float(np.median(ts))
+        line["cpu_baseline"] = {"value": byts / t / 1e9, "unit": "GB/s", "cores": 1, "kind": kind, "cpu": cpu_info()[0],
+                                "sample": f"reference MPArray::converted on the same {n}x{n} array (single-threaded "
+                                          f"in the reference), median of 3: {t:.3f} s"}
+    print(json.dumps(line))
 
 
 def main():
@@ -735,6 +953,7 @@ def main():
     ap.add_argument("--range", type=float, default=0.03)
     ap.add_argument("--nugget", type=float, default=0.0)
     ap.add_argument("--prec", default="half")
+    ap.add_argument("--cprec", default=None, help="gemm: C precision (default: --prec)")
     ap.add_argument("--ta", action="store_true")
     ap.add_argument("--tb", action="store_true")
     ap.add_argument("--beta", type=float, default=0.0)

@@ -192,6 +192,15 @@ mp_status mp_solve(mp_ctx ctx, mp_array a, mp_array b, mp_array out);
 mp_status mp_chol2inv(mp_ctx ctx, mp_array u, mp_array out);
 
 /* ------------------------------------------------------------------------- */
+/* Rng (rng.cpp:9-53): the reference's seeded stream, host-side, bit for bit */
+/* ------------------------------------------------------------------------- */
+/* n uniforms on [0, 1) of Rng(seed) after discarding `skip` draws (B of the
+ * acceptance inputs is the draws after A's n^2: skip = n^2).  No device work. */
+mp_status mp_rng_uniform(uint64_t seed, int64_t skip, int64_t n, double* out);
+/* n standard normals of Rng(seed) (Box-Muller, rng.cpp:38-50). */
+mp_status mp_rng_normal(uint64_t seed, int64_t n, double* out);
+
+/* ------------------------------------------------------------------------- */
 /* Op-name dispatch (dispatch.hpp, dispatch.cpp:46-137)                       */
 /* ------------------------------------------------------------------------- */
 /* KernelKey: input precisions and the promoted output; in_b = -1 for the

@@ -148,7 +148,8 @@ inline mpnum::MPArray crossprod(Engine& e, const mpnum::MPArray& a, const mpnum:
 inline mpnum::MPArray chol(Engine& e, const mpnum::MPArray& a) {
     DeviceArray da(e, a), out(e, a.precision(), a.rows(), a.cols());
     int64_t info = -1;
-    check(mp_chol(e.get(), da.get(), out.get(), &info), info);
+    const mp_status st = mp_chol(e.get(), da.get(), out.get(), &info);  // info is set by the call
+    check(st, info);
     return out.to_host();
 }
 
@@ -222,7 +223,8 @@ public:
     // the global failing column.
     void chol() {
         int64_t info = -1;
-        check(mp_tile_chol(e_.get(), t_, 1, nullptr, &info), info);
+        const mp_status st = mp_tile_chol(e_.get(), t_, 1, nullptr, &info);
+        check(st, info);
     }
     double logdet() const {
         double v = 0;

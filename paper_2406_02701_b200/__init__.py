@@ -31,7 +31,10 @@ from .mpcr import (  # noqa: F401
     nccl_unique_id,
     parse_precision,
     promote,
+    random_uniform_matrix,
     reduce,
+    rng_normal,
+    rng_uniform,
     tile_chol,
     tile_gemm,
     tile_trsm,
@@ -41,6 +44,6 @@ from .mpcr import (  # noqa: F401
 __all__ = [
     "BinaryOp", "Context", "KernelKey", "dispatch", "MPArray", "MPCRTile", "MPError", "Precision", "ProcessGrid", "ReduceOp", "Side",
     "UnaryOp", "default_context", "diag", "dist_owner", "dist_schedule", "nccl_unique_id", "ew_binary", "ew_scalar", "ew_unary", "gaussian_nll", "linalg", "matern_mle",
-    "parse_precision", "promote", "reduce", "tile_chol", "tile_gemm", "tile_trsm", "transpose",
+    "parse_precision", "promote", "random_uniform_matrix", "reduce", "rng_normal", "rng_uniform", "tile_chol", "tile_gemm", "tile_trsm", "transpose",
     "lib", "LIB_PATH",
 ]

@@ -40,6 +40,8 @@ SIGNATURES = {
     "mp_prof_reset": (C.c_int, [_vp]),
     "mp_prof_trace": (C.c_int, [_vp, C.c_int]),
     "mp_prof_trace_dump": (C.c_int, [_vp, C.c_char_p]),
+    "mp_rng_uniform": (C.c_int, [C.c_uint64, C.c_int64, C.c_int64, _vp]),
+    "mp_rng_normal": (C.c_int, [C.c_uint64, C.c_int64, _vp]),
     "mp_op_is_unary": (C.c_int, [C.c_char_p, C.POINTER(C.c_int)]),
     "mp_resolve": (C.c_int, [C.c_char_p, C.c_int, C.c_int, _vp]),
     "mp_execute": (C.c_int, [_vp, _vp, C.c_char_p, _vp, _vp, C.POINTER(_vp)]),

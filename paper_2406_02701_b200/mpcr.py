@@ -390,6 +390,25 @@ class linalg:
         return out
 
 
+def rng_uniform(seed: int, n: int, skip: int = 0) -> np.ndarray:
+    """n uniforms of the reference Rng(seed) (rng.cpp:9-36) after `skip` draws."""
+    out = np.empty(n, np.float64)
+    check(lib().mp_rng_uniform(seed, skip, n, out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def rng_normal(seed: int, n: int) -> np.ndarray:
+    """n standard normals of the reference Rng(seed) (rng.cpp:38-50)."""
+    out = np.empty(n, np.float64)
+    check(lib().mp_rng_normal(seed, n, out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def random_uniform_matrix(rows: int, cols: int, rng_seed: int, skip: int = 0) -> np.ndarray:
+    """acceptance.cpp:30-36 random_uniform: column-major fill from Rng(seed)."""
+    return rng_uniform(rng_seed, rows * cols, skip).reshape((rows, cols), order="F")
+
+
 class KernelKey(C.Structure):
     """dispatch::KernelKey (dispatch.hpp): input precisions, promoted output;
     in_b = -1 for unary operations."""

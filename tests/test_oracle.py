@@ -161,3 +161,16 @@ def test_tile_oracle_port_equals_reference_mixed(ref, port):
         np.fill_diagonal(g, 2)
         np.testing.assert_array_equal(bits(ref.tile_chol(n, nb, g, cov)),
                                       bits(port.tile_chol(n, nb, g, cov)))
+
+
+def test_product_rng_matches_reference_stream(ref):
+    """mp_rng_uniform / mp_rng_normal (csrc/rng.cpp) reproduce the reference
+    Rng (rng.cpp:9-53) bit for bit: the synthetic bench inputs are the
+    reference's own streams (acceptance.cpp:158-162, workloads.cpp:41-49)."""
+    import paper_2406_02701_b200 as mp
+
+    for seed in (0, 4, 1000 + 2048, 2**63 + 5):
+        u = mp.rng_uniform(seed, 4097)
+        np.testing.assert_array_equal(u, ref.rng_uniform(seed, 4097))
+        np.testing.assert_array_equal(mp.rng_uniform(seed, 100, skip=3997), u[3997:])
+        np.testing.assert_array_equal(mp.rng_normal(seed, 1001), ref.rng_normal(seed, 1001))
