@@ -3,6 +3,7 @@
 // at_linear per element (see device.cuh); 8 elements per thread per
 // iteration with 16-byte loads and stores, grid-stride over a grid sized to
 // the SM count.
+#include <cstdlib>
 #include <type_traits>
 
 #include "device.cuh"
@@ -53,12 +54,11 @@ template <> __device__ __forceinline__ uint16_t cvt1<double, uint16_t>(double x)
 template <> __device__ __forceinline__ float cvt1<double, float>(double x) { return d2f(x); }
 template <> __device__ __forceinline__ double cvt1<double, double>(double x) { return x; }
 
-// Same-width and narrowing casts: 8 elements per thread per iteration
-// (U groups loaded before any is converted and stored; U = 1 measured best).
-template <typename TI, typename TO>
+// Same-width, narrowing and 2x-widening casts: 8 elements per thread per
+// iteration, U groups loaded before any is converted and stored.
+template <typename TI, typename TO, int U>
 __global__ void __launch_bounds__(256) convert_vec_kernel(const TI* __restrict__ in,
                                                           TO* __restrict__ out, int64_t n8) {
-    constexpr int U = 1;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     for (; t + (U - 1) * stride < n8; t += U * stride) {
@@ -179,6 +179,27 @@ __global__ void __launch_bounds__(256) convert_2d_kernel(const TI* __restrict__ 
     }
 }
 
+// Tuning knobs (environment, read once; tools/cast_sweep.py): CTAs per SM of
+// the stream kernels, groups in flight per thread, staged widening on/off.
+struct CastTune {
+    int ctas_per_sm = 4, unroll = 1, widen_smem = 1, widen_ctas = 4;
+};
+const CastTune& cast_tune() {
+    static const CastTune t = [] {
+        CastTune c;
+        auto env = [](const char* k, int d) {
+            const char* e = getenv(k);
+            return e ? atoi(e) : d;
+        };
+        c.ctas_per_sm = env("MPCR_CAST_CTAS", c.ctas_per_sm);
+        c.unroll = env("MPCR_CAST_U", c.unroll);
+        c.widen_smem = env("MPCR_CAST_WIDEN_SMEM", c.widen_smem);
+        c.widen_ctas = env("MPCR_CAST_WIDEN_CTAS", c.widen_ctas);
+        return c;
+    }();
+    return t;
+}
+
 template <typename TI, typename TO>
 void run_convert(Ctx* ctx, cudaStream_t s, const void* src, int64_t lds, void* dst, int64_t ldd,
                  int64_t rows, int64_t cols) {
@@ -186,14 +207,15 @@ void run_convert(Ctx* ctx, cudaStream_t s, const void* src, int64_t lds, void* d
     TO* out = static_cast<TO*>(dst);
     const int64_t n = rows * cols;
     if (n == 0) return;
+    const CastTune& tn = cast_tune();
     const bool contiguous = (lds == rows && ldd == rows) || cols == 1;
     const bool aligned = (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-    if (contiguous && aligned && sizeof(TO) == 8 && sizeof(TI) < 8) {
+    if (contiguous && aligned && sizeof(TO) == 8 && sizeof(TI) < 8 && tn.widen_smem) {
         constexpr int EIN = 16 / sizeof(TI);
         const int64_t n16 = n / EIN;
         if (n16 > 0) {
-            convert_widen_smem_kernel<TI, TO><<<4 * ctx->sm_count, 256, 0, s>>>(in, out, n16);
+            convert_widen_smem_kernel<TI, TO><<<tn.widen_ctas * ctx->sm_count, 256, 0, s>>>(in, out, n16);
             count_launch(ctx);
         }
         const int64_t done = n16 * EIN;
@@ -219,8 +241,13 @@ void run_convert(Ctx* ctx, cudaStream_t s, const void* src, int64_t lds, void* d
     } else if (contiguous && aligned) {
         const int64_t n8 = n / 8;
         if (n8 > 0) {
-            convert_vec_kernel<TI, TO><<<grid_for(n8, 256, ctx->sm_count, 4), 256, 0, s>>>(
-                in, out, n8);
+            const int g = grid_for(n8, 256, ctx->sm_count, tn.ctas_per_sm);
+            if (tn.unroll >= 4)
+                convert_vec_kernel<TI, TO, 4><<<g, 256, 0, s>>>(in, out, n8);
+            else if (tn.unroll == 2)
+                convert_vec_kernel<TI, TO, 2><<<g, 256, 0, s>>>(in, out, n8);
+            else
+                convert_vec_kernel<TI, TO, 1><<<g, 256, 0, s>>>(in, out, n8);
             count_launch(ctx);
         }
         const int64_t done = n8 * 8;
