@@ -312,11 +312,19 @@ mp_status mp_nccl_unique_id(unsigned char* out128);
 mp_status mp_dist_create(mp_ctx ctx, int rank, int world, int P, int Q,
                          const unsigned char* uid128, mp_dist* out);
 mp_status mp_dist_destroy(mp_dist d);
+/* Test harness: `world` ranks simulated on ONE GPU in one process (rank r on
+ * ctxs[r], each context with its own streams), collectives as event-ordered
+ * device copies; the ranks must run concurrently from `world` host threads.
+ * Exercises the multi-rank executor bit for bit without a second GPU. */
+mp_status mp_dist_create_sim(mp_ctx* ctxs, int world, int P, int Q, mp_dist* out);
 /* Owner rank of tile (i, j). */
 int mp_dist_owner(int64_t i, int64_t j, int P, int Q);
 /* The per-rank action list the distributed chol executes, as int32 records
- * {op, k, i, j, root, prec} (op: 1 POTRF, 2 BCAST_DIAG, 3 TRSM, 4
- * BCAST_PANEL, 5 UPDATE).  actions may be NULL to query *count. */
+ * {op, k, i, j, root, prec, comm} (op: 1 POTRF, 2 BCAST_DIAG, 3 TRSM, 4
+ * BCAST_PANEL, 5 UPDATE; root: global rank; comm: 0 world, 1 this rank's
+ * process row, 2 its process column).  L_kk^-1 goes down process column
+ * k mod Q; panel tile L_ik along process row i mod P, then down process
+ * column i mod Q (P + Q - 2 copies).  actions may be NULL to query *count. */
 mp_status mp_dist_schedule(int rank, int P, int Q, int64_t tiles, const int* precisions,
                            int32_t* actions, int64_t capacity, int64_t* count);
 /* MPCRTile whose lower-triangle tiles are distributed; this rank stores only

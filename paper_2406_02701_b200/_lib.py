@@ -108,6 +108,7 @@ SIGNATURES = {
     # multi-GPU (2D block-cyclic MPCRTile)
     "mp_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "mp_dist_create": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(_vp)]),
+    "mp_dist_create_sim": (C.c_int, [C.POINTER(_vp), C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]),
     "mp_dist_destroy": (C.c_int, [_vp]),
     "mp_dist_owner": (C.c_int, [_i64, _i64, C.c_int, C.c_int]),
     "mp_dist_schedule": (C.c_int, [C.c_int, C.c_int, C.c_int, _i64, C.POINTER(C.c_int),

@@ -183,7 +183,13 @@ struct StepLists {
     size_t digits[3] = {0, 0, 0};  // INT8 digit slicing of FP16 panel tiles (same split)
     int64_t n_digits[3] = {0, 0, 0};
     UpLists up[3];  // 0: tile column k+1 below the diagonal, 1: the rest, 2: tile (k+1, k+1)
-    std::vector<std::pair<int, int>> bcasts;  // (i, root) panel broadcasts
+    bool diag_bcast = false;  // receive / send L_kk^-1 down this process column
+    struct Bcast {
+        int i, root, comm;
+    };
+    // panel broadcasts in schedule order (row then column per tile), [0]: the
+    // head tile k+1 (critical path), [1]: the rest of the column
+    std::vector<Bcast> bcasts[2];
 };
 
 }  // namespace
@@ -208,7 +214,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     auto read_info = [&]() {
         int64_t info = -1;
         MP_CUDA(cudaMemcpyAsync(&info, dinfo, sizeof(info), cudaMemcpyDeviceToHost, s));
-        MP_CUDA(cudaStreamSynchronize(s));
+        // multi-rank: poll NCCL for asynchronous errors instead of blocking
+        dist_wait(t.dist, s);
         return info;
     };
     // Graph replay: the factorization of this tile was captured once (lists,
@@ -218,7 +225,16 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         const char* e = getenv("MPCR_GRAPH");
         return !(e && e[0] == '0');
     }();
-    const bool want_graph = graph_env && !c->prof.enabled && !(t.dist && t.dist->world > 1);
+    // multi-rank (real NCCL) factorizations are captured too: NCCL
+    // collectives are graph-capturable; the single-GPU rank simulation is not
+    // (its host rendezvous), and MPCR_DIST_GRAPH=0 keeps NCCL runs eager
+    static const bool dist_graph_env = [] {
+        const char* e = getenv("MPCR_DIST_GRAPH");
+        return !(e && e[0] == '0');
+    }();
+    const bool multi = t.dist && t.dist->world > 1;
+    const bool want_graph =
+        graph_env && !c->prof.enabled && !(multi && (t.dist->sim || !dist_graph_env));
     if (t.graph && t.graph_scr_gen != c->scr_gen) {
         // a context scratch slot the graph captured (POTRF barriers / leaf
         // inverses, 3xTF32 splits) was reallocated since: re-capture
@@ -299,7 +315,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         return !(e && e[0] == '0');
     }();
     // (also without lookahead, on one stream: the same launches, serialised)
-    const bool tsplit = tsplit_env && NT > 1 && P * Q == 1;
+    const bool tsplit = tsplit_env && NT > 1;
     std::vector<StepAcc> acc(NT);
     std::vector<StepLists> steps(NT);
     const size_t nn0 = static_cast<size_t>(nb) * nb;
@@ -339,6 +355,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             A.digits[hd].push_back(
                 OzSliceItem{pan(MP_HALF, i, k), dig(i, k), rex(i, k), ndg(i, k), nb, nb, nb, nb, tt, 0, 0});
     };
+    std::vector<char> have(NT * NT, 0);  // panel tile (i, k) present on this rank (conversions made)
     for (const DistAction& a : sched) {
         StepAcc& A = acc[a.k];
         StepLists& L = steps[a.k];
@@ -362,9 +379,13 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 if (P * Q == 1) consumers(k, i, A);
                 break;
             }
+            case DA_BCAST_DIAG:
+                L.diag_bcast = true;
+                break;
             case DA_BCAST_PANEL:
-                L.bcasts.push_back({static_cast<int>(i), a.root});
-                consumers(k, i, A);
+                L.bcasts[(tsplit && i == k + 1) ? 0 : 1].push_back({static_cast<int>(i), a.root, a.comm});
+                if (!have[k * NT + i]) consumers(k, i, A);
+                have[k * NT + i] = 1;
                 break;
             case DA_UPDATE: {
                 UpAcc& U = A.up[j != k + 1 ? 1 : i == j ? 2 : 0];
@@ -564,6 +585,24 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         }
     };
 
+    // Distributed: panel tiles of one part along their process rows (one NCCL
+    // group), then down their process columns (a second group: a column
+    // root receives the tile in the row broadcast).
+    auto broadcast = [&](int64_t k, int part, cudaStream_t st) {
+        const auto& B = steps[k].bcasts[part];
+        for (int c : {DC_ROW, DC_COL}) {
+            bool any = false;
+            for (const auto& br : B) any = any || br.comm == c;
+            if (!any) continue;
+            dist_group_start(t.dist);
+            for (const auto& br : B)
+                if (br.comm == c) {
+                    const mp_precision q = t.p(br.i, k);
+                    dist_bcast(t.dist, pan(q, br.i, k), tt * elem_bytes(q), br.root, static_cast<DistComm>(c), st);
+                }
+            dist_group_end(t.dist);
+        }
+    };
     // Panel k, critical part (stream st): factor A_kk, invert, round Linv to
     // the panel precisions, TRSM of the head tile (k+1) and its lookahead
     // conversions.  Without the head/tail split the whole column follows here.
@@ -599,9 +638,9 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             }
         }
         if (k + 1 == NT) return;
-        // distributed: the FP64 inverse of L_kk travels from its owner
-        if (t.dist && t.dist->world > 1)
-            dist_bcast(t.dist, linv64, nn * sizeof(double), dist_owner(k, k, P, Q), st);
+        // distributed: the FP64 inverse of L_kk travels down process column k mod Q
+        if (L.diag_bcast)
+            dist_bcast(t.dist, linv64, nn * sizeof(double), dist_owner(k, k, P, Q), DC_COL, st);
         // Linv rounded to the panel precisions (the reference rounds U_kk to
         // p_ik before trsm: U_kk.converted(p_ik)).  FP16 panels apply the
         // inverse as hi + lo FP16 halves accumulated in one FP32 accumulator:
@@ -619,23 +658,15 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         // the tile column has its update from step k-1
         if (before_trsm) MP_CUDA(cudaStreamWaitEvent(st, before_trsm, 0));
         trsm_part(k, 0, st);
+        broadcast(k, 0, st);  // distributed: the head tile to its row and column
         convert_panel(k, 2, st);
     };
     // Panel k, the rest of the column (stream st): TRSM, broadcasts, lookahead
     // conversions.
     auto panel_tail = [&](int64_t k, cudaStream_t st) {
         if (k + 1 == NT) return;
-        const StepLists& L = steps[k];
         trsm_part(k, 1, st);
-        // distributed: every panel tile travels from its owner to all ranks
-        if (!L.bcasts.empty()) {
-            dist_group_start(t.dist);
-            for (const auto& br : L.bcasts) {
-                const mp_precision q = t.p(br.first, k);
-                dist_bcast(t.dist, pan(q, br.first, k), tt * elem_bytes(q), br.second, st);
-            }
-            dist_group_end(t.dist);
-        }
+        broadcast(k, 1, st);  // distributed: the rest of the column
         convert_panel(k, 0, st);
     };
 
@@ -966,7 +997,7 @@ void tile_nll(Ctx* c, mp_tile_s& t, const double* host_z, double jitter, double 
     for (int64_t i = 0; i < NT; ++i) {
         if (D) dist_allreduce_sum_f64(D, r + i * nb, nb, s);
         if (t.has(i, i)) launch_tile_trsv(c, s, t.p(i, i), t.ptr(i, i), nb, static_cast<int>(nb), r + i * nb);
-        if (D) dist_bcast(D, r + i * nb, nb * sizeof(double), dist_owner(i, i, D->P, D->Q), s);
+        if (D) dist_bcast(D, r + i * nb, nb * sizeof(double), dist_owner(i, i, D->P, D->Q), DC_WORLD, s);
         for (int q = 0; q < 3; ++q)
             if (cnt[i * 3 + q])
                 launch_tile_gemv(c, s, (mp_precision)q, ditems + off[i * 3 + q], cnt[i * 3 + q],

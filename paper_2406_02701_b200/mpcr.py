@@ -622,15 +622,16 @@ def dist_owner(i: int, j: int, P: int, Q: int) -> int:
 
 def dist_schedule(rank: int, P: int, Q: int, tiles: int, precisions=None) -> np.ndarray:
     """The rank's action list of the distributed tiled Cholesky, as an
-    (count, 6) int32 array of (op, k, i, j, root, precision) rows — the same
-    plan the GPU executor runs (csrc/dist.cpp)."""
+    (count, 7) int32 array of (op, k, i, j, root, precision, comm) rows (comm
+    0 world, 1 process row, 2 process column) — the same plan the GPU
+    executor runs (csrc/dist.cpp)."""
     if precisions is None:
         precisions = np.full((tiles, tiles), 2)
     pcol = np.asfortranarray(np.asarray(precisions, dtype=np.int32)).ravel(order="F")
     cnt = C.c_int64()
     pp = pcol.ctypes.data_as(C.POINTER(C.c_int))
     check(lib().mp_dist_schedule(rank, P, Q, tiles, pp, None, 0, C.byref(cnt)))
-    out = np.zeros((cnt.value, 6), dtype=np.int32)
+    out = np.zeros((cnt.value, 7), dtype=np.int32)
     check(lib().mp_dist_schedule(rank, P, Q, tiles, pp, out.ctypes.data_as(C.POINTER(C.c_int32)),
                                  cnt.value, C.byref(cnt)))
     return out
@@ -657,6 +658,23 @@ class ProcessGrid:
 
     def owner(self, i: int, j: int) -> int:
         return dist_owner(i, j, self.P, self.Q)
+
+    @classmethod
+    def simulated(cls, ctxs, P: int, Q: int) -> list:
+        """P x Q ranks on ONE GPU (test harness, mp_dist_create_sim): one grid
+        handle per rank, rank r on ctxs[r]; run the ranks' calls concurrently
+        from one thread each."""
+        world = P * Q
+        arr = (C.c_void_p * world)(*[c.h for c in ctxs])
+        hs = (C.c_void_p * world)()
+        check(lib().mp_dist_create_sim(arr, world, P, Q, hs))
+        out = []
+        for r in range(world):
+            g = cls.__new__(cls)
+            g.ctx, g.rank, g.world, g.P, g.Q = ctxs[r], r, world, P, Q
+            g.h = C.c_void_p(hs[r])
+            out.append(g)
+        return out
 
     def close(self):
         if self.h:
