@@ -348,9 +348,17 @@ constexpr int c2_chunk() { return NST == 5 ? C_CHUNK : C_CHUNK / 2; }
 template <int NST>
 constexpr int smem2_bytes() { return NST * (A_STAGE + B2_STAGE) + 2 * c2_chunk<NST>() + 1024 + 256; }
 
-template <bool A_MN, bool B_MN, typename TC, int STAGES2>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
+// MC = 2: two pairs per cluster (4 CTAs) compute horizontally adjacent
+// 256 x 256 tiles (same A rows, N-blocks 2q and 2q+1); each CTA loads half of
+// its 128 A rows and multicasts them to the CTA of the other pair that needs
+// the same rows, so the pair-of-pairs reads A from L2 once (48 KB of L2->SMEM
+// traffic per pair and K step instead of 64 KB).  Requires MN-major A (64-row
+// boxes) and an even number of N-blocks.  A stage is free again only once
+// both pairs' MMAs have read it (empty barriers count MC commits).
+template <bool A_MN, bool B_MN, typename TC, int STAGES2, int MC>
+__global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(NTHREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ Params p) {
+    static_assert(MC == 1 || (MC == 2 && A_MN), "multicast pairs need MN-major A");
     constexpr int ES = 2, BK = 64, BW = 64;
     constexpr int BOX = BW * BK * ES;          // 8 KB MN-major box
     constexpr int KSTEP_MN = (32 / ES) * 128;  // UMMA K (32 bytes) in MN-major rows
@@ -372,7 +380,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     auto cbuf_of = [&](int b) { return reinterpret_cast<TC*>(reinterpret_cast<uint8_t*>(cbuf0) + b * C2_CHUNK); };
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const uint32_t rank = ptx::cluster_ctarank();
+    const uint32_t crank = ptx::cluster_ctarank();
+    const uint32_t rank = crank & 1u;  // CTA within its pair
+    const uint32_t pair = crank >> 1;  // pair within the cluster (MC == 2)
+    const uint32_t lead = crank & ~1u;  // the pair's even CTA
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&p.map_a[0]);
         ptx::tma_prefetch_desc(&p.map_a[1]);
@@ -381,7 +392,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         ptx::tma_prefetch_desc(&p.map_c);
         for (int s = 0; s < STAGES2; ++s) {
             ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], 1);
+            ptx::mbar_init(&empty[s], MC);  // one MMA commit per pair of the cluster
         }
         for (int s = 0; s < 2; ++s) {
             ptx::mbar_init(&tfull[s], 1);
@@ -398,9 +409,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     const int mpairs = (p.mblocks + 1) / 2;  // an odd last block pairs with an out-of-range one
-    const int tiles_per_prob = mpairs * p.nblocks;
+    const int nq = p.nblocks / MC;           // N-block groups (one block per pair)
+    const int tiles_per_prob = mpairs * nq;
     const int64_t total = static_cast<int64_t>(p.nprob) * tiles_per_prob;
-    const int64_t cid = blockIdx.x >> 1;
+    const int64_t cid = blockIdx.x / (2 * MC);
     const int64_t wave0 = (cid / p.lanes) * static_cast<int64_t>(p.lanes) * p.per;
     const int64_t t_first = wave0 + cid % p.lanes;
     const int64_t t_end = min(total, wave0 + static_cast<int64_t>(p.lanes) * p.per);
@@ -415,17 +427,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         const int64_t pi = t / tiles_per_prob;
         const int r = static_cast<int>(t - pi * tiles_per_prob);
         pr = p.problems ? p.problems[pi] : p.single;
-        const int per_group = GROUP_M * p.nblocks;
+        const int per_group = GROUP_M * nq;
         const int g = r / per_group, rem = r - g * per_group;
         const int gm = min(GROUP_M, mpairs - g * GROUP_M);  // the last group may be narrower
         m0 = (g * GROUP_M + rem % gm) * (2 * BM) + static_cast<int>(rank) * BM;
-        n0 = (rem / gm) * BN;
+        n0 = ((rem / gm) * MC + static_cast<int>(pair)) * BN;
     };
 
     if (warp == 0) {
         // ===== TMA producer (both CTAs): own A rows, own half of B =====
         if (lane == 0) {
-            const uint32_t full0 = ptx::mapa_shared(ptx::smem_u32(full), 0);  // even CTA's barriers
+            const uint32_t full0 = ptx::mapa_shared(ptx::smem_u32(full), lead);  // the pair's even CTA
+            // multicast A: this CTA's A box `pair` also lands in the CTA of the
+            // other pair holding the same rows (same `rank`)
+            const uint16_t a_mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + 2)));
             int stage = 0;
             uint32_t phase = 0;
             for (int64_t t = t_first; t < t_end; t += ncl) {
@@ -443,7 +458,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                     const int kk = (kb - sg * p.kblocks1) * BK;
                     const CUtensorMap* ma = &p.map_a[p.seg_a[sg]];
                     const CUtensorMap* mb = &p.map_b[p.seg_b[sg]];
-                    if (A_MN) {
+                    if (MC == 2) {
+                        ptx::tma_load_3d_2sm_mc(a_dst + pair * BOX, ma, ptx::smem_u32(&full[stage]) & ptx::PEER_BIT_MASK,
+                                                m0 + static_cast<int>(pair) * BW, kk, pr.a_tile, a_mask);
+                    } else if (A_MN) {
 #pragma unroll
                         for (int j = 0; j < BM / BW; ++j)
                             ptx::tma_load_3d_2sm(a_dst + j * BOX, ma, fb, m0 + j * BW, kk, pr.a_tile);
@@ -489,13 +507,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
                                                  : ptx::umma_desc_sw128(b_base + k * 32, 0, 1024);
                         ptx::mma_f16_ss_2sm(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
                     }
-                    ptx::mma_commit_2sm_mc(&empty[stage], 0x3);
+                    // both pairs' producers write this stage (A multicast): free it in all CTAs
+                    ptx::mma_commit_2sm_mc(&empty[stage], MC == 2 ? 0xF : 0x3);
                     if (++stage == STAGES2) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                ptx::mma_commit_2sm_mc(&tfull[acc], 0x3);
+                ptx::mma_commit_2sm_mc(&tfull[acc], static_cast<uint16_t>(0x3u << lead));
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -531,7 +550,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
         const int q = warp - 4;
         const int r = q * 32 + lane;
         const bool is_leader = threadIdx.x == 128;
-        const uint32_t tempty0 = ptx::mapa_shared(ptx::smem_u32(tempty), 0);
+        const uint32_t tempty0 = ptx::mapa_shared(ptx::smem_u32(tempty), lead);
         int acc = 0;
         uint32_t acc_phase = 0, g = 0;
         for (int64_t t = t_first; t < t_end; t += ncl) {
@@ -669,28 +688,49 @@ void launch_kernel(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total, int
 }
 
 
-template <bool A_MN, bool B_MN, typename TC, int NST>
+template <bool A_MN, bool B_MN, typename TC, int NST, int MC>
 void launch_kernel2(Ctx* ctx, cudaStream_t s, const Params& p, int64_t total_pairs, int tiles_per_cta) {
-    auto kern = gemm_tc2_kernel<A_MN, B_MN, TC, NST>;
+    auto kern = gemm_tc2_kernel<A_MN, B_MN, TC, NST, MC>;
     constexpr int SMEM2_BYTES = smem2_bytes<NST>();
     static unsigned long long configured = 0;  // per-device bitmask
+    static int max_clusters[64] = {};
+    int dev = 0;
+    MP_CUDA(cudaGetDevice(&dev));
     if (first_on_device(configured)) {
         MP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM2_BYTES));
+        // clusters of 2 MC CTAs (one per SM) that fit at once: with MC = 2 a
+        // GPC whose SM count is not a multiple of 4 leaves SMs unused
+        cudaLaunchConfig_t oc = {};
+        oc.gridDim = dim3(static_cast<unsigned>(2 * MC * (ctx->sm_count / (2 * MC))));
+        oc.blockDim = dim3(NTHREADS);
+        oc.dynamicSmemBytes = SMEM2_BYTES;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, kern, &oc) != cudaSuccess || nc < 1) {
+            (void)cudaGetLastError();
+            nc = ctx->sm_count / (2 * MC);
+        }
+        max_clusters[dev & 63] = nc;
+        static const bool dbg = getenv("MPCR_DEBUG_TC") != nullptr;
+        if (dbg) std::fprintf(stderr, "[mpcr] pair kernel MC=%d: %d clusters resident\n", MC, nc);
     }
-    const int64_t clusters = persistent_grid(total_pairs, ctx->sm_count / 2, tiles_per_cta);
+    const int resident = std::max(1, std::min(max_clusters[dev & 63], ctx->sm_count / (2 * MC)));
+    const int64_t units = total_pairs / MC;  // a cluster takes MC horizontally adjacent pair tiles
+    // bounded persistence counts pair tiles: a cluster unit holds MC of them
+    const int tpc = tiles_per_cta > 0 ? std::max(1, tiles_per_cta / MC) : tiles_per_cta;
+    const int64_t clusters = persistent_grid(units, resident, tpc);
     Params q = p;
-    q.lanes = static_cast<int32_t>(std::min<int64_t>(ctx->sm_count / 2, clusters));
-    q.per = static_cast<int32_t>((total_pairs + clusters - 1) / clusters);
+    q.lanes = static_cast<int32_t>(std::min<int64_t>(resident, clusters));
+    q.per = static_cast<int32_t>((units + clusters - 1) / clusters);
     static const bool strided = [] {  // MPCR_UNIT_STRIDED=1: classic grid-stride assignment
         const char* e = getenv("MPCR_UNIT_STRIDED");
         return e && e[0] == '1';
     }();
     if (strided) {
         q.lanes = static_cast<int32_t>(clusters);
-        q.per = static_cast<int32_t>((total_pairs + clusters - 1) / clusters);
+        q.per = static_cast<int32_t>((units + clusters - 1) / clusters);
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(static_cast<unsigned>(2 * clusters));
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * MC * clusters));
     cfg.blockDim = dim3(NTHREADS);
     cfg.dynamicSmemBytes = SMEM2_BYTES;
     cfg.stream = s;
@@ -796,17 +836,32 @@ void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
             std::fprintf(stderr, "[mpcr] tc2 launch %lld: C %s, %d problem(s) of %dx%dx%d, beta %g\n",
                          static_cast<long long>(dbg_idx++), half_c ? "half" : "single", p.nprob, p.M,
                          p.N, p.K, p.beta);
+        // MPCR_TC4=1: clusters of two pairs with A multicast (even N-block
+        // count, MN-major A, six stages)
+        static const bool tc4_env = [] {
+            const char* e = getenv("MPCR_TC4");
+            return e && e[0] == '1';
+        }();
+        if (tc4_env && a_mn && p.nblocks % 2 == 0 && tc2_stages == 6) {
+            if (b_mn)
+                half_c ? launch_kernel2<true, true, uint16_t, 6, 2>(ctx, s, p, pairs, g.tiles_per_cta)
+                       : launch_kernel2<true, true, float, 6, 2>(ctx, s, p, pairs, g.tiles_per_cta);
+            else
+                half_c ? launch_kernel2<true, false, uint16_t, 6, 2>(ctx, s, p, pairs, g.tiles_per_cta)
+                       : launch_kernel2<true, false, float, 6, 2>(ctx, s, p, pairs, g.tiles_per_cta);
+            return;
+        }
 #define MP_TC2(AM, BMJ)                                                                 \
         if (a_mn == AM && b_mn == BMJ) {                                                \
             if (tc2_stages == 6) {                                                      \
                 if (half_c)                                                             \
-                    launch_kernel2<AM, BMJ, uint16_t, 6>(ctx, s, p, pairs, g.tiles_per_cta); \
+                    launch_kernel2<AM, BMJ, uint16_t, 6, 1>(ctx, s, p, pairs, g.tiles_per_cta); \
                 else                                                                    \
-                    launch_kernel2<AM, BMJ, float, 6>(ctx, s, p, pairs, g.tiles_per_cta); \
+                    launch_kernel2<AM, BMJ, float, 6, 1>(ctx, s, p, pairs, g.tiles_per_cta); \
             } else if (half_c) {                                                        \
-                launch_kernel2<AM, BMJ, uint16_t, 5>(ctx, s, p, pairs, g.tiles_per_cta); \
+                launch_kernel2<AM, BMJ, uint16_t, 5, 1>(ctx, s, p, pairs, g.tiles_per_cta); \
             } else {                                                                    \
-                launch_kernel2<AM, BMJ, float, 5>(ctx, s, p, pairs, g.tiles_per_cta);   \
+                launch_kernel2<AM, BMJ, float, 5, 1>(ctx, s, p, pairs, g.tiles_per_cta);   \
             }                                                                           \
             return;                                                                     \
         }

@@ -211,6 +211,19 @@ __device__ __forceinline__ void tma_load_3d_2sm(void* dst, const CUtensorMap* ma
         "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
+// Same, multicast to the CTAs of `mask` (same shared-memory offset in each);
+// every destination's bytes complete on the barrier at `bar`'s offset in the
+// even CTA of that destination's pair (bar: a CTA-local address with the pair
+// bit cleared, as CUTLASS's SM100_TMA_2SM_LOAD_MULTICAST passes it).
+__device__ __forceinline__ void tma_load_3d_2sm_mc(void* dst, const CUtensorMap* map, uint32_t bar_pair,
+                                                   int c0, int c1, int c2, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_pair), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+        : "memory");
+}
+constexpr uint32_t PEER_BIT_MASK = 0xFEFFFFFFu;  // clears the CTA-pair bit of a shared::cluster address
 template <int NCOLS>
 __device__ __forceinline__ void tmem_alloc_2sm(uint32_t* smem_dst) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(smem_dst)),

@@ -816,8 +816,13 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         const bool wb_async = wb_env && tsplit;
         for (int64_t k = 0; k < NT; ++k) {
             if (la) MP_CUDA(cudaStreamWaitEvent(s, ev_panel[k], 0));
-            convert_panel(k, 1, s);
-            update_phase(k, 1, s, bulk_tpc);
+            // MPCR_CHAIN_ONLY=1 (diagnostic; the factor is meaningless): skip
+            // the bulk update so a timing measures the critical chain alone
+            static const bool chain_only = getenv("MPCR_CHAIN_ONLY") != nullptr;
+            if (!chain_only) {
+                convert_panel(k, 1, s);
+                update_phase(k, 1, s, bulk_tpc);
+            }
             if (!wb_async || k + 1 >= NT) write_back(k, s);
             if (la) MP_CUDA(cudaEventRecord(ev_rest[k], s));
             if (k + 1 < NT) {

@@ -553,3 +553,52 @@ def test_dispatch_registry_ops(ctx, ref, rng, pa, pb):
         mp.dispatch.execute(mp.dispatch.resolve("add", pb, pb), "add", da, db) if pa != pb else \
             mp.dispatch.execute(mp.dispatch.resolve("add", D if pa != D else H, pb), "add", da, db)
     assert e.value.kind == "PrecisionMismatch"
+
+
+_TC4_PROBE = r"""
+import hashlib, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2406_02701_b200 as mp
+ctx = mp.Context(0)
+h = hashlib.sha256()
+for (m, n, k, ta, tb, pc) in ((4096, 4096, 1024, False, True, 0), (3000, 2048, 700, False, False, 1),
+                              (2048, 1536, 4096, False, True, 1), (4096, 4096, 4096, True, False, 0)):
+    A = mp.random_uniform_matrix(k if ta else m, m if ta else k, 11)
+    B = mp.random_uniform_matrix(n if tb else k, k if tb else n, 12)
+    a = mp.MPArray.from_numpy(A - 0.5, mp.Precision.Half, ctx)
+    b = mp.MPArray.from_numpy(B - 0.5, mp.Precision.Half, ctx)
+    c = mp.MPArray.from_numpy(np.full((m, n), 0.25), mp.Precision(pc), ctx)
+    mp.linalg.gemm(a, b, c, ta, tb, 1.0, -1.0)
+    h.update(c.storage().tobytes())
+n, nb = 8192, 1024
+nt = n // nb
+i, j = np.indices((nt, nt))
+g = np.where(i == j, 2, np.where(abs(i - j) == 1, 1, 0))
+t = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+t.fill_matern(91, 0.5, 0.03, 1.0)
+mp.tile_chol(t)
+h.update(np.ascontiguousarray(t.to_numpy()).tobytes())
+print(h.hexdigest())
+"""
+
+
+def test_gemm_pair_multicast_bitwise():
+    """MPCR_TC4=1 (clusters of two CTA pairs sharing A by TMA multicast) only
+    changes how operands reach shared memory: dense FP16 GEMMs (even and odd
+    N-block counts, ragged M) and an nb = 1024 tiled Cholesky are bit-identical
+    to the pair kernel."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+    def run(tc4):
+        e = dict(os.environ, MPCR_TC4=tc4)
+        out = subprocess.run([sys.executable, "-c", _TC4_PROBE, root], env=e, capture_output=True, text=True,
+                             timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        return out.stdout.strip().splitlines()[-1]
+
+    assert run("1") == run("0")
