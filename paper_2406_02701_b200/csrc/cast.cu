@@ -179,25 +179,35 @@ __global__ void __launch_bounds__(256) convert_2d_kernel(const TI* __restrict__ 
     }
 }
 
-// Tuning knobs (environment, read once; tools/cast_sweep.py): CTAs per SM of
-// the stream kernels, groups in flight per thread, staged widening on/off.
+// Stream-kernel shape per direction (CTAs per SM, 8-element groups in flight
+// per thread, shared-memory staged widening), from the sweep in
+// profiles/r02_cast_sweep.txt (tools/cast_sweep.py): the 8 -> 4 byte
+// narrowing wants fewer CTAs with four groups in flight (+15 %), 4 -> 2 many
+// CTAs, 4 -> 8 widening the staged kernel with 16 CTAs per SM.  The
+// MPCR_CAST_* variables override every direction (sweeps).
 struct CastTune {
-    int ctas_per_sm = 4, unroll = 1, widen_smem = 1, widen_ctas = 4;
+    int ctas_per_sm, unroll, widen_smem, widen_ctas;
 };
-const CastTune& cast_tune() {
-    static const CastTune t = [] {
-        CastTune c;
-        auto env = [](const char* k, int d) {
+template <typename TI, typename TO>
+CastTune cast_tune() {
+    constexpr int si = sizeof(TI), so = sizeof(TO);
+    CastTune c{4, 1, 1, 4};
+    if (si == 8 && so == 4) c = {2, 4, 1, 4};
+    if (si == 4 && so == 2) c = {16, 4, 1, 4};
+    if (si == 4 && so == 8) c = {4, 1, 1, 16};
+    if (si == 2 && so == 4) c = {4, 1, 0, 8};  // half -> single: staged widening off unless swept on
+    static const CastTune env = [] {
+        auto rd = [](const char* k) {
             const char* e = getenv(k);
-            return e ? atoi(e) : d;
+            return e ? atoi(e) : -1;
         };
-        c.ctas_per_sm = env("MPCR_CAST_CTAS", c.ctas_per_sm);
-        c.unroll = env("MPCR_CAST_U", c.unroll);
-        c.widen_smem = env("MPCR_CAST_WIDEN_SMEM", c.widen_smem);
-        c.widen_ctas = env("MPCR_CAST_WIDEN_CTAS", c.widen_ctas);
-        return c;
+        return CastTune{rd("MPCR_CAST_CTAS"), rd("MPCR_CAST_U"), rd("MPCR_CAST_WIDEN_SMEM"), rd("MPCR_CAST_WIDEN_CTAS")};
     }();
-    return t;
+    if (env.ctas_per_sm > 0) c.ctas_per_sm = env.ctas_per_sm;
+    if (env.unroll > 0) c.unroll = env.unroll;
+    if (env.widen_smem >= 0) c.widen_smem = env.widen_smem;
+    if (env.widen_ctas > 0) c.widen_ctas = env.widen_ctas;
+    return c;
 }
 
 template <typename TI, typename TO>
@@ -207,11 +217,11 @@ void run_convert(Ctx* ctx, cudaStream_t s, const void* src, int64_t lds, void* d
     TO* out = static_cast<TO*>(dst);
     const int64_t n = rows * cols;
     if (n == 0) return;
-    const CastTune& tn = cast_tune();
+    const CastTune tn = cast_tune<TI, TO>();
     const bool contiguous = (lds == rows && ldd == rows) || cols == 1;
     const bool aligned = (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
                          (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-    if (contiguous && aligned && sizeof(TO) == 8 && sizeof(TI) < 8 && tn.widen_smem) {
+    if (contiguous && aligned && sizeof(TO) > sizeof(TI) && tn.widen_smem) {
         constexpr int EIN = 16 / sizeof(TI);
         const int64_t n16 = n / EIN;
         if (n16 > 0) {
