@@ -408,7 +408,7 @@ void launch_dmma_gemm(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count
     const bool small = ctas < ctx->sm_count;
     DmmaArgs h = g;
     h.ksplit = 1;
-    if (small) {
+    if (small && g.allow_ksplit) {
         // latency-bound launches (TRTRI levels): split K over a cluster while
         // the 64x64 tiles leave most SMs idle, keeping >= 2 slabs per CTA
         const int64_t t64m = (g.m + 63) / 64, t64n = (g.n + 63) / 64;

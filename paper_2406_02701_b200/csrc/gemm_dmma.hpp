@@ -29,6 +29,12 @@ struct DmmaArgs {
     // op(B)[k][n] == 0 for k > n (B = L^T of a lower-triangular L, the TRSM
     // as X = A L^-T): each CTA stops its K loop at its last column
     bool k_tri = false;
+    // The launcher may split K over a cluster when a launch leaves SMs idle;
+    // that changes the summation order with the launch's problem COUNT, so
+    // the scheduler's update and tail-TRSM lists (whose counts differ between
+    // a single-GPU and a distributed run) turn it off: a tile's result then
+    // depends only on its own operands.
+    bool allow_ksplit = true;
 };
 
 void launch_dmma_gemm(Ctx* ctx, cudaStream_t s, const DmmaArgs& g, int64_t count);

@@ -575,6 +575,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 d.k_tri = true;
                 d.pin_b = MP_DOUBLE;
                 d.exclusive = hb == 0;  // the head tile is on the critical path
+                d.allow_ksplit = hb == 0;  // one tile on every rank: grouping-independent
                 ProfScope ps(c, MP_PROF_TRSM, st, static_cast<double>(nb) * nb * nb * L.n_trsm_p[hb][q]);
                 launch_dmma_gemm(c, st, d, L.n_trsm_p[hb][q]);
                 continue;
@@ -750,6 +751,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                     d.pin_b = pb;
                     d.pout = c2 ? MP_DOUBLE : MP_SINGLE;
                     d.exclusive = part == 2;  // the diagonal SYRK feeding the next POTRF
+                    d.allow_ksplit = part == 2;  // (k+1, k+1) alone on every rank
                     ProfScope ps(c, c2 ? MP_PROF_GEMM_F64 : MP_PROF_GEMM_F32, st,
                                  2.0 * static_cast<double>(nb) * nb * nb * cnt);
                     launch_dmma_gemm(c, st, d, cnt);
