@@ -66,7 +66,16 @@ struct Params {
     // clusters resident together (one wave of `lanes`) work on neighbouring
     // units through one contiguous chunk of the list instead of striding it
     int32_t lanes, per;
+    // B = L^-T of a lower-triangular L (the panel TRSM X = A L^-T): a unit
+    // with output columns [n0, n0 + BN) needs only K < n0 + BN
+    int32_t k_tri;
 };
+
+// K blocks per segment a unit with output columns from n0 runs, and the
+// segment / K offset of its block kb.
+__device__ __forceinline__ int unit_kb1(const Params& p, int n0, int bn, int bk) {
+    return p.k_tri ? min(p.kblocks1, (n0 + bn + bk - 1) / bk) : p.kblocks1;
+}
 
 __device__ __forceinline__ bool skip_tile(const TcProblem& pr, int m0, int n0) {
     return pr.lower_only && (m0 + BM - 1 < n0);
@@ -162,14 +171,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
                 int m0, n0;
                 decode(t, pr, m0, n0);
                 if (skip_tile(pr, m0, n0)) continue;
-                for (int kb = 0; kb < p.kblocks; ++kb) {
+                const int kb1 = unit_kb1(p, n0, BN, BK), nkb = (p.kblocks / p.kblocks1) * kb1;
+                for (int kb = 0; kb < nkb; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     ptx::mbar_arrive_expect_tx(&full[stage], A_STAGE + B_STAGE);
                     uint8_t* a_dst = sA + stage * A_STAGE;
                     uint8_t* b_dst = sB + stage * B_STAGE;
                     // K segments: (A|A_lo) x (B|B_lo) products into one accumulator
-                    const int sg = kb / p.kblocks1;
-                    const int kk = (kb - sg * p.kblocks1) * BK;
+                    const int sg = kb / kb1;
+                    const int kk = (kb - sg * kb1) * BK;
                     const CUtensorMap* ma = &p.map_a[p.seg_a[sg]];
                     const CUtensorMap* mb = &p.map_b[p.seg_b[sg]];
                     if (A_MN) {
@@ -211,7 +221,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-                for (int kb = 0; kb < p.kblocks; ++kb) {
+                const int nkb = (p.kblocks / p.kblocks1) * unit_kb1(p, n0, BN, BK);
+                for (int kb = 0; kb < nkb; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     const uint32_t a_base = ptx::smem_u32(sA + stage * A_STAGE);
@@ -448,14 +459,17 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(NTHREADS, 1)
                 int m0, n0;
                 decode(t, pr, m0, n0);
                 const int nb0 = n0 + static_cast<int>(rank) * (BN / 2);
-                for (int kb = 0; kb < p.kblocks; ++kb) {
+                // (multicast pairs run the whole K: the two pairs' units must stay in lockstep)
+                const int kb1 = MC == 1 ? unit_kb1(p, n0, BN, BK) : p.kblocks1;
+                const int nkb = (p.kblocks / p.kblocks1) * kb1;
+                for (int kb = 0; kb < nkb; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], 2 * (A_STAGE + B2_STAGE));
                     const uint32_t fb = full0 + stage * 8;
                     uint8_t* a_dst = sA + stage * A_STAGE;
                     uint8_t* b_dst = sB + stage * B2_STAGE;
-                    const int sg = kb / p.kblocks1;
-                    const int kk = (kb - sg * p.kblocks1) * BK;
+                    const int sg = kb / kb1;
+                    const int kk = (kb - sg * kb1) * BK;
                     const CUtensorMap* ma = &p.map_a[p.seg_a[sg]];
                     const CUtensorMap* mb = &p.map_b[p.seg_b[sg]];
                     if (MC == 2) {
@@ -494,7 +508,11 @@ __global__ void __cluster_dims__(2 * MC, 1, 1) __launch_bounds__(NTHREADS, 1)
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-                for (int kb = 0; kb < p.kblocks; ++kb) {
+                TcProblem pr_;
+                int m0_, n0_;
+                decode(t, pr_, m0_, n0_);
+                const int nkb = (p.kblocks / p.kblocks1) * (MC == 1 ? unit_kb1(p, n0_, BN, BK) : p.kblocks1);
+                for (int kb = 0; kb < nkb; ++kb) {
                     ptx::mbar_wait(&full[stage], phase);
                     ptx::tc_fence_after();
                     const uint32_t a_base = ptx::smem_u32(sA + stage * A_STAGE);
@@ -822,6 +840,7 @@ void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
     const int bk = kind == 0 ? 64 : 32;
     p.kblocks1 = static_cast<int32_t>((g.k + bk - 1) / bk);
     p.kblocks = nseg * p.kblocks1;
+    p.k_tri = g.k_tri ? 1 : 0;
     const int64_t total = static_cast<int64_t>(p.nprob) * p.mblocks * p.nblocks;
     ProfScope ps(ctx, kind == 0 ? MP_PROF_GEMM_F16 : MP_PROF_GEMM_F32, s,
                  2.0 * static_cast<double>(g.m) * g.n * g.k * p.nprob *

@@ -47,6 +47,9 @@ struct TcGemm {
     // tiles per CTA, so SMs are handed back at that granularity and kernels
     // of a higher-priority stream (the Cholesky critical path) get in.
     int tiles_per_cta = 0;
+    // op(B)[k][n] == 0 for k > n (B^T of a lower-triangular inverse: the
+    // panel TRSM): a unit stops its K loop at its last column
+    bool k_tri = false;
 };
 
 bool tc_gemm_supported(const TcGemm& g);

@@ -558,6 +558,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             g.c_tile_stride = tt;
             g.problems = reinterpret_cast<const TcProblem*>(dl + L.trsm_tc[hb]);
             g.count = L.n_trsm_tc[hb];
+            g.k_tri = true;  // Linv^T is upper triangular: skip its zero K blocks
             launch_tc_gemm(c, st, g);
         }
         for (int q = 0; q < 3; ++q) {
