@@ -425,7 +425,7 @@ def run_chol(args, world, rank, local):
     prof_step_ms = pe[0].elapsed_time(pe[1])
     prof_pairs = ctx.prof_digit_products()
     ctx.prof_enable(False)
-    cls_names = ["gemm_f16", "gemm_f32", "gemm_f64", "potrf_trtri", "trsm", "cast", "other"]
+    cls_names = ["gemm_f16", "gemm_f32", "gemm_f64", "potrf_trtri", "trsm", "cast", "other", "gemm_f64_int8"]
     prof = {}
     for c, nm in enumerate(cls_names):
         t, cnt, work = ctx.prof_query(c)

@@ -88,7 +88,8 @@ typedef enum {
     MP_PROF_TRSM = 4,
     MP_PROF_CAST = 5,
     MP_PROF_OTHER = 6,
-    MP_PROF_NUM_CLASSES = 7
+    MP_PROF_GEMM_I8 = 7, /* FP64 products of FP16 operands on INT8 digits */
+    MP_PROF_NUM_CLASSES = 8
 } mp_prof_class;
 mp_status mp_prof_enable(mp_ctx ctx, int enable);
 mp_status mp_prof_reset(mp_ctx ctx);

@@ -670,7 +670,7 @@ void launch_oz_gemm(Ctx* ctx, cudaStream_t s, const OzGemm& g) {
     p.ndig_b = g.ndig_b;
     p.stats = ctx->prof.enabled ? ctx->prof.dev_stats : nullptr;
     const int64_t total = static_cast<int64_t>(p.nprob) * p.mblocks * p.nblocks;
-    ProfScope ps(ctx, MP_PROF_GEMM_F64, s,
+    ProfScope ps(ctx, MP_PROF_GEMM_I8, s,
                  2.0 * static_cast<double>(g.m) * g.n * g.k * p.nprob * (g.lower_only ? 0.5 : 1.0));
     static unsigned long long configured = 0;  // per-device bitmask
     if (first_on_device(configured)) {

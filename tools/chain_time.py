@@ -44,7 +44,7 @@ mp.tile_chol(A)
 ctx.synchronize()
 ctx.prof_enable(False)
 cls = {}
-for c, nm in enumerate(["gemm_f16", "gemm_f32", "gemm_f64", "potrf_trtri", "trsm", "cast", "other"]):
+for c, nm in enumerate(["gemm_f16", "gemm_f32", "gemm_f64", "potrf_trtri", "trsm", "cast", "other", "gemm_f64_int8"]):
     t, cnt, w = ctx.prof_query(c)
     if cnt:
         cls[nm] = (round(t / nt * 1e3, 1), cnt)

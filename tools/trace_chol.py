@@ -8,7 +8,7 @@ sys.path.insert(0, ".")
 import bench  # noqa: E402
 import paper_2406_02701_b200 as mp  # noqa: E402
 
-CLS = ["gemm_f16", "gemm_f32", "gemm_f64", "potrf_trtri", "trsm", "cast", "other"]
+CLS = ["gemm_f16", "gemm_f32", "gemm_f64", "potrf_trtri", "trsm", "cast", "other", "gemm_f64_int8"]
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 65536
 nb = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 out = sys.argv[3] if len(sys.argv) > 3 else "gpurun_out/trace.csv"
