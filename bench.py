@@ -707,7 +707,7 @@ def run_gemm(args, world, rank, local):
     rel = float(np.linalg.norm(Cg - C64) / np.linalg.norm(C64))
     # e2e: host doubles -> device (set_linear rounding) -> gemm -> host doubles
     e2e = []
-    for _ in range(max(1, args.steps)):
+    for _ in range(max(1, min(args.steps, 10))):
         ctx.synchronize()
         t0 = time.perf_counter()
         a_ = mp.MPArray.from_numpy(A, p, ctx)
@@ -879,7 +879,7 @@ def run_mle(args, world, rank, local):
     z = np.random.default_rng(5).standard_normal(n)  # white-noise observations (synthetic)
     A = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
     fits = []
-    for _ in range(max(1, args.steps)):
+    for _ in range(max(1, min(args.steps, 20))):
         ctx.synchronize()
         t0 = time.perf_counter()
         r = mp.matern_mle(A, x, y, z, np.log(args.range / 2), np.log(0.5), max_iter=200, tol=1e-4)
