@@ -937,7 +937,7 @@ def run_cast(args, world, rank, local):
     gbs = byts / (ms * 1e-3) / 1e9
     # e2e through the public API: raw source storage up, convert, raw result down
     e2e = []
-    for _ in range(max(1, args.steps)):
+    for _ in range(max(1, min(args.steps, 20))):
         ctx.synchronize()
         t0 = time.perf_counter()
         a_ = mp.MPArray.from_storage(raw.reshape((n, n), order="F"), n, n, pin, ctx)
