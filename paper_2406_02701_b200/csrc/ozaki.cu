@@ -522,74 +522,45 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(const OzSliceItem* items)
     oz_slice_generic(it, r0);
 }
 
-// Digits of one value when only the first nd are nonzero (the row's need):
-// the rest are exact zeros and are not computed.
-__device__ __forceinline__ void oz_digits_n(uint16_t h, float scale, int8_t (&dig)[S][16], int j, int nd) {
-    constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23
-    float Y = __half2float(__ushort_as_half(h)) * scale;
-#pragma unroll
-    for (int d = 0; d < S - 1; ++d) {
-        if (d < nd) {
-            const float w = __int_as_float((127 + 35 - 7 * d) << 23), iw = __int_as_float((127 - 35 + 7 * d) << 23);
-            const float t = fmaf(Y, iw, MAGIC);
-            dig[d][j] = static_cast<int8_t>(__float_as_int(t) - 0x4B400000);
-            Y = fmaf(-(t - MAGIC), w, Y);
-        } else {
-            dig[d][j] = 0;
-        }
-    }
-    dig[S - 1][j] = nd >= S ? static_cast<int8_t>(__float_as_int(Y + MAGIC) - 0x4B400000) : int8_t(0);
-}
-
-// Tiles (K <= OZ_STRIPE_K): a ROWS-row stripe is staged in shared memory by
-// one round of 16-byte loads (all in flight at once), the row exponents and
-// digit counts come from the registers on the way, and the digits are cut
-// from shared memory -- one HBM read of the operand.  16-row stripes (33 KB
-// of shared memory) let six CTAs share an SM, so one CTA's loads overlap
-// another's digit cutting; digits beyond the stripe's need are zeros and
-// are written without being computed (the GEMM reads up to the tile's need).
+// Tiles (K <= OZ_STRIPE_K): the whole 32-row stripe is staged in shared
+// memory by one round of 16-byte loads (all in flight at once), the row
+// exponents and digit counts come from the registers on the way, and the
+// digits are cut from shared memory -- one HBM read of the operand.
 constexpr int OZ_STRIPE_K = 1024;
-template <int ROWS>
 __global__ void __launch_bounds__(256) oz_slice_stripe_kernel(const OzSliceItem* items) {
-    constexpr int RG = ROWS / 8;      // 8-row groups (one 16-byte load each)
-    constexpr int CPASS = 256 / RG;   // columns per load pass
-    constexpr int TPR = 256 / ROWS;   // threads per row in the digit phase
     const OzSliceItem it = items[blockIdx.y];
-    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * ROWS;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
     if (r0 >= it.rows) return;
     const uint16_t* x = static_cast<const uint16_t*>(it.x);
-    // decided per 32-row pair, so a 16-row stripe never falls back alone: the
-    // even stripe of a pair cuts all 32 rows in the generic path
-    const int64_t rp = r0 / 32 * 32;
-    const bool vec = !it.trans && rp + 32 <= it.rows && (it.ld % 8) == 0 &&
+    const bool vec = !it.trans && r0 + 32 <= it.rows && (it.ld % 8) == 0 &&
                      (reinterpret_cast<uintptr_t>(x) & 15) == 0 && it.kpad <= OZ_STRIPE_K;
     if (!vec) {
-        if (r0 == rp) oz_slice_generic(it, rp);
+        oz_slice_generic(it, r0);
         return;
     }
-    extern __shared__ __align__(16) uint16_t sxf[];  // [ROWS][KS]
+    extern __shared__ __align__(16) uint16_t sxf[];  // [32][KS]
     const int KS = static_cast<int>(it.kpad) + 8;
-    __shared__ uint32_t smax[2][ROWS];
-    __shared__ int sexp[ROWS], sneed[ROWS];
-    if (threadIdx.x < ROWS) {
+    __shared__ uint32_t smax[2][32];
+    __shared__ int sexp[32];
+    if (threadIdx.x < 32) {
         smax[0][threadIdx.x] = 0;
         smax[1][threadIdx.x] = 31;
     }
-    const int rg = threadIdx.x % RG;  // rows rg*8 .. rg*8+7
+    const int rg = threadIdx.x % 4;  // rows rg*8 .. rg*8+7
     uint32_t mx[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t mn[8] = {31, 31, 31, 31, 31, 31, 31, 31};  // min exponent field of nonzeros
     const int cols = static_cast<int>(it.cols), kp = static_cast<int>(it.kpad);
-    for (int c0 = threadIdx.x / RG; c0 < kp; c0 += CPASS * 4) {
+    for (int c0 = threadIdx.x / 4; c0 < kp; c0 += 64 * 4) {
         uint4 v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {  // four independent loads in flight per thread
-            const int c = c0 + CPASS * u;
+            const int c = c0 + 64 * u;
             v[u] = (c < cols) ? *reinterpret_cast<const uint4*>(x + static_cast<int64_t>(c) * it.ld + r0 + rg * 8)
                               : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const int c = c0 + CPASS * u;
+            const int c = c0 + 64 * u;
             if (c >= kp) break;
             const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
@@ -613,38 +584,35 @@ __global__ void __launch_bounds__(256) oz_slice_stripe_kernel(const OzSliceItem*
     }
     __syncthreads();
     if (threadIdx.x < 32) {
+        const uint32_t m = smax[0][threadIdx.x];
         int e = 0, need = 0;
-        if (threadIdx.x < ROWS) {
-            const uint32_t m = smax[0][threadIdx.x];
-            if (m >= 0x7c00u) {
-                e = ROWEXP_NONFINITE;
-            } else if (m != 0) {
-                frexp(h2d(static_cast<uint16_t>(m)), &e);
-                const int lsb = static_cast<int>(smax[1][threadIdx.x]) - 25;
-                need = 1 + (max(0, e - 6 - lsb) + 6) / 7;
-            }
-            sexp[threadIdx.x] = e;
-            sneed[threadIdx.x] = e == ROWEXP_NONFINITE ? 0 : min(need, S);
-            it.rexp[r0 + threadIdx.x] = e;
+        if (m >= 0x7c00u) {
+            e = ROWEXP_NONFINITE;
+        } else if (m != 0) {
+            frexp(h2d(static_cast<uint16_t>(m)), &e);
+            const int lsb = static_cast<int>(smax[1][threadIdx.x]) - 25;
+            need = 1 + (max(0, e - 6 - lsb) + 6) / 7;
         }
+        sexp[threadIdx.x] = e;
+        it.rexp[r0 + threadIdx.x] = e;
         if (it.ndig) {
             for (int o = 16; o; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
             if (threadIdx.x == 0) atomicMax(it.ndig, min(need, S));
         }
     }
     __syncthreads();
-    const int lr = threadIdx.x / TPR, cg = (threadIdx.x % TPR) * 16;
-    const int er = sexp[lr], nd = sneed[lr];
+    const int lr = threadIdx.x / 8, cg = (threadIdx.x % 8) * 16;
+    const int er = sexp[lr];
     const float scale = er == ROWEXP_NONFINITE ? 0.0f : __int_as_float((127 + 41 - er) << 23);
     const uint16_t* row = sxf + lr * KS;
     int8_t* outr = static_cast<int8_t*>(it.out) + (r0 + lr) * it.kpad;
-    for (int c0 = cg; c0 < kp; c0 += TPR * 16) {
+    for (int c0 = cg; c0 < kp; c0 += 128) {
         alignas(16) int8_t dig[S][16];
         alignas(16) uint16_t hv[16];
         *reinterpret_cast<uint4*>(hv) = *reinterpret_cast<const uint4*>(row + c0);
         *reinterpret_cast<uint4*>(hv + 8) = *reinterpret_cast<const uint4*>(row + c0 + 8);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) oz_digits_n(hv[j], scale, dig, j, nd);
+        for (int j = 0; j < 16; ++j) oz_digits(hv[j], scale, dig, j);
 #pragma unroll
         for (int d = 0; d < S; ++d)
             *reinterpret_cast<int4*>(outr + d * it.slice_stride + c0) = *reinterpret_cast<const int4*>(dig[d]);
@@ -657,30 +625,15 @@ void launch_oz_slices(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_
     if (count == 0) return;
     ProfScope ps(ctx, MP_PROF_CAST, s, 0.0);
     const dim3 grid(static_cast<unsigned>((max_rows + 31) / 32), static_cast<unsigned>(count));
-    // MPCR_OZ_SLICE_ROWS=32: the round-1 32-row stripes (three CTAs per SM)
-    static const int stripe_rows = [] {
-        const char* e = getenv("MPCR_OZ_SLICE_ROWS");
-        return (e && atoi(e) == 32) ? 32 : 16;
-    }();
-    if (max_cols <= oz::OZ_STRIPE_K && stripe_rows == 16) {
-        const int kpad = static_cast<int>((max_cols + 15) / 16 * 16);
-        const int smem = 16 * (kpad + 8) * 2;
-        static unsigned long long cfg16 = 0;  // per-device bitmask
-        if (first_on_device(cfg16)) {
-            MP_CUDA(cudaFuncSetAttribute(oz::oz_slice_stripe_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         16 * (oz::OZ_STRIPE_K + 8) * 2));
-        }
-        const dim3 grid16(static_cast<unsigned>((max_rows + 15) / 16), static_cast<unsigned>(count));
-        oz::oz_slice_stripe_kernel<16><<<grid16, 256, smem, s>>>(items);
-    } else if (max_cols <= oz::OZ_STRIPE_K) {
+    if (max_cols <= oz::OZ_STRIPE_K) {
         const int kpad = static_cast<int>((max_cols + 15) / 16 * 16);
         const int smem = 32 * (kpad + 8) * 2;
         static unsigned long long cfg = 0;  // per-device bitmask
         if (first_on_device(cfg)) {
-            MP_CUDA(cudaFuncSetAttribute(oz::oz_slice_stripe_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            MP_CUDA(cudaFuncSetAttribute(oz::oz_slice_stripe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          32 * (oz::OZ_STRIPE_K + 8) * 2));
         }
-        oz::oz_slice_stripe_kernel<32><<<grid, 256, smem, s>>>(items);
+        oz::oz_slice_stripe_kernel<<<grid, 256, smem, s>>>(items);
     } else {
         oz::oz_slice_kernel<<<grid, 256, 0, s>>>(items);
     }

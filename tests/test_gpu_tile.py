@@ -303,7 +303,7 @@ print(hashlib.sha256(np.ascontiguousarray(A.to_numpy()).tobytes()).hexdigest())
 
 @pytest.mark.parametrize("env", [{"MPCR_UPDATE_GROUP": "1"}, {"MPCR_UPDATE_GROUP": "3"},
                                  {"MPCR_TC2_STAGES": "5"}, {"MPCR_LOOKAHEAD": "0"},
-                                 {"MPCR_WB_ASYNC": "1"}, {"MPCR_OZ_SLICE_ROWS": "32"}])
+                                 {"MPCR_WB_ASYNC": "1"}])
 def test_tile_chol_schedule_knobs_bitwise(env):
     """Update-tile order (MPCR_UPDATE_GROUP), the pair kernel's stage count and
     the lookahead and the write-back stream (MPCR_WB_ASYNC) change only the schedule, never the arithmetic: the factor
@@ -316,7 +316,7 @@ def test_tile_chol_schedule_knobs_bitwise(env):
 
     def run(extra):
         e = dict(os.environ)
-        for k in ("MPCR_UPDATE_GROUP", "MPCR_TC2_STAGES", "MPCR_LOOKAHEAD", "MPCR_WB_ASYNC", "MPCR_OZ_SLICE_ROWS"):
+        for k in ("MPCR_UPDATE_GROUP", "MPCR_TC2_STAGES", "MPCR_LOOKAHEAD", "MPCR_WB_ASYNC"):
             e.pop(k, None)
         e.update(extra)
         out = subprocess.run([sys.executable, "-c", _ENV_PROBE, root], env=e, capture_output=True,
