@@ -817,6 +817,10 @@ void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
         p.seg_a[0] = 0; p.seg_b[0] = 1;
         p.seg_a[1] = 1; p.seg_b[1] = 0;
         p.seg_a[2] = 0; p.seg_b[2] = 0;
+    } else if (g.two_panels && g.A2 && g.B2) {  // A B (step k) then A2 B2 (step k+1)
+        nseg = 2;
+        p.seg_a[0] = 0; p.seg_b[0] = 0;
+        p.seg_a[1] = 1; p.seg_b[1] = 1;
     } else if (g.B2) {  // A * B_lo + A * B
         nseg = 2;
         p.seg_a[0] = 0; p.seg_b[0] = 1;
@@ -843,7 +847,7 @@ void launch_tc_gemm(Ctx* ctx, cudaStream_t s, const TcGemm& g) {
     p.k_tri = g.k_tri ? 1 : 0;
     const int64_t total = static_cast<int64_t>(p.nprob) * p.mblocks * p.nblocks;
     ProfScope ps(ctx, kind == 0 ? MP_PROF_GEMM_F16 : MP_PROF_GEMM_F32, s,
-                 2.0 * static_cast<double>(g.m) * g.n * g.k * p.nprob *
+                 2.0 * static_cast<double>(g.m) * g.n * g.k * p.nprob * (g.two_panels ? 2 : 1) *
                      (g.lower_only ? 0.5 : 1.0));
     if (pair) {
         const int64_t pairs = static_cast<int64_t>(p.nprob) * ((p.mblocks + 1) / 2) * p.nblocks;

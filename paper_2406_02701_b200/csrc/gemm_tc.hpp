@@ -50,6 +50,9 @@ struct TcGemm {
     // op(B)[k][n] == 0 for k > n (B^T of a lower-triangular inverse: the
     // panel TRSM): a unit stops its K loop at its last column
     bool k_tri = false;
+    // kind 0 with A2 and B2: C = alpha (A B + A2 B2) + beta C, the two K
+    // segments in that order (two Cholesky steps' panels in one pass over C)
+    bool two_panels = false;
 };
 
 bool tc_gemm_supported(const TcGemm& g);

@@ -130,16 +130,20 @@ struct WorkLayout {
     static char* b(void* w) { return static_cast<char*>(w); }
 };
 
+// Panel generations (step k uses generation k mod 3): the lookahead panel of
+// step k+1 is produced while the trailing update still reads panel k, and
+// with paired steps (below) the bulk update of an even step k runs during
+// step k+1, still reading panel k while panel k+2 is produced.
+constexpr int PANEL_GENS = 3;
+
 void ensure_panels(mp_tile_s& t) {
-    // two panel generations (step parity): the lookahead panel of step k+1 is
-    // produced while the trailing update of step k still reads panel k
     for (int q = 0; q < 3; ++q)
         if (!t.panel[q])
-            MP_CUDA(cudaMalloc(&t.panel[q], 2 * static_cast<size_t>(t.tr) * t.tt() * elem_bytes((mp_precision)q)));
+            MP_CUDA(cudaMalloc(&t.panel[q], PANEL_GENS * static_cast<size_t>(t.tr) * t.tt() * elem_bytes((mp_precision)q)));
     if (!t.digits && ozaki_enabled()) {
-        MP_CUDA(cudaMalloc(&t.digits, 2 * static_cast<size_t>(t.tr) * OZ_SLICES * t.tt()));
-        MP_CUDA(cudaMalloc(&t.rexp, 2 * static_cast<size_t>(t.tr) * t.br * sizeof(int32_t)));
-        MP_CUDA(cudaMalloc(&t.ndig, 2 * static_cast<size_t>(t.tr) * sizeof(int32_t)));
+        MP_CUDA(cudaMalloc(&t.digits, PANEL_GENS * static_cast<size_t>(t.tr) * OZ_SLICES * t.tt()));
+        MP_CUDA(cudaMalloc(&t.rexp, PANEL_GENS * static_cast<size_t>(t.tr) * t.br * sizeof(int32_t)));
+        MP_CUDA(cudaMalloc(&t.ndig, PANEL_GENS * static_cast<size_t>(t.tr) * sizeof(int32_t)));
     }
     if (!t.work) MP_CUDA(cudaMalloc(&t.work, WorkLayout(t.br).bytes()));
     if (t.events.empty()) {
@@ -161,9 +165,13 @@ void append(std::vector<char>& buf, const std::vector<V>& v, size_t& off) {
 // FP16 (tile sizes the tcgen05 path cannot map), and DMMA for every other
 // FP32 / FP64 tile, keyed [A panel precision][B panel precision][C: FP32, FP64]
 // with the panel tiles read natively (widened exactly on load).
+// With paired steps a list belongs to one source panel (src 0: the panel of
+// the previous, even step whose update was deferred; src 1: the step's own
+// panel); tcf / tcf16s hold the tiles that take both panels in one pass
+// (two K segments, one read-modify-write of C).
 struct UpLists {
-    size_t tc = 0, tc16s = 0, simt16 = 0, oz = 0, dm[3][3][2] = {};
-    int64_t n_tc = 0, n_tc16s = 0, n_simt16 = 0, n_oz = 0, n_dm[3][3][2] = {};
+    size_t tc = 0, tc16s = 0, simt16 = 0, oz = 0, dm[3][3][2] = {}, tcf = 0, tcf16s = 0;
+    int64_t n_tc = 0, n_tc16s = 0, n_simt16 = 0, n_oz = 0, n_dm[3][3][2] = {}, n_tcf = 0, n_tcf16s = 0;
 };
 
 struct StepLists {
@@ -182,7 +190,7 @@ struct StepLists {
     int64_t n_cv[3][3][3] = {};
     size_t digits[3] = {0, 0, 0};  // INT8 digit slicing of FP16 panel tiles (same split)
     int64_t n_digits[3] = {0, 0, 0};
-    UpLists up[3];  // 0: tile column k+1 below the diagonal, 1: the rest, 2: tile (k+1, k+1)
+    UpLists up[3][2];  // [0: tile column k+1 below the diagonal, 1: the rest, 2: tile (k+1, k+1)][source panel]
     bool diag_bcast = false;  // receive / send L_kk^-1 down this process column
     struct Bcast {
         int i, root, comm;
@@ -256,7 +264,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     cudaStream_t sl = la ? c->hi : s;  // critical-path stream
 
     auto pan = [&](mp_precision q, int64_t i, int64_t k) -> void* {
-        return static_cast<char*>(t.panel[q]) + ((k & 1) * NT + i) * tt * elem_bytes(q);
+        return static_cast<char*>(t.panel[q]) + ((k % PANEL_GENS) * NT + i) * tt * elem_bytes(q);
     };
 
     // ---- host plan: the rank's action list (dist.hpp) turned into grouped
@@ -265,7 +273,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     std::vector<int> pgrid(t.prec.begin(), t.prec.end());
     const auto sched = dist_schedule(rank, P, Q, NT, pgrid.data());
     struct UpAcc {
-        std::vector<TcProblem> tc, tc16s;
+        std::vector<TcProblem> tc, tc16s, tcf, tcf16s;
         std::vector<TileProblem> simt16;
         std::vector<OzProblem> oz;           // FP64 tiles fed by FP16 panels: INT8 digit products
         std::vector<TileProblem> dm[3][3][2];  // DMMA, native panel precisions
@@ -295,16 +303,16 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     };
     const int64_t dig_tile = OZ_SLICES * tt;  // bytes of one tile's digit planes
     auto dig = [&](int64_t i, int64_t k) -> int8_t* {
-        return static_cast<int8_t*>(t.digits) + ((k & 1) * NT + i) * dig_tile;
+        return static_cast<int8_t*>(t.digits) + ((k % PANEL_GENS) * NT + i) * dig_tile;
     };
-    auto rex = [&](int64_t i, int64_t k) -> int32_t* { return t.rexp + ((k & 1) * NT + i) * nb; };
-    auto ndg = [&](int64_t i, int64_t k) -> int32_t* { return t.ndig + (k & 1) * NT + i; };
+    auto rex = [&](int64_t i, int64_t k) -> int32_t* { return t.rexp + ((k % PANEL_GENS) * NT + i) * nb; };
+    auto ndg = [&](int64_t i, int64_t k) -> int32_t* { return t.ndig + (k % PANEL_GENS) * NT + i; };
     struct StepAcc {
         std::vector<TcProblem> trsm_tc[2];
         std::vector<TileProblem> trsm_p[2][3];
         std::vector<CopyItem> wb[3], cv[3][3][3];
         std::vector<OzSliceItem> digits[3];
-        UpAcc up[3];
+        UpAcc up[3][2];
     };
     // Head/tail split of the panel TRSM (single GPU with lookahead): the head
     // tile runs on the critical-path stream, the rest of the column on the
@@ -356,6 +364,21 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 OzSliceItem{pan(MP_HALF, i, k), dig(i, k), rex(i, k), ndg(i, k), nb, nb, nb, nb, tt, 0, 0});
     };
     std::vector<char> have(NT * NT, 0);  // panel tile (i, k) present on this rank (conversions made)
+    // Paired steps (MPCR_PAIR_STEPS=0 turns them off): the trailing update of
+    // an even step k is deferred into step k+1, where tensor-core tiles take
+    // both panels in one pass (K = 2 nb, C read and written once instead of
+    // twice, rounded once).
+    static const bool pair_env = [] {
+        const char* e = getenv("MPCR_PAIR_STEPS");
+        return !(e && e[0] == '0');
+    }();
+    const bool pair_steps = pair_env && NT > 2;
+    struct TcCand {
+        int64_t ks;
+        int part, kind, src;  // kind 0: FP16 tile, 1: FP32 tile fed by FP16 panels
+        TcProblem p;
+    };
+    std::vector<TcCand> tc_cand;
     for (const DistAction& a : sched) {
         StepAcc& A = acc[a.k];
         StepLists& L = steps[a.k];
@@ -388,16 +411,22 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 have[k * NT + i] = 1;
                 break;
             case DA_UPDATE: {
-                UpAcc& U = A.up[j != k + 1 ? 1 : i == j ? 2 : 0];
+                // paired steps: an even step's update of tiles j >= k+2 runs in
+                // step k+1 (source 0) next to that step's own update (source 1)
+                const bool defer = pair_steps && (k % 2 == 0) && j >= k + 2;
+                const int64_t ks = defer ? k + 1 : k;
+                const int src = defer ? 0 : 1;
+                const int part = j != ks + 1 ? 1 : i == j ? 2 : 0;
+                UpAcc& U = acc[ks].up[part][src];
                 const int32_t lo = (i == j) ? 1 : 0;
+                const TcProblem tp{static_cast<int32_t>(i), static_cast<int32_t>(j),
+                                   static_cast<int32_t>(t.slot[j * NT + i]), lo};
                 if (q == MP_HALF && tc_ok)
-                    U.tc.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
-                                             static_cast<int32_t>(t.slot[j * NT + i]), lo});
+                    tc_cand.push_back({ks, part, 0, src, tp});
                 else if (q == MP_HALF)
                     U.simt16.push_back(TileProblem{pan(MP_HALF, i, k), pan(MP_HALF, j, k), t.ptr(i, j), lo, 0});
                 else if (q == MP_SINGLE && half_into_single(i, j, k))
-                    U.tc16s.push_back(TcProblem{static_cast<int32_t>(i), static_cast<int32_t>(j),
-                                                static_cast<int32_t>(t.slot[j * NT + i]), lo});
+                    tc_cand.push_back({ks, part, 1, src, tp});
                 else if (q == MP_DOUBLE && ozaki64(i, j, k))
                     U.oz.push_back(OzProblem{static_cast<int32_t>(i), static_cast<int32_t>(j), t.ptr(i, j), lo, 0});
                 else {
@@ -411,6 +440,30 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 break;
         }
     }
+    // tensor-core candidates: a tile with both sources of the same kind in one
+    // step goes to the fused two-panel list, otherwise to its source's list
+    {
+        std::sort(tc_cand.begin(), tc_cand.end(), [](const TcCand& x, const TcCand& y) {
+            if (x.ks != y.ks) return x.ks < y.ks;
+            if (x.part != y.part) return x.part < y.part;
+            if (x.p.a_tile != y.p.a_tile) return x.p.a_tile < y.p.a_tile;
+            if (x.p.b_tile != y.p.b_tile) return x.p.b_tile < y.p.b_tile;
+            return x.src < y.src;
+        });
+        for (size_t q = 0; q < tc_cand.size(); ++q) {
+            const TcCand& x = tc_cand[q];
+            const bool both = q + 1 < tc_cand.size() && tc_cand[q + 1].ks == x.ks && tc_cand[q + 1].part == x.part &&
+                              tc_cand[q + 1].p.a_tile == x.p.a_tile && tc_cand[q + 1].p.b_tile == x.p.b_tile;
+            if (both && tc_cand[q + 1].kind == x.kind) {
+                UpAcc& U = acc[x.ks].up[x.part][1];
+                (x.kind == 0 ? U.tcf : U.tcf16s).push_back(x.p);
+                ++q;
+                continue;
+            }
+            UpAcc& U = acc[x.ks].up[x.part][x.src];
+            (x.kind == 0 ? U.tc : U.tc16s).push_back(x.p);
+        }
+    }
     // FP16 update tiles of a step in groups of G tile columns, rows within a
     // group, the group's columns within a row: each panel tile L_ik serves G
     // consecutive tiles and the group's G tiles L_jk stay in L2, so the panel
@@ -420,15 +473,18 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         const char* e = getenv("MPCR_UPDATE_GROUP");
         return e ? std::max(1, atoi(e)) : 8;
     }();
+    auto grouped = [](const TcProblem& x, const TcProblem& y) {
+        const int gx = x.b_tile / upd_group, gy = y.b_tile / upd_group;
+        if (gx != gy) return gx < gy;
+        if (x.a_tile != y.a_tile) return x.a_tile < y.a_tile;
+        return x.b_tile < y.b_tile;
+    };
     for (int64_t k = 0; k < NT; ++k)
         for (int w = 0; w < 3; ++w)
-            std::stable_sort(acc[k].up[w].tc.begin(), acc[k].up[w].tc.end(),
-                             [](const TcProblem& x, const TcProblem& y) {
-                                 const int gx = x.b_tile / upd_group, gy = y.b_tile / upd_group;
-                                 if (gx != gy) return gx < gy;
-                                 if (x.a_tile != y.a_tile) return x.a_tile < y.a_tile;
-                                 return x.b_tile < y.b_tile;
-                             });
+            for (int sc = 0; sc < 2; ++sc) {
+                std::stable_sort(acc[k].up[w][sc].tc.begin(), acc[k].up[w][sc].tc.end(), grouped);
+                std::stable_sort(acc[k].up[w][sc].tcf.begin(), acc[k].up[w][sc].tcf.end(), grouped);
+            }
     std::vector<char> buf;
     for (int64_t k = 0; k < NT; ++k) {
         StepLists& L = steps[k];
@@ -454,22 +510,29 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             append(buf, A.digits[h], L.digits[h]);
             L.n_digits[h] = A.digits[h].size();
         }
-        for (int w = 0; w < 3; ++w) {
-            append(buf, A.up[w].tc, L.up[w].tc);
-            L.up[w].n_tc = A.up[w].tc.size();
-            append(buf, A.up[w].tc16s, L.up[w].tc16s);
-            L.up[w].n_tc16s = A.up[w].tc16s.size();
-            append(buf, A.up[w].simt16, L.up[w].simt16);
-            L.up[w].n_simt16 = A.up[w].simt16.size();
-            append(buf, A.up[w].oz, L.up[w].oz);
-            L.up[w].n_oz = A.up[w].oz.size();
-            for (int a = 0; a < 3; ++a)
-                for (int b = 0; b < 3; ++b)
-                    for (int c2 = 0; c2 < 2; ++c2) {
-                        append(buf, A.up[w].dm[a][b][c2], L.up[w].dm[a][b][c2]);
-                        L.up[w].n_dm[a][b][c2] = A.up[w].dm[a][b][c2].size();
-                    }
-        }
+        for (int w = 0; w < 3; ++w)
+            for (int sc = 0; sc < 2; ++sc) {
+                const UpAcc& U = A.up[w][sc];
+                UpLists& D = L.up[w][sc];
+                append(buf, U.tc, D.tc);
+                D.n_tc = U.tc.size();
+                append(buf, U.tc16s, D.tc16s);
+                D.n_tc16s = U.tc16s.size();
+                append(buf, U.tcf, D.tcf);
+                D.n_tcf = U.tcf.size();
+                append(buf, U.tcf16s, D.tcf16s);
+                D.n_tcf16s = U.tcf16s.size();
+                append(buf, U.simt16, D.simt16);
+                D.n_simt16 = U.simt16.size();
+                append(buf, U.oz, D.oz);
+                D.n_oz = U.oz.size();
+                for (int a = 0; a < 3; ++a)
+                    for (int b = 0; b < 3; ++b)
+                        for (int c2 = 0; c2 < 2; ++c2) {
+                            append(buf, U.dm[a][b][c2], D.dm[a][b][c2]);
+                            D.n_dm[a][b][c2] = U.dm[a][b][c2].size();
+                        }
+            }
     }
     // final clean-up lists: upper part of diagonal tiles, strictly-upper tiles
     std::vector<void*> diag_ptrs[3], upper_ptrs[3];
@@ -673,90 +736,85 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     };
 
     // ---- trailing update A_ij -= L_ik L_jk^T of one part of step k ------------
+    // (with paired steps, odd k also applies the deferred update of panel k-1:
+    // its source-0 lists first, then source 1, then the two-panel lists)
+    auto tc_update = [&](mp_precision pc, size_t off, int64_t cnt, int64_t kp, bool both, int tiles_per_cta,
+                         cudaStream_t st) {
+        TcGemm g;
+        g.pc = pc;
+        g.ta = false;
+        g.tb = true;
+        g.m = g.n = g.k = nb;
+        g.alpha = -1.0;
+        g.beta = 1.0;
+        g.A = g.B = pan(MP_HALF, 0, both ? kp - 1 : kp);
+        if (both) {  // C -= L_{k-1} L_{k-1}^T + L_k L_k^T in one pass
+            g.A2 = g.B2 = pan(MP_HALF, 0, kp);
+            g.two_panels = true;
+        }
+        g.lda = g.ldb = nb;
+        g.a_tiles = g.b_tiles = NT;
+        g.a_tile_stride = g.b_tile_stride = tt;
+        g.C = t.slab[pc];
+        g.ldc = nb;
+        g.c_tiles = t.nslot[pc];
+        g.c_tile_stride = tt;
+        g.problems = reinterpret_cast<const TcProblem*>(dl + off);
+        g.count = cnt;
+        g.tiles_per_cta = tiles_per_cta;
+        launch_tc_gemm(c, st, g);
+    };
     auto update_phase = [&](int64_t k, int part, cudaStream_t st, int tiles_per_cta) {
-        const UpLists& U = steps[k].up[part];
-        if (U.n_tc16s) {  // FP32 tiles from FP16 panels
-            TcGemm g;
-            g.pc = MP_SINGLE;
-            g.ta = false;
-            g.tb = true;
-            g.m = g.n = g.k = nb;
-            g.alpha = -1.0;
-            g.beta = 1.0;
-            g.A = g.B = pan(MP_HALF, 0, k);
-            g.lda = g.ldb = nb;
-            g.a_tiles = g.b_tiles = NT;
-            g.a_tile_stride = g.b_tile_stride = tt;
-            g.C = t.slab[MP_SINGLE];
-            g.ldc = nb;
-            g.c_tiles = t.nslot[MP_SINGLE];
-            g.c_tile_stride = tt;
-            g.problems = reinterpret_cast<const TcProblem*>(dl + U.tc16s);
-            g.count = U.n_tc16s;
-            g.tiles_per_cta = tiles_per_cta;
-            launch_tc_gemm(c, st, g);
+        for (int sc = 0; sc < 2; ++sc) {
+            const UpLists& U = steps[k].up[part][sc];
+            const int64_t kp = sc == 0 ? k - 1 : k;  // the source panel's step
+            if (U.n_tc16s) tc_update(MP_SINGLE, U.tc16s, U.n_tc16s, kp, false, tiles_per_cta, st);  // FP32 tiles, FP16 panels
+            if (U.n_tc) tc_update(MP_HALF, U.tc, U.n_tc, kp, false, tiles_per_cta, st);
+            if (U.n_simt16) {  // FP16 tiles of a size the tcgen05 maps cannot take
+                GroupedGemm g{MP_HALF, MP_HALF, true, nb, nb, nb, nb, nb, nb, -1.0, 1.0,
+                              reinterpret_cast<const TileProblem*>(dl + U.simt16), U.n_simt16};
+                launch_grouped_gemm(c, st, g);
+            }
+            if (U.n_oz) {  // FP64 tiles from FP16 panels: exact INT8 digit products
+                OzGemm o;
+                o.A = o.B = dig(0, kp);
+                o.a_tiles = o.b_tiles = NT;
+                o.a_slice_stride = o.b_slice_stride = tt;
+                o.kpad = nb;
+                o.m = o.n = o.k = nb;
+                o.ldc = nb;
+                o.alpha = -1.0;
+                o.beta = 1.0;
+                o.problems = reinterpret_cast<const OzProblem*>(dl + U.oz);
+                o.count = U.n_oz;
+                o.rexp_a = o.rexp_b = rex(0, kp);
+                o.ndig_a = o.ndig_b = ndg(0, kp);
+                o.rexp_stride_a = o.rexp_stride_b = nb;
+                o.tiles_per_cta = tiles_per_cta;
+                launch_oz_gemm(c, st, o);
+            }
+            // FP32 / FP64 tiles on DMMA: exact products of the widened panel
+            // tiles, FP64 accumulation, one rounding into the tile
+            for (int pa = 0; pa < 3; ++pa)
+                for (int pb = 0; pb < 3; ++pb)
+                    for (int c2 = 0; c2 < 2; ++c2) {
+                        const int64_t cnt = U.n_dm[pa][pb][c2];
+                        if (!cnt) continue;
+                        DmmaArgs d{false, true, nb, nb, nb, -1.0, 1.0, nullptr, nb, nullptr, nb, nullptr, nb, false,
+                                   reinterpret_cast<const TileProblem*>(dl + U.dm[pa][pb][c2]), (mp_precision)pa};
+                        d.pin_b = pb;
+                        d.pout = c2 ? MP_DOUBLE : MP_SINGLE;
+                        d.exclusive = part == 2;  // the diagonal SYRK feeding the next POTRF
+                        d.allow_ksplit = part == 2;  // (k+1, k+1) alone on every rank
+                        ProfScope ps(c, c2 ? MP_PROF_GEMM_F64 : MP_PROF_GEMM_F32, st,
+                                     2.0 * static_cast<double>(nb) * nb * nb * cnt);
+                        launch_dmma_gemm(c, st, d, cnt);
+                    }
+            if (sc == 1) {  // tiles that take both panels in one pass
+                if (U.n_tcf16s) tc_update(MP_SINGLE, U.tcf16s, U.n_tcf16s, k, true, tiles_per_cta, st);
+                if (U.n_tcf) tc_update(MP_HALF, U.tcf, U.n_tcf, k, true, tiles_per_cta, st);
+            }
         }
-        if (U.n_tc) {
-            TcGemm g;
-            g.pc = MP_HALF;
-            g.ta = false;
-            g.tb = true;
-            g.m = g.n = g.k = nb;
-            g.alpha = -1.0;
-            g.beta = 1.0;
-            g.A = g.B = pan(MP_HALF, 0, k);
-            g.lda = g.ldb = nb;
-            g.a_tiles = g.b_tiles = NT;
-            g.a_tile_stride = g.b_tile_stride = tt;
-            g.C = t.slab[MP_HALF];
-            g.ldc = nb;
-            g.c_tiles = t.nslot[MP_HALF];
-            g.c_tile_stride = tt;
-            g.problems = reinterpret_cast<const TcProblem*>(dl + U.tc);
-            g.count = U.n_tc;
-            g.tiles_per_cta = tiles_per_cta;
-            launch_tc_gemm(c, st, g);
-        }
-        if (U.n_simt16) {  // FP16 tiles of a size the tcgen05 maps cannot take
-            GroupedGemm g{MP_HALF, MP_HALF, true, nb, nb, nb, nb, nb, nb, -1.0, 1.0,
-                          reinterpret_cast<const TileProblem*>(dl + U.simt16), U.n_simt16};
-            launch_grouped_gemm(c, st, g);
-        }
-        if (U.n_oz) {  // FP64 tiles from FP16 panels: exact INT8 digit products
-            OzGemm o;
-            o.A = o.B = dig(0, k);
-            o.a_tiles = o.b_tiles = NT;
-            o.a_slice_stride = o.b_slice_stride = tt;
-            o.kpad = nb;
-            o.m = o.n = o.k = nb;
-            o.ldc = nb;
-            o.alpha = -1.0;
-            o.beta = 1.0;
-            o.problems = reinterpret_cast<const OzProblem*>(dl + U.oz);
-            o.count = U.n_oz;
-            o.rexp_a = o.rexp_b = rex(0, k);
-            o.ndig_a = o.ndig_b = ndg(0, k);
-            o.rexp_stride_a = o.rexp_stride_b = nb;
-            o.tiles_per_cta = tiles_per_cta;
-            launch_oz_gemm(c, st, o);
-        }
-        // FP32 / FP64 tiles on DMMA: exact products of the widened panel
-        // tiles, FP64 accumulation, one rounding into the tile
-        for (int pa = 0; pa < 3; ++pa)
-            for (int pb = 0; pb < 3; ++pb)
-                for (int c2 = 0; c2 < 2; ++c2) {
-                    const int64_t cnt = U.n_dm[pa][pb][c2];
-                    if (!cnt) continue;
-                    DmmaArgs d{false, true, nb, nb, nb, -1.0, 1.0, nullptr, nb, nullptr, nb, nullptr, nb, false,
-                               reinterpret_cast<const TileProblem*>(dl + U.dm[pa][pb][c2]), (mp_precision)pa};
-                    d.pin_b = pb;
-                    d.pout = c2 ? MP_DOUBLE : MP_SINGLE;
-                    d.exclusive = part == 2;  // the diagonal SYRK feeding the next POTRF
-                    d.allow_ksplit = part == 2;  // (k+1, k+1) alone on every rank
-                    ProfScope ps(c, c2 ? MP_PROF_GEMM_F64 : MP_PROF_GEMM_F32, st,
-                                 2.0 * static_cast<double>(nb) * nb * nb * cnt);
-                    launch_dmma_gemm(c, st, d, cnt);
-                }
     };
 
     auto issue_all = [&]() {
