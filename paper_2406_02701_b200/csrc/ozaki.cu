@@ -282,6 +282,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
             if (skip_tile(pr, m0, n0)) continue;
             int sa, sb;
             digits_of(p, pr, sa, sb);
+            // C of this unit is read only after the last digit group: pull its
+            // lines into L2 now, while the MMAs run (one lane per 16 rows, the
+            // 64 columns of this warp's half), so the final pass does not wait
+            // on DRAM latency per 8-column chunk
+            if (p.beta != 0.0 && (lane & 15) == 0 && m0 + r < p.M) {
+                const double* Cp = static_cast<const double*>(pr.c) + (m0 + r);
+                for (int jb = 0; jb < 64; ++jb) {
+                    const int col = n0 + ch * 64 + jb;
+                    if (col < p.N)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(Cp + static_cast<int64_t>(col) * p.ldc));
+                }
+            }
             double sum[64];
 #pragma unroll
             for (int j = 0; j < 64; ++j) sum[j] = 0.0;
