@@ -397,3 +397,51 @@ print(hashlib.sha256(np.ascontiguousarray(B.to_numpy()).tobytes()).hexdigest())
         return out.stdout.strip().splitlines()[-1]
 
     assert run({}) == run({"MPCR_LOOKAHEAD": "0"})
+
+
+_PAIR_PROBE = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2406_02701_b200 as mp
+ctx = mp.Context(0)
+n, nb = 4096, 512
+nt = n // nb
+i, j = np.indices((nt, nt))
+g = np.where(i == j, 2, np.where(abs(i - j) == 1, 1, 0))
+A = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+A.fill_matern(64, 0.5, 0.03, 1.0)
+mp.tile_chol(A)
+np.save(sys.argv[2], A.to_numpy())
+"""
+
+
+def test_paired_steps_match_unpaired_within_rounding(ctx, ref, tmp_path):
+    """Paired steps (default) apply two panels to a tile in one pass and round
+    once; MPCR_PAIR_STEPS=0 rounds after every step.  Both are checked against
+    the composed reference oracle with the 4x rule."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for v in ("1", "0"):
+        f = tmp_path / f"L{v}.npy"
+        e = dict(os.environ, MPCR_PAIR_STEPS=v)
+        r = subprocess.run([sys.executable, "-c", _PAIR_PROBE, root, str(f)], env=e, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[v] = np.load(f)
+    n, nb = 4096, 512
+    nt = n // nb
+    i, j = np.indices((nt, nt))
+    g = np.where(i == j, 2, np.where(abs(i - j) == 1, 1, 0))
+    cov = ref.grid_matern(64, n, 0.5, 0.03, 1.0, 2)
+    Lref = ref.tile_chol(n, nb, g, cov)
+    dense = np.linalg.cholesky(ref_round_grid(cov, g, nb))
+    err_dense = np.linalg.norm(Lref - dense) / np.linalg.norm(dense)
+    for v, L in outs.items():
+        err = np.linalg.norm(L - Lref) / np.linalg.norm(Lref)
+        assert err <= 4 * err_dense, (v, err, err_dense)
+    assert not np.array_equal(outs["1"], outs["0"])  # the pairing is really on by default
