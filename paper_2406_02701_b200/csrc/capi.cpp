@@ -214,6 +214,8 @@ mp_status mp_ctx_create(int device, mp_ctx* out) {
     MP_CUDA(cudaStreamCreateWithPriority(&c->hi, cudaStreamNonBlocking, hi));
     MP_CUDA(cudaStreamCreateWithPriority(&c->hi2, cudaStreamNonBlocking, hi));
     for (auto& s : c->aux) MP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    MP_CUDA(cudaMalloc(&c->sched_pool, 2 * Ctx::SCHED_SLOTS * sizeof(unsigned int)));
+    MP_CUDA(cudaMemset(c->sched_pool, 0, 2 * Ctx::SCHED_SLOTS * sizeof(unsigned int)));
     *out = c;
     MP_API_END
 }
@@ -231,6 +233,7 @@ mp_status mp_ctx_destroy(mp_ctx ctx) {
     for (void* p : ctx->scr)
         if (p) cudaFree(p);
     if (ctx->prof.dev_stats) cudaFree(ctx->prof.dev_stats);
+    if (ctx->sched_pool) cudaFree(ctx->sched_pool);
     for (auto& s : ctx->aux) cudaStreamDestroy(s);
     cudaStreamDestroy(ctx->hi);
     cudaStreamDestroy(ctx->hi2);

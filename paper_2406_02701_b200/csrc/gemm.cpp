@@ -32,17 +32,17 @@ static void launch_gemm_ozaki(Ctx* ctx, cudaStream_t s, const GemmDesc& g) {
     const size_t dig = OZ_SLICES * (sa + sb);
     const size_t items_off = (dig + 255) / 256 * 256;
     const size_t rexp_off = items_off + 256;
-    char* w = static_cast<char*>(ctx->ensure_scratch(rexp_off + (g.m + g.n + 2) * 4 + 256, 2));
+    const int64_t mbk = (g.m + 127) / 128, nbk = (g.n + 127) / 128;  // digit counts per 128-row block
+    char* w = static_cast<char*>(ctx->ensure_scratch(rexp_off + (g.m + g.n + mbk + nbk) * 4 + 256, 2));
     int8_t* da = reinterpret_cast<int8_t*>(w);
     int8_t* db = da + OZ_SLICES * sa;
     int32_t* ea = reinterpret_cast<int32_t*>(w + rexp_off);
     int32_t* eb = ea + g.m;
-    int32_t* nd = eb + g.n;  // digits needed by A and B
-    MP_CUDA(cudaMemsetAsync(nd, 0, 2 * sizeof(int32_t), s));
+    int32_t* nd = eb + g.n;  // digits needed by the row blocks of A, then of B
     // op(A)(r = m, c = k); op(B)^T(r = n, c = k).  trans: element (r, c) at x[r * ld + c]
     OzSliceItem it[2] = {
         {g.A, da, ea, nd, g.lda, g.m, g.k, kpad, static_cast<int64_t>(sa), g.ta ? 1 : 0, 0},
-        {g.B, db, eb, nd + 1, g.ldb, g.n, g.k, kpad, static_cast<int64_t>(sb), g.tb ? 0 : 1, 0}};
+        {g.B, db, eb, nd + mbk, g.ldb, g.n, g.k, kpad, static_cast<int64_t>(sb), g.tb ? 0 : 1, 0}};
     OzSliceItem* dit = reinterpret_cast<OzSliceItem*>(w + items_off);
     MP_CUDA(cudaMemcpyAsync(dit, it, sizeof(it), cudaMemcpyHostToDevice, s));
     launch_oz_slices(ctx, s, dit, 2, std::max(g.m, g.n), kpad);
@@ -63,7 +63,7 @@ static void launch_gemm_ozaki(Ctx* ctx, cudaStream_t s, const GemmDesc& g) {
     o.rexp_a = ea;
     o.rexp_b = eb;
     o.ndig_a = nd;
-    o.ndig_b = nd + 1;
+    o.ndig_b = nd + mbk;
     launch_oz_gemm(ctx, s, o);
 }
 

@@ -89,6 +89,13 @@ struct Ctx {
     // over scratch pointers are stale once it changes
     uint64_t scr_gen = 0;
     void* ensure_scratch(size_t bytes, int which = 0);
+    // Work counters of dynamically scheduled persistent kernels: one pair
+    // [next unit, CTAs finished] per launch, handed out round robin; the last
+    // CTA of a launch resets its pair, so captured graphs replay unchanged.
+    static constexpr int SCHED_SLOTS = 1024;
+    unsigned int* sched_pool = nullptr;  // 2 * SCHED_SLOTS, zeroed at context creation
+    int sched_next = 0;
+    unsigned int* sched_slot() { return sched_pool + 2 * (sched_next++ % SCHED_SLOTS); }
 };
 
 // Make ctx's device current for this thread (every C-ABI entry point does

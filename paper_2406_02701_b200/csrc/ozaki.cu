@@ -51,10 +51,11 @@ constexpr int S = OZ_SLICES;  // digits per value
 // so each A k-block feeds two MMAs (a quarter less operand ingress).
 constexpr int BM = 128, BN = 128, BK = 128, STAGES = 4;
 constexpr int A_STAGE = BM * BK, B_STAGE = BN * BK;  // 16 KB each
-constexpr int SMEM_BYTES = STAGES * (A_STAGE + 2 * B_STAGE) + 1024 + 256;  // + barriers
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + 2 * B_STAGE) + 1024 + 256;  // + barriers, unit ring
 constexpr int NACC = 4;          // int32 accumulators in flight (MMA runs NACC groups ahead)
 constexpr int TMEM_COLS = 512;  // NACC x 128 columns
 constexpr int NTHREADS = 320;   // 10 warps
+constexpr int UR = 4;           // unit ring: the producer runs up to UR units ahead
 constexpr int ROWEXP_NONFINITE = 0x7fffffff;
 
 struct Params {
@@ -62,6 +63,7 @@ struct Params {
     const OzProblem* problems;
     OzProblem single;
     int32_t nprob;
+    int32_t nlower;  // the first nlower problems are lower_only: only their live units are enumerated
     int32_t M, N, K;
     int32_t mblocks, nblocks, kblocks;
     int64_t ldc;
@@ -69,19 +71,20 @@ struct Params {
     const int32_t* rexp_a;  // row exponents of A tile t at rexp_a + t * rexp_stride_a
     const int32_t* rexp_b;
     int64_t rexp_stride_a, rexp_stride_b;
-    const int32_t* ndig_a;  // digits per tile (nullptr: all S)
+    const int32_t* ndig_a;  // digits per 128-row block: tile t, block b at ndig_a[t * ndig_stride_a + b] (nullptr: all S)
     const int32_t* ndig_b;
-    // CTA c takes units (c / lanes) * lanes * per + c % lanes + r * lanes,
-    // r < per: the CTAs resident together sweep one contiguous chunk
-    int32_t lanes, per;
+    int32_t ndig_stride_a, ndig_stride_b;
+    // dynamic unit scheduling: [0] next unit, [1] CTAs finished (the last
+    // CTA resets both)
+    unsigned int* sched;
     unsigned long long* stats;  // profiling: [0] += sa*sb per output tile, [1] += 1 (or nullptr)
 };
 
 // Digit counts of a problem: pairs (dp, dq) with dp <= sa, dq <= sb; groups
 // g = sa + sb .. 2.
-__device__ __forceinline__ void digits_of(const Params& p, const OzProblem& pr, int& sa, int& sb) {
-    sa = p.ndig_a ? max(1, min(S, p.ndig_a[pr.a_tile])) : S;
-    sb = p.ndig_b ? max(1, min(S, p.ndig_b[pr.b_tile])) : S;
+__device__ __forceinline__ void digits_of(const Params& p, const OzProblem& pr, int m0, int n0, int& sa, int& sb) {
+    sa = p.ndig_a ? max(1, min(S, p.ndig_a[pr.a_tile * p.ndig_stride_a + m0 / BM])) : S;
+    sb = p.ndig_b ? max(1, min(S, p.ndig_b[pr.b_tile * p.ndig_stride_b + n0 / BN])) : S;
 }
 
 __device__ __forceinline__ void mma_i8_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -120,7 +123,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + NACC;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + NACC);
+    uint64_t* ufull = tempty + NACC;
+    uint64_t* uempty = ufull + UR;
+    int32_t* uring = reinterpret_cast<int32_t*>(uempty + UR);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uring + UR);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (warp == 0 && lane == 0) {
@@ -134,6 +140,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
             ptx::mbar_init(&tfull[s], 1);
             ptx::mbar_init(&tempty[s], 256);
         }
+        for (int s = 0; s < UR; ++s) {
+            ptx::mbar_init(&ufull[s], 1);
+            ptx::mbar_init(&uempty[s], 9);  // the MMA warp + 8 epilogue warps
+        }
         ptx::fence_barrier_init();
     }
     if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
@@ -142,17 +152,48 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
+    // Units: the live (lower-triangle) output blocks of the lower-only
+    // problems, column by column, then every block of the others.  The
+    // producer draws them from a global counter and passes them to the MMA
+    // and epilogue warps through a shared ring: a CTA that starts late (its
+    // SM held by another stream's kernel) simply takes fewer units.
     const int tiles_per_prob = p.mblocks * p.nblocks;
-    const int64_t total = static_cast<int64_t>(p.nprob) * tiles_per_prob;
-    const int64_t wave0 = (blockIdx.x / p.lanes) * static_cast<int64_t>(p.lanes) * p.per;
-    const int64_t t_first = wave0 + blockIdx.x % p.lanes;
-    const int64_t t_end = min(total, wave0 + static_cast<int64_t>(p.lanes) * p.per);
+    const int jl = min(p.mblocks, p.nblocks);
+    const int live_per_lower = jl * p.mblocks - jl * (jl - 1) / 2;
+    const int64_t lower_units = static_cast<int64_t>(p.nlower) * live_per_lower;
+    const int64_t total = lower_units + static_cast<int64_t>(p.nprob - p.nlower) * tiles_per_prob;
+    // consumer side of the unit ring: the next unit (>= total: done)
+    auto next_unit = [&](int it) -> int64_t {
+        const int slot = it % UR;
+        ptx::mbar_wait(&ufull[slot], static_cast<uint32_t>((it / UR) & 1));
+        const int64_t t = *reinterpret_cast<volatile int32_t*>(&uring[slot]);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&uempty[slot]);
+        return t;
+    };
     auto decode = [&](int64_t t, OzProblem& pr, int& m0, int& n0) {
-        const int64_t pi = t / tiles_per_prob;
-        const int r = static_cast<int>(t - pi * tiles_per_prob);
+        int64_t pi;
+        if (t < lower_units) {
+            pi = t / live_per_lower;
+            const int u = static_cast<int>(t - pi * live_per_lower);
+            // column j starts at j * mb - j (j - 1) / 2
+            const double b = 2.0 * p.mblocks + 1.0;
+            int j = static_cast<int>((b - sqrt(b * b - 8.0 * u)) * 0.5);
+            j = max(0, min(j, jl - 1));
+            auto start = [&](int c) { return c * p.mblocks - c * (c - 1) / 2; };
+            while (j > 0 && start(j) > u) --j;
+            while (j + 1 < jl && start(j + 1) <= u) ++j;
+            m0 = (j + (u - start(j))) * BM;
+            n0 = j * BN;
+        } else {
+            const int64_t t2 = t - lower_units;
+            const int64_t q = t2 / tiles_per_prob;
+            const int r = static_cast<int>(t2 - q * tiles_per_prob);
+            pi = p.nlower + q;
+            m0 = (r % p.mblocks) * BM;
+            n0 = (r / p.mblocks) * BN;
+        }
         pr = p.problems ? p.problems[pi] : p.single;
-        m0 = (r % p.mblocks) * BM;
-        n0 = (r / p.mblocks) * BN;
     };
 
     if (warp == 0) {
@@ -160,13 +201,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int64_t t = t_first; t < t_end; t += p.lanes) {
+            for (int it = 0;; ++it) {
+                const int slot = it % UR;
+                ptx::mbar_wait(&uempty[slot], static_cast<uint32_t>(((it / UR) & 1) ^ 1));
+                const int64_t t = static_cast<int64_t>(atomicAdd(p.sched, 1u));
+                uring[slot] = static_cast<int32_t>(t < total ? t : total);
+                ptx::mbar_arrive(&ufull[slot]);
+                if (t >= total) break;
                 OzProblem pr;
                 int m0, n0;
                 decode(t, pr, m0, n0);
                 if (skip_tile(pr, m0, n0)) continue;
                 int sa, sb;
-                digits_of(p, pr, sa, sb);
+                digits_of(p, pr, m0, n0, sa, sb);
                 for (int g = sa + sb; g >= 2; g -= 2) {
                     const bool two = g - 1 >= 2;  // group g-1 rides along
                     const int lo = max(1, (two ? g - 1 : g) - sb), hi = min(sa, g - 1);
@@ -196,75 +243,83 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
         }
     } else if (warp == 1) {
         // ===== MMA issuer: one accumulator per digit group =====
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_i8(BM, BN);
-            int stage = 0;
-            uint32_t phase = 0;
-            int acc = 0;
-            uint32_t acc_phase = 0;
-            for (int64_t t = t_first; t < t_end; t += p.lanes) {
-                OzProblem pr;
-                int m0, n0;
-                decode(t, pr, m0, n0);
-                if (skip_tile(pr, m0, n0)) continue;
-                int sa, sb;
-                digits_of(p, pr, sa, sb);
-                if (p.stats) {
-                    atomicAdd(p.stats, static_cast<unsigned long long>(sa * sb));
-                    atomicAdd(p.stats + 1, 1ull);
-                }
-                for (int g = sa + sb; g >= 2; g -= 2) {
-                    const bool two = g - 1 >= 2;
-                    // accumulators of groups g and g-1 (the next one in the rotation)
-                    const int acc2 = acc + 1 == NACC ? 0 : acc + 1;
-                    const uint32_t ph2 = acc + 1 == NACC ? acc_phase ^ 1 : acc_phase;
-                    ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
-                    if (two) ptx::mbar_wait(&tempty[acc2], ph2 ^ 1);
-                    ptx::tc_fence_after();
-                    const uint32_t d1 = tmem_base + static_cast<uint32_t>(acc * BN);
-                    const uint32_t d2 = tmem_base + static_cast<uint32_t>(acc2 * BN);
-                    bool first1 = true, first2 = true;
-                    const int lo = max(1, (two ? g - 1 : g) - sb), hi = min(sa, g - 1);
-                    for (int dp = lo; dp <= hi; ++dp) {
-                        const bool v1 = dp >= max(1, g - sb);
-                        const bool v2 = two && dp <= min(sa, g - 2);
-                        for (int kb = 0; kb < p.kblocks; ++kb) {
-                            ptx::mbar_wait(&full[stage], phase);
-                            ptx::tc_fence_after();
-                            const uint32_t a_base = ptx::smem_u32(sA + stage * A_STAGE);
-                            const uint32_t b1 = ptx::smem_u32(sB + (stage * 2) * B_STAGE);
-                            const uint32_t b2 = ptx::smem_u32(sB + (stage * 2 + 1) * B_STAGE);
+        // The whole warp runs the (warp-uniform) loop so its state stays in
+        // uniform registers; one elected lane issues the MMAs and commits.
+        // (Issued from a lane-0 branch, every MMA paid ~20 instructions of
+        // register-to-uniform moves and predicates: at 1 MOP per INT8 MMA the
+        // issue loop, not the tensor pipe, set the pace -- 22 % tensor active
+        // in situ.)
+        constexpr uint32_t idesc = idesc_i8(BM, BN);
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int it = 0;; ++it) {
+            const int64_t t = next_unit(it);
+            if (t >= total) break;
+            OzProblem pr;
+            int m0, n0;
+            decode(t, pr, m0, n0);
+            if (skip_tile(pr, m0, n0)) continue;
+            int sa, sb;
+            digits_of(p, pr, m0, n0, sa, sb);
+            if (p.stats && lane == 0) {
+                atomicAdd(p.stats, static_cast<unsigned long long>(sa * sb));
+                atomicAdd(p.stats + 1, 1ull);
+            }
+            for (int g = sa + sb; g >= 2; g -= 2) {
+                const bool two = g - 1 >= 2;
+                // accumulators of groups g and g-1 (the next one in the rotation)
+                const int acc2 = acc + 1 == NACC ? 0 : acc + 1;
+                const uint32_t ph2 = acc + 1 == NACC ? acc_phase ^ 1 : acc_phase;
+                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                if (two) ptx::mbar_wait(&tempty[acc2], ph2 ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d1 = tmem_base + static_cast<uint32_t>(acc * BN);
+                const uint32_t d2 = tmem_base + static_cast<uint32_t>(acc2 * BN);
+                bool first1 = true, first2 = true;
+                const int lo = max(1, (two ? g - 1 : g) - sb), hi = min(sa, g - 1);
+                for (int dp = lo; dp <= hi; ++dp) {
+                    const bool v1 = dp >= max(1, g - sb);
+                    const bool v2 = two && dp <= min(sa, g - 2);
+                    for (int kb = 0; kb < p.kblocks; ++kb) {
+                        ptx::mbar_wait(&full[stage], phase);
+                        ptx::tc_fence_after();
+                        // K steps of 32 bytes advance the descriptors' start address field by 2
+                        const uint64_t ad = ptx::umma_desc_sw128(ptx::smem_u32(sA + stage * A_STAGE), 0, 1024);
+                        const uint64_t bd1 = ptx::umma_desc_sw128(ptx::smem_u32(sB + (stage * 2) * B_STAGE), 0, 1024);
+                        const uint64_t bd2 =
+                            ptx::umma_desc_sw128(ptx::smem_u32(sB + (stage * 2 + 1) * B_STAGE), 0, 1024);
+                        const uint32_t acc1_0 = first1 ? 0u : 1u, acc2_0 = first2 ? 0u : 1u;
+                        if (ptx::elect_one()) {
 #pragma unroll
-                            for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K per stage
-                                const uint64_t ad = ptx::umma_desc_sw128(a_base + k * 32, 0, 1024);
-                                if (v1)
-                                    mma_i8_ss(d1, ad, ptx::umma_desc_sw128(b1 + k * 32, 0, 1024), idesc,
-                                              (first1 && k == 0) ? 0u : 1u);
-                                if (v2)
-                                    mma_i8_ss(d2, ad, ptx::umma_desc_sw128(b2 + k * 32, 0, 1024), idesc,
-                                              (first2 && k == 0) ? 0u : 1u);
+                            for (int k = 0; k < 4; ++k) {
+                                if (v1) mma_i8_ss(d1, ad + 2 * k, bd1 + 2 * k, idesc, k == 0 ? acc1_0 : 1u);
+                                if (v2) mma_i8_ss(d2, ad + 2 * k, bd2 + 2 * k, idesc, k == 0 ? acc2_0 : 1u);
                             }
-                            if (v1) first1 = false;
-                            if (v2) first2 = false;
                             ptx::mma_commit(&empty[stage]);
-                            if (++stage == STAGES) {
-                                stage = 0;
-                                phase ^= 1;
-                            }
+                        }
+                        __syncwarp();
+                        if (v1) first1 = false;
+                        if (v2) first2 = false;
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            phase ^= 1;
                         }
                     }
+                }
+                if (ptx::elect_one()) {
                     ptx::mma_commit(&tfull[acc]);
-                    if (++acc == NACC) {
-                        acc = 0;
-                        acc_phase ^= 1;
-                    }
-                    if (two) {
-                        ptx::mma_commit(&tfull[acc]);
-                        if (++acc == NACC) {
-                            acc = 0;
-                            acc_phase ^= 1;
-                        }
-                    }
+                    if (two) ptx::mma_commit(&tfull[acc2]);
+                }
+                __syncwarp();
+                if (++acc == NACC) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+                if (two && ++acc == NACC) {
+                    acc = 0;
+                    acc_phase ^= 1;
                 }
             }
         }
@@ -275,13 +330,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
         const int r = lg * 32 + lane;       // tile row (TMEM lane)
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int64_t t = t_first; t < t_end; t += p.lanes) {
+        for (int it = 0;; ++it) {
+            const int64_t t = next_unit(it);
+            if (t >= total) break;
             OzProblem pr;
             int m0, n0;
             decode(t, pr, m0, n0);
             if (skip_tile(pr, m0, n0)) continue;
             int sa, sb;
-            digits_of(p, pr, sa, sb);
+            digits_of(p, pr, m0, n0, sa, sb);
             // C of this unit is read only after the last digit group: pull its
             // lines into L2 now, while the MMAs run (one lane per 16 rows, the
             // 64 columns of this warp's half), so the final pass does not wait
@@ -308,9 +365,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                                                 static_cast<uint32_t>(acc * BN + ch * 64 + c * 16),
                                             v);
                     ptx::tmem_ld_wait();
+                    // int32 -> double exactly on the FP64 pipe: the bits (0x43300000,
+                    // v ^ 2^31) are 2^52 + 2^31 + v (the conversion pipe's I2F.F64
+                    // runs at a quarter of the DFMA rate)
 #pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        sum[c * 16 + j] = fma(w, static_cast<double>(static_cast<int32_t>(v[j])), sum[c * 16 + j]);
+                    for (int j = 0; j < 16; ++j) {
+                        const double x = __hiloint2double(0x43300000, static_cast<int>(v[j] ^ 0x80000000u)) -
+                                         4503601774854144.0;
+                        sum[c * 16 + j] = fma(w, x, sum[c * 16 + j]);
+                    }
                 }
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&tempty[acc]);
@@ -361,9 +424,47 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
         ptx::tc_fence_after();
         ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
     }
+    if (threadIdx.x == 0) {  // the last CTA out resets the counters for the next launch
+        __threadfence();
+        if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
+            p.sched[0] = 0;
+            p.sched[1] = 0;
+        }
+    }
 }
 
 // ---- digit slicing -------------------------------------------------------------
+
+// Digit counts are kept per 128-row block (the GEMM's BM = BN): the four
+// 32-row stripes of a block run as one cluster, exchange their stripes' needs
+// through distributed shared memory, and write only the digit planes their
+// block needs (the GEMM reads no others).  Planes beyond a row's own need are
+// zeros, so a block's planes are exact for each of its rows.
+constexpr int OZ_BLOCK = 128, OZ_CLUSTER = OZ_BLOCK / 32;
+static_assert(BM == OZ_BLOCK && BN == OZ_BLOCK, "digit counts are per GEMM block");
+
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+
+// max over the cluster of thread 0's `need`; the kernel started with
+// cluster_arrive_relaxed() (peers must be running before their shared memory
+// is written)
+__device__ __forceinline__ int cluster_block_need(int need) {
+    __shared__ int sneed[OZ_CLUSTER];
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    if (threadIdx.x == 0) {
+        const uint32_t local = ptx::smem_u32(&sneed[ptx::cluster_ctarank()]);
+#pragma unroll
+        for (uint32_t r = 0; r < OZ_CLUSTER; ++r)
+            asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(ptx::mapa_shared(local, r)), "r"(need) : "memory");
+    }
+    ptx::cluster_sync_all();
+    int m = sneed[0];
+#pragma unroll
+    for (int r = 1; r < OZ_CLUSTER; ++r) m = max(m, sneed[r]);
+    return max(1, min(m, S));
+}
 
 // Digits of one FP16 value: Y = x * 2^(41 - e_r) is an integer |Y| < 2^41
 // with at most 11 significant bits, so it and every remainder Y - q 2^w (at
@@ -371,17 +472,39 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
 // q = rint(Y 2^-w), most significant first (weights 2^35 .. 2^0), |q| <= 64.
 // The rounding uses the 1.5 * 2^23 bias (FP32 adds, round-to-nearest-even),
 // and q is read from the biased value's bits: no conversion-pipe ops.
-__device__ __forceinline__ void oz_digits(uint16_t h, float scale, int8_t (&dig)[S][16], int j) {
+// Digit planes 0 .. nd-1 of 16 consecutive FP16 values of one row, one
+// 16-byte store per plane.  The low byte of the biased value's bits is q
+// itself (two's complement), so packing is three byte permutes per four
+// digits; planes past nd are neither computed nor stored.
+__device__ __forceinline__ void oz_digits16(const uint16_t (&h)[16], float scale, int nd, int8_t* out,
+                                            int64_t stride) {
     constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23
-    float Y = __half2float(__ushort_as_half(h)) * scale;
+    float Y[16];
 #pragma unroll
-    for (int d = 0; d < S - 1; ++d) {
-        const float w = __int_as_float((127 + 35 - 7 * d) << 23), iw = __int_as_float((127 - 35 + 7 * d) << 23);
-        const float t = fmaf(Y, iw, MAGIC);  // rint(Y 2^-w) + 1.5 * 2^23, exact
-        dig[d][j] = static_cast<int8_t>(__float_as_int(t) - 0x4B400000);
-        Y = fmaf(-(t - MAGIC), w, Y);
+    for (int j = 0; j < 16; ++j) Y[j] = __half2float(__ushort_as_half(h[j])) * scale;
+#pragma unroll
+    for (int d = 0; d < S; ++d) {
+        if (d >= nd) break;
+        uint32_t b[16];
+        if (d < S - 1) {
+            const float w = __int_as_float((127 + 35 - 7 * d) << 23), iw = __int_as_float((127 - 35 + 7 * d) << 23);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const float t = fmaf(Y[j], iw, MAGIC);  // rint(Y 2^-w) + 1.5 * 2^23, exact
+                b[j] = __float_as_uint(t);
+                Y[j] = fmaf(-(t - MAGIC), w, Y[j]);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) b[j] = __float_as_uint(Y[j] + MAGIC);  // |Y| <= 64, weight 2^0
+        }
+        uint4 v;
+        v.x = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+        v.y = __byte_perm(__byte_perm(b[4], b[5], 0x0040), __byte_perm(b[6], b[7], 0x0040), 0x5410);
+        v.z = __byte_perm(__byte_perm(b[8], b[9], 0x0040), __byte_perm(b[10], b[11], 0x0040), 0x5410);
+        v.w = __byte_perm(__byte_perm(b[12], b[13], 0x0040), __byte_perm(b[14], b[15], 0x0040), 0x5410);
+        *reinterpret_cast<uint4*>(out + d * stride) = v;
     }
-    dig[S - 1][j] = static_cast<int8_t>(__float_as_int(Y + MAGIC) - 0x4B400000);  // |Y| <= 64, weight 2^0
 }
 
 // One CTA per 32-row stripe of one matrix: (1) row exponent e_r with
@@ -391,6 +514,7 @@ __device__ __forceinline__ void oz_digits(uint16_t h, float scale, int8_t (&dig)
 // row per plane (16-byte stores).
 __device__ __forceinline__ void oz_slice_generic(const OzSliceItem& it, int64_t r0) {
     const uint16_t* x = static_cast<const uint16_t*>(it.x);
+    int need_stripe = 0;  // thread 0: digits this stripe's rows need
     __shared__ uint16_t sx[32][128 + 2];
     __shared__ uint32_t smax[8][33];
     __shared__ int sexp[32];
@@ -442,10 +566,8 @@ __device__ __forceinline__ void oz_slice_generic(const OzSliceItem& it, int64_t 
             }
             sexp[threadIdx.x] = e;
             it.rexp[r0 + threadIdx.x] = e;
-            if (it.ndig) {
-                for (int o = 16; o; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
-                if (threadIdx.x == 0) atomicMax(it.ndig, min(need, S));
-            }
+            for (int o = 16; o; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
+            need_stripe = need;
         }
         __syncthreads();
     } else {
@@ -475,10 +597,14 @@ __device__ __forceinline__ void oz_slice_generic(const OzSliceItem& it, int64_t 
                 frexp(h2d(static_cast<uint16_t>(m)), &e);
             sexp[threadIdx.x] = e;
             if (r0 + threadIdx.x < it.rows) it.rexp[r0 + threadIdx.x] = e;
-            if (it.ndig && threadIdx.x == 0) atomicMax(it.ndig, S);  // no digit analysis here
+            need_stripe = S;  // no digit analysis here
         }
         __syncthreads();
     }
+    // planes written: the block's need (all S when the caller keeps no counts)
+    const int bn = cluster_block_need(need_stripe);  // every CTA of the cluster takes part
+    const int bneed = it.ndig ? bn : S;
+    if (it.ndig && threadIdx.x == 0 && ptx::cluster_ctarank() == 0) it.ndig[r0 / OZ_BLOCK] = bneed;
     // (2) digits
     const int lr = threadIdx.x / 8, cg = (threadIdx.x % 8) * 16;
     const int64_t gr = r0 + lr;
@@ -513,24 +639,25 @@ __device__ __forceinline__ void oz_slice_generic(const OzSliceItem& it, int64_t 
         }
         __syncthreads();
         if (gr < it.rows && c0 + cg < it.kpad) {
-            alignas(16) int8_t dig[S][16];
             const float scale = zero ? 0.0f : __int_as_float((127 + 41 - er) << 23);
+            uint16_t hv[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) oz_digits(sx[lr][cg + j], scale, dig, j);
-            int8_t* out = static_cast<int8_t*>(it.out) + gr * it.kpad + c0 + cg;
-#pragma unroll
-            for (int d = 0; d < S; ++d)
-                *reinterpret_cast<int4*>(out + d * it.slice_stride) = *reinterpret_cast<const int4*>(dig[d]);
+            for (int j = 0; j < 16; ++j) hv[j] = sx[lr][cg + j];
+            oz_digits16(hv, scale, bneed, static_cast<int8_t*>(it.out) + gr * it.kpad + c0 + cg, it.slice_stride);
         }
         __syncthreads();
     }
 }
 
 
-__global__ void __launch_bounds__(256) oz_slice_kernel(const OzSliceItem* items) {
+__global__ void __cluster_dims__(OZ_CLUSTER, 1, 1) __launch_bounds__(256) oz_slice_kernel(const OzSliceItem* items) {
+    cluster_arrive_relaxed();
     const OzSliceItem it = items[blockIdx.y];
     const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
-    if (r0 >= it.rows) return;
+    if (r0 >= it.rows) {  // past this matrix's rows: only the exchange
+        cluster_block_need(0);
+        return;
+    }
     oz_slice_generic(it, r0);
 }
 
@@ -539,10 +666,15 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(const OzSliceItem* items)
 // exponents and digit counts come from the registers on the way, and the
 // digits are cut from shared memory -- one HBM read of the operand.
 constexpr int OZ_STRIPE_K = 1024;
-__global__ void __launch_bounds__(256) oz_slice_stripe_kernel(const OzSliceItem* items) {
+__global__ void __cluster_dims__(OZ_CLUSTER, 1, 1) __launch_bounds__(256)
+    oz_slice_stripe_kernel(const OzSliceItem* items) {
+    cluster_arrive_relaxed();
     const OzSliceItem it = items[blockIdx.y];
     const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
-    if (r0 >= it.rows) return;
+    if (r0 >= it.rows) {
+        cluster_block_need(0);
+        return;
+    }
     const uint16_t* x = static_cast<const uint16_t*>(it.x);
     const bool vec = !it.trans && r0 + 32 <= it.rows && (it.ld % 8) == 0 &&
                      (reinterpret_cast<uintptr_t>(x) & 15) == 0 && it.kpad <= OZ_STRIPE_K;
@@ -561,6 +693,7 @@ __global__ void __launch_bounds__(256) oz_slice_stripe_kernel(const OzSliceItem*
     const int rg = threadIdx.x % 4;  // rows rg*8 .. rg*8+7
     uint32_t mx[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     uint32_t mn[8] = {31, 31, 31, 31, 31, 31, 31, 31};  // min exponent field of nonzeros
+    int need_stripe = 0;
     const int cols = static_cast<int>(it.cols), kp = static_cast<int>(it.kpad);
     for (int c0 = threadIdx.x / 4; c0 < kp; c0 += 64 * 4) {
         uint4 v[4];
@@ -607,27 +740,24 @@ __global__ void __launch_bounds__(256) oz_slice_stripe_kernel(const OzSliceItem*
         }
         sexp[threadIdx.x] = e;
         it.rexp[r0 + threadIdx.x] = e;
-        if (it.ndig) {
-            for (int o = 16; o; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
-            if (threadIdx.x == 0) atomicMax(it.ndig, min(need, S));
-        }
+        for (int o = 16; o; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
+        need_stripe = need;
     }
     __syncthreads();
+    // planes written: the block's need (all S when the caller keeps no counts)
+    const int bn = cluster_block_need(need_stripe);  // every CTA of the cluster takes part
+    const int bneed = it.ndig ? bn : S;
+    if (it.ndig && threadIdx.x == 0 && ptx::cluster_ctarank() == 0) it.ndig[r0 / OZ_BLOCK] = bneed;
     const int lr = threadIdx.x / 8, cg = (threadIdx.x % 8) * 16;
     const int er = sexp[lr];
     const float scale = er == ROWEXP_NONFINITE ? 0.0f : __int_as_float((127 + 41 - er) << 23);
     const uint16_t* row = sxf + lr * KS;
     int8_t* outr = static_cast<int8_t*>(it.out) + (r0 + lr) * it.kpad;
     for (int c0 = cg; c0 < kp; c0 += 128) {
-        alignas(16) int8_t dig[S][16];
         alignas(16) uint16_t hv[16];
         *reinterpret_cast<uint4*>(hv) = *reinterpret_cast<const uint4*>(row + c0);
         *reinterpret_cast<uint4*>(hv + 8) = *reinterpret_cast<const uint4*>(row + c0 + 8);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) oz_digits(hv[j], scale, dig, j);
-#pragma unroll
-        for (int d = 0; d < S; ++d)
-            *reinterpret_cast<int4*>(outr + d * it.slice_stride + c0) = *reinterpret_cast<const int4*>(dig[d]);
+        oz_digits16(hv, scale, bneed, outr + c0, it.slice_stride);
     }
 }
 }  // namespace oz
@@ -636,7 +766,9 @@ void launch_oz_slices(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_
                       int64_t max_cols) {
     if (count == 0) return;
     ProfScope ps(ctx, MP_PROF_CAST, s, 0.0);
-    const dim3 grid(static_cast<unsigned>((max_rows + 31) / 32), static_cast<unsigned>(count));
+    // 32-row stripes, whole 128-row blocks (clusters of four stripes)
+    const dim3 grid(static_cast<unsigned>((max_rows + oz::OZ_BLOCK - 1) / oz::OZ_BLOCK * oz::OZ_CLUSTER),
+                    static_cast<unsigned>(count));
     if (max_cols <= oz::OZ_STRIPE_K) {
         const int kpad = static_cast<int>((max_cols + 15) / 16 * 16);
         const int smem = 32 * (kpad + 8) * 2;
@@ -665,6 +797,7 @@ void launch_oz_gemm(Ctx* ctx, cudaStream_t s, const OzGemm& g) {
     p.problems = g.problems;
     p.single = OzProblem{0, 0, g.C, g.lower_only ? 1 : 0};
     p.nprob = g.problems ? static_cast<int32_t>(g.count) : 1;
+    p.nlower = g.problems ? static_cast<int32_t>(g.n_lower) : (g.lower_only ? 1 : 0);
     p.M = static_cast<int32_t>(g.m);
     p.N = static_cast<int32_t>(g.n);
     p.K = static_cast<int32_t>(g.k);
@@ -680,21 +813,21 @@ void launch_oz_gemm(Ctx* ctx, cudaStream_t s, const OzGemm& g) {
     p.rexp_stride_b = g.rexp_stride_b;
     p.ndig_a = g.ndig_a;
     p.ndig_b = g.ndig_b;
+    p.ndig_stride_a = static_cast<int32_t>(g.ndig_stride_a);
+    p.ndig_stride_b = static_cast<int32_t>(g.ndig_stride_b);
     p.stats = ctx->prof.enabled ? ctx->prof.dev_stats : nullptr;
-    const int64_t total = static_cast<int64_t>(p.nprob) * p.mblocks * p.nblocks;
+    const int64_t jl = std::min(p.mblocks, p.nblocks);
+    const int64_t total = static_cast<int64_t>(p.nlower) * (jl * p.mblocks - jl * (jl - 1) / 2) +
+                          static_cast<int64_t>(p.nprob - p.nlower) * p.mblocks * p.nblocks;
     ProfScope ps(ctx, MP_PROF_GEMM_I8, s,
                  2.0 * static_cast<double>(g.m) * g.n * g.k * p.nprob * (g.lower_only ? 0.5 : 1.0));
     static unsigned long long configured = 0;  // per-device bitmask
     if (first_on_device(configured)) {
         MP_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     }
-    const int64_t grid = std::max<int64_t>(persistent_grid(total, ctx->sm_count, g.tiles_per_cta), 1);
-    static const bool strided = [] {  // MPCR_UNIT_STRIDED=1: classic grid-stride assignment
-        const char* e = getenv("MPCR_UNIT_STRIDED");
-        return e && e[0] == '1';
-    }();
-    p.lanes = static_cast<int32_t>(strided ? grid : std::min<int64_t>(ctx->sm_count, grid));
-    p.per = static_cast<int32_t>((std::max<int64_t>(total, 1) + grid - 1) / grid);
+    // one CTA per SM (or per unit), units drawn dynamically
+    const int64_t grid = std::max<int64_t>(std::min<int64_t>(total, ctx->sm_count), 1);
+    p.sched = ctx->sched_slot();
     oz_gemm_kernel<<<static_cast<unsigned>(grid), NTHREADS, SMEM_BYTES, s>>>(p);
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());

@@ -27,13 +27,13 @@ struct OzProblem {
 // Slice one FP16 matrix (rows x cols, element (r, c) at x[c * ld + r], or
 // x[r * ld + c] when trans) into OZ_SLICES int8 digit planes [S][rows][kpad]
 // (planes slice_stride bytes apart) and per-row exponents rexp[rows].  The
-// number of planes that are not all zero (exactness needs only those) is
-// max-reduced into *ndig.
+// number of planes each 128-row block needs (exactness needs only those; the
+// others are not written) goes to ndig[block].
 struct OzSliceItem {
     const void* x;
     void* out;
     int32_t* rexp;
-    int32_t* ndig;  // optional: atomicMax of the digits this matrix needs (pre-zeroed)
+    int32_t* ndig;  // optional: digits per 128-row block [ceil(rows / 128)] (without it every plane is written)
     int64_t ld, rows, cols, kpad, slice_stride;
     int32_t trans;
     int32_t pad;
@@ -54,12 +54,14 @@ struct OzGemm {
     bool lower_only = false;
     const OzProblem* problems = nullptr;  // device array (grouped) or nullptr
     int64_t count = 0;
+    int64_t n_lower = 0;  // grouped: the first n_lower problems are lower_only (the rest are not)
     const int32_t* rexp_a = nullptr;
     const int32_t* rexp_b = nullptr;
-    const int32_t* ndig_a = nullptr;  // optional digits needed per tile (<= OZ_SLICES)
+    const int32_t* ndig_a = nullptr;  // digits per 128-row block (<= OZ_SLICES), ndig_stride_* blocks per tile
     const int32_t* ndig_b = nullptr;
+    int64_t ndig_stride_a = 0, ndig_stride_b = 0;
     int64_t rexp_stride_a = 0, rexp_stride_b = 0;  // between tiles
-    int tiles_per_cta = 0;
+
 };
 
 void launch_oz_slices(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_t count, int64_t max_rows,

@@ -48,7 +48,7 @@ struct mp_tile_s {
     void* panel[3] = {nullptr, nullptr, nullptr};
     void* digits = nullptr;  // INT8 digit planes of FP16 panel tiles [2][tr][S][br][br]
     int32_t* rexp = nullptr;  // their row exponents [2][tr][br]
-    int32_t* ndig = nullptr;  // digits each of them needs [2][tr]
+    int32_t* ndig = nullptr;  // digits each 128-row block of them needs [gens][tr][ceil(br / 128)]
     void* backup[3] = {nullptr, nullptr, nullptr};  // jittered-NLL copy of the input slabs
     void* work = nullptr;  // FP64 + FP32 diagonal work, two Linv generations, info (WorkLayout)
     void* lists = nullptr;
@@ -134,7 +134,7 @@ struct WorkLayout {
 // step k+1 is produced while the trailing update still reads panel k, and
 // with paired steps (below) the bulk update of an even step k runs during
 // step k+1, still reading panel k while panel k+2 is produced.
-constexpr int PANEL_GENS = 3;
+constexpr int PANEL_GENS = 4;
 
 void ensure_panels(mp_tile_s& t) {
     for (int q = 0; q < 3; ++q)
@@ -143,7 +143,7 @@ void ensure_panels(mp_tile_s& t) {
     if (!t.digits && ozaki_enabled()) {
         MP_CUDA(cudaMalloc(&t.digits, PANEL_GENS * static_cast<size_t>(t.tr) * OZ_SLICES * t.tt()));
         MP_CUDA(cudaMalloc(&t.rexp, PANEL_GENS * static_cast<size_t>(t.tr) * t.br * sizeof(int32_t)));
-        MP_CUDA(cudaMalloc(&t.ndig, PANEL_GENS * static_cast<size_t>(t.tr) * sizeof(int32_t)));
+        MP_CUDA(cudaMalloc(&t.ndig, PANEL_GENS * static_cast<size_t>(t.tr) * ((t.br + 127) / 128) * sizeof(int32_t)));
     }
     if (!t.work) MP_CUDA(cudaMalloc(&t.work, WorkLayout(t.br).bytes()));
     if (t.events.empty()) {
@@ -171,7 +171,7 @@ void append(std::vector<char>& buf, const std::vector<V>& v, size_t& off) {
 // (two K segments, one read-modify-write of C).
 struct UpLists {
     size_t tc = 0, tc16s = 0, simt16 = 0, oz = 0, dm[3][3][2] = {}, tcf = 0, tcf16s = 0;
-    int64_t n_tc = 0, n_tc16s = 0, n_simt16 = 0, n_oz = 0, n_dm[3][3][2] = {}, n_tcf = 0, n_tcf16s = 0;
+    int64_t n_tc = 0, n_tc16s = 0, n_simt16 = 0, n_oz = 0, n_oz_lower = 0, n_dm[3][3][2] = {}, n_tcf = 0, n_tcf16s = 0;
 };
 
 struct StepLists {
@@ -190,7 +190,9 @@ struct StepLists {
     int64_t n_cv[3][3][3] = {};
     size_t digits[3] = {0, 0, 0};  // INT8 digit slicing of FP16 panel tiles (same split)
     int64_t n_digits[3] = {0, 0, 0};
-    UpLists up[3][2];  // [0: tile column k+1 below the diagonal, 1: the rest, 2: tile (k+1, k+1)][source panel]
+    // [0: tile column k+1 below the diagonal, 1: the rest, 2: tile (k+1, k+1),
+    //  3: tile column k+2 of a paired step][source panel]
+    UpLists up[4][2];
     bool diag_bcast = false;  // receive / send L_kk^-1 down this process column
     struct Bcast {
         int i, root, comm;
@@ -306,13 +308,14 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         return static_cast<int8_t*>(t.digits) + ((k % PANEL_GENS) * NT + i) * dig_tile;
     };
     auto rex = [&](int64_t i, int64_t k) -> int32_t* { return t.rexp + ((k % PANEL_GENS) * NT + i) * nb; };
-    auto ndg = [&](int64_t i, int64_t k) -> int32_t* { return t.ndig + (k % PANEL_GENS) * NT + i; };
+    const int64_t NDB = (nb + 127) / 128;  // digit-count blocks per tile
+    auto ndg = [&](int64_t i, int64_t k) -> int32_t* { return t.ndig + ((k % PANEL_GENS) * NT + i) * NDB; };
     struct StepAcc {
         std::vector<TcProblem> trsm_tc[2];
         std::vector<TileProblem> trsm_p[2][3];
         std::vector<CopyItem> wb[3], cv[3][3][3];
         std::vector<OzSliceItem> digits[3];
-        UpAcc up[3][2];
+        UpAcc up[4][2];
     };
     // Head/tail split of the panel TRSM (single GPU with lookahead): the head
     // tile runs on the critical-path stream, the rest of the column on the
@@ -334,19 +337,36 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                : q == MP_SINGLE ? static_cast<const void*>(WL.linvS(t.work, g))
                                 : static_cast<const void*>(WL.linv64(t.work, g));
     };
+    // Paired steps (MPCR_PAIR_STEPS=0 turns them off): the trailing update of
+    // an even step k is deferred into step k+1, where tensor-core tiles take
+    // both panels in one pass (K = 2 nb, C read and written once instead of
+    // twice, rounded once).  Tile column k+2 of an odd step k leaves the
+    // paired bulk for the lookahead stream (part 3), so neither of the next
+    // two critical chains waits on the paired bulk that precedes them; the
+    // panel, digit and exponent buffers live in four generations (panel k+1
+    // is produced while the bulk still reads panels k-2 and k-1).
+    static const bool pair_env = [] {
+        const char* e = getenv("MPCR_PAIR_STEPS");
+        return !(e && e[0] == '0');
+    }();
+    const bool pair_steps = pair_env && NT > 2;
+    // tile columns whose updates from panel k run on the lookahead streams:
+    // their operand copies / digits are made with the panel, not with the bulk
+    auto la_col = [&](int64_t k, int64_t j) { return j == k + 1 || (pair_steps && j == k + 2); };
     auto consumers = [&](int64_t k, int64_t i, StepAcc& A) {
         // every rank receives every panel tile: convert it once to each
         // precision the rank's own consumers (A_ij.converted(p) operands)
-        // need.  Copies read by the lookahead updates (tile column k+1) are
-        // made on the critical path ([0]); the rest with the bulk update ([1]).
+        // need.  Copies read by the lookahead updates (tile column k+1, and
+        // k+2 with paired steps) are made on the critical path ([0]); the rest
+        // with the bulk update ([1]).
         const mp_precision q = t.p(i, k);
         bool need[2][3] = {{false, false, false}, {false, false, false}};
         for (int64_t j = k + 1; j <= i; ++j)  // A operand of (owned) row-i updates
             if (t.has(i, j) && !(t.p(i, j) == MP_DOUBLE && ozaki64(i, j, k)))
-                need[j == k + 1 ? 0 : 1][opnd_prec(t.p(i, j), i, k)] = true;
+                need[la_col(k, j) ? 0 : 1][opnd_prec(t.p(i, j), i, k)] = true;
         for (int64_t m = i; m < NT; ++m)  // B operand of (owned) column-i updates
             if (t.has(m, i) && !(t.p(m, i) == MP_DOUBLE && ozaki64(m, i, k)))
-                need[i == k + 1 ? 0 : 1][opnd_prec(t.p(m, i), i, k)] = true;
+                need[la_col(k, i) ? 0 : 1][opnd_prec(t.p(m, i), i, k)] = true;
         const int h0 = (tsplit && i == k + 1) ? 2 : 0;  // the head tile's part-0 work
         for (int r = 0; r < 3; ++r) {
             if (r == q) continue;
@@ -355,24 +375,15 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         }
         bool need_dig[2] = {false, false};
         for (int64_t j = k + 1; j <= i; ++j)
-            if (t.has(i, j) && t.p(i, j) == MP_DOUBLE && ozaki64(i, j, k)) need_dig[j == k + 1 ? 0 : 1] = true;
+            if (t.has(i, j) && t.p(i, j) == MP_DOUBLE && ozaki64(i, j, k)) need_dig[la_col(k, j) ? 0 : 1] = true;
         for (int64_t m = i; m < NT; ++m)
-            if (t.has(m, i) && t.p(m, i) == MP_DOUBLE && ozaki64(m, i, k)) need_dig[i == k + 1 ? 0 : 1] = true;
+            if (t.has(m, i) && t.p(m, i) == MP_DOUBLE && ozaki64(m, i, k)) need_dig[la_col(k, i) ? 0 : 1] = true;
         const int hd = need_dig[0] ? h0 : need_dig[1] ? 1 : -1;
         if (hd >= 0)
             A.digits[hd].push_back(
                 OzSliceItem{pan(MP_HALF, i, k), dig(i, k), rex(i, k), ndg(i, k), nb, nb, nb, nb, tt, 0, 0});
     };
     std::vector<char> have(NT * NT, 0);  // panel tile (i, k) present on this rank (conversions made)
-    // Paired steps (MPCR_PAIR_STEPS=0 turns them off): the trailing update of
-    // an even step k is deferred into step k+1, where tensor-core tiles take
-    // both panels in one pass (K = 2 nb, C read and written once instead of
-    // twice, rounded once).
-    static const bool pair_env = [] {
-        const char* e = getenv("MPCR_PAIR_STEPS");
-        return !(e && e[0] == '0');
-    }();
-    const bool pair_steps = pair_env && NT > 2;
     struct TcCand {
         int64_t ks;
         int part, kind, src;  // kind 0: FP16 tile, 1: FP32 tile fed by FP16 panels
@@ -416,7 +427,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 const bool defer = pair_steps && (k % 2 == 0) && j >= k + 2;
                 const int64_t ks = defer ? k + 1 : k;
                 const int src = defer ? 0 : 1;
-                const int part = j != ks + 1 ? 1 : i == j ? 2 : 0;
+                const int part = j == ks + 1 ? (i == j ? 2 : 0) : (pair_steps && ks % 2 == 1 && j == ks + 2) ? 3 : 1;
                 UpAcc& U = acc[ks].up[part][src];
                 const int32_t lo = (i == j) ? 1 : 0;
                 const TcProblem tp{static_cast<int32_t>(i), static_cast<int32_t>(j),
@@ -480,7 +491,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         return x.b_tile < y.b_tile;
     };
     for (int64_t k = 0; k < NT; ++k)
-        for (int w = 0; w < 3; ++w)
+        for (int w = 0; w < 4; ++w)
             for (int sc = 0; sc < 2; ++sc) {
                 std::stable_sort(acc[k].up[w][sc].tc.begin(), acc[k].up[w][sc].tc.end(), grouped);
                 std::stable_sort(acc[k].up[w][sc].tcf.begin(), acc[k].up[w][sc].tcf.end(), grouped);
@@ -510,7 +521,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             append(buf, A.digits[h], L.digits[h]);
             L.n_digits[h] = A.digits[h].size();
         }
-        for (int w = 0; w < 3; ++w)
+        for (int w = 0; w < 4; ++w)
             for (int sc = 0; sc < 2; ++sc) {
                 const UpAcc& U = A.up[w][sc];
                 UpLists& D = L.up[w][sc];
@@ -524,8 +535,14 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 D.n_tcf16s = U.tcf16s.size();
                 append(buf, U.simt16, D.simt16);
                 D.n_simt16 = U.simt16.size();
-                append(buf, U.oz, D.oz);
-                D.n_oz = U.oz.size();
+                // diagonal (lower-only) problems first: the kernel enumerates
+                // only their live units
+                std::vector<OzProblem> oz = U.oz;
+                const auto lower_end =
+                    std::stable_partition(oz.begin(), oz.end(), [](const OzProblem& o) { return o.lower_only != 0; });
+                D.n_oz_lower = lower_end - oz.begin();
+                append(buf, oz, D.oz);
+                D.n_oz = oz.size();
                 for (int a = 0; a < 3; ++a)
                     for (int b = 0; b < 3; ++b)
                         for (int c2 = 0; c2 < 2; ++c2) {
@@ -575,11 +592,12 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             launch_oz_slices(c, st, reinterpret_cast<const OzSliceItem*>(dl + L.digits[h]), L.n_digits[h], nb, nb);
             static const bool dbg = getenv("MPCR_DEBUG_NDIG") != nullptr;  // diagnostics (eager runs only)
             if (dbg && h == 1) {
-                std::vector<int32_t> nd(NT);
-                MP_CUDA(cudaMemcpyAsync(nd.data(), ndg(0, k), NT * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+                std::vector<int32_t> nd(NT * NDB);
+                MP_CUDA(cudaMemcpyAsync(nd.data(), ndg(0, k), nd.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
                 MP_CUDA(cudaStreamSynchronize(st));
-                int hist[8] = {};
-                for (int64_t i = k + 1; i < NT; ++i) hist[std::min(7, std::max(0, nd[i]))]++;
+                int hist[8] = {};  // per 128-row block
+                for (int64_t i = k + 1; i < NT; ++i)
+                    for (int64_t b = 0; b < NDB; ++b) hist[std::min(7, std::max(0, nd[i * NDB + b]))]++;
                 std::fprintf(stderr, "[mpcr] step %lld digits:", static_cast<long long>(k));
                 for (int q = 0; q < 8; ++q) std::fprintf(stderr, " %d", hist[q]);
                 std::fprintf(stderr, "\n");
@@ -673,8 +691,6 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     // conversions.  Without the head/tail split the whole column follows here.
     auto panel_head = [&](int64_t k, cudaStream_t st, cudaEvent_t before_trsm) {
         const StepLists& L = steps[k];
-        if (L.n_digits[0] + L.n_digits[1] + L.n_digits[2])  // digit counts of panel k are max-reduced
-            MP_CUDA(cudaMemsetAsync(ndg(0, k), 0, NT * sizeof(int32_t), st));
         const mp_precision pk = t.p(k, k);
         void* akk = t.ptr(k, k);
         const int lg = static_cast<int>(k & 1);  // Linv generation of this step
@@ -787,10 +803,11 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 o.beta = 1.0;
                 o.problems = reinterpret_cast<const OzProblem*>(dl + U.oz);
                 o.count = U.n_oz;
+                o.n_lower = U.n_oz_lower;
                 o.rexp_a = o.rexp_b = rex(0, kp);
                 o.ndig_a = o.ndig_b = ndg(0, kp);
+                o.ndig_stride_a = o.ndig_stride_b = NDB;
                 o.rexp_stride_a = o.rexp_stride_b = nb;
-                o.tiles_per_cta = tiles_per_cta;
                 launch_oz_gemm(c, st, o);
             }
             // FP32 / FP64 tiles on DMMA: exact products of the widened panel
@@ -887,13 +904,17 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             if (!wb_async || k + 1 >= NT) write_back(k, s);
             if (la) MP_CUDA(cudaEventRecord(ev_rest[k], s));
             if (k + 1 < NT) {
+                // after a paired bulk (odd k-1) the lookahead work of step k
+                // touches only columns that bulk left to the lookahead stream
+                const bool after_bulk = k >= 1 && !(pair_steps && (k - 1) % 2 == 1);
                 if (la) {
                     MP_CUDA(cudaStreamWaitEvent(sl2, ev_panel[k], 0));
-                    if (k >= 1) MP_CUDA(cudaStreamWaitEvent(sl2, ev_rest[k - 1], 0));
+                    if (after_bulk) MP_CUDA(cudaStreamWaitEvent(sl2, ev_rest[k - 1], 0));
                 }
                 update_phase(k, 0, sl2, 0);
+                update_phase(k, 3, sl2, 0);  // paired odd step: tile column k+2
                 if (la) MP_CUDA(cudaEventRecord(ev_next[k], sl2));
-                if (la && k >= 1) MP_CUDA(cudaStreamWaitEvent(sl, ev_rest[k - 1], 0));
+                if (la && after_bulk) MP_CUDA(cudaStreamWaitEvent(sl, ev_rest[k - 1], 0));
                 update_phase(k, 2, sl, 0);
                 panel_phase(k + 1, la ? ev_next[k] : nullptr);
                 if (wb_async) write_back(k, sl2);

@@ -346,6 +346,44 @@ def test_gemm_half_to_double_large_k_chunks(ctx, ta, tb):
     assert err.max() <= 16 * 2.0 ** -53, float(err.max())
 
 
+def test_gemm_half_to_double_block_digit_counts(ctx):
+    """Digit counts are kept per 128-row block and the slicer writes only the
+    planes a block needs: blocks of one operand needing 1, 2, .. 6 digits (and
+    an all-zero block), after a call that filled every plane of the same
+    scratch with nonzero digits -- the stale planes must never be read."""
+    import paper_2406_02701_b200 as mp
+    from oracle.oracle import round_to
+
+    r = np.random.default_rng(11)
+    m, n, k = 896, 256, 512
+    # warm-up: every row spans 2^-24 .. 2^5 -> six digits in every block
+    W = round_to(r.standard_normal((m, k)) * np.exp2(r.integers(-24, 5, size=(m, k))), H)
+    dw = mp.MPArray.from_numpy(W, mp.Precision.Half, ctx)
+    dwb = mp.MPArray.from_numpy(W[:n].T.copy(), mp.Precision.Half, ctx)
+    dc0 = mp.MPArray.zeros_matrix(m, n, mp.Precision.Double, ctx)
+    mp.linalg.gemm(dw, dwb, dc0)
+    # block b of A: dynamic range growing with b (block 6 all zero)
+    A = np.zeros((m, k))
+    for b in range(7):
+        rows = slice(b * 128, (b + 1) * 128)
+        if b == 6:
+            continue
+        span = 1 + 7 * b  # binades
+        A[rows] = r.standard_normal((128, k)) * np.exp2(-r.integers(0, span, size=(128, k)))
+    A = round_to(A, H)
+    B = round_to(r.standard_normal((k, n)), H)
+    da = mp.MPArray.from_numpy(A, mp.Precision.Half, ctx)
+    db = mp.MPArray.from_numpy(B, mp.Precision.Half, ctx)
+    dc = mp.MPArray.zeros_matrix(m, n, mp.Precision.Double, ctx)
+    mp.linalg.gemm(da, db, dc)
+    got = dc.to_numpy()
+    exact = A.astype(np.longdouble) @ B.astype(np.longdouble)
+    scale = np.abs(A) @ np.abs(B)
+    err = np.abs(got.astype(np.longdouble) - exact) / np.where(scale > 0, scale, 1.0)
+    assert err.max() <= 16 * 2.0 ** -53, float(err.max())
+    assert np.all(got[768:] == 0.0)
+
+
 def test_gemm_half_to_double_nonfinite(ctx):
     """Inf/NaN in an FP16 operand row propagate as NaN to that output row."""
     import paper_2406_02701_b200 as mp
