@@ -112,11 +112,14 @@ def flops_by_pipe(nt, nb, g):
                   panel tiles are FP16 (exact products, FP32 accumulate), the
                   FP16 panel TRSM (tcgen05 kind::f16);
       int8_digits FP64-destination updates with two FP16 panel tiles (exact
-                  INT8 digit products, tcgen05 kind::i8);
+                  INT8 digit products, tcgen05 kind::i8) and FP32-destination
+                  updates with FP32 (or FP32 + FP16) panel tiles (the same
+                  digits; MPCR_OZAKI32=0 sends these to DMMA);
       dmma        every other FP32/FP64-destination update (panel tiles widened
                   exactly, FP64 accumulate), the FP32 and FP64 panel TRSM,
                   POTRF (mma.sync .f64)."""
     f = dict.fromkeys(PIPES, 0.0)
+    oz32 = os.environ.get("MPCR_OZAKI32", "1") != "0"
     b3 = float(nb) ** 3
     for k in range(nt):
         f["dmma"] += b3 / 3
@@ -128,7 +131,12 @@ def flops_by_pipe(nt, nb, g):
                 if d == 0:
                     f["tc_f16"] += w
                 elif d == 1:
-                    f["tc_f16" if pa == 0 and pb == 0 else "dmma"] += w
+                    if pa == 0 and pb == 0:
+                        f["tc_f16"] += w
+                    elif oz32 and pa <= 1 and pb <= 1:
+                        f["int8_digits"] += w
+                    else:
+                        f["dmma"] += w
                 else:
                     f["int8_digits" if pa == 0 and pb == 0 else "dmma"] += w
     return f

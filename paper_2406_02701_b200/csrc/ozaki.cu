@@ -51,7 +51,8 @@ constexpr int S = OZ_SLICES;  // digits per value
 // so each A k-block feeds two MMAs (a quarter less operand ingress).
 constexpr int BM = 128, BN = 128, BK = 128, STAGES = 4;
 constexpr int A_STAGE = BM * BK, B_STAGE = BN * BK;  // 16 KB each
-constexpr int SMEM_BYTES = STAGES * (A_STAGE + 2 * B_STAGE) + 1024 + 256;  // + barriers, unit ring
+// + barriers, unit ring, the epilogue warps' column scales
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + 2 * B_STAGE) + 1024 + 256 + 8 * 64 * 8;
 constexpr int NACC = 4;          // int32 accumulators in flight (MMA runs NACC groups ahead)
 constexpr int TMEM_COLS = 512;  // NACC x 128 columns
 constexpr int NTHREADS = 320;   // 10 warps
@@ -77,6 +78,7 @@ struct Params {
     // dynamic unit scheduling: [0] next unit, [1] CTAs finished (the last
     // CTA resets both)
     unsigned int* sched;
+    int32_t c_f32;  // C is FP32 (one rounding of the FP64 result), else FP64
     unsigned long long* stats;  // profiling: [0] += sa*sb per output tile, [1] += 1 (or nullptr)
 };
 
@@ -108,6 +110,37 @@ __device__ __forceinline__ double pow2(int e) {
     return __longlong_as_double(static_cast<long long>(1023 + e) << 52);
 }
 
+// One row's 64 (or ncol) outputs: C = sum * (2^e_r * alpha 2^e_c) + beta C,
+// one rounding into TC.  All loads of a chunk of 8 precede its stores.
+template <typename TC>
+__device__ __forceinline__ void store_row(TC* Cr, int64_t ldc, const double (&sum)[64], const double* cs, double sr,
+                                          double beta, int ncol) {
+    if (ncol == 64) {
+#pragma unroll
+        for (int jb = 0; jb < 64; jb += 8) {
+            double cv[8];
+            if (beta != 0.0) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) cv[u] = static_cast<double>(Cr[(jb + u) * ldc]);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                double out = sum[jb + u] * (sr * cs[jb + u]);
+                if (beta != 0.0) out = fma(beta, cv[u], out);
+                Cr[(jb + u) * ldc] = static_cast<TC>(out);
+            }
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < 64; ++j) {
+            if (j >= ncol) break;
+            double out = sum[j] * (sr * cs[j]);
+            if (beta != 0.0) out = fma(beta, static_cast<double>(Cr[j * ldc]), out);
+            Cr[j * ldc] = static_cast<TC>(out);
+        }
+    }
+}
+
 __device__ __forceinline__ bool skip_tile(const OzProblem& pr, int m0, int n0) {
     return pr.lower_only && (m0 + BM - 1 < n0);
 }
@@ -127,6 +160,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
     uint64_t* uempty = ufull + UR;
     int32_t* uring = reinterpret_cast<int32_t*>(uempty + UR);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uring + UR);
+    double* colscale = reinterpret_cast<double*>(tmem_slot + 2);  // [8 epilogue warps][64]
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (warp == 0 && lane == 0) {
@@ -201,13 +235,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            // the next unit is drawn one unit ahead: the atomic's round trip
+            // overlaps this unit's loads instead of stalling the MMA warp
+            int64_t t_next = static_cast<int64_t>(atomicAdd(p.sched, 1u));
             for (int it = 0;; ++it) {
                 const int slot = it % UR;
+                const int64_t t = t_next;
                 ptx::mbar_wait(&uempty[slot], static_cast<uint32_t>(((it / UR) & 1) ^ 1));
-                const int64_t t = static_cast<int64_t>(atomicAdd(p.sched, 1u));
                 uring[slot] = static_cast<int32_t>(t < total ? t : total);
                 ptx::mbar_arrive(&ufull[slot]);
                 if (t >= total) break;
+                t_next = static_cast<int64_t>(atomicAdd(p.sched, 1u));
                 OzProblem pr;
                 int m0, n0;
                 decode(t, pr, m0, n0);
@@ -344,11 +382,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
             // 64 columns of this warp's half), so the final pass does not wait
             // on DRAM latency per 8-column chunk
             if (p.beta != 0.0 && (lane & 15) == 0 && m0 + r < p.M) {
-                const double* Cp = static_cast<const double*>(pr.c) + (m0 + r);
+                const int64_t es = p.c_f32 ? 4 : 8;
+                const char* Cp = static_cast<const char*>(pr.c) + (m0 + r) * es;
                 for (int jb = 0; jb < 64; ++jb) {
                     const int col = n0 + ch * 64 + jb;
                     if (col < p.N)
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(Cp + static_cast<int64_t>(col) * p.ldc));
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(Cp + static_cast<int64_t>(col) * p.ldc * es));
                 }
             }
             double sum[64];
@@ -382,41 +421,34 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                     acc_phase ^= 1;
                 }
             }
-            // C = alpha * 2^(e_r + e_c) * sum + beta * C, 8 columns at a time:
-            // all loads of a chunk are issued before its stores (a store may
-            // alias a later load, so interleaving would serialise the misses)
+            // C = alpha * 2^(e_r + e_c) * sum + beta * C.  The warp's 64 column
+            // scales alpha 2^(e_c) (NaN for a column holding Inf/NaN) go through
+            // shared memory once per unit; 2^(e_r) 2^(e_c) is exact, so one
+            // product per element replaces the two scalings.
+            double* cs = colscale + (warp - 2) * 64;
+            const int32_t* ecol = p.rexp_b + static_cast<int64_t>(pr.b_tile) * p.rexp_stride_b;
+            const int c0 = n0 + ch * 64;
+#pragma unroll
+            for (int q = lane; q < 64; q += 32) {
+                const int e = c0 + q < p.N ? __ldg(ecol + c0 + q) : 0;
+                cs[q] = e == ROWEXP_NONFINITE ? __longlong_as_double(0x7ff8000000000000ll) : p.alpha * pow2(e);
+            }
+            __syncwarp();
             const int row = m0 + r;
             if (row < p.M) {
                 const int er = p.rexp_a[static_cast<int64_t>(pr.a_tile) * p.rexp_stride_a + row];
-                const double sr = pow2(er == ROWEXP_NONFINITE ? 0 : er);
-                double* C = static_cast<double*>(pr.c);
-                const int32_t* ecol = p.rexp_b + static_cast<int64_t>(pr.b_tile) * p.rexp_stride_b;
-#pragma unroll
-                for (int jb = 0; jb < 64; jb += 8) {
-                    double cv[8];
-                    int ec[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int col = n0 + ch * 64 + jb + u;
-                        const bool ok = col < p.N && !(pr.lower_only && row < col);
-                        ec[u] = ok ? __ldg(ecol + col) : 0;
-                        cv[u] = (ok && p.beta != 0.0) ? C[static_cast<int64_t>(col) * p.ldc + row] : 0.0;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int col = n0 + ch * 64 + jb + u;
-                        if (col >= p.N || (pr.lower_only && row < col)) continue;
-                        double v;
-                        if (er == ROWEXP_NONFINITE || ec[u] == ROWEXP_NONFINITE)
-                            v = __longlong_as_double(0x7ff8000000000000ll);
-                        else  // exact power-of-two scalings (FP16 rows: |e| <= 40)
-                            v = sum[jb + u] * sr * pow2(ec[u]);
-                        double out = p.alpha * v;
-                        if (p.beta != 0.0) out = fma(p.beta, cv[u], out);
-                        C[static_cast<int64_t>(col) * p.ldc + row] = out;
-                    }
-                }
+                const double sr = er == ROWEXP_NONFINITE ? __longlong_as_double(0x7ff8000000000000ll) : pow2(er);
+                // columns [c0, c0 + ncol) of this row (lower-only units: col <= row)
+                int ncol = min(64, p.N - c0);
+                if (pr.lower_only) ncol = min(ncol, row - c0 + 1);
+                if (p.c_f32)
+                    store_row(static_cast<float*>(pr.c) + static_cast<int64_t>(c0) * p.ldc + row, p.ldc, sum, cs, sr,
+                              p.beta, ncol);
+                else
+                    store_row(static_cast<double*>(pr.c) + static_cast<int64_t>(c0) * p.ldc + row, p.ldc, sum, cs, sr,
+                              p.beta, ncol);
             }
+            __syncwarp();  // cs is rewritten for the next unit
         }
     }
     __syncthreads();
@@ -476,12 +508,9 @@ __device__ __forceinline__ int cluster_block_need(int need) {
 // 16-byte store per plane.  The low byte of the biased value's bits is q
 // itself (two's complement), so packing is three byte permutes per four
 // digits; planes past nd are neither computed nor stored.
-__device__ __forceinline__ void oz_digits16(const uint16_t (&h)[16], float scale, int nd, int8_t* out,
-                                            int64_t stride) {
+// Y: the values already scaled by 2^(41 - e_r).
+__device__ __forceinline__ void oz_digits16_y(float (&Y)[16], int nd, int8_t* out, int64_t stride) {
     constexpr float MAGIC = 12582912.0f;  // 1.5 * 2^23
-    float Y[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) Y[j] = __half2float(__ushort_as_half(h[j])) * scale;
 #pragma unroll
     for (int d = 0; d < S; ++d) {
         if (d >= nd) break;
@@ -505,6 +534,14 @@ __device__ __forceinline__ void oz_digits16(const uint16_t (&h)[16], float scale
         v.w = __byte_perm(__byte_perm(b[12], b[13], 0x0040), __byte_perm(b[14], b[15], 0x0040), 0x5410);
         *reinterpret_cast<uint4*>(out + d * stride) = v;
     }
+}
+
+__device__ __forceinline__ void oz_digits16(const uint16_t (&h)[16], float scale, int nd, int8_t* out,
+                                            int64_t stride) {
+    float Y[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) Y[j] = __half2float(__ushort_as_half(h[j])) * scale;
+    oz_digits16_y(Y, nd, out, stride);
 }
 
 // One CTA per 32-row stripe of one matrix: (1) row exponent e_r with
@@ -760,6 +797,91 @@ __global__ void __cluster_dims__(OZ_CLUSTER, 1, 1) __launch_bounds__(256)
         oz_digits16(hv, scale, bneed, outr + c0, it.slice_stride);
     }
 }
+
+// FP32 operands (FP32 destination tiles fed by FP32 panel tiles).  The same
+// digits: Y = x 2^(41 - e_r) is exact (a power-of-two scaling, applied in two
+// halves so the FP32 scale factors stay normal) and every remainder keeps
+// Y's <= 24 significant bits, so the digits are exact down to 2^(e_r - 41).
+// A row whose values reach below that (FP32 rows span up to 2^277) has its
+// sixth digit rounded: the product error is then at most 2^-42 |row max| per
+// term, far below the FP32 rounding of the result.  Column-major, no
+// transpose (the tile scheduler's panel tiles).
+__global__ void __cluster_dims__(OZ_CLUSTER, 1, 1) __launch_bounds__(256)
+    oz_slice_f32_kernel(const OzSliceItem* items) {
+    cluster_arrive_relaxed();
+    const OzSliceItem it = items[blockIdx.y];
+    const int64_t r0 = static_cast<int64_t>(blockIdx.x) * 32;
+    if (r0 >= it.rows) {
+        cluster_block_need(0);
+        return;
+    }
+    const uint32_t* x = static_cast<const uint32_t*>(it.x);
+    __shared__ float sx[32][128 + 1];
+    __shared__ uint32_t smax[8][33], smin[8][33];
+    __shared__ int sexp[32];
+    // (1) per row: largest magnitude and the smallest exponent field of a nonzero
+    {
+        const int lr = threadIdx.x % 32, cs = threadIdx.x / 32;
+        const int64_t r = r0 + lr;
+        uint32_t mx = 0, mn = 255;
+        if (r < it.rows)
+            for (int64_t c = cs; c < it.cols; c += 8) {
+                const uint32_t m = x[c * it.ld + r] & 0x7fffffffu;
+                mx = max(mx, m);
+                if (m) mn = min(mn, max(m >> 23, 1u));
+            }
+        smax[cs][lr] = mx;
+        smin[cs][lr] = mn;
+    }
+    __syncthreads();
+    int need_stripe = 0;
+    if (threadIdx.x < 32) {
+        uint32_t m = 0, mn = 255;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            m = max(m, smax[q][threadIdx.x]);
+            mn = min(mn, smin[q][threadIdx.x]);
+        }
+        int e = 0, need = 0;
+        if (m >= 0x7f800000u) {
+            e = ROWEXP_NONFINITE;
+        } else if (m != 0) {
+            frexpf(__uint_as_float(m), &e);
+            const int lsb = static_cast<int>(mn) - 150;  // ulp of the smallest nonzero
+            need = 1 + (max(0, e - 6 - lsb) + 6) / 7;
+        }
+        sexp[threadIdx.x] = e;
+        if (r0 + threadIdx.x < it.rows) it.rexp[r0 + threadIdx.x] = e;
+        for (int o = 16; o; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
+        need_stripe = need;
+    }
+    __syncthreads();
+    const int bn = cluster_block_need(need_stripe);
+    const int bneed = it.ndig ? bn : S;
+    if (it.ndig && threadIdx.x == 0 && ptx::cluster_ctarank() == 0) it.ndig[r0 / OZ_BLOCK] = bneed;
+    // (2) digits, 32 x 128 blocks staged through shared memory
+    const int lr = threadIdx.x / 8, cg = (threadIdx.x % 8) * 16;
+    const int64_t gr = r0 + lr;
+    const int er = sexp[lr];
+    const bool zero = er == ROWEXP_NONFINITE;
+    const int sh = zero ? 0 : 41 - er, sh1 = sh / 2, sh2 = sh - sh / 2;
+    const float s1 = zero ? 0.0f : __int_as_float((127 + sh1) << 23), s2 = __int_as_float((127 + sh2) << 23);
+    for (int64_t c0 = 0; c0 < it.kpad; c0 += 128) {
+        for (int e = threadIdx.x; e < 32 * 128; e += 256) {
+            const int a = e % 32, b = e / 32;
+            const int64_t rr = r0 + a, cc = c0 + b;
+            sx[a][b] = (rr < it.rows && cc < it.cols) ? __uint_as_float(x[cc * it.ld + rr]) : 0.0f;
+        }
+        __syncthreads();
+        if (gr < it.rows && c0 + cg < it.kpad) {
+            float Y[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) Y[j] = (sx[lr][cg + j] * s1) * s2;
+            oz_digits16_y(Y, bneed, static_cast<int8_t*>(it.out) + gr * it.kpad + c0 + cg, it.slice_stride);
+        }
+        __syncthreads();
+    }
+}
 }  // namespace oz
 
 void launch_oz_slices(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_t count, int64_t max_rows,
@@ -781,6 +903,16 @@ void launch_oz_slices(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_
     } else {
         oz::oz_slice_kernel<<<grid, 256, 0, s>>>(items);
     }
+    count_launch(ctx);
+    MP_CUDA(cudaGetLastError());
+}
+
+void launch_oz_slices_f32(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_t count, int64_t max_rows) {
+    if (count == 0) return;
+    ProfScope ps(ctx, MP_PROF_CAST, s, 0.0);
+    const dim3 grid(static_cast<unsigned>((max_rows + oz::OZ_BLOCK - 1) / oz::OZ_BLOCK * oz::OZ_CLUSTER),
+                    static_cast<unsigned>(count));
+    oz::oz_slice_f32_kernel<<<grid, 256, 0, s>>>(items);
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());
 }
@@ -815,6 +947,7 @@ void launch_oz_gemm(Ctx* ctx, cudaStream_t s, const OzGemm& g) {
     p.ndig_b = g.ndig_b;
     p.ndig_stride_a = static_cast<int32_t>(g.ndig_stride_a);
     p.ndig_stride_b = static_cast<int32_t>(g.ndig_stride_b);
+    p.c_f32 = g.c_single ? 1 : 0;
     p.stats = ctx->prof.enabled ? ctx->prof.dev_stats : nullptr;
     const int64_t jl = std::min(p.mblocks, p.nblocks);
     const int64_t total = static_cast<int64_t>(p.nlower) * (jl * p.mblocks - jl * (jl - 1) / 2) +

@@ -52,6 +52,7 @@ struct OzGemm {
     int64_t ldc = 0;
     double alpha = 1.0, beta = 0.0;
     bool lower_only = false;
+    bool c_single = false;  // C is FP32 (else FP64)
     const OzProblem* problems = nullptr;  // device array (grouped) or nullptr
     int64_t count = 0;
     int64_t n_lower = 0;  // grouped: the first n_lower problems are lower_only (the rest are not)
@@ -66,6 +67,9 @@ struct OzGemm {
 
 void launch_oz_slices(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_t count, int64_t max_rows,
                       int64_t max_cols);
+// FP32 operands (column-major, no transpose): the same digits, exact down to
+// 2^(e_r - 41) of each row (OzSliceItem::x points to floats).
+void launch_oz_slices_f32(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_t count, int64_t max_rows);
 void launch_oz_gemm(Ctx* ctx, cudaStream_t s, const OzGemm& g);
 
 }  // namespace mpcr

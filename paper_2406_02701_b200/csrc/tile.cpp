@@ -170,8 +170,9 @@ void append(std::vector<char>& buf, const std::vector<V>& v, size_t& off) {
 // panel); tcf / tcf16s hold the tiles that take both panels in one pass
 // (two K segments, one read-modify-write of C).
 struct UpLists {
-    size_t tc = 0, tc16s = 0, simt16 = 0, oz = 0, dm[3][3][2] = {}, tcf = 0, tcf16s = 0;
-    int64_t n_tc = 0, n_tc16s = 0, n_simt16 = 0, n_oz = 0, n_oz_lower = 0, n_dm[3][3][2] = {}, n_tcf = 0, n_tcf16s = 0;
+    size_t tc = 0, tc16s = 0, simt16 = 0, oz = 0, oz32 = 0, dm[3][3][2] = {}, tcf = 0, tcf16s = 0;
+    int64_t n_tc = 0, n_tc16s = 0, n_simt16 = 0, n_oz = 0, n_oz_lower = 0, n_oz32 = 0, n_oz32_lower = 0,
+            n_dm[3][3][2] = {}, n_tcf = 0, n_tcf16s = 0;
 };
 
 struct StepLists {
@@ -190,6 +191,8 @@ struct StepLists {
     int64_t n_cv[3][3][3] = {};
     size_t digits[3] = {0, 0, 0};  // INT8 digit slicing of FP16 panel tiles (same split)
     int64_t n_digits[3] = {0, 0, 0};
+    size_t digits32[3] = {0, 0, 0};  // ... and of FP32 panel tiles
+    int64_t n_digits32[3] = {0, 0, 0};
     // [0: tile column k+1 below the diagonal, 1: the rest, 2: tile (k+1, k+1),
     //  3: tile column k+2 of a paired step][source panel]
     UpLists up[4][2];
@@ -278,6 +281,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         std::vector<TcProblem> tc, tc16s, tcf, tcf16s;
         std::vector<TileProblem> simt16;
         std::vector<OzProblem> oz;           // FP64 tiles fed by FP16 panels: INT8 digit products
+        std::vector<OzProblem> oz32;         // FP32 tiles fed by FP32 (or FP32 + FP16) panels: the same
         std::vector<TileProblem> dm[3][3][2];  // DMMA, native panel precisions
     };
     // FP32 tiles whose two panel tiles are both FP16: the FP16 tensor-core
@@ -303,6 +307,23 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
     auto ozaki64 = [&](int64_t i, int64_t j, int64_t k) {
         return oz_ok && t.p(i, k) == MP_HALF && t.p(j, k) == MP_HALF;
     };
+    // FP32 tiles fed by FP32 panel tiles (or one FP32 and one FP16): INT8
+    // digits of the FP32 / FP16 panel tiles, FP64 combination, one rounding to
+    // FP32 -- the tensor cores instead of DMMA (MPCR_OZAKI32=0: DMMA).  Digits
+    // of an FP32 row are exact down to 2^-41 of the row's largest entry.
+    static const bool oz32_env = [] {
+        const char* e = getenv("MPCR_OZAKI32");
+        return !(e && e[0] == '0');
+    }();
+    auto ozaki32 = [&](int64_t i, int64_t j, int64_t k) {
+        return oz_ok && oz32_env && !(t.p(i, k) == MP_HALF && t.p(j, k) == MP_HALF) && t.p(i, k) != MP_DOUBLE &&
+               t.p(j, k) != MP_DOUBLE;
+    };
+    // the update of tile (i, j) by panel k reads INT8 digits of the panel tiles
+    auto uses_digits = [&](int64_t i, int64_t j, int64_t k) {
+        const mp_precision q = t.p(i, j);
+        return (q == MP_DOUBLE && ozaki64(i, j, k)) || (q == MP_SINGLE && ozaki32(i, j, k));
+    };
     const int64_t dig_tile = OZ_SLICES * tt;  // bytes of one tile's digit planes
     auto dig = [&](int64_t i, int64_t k) -> int8_t* {
         return static_cast<int8_t*>(t.digits) + ((k % PANEL_GENS) * NT + i) * dig_tile;
@@ -314,7 +335,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         std::vector<TcProblem> trsm_tc[2];
         std::vector<TileProblem> trsm_p[2][3];
         std::vector<CopyItem> wb[3], cv[3][3][3];
-        std::vector<OzSliceItem> digits[3];
+        std::vector<OzSliceItem> digits[3], digits32[3];
         UpAcc up[4][2];
     };
     // Head/tail split of the panel TRSM (single GPU with lookahead): the head
@@ -362,10 +383,10 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         const mp_precision q = t.p(i, k);
         bool need[2][3] = {{false, false, false}, {false, false, false}};
         for (int64_t j = k + 1; j <= i; ++j)  // A operand of (owned) row-i updates
-            if (t.has(i, j) && !(t.p(i, j) == MP_DOUBLE && ozaki64(i, j, k)))
+            if (t.has(i, j) && !uses_digits(i, j, k))
                 need[la_col(k, j) ? 0 : 1][opnd_prec(t.p(i, j), i, k)] = true;
         for (int64_t m = i; m < NT; ++m)  // B operand of (owned) column-i updates
-            if (t.has(m, i) && !(t.p(m, i) == MP_DOUBLE && ozaki64(m, i, k)))
+            if (t.has(m, i) && !uses_digits(m, i, k))
                 need[la_col(k, i) ? 0 : 1][opnd_prec(t.p(m, i), i, k)] = true;
         const int h0 = (tsplit && i == k + 1) ? 2 : 0;  // the head tile's part-0 work
         for (int r = 0; r < 3; ++r) {
@@ -375,13 +396,15 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         }
         bool need_dig[2] = {false, false};
         for (int64_t j = k + 1; j <= i; ++j)
-            if (t.has(i, j) && t.p(i, j) == MP_DOUBLE && ozaki64(i, j, k)) need_dig[la_col(k, j) ? 0 : 1] = true;
+            if (t.has(i, j) && uses_digits(i, j, k)) need_dig[la_col(k, j) ? 0 : 1] = true;
         for (int64_t m = i; m < NT; ++m)
-            if (t.has(m, i) && t.p(m, i) == MP_DOUBLE && ozaki64(m, i, k)) need_dig[la_col(k, i) ? 0 : 1] = true;
+            if (t.has(m, i) && uses_digits(m, i, k)) need_dig[la_col(k, i) ? 0 : 1] = true;
         const int hd = need_dig[0] ? h0 : need_dig[1] ? 1 : -1;
-        if (hd >= 0)
-            A.digits[hd].push_back(
-                OzSliceItem{pan(MP_HALF, i, k), dig(i, k), rex(i, k), ndg(i, k), nb, nb, nb, nb, tt, 0, 0});
+        if (hd >= 0) {  // from the panel tile's own precision (FP16 or FP32)
+            const bool f32 = q != MP_HALF;
+            (f32 ? A.digits32 : A.digits)[hd].push_back(OzSliceItem{pan(f32 ? MP_SINGLE : MP_HALF, i, k), dig(i, k),
+                                                                    rex(i, k), ndg(i, k), nb, nb, nb, nb, tt, 0, 0});
+        }
     };
     std::vector<char> have(NT * NT, 0);  // panel tile (i, k) present on this rank (conversions made)
     struct TcCand {
@@ -440,6 +463,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                     tc_cand.push_back({ks, part, 1, src, tp});
                 else if (q == MP_DOUBLE && ozaki64(i, j, k))
                     U.oz.push_back(OzProblem{static_cast<int32_t>(i), static_cast<int32_t>(j), t.ptr(i, j), lo, 0});
+                else if (q == MP_SINGLE && ozaki32(i, j, k))
+                    U.oz32.push_back(OzProblem{static_cast<int32_t>(i), static_cast<int32_t>(j), t.ptr(i, j), lo, 0});
                 else {
                     const mp_precision pa = opnd_prec(q, i, k), pb = opnd_prec(q, j, k);
                     U.dm[pa][pb][q == MP_DOUBLE ? 1 : 0].push_back(
@@ -520,6 +545,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         for (int h = 0; h < 3; ++h) {
             append(buf, A.digits[h], L.digits[h]);
             L.n_digits[h] = A.digits[h].size();
+            append(buf, A.digits32[h], L.digits32[h]);
+            L.n_digits32[h] = A.digits32[h].size();
         }
         for (int w = 0; w < 4; ++w)
             for (int sc = 0; sc < 2; ++sc) {
@@ -537,12 +564,14 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 D.n_simt16 = U.simt16.size();
                 // diagonal (lower-only) problems first: the kernel enumerates
                 // only their live units
-                std::vector<OzProblem> oz = U.oz;
-                const auto lower_end =
-                    std::stable_partition(oz.begin(), oz.end(), [](const OzProblem& o) { return o.lower_only != 0; });
-                D.n_oz_lower = lower_end - oz.begin();
-                append(buf, oz, D.oz);
-                D.n_oz = oz.size();
+                for (int w32 = 0; w32 < 2; ++w32) {
+                    std::vector<OzProblem> oz = w32 ? U.oz32 : U.oz;
+                    const auto lower_end = std::stable_partition(
+                        oz.begin(), oz.end(), [](const OzProblem& o) { return o.lower_only != 0; });
+                    (w32 ? D.n_oz32_lower : D.n_oz_lower) = lower_end - oz.begin();
+                    append(buf, oz, w32 ? D.oz32 : D.oz);
+                    (w32 ? D.n_oz32 : D.n_oz) = oz.size();
+                }
                 for (int a = 0; a < 3; ++a)
                     for (int b = 0; b < 3; ++b)
                         for (int c2 = 0; c2 < 2; ++c2) {
@@ -588,6 +617,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                     launch_batched_convert(c, st, (mp_precision)q, (mp_precision)r,
                                            reinterpret_cast<const CopyItem*>(dl + L.cv[h][q][r]),
                                            L.n_cv[h][q][r], tt);
+        if (L.n_digits32[h])
+            launch_oz_slices_f32(c, st, reinterpret_cast<const OzSliceItem*>(dl + L.digits32[h]), L.n_digits32[h], nb);
         if (L.n_digits[h]) {
             launch_oz_slices(c, st, reinterpret_cast<const OzSliceItem*>(dl + L.digits[h]), L.n_digits[h], nb, nb);
             static const bool dbg = getenv("MPCR_DEBUG_NDIG") != nullptr;  // diagnostics (eager runs only)
@@ -791,7 +822,11 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                               reinterpret_cast<const TileProblem*>(dl + U.simt16), U.n_simt16};
                 launch_grouped_gemm(c, st, g);
             }
-            if (U.n_oz) {  // FP64 tiles from FP16 panels: exact INT8 digit products
+            // FP64 tiles from FP16 panels (exact INT8 digit products) and FP32
+            // tiles from FP32 panels (digits exact to 2^-41 of each row's max)
+            for (int w32 = 0; w32 < 2; ++w32) {
+                const int64_t cnt = w32 ? U.n_oz32 : U.n_oz;
+                if (!cnt) continue;
                 OzGemm o;
                 o.A = o.B = dig(0, kp);
                 o.a_tiles = o.b_tiles = NT;
@@ -801,9 +836,10 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 o.ldc = nb;
                 o.alpha = -1.0;
                 o.beta = 1.0;
-                o.problems = reinterpret_cast<const OzProblem*>(dl + U.oz);
-                o.count = U.n_oz;
-                o.n_lower = U.n_oz_lower;
+                o.c_single = w32 == 1;
+                o.problems = reinterpret_cast<const OzProblem*>(dl + (w32 ? U.oz32 : U.oz));
+                o.count = cnt;
+                o.n_lower = w32 ? U.n_oz32_lower : U.n_oz_lower;
                 o.rexp_a = o.rexp_b = rex(0, kp);
                 o.ndig_a = o.ndig_b = ndg(0, kp);
                 o.ndig_stride_a = o.ndig_stride_b = NDB;

@@ -445,3 +445,59 @@ def test_paired_steps_match_unpaired_within_rounding(ctx, ref, tmp_path):
         err = np.linalg.norm(L - Lref) / np.linalg.norm(Lref)
         assert err <= 4 * err_dense, (v, err, err_dense)
     assert not np.array_equal(outs["1"], outs["0"])  # the pairing is really on by default
+
+
+_OZ32_PROBE = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2406_02701_b200 as mp
+ctx = mp.Context(0)
+n, nb = 4096, 512
+nt = n // nb
+i, j = np.indices((nt, nt))
+g = np.where(i == j, 2, np.where(abs(i - j) < 4, 1, 0))
+A = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+A.fill_matern(64, 0.5, 0.03, 1.0)
+ctx.prof_enable(True)
+mp.tile_chol(A)
+ctx.synchronize()
+print("int8_launches", ctx.prof_query(7)[1])
+np.save(sys.argv[2], A.to_numpy())
+"""
+
+
+def test_fp32_band_on_int8_digits_matches_oracle(ctx, ref, tmp_path):
+    """FP32 tiles fed by FP32 panel tiles (an FP32 band of width 4, SURVEY
+    §8d's example) run on INT8 digits by default (digits exact to 2^-41 of
+    each row's maximum, FP64 combination, one rounding to FP32) and on DMMA
+    with MPCR_OZAKI32=0.  Both factors satisfy the 4x oracle rule and differ
+    from each other by less than the oracle differs from FP64."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs, i8 = {}, {}
+    for v in ("1", "0"):
+        f = tmp_path / f"L{v}.npy"
+        e = dict(os.environ, MPCR_OZAKI32=v)
+        r = subprocess.run([sys.executable, "-c", _OZ32_PROBE, root, str(f)], env=e, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[v] = np.load(f)
+        i8[v] = int(r.stdout.split("int8_launches")[1].split()[0])
+    assert i8["1"] > i8["0"], i8  # the FP32 band really runs on the INT8 kernel by default
+    n, nb = 4096, 512
+    nt = n // nb
+    i, j = np.indices((nt, nt))
+    g = np.where(i == j, 2, np.where(abs(i - j) < 4, 1, 0))
+    cov = ref.grid_matern(64, n, 0.5, 0.03, 1.0, 2)
+    Lref = ref.tile_chol(n, nb, g, cov)
+    dense = np.linalg.cholesky(ref_round_grid(cov, g, nb))
+    err_dense = np.linalg.norm(Lref - dense) / np.linalg.norm(dense)
+    for v, L in outs.items():
+        err = np.linalg.norm(L - Lref) / np.linalg.norm(Lref)
+        assert err <= 4 * err_dense, (v, err, err_dense)
+    d = np.linalg.norm(outs["1"] - outs["0"]) / np.linalg.norm(outs["0"])
+    assert d <= err_dense, d
