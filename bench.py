@@ -470,9 +470,11 @@ def run_chol(args, world, rank, local):
         peak = pk["bf16_tflops_sustained"]
         traffic, tnote = None, None
         # the ncu capture of this n's bulk launch when one is committed
-        tpath = os.path.join(ROOT, "profiles", f"r01_ncu_traffic_n{n}.json")
-        if not os.path.exists(tpath):
-            tpath = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+        tpath = None
+        for cand in (f"r02_ncu_traffic_n{n}.json", f"r01_ncu_traffic_n{n}.json", "r01_ncu_traffic.json"):
+            tpath = os.path.join(ROOT, "profiles", cand)
+            if os.path.exists(tpath):
+                break
         try:
             with open(tpath) as f:
                 tj = json.load(f)

@@ -397,22 +397,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                 ptx::mbar_wait(&tfull[acc], acc_phase);
                 ptx::tc_fence_after();
                 const double w = __longlong_as_double(static_cast<long long>(1023 - 12 - 7 * (g - 2)) << 52);
+                // two TMEM loads per wait (the wait covers every load in flight)
 #pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    uint32_t v[16];
-                    ptx::tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(lg * 32) << 16) +
-                                                static_cast<uint32_t>(acc * BN + ch * 64 + c * 16),
-                                            v);
+                for (int c = 0; c < 4; c += 2) {
+                    uint32_t v[2][16];
+                    const uint32_t ta = tmem_base + (static_cast<uint32_t>(lg * 32) << 16) +
+                                        static_cast<uint32_t>(acc * BN + ch * 64 + c * 16);
+                    ptx::tmem_ld_32x32b_x16(ta, v[0]);
+                    ptx::tmem_ld_32x32b_x16(ta + 16, v[1]);
                     ptx::tmem_ld_wait();
                     // int32 -> double exactly on the FP64 pipe: the bits (0x43300000,
                     // v ^ 2^31) are 2^52 + 2^31 + v (the conversion pipe's I2F.F64
                     // runs at a quarter of the DFMA rate)
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const double x = __hiloint2double(0x43300000, static_cast<int>(v[j] ^ 0x80000000u)) -
-                                         4503601774854144.0;
-                        sum[c * 16 + j] = fma(w, x, sum[c * 16 + j]);
-                    }
+                    for (int h = 0; h < 2; ++h)
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const double x =
+                                __hiloint2double(0x43300000, static_cast<int>(v[h][j] ^ 0x80000000u)) -
+                                4503601774854144.0;
+                            sum[(c + h) * 16 + j] = fma(w, x, sum[(c + h) * 16 + j]);
+                        }
                 }
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&tempty[acc]);
@@ -805,7 +810,16 @@ __global__ void __cluster_dims__(OZ_CLUSTER, 1, 1) __launch_bounds__(256)
 // A row whose values reach below that (FP32 rows span up to 2^277) has its
 // sixth digit rounded: the product error is then at most 2^-42 |row max| per
 // term, far below the FP32 rounding of the result.  Column-major, no
-// transpose (the tile scheduler's panel tiles).
+// transpose (the tile scheduler's panel tiles), kpad <= OZ_STRIPE_K.
+// The stripe (32 rows x kpad) is staged whole into shared memory by 16-byte
+// cp.async copies (4 rows of one column each, all in flight at once): the
+// FP32 head tile of every step is sliced on the critical path.
+constexpr int OZ_F32_PITCH = 36;  // floats per staged column: 16-byte aligned, conflict-free row reads
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0)
+                 : "memory");
+}
 __global__ void __cluster_dims__(OZ_CLUSTER, 1, 1) __launch_bounds__(256)
     oz_slice_f32_kernel(const OzSliceItem* items) {
     cluster_arrive_relaxed();
@@ -815,23 +829,39 @@ __global__ void __cluster_dims__(OZ_CLUSTER, 1, 1) __launch_bounds__(256)
         cluster_block_need(0);
         return;
     }
-    const uint32_t* x = static_cast<const uint32_t*>(it.x);
-    __shared__ float sx[32][128 + 1];
+    const float* x = static_cast<const float*>(it.x);
+    extern __shared__ __align__(16) float sxc[];  // [kpad][OZ_F32_PITCH], column c's rows at c * PITCH
     __shared__ uint32_t smax[8][33], smin[8][33];
     __shared__ int sexp[32];
-    // (1) per row: largest magnitude and the smallest exponent field of a nonzero
+    const int kp = static_cast<int>(it.kpad), cols = static_cast<int>(it.cols);
+    const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+    const bool vec = r0 + 32 <= it.rows && (it.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    if (vec) {
+        for (int e = threadIdx.x; e < kp * 8; e += 256) {
+            const int c = e / 8, q = e % 8;
+            const bool ok = c < cols;
+            cp_async16_zfill(sxc + c * OZ_F32_PITCH + 4 * q, ok ? x + static_cast<int64_t>(c) * it.ld + r0 + 4 * q : x,
+                             ok);
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    } else {
+        for (int e = threadIdx.x; e < kp * 32; e += 256) {
+            const int c = e / 32, rr = e % 32;
+            sxc[c * OZ_F32_PITCH + rr] =
+                (c < cols && r0 + rr < it.rows) ? x[static_cast<int64_t>(c) * it.ld + r0 + rr] : 0.0f;
+        }
+    }
+    __syncthreads();
+    // (1) per row (lane): largest magnitude, smallest exponent field of a nonzero
     {
-        const int lr = threadIdx.x % 32, cs = threadIdx.x / 32;
-        const int64_t r = r0 + lr;
         uint32_t mx = 0, mn = 255;
-        if (r < it.rows)
-            for (int64_t c = cs; c < it.cols; c += 8) {
-                const uint32_t m = x[c * it.ld + r] & 0x7fffffffu;
-                mx = max(mx, m);
-                if (m) mn = min(mn, max(m >> 23, 1u));
-            }
-        smax[cs][lr] = mx;
-        smin[cs][lr] = mn;
+        for (int c = w; c < kp; c += 8) {
+            const uint32_t m = __float_as_uint(sxc[c * OZ_F32_PITCH + lane]) & 0x7fffffffu;
+            mx = max(mx, m);
+            if (m) mn = min(mn, max(m >> 23, 1u));
+        }
+        smax[w][lane] = mx;
+        smin[w][lane] = mn;
     }
     __syncthreads();
     int need_stripe = 0;
@@ -859,27 +889,19 @@ __global__ void __cluster_dims__(OZ_CLUSTER, 1, 1) __launch_bounds__(256)
     const int bn = cluster_block_need(need_stripe);
     const int bneed = it.ndig ? bn : S;
     if (it.ndig && threadIdx.x == 0 && ptx::cluster_ctarank() == 0) it.ndig[r0 / OZ_BLOCK] = bneed;
-    // (2) digits, 32 x 128 blocks staged through shared memory
-    const int lr = threadIdx.x / 8, cg = (threadIdx.x % 8) * 16;
-    const int64_t gr = r0 + lr;
-    const int er = sexp[lr];
+    // (2) digits: lane = row, warp w takes 16-column groups w, w + 8, ...
+    const int64_t gr = r0 + lane;
+    if (gr >= it.rows) return;
+    const int er = sexp[lane];
     const bool zero = er == ROWEXP_NONFINITE;
     const int sh = zero ? 0 : 41 - er, sh1 = sh / 2, sh2 = sh - sh / 2;
     const float s1 = zero ? 0.0f : __int_as_float((127 + sh1) << 23), s2 = __int_as_float((127 + sh2) << 23);
-    for (int64_t c0 = 0; c0 < it.kpad; c0 += 128) {
-        for (int e = threadIdx.x; e < 32 * 128; e += 256) {
-            const int a = e % 32, b = e / 32;
-            const int64_t rr = r0 + a, cc = c0 + b;
-            sx[a][b] = (rr < it.rows && cc < it.cols) ? __uint_as_float(x[cc * it.ld + rr]) : 0.0f;
-        }
-        __syncthreads();
-        if (gr < it.rows && c0 + cg < it.kpad) {
-            float Y[16];
+    int8_t* outr = static_cast<int8_t*>(it.out) + gr * it.kpad;
+    for (int c0 = 16 * w; c0 < kp; c0 += 128) {
+        float Y[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) Y[j] = (sx[lr][cg + j] * s1) * s2;
-            oz_digits16_y(Y, bneed, static_cast<int8_t*>(it.out) + gr * it.kpad + c0 + cg, it.slice_stride);
-        }
-        __syncthreads();
+        for (int j = 0; j < 16; ++j) Y[j] = (sxc[(c0 + j) * OZ_F32_PITCH + lane] * s1) * s2;
+        oz_digits16_y(Y, bneed, outr + c0, it.slice_stride);
     }
 }
 }  // namespace oz
@@ -907,12 +929,19 @@ void launch_oz_slices(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_
     MP_CUDA(cudaGetLastError());
 }
 
-void launch_oz_slices_f32(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_t count, int64_t max_rows) {
+void launch_oz_slices_f32(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_t count, int64_t max_rows,
+                          int64_t max_cols) {
     if (count == 0) return;
+    if (max_cols > oz::OZ_STRIPE_K) fail(MP_INVALID_PARAM, "FP32 digit slicer: K > 1024");
     ProfScope ps(ctx, MP_PROF_CAST, s, 0.0);
     const dim3 grid(static_cast<unsigned>((max_rows + oz::OZ_BLOCK - 1) / oz::OZ_BLOCK * oz::OZ_CLUSTER),
                     static_cast<unsigned>(count));
-    oz::oz_slice_f32_kernel<<<grid, 256, 0, s>>>(items);
+    // the tile scheduler slices nb x nb panel tiles (kpad = nb <= OZ_STRIPE_K)
+    const int smem = oz::OZ_STRIPE_K * oz::OZ_F32_PITCH * 4;
+    static unsigned long long cfg = 0;  // per-device bitmask
+    if (first_on_device(cfg))
+        MP_CUDA(cudaFuncSetAttribute(oz::oz_slice_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    oz::oz_slice_f32_kernel<<<grid, 256, smem, s>>>(items);
     count_launch(ctx);
     MP_CUDA(cudaGetLastError());
 }

@@ -67,9 +67,10 @@ struct OzGemm {
 
 void launch_oz_slices(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_t count, int64_t max_rows,
                       int64_t max_cols);
-// FP32 operands (column-major, no transpose): the same digits, exact down to
-// 2^(e_r - 41) of each row (OzSliceItem::x points to floats).
-void launch_oz_slices_f32(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_t count, int64_t max_rows);
+// FP32 operands (column-major, no transpose, K <= 1024): the same digits,
+// exact down to 2^(e_r - 41) of each row (OzSliceItem::x points to floats).
+void launch_oz_slices_f32(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_t count, int64_t max_rows,
+                          int64_t max_cols);
 void launch_oz_gemm(Ctx* ctx, cudaStream_t s, const OzGemm& g);
 
 }  // namespace mpcr

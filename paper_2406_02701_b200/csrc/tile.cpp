@@ -316,7 +316,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         return !(e && e[0] == '0');
     }();
     auto ozaki32 = [&](int64_t i, int64_t j, int64_t k) {
-        return oz_ok && oz32_env && !(t.p(i, k) == MP_HALF && t.p(j, k) == MP_HALF) && t.p(i, k) != MP_DOUBLE &&
+        return oz_ok && oz32_env && nb <= 1024 && !(t.p(i, k) == MP_HALF && t.p(j, k) == MP_HALF) &&
+               t.p(i, k) != MP_DOUBLE &&
                t.p(j, k) != MP_DOUBLE;
     };
     // the update of tile (i, j) by panel k reads INT8 digits of the panel tiles
@@ -618,7 +619,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                                            reinterpret_cast<const CopyItem*>(dl + L.cv[h][q][r]),
                                            L.n_cv[h][q][r], tt);
         if (L.n_digits32[h])
-            launch_oz_slices_f32(c, st, reinterpret_cast<const OzSliceItem*>(dl + L.digits32[h]), L.n_digits32[h], nb);
+            launch_oz_slices_f32(c, st, reinterpret_cast<const OzSliceItem*>(dl + L.digits32[h]), L.n_digits32[h], nb,
+                                 nb);
         if (L.n_digits[h]) {
             launch_oz_slices(c, st, reinterpret_cast<const OzSliceItem*>(dl + L.digits[h]), L.n_digits[h], nb, nb);
             static const bool dbg = getenv("MPCR_DEBUG_NDIG") != nullptr;  // diagnostics (eager runs only)
