@@ -147,7 +147,7 @@ void ensure_panels(mp_tile_s& t) {
     }
     if (!t.work) MP_CUDA(cudaMalloc(&t.work, WorkLayout(t.br).bytes()));
     if (t.events.empty()) {
-        t.events.resize(4 * t.tr + 4);
+        t.events.resize(5 * t.tr + 4);
         for (auto& e : t.events) MP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
 }
@@ -897,6 +897,18 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         cudaEvent_t* ev_next = t.events.data() + 2 * NT;  // NT
         cudaEvent_t ev_join = t.events[3 * NT + 1], ev_join2 = t.events[3 * NT + 2];
         cudaEvent_t* ev_head = t.events.data() + 3 * NT + 4;  // NT
+        cudaEvent_t* ev_cv = t.events.data() + 4 * NT + 4;    // NT
+        // MPCR_CONVERT_SIDE=1: the bulk's operand copies and digit planes of
+        // panel k on a side stream as soon as the panel exists, next to the
+        // bulk update of the previous step.  Off: measured neutral at
+        // n = 131072 (1155-1162 TF/s either way, tools/r02_gpu24.sh) -- the
+        // side kernels wait for SMs behind the persistent bulk GEMM.
+        static const bool cv_side_env = [] {
+            const char* e = getenv("MPCR_CONVERT_SIDE");
+            return e && e[0] == '1';
+        }();
+        const bool cv_side = la && cv_side_env;
+        cudaStream_t scv = cv_side ? c->aux[0] : s;
         // panel k: head on the critical-path stream, tail on the lookahead stream
         auto panel_phase = [&](int64_t k, cudaEvent_t before_trsm) {
             panel_head(k, sl, before_trsm);
@@ -936,7 +948,14 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             // the bulk update so a timing measures the critical chain alone
             static const bool chain_only = getenv("MPCR_CHAIN_ONLY") != nullptr;
             if (!chain_only) {
-                convert_panel(k, 1, s);
+                if (cv_side) {
+                    MP_CUDA(cudaStreamWaitEvent(scv, ev_panel[k], 0));
+                    convert_panel(k, 1, scv);
+                    MP_CUDA(cudaEventRecord(ev_cv[k], scv));
+                    MP_CUDA(cudaStreamWaitEvent(s, ev_cv[k], 0));
+                } else {
+                    convert_panel(k, 1, s);
+                }
                 update_phase(k, 1, s, bulk_tpc);
             }
             if (!wb_async || k + 1 >= NT) write_back(k, s);
