@@ -516,7 +516,12 @@ def run_chol(args, world, rank, local):
                    "covariance": f"Matern nu=0.5 range {args.range} sigma2 1 nugget {args.nugget}, "
                                  f"first {n} points of a {side}x{side} unit grid",
                    "fp32_method": "FP16 panels: tcgen05 kind::f16 (exact products, FP32 accumulate); "
-                                  "FP32 panels: DMMA (widened exactly, FP64 accumulate, one rounding)",
+                                  + ("FP32 panels: 7-bit digits of the FP16/FP32 panel rows (exact to 2^-41 of "
+                                     "the row max), tcgen05 kind::i8, FP64 combination, one rounding"
+                                     if os.environ.get("MPCR_OZAKI32", "1") != "0" else
+                                     "FP32 panels: DMMA (widened exactly, FP64 accumulate, one rounding)"),
+                   "steps": "paired (two panels per tensor-core tile pass)"
+                            if os.environ.get("MPCR_PAIR_STEPS", "1") != "0" else "one panel per pass",
                    "fp64_method": "FP16 panels: exact 7-bit digit slicing, tcgen05 kind::i8 (Ozaki); "
                                   "FP32/FP64 panels: DMMA",
                    "l2": "inputs 8+ GB >> 126 MB L2 (no flush needed)",
