@@ -84,9 +84,9 @@ struct Params {
 
 // Digit counts of a problem: pairs (dp, dq) with dp <= sa, dq <= sb; groups
 // g = sa + sb .. 2.
-__device__ __forceinline__ void digits_of(const Params& p, const OzProblem& pr, int m0, int n0, int& sa, int& sb) {
-    sa = p.ndig_a ? max(1, min(S, p.ndig_a[pr.a_tile * p.ndig_stride_a + m0 / BM])) : S;
-    sb = p.ndig_b ? max(1, min(S, p.ndig_b[pr.b_tile * p.ndig_stride_b + n0 / BN])) : S;
+__device__ __forceinline__ void digits_of(const Params& p, int at, int bt, int m0, int n0, int& sa, int& sb) {
+    sa = p.ndig_a ? max(1, min(S, p.ndig_a[at * p.ndig_stride_a + m0 / BM])) : S;
+    sb = p.ndig_b ? max(1, min(S, p.ndig_b[bt * p.ndig_stride_b + n0 / BN])) : S;
 }
 
 __device__ __forceinline__ void mma_i8_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -250,15 +250,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                 int m0, n0;
                 decode(t, pr, m0, n0);
                 if (skip_tile(pr, m0, n0)) continue;
+                const int np = pr.a_tile2 >= 0 ? 2 : 1;
+                for (int ps = 0; ps < np; ++ps) {
+                const int at = ps ? pr.a_tile2 : pr.a_tile, bt = ps ? pr.b_tile2 : pr.b_tile;
                 int sa, sb;
-                digits_of(p, pr, m0, n0, sa, sb);
+                digits_of(p, at, bt, m0, n0, sa, sb);
                 for (int g = sa + sb; g >= 2; g -= 2) {
                     const bool two = g - 1 >= 2;  // group g-1 rides along
                     const int lo = max(1, (two ? g - 1 : g) - sb), hi = min(sa, g - 1);
                     for (int dp = lo; dp <= hi; ++dp) {
                         const bool v1 = dp >= max(1, g - sb);                 // pair (dp, g - dp)
                         const bool v2 = two && dp <= min(sa, g - 2);          // pair (dp, g - 1 - dp)
-                        const int za = pr.a_tile * S + dp - 1;
+                        const int za = at * S + dp - 1;
                         for (int kb = 0; kb < p.kblocks; ++kb) {
                             ptx::mbar_wait(&empty[stage], phase ^ 1);
                             ptx::mbar_arrive_expect_tx(&full[stage],
@@ -266,10 +269,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                             ptx::tma_load_3d(sA + stage * A_STAGE, &p.map_a, &full[stage], kb * BK, m0, za);
                             if (v1)
                                 ptx::tma_load_3d(sB + (stage * 2) * B_STAGE, &p.map_b, &full[stage], kb * BK, n0,
-                                                 pr.b_tile * S + (g - dp) - 1);
+                                                 bt * S + (g - dp) - 1);
                             if (v2)
                                 ptx::tma_load_3d(sB + (stage * 2 + 1) * B_STAGE, &p.map_b, &full[stage], kb * BK,
-                                                 n0, pr.b_tile * S + (g - 1 - dp) - 1);
+                                                 n0, bt * S + (g - 1 - dp) - 1);
                             if (++stage == STAGES) {
                                 stage = 0;
                                 phase ^= 1;
@@ -277,6 +280,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                         }
                     }
                 }
+                }  // panels
             }
         }
     } else if (warp == 1) {
@@ -299,8 +303,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
             int m0, n0;
             decode(t, pr, m0, n0);
             if (skip_tile(pr, m0, n0)) continue;
+            const int np = pr.a_tile2 >= 0 ? 2 : 1;
+            for (int ps = 0; ps < np; ++ps) {
             int sa, sb;
-            digits_of(p, pr, m0, n0, sa, sb);
+            digits_of(p, ps ? pr.a_tile2 : pr.a_tile, ps ? pr.b_tile2 : pr.b_tile, m0, n0, sa, sb);
             if (p.stats && lane == 0) {
                 atomicAdd(p.stats, static_cast<unsigned long long>(sa * sb));
                 atomicAdd(p.stats + 1, 1ull);
@@ -360,6 +366,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                     acc_phase ^= 1;
                 }
             }
+            }  // panels
         }
     } else {
         // ===== epilogue: warps 2..9 =====
@@ -375,8 +382,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
             int m0, n0;
             decode(t, pr, m0, n0);
             if (skip_tile(pr, m0, n0)) continue;
-            int sa, sb;
-            digits_of(p, pr, m0, n0, sa, sb);
+            const int np = pr.a_tile2 >= 0 ? 2 : 1;
             // C of this unit is read only after the last digit group: pull its
             // lines into L2 now, while the MMAs run (one lane per 16 rows, the
             // 64 columns of this warp's half), so the final pass does not wait
@@ -390,9 +396,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(Cp + static_cast<int64_t>(col) * p.ldc * es));
                 }
             }
+            double* cs = colscale + (warp - 2) * 64;
+            const int c0 = n0 + ch * 64;
+            const int row = m0 + r;
             double sum[64];
 #pragma unroll
             for (int j = 0; j < 64; ++j) sum[j] = 0.0;
+            for (int ps = 0; ps < np; ++ps) {
+            int sa, sb;
+            digits_of(p, ps ? pr.a_tile2 : pr.a_tile, ps ? pr.b_tile2 : pr.b_tile, m0, n0, sa, sb);
             for (int g = sa + sb; g >= 2; --g) {
                 ptx::mbar_wait(&tfull[acc], acc_phase);
                 ptx::tc_fence_after();
@@ -426,22 +438,46 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                     acc_phase ^= 1;
                 }
             }
-            // C = alpha * 2^(e_r + e_c) * sum + beta * C.  The warp's 64 column
-            // scales alpha 2^(e_c) (NaN for a column holding Inf/NaN) go through
-            // shared memory once per unit; 2^(e_r) 2^(e_c) is exact, so one
-            // product per element replaces the two scalings.
-            double* cs = colscale + (warp - 2) * 64;
-            const int32_t* ecol = p.rexp_b + static_cast<int64_t>(pr.b_tile) * p.rexp_stride_b;
-            const int c0 = n0 + ch * 64;
+            if (ps + 1 < np) {
+                // the first panel's sums to the second panel's scale: times
+                // 2^(e_r - e_r2 + e_c - e_c2), exact (NaN if an exponent marks a
+                // non-finite row or column of the first panel)
+                const int32_t* ec1 = p.rexp_b + static_cast<int64_t>(pr.b_tile) * p.rexp_stride_b;
+                const int32_t* ec2 = p.rexp_b + static_cast<int64_t>(pr.b_tile2) * p.rexp_stride_b;
+#pragma unroll
+                for (int q = lane; q < 64; q += 32) {
+                    const int e1 = c0 + q < p.N ? __ldg(ec1 + c0 + q) : 0;
+                    const int e2 = c0 + q < p.N ? __ldg(ec2 + c0 + q) : 0;
+                    cs[q] = e1 == ROWEXP_NONFINITE ? __longlong_as_double(0x7ff8000000000000ll)
+                            : e2 == ROWEXP_NONFINITE ? 0.0 : pow2(e1 - e2);
+                }
+                __syncwarp();
+                if (row < p.M) {
+                    const int er1 = p.rexp_a[static_cast<int64_t>(pr.a_tile) * p.rexp_stride_a + row];
+                    const int er2 = p.rexp_a[static_cast<int64_t>(pr.a_tile2) * p.rexp_stride_a + row];
+                    const double rf = er1 == ROWEXP_NONFINITE ? __longlong_as_double(0x7ff8000000000000ll)
+                                      : er2 == ROWEXP_NONFINITE ? 0.0 : pow2(er1 - er2);
+#pragma unroll
+                    for (int j = 0; j < 64; ++j) sum[j] *= rf * cs[j];
+                }
+                __syncwarp();
+            }
+            }  // panels
+            // C = alpha * 2^(e_r + e_c) * sum + beta * C (the last panel's
+            // exponents).  The warp's 64 column scales alpha 2^(e_c) (NaN for a
+            // column holding Inf/NaN) go through shared memory once per unit;
+            // 2^(e_r) 2^(e_c) is exact, so one product per element replaces
+            // the two scalings.
+            const int32_t* ecol =
+                p.rexp_b + static_cast<int64_t>(np == 2 ? pr.b_tile2 : pr.b_tile) * p.rexp_stride_b;
 #pragma unroll
             for (int q = lane; q < 64; q += 32) {
                 const int e = c0 + q < p.N ? __ldg(ecol + c0 + q) : 0;
                 cs[q] = e == ROWEXP_NONFINITE ? __longlong_as_double(0x7ff8000000000000ll) : p.alpha * pow2(e);
             }
             __syncwarp();
-            const int row = m0 + r;
             if (row < p.M) {
-                const int er = p.rexp_a[static_cast<int64_t>(pr.a_tile) * p.rexp_stride_a + row];
+                const int er = p.rexp_a[static_cast<int64_t>(np == 2 ? pr.a_tile2 : pr.a_tile) * p.rexp_stride_a + row];
                 const double sr = er == ROWEXP_NONFINITE ? __longlong_as_double(0x7ff8000000000000ll) : pow2(er);
                 // columns [c0, c0 + ncol) of this row (lower-only units: col <= row)
                 int ncol = min(64, p.N - c0);
@@ -948,15 +984,14 @@ void launch_oz_slices_f32(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, in
 
 void launch_oz_gemm(Ctx* ctx, cudaStream_t s, const OzGemm& g) {
     using namespace oz;
-    Params p;
-    std::memset(&p, 0, sizeof(p));
+    Params p{};
     // [tiles * S][rows][K] int8 digits, rows kpad bytes apart
     tma_map_3d(&p.map_a, g.A, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.k, g.m, g.a_tiles * S, g.kpad,
                g.a_slice_stride, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
     tma_map_3d(&p.map_b, g.B, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, g.k, g.n, g.b_tiles * S, g.kpad,
                g.b_slice_stride, BK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
     p.problems = g.problems;
-    p.single = OzProblem{0, 0, g.C, g.lower_only ? 1 : 0};
+    p.single = OzProblem{0, 0, g.C, g.lower_only ? 1 : 0, -1, -1, 0};
     p.nprob = g.problems ? static_cast<int32_t>(g.count) : 1;
     p.nlower = g.problems ? static_cast<int32_t>(g.n_lower) : (g.lower_only ? 1 : 0);
     p.M = static_cast<int32_t>(g.m);
@@ -982,7 +1017,7 @@ void launch_oz_gemm(Ctx* ctx, cudaStream_t s, const OzGemm& g) {
     const int64_t total = static_cast<int64_t>(p.nlower) * (jl * p.mblocks - jl * (jl - 1) / 2) +
                           static_cast<int64_t>(p.nprob - p.nlower) * p.mblocks * p.nblocks;
     ProfScope ps(ctx, MP_PROF_GEMM_I8, s,
-                 2.0 * static_cast<double>(g.m) * g.n * g.k * p.nprob * (g.lower_only ? 0.5 : 1.0));
+                 2.0 * static_cast<double>(g.m) * g.n * g.k * (p.nprob + g.n_two) * (g.lower_only ? 0.5 : 1.0));
     static unsigned long long configured = 0;  // per-device bitmask
     if (first_on_device(configured)) {
         MP_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));

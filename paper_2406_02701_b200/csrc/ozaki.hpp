@@ -15,13 +15,17 @@ constexpr int OZ_SLICES = 6;  // 6 x 7-bit digits: exact for any FP16 row
 constexpr int64_t OZ_MAX_K = 65536;
 
 // One problem of a grouped launch: digit tiles of A and B (indices into the
-// slabs), the FP64 C tile, lower triangle only (SYRK).
+// slabs), the C tile, lower triangle only (SYRK).  A second pair of digit
+// tiles (a_tile2 >= 0) is a second panel accumulated into the same output
+// before C is read and written once: C += alpha (A B^T + A2 B2^T).
 struct OzProblem {
     int32_t a_tile;
     int32_t b_tile;
     void* c;
     int32_t lower_only;
-    int32_t pad;
+    int32_t a_tile2 = -1;
+    int32_t b_tile2 = -1;
+    int32_t pad = 0;
 };
 
 // Slice one FP16 matrix (rows x cols, element (r, c) at x[c * ld + r], or
@@ -56,6 +60,7 @@ struct OzGemm {
     const OzProblem* problems = nullptr;  // device array (grouped) or nullptr
     int64_t count = 0;
     int64_t n_lower = 0;  // grouped: the first n_lower problems are lower_only (the rest are not)
+    int64_t n_two = 0;    // grouped: problems with a second panel (profiling work count)
     const int32_t* rexp_a = nullptr;
     const int32_t* rexp_b = nullptr;
     const int32_t* ndig_a = nullptr;  // digits per 128-row block (<= OZ_SLICES), ndig_stride_* blocks per tile

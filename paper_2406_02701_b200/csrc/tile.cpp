@@ -171,8 +171,8 @@ void append(std::vector<char>& buf, const std::vector<V>& v, size_t& off) {
 // (two K segments, one read-modify-write of C).
 struct UpLists {
     size_t tc = 0, tc16s = 0, simt16 = 0, oz = 0, oz32 = 0, dm[3][3][2] = {}, tcf = 0, tcf16s = 0;
-    int64_t n_tc = 0, n_tc16s = 0, n_simt16 = 0, n_oz = 0, n_oz_lower = 0, n_oz32 = 0, n_oz32_lower = 0,
-            n_dm[3][3][2] = {}, n_tcf = 0, n_tcf16s = 0;
+    int64_t n_tc = 0, n_tc16s = 0, n_simt16 = 0, n_oz = 0, n_oz_lower = 0, n_oz_two = 0, n_oz32 = 0, n_oz32_lower = 0,
+            n_oz32_two = 0, n_dm[3][3][2] = {}, n_tcf = 0, n_tcf16s = 0;
 };
 
 struct StepLists {
@@ -414,6 +414,16 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         TcProblem p;
     };
     std::vector<TcCand> tc_cand;
+    // INT8-digit candidates (kind 0: FP64 tile, 1: FP32 tile); digit tiles are
+    // indexed over all panel generations (gen * NT + row)
+    struct OzCand {
+        int64_t ks;
+        int part, kind, src;
+        int64_t i, j;
+        OzProblem p;
+    };
+    std::vector<OzCand> oz_cand;
+    auto gtile = [&](int64_t i, int64_t k) { return static_cast<int32_t>((k % PANEL_GENS) * NT + i); };
     for (const DistAction& a : sched) {
         StepAcc& A = acc[a.k];
         StepLists& L = steps[a.k];
@@ -462,10 +472,9 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                     U.simt16.push_back(TileProblem{pan(MP_HALF, i, k), pan(MP_HALF, j, k), t.ptr(i, j), lo, 0});
                 else if (q == MP_SINGLE && half_into_single(i, j, k))
                     tc_cand.push_back({ks, part, 1, src, tp});
-                else if (q == MP_DOUBLE && ozaki64(i, j, k))
-                    U.oz.push_back(OzProblem{static_cast<int32_t>(i), static_cast<int32_t>(j), t.ptr(i, j), lo, 0});
-                else if (q == MP_SINGLE && ozaki32(i, j, k))
-                    U.oz32.push_back(OzProblem{static_cast<int32_t>(i), static_cast<int32_t>(j), t.ptr(i, j), lo, 0});
+                else if ((q == MP_DOUBLE && ozaki64(i, j, k)) || (q == MP_SINGLE && ozaki32(i, j, k)))
+                    oz_cand.push_back({ks, part, q == MP_SINGLE ? 1 : 0, src, i, j,
+                                       OzProblem{gtile(i, k), gtile(j, k), t.ptr(i, j), lo, -1, -1, 0}});
                 else {
                     const mp_precision pa = opnd_prec(q, i, k), pb = opnd_prec(q, j, k);
                     U.dm[pa][pb][q == MP_DOUBLE ? 1 : 0].push_back(
@@ -499,6 +508,34 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             }
             UpAcc& U = acc[x.ks].up[x.part][x.src];
             (x.kind == 0 ? U.tc : U.tc16s).push_back(x.p);
+        }
+    }
+    // INT8-digit tiles with both sources in one step take both panels in one
+    // pass (C read and written once): src 0's digits first, then src 1's
+    {
+        std::sort(oz_cand.begin(), oz_cand.end(), [](const OzCand& x, const OzCand& y) {
+            if (x.ks != y.ks) return x.ks < y.ks;
+            if (x.part != y.part) return x.part < y.part;
+            if (x.kind != y.kind) return x.kind < y.kind;
+            if (x.j != y.j) return x.j < y.j;
+            if (x.i != y.i) return x.i < y.i;
+            return x.src < y.src;
+        });
+        for (size_t q = 0; q < oz_cand.size(); ++q) {
+            const OzCand& x = oz_cand[q];
+            const bool both = q + 1 < oz_cand.size() && oz_cand[q + 1].ks == x.ks && oz_cand[q + 1].part == x.part &&
+                              oz_cand[q + 1].kind == x.kind && oz_cand[q + 1].i == x.i && oz_cand[q + 1].j == x.j;
+            if (both) {
+                OzProblem f = x.p;
+                f.a_tile2 = oz_cand[q + 1].p.a_tile;
+                f.b_tile2 = oz_cand[q + 1].p.b_tile;
+                UpAcc& U = acc[x.ks].up[x.part][1];
+                (x.kind ? U.oz32 : U.oz).push_back(f);
+                ++q;
+                continue;
+            }
+            UpAcc& U = acc[x.ks].up[x.part][x.src];
+            (x.kind ? U.oz32 : U.oz).push_back(x.p);
         }
     }
     // FP16 update tiles of a step in groups of G tile columns, rows within a
@@ -570,6 +607,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                     const auto lower_end = std::stable_partition(
                         oz.begin(), oz.end(), [](const OzProblem& o) { return o.lower_only != 0; });
                     (w32 ? D.n_oz32_lower : D.n_oz_lower) = lower_end - oz.begin();
+                    (w32 ? D.n_oz32_two : D.n_oz_two) =
+                        std::count_if(oz.begin(), oz.end(), [](const OzProblem& o) { return o.a_tile2 >= 0; });
                     append(buf, oz, w32 ? D.oz32 : D.oz);
                     (w32 ? D.n_oz32 : D.n_oz) = oz.size();
                 }
@@ -830,8 +869,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 const int64_t cnt = w32 ? U.n_oz32 : U.n_oz;
                 if (!cnt) continue;
                 OzGemm o;
-                o.A = o.B = dig(0, kp);
-                o.a_tiles = o.b_tiles = NT;
+                o.A = o.B = t.digits;  // every generation: problems carry gen * NT + row
+                o.a_tiles = o.b_tiles = PANEL_GENS * NT;
                 o.a_slice_stride = o.b_slice_stride = tt;
                 o.kpad = nb;
                 o.m = o.n = o.k = nb;
@@ -842,8 +881,9 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 o.problems = reinterpret_cast<const OzProblem*>(dl + (w32 ? U.oz32 : U.oz));
                 o.count = cnt;
                 o.n_lower = w32 ? U.n_oz32_lower : U.n_oz_lower;
-                o.rexp_a = o.rexp_b = rex(0, kp);
-                o.ndig_a = o.ndig_b = ndg(0, kp);
+                o.n_two = w32 ? U.n_oz32_two : U.n_oz_two;
+                o.rexp_a = o.rexp_b = t.rexp;
+                o.ndig_a = o.ndig_b = t.ndig;
                 o.ndig_stride_a = o.ndig_stride_b = NDB;
                 o.rexp_stride_a = o.rexp_stride_b = nb;
                 launch_oz_gemm(c, st, o);
