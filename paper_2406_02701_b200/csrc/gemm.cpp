@@ -170,6 +170,7 @@ void launch_grouped_gemm(Ctx* ctx, cudaStream_t s, const GroupedGemm& g) {
     if (g.pc == MP_DOUBLE) {  // FP64 output: DMMA, narrow operands widened on load
         DmmaArgs d{false, g.tb, g.m, g.n, g.k, g.alpha, g.beta, nullptr, g.lda,
                    nullptr, g.ldb, nullptr, g.ldc, false, g.problems, g.pab, g.exclusive};
+        d.k_lower = g.k_lower;
         ProfScope ps(ctx, MP_PROF_GEMM_F64, s, 2.0 * g.m * g.n * g.k * g.count);
         launch_dmma_gemm(ctx, s, d, g.count);
         return;

@@ -200,9 +200,11 @@ __global__ void __launch_bounds__(DCfg<BT>::NTHR, BT == 64 ? 2 : 1) dmma_gemm_ke
     const int64_t m0 = static_cast<int64_t>(S > 1 ? blockIdx.x / S : blockIdx.x) * BMd;
     const int64_t n0 = static_cast<int64_t>(blockIdx.y) * BNd;
     if (pr.lower_only && m0 + BMd - 1 < n0) return;  // the whole cluster leaves together
-    const int64_t kext = g.k_tri ? std::min<int64_t>(g.k, n0 + BNd) : g.k;
-    const int64_t kchunk = S > 1 ? ((kext + S - 1) / S + BKd - 1) / BKd * BKd : kext;
-    const int64_t kbeg = rank * kchunk, kend = std::min<int64_t>(kext, kbeg + kchunk);
+    int64_t kext = g.k_tri ? std::min<int64_t>(g.k, n0 + BNd) : g.k;
+    if (g.k_lower == 2) kext = std::min<int64_t>(kext, m0 + BMd);
+    const int64_t klo = g.k_lower == 1 ? std::min<int64_t>(kext, n0 / BKd * BKd) : 0;
+    const int64_t kchunk = S > 1 ? ((kext - klo + S - 1) / S + BKd - 1) / BKd * BKd : kext - klo;
+    const int64_t kbeg = klo + rank * kchunk, kend = std::min<int64_t>(kext, kbeg + kchunk);
     constexpr bool WA = std::is_same<TA, double>::value, WB = std::is_same<TB, double>::value;
     constexpr bool ANY_WIDE = WA || WB;
     const TA* __restrict__ A = static_cast<const TA*>(pr.A);

@@ -29,6 +29,11 @@ struct DmmaArgs {
     // op(B)[k][n] == 0 for k > n (B = L^T of a lower-triangular L, the TRSM
     // as X = A L^-T): each CTA stops its K loop at its last column
     bool k_tri = false;
+    // lower-triangular operand (TRTRI levels): 1 = op(B)[k][n] == 0 for k < n
+    // (each CTA starts its K loop at its first column), 2 = op(A)[m][k] == 0
+    // for k > m (each CTA stops at its last row).  The skipped products are
+    // exact zeros.
+    int k_lower = 0;
     // The launcher may split K over a cluster when a launch leaves SMs idle;
     // that changes the summation order with the launch's problem COUNT, so
     // the scheduler's update and tail-TRSM lists (whose counts differ between

@@ -207,6 +207,7 @@ struct GroupedGemm {
     int64_t slab_tiles = 0;
     // Critical-path launch: each CTA reserves its SM (no co-resident CTAs).
     bool exclusive = false;
+    int k_lower = 0;  // FP64: lower-triangular operand, see DmmaArgs::k_lower
 };
 void launch_grouped_gemm(Ctx* ctx, cudaStream_t s, const GroupedGemm& g);
 

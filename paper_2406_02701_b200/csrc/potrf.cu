@@ -707,10 +707,12 @@ void launch_trtri_plan(Ctx* ctx, cudaStream_t s, TrtriPlan* P, bool leaves_done)
             GroupedGemm g1{MP_DOUBLE, MP_DOUBLE, false, h, h, h, ldl, ldi, h, 1.0, 0.0,
                            P->dev + lv.off1, lv.cnt};
             g1.exclusive = true;  // TRTRI sits on the Cholesky critical path
+            g1.k_lower = 1;       // Ainv lower: column block n0 needs K >= n0
             launch_grouped_gemm(ctx, s, g1);
             GroupedGemm g2{MP_DOUBLE, MP_DOUBLE, false, h, h, h, ldi, h, ldi, -1.0, 0.0,
                            P->dev + lv.off2, lv.cnt};
             g2.exclusive = true;
+            g2.k_lower = 2;  // Cinv lower: row block m0 needs K < m0 + BM
             launch_grouped_gemm(ctx, s, g2);
         }
         for (const auto& rg : lv.rag) {
