@@ -740,10 +740,18 @@ __global__ void __cluster_dims__(OZ_CLUSTER, 1, 1) __launch_bounds__(256) oz_sli
 }
 
 // Tiles (K <= OZ_STRIPE_K): the whole 32-row stripe is staged in shared
-// memory by one round of 16-byte loads (all in flight at once), the row
-// exponents and digit counts come from the registers on the way, and the
-// digits are cut from shared memory -- one HBM read of the operand.
+// memory column by column by 16-byte cp.async copies (8 rows of one column
+// each, every copy of the stripe in flight at once), then the row exponents
+// and digit counts and the digits are cut from shared memory -- one HBM read
+// of the operand, no register round trip.  Lane = row in both passes, so the
+// column-major staging is read without bank conflicts.
 constexpr int OZ_STRIPE_K = 1024;
+constexpr int OZ_H_PITCH = 32;  // halves per staged column (64 bytes: 16-byte aligned, lane-per-row reads conflict-free)
+__device__ __forceinline__ void cp_async16_zfill_h(void* smem, const void* gmem, bool valid) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0)
+                 : "memory");
+}
 __global__ void __cluster_dims__(OZ_CLUSTER, 1, 1) __launch_bounds__(256)
     oz_slice_stripe_kernel(const OzSliceItem* items) {
     cluster_arrive_relaxed();
@@ -755,69 +763,63 @@ __global__ void __cluster_dims__(OZ_CLUSTER, 1, 1) __launch_bounds__(256)
     }
     const uint16_t* x = static_cast<const uint16_t*>(it.x);
     const bool vec = !it.trans && r0 + 32 <= it.rows && (it.ld % 8) == 0 &&
-                     (reinterpret_cast<uintptr_t>(x) & 15) == 0 && it.kpad <= OZ_STRIPE_K;
-    if (!vec) {
-        oz_slice_generic(it, r0);
-        return;
-    }
-    extern __shared__ __align__(16) uint16_t sxf[];  // [32][KS]
-    const int KS = static_cast<int>(it.kpad) + 8;
-    __shared__ uint32_t smax[2][32];
+                     (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+    extern __shared__ __align__(16) uint16_t sxh[];  // [kpad][OZ_H_PITCH]: column c's 32 rows at c * PITCH
+    __shared__ uint32_t smax[8][33], smin[8][33];
     __shared__ int sexp[32];
-    if (threadIdx.x < 32) {
-        smax[0][threadIdx.x] = 0;
-        smax[1][threadIdx.x] = 31;
-    }
-    const int rg = threadIdx.x % 4;  // rows rg*8 .. rg*8+7
-    uint32_t mx[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    uint32_t mn[8] = {31, 31, 31, 31, 31, 31, 31, 31};  // min exponent field of nonzeros
-    int need_stripe = 0;
-    const int cols = static_cast<int>(it.cols), kp = static_cast<int>(it.kpad);
-    for (int c0 = threadIdx.x / 4; c0 < kp; c0 += 64 * 4) {
-        uint4 v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {  // four independent loads in flight per thread
-            const int c = c0 + 64 * u;
-            v[u] = (c < cols) ? *reinterpret_cast<const uint4*>(x + static_cast<int64_t>(c) * it.ld + r0 + rg * 8)
-                              : make_uint4(0, 0, 0, 0);
+    const int kp = static_cast<int>(it.kpad), cols = static_cast<int>(it.cols);
+    const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+    if (vec) {
+        for (int e = threadIdx.x; e < kp * 4; e += 256) {
+            const int c = e / 4, q = e % 4;
+            const bool ok = c < cols;
+            cp_async16_zfill_h(sxh + c * OZ_H_PITCH + 8 * q,
+                               ok ? x + static_cast<int64_t>(c) * it.ld + r0 + 8 * q : x, ok);
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int c = c0 + 64 * u;
-            if (c >= kp) break;
-            const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const uint32_t lo = w[q] & 0xffffu, hi = w[q] >> 16;
-                const uint32_t ml = lo & 0x7fffu, mh = hi & 0x7fffu;
-                mx[2 * q] = max(mx[2 * q], ml);
-                mx[2 * q + 1] = max(mx[2 * q + 1], mh);
-                if (ml) mn[2 * q] = min(mn[2 * q], max(ml >> 10, 1u));
-                if (mh) mn[2 * q + 1] = min(mn[2 * q + 1], max(mh >> 10, 1u));
-                sxf[(rg * 8 + 2 * q) * KS + c] = static_cast<uint16_t>(lo);
-                sxf[(rg * 8 + 2 * q + 1) * KS + c] = static_cast<uint16_t>(hi);
-            }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    } else {  // ragged last stripe, transposed or unaligned operand
+        for (int e = threadIdx.x; e < kp * 32; e += 256) {
+            const int c = e / 32, rr = e % 32;
+            const int64_t gr = r0 + rr;
+            sxh[c * OZ_H_PITCH + rr] =
+                (c < cols && gr < it.rows) ? (it.trans ? x[gr * it.ld + c] : x[static_cast<int64_t>(c) * it.ld + gr])
+                                           : static_cast<uint16_t>(0);
         }
-    }
-    __syncthreads();  // smax initialised
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-        atomicMax(&smax[0][rg * 8 + j], mx[j]);
-        atomicMin(&smax[1][rg * 8 + j], mn[j]);
     }
     __syncthreads();
+    // (1) per row (lane): largest magnitude, smallest exponent field of a nonzero
+    {
+        uint32_t mx = 0, mn = 31;
+#pragma unroll 8
+        for (int c = w; c < kp; c += 8) {
+            const uint32_t m = sxh[c * OZ_H_PITCH + lane] & 0x7fffu;
+            mx = max(mx, m);
+            if (m) mn = min(mn, max(m >> 10, 1u));
+        }
+        smax[w][lane] = mx;
+        smin[w][lane] = mn;
+    }
+    __syncthreads();
+    int need_stripe = 0;
     if (threadIdx.x < 32) {
-        const uint32_t m = smax[0][threadIdx.x];
+        uint32_t m = 0, mn = 31;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            m = max(m, smax[q][threadIdx.x]);
+            mn = min(mn, smin[q][threadIdx.x]);
+        }
         int e = 0, need = 0;
         if (m >= 0x7c00u) {
             e = ROWEXP_NONFINITE;
         } else if (m != 0) {
             frexp(h2d(static_cast<uint16_t>(m)), &e);
-            const int lsb = static_cast<int>(smax[1][threadIdx.x]) - 25;
+            // lowest set bit of the row is >= 2^(minexp - 25); digits reach
+            // 2^(e - 6 - 7 (S - 1))
+            const int lsb = static_cast<int>(mn) - 25;
             need = 1 + (max(0, e - 6 - lsb) + 6) / 7;
         }
         sexp[threadIdx.x] = e;
-        it.rexp[r0 + threadIdx.x] = e;
+        if (r0 + threadIdx.x < it.rows) it.rexp[r0 + threadIdx.x] = e;
         for (int o = 16; o; o >>= 1) need = max(need, __shfl_xor_sync(0xffffffffu, need, o));
         need_stripe = need;
     }
@@ -826,15 +828,15 @@ __global__ void __cluster_dims__(OZ_CLUSTER, 1, 1) __launch_bounds__(256)
     const int bn = cluster_block_need(need_stripe);  // every CTA of the cluster takes part
     const int bneed = it.ndig ? bn : S;
     if (it.ndig && threadIdx.x == 0 && ptx::cluster_ctarank() == 0) it.ndig[r0 / OZ_BLOCK] = bneed;
-    const int lr = threadIdx.x / 8, cg = (threadIdx.x % 8) * 16;
-    const int er = sexp[lr];
+    // (2) digits: lane = row, warp w takes 16-column groups w, w + 8, ...
+    if (r0 + lane >= it.rows) return;
+    const int er = sexp[lane];
     const float scale = er == ROWEXP_NONFINITE ? 0.0f : __int_as_float((127 + 41 - er) << 23);
-    const uint16_t* row = sxf + lr * KS;
-    int8_t* outr = static_cast<int8_t*>(it.out) + (r0 + lr) * it.kpad;
-    for (int c0 = cg; c0 < kp; c0 += 128) {
-        alignas(16) uint16_t hv[16];
-        *reinterpret_cast<uint4*>(hv) = *reinterpret_cast<const uint4*>(row + c0);
-        *reinterpret_cast<uint4*>(hv + 8) = *reinterpret_cast<const uint4*>(row + c0 + 8);
+    int8_t* outr = static_cast<int8_t*>(it.out) + (r0 + lane) * it.kpad;
+    for (int c0 = 16 * w; c0 < kp; c0 += 128) {
+        uint16_t hv[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) hv[j] = sxh[(c0 + j) * OZ_H_PITCH + lane];
         oz_digits16(hv, scale, bneed, outr + c0, it.slice_stride);
     }
 }
@@ -951,11 +953,11 @@ void launch_oz_slices(Ctx* ctx, cudaStream_t s, const OzSliceItem* items, int64_
                     static_cast<unsigned>(count));
     if (max_cols <= oz::OZ_STRIPE_K) {
         const int kpad = static_cast<int>((max_cols + 15) / 16 * 16);
-        const int smem = 32 * (kpad + 8) * 2;
+        const int smem = kpad * oz::OZ_H_PITCH * 2;
         static unsigned long long cfg = 0;  // per-device bitmask
         if (first_on_device(cfg)) {
             MP_CUDA(cudaFuncSetAttribute(oz::oz_slice_stripe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         32 * (oz::OZ_STRIPE_K + 8) * 2));
+                                         oz::OZ_STRIPE_K * oz::OZ_H_PITCH * 2));
         }
         oz::oz_slice_stripe_kernel<<<grid, 256, smem, s>>>(items);
     } else {
