@@ -92,7 +92,7 @@ struct Ctx {
     // Work counters of dynamically scheduled persistent kernels: one pair
     // [next unit, CTAs finished] per launch, handed out round robin; the last
     // CTA of a launch resets its pair, so captured graphs replay unchanged.
-    static constexpr int SCHED_SLOTS = 1024;
+    static constexpr int SCHED_SLOTS = 8192;  // > the INT8-digit launches of any captured factorization
     unsigned int* sched_pool = nullptr;  // 2 * SCHED_SLOTS, zeroed at context creation
     int sched_next = 0;
     unsigned int* sched_slot() { return sched_pool + 2 * (sched_next++ % SCHED_SLOTS); }

@@ -52,10 +52,17 @@ constexpr int S = OZ_SLICES;  // digits per value
 constexpr int BM = 128, BN = 128, BK = 128, STAGES = 4;
 constexpr int A_STAGE = BM * BK, B_STAGE = BN * BK;  // 16 KB each
 // + barriers, unit ring, the epilogue warps' column scales
-constexpr int SMEM_BYTES = STAGES * (A_STAGE + 2 * B_STAGE) + 1024 + 256 + 8 * 64 * 8;
+// Epilogue: 12 warps, three per TMEM lane quarter, owning output columns
+// [0, 48), [48, 96), [96, 128) of the unit (the sums of a thread's row live
+// in registers: 48 doubles).
+constexpr int EPI_WARPS = 12;
+constexpr int CWMAX = 48;
+__host__ __device__ constexpr int epi_col0(int g) { return g * 48; }
+__host__ __device__ constexpr int epi_cols(int g) { return g < 2 ? 48 : 32; }
+constexpr int SMEM_BYTES = STAGES * (A_STAGE + 2 * B_STAGE) + 1024 + 256 + EPI_WARPS * CWMAX * 8;
 constexpr int NACC = 4;          // int32 accumulators in flight (MMA runs NACC groups ahead)
 constexpr int TMEM_COLS = 512;  // NACC x 128 columns
-constexpr int NTHREADS = 320;   // 10 warps
+constexpr int NTHREADS = 32 * (2 + EPI_WARPS);  // producer, MMA issuer, epilogue
 constexpr int UR = 4;           // unit ring: the producer runs up to UR units ahead
 constexpr int ROWEXP_NONFINITE = 0x7fffffff;
 
@@ -112,27 +119,32 @@ __device__ __forceinline__ double pow2(int e) {
 
 // One row's 64 (or ncol) outputs: C = sum * (2^e_r * alpha 2^e_c) + beta C,
 // one rounding into TC.  All loads of a chunk of 8 precede its stores.
-template <typename TC>
-__device__ __forceinline__ void store_row(TC* Cr, int64_t ldc, const double (&sum)[64], const double* cs, double sr,
-                                          double beta, int ncol) {
-    if (ncol == 64) {
+template <int CW, typename TC>
+__device__ __forceinline__ void store_row(TC* Cr, int64_t ldc, const double (&sum)[CWMAX], const double* cs,
+                                          double sr, double beta, int ncol) {
+    if (ncol == CW) {
+        // walking pointers keep one address live per chunk instead of eight
+        TC* cp = Cr;
 #pragma unroll
-        for (int jb = 0; jb < 64; jb += 8) {
+        for (int jb = 0; jb < CW; jb += 8) {
             double cv[8];
             if (beta != 0.0) {
+                const TC* q = cp;
 #pragma unroll
-                for (int u = 0; u < 8; ++u) cv[u] = static_cast<double>(Cr[(jb + u) * ldc]);
+                for (int u = 0; u < 8; ++u, q += ldc) cv[u] = static_cast<double>(*q);
             }
+            TC* q = cp;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < 8; ++u, q += ldc) {
                 double out = sum[jb + u] * (sr * cs[jb + u]);
                 if (beta != 0.0) out = fma(beta, cv[u], out);
-                Cr[(jb + u) * ldc] = static_cast<TC>(out);
+                *q = static_cast<TC>(out);
             }
+            cp = q;
         }
     } else {
 #pragma unroll
-        for (int j = 0; j < 64; ++j) {
+        for (int j = 0; j < CW; ++j) {
             if (j >= ncol) break;
             double out = sum[j] * (sr * cs[j]);
             if (beta != 0.0) out = fma(beta, static_cast<double>(Cr[j * ldc]), out);
@@ -160,7 +172,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
     uint64_t* uempty = ufull + UR;
     int32_t* uring = reinterpret_cast<int32_t*>(uempty + UR);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uring + UR);
-    double* colscale = reinterpret_cast<double*>(tmem_slot + 2);  // [8 epilogue warps][64]
+    double* colscale = reinterpret_cast<double*>(tmem_slot + 2);  // [EPI_WARPS][CWMAX]
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (warp == 0 && lane == 0) {
@@ -172,11 +184,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
         }
         for (int s = 0; s < NACC; ++s) {
             ptx::mbar_init(&tfull[s], 1);
-            ptx::mbar_init(&tempty[s], 256);
+            ptx::mbar_init(&tempty[s], 32 * EPI_WARPS);
         }
         for (int s = 0; s < UR; ++s) {
             ptx::mbar_init(&ufull[s], 1);
-            ptx::mbar_init(&uempty[s], 9);  // the MMA warp + 8 epilogue warps
+            ptx::mbar_init(&uempty[s], 1 + EPI_WARPS);  // the MMA warp + the epilogue warps
         }
         ptx::fence_barrier_init();
     }
@@ -369,9 +381,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
             }  // panels
         }
     } else {
-        // ===== epilogue: warps 2..9 =====
+        // ===== epilogue: warps 2 .. 2 + EPI_WARPS - 1 =====
         const int lg = warp & 3;            // TMEM lane group this warp may access
-        const int ch = (warp - 2) >> 2;     // column half: 0 -> cols 0..63, 1 -> 64..127
+        const int cgi = (warp - 2) >> 2;    // column group
+        const int cb = epi_col0(cgi), cw = epi_cols(cgi);
         const int r = lg * 32 + lane;       // tile row (TMEM lane)
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -390,18 +403,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
             if (p.beta != 0.0 && (lane & 15) == 0 && m0 + r < p.M) {
                 const int64_t es = p.c_f32 ? 4 : 8;
                 const char* Cp = static_cast<const char*>(pr.c) + (m0 + r) * es;
-                for (int jb = 0; jb < 64; ++jb) {
-                    const int col = n0 + ch * 64 + jb;
+                for (int jb = 0; jb < cw; ++jb) {
+                    const int col = n0 + cb + jb;
                     if (col < p.N)
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(Cp + static_cast<int64_t>(col) * p.ldc * es));
                 }
             }
-            double* cs = colscale + (warp - 2) * 64;
-            const int c0 = n0 + ch * 64;
+            double* cs = colscale + (warp - 2) * CWMAX;
+            const int c0 = n0 + cb;
             const int row = m0 + r;
-            double sum[64];
+            double sum[CWMAX];
 #pragma unroll
-            for (int j = 0; j < 64; ++j) sum[j] = 0.0;
+            for (int j = 0; j < CWMAX; ++j) sum[j] = 0.0;
             for (int ps = 0; ps < np; ++ps) {
             int sa, sb;
             digits_of(p, ps ? pr.a_tile2 : pr.a_tile, ps ? pr.b_tile2 : pr.b_tile, m0, n0, sa, sb);
@@ -409,27 +422,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                 ptx::mbar_wait(&tfull[acc], acc_phase);
                 ptx::tc_fence_after();
                 const double w = __longlong_as_double(static_cast<long long>(1023 - 12 - 7 * (g - 2)) << 52);
-                // two TMEM loads per wait (the wait covers every load in flight)
+                // 16-column TMEM loads, one wait each (the last group's third
+                // load is skipped: 32 columns)
 #pragma unroll
-                for (int c = 0; c < 4; c += 2) {
-                    uint32_t v[2][16];
-                    const uint32_t ta = tmem_base + (static_cast<uint32_t>(lg * 32) << 16) +
-                                        static_cast<uint32_t>(acc * BN + ch * 64 + c * 16);
-                    ptx::tmem_ld_32x32b_x16(ta, v[0]);
-                    ptx::tmem_ld_32x32b_x16(ta + 16, v[1]);
+                for (int c = 0; c < CWMAX / 16; ++c) {
+                    if (c * 16 >= cw) break;
+                    uint32_t v[16];
+                    ptx::tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(lg * 32) << 16) +
+                                                static_cast<uint32_t>(acc * BN + cb + c * 16),
+                                            v);
                     ptx::tmem_ld_wait();
                     // int32 -> double exactly on the FP64 pipe: the bits (0x43300000,
                     // v ^ 2^31) are 2^52 + 2^31 + v (the conversion pipe's I2F.F64
                     // runs at a quarter of the DFMA rate)
 #pragma unroll
-                    for (int h = 0; h < 2; ++h)
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const double x =
-                                __hiloint2double(0x43300000, static_cast<int>(v[h][j] ^ 0x80000000u)) -
-                                4503601774854144.0;
-                            sum[(c + h) * 16 + j] = fma(w, x, sum[(c + h) * 16 + j]);
-                        }
+                    for (int j = 0; j < 16; ++j) {
+                        const double x = __hiloint2double(0x43300000, static_cast<int>(v[j] ^ 0x80000000u)) -
+                                         4503601774854144.0;
+                        sum[c * 16 + j] = fma(w, x, sum[c * 16 + j]);
+                    }
                 }
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&tempty[acc]);
@@ -445,7 +456,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                 const int32_t* ec1 = p.rexp_b + static_cast<int64_t>(pr.b_tile) * p.rexp_stride_b;
                 const int32_t* ec2 = p.rexp_b + static_cast<int64_t>(pr.b_tile2) * p.rexp_stride_b;
 #pragma unroll
-                for (int q = lane; q < 64; q += 32) {
+                for (int q = lane; q < cw; q += 32) {
                     const int e1 = c0 + q < p.N ? __ldg(ec1 + c0 + q) : 0;
                     const int e2 = c0 + q < p.N ? __ldg(ec2 + c0 + q) : 0;
                     cs[q] = e1 == ROWEXP_NONFINITE ? __longlong_as_double(0x7ff8000000000000ll)
@@ -458,7 +469,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                     const double rf = er1 == ROWEXP_NONFINITE ? __longlong_as_double(0x7ff8000000000000ll)
                                       : er2 == ROWEXP_NONFINITE ? 0.0 : pow2(er1 - er2);
 #pragma unroll
-                    for (int j = 0; j < 64; ++j) sum[j] *= rf * cs[j];
+                    for (int j = 0; j < CWMAX; ++j)
+                        if (j < cw) sum[j] *= rf * cs[j];
                 }
                 __syncwarp();
             }
@@ -471,7 +483,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
             const int32_t* ecol =
                 p.rexp_b + static_cast<int64_t>(np == 2 ? pr.b_tile2 : pr.b_tile) * p.rexp_stride_b;
 #pragma unroll
-            for (int q = lane; q < 64; q += 32) {
+            for (int q = lane; q < cw; q += 32) {
                 const int e = c0 + q < p.N ? __ldg(ecol + c0 + q) : 0;
                 cs[q] = e == ROWEXP_NONFINITE ? __longlong_as_double(0x7ff8000000000000ll) : p.alpha * pow2(e);
             }
@@ -480,14 +492,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) oz_gemm_kernel(const __grid_const
                 const int er = p.rexp_a[static_cast<int64_t>(np == 2 ? pr.a_tile2 : pr.a_tile) * p.rexp_stride_a + row];
                 const double sr = er == ROWEXP_NONFINITE ? __longlong_as_double(0x7ff8000000000000ll) : pow2(er);
                 // columns [c0, c0 + ncol) of this row (lower-only units: col <= row)
-                int ncol = min(64, p.N - c0);
+                int ncol = min(cw, p.N - c0);
                 if (pr.lower_only) ncol = min(ncol, row - c0 + 1);
-                if (p.c_f32)
-                    store_row(static_cast<float*>(pr.c) + static_cast<int64_t>(c0) * p.ldc + row, p.ldc, sum, cs, sr,
-                              p.beta, ncol);
-                else
-                    store_row(static_cast<double*>(pr.c) + static_cast<int64_t>(c0) * p.ldc + row, p.ldc, sum, cs, sr,
-                              p.beta, ncol);
+                float* Cf = static_cast<float*>(pr.c) + static_cast<int64_t>(c0) * p.ldc + row;
+                double* Cd = static_cast<double*>(pr.c) + static_cast<int64_t>(c0) * p.ldc + row;
+                if (cw == 48) {
+                    if (p.c_f32) store_row<48>(Cf, p.ldc, sum, cs, sr, p.beta, ncol);
+                    else store_row<48>(Cd, p.ldc, sum, cs, sr, p.beta, ncol);
+                } else {
+                    if (p.c_f32) store_row<32>(Cf, p.ldc, sum, cs, sr, p.beta, ncol);
+                    else store_row<32>(Cd, p.ldc, sum, cs, sr, p.beta, ncol);
+                }
             }
             __syncwarp();  // cs is rewritten for the next unit
         }
