@@ -147,7 +147,7 @@ void ensure_panels(mp_tile_s& t) {
     }
     if (!t.work) MP_CUDA(cudaMalloc(&t.work, WorkLayout(t.br).bytes()));
     if (t.events.empty()) {
-        t.events.resize(5 * t.tr + 4);
+        t.events.resize(6 * t.tr + 4);
         for (auto& e : t.events) MP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
 }
@@ -193,9 +193,12 @@ struct StepLists {
     int64_t n_digits[3] = {0, 0, 0};
     size_t digits32[3] = {0, 0, 0};  // ... and of FP32 panel tiles
     int64_t n_digits32[3] = {0, 0, 0};
-    // [0: tile column k+1 below the diagonal, 1: the rest, 2: tile (k+1, k+1),
-    //  3: tile column k+2 of a paired step][source panel]
-    UpLists up[4][2];
+    // [0: tile column k+1 below tile k+2, 1: the rest (bulk), 2: tile (k+1, k+1),
+    //  3: tile column k+2 of a paired step below its diagonal, 4: tile (k+2, k+1)
+    //  (the next step's head tile), 5: tile (k+2, k+2) of a paired step]
+    //  [source panel].  Parts 4 and 5 run first on the lookahead stream: the
+    //  next head TRSM and diagonal SYRK wait for them, not for the columns.
+    UpLists up[6][2];
     bool diag_bcast = false;  // receive / send L_kk^-1 down this process column
     struct Bcast {
         int i, root, comm;
@@ -337,7 +340,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         std::vector<TileProblem> trsm_p[2][3];
         std::vector<CopyItem> wb[3], cv[3][3][3];
         std::vector<OzSliceItem> digits[3], digits32[3];
-        UpAcc up[4][2];
+        UpAcc up[6][2];
     };
     // Head/tail split of the panel TRSM (single GPU with lookahead): the head
     // tile runs on the critical-path stream, the rest of the column on the
@@ -461,7 +464,13 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                 const bool defer = pair_steps && (k % 2 == 0) && j >= k + 2;
                 const int64_t ks = defer ? k + 1 : k;
                 const int src = defer ? 0 : 1;
-                const int part = j == ks + 1 ? (i == j ? 2 : 0) : (pair_steps && ks % 2 == 1 && j == ks + 2) ? 3 : 1;
+                int part;  // see StepLists::up
+                if (j == ks + 1)
+                    part = i == j ? 2 : i == ks + 2 ? 4 : 0;
+                else if (pair_steps && ks % 2 == 1 && j == ks + 2)
+                    part = i == j ? 5 : 3;
+                else
+                    part = 1;
                 UpAcc& U = acc[ks].up[part][src];
                 const int32_t lo = (i == j) ? 1 : 0;
                 const TcProblem tp{static_cast<int32_t>(i), static_cast<int32_t>(j),
@@ -554,7 +563,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         return x.b_tile < y.b_tile;
     };
     for (int64_t k = 0; k < NT; ++k)
-        for (int w = 0; w < 4; ++w)
+        for (int w = 0; w < 6; ++w)
             for (int sc = 0; sc < 2; ++sc) {
                 std::stable_sort(acc[k].up[w][sc].tc.begin(), acc[k].up[w][sc].tc.end(), grouped);
                 std::stable_sort(acc[k].up[w][sc].tcf.begin(), acc[k].up[w][sc].tcf.end(), grouped);
@@ -586,7 +595,7 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
             append(buf, A.digits32[h], L.digits32[h]);
             L.n_digits32[h] = A.digits32[h].size();
         }
-        for (int w = 0; w < 4; ++w)
+        for (int w = 0; w < 6; ++w)
             for (int sc = 0; sc < 2; ++sc) {
                 const UpAcc& U = A.up[w][sc];
                 UpLists& D = L.up[w][sc];
@@ -899,8 +908,9 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                                    reinterpret_cast<const TileProblem*>(dl + U.dm[pa][pb][c2]), (mp_precision)pa};
                         d.pin_b = pb;
                         d.pout = c2 ? MP_DOUBLE : MP_SINGLE;
-                        d.exclusive = part == 2;  // the diagonal SYRK feeding the next POTRF
-                        d.allow_ksplit = part == 2;  // (k+1, k+1) alone on every rank
+                        // single critical-path tiles (alone in their launch on every rank)
+                        d.exclusive = part == 2 || part == 4 || part == 5;
+                        d.allow_ksplit = d.exclusive;
                         ProfScope ps(c, c2 ? MP_PROF_GEMM_F64 : MP_PROF_GEMM_F32, st,
                                      2.0 * static_cast<double>(nb) * nb * nb * cnt);
                         launch_dmma_gemm(c, st, d, cnt);
@@ -934,10 +944,10 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         cudaStream_t sl2 = la ? c->hi2 : s;
         cudaEvent_t* ev_panel = t.events.data();          // NT
         cudaEvent_t* ev_rest = t.events.data() + NT;      // NT
-        cudaEvent_t* ev_next = t.events.data() + 2 * NT;  // NT
         cudaEvent_t ev_join = t.events[3 * NT + 1], ev_join2 = t.events[3 * NT + 2];
         cudaEvent_t* ev_head = t.events.data() + 3 * NT + 4;  // NT
         cudaEvent_t* ev_cv = t.events.data() + 4 * NT + 4;    // NT
+        cudaEvent_t* ev_hu = t.events.data() + 5 * NT + 4;    // NT: parts 4 and 5 of step k done
         // MPCR_CONVERT_SIDE=1: the bulk's operand copies and digit planes of
         // panel k on a side stream as soon as the panel exists, next to the
         // bulk update of the previous step.  Off: measured neutral at
@@ -975,8 +985,8 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
         // the high-priority copy steals SMs from the bulk GEMM; tools/ab_wb_async.sh):
         // write-back of tile column k off the bulk stream: on sl2 right after the tail of
         // panel k+1 (ev_panel[k+1] is recorded before it, so bulk k+1 does not wait on it).
-        // The panel buffer (k & 1) is next written by panel k+2, whose head TRSM waits
-        // ev_next[k+1] (recorded on sl2 after this copy) and whose tail runs on sl2.
+        // The panel buffer of generation k is next written by panel k + PANEL_GENS, whose
+        // head TRSM waits an ev_hu recorded on sl2 after this copy and whose tail runs on sl2.
         static const bool wb_env = [] {
             const char* e = getenv("MPCR_WB_ASYNC");
             return e && e[0] == '1';
@@ -1008,12 +1018,16 @@ int64_t tile_chol_inplace(Ctx* c, mp_tile_s& t) {
                     MP_CUDA(cudaStreamWaitEvent(sl2, ev_panel[k], 0));
                     if (after_bulk) MP_CUDA(cudaStreamWaitEvent(sl2, ev_rest[k - 1], 0));
                 }
+                // the next head tile (and a paired step's tile (k+2, k+2)) first:
+                // the critical stream waits for these, not for the whole columns
+                update_phase(k, 4, sl2, 0);
+                update_phase(k, 5, sl2, 0);
+                if (la) MP_CUDA(cudaEventRecord(ev_hu[k], sl2));
                 update_phase(k, 0, sl2, 0);
                 update_phase(k, 3, sl2, 0);  // paired odd step: tile column k+2
-                if (la) MP_CUDA(cudaEventRecord(ev_next[k], sl2));
                 if (la && after_bulk) MP_CUDA(cudaStreamWaitEvent(sl, ev_rest[k - 1], 0));
                 update_phase(k, 2, sl, 0);
-                panel_phase(k + 1, la ? ev_next[k] : nullptr);
+                panel_phase(k + 1, la ? ev_hu[k] : nullptr);
                 if (wb_async) write_back(k, sl2);
             }
             if (dbg_host)
