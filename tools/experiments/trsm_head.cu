@@ -5,8 +5,12 @@
 // step at n = 131072, and the bench 1.5 % slower (tools/r02_gpu32.sh): each of
 // the 64 CTAs streams all of L through one cp.async chunk in flight, so the
 // solve is L2-latency bound (~190 us vs the inverse-based GEMM's ~100 us).
-// A version worth wiring in needs several chunks in flight per SM (less
-// shared memory for the X rows) or a split of the rows over a cluster.
+// Retried after the lookahead stream started updating the next head tile
+// first (so the TRTRI path no longer waits for whole columns) and with three
+// L chunks in flight: chain 1060 vs 1070 us per step, but the bench 1.8 %
+// slower (TRTRI on the lookahead stream competes with the bulk; the solve
+// itself ~300 us in situ; tools/r02_gpu37.sh).  A version worth wiring in
+// needs the rows of a tile split over a cluster sharing L by multicast.
 // Direct panel solve of the head tile: X = A L^-T with L the freshly factored
 // diagonal tile (lower, FP64) and the 64 x 64 inverses of its diagonal blocks
 // that POTRF leaves on the diagonal of the Linv workspace.
