@@ -284,6 +284,25 @@ def test_tile_fill_matern_points_half_bit_exact(ctx, ref):
         np.testing.assert_array_equal(t.to_numpy(), round_to(want, 0))
 
 
+def test_tile_fill_matern_points_half_narrow_strips(ctx, ref):
+    """The same bit-exactness for a tile size that is a multiple of 32 but not
+    of 128 (the generator's one-block strips) and for 128-multiples
+    (four-block strips), upper tiles included."""
+    import paper_2406_02701_b200 as mp
+    from oracle.oracle import round_to
+
+    rng = np.random.default_rng(5)
+    for n, nb in ((960, 96), (1024, 128)):
+        x = rng.random(n)
+        y = rng.random(n)
+        d = np.hypot(x[:, None] - x[None], y[:, None] - y[None])
+        g = np.zeros((n // nb, n // nb), int)
+        t = mp.MPCRTile(n, n, nb, nb, None, g, ctx)
+        t.fill_matern_points(x, y, 0.5, 0.05, 1.5, 0.1)
+        want = 1.5 * np.exp(-d / 0.05) + 0.1 * np.eye(n)
+        np.testing.assert_array_equal(t.to_numpy(), round_to(want, 0))
+
+
 _ENV_PROBE = r"""
 import hashlib, sys
 import numpy as np
