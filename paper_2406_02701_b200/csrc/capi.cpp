@@ -216,6 +216,9 @@ mp_status mp_ctx_create(int device, mp_ctx* out) {
     for (auto& s : c->aux) MP_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     MP_CUDA(cudaMalloc(&c->sched_pool, 2 * Ctx::SCHED_SLOTS * sizeof(unsigned int)));
     MP_CUDA(cudaMemset(c->sched_pool, 0, 2 * Ctx::SCHED_SLOTS * sizeof(unsigned int)));
+    // the context's streams are non-blocking: the zeroing must be complete
+    // before any of them can launch a kernel that draws from the pool
+    MP_CUDA(cudaDeviceSynchronize());
     *out = c;
     MP_API_END
 }
