@@ -1,35 +1,37 @@
-// FP64 GEMM of FP16-valued operands on the INT8 tensor cores (Ozaki scheme,
-// exact digit slicing).
+// FP64 (or FP32-output) GEMM of FP16- or FP32-valued operands on the INT8
+// tensor cores (Ozaki scheme, exact digit slicing).
 //
 // Where it serves: the FP64 tiles of the mixed-precision Cholesky are updated
 // with panel tiles that are stored in FP16 (the reference converts them to
-// double and calls an FP64 GEMM, linalg.cpp:349-356), and linalg::gemm with
-// FP16 operands and a double C.  B200 runs FP64 at 37 TFLOP/s but INT8 MMA at
-// ~4.5 POPS, so the FP64 product is rebuilt from INT8 products:
+// double and calls an FP64 GEMM, linalg.cpp:349-356), FP32 tiles with FP32
+// panel tiles, and linalg::gemm with FP16 operands and a double C.  B200 runs
+// FP64 at 37 TFLOP/s but INT8 MMA at ~4.5 POPS, so the product is rebuilt
+// from INT8 products:
 //
 //   every row r of an operand is scaled by 2^-e_r (e_r: exponent of its
-//   largest magnitude) and split into S = 6 signed 7-bit digits
+//   largest magnitude) and split into up to S = 6 signed 7-bit digits
 //     x = 2^e_r * sum_p d_p 2^(-6-7(p-1)),  d_p in [-64, 64]  (int8).
 //   An FP16 row spans at most 40 significant bits below its maximum (2^5 ..
 //   2^-24 plus 11 significand bits), and 6 digits hold 41, so the split is
-//   EXACT.  All S^2 = 36 digit products d_p d_q^T are computed (int32 sums
-//   are exact: |sum| <= 6 * K * 64^2 < 2^31 for K < 87381; callers split
-//   longer K into OZ_MAX_K chunks) and
-//   combined in FP64 with one rounding per group: the result is as accurate
-//   as a correctly-ordered FP64 dot product, usually better.
+//   EXACT (FP32 rows: exact down to 2^(e_r - 41)).  Only the digits a 128-row
+//   block needs are produced and multiplied; int32 group sums are exact
+//   (|sum| <= 6 * K * 64^2 < 2^31 for K < 87381; callers split longer K into
+//   OZ_MAX_K chunks) and combined in FP64 with one rounding per group: the
+//   result is as accurate as a correctly-ordered FP64 dot product.
 //
-// Kernel: persistent, warp-specialised, 128 x 128 output tiles.
-//   warp 0      TMA producer: 6-stage ring of {A 128x128, B 128x128} int8 digit
-//               tiles (128B swizzle).
-//   warp 1      TMEM allocator + MMA issuer: tcgen05.mma kind::i8 (M=128,
-//               N=128, K=32) into 4 rotating int32 TMEM accumulators; the 36
-//               digit pairs are issued grouped by t = p + q (11 groups, all
-//               pairs of a group share the scale 2^(-12-7(t-2)) and one
-//               accumulator), smallest magnitude first.
-//   warps 2-9   epilogue: each thread owns one tile row and 64 columns of
-//               FP64 running sums in registers; per group it adds
-//               2^(-12-7(t-2)) * acc, then C = alpha * 2^(e_r+e_c) * sum
-//               + beta * C (lower triangle only for SYRK tiles).
+// Kernel: persistent, warp-specialised, 128 x 128 output units drawn from a
+// global counter (dynamic scheduling; a problem may carry two panels).
+//   warp 0      TMA producer: 4-stage ring of {A 128x128, up to two B 128x128}
+//               int8 digit tiles (128B swizzle); draws the units.
+//   warp 1      TMEM allocator + MMA issuer (warp-uniform, elect.sync):
+//               tcgen05.mma kind::i8 (M=128, N=128, K=32) into 4 rotating
+//               int32 TMEM accumulators, one per digit group t = p + q (all
+//               pairs of a group share the scale 2^(-12-7(t-2))), groups
+//               issued in pairs (g, g-1) sharing the A digit plane.
+//   warps 2-13  epilogue (three per TMEM lane quarter, 48/48/32 columns):
+//               FP64 running sums in registers; per group sum += 2^(..) acc,
+//               then C = alpha * 2^(e_r+e_c) * sum + beta * C rounded once
+//               (lower triangle only for SYRK tiles).
 #include <cuda.h>
 
 #include <algorithm>
