@@ -303,7 +303,10 @@ __device__ __forceinline__ bool matern_half_fast(double dx, double dy, double c_
     r = r * fma(-0.5 * s2 * r, r, 1.5);  // one Newton step
     const double t = s2 * r * c_log2;      // d / range * log2(e)
     const double fl = floor(t);
-    if (!(fl <= 60.0)) return false;       // NaN, coincident points, or tiny values: FP64 path
+    // NaN or coincident points: FP64 path.  Up to 2^-120 the FP32 scaling
+    // below stays normal (tiny values round to +0 in half, exactly as the
+    // reference's: no FP64 fallback for far-apart points)
+    if (!(fl <= 120.0)) return false;
     float e;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-static_cast<float>(t - fl)));
     const float v = e * __int_as_float((127 - static_cast<int>(fl)) << 23) * var32;  // exact 2^-fl
@@ -342,8 +345,11 @@ __device__ __forceinline__ void matern_half_tiles(const MaternItem& it, int nb, 
     __shared__ int nfail;
     __shared__ uint16_t flist[32 * 32];  // elements left to the FP64 path (rare)
     __shared__ double cxs[32], cys[32];  // the block's column points
+    const bool bpr_p2 = (bpr & (bpr - 1)) == 0;  // tile sizes of 32 x 2^k: shifts, not divisions
+    const int bpr_lg = __ffs(bpr) - 1;
     for (int blk = blockIdx.x; blk < bpr * bpr; blk += gridDim.x) {
-        const int bi = blk % bpr, bj = blk / bpr;
+        const int bi = bpr_p2 ? (blk & (bpr - 1)) : blk % bpr;
+        const int bj = bpr_p2 ? (blk >> bpr_lg) : blk / bpr;
         const int i = bi * 32 + tx;
         const int64_t pi = it.row0 + i, pc0 = it.col0 + bj * 32;
         double xi, yi;
@@ -382,11 +388,11 @@ __device__ __forceinline__ void matern_half_tiles(const MaternItem& it, int nb, 
         }
         if (!up) continue;
         __syncthreads();
-        uint16_t* upb = up + static_cast<int64_t>(bi * 32) * nb + bj * 32 + tx;
+        uint16_t* upb = up + static_cast<int64_t>(bi * 32 + ty) * nb + bj * 32 + tx;  // column bi*32+ty
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const int li = ty + 8 * q;
-            upb[static_cast<int64_t>(li) * nb] = sh[tx][li];
+            *upb = sh[tx][ty + 8 * q];
+            upb += 8 * static_cast<int64_t>(nb);
         }
     }
 }
